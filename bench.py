@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py -- WildCat coreset attention on B200: queries/s at n = 64K, d = 128, r = 256 (bf16).
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config headline] [--impl wildcat|reference]
+One step = one pass of the whole hot path (prologue, RPCholesky selection, Nystrom weights,
+weighted attend) over one batch of synthetic inputs resident in HBM, through the C ABI
+(wildcat_forward).  L2 is flushed (a 512 MB write) before every timed step, outside the timed
+events.  Multi-GPU (torchrun): each rank runs an independent replica (units sharded, no
+data-path collective) -> weak scaling; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "coreset-attention queries/s at n=64K,d=128,r=256; HBM GB/s; rel err vs exact"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def select_bytes(n, d, r, e):
+    """Algorithmic HBM bytes of the selection loop per unit:
+    n r (d e + 24) + 4 n r (r - 1)."""
+    return n * r * (d * e + 24) + 4 * n * r * (r - 1)
+
+
+def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048):
+    """Time the fp64 oracle (as it stands) on a bounded sample: unit 0's full prologue + selection +
+    weights over all n keys, and the attend on `max_queries` query rows; extrapolate linearly in the
+    number of query rows and units to the whole workload.  Returns (queries/s, seconds, details)."""
+    import oracle
+
+    threads = len(os.sched_getaffinity(0))
+    oracle.set_threads(threads)
+    d = cfg.d
+    group = cfg.hq // cfg.hkv
+    K64 = K[0, 0].double().numpy()
+    V64 = V[0, 0].double().numpy()
+    Qg = Q[0, :group].double().numpy().reshape(-1, d)
+    beta = 1.0 / math.sqrt(d)
+    t0 = time.perf_counter()
+    kbar, st = oracle.prologue(K64, Qg)
+    sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
+    t1 = time.perf_counter()
+    X = oracle.weights(K64, V64, sel["S"], sel["r_eff"], kbar, st["g"], st["mstar"])
+    t2 = time.perf_counter()
+    ms = min(max_queries, Qg.shape[0])
+    oracle.attend(Qg[:ms], K64[sel["S"]], X, sel["r_eff"], beta, V64.min(0), V64.max(0))
+    t3 = time.perf_counter()
+    per_unit = (t1 - t0) + (t2 - t1) + (t3 - t2) * (Qg.shape[0] / ms)
+    total = per_unit * cfg.units
+    queries = cfg.batch * cfg.hq * cfg.m
+    info = dict(select_s=t1 - t0, weights_s=t2 - t1, attend_s=t3 - t2, attend_rows=ms, threads=threads,
+                sample=(f"oracle on unit 0 of {cfg.units}: full prologue+selection+weights over n={cfg.n} keys, "
+                        f"attend on {ms} of {Qg.shape[0]} query rows; extrapolated linearly to all rows/units"))
+    return queries / total, total, info
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, cfg):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    from paper_2602_10056_b200.inputs import make_config
+
+    Q, K, V = make_config(cfg)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries)
+    vals, secs = [], []
+    info = None
+    for _ in range(args.steps):
+        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries)
+        vals.append(v)
+        secs.append(s)
+    tot = sum(secs)
+    value = cfg.batch * cfg.hq * cfg.m * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r,
+                   "input_dtype": cfg.dtype, "family": cfg.family},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
+                         "sample": info["sample"], "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="headline")
+    ap.add_argument("--impl", default="wildcat", choices=["wildcat", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-queries", type=int, default=2048)
+    ap.add_argument("--flush-mb", type=int, default=512)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    from paper_2602_10056_b200.inputs import CONFIGS, make_config
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_10056_b200 as wc
+    from paper_2602_10056_b200 import _binding as B
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # replica per rank (weak scaling): same workload, rank-specific seed
+    Q, K, V = make_config(cfg, seed=cfg.seed + rank)
+    Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+    units = cfg.units
+    S = torch.empty(units, cfg.r, dtype=torch.int32, device=dev)
+    R = torch.empty(units, dtype=torch.int32, device=dev)
+    flush = torch.empty(args.flush_mb * (1 << 20), dtype=torch.uint8, device=dev)
+    seed = cfg.seed + rank
+
+    def step():
+        return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = B.last_launch_count()
+
+    B.timing_enable(True)
+    stages = []
+    step_ms = []
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        O = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        stages.append(B.timing_read())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    B.timing_enable(False)
+
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    queries_per_rank = cfg.batch * cfg.hq * cfg.m
+    value = queries_per_rank * world * args.steps / (total_ms / 1e3)
+
+    # stage breakdown (ms, mean over timed steps): prologue, select, weights, attend
+    st_names = ["prologue", "select", "weights", "attend"]
+    st_mean = [statistics.mean(s[i] for s in stages) for i in range(4)]
+    e = 2 if cfg.dtype == "bf16" else 4
+    r_eff = int(R.min().item())
+    alg_bytes = units * select_bytes(cfg.n, cfg.d, r_eff, e)
+    achieved = alg_bytes / (st_mean[1] / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # end to end through the public API with host buffers (pinned), H2D + forward + D2H per step
+    e2e = None
+    if not args.no_e2e:
+        Qh, Kh, Vh = (x.pin_memory() for x in (Q, K, V))
+        for _ in range(max(1, args.warmup)):
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev)
+        tt = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev)
+            tt.append(time.perf_counter() - t0)
+        te = torch.tensor([sum(tt)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * x.element_size() for x in (Q, K, V))
+        d2h = O.numel() * O.element_size()
+        e2e = {"value": queries_per_rank * world * args.steps / float(te.item()), "unit": "queries/s",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "timing": "host wall clock around forward_host (H2D, wildcat_forward, D2H, sync)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, secs, info = cpu_oracle_sample(cfg, Q, K, V)
+        cpu = {"value": v, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
+               "sample": info["sample"], "cpu": cpu_model(), "seconds_extrapolated": secs,
+               "select_s": info["select_s"], "weights_s": info["weights_s"], "attend_s": info["attend_s"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64-select/f32-gemm",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "units_per_gpu": units, "n": cfg.n, "m": cfg.m, "d": cfg.d,
+                       "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
+                       "parallelism": f"replicas{world}", "l2": f"flushed ({args.flush_mb} MB write) before each step"},
+            "stages_ms": dict(zip(st_names, st_mean)),
+            "roofline": {"kernel": "rpc_select_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

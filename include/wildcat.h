@@ -1,0 +1,141 @@
+/*
+ * wildcat.h -- C ABI of libwildcat.so: WildCat weighted-coreset attention
+ * (Schroeder & Mackey, arxiv 2602.10056) on NVIDIA B200 (sm_100a).
+ *
+ * Citations "P:<line>" refer to PAPER.md of the paper; "Z<k>" to the readings
+ * listed in DESIGN.md (where the paper is silent or ambiguous).
+ *
+ * Problem (Alg 4): queries Q, keys K, values V, scale beta, rank r
+ *   -> O^ = WtdAttn(Q, CompressKV(K, V, R_Q, beta, r)),
+ * computed independently for every "unit" u = b*heads_kv + h (one (batch,
+ * kv-head) pair; bins B = 1).  Query head hq uses unit (b, hq / (heads_q/heads_kv)).
+ *
+ * Layouts (row-major, contiguous, device memory unless stated):
+ *   Q, O   [batch][heads_q ][m][d]   dtype
+ *   K, V   [batch][heads_kv][n][d]   dtype
+ *   S      int32  [units][r]         global key index (0..n-1) of the i-th pivot, -1 past r_eff
+ *   r_eff  int32  [units]            number of pivots actually drawn (<= r, Z3)
+ *   L      double [units][r][r]      lower-triangular Cholesky factor of h~(K_S,K_S) in pivot
+ *                                    order, L[a][b] = F[b, S[a]] (b <= a), 0 elsewhere (Z6)
+ *   stats  double [units][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, 0, 0, kbar[d]
+ *   KS     dtype  [units][r][d]      coreset keys, uncentred (Alg 2 "K_S <- K_S + kbar")
+ *   X      float  [units][r][d+1]    [V_S, w] = W [V, 1_n]  (Alg 2 "Compress values")
+ *   vmin, vmax dtype [units][d]      columnwise range of V (Alg 4)
+ *
+ * Conventions:
+ *   - Every call is asynchronous on `stream` (a cudaStream_t); nothing synchronises
+ *     the host.  Argument errors are returned before any launch and nothing is
+ *     written; launch errors are reported via cudaGetLastError as WC_ECUDA.
+ *   - The caller owns every buffer including the workspace `ws` (ws_bytes >=
+ *     wc_workspace_bytes(shape, op)); the library allocates nothing.
+ *   - Reentrant for distinct workspaces; no global mutable state.
+ *   - NaN/Inf inputs give undefined outputs.
+ */
+#ifndef WILDCAT_H_
+#define WILDCAT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WC_OK 0
+#define WC_EINVAL -1        /* null pointer, bad enum, unknown flag */
+#define WC_ESHAPE -2        /* r < 1, r > n, bins != 1, heads_q % heads_kv != 0, d not in {16,32,64,128}, m < 0 */
+#define WC_EDTYPE -3        /* dtype not WC_F32 / WC_BF16 */
+#define WC_EWORKSPACE -4    /* ws too small or misaligned (needs 256-byte alignment) */
+#define WC_ECUDA -5         /* CUDA launch / runtime error */
+#define WC_EUNSUPPORTED -7  /* valid request this build does not implement */
+
+#define WC_F32 0
+#define WC_BF16 1
+
+#define WC_OP_SELECT 0
+#define WC_OP_WEIGHTS 1
+#define WC_OP_ATTEND 2
+#define WC_OP_FORWARD 3
+
+/* flags */
+#define WC_NO_CLIP 1u       /* skip the clip of Alg 3 (reading Z15) */
+
+#define WC_STATS_STRIDE(d) (8 + (d))
+
+typedef struct wc_shape {
+    int32_t batch;     /* >= 1 */
+    int32_t heads_q;   /* >= 1, multiple of heads_kv */
+    int32_t heads_kv;  /* >= 1 */
+    int32_t d;         /* head dim: 16, 32, 64 or 128 */
+    int32_t r;         /* coreset size, 1 <= r <= n ("rank r") */
+    int32_t bins;      /* B of Alg 2; must be 1 in this build */
+    int32_t dtype;     /* WC_F32 or WC_BF16 (element type of Q, K, V, O, KS, vmin, vmax) */
+    int32_t reserved;
+    int64_t m;         /* queries per q-head, >= 0 */
+    int64_t n;         /* keys per kv-head, >= 1 */
+} wc_shape;
+
+typedef struct wc_opts {
+    double beta;       /* softmax scale; <= 0 selects 1/sqrt(d) (reading Z7) */
+    double rq;         /* R_Q of Alg 2; < 0 (or NaN) computes max ||q|| over the unit's query group */
+    uint64_t seed;     /* Philox4x32-10 key for the pivot draws (reading Z2) */
+    uint32_t flags;    /* WC_NO_CLIP */
+    uint32_t reserved;
+} wc_opts;
+
+/* Bytes of workspace the op needs for this shape (0 on invalid shape). */
+size_t wc_workspace_bytes(const wc_shape *shape, int op);
+
+/* Alg 2 lines "Recenter keys" .. RPNys + Alg 1:
+ * per unit, recentre K, compute R_K, R_Q (from Q, or opts->rq if >= 0; Q may then be
+ * NULL), tau (Eq. 7), and run r rounds of randomly pivoted Cholesky on
+ * h~(a,b) = exp(beta/tau^2 <a-kbar, b-kbar> - mstar) with the Philox pivot stream.
+ * Writes S, r_eff, L, stats.  Outputs S, r_eff, L, stats are required. */
+int wildcat_select(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *K,
+                   int32_t *S, int32_t *r_eff, double *L, double *stats,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/* Nystrom weights applied to [V, 1_n] (Alg 2 "Compress values"):
+ * X = h~(K_S,K_S)^{-1} h~(K_S,K) [V, 1_n], via L from wildcat_select; gathers KS = K[S]
+ * and the value range vmin/vmax of V.  Inputs S, r_eff, L, stats come from wildcat_select. */
+int wildcat_weights(const wc_shape *shape, const wc_opts *opts, const void *K, const void *V,
+                    const int32_t *S, const int32_t *r_eff, const double *L, const double *stats,
+                    void *KS, float *X, void *vmin, void *vmax,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/* Alg 3 WtdAttn: O = clip( diag(A^ w)^{-1} A^ V_S where A^ w > 0 else 0, vmin, vmax ),
+ * A^ = exp(beta Q K_S^T) over the first r_eff coreset rows.  `m` of the shape is the
+ * number of queries per q-head (e.g. 1 for decode). */
+int wildcat_attend(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *KS,
+                   const float *X, const int32_t *r_eff, const void *vmin, const void *vmax,
+                   void *O, void *ws, size_t ws_bytes, void *stream);
+
+/* Alg 4 WildCat = select + weights + attend.  S and r_eff may be NULL
+ * (then kept in the workspace). */
+int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *K,
+                    const void *V, void *O, int32_t *S, int32_t *r_eff,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/* Human-readable status. */
+const char *wc_strerror(int status);
+
+/* Number of kernel launches the last successful call on this thread enqueued
+ * (instrumentation for bench.py's gpu_launches; thread-local). */
+int wc_last_launch_count(void);
+
+/* Stage timing instrumentation (thread-local; off by default).  When enabled, the
+ * calls record CUDA events on their stream between stages:
+ *   wildcat_forward: [prologue, select, weights, attend];  wildcat_select: [prologue, select];
+ *   wildcat_weights: [vrange, weights];  wildcat_attend: [attend].
+ * wc_timing_read waits for the last event and writes the stage durations in ms; it
+ * returns the number of stages written (<= cap), or a negative status. */
+int wc_timing_enable(int on);
+int wc_timing_read(float *ms, int cap);
+
+/* ABI version (major*100 + minor). */
+int wc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WILDCAT_H_ */

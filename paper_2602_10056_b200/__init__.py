@@ -1,0 +1,146 @@
+"""paper_2602_10056_b200 -- WildCat weighted-coreset attention on NVIDIA B200.
+
+Public API (torch tensors in the BHND layout [batch, heads, seq, d], CUDA only):
+
+    O = forward(Q, K, V, r, seed=0)                         # Alg 4 WildCat
+    sel = select(Q, K, r, seed=0)                           # Alg 2 lines 1-6 + Alg 1 (RPNys)
+    cache = weights(K, V, sel)                              # Alg 2 "Compress values"
+    O = attend(Q, cache)                                    # Alg 3 WtdAttn
+    O = forward_host(Q_cpu, K_cpu, V_cpu, r)                # host buffers in, host result out
+
+Everything runs in libwildcat.so (hand-written sm_100a kernels behind a C ABI,
+include/wildcat.h).  There is no CPU fallback: CPU tensors raise (except
+forward_host, which only copies host<->device around the same CUDA call).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _binding as B
+from ._binding import WildcatError, lib  # noqa: F401
+
+__all__ = ["forward", "forward_host", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
+           "STATS_STRIDE"]
+
+
+def STATS_STRIDE(d: int) -> int:
+    return 8 + d
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise WildcatError("WildCat runs on CUDA tensors only (no CPU fallback)")
+
+
+def _cont(t):
+    return None if t is None else t.contiguous()
+
+
+@dataclass
+class Selection:
+    S: torch.Tensor       # int32 [units, r]
+    r_eff: torch.Tensor   # int32 [units]
+    L: torch.Tensor       # float64 [units, r, r]
+    stats: torch.Tensor   # float64 [units, 8 + d]: tau, g, mstar, R_K, R_Q, T0, -, -, kbar
+    shape: B.wc_shape
+    opts: B.wc_opts
+
+
+@dataclass
+class Cache:
+    KS: torch.Tensor      # dtype [units, r, d]
+    X: torch.Tensor       # float32 [units, r, d+1] = [V_S, w]
+    vmin: torch.Tensor    # dtype [units, d]
+    vmax: torch.Tensor
+    r_eff: torch.Tensor
+    heads_kv: int
+    opts: B.wc_opts
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(shape, op, device):
+    nb = B.workspace_bytes(shape, op)
+    key = (device, op)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nb:
+        t = torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def select(Q, K, r, seed=0, beta=None, rq=None, stream=None) -> Selection:
+    Q, K = _cont(Q), _cont(K)
+    _require_cuda(Q, K)
+    shape = B.make_shape(Q, K, r)
+    opts = B.make_opts(seed, beta, rq)
+    units = shape.batch * shape.heads_kv
+    dev = K.device
+    S = torch.empty(units, r, dtype=torch.int32, device=dev)
+    reff = torch.empty(units, dtype=torch.int32, device=dev)
+    L = torch.empty(units, r, r, dtype=torch.float64, device=dev)
+    stats = torch.empty(units, STATS_STRIDE(shape.d), dtype=torch.float64, device=dev)
+    ws = _workspace(shape, B.WC_OP_SELECT, dev)
+    B.wildcat_select(shape, opts, Q, K, S, reff, L, stats, ws, stream)
+    return Selection(S, reff, L, stats, shape, opts)
+
+
+def weights(K, V, sel: Selection, stream=None) -> Cache:
+    K, V = _cont(K), _cont(V)
+    _require_cuda(K, V)
+    shape = sel.shape
+    units, r, d = shape.batch * shape.heads_kv, shape.r, shape.d
+    dev = K.device
+    KS = torch.empty(units, r, d, dtype=K.dtype, device=dev)
+    X = torch.empty(units, r, d + 1, dtype=torch.float32, device=dev)
+    vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
+    vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
+    ws = _workspace(shape, B.WC_OP_WEIGHTS, dev)
+    B.wildcat_weights(shape, sel.opts, K, V, sel.S, sel.r_eff, sel.L, sel.stats, KS, X, vmin, vmax, ws, stream)
+    return Cache(KS, X, vmin, vmax, sel.r_eff, shape.heads_kv, sel.opts)
+
+
+def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
+    Q = _cont(Q)
+    _require_cuda(Q)
+    b, hq, m, d = Q.shape
+    units, r, _ = cache.KS.shape
+    shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=r, bins=1,
+                       dtype=B._dtype_code(Q), reserved=0, m=m, n=max(r, 1))
+    opts = B.wc_opts(beta=cache.opts.beta if beta is None else float(beta), rq=cache.opts.rq,
+                     seed=cache.opts.seed,
+                     flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), reserved=0)
+    O = torch.empty_like(Q)
+    B.wildcat_attend(shape, opts, Q, cache.KS, cache.X, cache.r_eff, cache.vmin, cache.vmax, O, None, stream)
+    return O
+
+
+def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None, r_eff=None, stream=None):
+    """Alg 4 WildCat on device tensors.  Returns O (and fills S / r_eff if given)."""
+    Q, K, V = _cont(Q), _cont(K), _cont(V)
+    _require_cuda(Q, K, V)
+    shape = B.make_shape(Q, K, r)
+    opts = B.make_opts(seed, beta, rq, clip)
+    O = torch.empty_like(Q) if out is None else out
+    ws = _workspace(shape, B.WC_OP_FORWARD, K.device)
+    B.wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream)
+    return O
+
+
+def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", stream=None):
+    """End-to-end call with host (CPU) buffers: H2D copies, the CUDA forward, D2H copy of O."""
+    dev = torch.device(device)
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    with torch.cuda.stream(s):
+        Qd = Q.to(dev, non_blocking=True)
+        Kd = K.to(dev, non_blocking=True)
+        Vd = V.to(dev, non_blocking=True)
+        Od = forward(Qd, Kd, Vd, r, seed=seed, beta=beta, rq=rq, clip=clip, stream=s)
+        O = torch.empty(Od.shape, dtype=Od.dtype, pin_memory=True)
+        O.copy_(Od, non_blocking=True)
+    s.synchronize()
+    return O

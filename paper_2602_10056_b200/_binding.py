@@ -1,0 +1,160 @@
+"""ctypes binding of libwildcat.so -- argument marshalling only.
+
+Every function here has the name of the C entry point it wraps (include/wildcat.h)
+and does nothing but turn torch tensors into pointers and sizes.  All arithmetic of
+the method runs in the CUDA kernels behind the C ABI.  There is no CPU fallback:
+if the shared library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwildcat.so")
+
+WC_F32, WC_BF16 = 0, 1
+WC_OP_SELECT, WC_OP_WEIGHTS, WC_OP_ATTEND, WC_OP_FORWARD = 0, 1, 2, 3
+WC_NO_CLIP = 1
+
+
+class WildcatError(RuntimeError):
+    pass
+
+
+class wc_shape(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("heads_q", ctypes.c_int32), ("heads_kv", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("r", ctypes.c_int32), ("bins", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("m", ctypes.c_int64), ("n", ctypes.c_int64)]
+
+
+class wc_opts(ctypes.Structure):
+    _fields_ = [("beta", ctypes.c_double), ("rq", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libwildcat.so (building it first if the sources are newer).  Raises if unavailable."""
+    global _lib
+    if _lib is None:
+        from . import build as _build
+
+        try:
+            _build.build()
+        except Exception as e:  # nvcc missing on the box: use the shipped .so if present
+            if not os.path.exists(LIB_PATH):
+                raise WildcatError(f"libwildcat.so is missing and could not be built: {e}") from e
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        S = ctypes.POINTER(wc_shape)
+        O = ctypes.POINTER(wc_opts)
+        L.wc_workspace_bytes.argtypes = [S, ctypes.c_int]
+        L.wc_workspace_bytes.restype = ctypes.c_size_t
+        L.wildcat_select.argtypes = [S, O, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        L.wildcat_weights.argtypes = [S, O, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        L.wildcat_attend.argtypes = [S, O, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        L.wildcat_forward.argtypes = [S, O, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        for f in ("wildcat_select", "wildcat_weights", "wildcat_attend", "wildcat_forward"):
+            getattr(L, f).restype = ctypes.c_int
+        L.wc_strerror.argtypes = [ctypes.c_int]
+        L.wc_strerror.restype = ctypes.c_char_p
+        L.wc_last_launch_count.restype = ctypes.c_int
+        L.wc_version.restype = ctypes.c_int
+        L.wc_timing_enable.argtypes = [ctypes.c_int]
+        L.wc_timing_enable.restype = ctypes.c_int
+        L.wc_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+        L.wc_timing_read.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise WildcatError(f"{what}: {lib().wc_strerror(rc).decode()} ({rc})")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return WC_F32
+    if t.dtype == torch.bfloat16:
+        return WC_BF16
+    raise WildcatError(f"unsupported dtype {t.dtype}")
+
+
+def make_shape(Q, K, r, m=None) -> wc_shape:
+    b, hkv, n, d = K.shape
+    hq = Q.shape[1] if Q is not None else hkv
+    mm = (Q.shape[2] if Q is not None else 0) if m is None else m
+    return wc_shape(batch=b, heads_q=hq, heads_kv=hkv, d=d, r=int(r), bins=1, dtype=_dtype_code(K),
+                    reserved=0, m=mm, n=n)
+
+
+def make_opts(seed=0, beta=None, rq=None, clip=True) -> wc_opts:
+    return wc_opts(beta=-1.0 if beta is None else float(beta), rq=-1.0 if rq is None else float(rq),
+                   seed=int(seed) & 0xFFFFFFFFFFFFFFFF, flags=0 if clip else WC_NO_CLIP, reserved=0)
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def workspace_bytes(shape: wc_shape, op: int) -> int:
+    return int(lib().wc_workspace_bytes(ctypes.byref(shape), op))
+
+
+def alloc_workspace(shape: wc_shape, op: int, device) -> torch.Tensor:
+    nb = workspace_bytes(shape, op)
+    return torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
+
+
+def wildcat_select(shape, opts, Q, K, S, r_eff, L, stats, ws, stream=None):
+    rc = lib().wildcat_select(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(S), _ptr(r_eff),
+                              _ptr(L), _ptr(stats), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "wildcat_select")
+
+
+def wildcat_weights(shape, opts, K, V, S, r_eff, L, stats, KS, X, vmin, vmax, ws, stream=None):
+    rc = lib().wildcat_weights(ctypes.byref(shape), ctypes.byref(opts), _ptr(K), _ptr(V), _ptr(S), _ptr(r_eff),
+                               _ptr(L), _ptr(stats), _ptr(KS), _ptr(X), _ptr(vmin), _ptr(vmax), _ptr(ws),
+                               ws.numel(), _stream(stream))
+    _check(rc, "wildcat_weights")
+
+
+def wildcat_attend(shape, opts, Q, KS, X, r_eff, vmin, vmax, O, ws=None, stream=None):
+    rc = lib().wildcat_attend(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(KS), _ptr(X), _ptr(r_eff),
+                              _ptr(vmin), _ptr(vmax), _ptr(O), _ptr(ws), 0 if ws is None else ws.numel(),
+                              _stream(stream))
+    _check(rc, "wildcat_attend")
+
+
+def wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream=None):
+    rc = lib().wildcat_forward(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
+                               _ptr(S), _ptr(r_eff), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "wildcat_forward")
+
+
+def last_launch_count() -> int:
+    return int(lib().wc_last_launch_count())
+
+
+def timing_enable(on: bool = True) -> None:
+    lib().wc_timing_enable(1 if on else 0)
+
+
+def timing_read(cap: int = 8) -> list:
+    buf = (ctypes.c_float * cap)()
+    k = lib().wc_timing_read(buf, cap)
+    if k < 0:
+        raise WildcatError(f"wc_timing_read: {lib().wc_strerror(k).decode()}")
+    return [float(buf[i]) for i in range(k)]

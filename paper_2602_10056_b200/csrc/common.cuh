@@ -1,0 +1,162 @@
+// common.cuh -- device helpers shared by the WildCat sm_100a kernels.
+// (Product path only; the fp64 CPU oracle under oracle/ shares nothing with this.)
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wc {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------- element loads
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ double to_f64(float x) { return (double)x; }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f32(float x);
+template <> __device__ __forceinline__ float from_f32<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Counter-based generator of Salmon et al. (SC'11).  The pivot uniform of round i of
+// unit u is built from Philox4x32-10(key = seed, ctr = (i, u_lo, u_hi, 'PIVT')) with
+// 53 random bits (reading Z2).
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int rnd = 0; rnd < 10; ++rnd) {
+        const uint32_t lo0 = 0xD2511F53u * c[0];
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0;
+        const uint32_t n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__device__ __forceinline__ double pivot_uniform(uint64_t seed, uint32_t round_i, uint64_t unit) {
+    uint32_t c[4] = {round_i, (uint32_t)unit, (uint32_t)(unit >> 32), 0x50495654u};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const double a = (double)(c[0] >> 5), b = (double)(c[1] >> 6);
+    return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+}
+
+// ---------------------------------------------------------------- Lambert W0 (device)
+// Loczi iteration, 6 steps; z >= e uses log z - log log z.
+__device__ __forceinline__ double lambert_w0_dev(double z) {
+    if (z == 0.0) return 0.0;
+    const double lz = log(z);
+    double b = (z >= 2.718281828459045) ? lz - log(lz) : exp(lz - 1.0);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b = b / (1.0 + b) * (1.0 + lz - log(b));
+    return b;
+}
+
+// ---------------------------------------------------------------- reductions
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T> __device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block sum (fixed tree order); result valid in all threads.
+// `scratch` needs blockDim/32 doubles.  Contains __syncthreads.
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = lane < nw ? scratch[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) scratch[0] = t;
+    }
+    __syncthreads();
+    t = scratch[0];
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ double block_max(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) scratch[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double t = lane < nw ? scratch[lane] : -1.0e308;
+        t = warp_max(t);
+        if (lane == 0) scratch[0] = t;
+    }
+    __syncthreads();
+    const double t = scratch[0];
+    __syncthreads();
+    return t;
+}
+
+// Block-wide exclusive scan of one double per thread in a fixed order (warp shuffle
+// scan + scan of warp totals).  Returns the exclusive prefix; *total gets the sum.
+__device__ __forceinline__ double block_exclusive_scan(double v, double *scratch, double *total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) scratch[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        double t = lane < nw ? scratch[lane] : 0.0;
+        double ti = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += y;
+        }
+        if (lane < nw) scratch[lane] = ti - t;  // exclusive warp offsets
+        if (lane == nw - 1) scratch[32] = ti;
+    }
+    __syncthreads();
+    const double excl = scratch[w] + (incl - v);
+    *total = scratch[32];
+    __syncthreads();
+    return excl;
+}
+
+// ---------------------------------------------------------------- grid-group barrier
+// Barrier among the `count` co-resident CTAs that share `ctr` (one counter per unit).
+// Monotone counter: the e-th barrier waits until ctr >= e*count.  The caller zeroes
+// ctr before the launch.  Release/acquire at gpu scope orders the global writes.
+__device__ __forceinline__ void group_barrier(unsigned int *ctr, unsigned int count, unsigned int epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+        const unsigned int target = epoch * count;
+        unsigned int v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace wc

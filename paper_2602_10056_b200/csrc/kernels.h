@@ -1,0 +1,59 @@
+// kernels.h -- private host-side launchers of the WildCat sm_100a kernels (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wc {
+
+struct Dims {
+    int batch, hq, hkv, d, r, dtype;
+    int64_t m, n;
+    int units() const { return batch * hkv; }
+    int group() const { return hq / hkv; }
+};
+
+// Workspace blocks used by the prologue (A0).
+struct ProloguePartials {
+    double *colsum;  // [units][P][d]
+    float *vmin;     // [units][P][d]
+    float *vmax;     // [units][P][d]
+    double *rq2;     // [units][P]
+    double *rk2;     // [units][P]
+    int P;
+};
+
+int prologue_num_splits(const Dims &D);
+
+// A0: kbar, R_K, R_Q, tau, g, mstar -> stats[u][8+d]; nrm2[u][l] = ||k_l - kbar||^2;
+// vmin/vmax (dtype) when non-null.  Returns number of launches (>0) or -1 on error.
+int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
+                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                    cudaStream_t st);
+
+// Columnwise range of V only (wildcat_weights).
+int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st);
+
+struct SelectBufs {
+    double *nrm2;   // [units][n]
+    double *p;      // [2][units][n]
+    double *F;      // [units][r][n]
+    double *part;   // [units][2][kMaxCpu]
+    unsigned *bar;  // [units]
+};
+constexpr int kMaxCpu = 1024;
+
+int select_ctas_per_unit(const Dims &D);
+// A1+A2: r rounds of RP-Cholesky.  Returns launches or -1.
+int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed,
+                  int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
+
+int weights_num_splits(const Dims &D);
+// A3+A4: X = L^{-T} L^{-1} h~(K_S,K)[V,1]; KS gather.  Ypart: [units][splits][r][d+1] fp32.
+int launch_weights(const Dims &D, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
+                   const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st);
+
+// A5: attend.
+int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                  const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st);
+
+}  // namespace wc

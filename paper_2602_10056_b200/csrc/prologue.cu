@@ -1,0 +1,228 @@
+// prologue.cu -- A0 of the hot path: per-unit recentring statistics and temperature.
+//   kbar = row mean of K (Alg 2 "Recenter keys")
+//   R_K  = max_l ||k_l - kbar||,  R_Q = max_i ||q_i|| over the unit's query group (Alg 4)
+//   tau  = Eq. 7, g = beta/tau^2, mstar = g R_K^2 (reading Z10)
+//   (vmin, vmax) = columnwise range of V (Alg 4)
+// HBM-bound streaming passes (one over K, Q, V; one over K), fp64 accumulation.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace wc {
+
+namespace {
+
+constexpr int kPT = 256;  // threads per prologue block
+
+// Pass 1: per (split p, unit u): column sums of K (fp64), column min/max of V, max ||q||^2.
+template <typename T>
+__global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, const T *__restrict__ K,
+                                                      const T *__restrict__ V, int64_t n, int64_t mq, int d,
+                                                      int P, int want_q, int want_v, double *colsum,
+                                                      float *vmin, float *vmax, double *rq2,
+                                                      int64_t q_unit_stride_rows) {
+    extern __shared__ double sm1[];
+    const int p = blockIdx.x, u = blockIdx.y;
+    const int G = kPT / d;  // row groups
+    const int grp = threadIdx.x / d, j = threadIdx.x % d;
+    const int64_t rows = ceil_div(n, P);
+    const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
+    const T *Ku = K + (int64_t)u * n * d;
+    const T *Vu = V + (int64_t)u * n * d;
+    double cs = 0.0;
+    float lo_v = 3.0e38f, hi_v = -3.0e38f;
+    if (grp < G) {
+        for (int64_t l = lo + grp; l < hi; l += G) {
+            cs += to_f64(Ku[l * d + j]);
+            if (want_v) {
+                const float v = to_f32(Vu[l * d + j]);
+                lo_v = fminf(lo_v, v);
+                hi_v = fmaxf(hi_v, v);
+            }
+        }
+    }
+    double *s_cs = sm1;                                // [G][d]
+    float *s_lo = reinterpret_cast<float *>(sm1 + G * d);  // [G][d]
+    float *s_hi = s_lo + G * d;
+    if (grp < G) {
+        s_cs[grp * d + j] = cs;
+        s_lo[grp * d + j] = lo_v;
+        s_hi[grp * d + j] = hi_v;
+    }
+    __syncthreads();
+    if (threadIdx.x < d) {
+        double t = 0.0;
+        float a = 3.0e38f, b = -3.0e38f;
+        for (int g2 = 0; g2 < G; ++g2) {
+            t += s_cs[g2 * d + threadIdx.x];
+            a = fminf(a, s_lo[g2 * d + threadIdx.x]);
+            b = fmaxf(b, s_hi[g2 * d + threadIdx.x]);
+        }
+        const int64_t o = ((int64_t)u * P + p) * d + threadIdx.x;
+        colsum[o] = t;
+        vmin[o] = a;
+        vmax[o] = b;
+    }
+    if (want_q) {
+        // one warp per query row, lanes over d
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kPT / 32;
+        const int64_t qrows = ceil_div(mq, P);
+        const int64_t qlo = (int64_t)p * qrows, qhi = min(mq, qlo + qrows);
+        const T *Qu = Q + (int64_t)u * q_unit_stride_rows * d;
+        double mx = 0.0;
+        for (int64_t i = qlo + w; i < qhi; i += nw) {
+            double s = 0.0;
+            for (int jj = lane; jj < d; jj += 32) {
+                const double x = to_f64(Qu[i * d + jj]);
+                s += x * x;
+            }
+            s = warp_sum(s);
+            mx = fmax(mx, s);
+        }
+        __shared__ double scr[40];
+        mx = block_max(mx, scr);
+        if (threadIdx.x == 0) rq2[(int64_t)u * P + p] = mx;
+    }
+}
+
+// Finalise kbar (fixed-order sum over splits) and the value range.
+template <typename T>
+__global__ void prologue_kbar(int64_t n, int d, int P, const double *colsum, const float *vmin_p,
+                              const float *vmax_p, double *stats, T *vmin, T *vmax) {
+    const int u = blockIdx.x, j = threadIdx.x;
+    if (j >= d) return;
+    double t = 0.0;
+    float a = 3.0e38f, b = -3.0e38f;
+    for (int p = 0; p < P; ++p) {
+        const int64_t o = ((int64_t)u * P + p) * d + j;
+        t += colsum[o];
+        a = fminf(a, vmin_p[o]);
+        b = fmaxf(b, vmax_p[o]);
+    }
+    if (stats) stats[(int64_t)u * (8 + d) + 8 + j] = t / (double)n;
+    if (vmin) {
+        vmin[(int64_t)u * d + j] = from_f32<T>(a);
+        vmax[(int64_t)u * d + j] = from_f32<T>(b);
+    }
+}
+
+// Pass 2: nrm2_l = ||k_l - kbar||^2 (fp64) and the split max.  One warp per key.
+template <typename T>
+__global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, int64_t n, int d, int P,
+                                                      const double *stats, double *nrm2, double *rk2) {
+    __shared__ double kb[128];
+    __shared__ double scr[40];
+    const int p = blockIdx.x, u = blockIdx.y;
+    const double *st = stats + (int64_t)u * (8 + d);
+    for (int j = threadIdx.x; j < d; j += kPT) kb[j] = st[8 + j];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kPT / 32;
+    const int64_t rows = ceil_div(n, P);
+    const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
+    const T *Ku = K + (int64_t)u * n * d;
+    double mx = 0.0;
+    for (int64_t l = lo + w; l < hi; l += nw) {
+        double s = 0.0;
+        for (int j = lane; j < d; j += 32) {
+            const double c = __dadd_rn(to_f64(Ku[l * d + j]), -kb[j]);
+            s = __dadd_rn(s, __dmul_rn(c, c));
+        }
+        s = warp_sum(s);
+        if (lane == 0) nrm2[(int64_t)u * n + l] = s;
+        mx = fmax(mx, s);
+    }
+    mx = block_max(mx, scr);
+    if (threadIdx.x == 0) rk2[(int64_t)u * P + p] = mx;
+}
+
+// tau (Eq. 7), g, mstar.  One thread per unit.
+__global__ void prologue_tau(int units, int64_t n, int d, int P, const double *rk2, const double *rq2,
+                             double rq_given, double beta, double *stats) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= units) return;
+    double mk = 0.0, mq = 0.0;
+    for (int p = 0; p < P; ++p) {
+        mk = fmax(mk, rk2[(int64_t)u * P + p]);
+        if (rq_given < 0.0) mq = fmax(mq, rq2[(int64_t)u * P + p]);
+    }
+    const double rk = sqrt(mk);
+    const double rq = rq_given >= 0.0 ? rq_given : sqrt(mq);
+    double tau = 1.0;
+    if (rq * rk > 0.0) {
+        const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
+        const double b0 = log((double)n) / (beta * rq * rk) + 2.0;
+        const double w = lambert_w0_dev(b0 / (2.0 * rho0));
+        tau = sqrt((rk / rq) * b0 / (2.0 * w));
+    }
+    const double g = beta / (tau * tau);
+    double *st = stats + (int64_t)u * (8 + d);
+    st[0] = tau;
+    st[1] = g;
+    st[2] = g * rk * rk;
+    st[3] = rk;
+    st[4] = rq;
+    st[5] = 0.0;
+    st[6] = 0.0;
+    st[7] = 0.0;
+}
+
+template <typename T>
+int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
+                      ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                      cudaStream_t st) {
+    const int units = D.units();
+    const int P = pp.P;
+    const int G = kPT / D.d;
+    const size_t smem = (size_t)G * D.d * (sizeof(double) + 2 * sizeof(float));
+    const int want_q = (rq < 0.0 && Q != nullptr) ? 1 : 0;
+    const int want_v = (V != nullptr) ? 1 : 0;
+    const int64_t mq = want_q ? (int64_t)D.group() * D.m : 0;
+    dim3 grid(P, units);
+    prologue_pass1<T><<<grid, kPT, smem, st>>>(static_cast<const T *>(Q), static_cast<const T *>(K),
+                                               static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
+                                               want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
+                                               (int64_t)D.group() * D.m);
+    prologue_kbar<T><<<units, 128, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
+                                            want_v ? static_cast<T *>(vmin) : nullptr,
+                                            want_v ? static_cast<T *>(vmax) : nullptr);
+    prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, P, stats, nrm2, pp.rk2);
+    prologue_tau<<<ceil_div(units, 128), 128, 0, st>>>(units, D.n, D.d, P, pp.rk2, pp.rq2,
+                                                      want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats);
+    return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
+}
+
+template <typename T>
+int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st) {
+    const int units = D.units();
+    const int G = kPT / D.d;
+    const size_t smem = (size_t)G * D.d * (sizeof(double) + 2 * sizeof(float));
+    dim3 grid(pp.P, units);
+    prologue_pass1<T><<<grid, kPT, smem, st>>>(nullptr, static_cast<const T *>(V), static_cast<const T *>(V), D.n,
+                                               0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0);
+    prologue_kbar<T><<<units, 128, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
+                                            static_cast<T *>(vmin), static_cast<T *>(vmax));
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+}
+
+}  // namespace
+
+int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st) {
+    if (D.dtype == 0) return launch_vrange_t<float>(D, V, pp, vmin, vmax, st);
+    return launch_vrange_t<__nv_bfloat16>(D, V, pp, vmin, vmax, st);
+}
+
+int prologue_num_splits(const Dims &D) {
+    const int64_t by_rows = ceil_div(std::max<int64_t>(D.n, (int64_t)D.group() * D.m), 256);
+    const int64_t cap = std::max<int64_t>(1, 1184 / D.units());
+    return (int)std::max<int64_t>(1, std::min<int64_t>(by_rows, cap));
+}
+
+int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
+                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                    cudaStream_t st) {
+    if (D.dtype == 0) return launch_prologue_t<float>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, st);
+    return launch_prologue_t<__nv_bfloat16>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, st);
+}
+
+}  // namespace wc

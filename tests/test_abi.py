@@ -1,0 +1,95 @@
+"""C ABI checks that need no GPU: the library builds and loads, exports every symbol declared in
+include/wildcat.h, and rejects invalid arguments before any CUDA call (nothing is launched)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "wildcat.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\**\s*(\w+)\s*\(", src, flags=re.M)) - {"if"})
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2602_10056_b200 as wc
+
+    return wc.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert {"wildcat_select", "wildcat_weights", "wildcat_attend", "wildcat_forward"} <= set(names)
+    for nm in names:
+        assert hasattr(L, nm), nm
+
+
+def test_library_is_sm100a():
+    import paper_2602_10056_b200.build as b
+
+    assert "arch=compute_100a,code=sm_100a" in " ".join(b.NVCC_FLAGS)
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {b.LIB} 2>/dev/null").read()
+    assert "sm_100a" in out
+
+
+def _shape(**kw):
+    from paper_2602_10056_b200 import _binding as B
+
+    base = dict(batch=1, heads_q=1, heads_kv=1, d=64, r=8, bins=1, dtype=1, reserved=0, m=16, n=100)
+    base.update(kw)
+    return B.wc_shape(**base)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(r=0), -2), (dict(r=101), -2), (dict(d=48), -2), (dict(heads_q=3, heads_kv=2), -2),
+    (dict(dtype=7), -3), (dict(bins=2), -7), (dict(m=-1), -2), (dict(n=0), -2),
+])
+def test_validation_before_launch(L, kw, code):
+    from paper_2602_10056_b200 import _binding as B
+
+    s = _shape(**kw)
+    o = B.make_opts()
+    dummy = ctypes.c_void_p(0x1000)
+    rc = L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), dummy, dummy, dummy, dummy, None, None, dummy, 1 << 30,
+                           None)
+    assert rc == code
+    assert L.wc_workspace_bytes(ctypes.byref(s), 3) == 0
+
+
+def test_null_and_workspace_errors(L):
+    from paper_2602_10056_b200 import _binding as B
+
+    s = _shape()
+    o = B.make_opts()
+    d = ctypes.c_void_p(0x1000)
+    assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, None, d, d, None, None, d, 1 << 30, None) == -1
+    need = L.wc_workspace_bytes(ctypes.byref(s), 3)
+    assert need > 0
+    assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, need - 1, None) == -4
+    assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None,
+                             ctypes.c_void_p(0x1001), 1 << 40, None) == -4
+    # rq < 0 requires Q
+    assert L.wildcat_select(ctypes.byref(s), ctypes.byref(o), None, d, d, d, d, d, d, 1 << 40, None) == -1
+    assert L.wc_strerror(-2).decode().startswith("invalid shape")
+
+
+def test_workspace_sizes_scale(L):
+    s1 = _shape(n=1000, r=10)
+    s2 = _shape(n=2000, r=20)
+    assert L.wc_workspace_bytes(ctypes.byref(s2), 0) > 3 * L.wc_workspace_bytes(ctypes.byref(s1), 0)
+    assert L.wc_workspace_bytes(ctypes.byref(s1), 2) == 0
+
+
+def test_product_package_has_no_oracle_dependency():
+    # the product path must never import or link the oracle (test infrastructure only)
+    pkg = os.path.join(ROOT, "paper_2602_10056_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "wildcat_oracle" not in txt, fn
