@@ -2,6 +2,8 @@
 // Argument validation, workspace carving and kernel sequencing only; every arithmetic step
 // of the method runs in the sm_100a kernels of prologue.cu / select.cu / weights.cu / attend.cu.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/wildcat.h"
@@ -17,7 +19,14 @@ thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev[kMaxEv] = {};
 thread_local int g_nev = 0;
 
+// WC_DEBUG_SYNC=1: synchronise after every stage and report the first CUDA error (debug only).
 void tmark(cudaStream_t st, bool first = false) {
+    static const bool dbg = std::getenv("WC_DEBUG_SYNC") != nullptr;
+    if (dbg) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) std::fprintf(stderr, "[wildcat] stage %d: %s\n", first ? 0 : g_nev, cudaGetErrorString(e));
+    }
     if (!g_timing) return;
     if (first) g_nev = 0;
     if (g_nev >= kMaxEv) return;
@@ -164,7 +173,7 @@ int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     if (rc) return rc;
     if (!o || !K || !S || !r_eff || !L || !stats) return WC_EINVAL;
     const double rq = rq_of(o);
-    if (rq < 0.0 && !Q) return WC_EINVAL;
+    if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_SELECT)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const wc::Dims D = dims_of(s);
@@ -230,7 +239,7 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     if (rc) return rc;
     if (!o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
     const double rq = rq_of(o);
-    if (rq < 0.0 && !Q) return WC_EINVAL;
+    if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const wc::Dims D = dims_of(s);

@@ -57,6 +57,15 @@ __device__ __forceinline__ double lambert_w0_dev(double z) {
 }
 
 // ---------------------------------------------------------------- reductions
+// Warp index computed through opaque PTX.  With a plain `threadIdx.x >> 5`, nvcc 12.9 (sm_100a)
+// folded `&scratch[w]` into `scratch_bytes + (tid >> 2)` -- correct only for lanes 0..3 -- and
+// reused it for every lane (misaligned shared access).  The opaque shift blocks that rewrite.
+__device__ __forceinline__ int warp_index() {
+    int w;
+    asm volatile("shr.u32 %0, %1, 5;" : "=r"(w) : "r"((unsigned)threadIdx.x));
+    return w;
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -71,7 +80,7 @@ template <typename T> __device__ __forceinline__ T warp_max(T v) {
 // Deterministic block sum (fixed tree order); result valid in all threads.
 // `scratch` needs blockDim/32 doubles.  Contains __syncthreads.
 __device__ __forceinline__ double block_sum(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_index(), nw = blockDim.x >> 5;
     v = warp_sum(v);
     __syncthreads();
     if (lane == 0) scratch[w] = v;
@@ -89,7 +98,7 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
 }
 
 __device__ __forceinline__ double block_max(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_index(), nw = blockDim.x >> 5;
     v = warp_max(v);
     __syncthreads();
     if (lane == 0) scratch[w] = v;
@@ -108,15 +117,16 @@ __device__ __forceinline__ double block_max(double v, double *scratch) {
 // Block-wide exclusive scan of one double per thread in a fixed order (warp shuffle
 // scan + scan of warp totals).  Returns the exclusive prefix; *total gets the sum.
 __device__ __forceinline__ double block_exclusive_scan(double v, double *scratch, double *total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = warp_index(), nw = blockDim.x >> 5;
     double incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const double y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
+    const double wtot = __shfl_sync(0xffffffffu, incl, 31);
     __syncthreads();
-    if (lane == 31) scratch[w] = incl;
+    if (lane == 0) scratch[w] = wtot;
     __syncthreads();
     if (w == 0) {
         double t = lane < nw ? scratch[lane] : 0.0;

@@ -175,7 +175,7 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
     const int P = pp.P;
     const int G = kPT / D.d;
     const size_t smem = (size_t)G * D.d * (sizeof(double) + 2 * sizeof(float));
-    const int want_q = (rq < 0.0 && Q != nullptr) ? 1 : 0;
+    const int want_q = (rq < 0.0 && Q != nullptr && D.m > 0) ? 1 : 0;
     const int want_v = (V != nullptr) ? 1 : 0;
     const int64_t mq = want_q ? (int64_t)D.group() * D.m : 0;
     dim3 grid(P, units);
