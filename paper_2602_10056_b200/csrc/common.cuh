@@ -19,6 +19,28 @@ template <typename T> __device__ __forceinline__ T from_f32(float x);
 template <> __device__ __forceinline__ float from_f32<float>(float x) { return x; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
+// Load 8 consecutive elements (16- or 32-byte aligned) and widen to fp64 (exact).
+template <typename T> struct Vec8;
+template <> struct Vec8<__nv_bfloat16> {
+    static __device__ __forceinline__ void load(const __nv_bfloat16 *p, double out[8]) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            out[2 * k] = (double)__uint_as_float(wd[k] << 16);
+            out[2 * k + 1] = (double)__uint_as_float(wd[k] & 0xffff0000u);
+        }
+    }
+};
+template <> struct Vec8<float> {
+    static __device__ __forceinline__ void load(const float *p, double out[8]) {
+        const float4 x = __ldg(reinterpret_cast<const float4 *>(p));
+        const float4 y = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+        out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+        out[4] = y.x; out[5] = y.y; out[6] = y.z; out[7] = y.w;
+    }
+};
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based generator of Salmon et al. (SC'11).  The pivot uniform of round i of
 // unit u is built from Philox4x32-10(key = seed, ctr = (i, u_lo, u_hi, 'PIVT')) with

@@ -16,6 +16,7 @@ namespace {
 constexpr int kPT = 256;  // threads per prologue block
 
 // Pass 1: per (split p, unit u): column sums of K (fp64), column min/max of V, max ||q||^2.
+// Each thread owns 8 consecutive columns (16/32-byte vector loads); CPR = d/8 threads per row.
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, const T *__restrict__ K,
                                                       const T *__restrict__ V, int64_t n, int64_t mq, int d,
@@ -24,37 +25,41 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
                                                       int64_t q_unit_stride_rows) {
     extern __shared__ double sm1[];
     const int p = blockIdx.x, u = blockIdx.y;
-    const int G = kPT / d;  // row groups
-    const int grp = threadIdx.x / d, j = threadIdx.x % d;
+    const int CPR = d / 8, RG = kPT / CPR;
+    const int rg = threadIdx.x / CPR, cj = threadIdx.x % CPR;
     const int64_t rows = ceil_div(n, P);
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
     const T *Ku = K + (int64_t)u * n * d;
     const T *Vu = V + (int64_t)u * n * d;
-    double cs = 0.0;
-    float lo_v = 3.0e38f, hi_v = -3.0e38f;
-    if (grp < G) {
-        for (int64_t l = lo + grp; l < hi; l += G) {
-            cs += to_f64(Ku[l * d + j]);
-            if (want_v) {
-                const float v = to_f32(Vu[l * d + j]);
-                lo_v = fminf(lo_v, v);
-                hi_v = fmaxf(hi_v, v);
-            }
+    double cs[8];
+    float mn[8], mx[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { cs[k] = 0.0; mn[k] = 3.0e38f; mx[k] = -3.0e38f; }
+    for (int64_t l = lo + rg; l < hi; l += RG) {
+        double x[8];
+        Vec8<T>::load(Ku + l * d + 8 * cj, x);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cs[k] += x[k];
+        if (want_v) {
+            Vec8<T>::load(Vu + l * d + 8 * cj, x);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { mn[k] = fminf(mn[k], (float)x[k]); mx[k] = fmaxf(mx[k], (float)x[k]); }
         }
     }
-    double *s_cs = sm1;                                // [G][d]
-    float *s_lo = reinterpret_cast<float *>(sm1 + G * d);  // [G][d]
-    float *s_hi = s_lo + G * d;
-    if (grp < G) {
-        s_cs[grp * d + j] = cs;
-        s_lo[grp * d + j] = lo_v;
-        s_hi[grp * d + j] = hi_v;
+    double *s_cs = sm1;                                    // [RG][d]
+    float *s_lo = reinterpret_cast<float *>(sm1 + RG * d);  // [RG][d]
+    float *s_hi = s_lo + RG * d;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        s_cs[rg * d + 8 * cj + k] = cs[k];
+        s_lo[rg * d + 8 * cj + k] = mn[k];
+        s_hi[rg * d + 8 * cj + k] = mx[k];
     }
     __syncthreads();
     if (threadIdx.x < d) {
         double t = 0.0;
         float a = 3.0e38f, b = -3.0e38f;
-        for (int g2 = 0; g2 < G; ++g2) {
+        for (int g2 = 0; g2 < RG; ++g2) {
             t += s_cs[g2 * d + threadIdx.x];
             a = fminf(a, s_lo[g2 * d + threadIdx.x]);
             b = fmaxf(b, s_hi[g2 * d + threadIdx.x]);
@@ -65,87 +70,115 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
         vmax[o] = b;
     }
     if (want_q) {
-        // one warp per query row, lanes over d
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kPT / 32;
         const int64_t qrows = ceil_div(mq, P);
         const int64_t qlo = (int64_t)p * qrows, qhi = min(mq, qlo + qrows);
         const T *Qu = Q + (int64_t)u * q_unit_stride_rows * d;
-        double mx = 0.0;
-        for (int64_t i = qlo + w; i < qhi; i += nw) {
-            double s = 0.0;
-            for (int jj = lane; jj < d; jj += 32) {
-                const double x = to_f64(Qu[i * d + jj]);
-                s += x * x;
+        double best = 0.0;
+        for (int64_t i0 = qlo; i0 < qhi; i0 += RG) {
+            const int64_t i = i0 + rg;
+            double sq = 0.0;
+            if (i < qhi) {
+                double x[8];
+                Vec8<T>::load(Qu + i * d + 8 * cj, x);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sq += x[k] * x[k];
             }
-            s = warp_sum(s);
-            mx = fmax(mx, s);
+            for (int o = 1; o < CPR; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            best = fmax(best, sq);
         }
         __shared__ double scr[40];
-        mx = block_max(mx, scr);
-        if (threadIdx.x == 0) rq2[(int64_t)u * P + p] = mx;
+        best = block_max(best, scr);
+        if (threadIdx.x == 0) rq2[(int64_t)u * P + p] = best;
     }
 }
 
-// Finalise kbar (fixed-order sum over splits) and the value range.
+// Finalise kbar (fixed-order sum over splits) and the value range.  G groups of d threads.
 template <typename T>
-__global__ void prologue_kbar(int64_t n, int d, int P, const double *colsum, const float *vmin_p,
-                              const float *vmax_p, double *stats, T *vmin, T *vmax) {
-    const int u = blockIdx.x, j = threadIdx.x;
-    if (j >= d) return;
+__global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, const double *colsum,
+                                                     const float *vmin_p, const float *vmax_p, double *stats,
+                                                     T *vmin, T *vmax) {
+    __shared__ double s_t[kPT];
+    __shared__ float s_a[kPT], s_b[kPT];
+    const int u = blockIdx.x, G = kPT / d, g = threadIdx.x / d, j = threadIdx.x % d;
     double t = 0.0;
     float a = 3.0e38f, b = -3.0e38f;
-    for (int p = 0; p < P; ++p) {
+#pragma unroll 8
+    for (int p = g; p < P; p += G) {
         const int64_t o = ((int64_t)u * P + p) * d + j;
         t += colsum[o];
         a = fminf(a, vmin_p[o]);
         b = fmaxf(b, vmax_p[o]);
     }
-    if (stats) stats[(int64_t)u * (8 + d) + 8 + j] = t / (double)n;
-    if (vmin) {
-        vmin[(int64_t)u * d + j] = from_f32<T>(a);
-        vmax[(int64_t)u * d + j] = from_f32<T>(b);
+    s_t[threadIdx.x] = t;
+    s_a[threadIdx.x] = a;
+    s_b[threadIdx.x] = b;
+    __syncthreads();
+    if (threadIdx.x < d) {
+        double tt = 0.0;
+        float aa = 3.0e38f, bb = -3.0e38f;
+        for (int gg = 0; gg < G; ++gg) {
+            tt += s_t[gg * d + j];
+            aa = fminf(aa, s_a[gg * d + j]);
+            bb = fmaxf(bb, s_b[gg * d + j]);
+        }
+        if (stats) stats[(int64_t)u * (8 + d) + 8 + j] = tt / (double)n;
+        if (vmin) {
+            vmin[(int64_t)u * d + j] = from_f32<T>(aa);
+            vmax[(int64_t)u * d + j] = from_f32<T>(bb);
+        }
     }
 }
 
-// Pass 2: nrm2_l = ||k_l - kbar||^2 (fp64) and the split max.  One warp per key.
+// Pass 2: nrm2_l = ||k_l - kbar||^2 (fp64) and the split max.  CPR threads per key.
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, int64_t n, int d, int P,
                                                       const double *stats, double *nrm2, double *rk2) {
     __shared__ double kb[128];
     __shared__ double scr[40];
     const int p = blockIdx.x, u = blockIdx.y;
+    const int CPR = d / 8, RG = kPT / CPR;
+    const int rg = threadIdx.x / CPR, cj = threadIdx.x % CPR;
     const double *st = stats + (int64_t)u * (8 + d);
     for (int j = threadIdx.x; j < d; j += kPT) kb[j] = st[8 + j];
     __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kPT / 32;
     const int64_t rows = ceil_div(n, P);
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
     const T *Ku = K + (int64_t)u * n * d;
-    double mx = 0.0;
-    for (int64_t l = lo + w; l < hi; l += nw) {
-        double s = 0.0;
-        for (int j = lane; j < d; j += 32) {
-            const double c = __dadd_rn(to_f64(Ku[l * d + j]), -kb[j]);
-            s = __dadd_rn(s, __dmul_rn(c, c));
+    double best = 0.0;
+    for (int64_t l0 = lo; l0 < hi; l0 += RG) {
+        const int64_t l = l0 + rg;
+        double sq = 0.0;
+        if (l < hi) {
+            double x[8];
+            Vec8<T>::load(Ku + l * d + 8 * cj, x);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double c = __dadd_rn(x[k], -kb[8 * cj + k]);
+                sq = __dadd_rn(sq, __dmul_rn(c, c));
+            }
         }
-        s = warp_sum(s);
-        if (lane == 0) nrm2[(int64_t)u * n + l] = s;
-        mx = fmax(mx, s);
+        for (int o = 1; o < CPR; o <<= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+        if (l < hi && cj == 0) nrm2[(int64_t)u * n + l] = sq;
+        best = fmax(best, sq);
     }
-    mx = block_max(mx, scr);
-    if (threadIdx.x == 0) rk2[(int64_t)u * P + p] = mx;
+    best = block_max(best, scr);
+    if (threadIdx.x == 0) rk2[(int64_t)u * P + p] = best;
 }
 
 // tau (Eq. 7), g, mstar.  One thread per unit.
+// One warp per unit: maxima over the P splits, then lane 0 evaluates Eq. 7.
 __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *rk2, const double *rq2,
                              double rq_given, double beta, double *stats) {
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (u >= units) return;
     double mk = 0.0, mq = 0.0;
-    for (int p = 0; p < P; ++p) {
+    for (int p = lane; p < P; p += 32) {
         mk = fmax(mk, rk2[(int64_t)u * P + p]);
         if (rq_given < 0.0) mq = fmax(mq, rq2[(int64_t)u * P + p]);
     }
+    mk = warp_max(mk);
+    mq = warp_max(mq);
+    if (lane != 0) return;
     const double rk = sqrt(mk);
     const double rq = rq_given >= 0.0 ? rq_given : sqrt(mq);
     double tau = 1.0;
@@ -173,8 +206,8 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                       cudaStream_t st) {
     const int units = D.units();
     const int P = pp.P;
-    const int G = kPT / D.d;
-    const size_t smem = (size_t)G * D.d * (sizeof(double) + 2 * sizeof(float));
+    const int RG = kPT / (D.d / 8);
+    const size_t smem = (size_t)RG * D.d * (sizeof(double) + 2 * sizeof(float));
     const int want_q = (rq < 0.0 && Q != nullptr && D.m > 0) ? 1 : 0;
     const int want_v = (V != nullptr) ? 1 : 0;
     const int64_t mq = want_q ? (int64_t)D.group() * D.m : 0;
@@ -183,11 +216,11 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                                                static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
                                                (int64_t)D.group() * D.m);
-    prologue_kbar<T><<<units, 128, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
+    prologue_kbar<T><<<units, kPT, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
                                             want_v ? static_cast<T *>(vmin) : nullptr,
                                             want_v ? static_cast<T *>(vmax) : nullptr);
     prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, P, stats, nrm2, pp.rk2);
-    prologue_tau<<<ceil_div(units, 128), 128, 0, st>>>(units, D.n, D.d, P, pp.rk2, pp.rq2,
+    prologue_tau<<<ceil_div(units, 4), 128, 0, st>>>(units, D.n, D.d, P, pp.rk2, pp.rq2,
                                                       want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats);
     return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
 }
@@ -195,12 +228,12 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
 template <typename T>
 int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st) {
     const int units = D.units();
-    const int G = kPT / D.d;
-    const size_t smem = (size_t)G * D.d * (sizeof(double) + 2 * sizeof(float));
+    const int RG = kPT / (D.d / 8);
+    const size_t smem = (size_t)RG * D.d * (sizeof(double) + 2 * sizeof(float));
     dim3 grid(pp.P, units);
     prologue_pass1<T><<<grid, kPT, smem, st>>>(nullptr, static_cast<const T *>(V), static_cast<const T *>(V), D.n,
                                                0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0);
-    prologue_kbar<T><<<units, 128, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
+    prologue_kbar<T><<<units, kPT, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
                                             static_cast<T *>(vmin), static_cast<T *>(vmax));
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }

@@ -45,39 +45,24 @@ struct SelArgs {
     uint64_t seed;
 };
 
-// load 8 consecutive elements as fp64
-template <typename T> struct Vec8;
-template <> struct Vec8<__nv_bfloat16> {
-    static __device__ __forceinline__ void load(const __nv_bfloat16 *p, double out[8]) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            out[2 * k] = (double)__uint_as_float(w[k] << 16);
-            out[2 * k + 1] = (double)__uint_as_float(w[k] & 0xffff0000u);
-        }
-    }
-};
-template <> struct Vec8<float> {
-    static __device__ __forceinline__ void load(const float *p, double out[8]) {
-        const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
-        const float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
-        out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
-        out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
-    }
-};
+constexpr int kST = 256;  // keys per super-tile (8 warp-tiles of 32 keys)
+constexpr int kTK = kST / 32;
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     extern __shared__ double sm[];
-    double *kb = sm;             // [D]   kbar
-    double *kcs = kb + D;        // [D]   centred pivot key
-    double *fs = kcs + D;        // [r]   F[0:i, s]
-    double *scr = fs + a.r;      // [40]  reduction scratch
-    __shared__ int sh_s, sh_cstar, sh_done;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, w = warp_index(), nw = nt >> 5;
+    const int H = nt / kST;           // threads per key in the kernel-dot phase (1 or 2)
+    double *kb = sm;                  // [D]    kbar
+    double *kcs = kb + D;             // [D]    centred pivot key
+    double *fs = kcs + D;             // [r]    F[0:i, s]
+    double *red = fs + a.r;           // [nw][kST] per-warp partial F-dots
+    double *kd = red + nw * kST;      // [H][kST] partial kernel dots
+    double *scr = kd + 2 * kST;       // [40]   reduction scratch
+    __shared__ int sh_s, sh_cstar, sh_done, sh_last;
     __shared__ double sh_t, sh_ps;
 
-    const int tid = threadIdx.x, nt = blockDim.x;
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
     const int64_t n = a.n;
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
@@ -106,7 +91,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     if (a.cpu > 1) group_barrier(bar, a.cpu, epoch++);
     else __syncthreads();
 
-    double T0 = 0.0, theta = 0.0;
+    double T0 = 0.0, theta = 0.0;  // meaningful in warp 0
     int i = 0;
     for (; i < a.r; ++i) {
         double *cur = (i & 1) ? p1 : p0;
@@ -114,43 +99,61 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
         const double *pc = partu + (i & 1) * kMaxCpu;
         double *pn = partu + ((i + 1) & 1) * kMaxCpu;
 
-        // ---- A1: totals, exhaustion, uniform, owning CTA (fixed order; identical in every CTA)
-        if (tid == 0) {
-            double Ttot = 0.0;
-            for (int cc = 0; cc < a.cpu; ++cc) Ttot += __ldcg(pc + cc);
+        // ---- A1a (warp 0): total T over the per-CTA residual sums, exhaustion test, uniform,
+        // owning CTA c* = min{c : prefix_c > t}.  Fixed order => identical in every CTA.
+        if (w == 0) {
+            const int per = (a.cpu + 31) / 32;
+            const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
+            double v = 0.0;
+            for (int cc = b0; cc < b1; ++cc) v += __ldcg(pc + cc);
+            double incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const double Ttot = __shfl_sync(0xffffffffu, incl, 31);
             if (i == 0) {
                 T0 = Ttot;
                 theta = 1000.0 * (double)a.r * 2.220446049250313e-16 * T0;
             }
-            sh_done = (Ttot <= theta) ? 1 : 0;
-            if (!sh_done) {
+            const bool done = Ttot <= theta;
+            if (!done) {
                 const double t = pivot_uniform(a.seed, (uint32_t)i, (uint64_t)u) * Ttot;
-                double acc = 0.0, excl = 0.0;
-                int cs = -1, last = -1;
-                double last_excl = 0.0;
-                for (int cc = 0; cc < a.cpu; ++cc) {
-                    const double v = __ldcg(pc + cc);
-                    if (v > 0.0) { last = cc; last_excl = acc; }
-                    const double nacc = acc + v;
-                    if (cs < 0 && nacc > t) { cs = cc; excl = acc; }
-                    acc = nacc;
+                const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
+                const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
+                const int L = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
+                if (lane == L) {
+                    double acc = incl - v;
+                    int cs = -1, last = -1;
+                    double excl = 0.0, last_excl = 0.0;
+                    for (int cc = b0; cc < b1; ++cc) {
+                        const double pv = __ldcg(pc + cc);
+                        if (pv > 0.0) { last = cc; last_excl = acc; }
+                        const double nacc = acc + pv;
+                        if (cs < 0 && hit && nacc > t) { cs = cc; excl = acc; }
+                        acc = nacc;
+                    }
+                    if (cs < 0) { cs = last; excl = last_excl; }  // rounding fallback (reading Z2)
+                    sh_cstar = cs;
+                    sh_t = t - excl;
                 }
-                if (cs < 0) { cs = last; excl = last_excl; }
-                sh_cstar = cs;
-                sh_t = t - excl;
             }
-            sh_s = 0x7fffffff;
+            if (lane == 0) {
+                sh_done = done ? 1 : 0;
+                sh_s = 0x7fffffff;
+                sh_last = -1;
+            }
         }
         __syncthreads();
         if (sh_done) break;
         const int cstar = sh_cstar;
         const double tp = sh_t;
-        // ---- A1: inverse CDF inside the owning CTA's slice (block scan, fixed order)
+        // ---- A1b: inverse CDF inside the owning CTA's slice (block scan, fixed order)
         {
             const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
             const int64_t shi = std::min<int64_t>(n, slo + chunk);
-            const int64_t len = shi - slo;
-            const int64_t per = ceil_div(len, nt);
+            const int64_t per = ceil_div(shi - slo, nt);
             const int64_t b0 = slo + (int64_t)tid * per, b1 = std::min<int64_t>(shi, b0 + per);
             double v = 0.0;
             for (int64_t l = b0; l < b1; ++l) v += __ldcg(cur + l);
@@ -165,16 +168,9 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
                 if (found < 0 && run > tp) found = (int)l;
             }
             if (found >= 0) atomicMin(&sh_s, found);
+            if (lastpos >= 0) atomicMax(&sh_last, lastpos);
             __syncthreads();
-            if (sh_s == 0x7fffffff) {
-                // rounding left no l with prefix > t': last l with p_l > 0 (reading Z2)
-                __shared__ int sh_last;
-                if (tid == 0) sh_last = -1;
-                __syncthreads();
-                if (lastpos >= 0) atomicMax(&sh_last, lastpos);
-                __syncthreads();
-                if (tid == 0) sh_s = sh_last;
-            }
+            if (tid == 0 && sh_s == 0x7fffffff) sh_s = sh_last;  // rounding fallback (reading Z2)
             __syncthreads();
         }
         const int s = sh_s;
@@ -183,48 +179,92 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
         for (int j = tid; j < i; j += nt) fs[j] = __ldcg(Fu + (int64_t)j * n + s);
         if (tid == 0) sh_ps = __ldcg(cur + s);
         __syncthreads();
-        const double ps = sh_ps;
-        const double rs = sqrt(ps);
-        const bool owner = (c == cstar);
-        if (owner) {
+        const double rs = sqrt(sh_ps);
+        if (c == cstar) {
             for (int j = tid; j < i; j += nt) a.L[((int64_t)u * a.r + i) * a.r + j] = fs[j];
             if (tid == 0) a.S[(int64_t)u * a.r + i] = s;
         }
-        // ---- A2: kernel column, rank update, downdate of own keys
+        // ---- A2: kernel column, rank update and downdate of own keys, one super-tile of
+        // kST keys at a time.  Phase A: warps split the rows j of F[0:i, tile] (coalesced
+        // 256-byte row segments, kTK independent loads per row per lane); phase B: kernel dot
+        // <k_l - kbar, k_s - kbar> (H threads per key); phase C: combine in fixed order.
         loc = 0.0;
         double *Fi = Fu + (int64_t)i * n;
-        for (int64_t l = lo + tid; l < hi; l += nt) {
-            double kv[8];
-            double dot = 0.0;
+        for (int64_t k0 = lo; k0 < hi; k0 += kST) {
+            {
+                double acc[kTK];
 #pragma unroll
-            for (int j0 = 0; j0 < D; j0 += 8) {
-                Vec8<T>::load(Ku + l * D + j0, kv);
+                for (int t = 0; t < kTK; ++t) acc[t] = 0.0;
+                int j = w;
+                for (; j + nw < i; j += 2 * nw) {
+                    const double *F0 = Fu + (int64_t)j * n + k0 + lane;
+                    const double *F1 = F0 + (int64_t)nw * n;
+                    double x0[kTK], x1[kTK];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    dot = __dadd_rn(dot, __dmul_rn(__dadd_rn(kv[k], -kb[j0 + k]), kcs[j0 + k]));
+                    for (int t = 0; t < kTK; ++t) {
+                        const bool ok = k0 + 32 * t + lane < hi;
+                        x0[t] = ok ? __ldcg(F0 + 32 * t) : 0.0;
+                        x1[t] = ok ? __ldcg(F1 + 32 * t) : 0.0;
+                    }
+                    const double f0 = fs[j], f1 = fs[j + nw];
+#pragma unroll
+                    for (int t = 0; t < kTK; ++t) {
+                        acc[t] = __dadd_rn(acc[t], __dmul_rn(x0[t], f0));
+                        acc[t] = __dadd_rn(acc[t], __dmul_rn(x1[t], f1));
+                    }
+                }
+                if (j < i) {
+                    const double *F0 = Fu + (int64_t)j * n + k0 + lane;
+                    const double f0 = fs[j];
+#pragma unroll
+                    for (int t = 0; t < kTK; ++t) {
+                        const bool ok = k0 + 32 * t + lane < hi;
+                        const double x0 = ok ? __ldcg(F0 + 32 * t) : 0.0;
+                        acc[t] = __dadd_rn(acc[t], __dmul_rn(x0, f0));
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < kTK; ++t) red[w * kST + 32 * t + lane] = acc[t];
             }
-            const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
-            double acc = 0.0;
-            const double *Fl = Fu + l;
-            int j = 0;
-            for (; j + 8 <= i; j += 8) {
-                double f[8];
+            {
+                const int kk = tid % kST, half = tid / kST;
+                const int64_t l = k0 + kk;
+                double dot = 0.0;
+                if (l < hi) {
+                    constexpr int Dh = D;  // elements per thread when H == 1
+                    const int len = Dh / H, j0 = half * len;
+                    for (int jj = 0; jj < len; jj += 8) {
+                        double kv[8];
+                        Vec8<T>::load(Ku + l * D + j0 + jj, kv);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) f[k] = __ldcg(Fl + (int64_t)(j + k) * n);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(f[k], fs[j + k]));
+                        for (int q = 0; q < 8; ++q)
+                            dot = __dadd_rn(dot, __dmul_rn(__dadd_rn(kv[q], -kb[j0 + jj + q]), kcs[j0 + jj + q]));
+                    }
+                }
+                kd[half * kST + kk] = dot;
             }
-            for (; j < i; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldcg(Fl + (int64_t)j * n), fs[j]));
-            const double f = (hval - acc) / rs;
-            Fi[l] = f;
-            double q = __dadd_rn(__ldcg(cur + l), -__dmul_rn(f, f));
-            q = q > 0.0 ? q : 0.0;
-            if (l == s) {
-                q = 0.0;
-                a.L[((int64_t)u * a.r + i) * a.r + i] = f;
+            __syncthreads();
+            if (tid < kST) {
+                const int64_t l = k0 + tid;
+                if (l < hi) {
+                    double acc = 0.0;
+                    for (int ww = 0; ww < nw; ++ww) acc = __dadd_rn(acc, red[ww * kST + tid]);
+                    double dot = kd[tid];
+                    for (int hh = 1; hh < H; ++hh) dot = __dadd_rn(dot, kd[hh * kST + tid]);
+                    const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
+                    const double f = (hval - acc) / rs;
+                    Fi[l] = f;
+                    double q = __dadd_rn(__ldcg(cur + l), -__dmul_rn(f, f));
+                    q = q > 0.0 ? q : 0.0;
+                    if (l == s) {
+                        q = 0.0;
+                        a.L[((int64_t)u * a.r + i) * a.r + i] = f;
+                    }
+                    nxt[l] = q;
+                    loc += q;
+                }
             }
-            nxt[l] = q;
-            loc += q;
+            __syncthreads();
         }
         loc = block_sum(loc, scr);
         if (tid == 0) pn[c] = loc;
@@ -244,12 +284,12 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
     a.cpu = select_ctas_per_unit(Dm); a.seed = seed;
-    const size_t smem = (size_t)(2 * D + Dm.r + 40) * sizeof(double);
+    const int threads = (Dm.n / a.cpu >= 384) ? kSelThreads : 256;
+    const size_t smem = (size_t)(2 * D + Dm.r + (threads / 32) * kST + 2 * kST + 40) * sizeof(double);
     auto kern = rpc_select_kernel<T, D>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
-    const int threads = (Dm.n / a.cpu >= 384) ? kSelThreads : 256;
     const dim3 grid(a.units * a.cpu);
     if (a.cpu > 1) {
         void *args[] = {&a};
