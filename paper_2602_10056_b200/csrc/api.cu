@@ -91,7 +91,7 @@ void carve_select(Carver &c, const wc_shape *s, SelectWs &w) {
     w.pp.rk2 = c.take<double>(U * P);
     w.sb.nrm2 = c.take<double>(U * D.n);
     w.sb.p = c.take<double>(2 * U * D.n);
-    w.sb.F = c.take<double>(U * (size_t)D.r * D.n);
+    w.sb.F = c.take<double>(U * wc::f_elems_per_unit(D.n, D.r, wc::select_ctas_per_unit(D)));
     w.sb.part = c.take<double>(U * 2 * wc::kMaxCpu);
     w.sb.bar = c.take<unsigned>(U);
 }

@@ -36,11 +36,23 @@ int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin,
 struct SelectBufs {
     double *nrm2;   // [units][n]
     double *p;      // [2][units][n]
-    double *F;      // [units][r][n]
+    double *F;      // [units][r][f_ld(n)]
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
 };
 constexpr int kMaxCpu = 1024;
+inline int64_t f_ld(int64_t n) { return (n + 31) / 32 * 32; }  // row stride of F (row-major kernel)
+// Tile-major F of the TMA kernel: per unit [cpu][nst][r][256] doubles, nst = 256-key super-tiles per slice.
+inline int f_tile_nst(int64_t n, int cpu) {
+    const int64_t chunk = ((n + cpu - 1) / cpu + 31) / 32 * 32;
+    return (int)((chunk + 255) / 256);
+}
+int select_ctas_per_unit(const struct Dims &D);
+inline size_t f_elems_per_unit(int64_t n, int r, int cpu) {
+    const size_t rowmajor = (size_t)r * f_ld(n);
+    const size_t tiles = (size_t)cpu * f_tile_nst(n, cpu) * r * 256;
+    return rowmajor > tiles ? rowmajor : tiles;
+}
 
 int select_ctas_per_unit(const Dims &D);
 // A1+A2: r rounds of RP-Cholesky.  Returns launches or -1.

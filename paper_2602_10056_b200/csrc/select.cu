@@ -19,6 +19,11 @@
 //
 // HBM traffic per unit: n r (d e + 24) + 4 n r (r-1) bytes.
 #include <algorithm>
+#include <type_traits>
+#include <cstdlib>
+#include <cstring>
+#include <cstdio>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -41,9 +46,23 @@ struct SelArgs {
     int32_t *r_eff;
     double *L;
     int64_t n;
+    int64_t ldF;  // row stride of F (n rounded up to 32: every row segment is 256-byte aligned)
     int units, r, cpu;
     uint64_t seed;
+    unsigned long long *trace;  // debug (WC_SELECT_TRACE): [r][16] globaltimer stamps of CTA 0
+    int rkeep;                  // F rows [0, rkeep) are kept L2-resident (evict_last); later rows evict_first
+    int nstm;                   // TMA kernel: super-tiles per CTA slice (tile-major F: [cpu][nstm][r][256])
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define WC_TR(k)                                                                              \
+    do {                                                                                      \
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && i < a.r) a.trace[i * 16 + (k)] = gtimer(); \
+    } while (0)
 
 constexpr int kST = 256;  // keys per super-tile (8 warp-tiles of 32 keys)
 constexpr int kTK = kST / 32;
@@ -73,7 +92,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     const double g = st[1], mstar = st[2];
     double *p0 = a.p + (int64_t)u * n;
     double *p1 = a.p + ((int64_t)a.units + u) * n;
-    double *Fu = a.F + (int64_t)u * a.r * n;
+    double *Fu = a.F + (int64_t)u * a.r * a.ldF;
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
     unsigned *bar = a.bar + u;
     for (int j = tid; j < D; j += nt) kb[j] = st[8 + j];
@@ -176,7 +195,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
         const int s = sh_s;
         // ---- pivot data: centred k_s (fp64) and F[0:i, s]
         for (int j = tid; j < D; j += nt) kcs[j] = __dadd_rn(to_f64(Ku[(int64_t)s * D + j]), -kb[j]);
-        for (int j = tid; j < i; j += nt) fs[j] = __ldcg(Fu + (int64_t)j * n + s);
+        for (int j = tid; j < i; j += nt) fs[j] = __ldcg(Fu + (int64_t)j * a.ldF + s);
         if (tid == 0) sh_ps = __ldcg(cur + s);
         __syncthreads();
         const double rs = sqrt(sh_ps);
@@ -189,7 +208,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
         // 256-byte row segments, kTK independent loads per row per lane); phase B: kernel dot
         // <k_l - kbar, k_s - kbar> (H threads per key); phase C: combine in fixed order.
         loc = 0.0;
-        double *Fi = Fu + (int64_t)i * n;
+        double *Fi = Fu + (int64_t)i * a.ldF;
         for (int64_t k0 = lo; k0 < hi; k0 += kST) {
             {
                 double acc[kTK];
@@ -197,8 +216,8 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
                 for (int t = 0; t < kTK; ++t) acc[t] = 0.0;
                 int j = w;
                 for (; j + nw < i; j += 2 * nw) {
-                    const double *F0 = Fu + (int64_t)j * n + k0 + lane;
-                    const double *F1 = F0 + (int64_t)nw * n;
+                    const double *F0 = Fu + (int64_t)j * a.ldF + k0 + lane;
+                    const double *F1 = F0 + (int64_t)nw * a.ldF;
                     double x0[kTK], x1[kTK];
 #pragma unroll
                     for (int t = 0; t < kTK; ++t) {
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
                     }
                 }
                 if (j < i) {
-                    const double *F0 = Fu + (int64_t)j * n + k0 + lane;
+                    const double *F0 = Fu + (int64_t)j * a.ldF + k0 + lane;
                     const double f0 = fs[j];
 #pragma unroll
                     for (int t = 0; t < kTK; ++t) {
@@ -277,20 +296,569 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     }
 }
 
+// =====================================================================================
+// TMA-pipelined variant.  8 compute warps + 1 producer warp.  The producer streams the CTA's
+// slice of F[0:i-1, :] (rows written >= 2 rounds ago) into a shared-memory ring of stages
+// (kRPS rows x 256 keys fp64 = 16 KB each) with 1-D bulk async copies (cp.async.bulk, the TMA
+// engine) completing on mbarriers.  It runs ahead of the compute warps by up to NS stages,
+// across round boundaries: while the compute warps wait at the grid barrier and search the next
+// pivot, the next round's F tiles are already landing in shared memory.  Row i-1 (written by
+// this CTA in the previous round) is read directly.  Compute warps synchronise among themselves
+// with named barrier 1 so the producer never joins a CTA-wide barrier.
+// =====================================================================================
+constexpr int kCW = 8;                // compute warps
+constexpr int kCT = kCW * 32;         // compute threads (= kST: one key per thread in phases B/C)
+constexpr int kRPS = 8;               // F rows per ring stage (one per compute warp)
+constexpr int kTmaThreads = kCT + 32; // + producer warp
+static_assert(kCT == kST, "one compute thread per super-tile key");
+
+__device__ __forceinline__ void cw_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory"); }
+
+__device__ __forceinline__ double cw_sum(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, w = warp_index();
+    v = warp_sum(v);
+    cw_sync();
+    if (lane == 0) scratch[w] = v;
+    cw_sync();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kCW; ++k) t += scratch[k];
+    cw_sync();
+    return t;
+}
+
+__device__ __forceinline__ double cw_exclusive_scan(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, w = warp_index();
+    double incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const double wtot = __shfl_sync(0xffffffffu, incl, 31);
+    cw_sync();
+    if (lane == 0) scratch[w] = wtot;
+    cw_sync();
+    double off = 0.0;
+    for (int k = 0; k < w; ++k) off += scratch[k];
+    const double excl = off + (incl - v);
+    cw_sync();
+    return excl;
+}
+
+// Grid-group barrier of the compute threads: bar.sync orders the CTA's writes before thread 0's
+// release-add (release is cumulative); the acquire-load orders everything after.  Thread 0 then
+// publishes `rounds` (this CTA's F rows complete) to the producer warp.
+__device__ __forceinline__ void cw_group_barrier(unsigned *ctr, unsigned count, unsigned epoch,
+                                                 volatile int *rounds_done, int rounds) {
+    cw_sync();
+    if (threadIdx.x == 0) {
+        if (count > 1) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+            const unsigned target = epoch * count;
+            unsigned v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                if (v >= target) break;
+                __nanosleep(20);
+            }
+        } else {
+            __threadfence();
+        }
+        *rounds_done = rounds;
+    }
+    cw_sync();
+}
+
+// Per-CTA round records (NCCL-LL style): the CTA's residual sum split into two 32-bit halves,
+// each stored together with a 32-bit epoch flag in one 8-byte release store.  A reader that sees
+// both flags equal to the epoch has the value and (acquire) every write the CTA made before it.
+// Polling all records replaces a separate grid barrier + totals load (one L2 round trip less).
+__device__ __forceinline__ void rec_publish(uint64_t *rec, double v, uint32_t epoch) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const uint64_t w0 = ((uint64_t)epoch << 32) | (uint32_t)b;
+    const uint64_t w1 = ((uint64_t)epoch << 32) | (uint32_t)(b >> 32);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // one release fence for both words
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(rec), "l"(w0), "l"(w1) : "memory");
+}
+// relaxed poll load; the caller issues one acquire fence after every flag matched
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int Q, int N, typename F> __device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (Q < N) {
+        f(std::integral_constant<int, Q>{});
+        static_for<Q + 1, N>(f);
+    }
+}
+
+// Raw K row of one key kept in registers (issued early, consumed after the pivot is known).
+template <typename T, int D> struct KRow {
+    static constexpr int kVec = D * (int)sizeof(T) / 16;  // 16-byte vectors per row
+    static constexpr int kEl = 16 / (int)sizeof(T);        // elements per vector
+    uint4 v[kVec];
+    __device__ __forceinline__ void load(const T *row) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(row);
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) v[q] = __ldg(p + q);
+    }
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) v[q] = make_uint4(0, 0, 0, 0);
+    }
+    // part[e % 4] += k_j * kc_j over the row (fp64, exact widening of k)
+    __device__ __forceinline__ void dot(const double *kc, double part[4]) const {
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) {
+            const uint32_t wd[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            if constexpr (sizeof(T) == 2) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t bits = (e & 1) ? (wd[e >> 1] & 0xffff0000u) : (wd[e >> 1] << 16);
+                    part[e & 3] = fma((double)__uint_as_float(bits), kc[q * 8 + e], part[e & 3]);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) part[e] = fma((double)__uint_as_float(wd[e]), kc[q * 4 + e], part[e]);
+            }
+        }
+    }
+};
+
+// Stage consumer: warp w folds row j0 + w of the ring stage into its 8 per-lane partial F-dots.
+struct Ring {
+    double *buf;
+    uint64_t *full, *empty;
+    int NS;
+    int stage = 0;
+    uint32_t ph = 0;
+    __device__ __forceinline__ void consume(int j0, int rows, const double *fs, double acc[kTK], int w, int lane) {
+        const int nr = min(kRPS, rows - j0);
+        mbar_wait(&full[stage], ph);
+        if (w < nr) {
+            const double *src = buf + ((size_t)stage * kRPS + w) * kST + lane;
+            const double fj = fs[j0 + w];
+#pragma unroll
+            for (int t = 0; t < kTK; ++t) acc[t] = fma(src[32 * t], fj, acc[t]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == NS) {
+            stage = 0;
+            ph ^= 1u;
+        }
+    }
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs a, int NS, int interleave) {
+    using KR = KRow<T, D>;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    double *ring = reinterpret_cast<double *>(smraw);  // [NS][kRPS][kST]
+    double *fs = ring + (size_t)NS * kRPS * kST;        // [r]
+    double *red = fs + a.r;                             // [kCW][kST]
+    double *kb = red + kCW * kST;                       // [D]
+    double *kcs = kb + D;                               // [D]
+    double *scr = kcs + D;                              // [40]
+    uint64_t *full = reinterpret_cast<uint64_t *>(scr + 40);
+    uint64_t *empty = full + NS;
+    __shared__ int sh_s, sh_cstar, sh_done, sh_last;
+    __shared__ volatile int sh_stop;
+    __shared__ volatile int sh_rounds_done;  // rounds whose F row (this CTA) is complete and visible
+    __shared__ double sh_ps, sh_c0, sh_t;
+
+    const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
+    const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
+    const int64_t n = a.n;
+    const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
+    const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
+    const int nst = (int)ceil_div(hi - lo, kST);
+
+    const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
+    const double *st = a.stats + (int64_t)u * (8 + D);
+    // tile-major F: block (c', k') = [r][kST] doubles for super-tile k' of CTA c'
+    double *Fu = a.F + (int64_t)u * a.cpu * a.nstm * a.r * kST;
+    double *Fc = Fu + (int64_t)c * a.nstm * a.r * kST;  // this CTA's blocks
+
+    if (tid == 0) {
+        for (int q = 0; q < NS; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kCW);
+        }
+        sh_stop = 0;
+        sh_rounds_done = 0;
+        fence_mbar_init();
+    }
+    __syncthreads();  // the only CTA-wide barrier: everything after is role-specific
+
+    if (w == kCW) {
+        // ================= producer warp (one elected lane) =================
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+            int stage = 0;
+            uint32_t ph = 0, issued = 0, par = 0;
+            for (int i = 2; i < a.r; ++i) {
+                const int rows = i - 1;  // TMA rows 0..i-2; row i-1 is read directly
+                while (sh_rounds_done < i - 1) {  // rows 0..i-2 of this CTA written and visible
+                    if (sh_stop) goto drain;
+                    __nanosleep(32);
+                }
+                for (int k = 0; k < nst; ++k) {
+                    const double *blk = Fc + (int64_t)k * a.r * kST;
+                    for (int j0 = 0; j0 < rows; j0 += kRPS) {
+                        const int nr = min(kRPS, rows - j0);
+                        const uint32_t bytes = (uint32_t)(nr * kST * sizeof(double));
+                        while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
+                            if (sh_stop) goto drain;
+                        }
+                        if (sh_stop) goto drain;
+                        mbar_arrive_expect_tx(&full[stage], bytes);
+                        // one contiguous bulk copy of nr rows x 256 keys (tile-major layout)
+                        bulk_g2s_hint(ring + (size_t)stage * kRPS * kST, blk + (int64_t)j0 * kST, bytes, &full[stage],
+                                      j0 < a.rkeep ? keep : stream);
+                        issued |= 1u << stage;
+                        par = (par & ~(1u << stage)) | (ph << stage);
+                        if (++stage == NS) { stage = 0; ph ^= 1u; }
+                    }
+                }
+            }
+        drain:
+            // never leave the CTA with bulk copies in flight
+            for (int q = 0; q < NS; ++q)
+                if (issued & (1u << q)) mbar_wait(&full[q], (par >> q) & 1u);
+        }
+        return;
+    }
+
+    // ================= compute warps (256 threads) =================
+    const double g = st[1], mstar = st[2];
+    double *p0 = a.p + (int64_t)u * n;
+    double *p1 = a.p + ((int64_t)a.units + u) * n;
+    for (int j = tid; j < D; j += kCT) kb[j] = st[8 + j];
+
+    double loc = 0.0;
+    double p_first = 0.0;  // residual of this thread's key in super-tile 0 (kept in a register)
+    for (int64_t l = lo + tid; l < hi; l += kCT) {
+        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
+        p0[l] = v;
+        if (l == lo + tid) p_first = v;
+        loc += v;
+    }
+    loc = cw_sum(loc, scr);
+    if (tid == 0) a.part[(int64_t)u * 2 * kMaxCpu + c] = loc;
+    unsigned epoch = 1;
+    cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_rounds_done, 0);
+
+    KR krow;  // K row of this thread's key for the next super-tile to process (prefetched)
+    if (nst > 0 && lo + tid < hi) krow.load(Ku + (lo + tid) * D);
+    else krow.zero();
+    double pcur_next = p_first;
+    double fkeep[2] = {0.0, 0.0};  // this thread's F[i-1, key] for super-tiles 0 and 1
+    int rstage = 0;
+    uint32_t rph = 0;
+
+    double T0 = 0.0, theta = 0.0;
+    int i = 0;
+    for (; i < a.r; ++i) {
+        double *cur = (i & 1) ? p1 : p0;
+        double *nxt = (i & 1) ? p0 : p1;
+        double p0_next = 0.0;
+
+        // ---- A1a (warp 0): totals over the per-CTA residual sums (one L2 round trip, cached in
+        // registers), exhaustion test, Philox uniform, owning CTA c*.  Fixed order.
+        if (w == 0) {
+            const double uni = pivot_uniform(a.seed, (uint32_t)i, (uint64_t)u);
+            const double *pc = a.part + (int64_t)u * 2 * kMaxCpu + (i & 1) * kMaxCpu;
+            const int per = (a.cpu + 31) / 32;
+            const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
+            constexpr int kPer = 8;  // fast path: cpu <= 256
+            double pv[kPer];
+            double v = 0.0;
+            if (per <= kPer) {
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) pv[q] = (b0 + q < b1) ? __ldcg(pc + b0 + q) : 0.0;
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) v += pv[q];
+            } else {
+                for (int cc = b0; cc < b1; ++cc) v += __ldcg(pc + cc);
+            }
+            double incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const double Ttot = __shfl_sync(0xffffffffu, incl, 31);
+            if (i == 0) {
+                T0 = Ttot;
+                theta = 1000.0 * (double)a.r * 2.220446049250313e-16 * T0;
+            }
+            const bool done = Ttot <= theta;
+            if (!done) {
+                const double t = uni * Ttot;
+                const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
+                const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
+                const int L = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
+                if (lane == L) {
+                    double acc = incl - v;
+                    int cs = -1, last = -1;
+                    double excl = 0.0, last_excl = 0.0;
+                    for (int cc = b0; cc < b1; ++cc) {
+                        double pvv = 0.0;
+                        if (per <= kPer) {
+#pragma unroll
+                            for (int q = 0; q < kPer; ++q) pvv = (q == cc - b0) ? pv[q] : pvv;
+                        } else {
+                            pvv = __ldcg(pc + cc);
+                        }
+                        if (pvv > 0.0) { last = cc; last_excl = acc; }
+                        const double nacc = acc + pvv;
+                        if (cs < 0 && hit && nacc > t) { cs = cc; excl = acc; }
+                        acc = nacc;
+                    }
+                    if (cs < 0) { cs = last; excl = last_excl; }  // rounding fallback (reading Z2)
+                    sh_cstar = cs;
+                    sh_t = t - excl;
+                }
+            }
+            if (lane == 0) {
+                sh_done = done ? 1 : 0;
+                sh_s = 0x7fffffff;
+                sh_last = -1;
+            }
+        }
+        cw_sync();
+        if (sh_done) break;
+        // ---- A1b: inverse CDF inside c*'s slice (all compute threads, block scan, fixed order)
+        {
+            const int64_t slo = std::min<int64_t>(n, (int64_t)sh_cstar * chunk);
+            const int64_t shi = std::min<int64_t>(n, slo + chunk);
+            const int64_t per = ceil_div(shi - slo, kCT);
+            const int64_t b0 = slo + (int64_t)tid * per, b1 = std::min<int64_t>(shi, b0 + per);
+            const double tp = sh_t;
+            double v = 0.0;
+            for (int64_t l = b0; l < b1; ++l) v += __ldcg(cur + l);
+            const double ex = cw_exclusive_scan(v, scr);
+            double run = ex;
+            int found = -1, lastpos = -1;
+            for (int64_t l = b0; l < b1; ++l) {
+                const double pl = __ldcg(cur + l);
+                if (pl > 0.0) lastpos = (int)l;
+                run += pl;
+                if (found < 0 && run > tp) found = (int)l;
+            }
+            if (found >= 0) atomicMin(&sh_s, found);
+            if (lastpos >= 0) atomicMax(&sh_last, lastpos);
+            cw_sync();
+            if (tid == 0) {
+                if (sh_s == 0x7fffffff) sh_s = sh_last;  // rounding fallback (reading Z2)
+                sh_ps = __ldcg(cur + sh_s);
+            }
+        }
+        WC_TR(0);
+        cw_sync();
+        WC_TR(2);
+        const int cstar = sh_cstar;
+        const int s = sh_s;
+        // ---- pivot data: centred k_s (fp64), c0 = <kbar, k_s - kbar>, F[0:i, s]
+        if (w < (D + 31) / 32) {  // warp-uniform
+            double pr = 0.0;
+            if (tid < D) {
+                const double kc = __dadd_rn(to_f64(Ku[(int64_t)s * D + tid]), -kb[tid]);
+                kcs[tid] = kc;
+                pr = kb[tid] * kc;
+            }
+            pr = warp_sum(pr);
+            if (lane == 0) scr[32 + w] = pr;
+        }
+        {
+            const int64_t cs_ = s / chunk, off = s - cs_ * chunk;
+            const double *fsrc = Fu + ((cs_ * a.nstm + off / kST) * a.r) * kST + (off % kST);
+            for (int j = tid; j < i; j += kCT) fs[j] = __ldcg(fsrc + (int64_t)j * kST);
+        }
+        cw_sync();
+        WC_TR(3);
+        const double rs = sqrt(sh_ps);
+        double c0v = 0.0;  // <kbar, k_s - kbar> from the per-warp partials, fixed order
+#pragma unroll
+        for (int q = 0; q < (D + 31) / 32; ++q) c0v += scr[32 + q];
+        if (c == cstar) {
+            for (int j = tid; j < i; j += kCT) a.L[((int64_t)u * a.r + i) * a.r + j] = fs[j];
+            if (tid == 0) a.S[(int64_t)u * a.r + i] = s;
+        }
+        // ---- A2 over super-tiles of 256 keys (one key per compute thread in phase C)
+        loc = 0.0;
+        const uint64_t fpol = i < a.rkeep ? policy_evict_last() : policy_evict_first();
+        const int rows = i - 1;  // rows streamed through the ring
+        const double flast = i > 0 ? fs[i - 1] : 0.0;
+        for (int k = 0; k < nst; ++k) {
+            const int64_t l = lo + (int64_t)k * kST + tid;
+            const bool own = l < hi;
+            double *Fk = Fc + (int64_t)k * a.r * kST + tid;  // this key's column in its block
+            const double pcur = pcur_next;
+            const double fprev = k < 2 ? fkeep[k & 1] : ((own && i > 0) ? __ldcg(Fk + (int64_t)(i - 1) * kST) : 0.0);
+            if (k < 2) WC_TR(4 + 3 * k);
+            // phases A+B interleaved: the kernel dot <k_l, k_s - kbar> is computed one 16-byte
+            // vector at a time between ring stages, hiding it under the F stream
+            double part[4] = {0.0, 0.0, 0.0, 0.0};
+            double acc[kTK];
+#pragma unroll
+            for (int t = 0; t < kTK; ++t) acc[t] = 0.0;
+            (void)interleave;
+            krow.dot(kcs, part);
+            for (int j0 = 0; j0 < rows; j0 += kRPS) {
+                const int nr = min(kRPS, rows - j0);
+                mbar_wait(&full[rstage], rph);
+                if (w < nr) {
+                    const double *src = ring + ((size_t)rstage * kRPS + w) * kST + lane;
+                    const double fj = fs[j0 + w];
+#pragma unroll
+                    for (int t = 0; t < kTK; ++t) acc[t] = fma(src[32 * t], fj, acc[t]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[rstage]);
+                if (++rstage == NS) {
+                    rstage = 0;
+                    rph ^= 1u;
+                }
+            }
+            const double dot = ((part[0] + part[1]) + (part[2] + part[3])) - c0v;
+            // prefetch the K row and residual of the next super-tile (wrapping to super-tile 0 of
+            // the next round, whose residual this thread computes below)
+            if (nst > 1) {
+                const int kn = (k + 1 == nst) ? 0 : k + 1;
+                const int64_t ln = lo + (int64_t)kn * kST + tid;
+                if (ln < hi) {
+                    krow.load(Ku + ln * D);
+                    if (kn != 0) pcur_next = __ldcg(cur + ln);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kTK; ++t) red[w * kST + 32 * t + lane] = acc[t];
+            if (k < 2) WC_TR(5 + 3 * k);
+            cw_sync();
+            // phase C: combine (fixed order), new F column entry, residual downdate
+            if (own) {
+                double accv = 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kCW; ++ww) accv += red[ww * kST + tid];
+                accv = fma(fprev, flast, accv);
+                const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
+                const double f = (hval - accv) / rs;
+                st_f64_hint(Fk + (int64_t)i * kST, f, fpol);
+                fence_proxy_async_global();
+                double q = __dadd_rn(pcur, -__dmul_rn(f, f));
+                q = q > 0.0 ? q : 0.0;
+                if (l == s) {
+                    q = 0.0;
+                    a.L[((int64_t)u * a.r + i) * a.r + i] = f;
+                }
+                nxt[l] = q;
+                loc += q;
+                if (k == 0) p0_next = q;  // next round's residual for super-tile 0
+                if (k < 2) fkeep[k] = f;
+            }
+            cw_sync();
+            if (k < 2) WC_TR(6 + 3 * k);
+        }
+        pcur_next = p0_next;
+        loc = cw_sum(loc, scr);
+        WC_TR(10);
+        if (tid == 0) a.part[(int64_t)u * 2 * kMaxCpu + ((i + 1) & 1) * kMaxCpu + c] = loc;
+        // rounds 0..i complete: this CTA's F row i is globally visible for the producer's TMA reads
+        cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_rounds_done, i + 1);
+        WC_TR(11);
+    }
+    if (tid == 0) sh_stop = 1;
+    if (c == 0 && tid == 0) {
+        a.r_eff[u] = i;
+        const_cast<double *>(st)[5] = T0;
+    }
+}
+
+// Debug: print the per-round phase durations of CTA 0 (ns, averaged over round bins).
+void dump_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
+    std::vector<unsigned long long> h((size_t)16 * r);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), dtrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(dtrace);
+    const char *names[] = {"a1a", "a1a_sync", "a1b", "pivld", "st0_B", "st0_A", "st0_C",
+                           "st1_B", "st1_A", "st1_C", "sum", "gbar"};
+    for (int b0 = 0; b0 < r; b0 += r / 8 > 0 ? r / 8 : 1) {
+        const int b1 = std::min(r, b0 + (r / 8 > 0 ? r / 8 : 1));
+        double acc[12] = {0};
+        int cnt = 0;
+        for (int i = b0; i < b1; ++i) {
+            const unsigned long long *t = &h[(size_t)i * 16];
+            const unsigned long long prev = i > 0 ? h[(size_t)(i - 1) * 16 + 11] : t[0];
+            if (!t[11]) continue;
+            unsigned long long last = prev;
+            for (int k = 0; k < 12; ++k) {
+                if (!t[k]) continue;
+                acc[k] += (double)(t[k] - last);
+                last = t[k];
+            }
+            ++cnt;
+        }
+        if (!cnt) continue;
+        std::fprintf(stderr, "[trace] rounds %4d-%4d:", b0, b1 - 1);
+        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s=%.0f", names[k], acc[k] / cnt);
+        std::fprintf(stderr, "\n");
+    }
+}
+
 template <typename T, int D>
 int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectBufs b, uint64_t seed,
                      int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     SelArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
-    a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
-    a.cpu = select_ctas_per_unit(Dm); a.seed = seed;
+    a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.ldF = f_ld(Dm.n); a.units = Dm.units(); a.r = Dm.r;
+    a.nstm = f_tile_nst(Dm.n, select_ctas_per_unit(Dm));
+    a.cpu = select_ctas_per_unit(Dm); a.seed = seed; a.trace = nullptr;
+    {
+        // keep the first F rows L2-resident: ~3/4 of L2 for F (the rest holds K, p and streams)
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        const char *env = std::getenv("WC_L2_KEEP_FRAC");
+        const double frac = env ? std::atof(env) : 0.75;
+        const double row_bytes = (double)a.units * (double)a.ldF * sizeof(double);
+        a.rkeep = (int)std::min<double>(Dm.r, std::max(0.0, frac * l2 / row_bytes));
+    }
+    static const bool tracing = std::getenv("WC_SELECT_TRACE") != nullptr;
+    if (tracing) cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * Dm.r);
+    if (a.trace) cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 16 * Dm.r, st);
+    if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
+    if (cudaMemsetAsync(b.part, 0, sizeof(double) * 2 * kMaxCpu * a.units, st) != cudaSuccess) return -1;
+    const dim3 grid(a.units * a.cpu);
+    static const char *mode = std::getenv("WC_SELECT");  // "simple": the non-TMA kernel (A/B tests)
+    if (!(mode && std::strcmp(mode, "simple") == 0)) {
+        const size_t fixed = (size_t)(Dm.r + kCW * kST + 2 * D + 40) * sizeof(double) + 64 * sizeof(uint64_t);
+        const size_t stage_bytes = (size_t)kRPS * kST * sizeof(double);
+        const int NS = (int)std::min<size_t>(16, (220 * 1024 - fixed) / stage_bytes);
+        const size_t smem = fixed + (size_t)NS * stage_bytes;
+        auto kt = rpc_select_tma_kernel<T, D>;
+        cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        static const char *ienv = std::getenv("WC_INTERLEAVE");
+        int interleave = ienv ? std::atoi(ienv) : 0;
+        if (a.cpu > 1) {
+            void *args[] = {&a, (void *)&NS, (void *)&interleave};
+            if (cudaLaunchCooperativeKernel((const void *)kt, grid, dim3(kTmaThreads), args, smem, st) != cudaSuccess)
+                return -1;
+        } else {
+            kt<<<grid, kTmaThreads, smem, st>>>(a, NS, interleave);
+        }
+        if (a.trace) dump_trace(a.trace, Dm.r, st);
+        return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+    }
     const int threads = (Dm.n / a.cpu >= 384) ? kSelThreads : 256;
     const size_t smem = (size_t)(2 * D + Dm.r + (threads / 32) * kST + 2 * kST + 40) * sizeof(double);
     auto kern = rpc_select_kernel<T, D>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
-    const dim3 grid(a.units * a.cpu);
     if (a.cpu > 1) {
         void *args[] = {&a};
         if (cudaLaunchCooperativeKernel((const void *)kern, grid, dim3(threads), args, smem, st) != cudaSuccess)
