@@ -19,7 +19,6 @@
 //
 // HBM traffic per unit: n r (d e + 24) + 4 n r (r-1) bytes.
 #include <algorithm>
-#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
@@ -370,31 +369,6 @@ __device__ __forceinline__ void cw_group_barrier(unsigned *ctr, unsigned count, 
     cw_sync();
 }
 
-// Per-CTA round records (NCCL-LL style): the CTA's residual sum split into two 32-bit halves,
-// each stored together with a 32-bit epoch flag in one 8-byte release store.  A reader that sees
-// both flags equal to the epoch has the value and (acquire) every write the CTA made before it.
-// Polling all records replaces a separate grid barrier + totals load (one L2 round trip less).
-__device__ __forceinline__ void rec_publish(uint64_t *rec, double v, uint32_t epoch) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    const uint64_t w0 = ((uint64_t)epoch << 32) | (uint32_t)b;
-    const uint64_t w1 = ((uint64_t)epoch << 32) | (uint32_t)(b >> 32);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // one release fence for both words
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(rec), "l"(w0), "l"(w1) : "memory");
-}
-// relaxed poll load; the caller issues one acquire fence after every flag matched
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-template <int Q, int N, typename F> __device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (Q < N) {
-        f(std::integral_constant<int, Q>{});
-        static_for<Q + 1, N>(f);
-    }
-}
-
 // Raw K row of one key kept in registers (issued early, consumed after the pivot is known).
 template <typename T, int D> struct KRow {
     static constexpr int kVec = D * (int)sizeof(T) / 16;  // 16-byte vectors per row
@@ -428,33 +402,8 @@ template <typename T, int D> struct KRow {
     }
 };
 
-// Stage consumer: warp w folds row j0 + w of the ring stage into its 8 per-lane partial F-dots.
-struct Ring {
-    double *buf;
-    uint64_t *full, *empty;
-    int NS;
-    int stage = 0;
-    uint32_t ph = 0;
-    __device__ __forceinline__ void consume(int j0, int rows, const double *fs, double acc[kTK], int w, int lane) {
-        const int nr = min(kRPS, rows - j0);
-        mbar_wait(&full[stage], ph);
-        if (w < nr) {
-            const double *src = buf + ((size_t)stage * kRPS + w) * kST + lane;
-            const double fj = fs[j0 + w];
-#pragma unroll
-            for (int t = 0; t < kTK; ++t) acc[t] = fma(src[32 * t], fj, acc[t]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == NS) {
-            stage = 0;
-            ph ^= 1u;
-        }
-    }
-};
-
 template <typename T, int D>
-__global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs a, int NS, int interleave) {
+__global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs a, int NS) {
     using KR = KRow<T, D>;
     extern __shared__ __align__(128) unsigned char smraw[];
     double *ring = reinterpret_cast<double *>(smraw);  // [NS][kRPS][kST]
@@ -701,13 +650,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
             const double pcur = pcur_next;
             const double fprev = k < 2 ? fkeep[k & 1] : ((own && i > 0) ? __ldcg(Fk + (int64_t)(i - 1) * kST) : 0.0);
             if (k < 2) WC_TR(4 + 3 * k);
-            // phases A+B interleaved: the kernel dot <k_l, k_s - kbar> is computed one 16-byte
-            // vector at a time between ring stages, hiding it under the F stream
+            // phase B: kernel dot <k_l, k_s - kbar> from the prefetched K row (dot = . - c0);
+            // phase A: F rows 0..i-2 from the ring, warp w takes row j0 + w of every stage
             double part[4] = {0.0, 0.0, 0.0, 0.0};
             double acc[kTK];
 #pragma unroll
             for (int t = 0; t < kTK; ++t) acc[t] = 0.0;
-            (void)interleave;
             krow.dot(kcs, part);
             for (int j0 = 0; j0 < rows; j0 += kRPS) {
                 const int nr = min(kRPS, rows - j0);
@@ -842,14 +790,12 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
         const size_t smem = fixed + (size_t)NS * stage_bytes;
         auto kt = rpc_select_tma_kernel<T, D>;
         cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        static const char *ienv = std::getenv("WC_INTERLEAVE");
-        int interleave = ienv ? std::atoi(ienv) : 0;
         if (a.cpu > 1) {
-            void *args[] = {&a, (void *)&NS, (void *)&interleave};
+            void *args[] = {&a, (void *)&NS};
             if (cudaLaunchCooperativeKernel((const void *)kt, grid, dim3(kTmaThreads), args, smem, st) != cudaSuccess)
                 return -1;
         } else {
-            kt<<<grid, kTmaThreads, smem, st>>>(a, NS, interleave);
+            kt<<<grid, kTmaThreads, smem, st>>>(a, NS);
         }
         if (a.trace) dump_trace(a.trace, Dm.r, st);
         return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
