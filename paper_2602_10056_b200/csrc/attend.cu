@@ -6,8 +6,12 @@
 // online max rescaling across coreset tiles (exact: the shift cancels in num/den).
 #include <algorithm>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace wc {
 
@@ -115,6 +119,213 @@ __global__ void __launch_bounds__(kAT) attend_kernel(const T *__restrict__ Q, co
     }
 }
 
+// =====================================================================================
+// tcgen05 path (bf16, d in {64, 128}, r <= 256).  One CTA of 128 threads per SM loops over
+// 128-query tiles.  Per tile:
+//   GEMM1 (tensor core)  S[128 x RP] = Q_tile . K_S^T          (fp32 in TMEM columns [0, RP))
+//   softmax epilogue      P = exp(beta (S - rowmax)), den = P . w (fp32, CUDA cores), P -> bf16 smem
+//   GEMM2 (tensor core)  O[128 x d]  = P . X_hi + P . X_lo       (fp32 in TMEM columns [256, 256+d))
+//   output epilogue       O / den (den > 0, else 0), clip to [vmin, vmax], bf16 store
+// X = [V_S, w] is split into bf16 hi + lo parts so the values keep ~16 bits.  Thread t owns
+// TMEM lane t = query row t.  Operands are K-major, 128-byte swizzled (see umma.cuh).
+// =====================================================================================
+constexpr int kTcThreads = 128;
+
+template <int D, int RP> struct TcSmem {
+    // K-major SW128 rows are at least 128 bytes (64 bf16) wide
+    static constexpr int kRK = RP < 64 ? 64 : RP;   // padded K extent of the [*, RP] operands
+    static constexpr int kQ = 128 * D * 2;          // Q tile
+    static constexpr int kK = RP * D * 2;           // K_S
+    static constexpr int kX = D * kRK * 2;          // one of X_hi / X_lo (B operand [d][RP])
+    static constexpr int kP = 128 * kRK * 2;        // P (A operand [128][RP])
+    static constexpr bool kAliasP = kP <= kQ + kK;  // P reuses the Q/K_S region after GEMM1
+    static constexpr int kOffQ = 0, kOffK = kQ, kOffXh = kQ + kK, kOffXl = kOffXh + kX;
+    static constexpr int kOffP = kAliasP ? 0 : kOffXl + kX;
+    static constexpr int kBytes = (kAliasP ? kOffXl + kX : kOffP + kP);
+    static constexpr int kTotal = kBytes + RP * 4 + 2 * D * 2 + 1024;  // + w, vmin, vmax (bf16), alignment
+};
+
+template <int D, int RP>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attend_tc_kernel(const __nv_bfloat16 *__restrict__ Q, const __nv_bfloat16 *__restrict__ KS,
+                     const float *__restrict__ X, const int32_t *__restrict__ r_eff,
+                     const __nv_bfloat16 *__restrict__ vmin, const __nv_bfloat16 *__restrict__ vmax, int64_t m,
+                     int r, int group, int hq, int hkv, float beta, int clip, __nv_bfloat16 *__restrict__ O,
+                     int64_t tiles_per_head, int64_t total_tiles) {
+    using L = TcSmem<D, RP>;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *sQ = sm + L::kOffQ, *sK = sm + L::kOffK, *sXh = sm + L::kOffXh, *sXl = sm + L::kOffXl;
+    unsigned char *sP = sm + L::kOffP;
+    float *sW = reinterpret_cast<float *>(sm + L::kBytes);
+    __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sW + RP), *sVmax = sVmin + D;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, w = tid >> 5;
+    constexpr int DC = D + 1;
+
+    if (w == 0) umma::tmem_alloc(&tbase, 512);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tS = tbase, tO = tbase + 256;
+    const uint32_t lane_off = (uint32_t)(w * 32) << 16;
+    uint32_t phase = 0;
+    int cur_unit = -1, re = 0;
+    const float bl2 = beta * 1.4426950408889634f;
+
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int64_t head = tile / tiles_per_head;  // b * hq + h
+        const int64_t q0 = (tile % tiles_per_head) * 128;
+        const int b = (int)(head / hq), h = (int)(head % hq);
+        const int u = b * hkv + h / group;
+        const __nv_bfloat16 *Qh = Q + head * m * D;
+        // ---- stage operands in shared memory (16-byte chunks -> 128B-swizzled K-major layout)
+        constexpr int CPR = D / 8;  // 16-byte chunks per row
+        for (int e = tid; e < 128 * CPR; e += kTcThreads) {
+            const int row = e / CPR, cc = e % CPR;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (q0 + row < m) v = __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc);
+            *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = v;
+        }
+        if (u != cur_unit) {
+            re = r_eff[u];
+            const float *Xu = X + (int64_t)u * r * DC;
+            for (int e = tid; e < D * RP; e += kTcThreads) {  // X^T split into bf16 hi + lo
+                const int c = e / RP, s = e % RP;
+                const float x = (s < re) ? Xu[(int64_t)s * DC + c] : 0.f;
+                const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+                const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
+                *reinterpret_cast<__nv_bfloat16 *>(sXh + umma::sw128_offset(c, s, D)) = xh;
+                *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
+            }
+            for (int s = tid; s < RP; s += kTcThreads) sW[s] = (s < re) ? Xu[(int64_t)s * DC + D] : 0.f;
+            for (int c = tid; c < D; c += kTcThreads) {
+                sVmin[c] = vmin[(int64_t)u * D + c];
+                sVmax[c] = vmax[(int64_t)u * D + c];
+            }
+        }
+        if (u != cur_unit || L::kAliasP) {  // K_S (reloaded each tile when P aliases it)
+            const __nv_bfloat16 *KSu = KS + (int64_t)u * r * D;
+            for (int e = tid; e < RP * CPR; e += kTcThreads) {
+                const int row = e / CPR, cc = e % CPR;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (row < re) v = __ldg(reinterpret_cast<const uint4 *>(KSu + (int64_t)row * D) + cc);
+                *reinterpret_cast<uint4 *>(sK + umma::sw128_offset(row, cc * 8, RP)) = v;
+            }
+        }
+        cur_unit = u;
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+        // ---- GEMM1: S = Q K_S^T
+        if (tid == 0) {
+            umma::gemm_128xNxK(tS, smem_u32(sQ), smem_u32(sK), RP, D, false);
+            umma::commit(&bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        umma::fence_after_sync();
+        // ---- softmax epilogue: row max, P = exp(beta (S - max)) in bf16, den = P . w
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < RP; c0 += 32) {
+            float v[32];
+            umma::ld32(tS + lane_off + c0, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (c0 + i < re) mx = fmaxf(mx, v[i]);
+        }
+        float den = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < RP; c0 += 32) {
+            float v[32];
+            umma::ld32(tS + lane_off + c0, v);
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int s0 = c0 + g8 * 8 + 2 * i;
+                    const float p0 = (s0 < re) ? exp2f((v[g8 * 8 + 2 * i] - mx) * bl2) : 0.f;
+                    const float p1 = (s0 + 1 < re) ? exp2f((v[g8 * 8 + 2 * i + 1] - mx) * bl2) : 0.f;
+                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                    den = fmaf(__bfloat162float(pb.x), sW[s0], den);
+                    den = fmaf(__bfloat162float(pb.y), sW[s0 + 1], den);
+                    pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
+                }
+                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(tid, c0 + g8 * 8, 128)) =
+                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+        // ---- GEMM2: O = P X_hi + P X_lo
+        if (tid == 0) {
+            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXh), D, RP, false);
+            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXl), D, RP, true);
+            umma::commit(&bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        umma::fence_after_sync();
+        // ---- output epilogue
+        const int64_t qi = q0 + tid;
+        const float inv = den > 0.f ? 1.f / den : 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            float v[32];
+            umma::ld32(tO + lane_off + c0, v);
+            if (qi < m) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
+                    if (clip) {
+                        o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[c0 + 2 * i])), __bfloat162float(sVmax[c0 + 2 * i]));
+                        o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[c0 + 2 * i + 1])), __bfloat162float(sVmax[c0 + 2 * i + 1]));
+                    }
+                    const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
+                    pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
+                }
+                uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + qi) * D + c0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            }
+        }
+        umma::fence_before_sync();
+        __syncthreads();  // TMEM and smem free for the next tile
+        umma::fence_after_sync();
+    }
+    if (w == 0) umma::tmem_dealloc(tbase, 512);
+}
+
+template <int D, int RP>
+int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                     const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
+    using L = TcSmem<D, RP>;
+    auto kern = attend_tc_kernel<D, RP>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    const int64_t tph = ceil_div(Dm.m, 128);
+    const int64_t total = tph * Dm.hq * Dm.batch;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>(total, sms);
+    kern<<<grid, kTcThreads, L::kTotal, st>>>(
+        static_cast<const __nv_bfloat16 *>(Q), static_cast<const __nv_bfloat16 *>(KS), X, r_eff,
+        static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(),
+        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 template <typename T, int D>
 int launch_attend_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                      const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
@@ -147,6 +358,26 @@ int launch_attend_t(const Dims &Dm, const void *Q, const void *KS, const float *
 
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                   const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
+    static const char *mode = std::getenv("WC_ATTEND");  // "cuda": CUDA-core kernel (A/B tests)
+    const bool tc_ok = D.dtype == 1 && (D.d == 64 || D.d == 128) && D.r <= 256 && D.m > 0 &&
+                       !(mode && std::strcmp(mode, "cuda") == 0);
+    if (tc_ok) {
+        const int rp = D.r <= 32 ? 32 : D.r <= 64 ? 64 : D.r <= 128 ? 128 : 256;
+        if (D.d == 64) {
+            switch (rp) {
+                case 32: return launch_attend_tc<64, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+                case 64: return launch_attend_tc<64, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+                case 128: return launch_attend_tc<64, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+                default: return launch_attend_tc<64, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+            }
+        }
+        switch (rp) {
+            case 32: return launch_attend_tc<128, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+            case 64: return launch_attend_tc<128, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+            case 128: return launch_attend_tc<128, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+            default: return launch_attend_tc<128, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+        }
+    }
     if (D.dtype == 0) return launch_attend_t<float>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
     return launch_attend_t<__nv_bfloat16>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
 }
