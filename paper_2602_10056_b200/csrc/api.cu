@@ -108,7 +108,9 @@ float *carve_weights(Carver &c, const wc_shape *s, wc::ProloguePartials *pp) {
         pp->rq2 = c.take<double>(U * P);
         pp->rk2 = c.take<double>(U * P);
     }
-    return c.take<float>(U * wc::weights_num_splits(D) * (size_t)D.r * (D.d + 1));
+    // fp32 split partials of Y~, followed by the fp64 reduced Y~ (8-byte aligned: the float count is even)
+    const size_t parts = U * wc::weights_num_splits(D) * (size_t)D.r * (D.d + 1);
+    return c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1));
 }
 
 int finish(int launches) {

@@ -9,8 +9,12 @@
 // in fp64 by the solve kernel.  A4 is a warp-per-RHS-column fp64 triangular solve.
 #include <algorithm>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace wc {
 
@@ -109,49 +113,132 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
     }
 }
 
-// Reduce split partials (fixed order, fp64) and solve L L^T X = Y~ for 8 RHS columns per CTA.
-// One warp per column: forward substitution reads rows of L (left-looking), backward
-// substitution is right-looking so it also reads rows of L (coalesced).
+// Reduce split partials (fixed order, fp64) and solve L L^T X = Y~ for 8 RHS columns per CTA
+// (256 threads: thread t owns panel row t/8 and column t%8).  Blocked in 32-row panels so the
+// sequential part only touches a 32 x 32 diagonal block held in shared memory:
+//   forward  (L Z = Y):   z_P -= L[P, 0:p0] z_{0:p0}  (parallel), then solve the panel's block
+//   backward (L^T X = Z): x_P -= L[pe:q, P]^T x_{pe:q} (parallel, reads rows of L), then the block
+// Y~ = sum over n-splits of the fp32 partials, in fixed split order, in fp64.
 template <int D>
-__global__ void __launch_bounds__(256) weights_solve_kernel(const float *__restrict__ Ypart,
+__global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__restrict__ Ypart,
+                                                             const int32_t *__restrict__ r_eff, int r, int splits,
+                                                             double *__restrict__ Y) {
+    constexpr int DC = D + 1;
+    const int u = blockIdx.y;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (a, c) flattened
+    if (e >= (int64_t)r * DC) return;
+    const int a = (int)(e / DC);
+    double y = 0.0;
+    if (a < r_eff[u]) {
+        const float *src = Ypart + (int64_t)u * splits * r * DC + e;
+#pragma unroll 8
+        for (int sp = 0; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
+    }
+    Y[(int64_t)u * r * DC + e] = y;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) weights_solve_kernel(const double *__restrict__ Y,
                                                             const double *__restrict__ L,
                                                             const int32_t *__restrict__ r_eff, int r,
-                                                            int splits, float *__restrict__ X) {
+                                                            float *__restrict__ X) {
     constexpr int DC = D + 1;
-    extern __shared__ double zs[];  // [8][r]
-    const int u = blockIdx.y;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int col = blockIdx.x * 8 + w;
+    constexpr int PB = 32;
+    constexpr int CB = 64;          // L columns (forward) / rows (backward) staged per block
+    extern __shared__ double zs[];  // z[r][8]
+    __shared__ double Ld[PB][PB + 1];
+    __shared__ double Lb[PB][CB + 1];  // staged block of L
+    const int u = blockIdx.y, tid = threadIdx.x;
+    const int w = warp_index(), lane = tid & 31;
+    const int cbase = blockIdx.x * 8;
     const int q = r_eff[u];
-    double *z = zs + w * r;
     const double *Lu = L + (int64_t)u * r * r;
     float *Xu = X + (int64_t)u * r * DC;
-    if (col >= DC) return;
-    for (int a = lane; a < q; a += 32) {
-        double y = 0.0;
-        for (int sp = 0; sp < splits; ++sp) y += (double)Ypart[(((int64_t)u * splits + sp) * r + a) * DC + col];
-        z[a] = y;
+    for (int e = tid; e < q * 8; e += 256) {
+        const int a = e / 8, cc = e % 8, col = cbase + cc;
+        zs[a * 8 + cc] = col < DC ? Y[((int64_t)u * r + a) * DC + col] : 0.0;
     }
-    __syncwarp();
-    // forward: z_a = (y_a - sum_{b<a} L[a][b] z_b) / L[a][a]
-    for (int a = 0; a < q; ++a) {
-        const double *La = Lu + (int64_t)a * r;
-        double t = 0.0;
-        for (int b = lane; b < a; b += 32) t += La[b] * z[b];
-        t = warp_sum(t);
-        if (lane == 0) z[a] = (z[a] - t) / La[a];
-        __syncwarp();
+    __syncthreads();
+    const int pr = tid / 8, pc = tid % 8;  // panel row, column
+    // ---- forward substitution
+    for (int p0 = 0; p0 < q; p0 += PB) {
+        const int nb = min(PB, q - p0);
+        double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
+        for (int b0 = 0; b0 < p0; b0 += CB) {  // z_P -= L[P, b0:b0+CB] z[b0:b0+CB], block staged in smem
+            const int nbk = min(CB, p0 - b0);
+            __syncthreads();
+            for (int e = tid; e < nb * CB; e += 256) {
+                const int rr = e / CB, cc2 = e % CB;
+                Lb[rr][cc2] = cc2 < nbk ? Lu[(int64_t)(p0 + rr) * r + b0 + cc2] : 0.0;
+            }
+            __syncthreads();
+            if (pr < nb)
+#pragma unroll 8
+                for (int b = 0; b < nbk; ++b) acc = fma(-Lb[pr][b], zs[(b0 + b) * 8 + pc], acc);
+        }
+        if (pr < nb) zs[(p0 + pr) * 8 + pc] = acc;
+        for (int e = tid; e < nb * nb; e += 256) Ld[e / nb][e % nb] = Lu[(int64_t)(p0 + e / nb) * r + p0 + e % nb];
+        __syncthreads();
+        if (w < 8) {  // warp w solves column w of the panel block; lane i owns row p0 + i
+            double zi = lane < nb ? zs[(p0 + lane) * 8 + w] : 0.0;
+            double lrow[PB];  // this lane's row of the diagonal block, in registers
+#pragma unroll
+            for (int j = 0; j < PB; ++j) lrow[j] = (lane < nb && j < nb) ? Ld[lane][j] : 0.0;
+            const double inv = lane < nb ? 1.0 / Ld[lane][lane] : 0.0;
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                if (j < nb) {
+                    const double zj = __shfl_sync(0xffffffffu, zi * inv, j);
+                    if (lane == j) zi = zj;
+                    else if (lane > j) zi = fma(-lrow[j], zj, zi);
+                }
+            }
+            if (lane < nb) zs[(p0 + lane) * 8 + w] = zi;
+        }
+        __syncthreads();
     }
-    // backward (right-looking): x_a = z_a / L[a][a];  z_b -= L[a][b] x_a  for b < a
-    for (int a = q - 1; a >= 0; --a) {
-        const double *La = Lu + (int64_t)a * r;
-        const double xa = z[a] / La[a];
-        __syncwarp();
-        for (int b = lane; b < a; b += 32) z[b] -= La[b] * xa;
-        if (lane == 0) z[a] = xa;
-        __syncwarp();
+    // ---- backward substitution (upper-triangular L^T)
+    const int npan = (q + PB - 1) / PB;
+    for (int pi = npan - 1; pi >= 0; --pi) {
+        const int p0 = pi * PB, nb = min(PB, q - p0), pe = p0 + nb;
+        double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
+        for (int b0 = pe; b0 < q; b0 += CB) {  // x_P -= L[b0:b0+CB, P]^T x[b0:b0+CB], staged transposed
+            const int nbk = min(CB, q - b0);
+            __syncthreads();
+            for (int e = tid; e < CB * PB; e += 256) {
+                const int bb = e / PB, cc2 = e % PB;  // row b0 + bb, column p0 + cc2 (coalesced)
+                Lb[cc2][bb] = (bb < nbk && cc2 < nb) ? Lu[(int64_t)(b0 + bb) * r + p0 + cc2] : 0.0;
+            }
+            __syncthreads();
+            if (pr < nb)
+#pragma unroll 8
+                for (int b = 0; b < nbk; ++b) acc = fma(-Lb[pr][b], zs[(b0 + b) * 8 + pc], acc);
+        }
+        if (pr < nb) zs[(p0 + pr) * 8 + pc] = acc;
+        for (int e = tid; e < nb * nb; e += 256) Ld[e / nb][e % nb] = Lu[(int64_t)(p0 + e / nb) * r + p0 + e % nb];
+        __syncthreads();
+        if (w < 8) {
+            double zi = lane < nb ? zs[(p0 + lane) * 8 + w] : 0.0;
+            double lcol[PB];  // column `lane` of the diagonal block (row j, col lane), in registers
+#pragma unroll
+            for (int j = 0; j < PB; ++j) lcol[j] = (lane < nb && j < nb) ? Ld[j][lane] : 0.0;
+            const double inv = lane < nb ? 1.0 / Ld[lane][lane] : 0.0;
+#pragma unroll
+            for (int j = PB - 1; j >= 0; --j) {
+                if (j < nb) {
+                    const double xj = __shfl_sync(0xffffffffu, zi * inv, j);
+                    if (lane == j) zi = xj;
+                    else if (lane < j) zi = fma(-lcol[j], xj, zi);
+                }
+            }
+            if (lane < nb) zs[(p0 + lane) * 8 + w] = zi;
+        }
+        __syncthreads();
     }
-    for (int a = lane; a < r; a += 32) Xu[(int64_t)a * DC + col] = a < q ? (float)z[a] : 0.f;
+    for (int e = tid; e < r * 8; e += 256) {
+        const int a = e / 8, cc = e % 8, col = cbase + cc;
+        if (col < DC) Xu[(int64_t)a * DC + col] = a < q ? (float)zs[a * 8 + cc] : 0.f;
+    }
 }
 
 template <typename T, int D>
@@ -164,11 +251,196 @@ __global__ void gather_ks_kernel(const T *__restrict__ K, const int32_t *__restr
         KS[((int64_t)u * r + a) * D + j] = s >= 0 ? K[((int64_t)u * n + s) * D + j] : from_f32<T>(0.f);
 }
 
+// =====================================================================================
+// tcgen05 path for A3 (bf16, d in {64, 128}).  CTA = (n-split, 128 coreset rows, unit), 128
+// threads; thread a owns coreset row a0 + a (= TMEM lane a).  Per slice of 128 keys:
+//   GEMM1  S[128 x 128] = K_S . K_slice^T  (raw bf16 keys, exact products, fp32 accumulation)
+//   P = exp(g S + alpha_a + gamma_l)  with alpha_a = g(|kbar|^2 - <k_a,kbar>) - mstar and
+//       gamma_l = -g <k_l, kbar>  (= exp(g <k_a - kbar, k_l - kbar> - mstar), no rounding of
+//       centred keys to bf16);  rowsum_a += P;  P -> bf16 smem
+//   GEMM2  O[128 x d] += P . V_slice       (accumulated in TMEM across the CTA's slices)
+// and the partial Y~[a][0:d] = O, Y~[a][d] = rowsum go to Ypart (summed in fp64 by the solve).
+// =====================================================================================
+constexpr int kWTc = 128;
+
+template <int D>
+__global__ void __launch_bounds__(kWTc, 1)
+    weights_tc_kernel(const __nv_bfloat16 *__restrict__ K, const __nv_bfloat16 *__restrict__ V,
+                      const int32_t *__restrict__ S, const int32_t *__restrict__ r_eff,
+                      const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
+    constexpr int DC = D + 1;
+    constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *sA = sm, *sB = sm + kA, *sP = sB + kB, *sV = sP + kP;
+    float *sG = reinterpret_cast<float *>(sV + kV);  // gamma_l of the slice [128]
+    float *sKb = sG + 128;                             // kbar (fp32) [D]
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, w = tid >> 5;
+    const int split = blockIdx.x, a0 = blockIdx.y * 128, u = blockIdx.z;
+    const int re = r_eff[u];
+    if (a0 >= re) return;  // uniform per CTA
+    const __nv_bfloat16 *Ku = K + (int64_t)u * n * D;
+    const __nv_bfloat16 *Vu = V + (int64_t)u * n * D;
+    const double *st = stats + (int64_t)u * (8 + D);
+    const double g = st[1], mstar = st[2];
+    constexpr int CPR = D / 8;
+
+    if (w == 0) umma::tmem_alloc(&tbase, 256);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    for (int j = tid; j < D; j += kWTc) sKb[j] = (float)st[8 + j];
+    // coreset rows (raw keys) -> A operand; alpha_a in fp64
+    for (int e = tid; e < 128 * CPR; e += kWTc) {
+        const int row = e / CPR, cc = e % CPR;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (a0 + row < re) {
+            const int sidx = S[(int64_t)u * r + a0 + row];
+            v = __ldg(reinterpret_cast<const uint4 *>(Ku + (int64_t)sidx * D) + cc);
+        }
+        *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(row, cc * 8, 128)) = v;
+    }
+    float alpha = 0.f;
+    const bool row_ok = a0 + tid < re;
+    if (row_ok) {
+        const int sidx = S[(int64_t)u * r + a0 + tid];
+        double kk = 0.0, bb = 0.0;
+        for (int j = 0; j < D; ++j) {
+            const double kbj = st[8 + j];
+            kk = fma(to_f64(Ku[(int64_t)sidx * D + j]), kbj, kk);
+            bb = fma(kbj, kbj, bb);
+        }
+        alpha = (float)(g * (bb - kk) - mstar);
+    }
+    const float gf = (float)g;
+    const int64_t rows = ceil_div(n, splits);
+    const int64_t lo = (int64_t)split * rows, hi = std::min<int64_t>(n, lo + rows);
+    const uint32_t tS = tbase, tO = tbase + 128, lane_off = (uint32_t)(w * 32) << 16;
+    uint32_t phase = 0;
+    float rowsum = 0.f;
+    bool first = true;
+    for (int64_t l0 = lo; l0 < hi; l0 += 128) {
+        // keys of the slice -> B operand of GEMM1 (K-major) and V^T -> B operand of GEMM2
+        for (int e = tid; e < 128 * CPR; e += kWTc) {
+            const int row = e / CPR, cc = e % CPR;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (l0 + row < hi) v = __ldg(reinterpret_cast<const uint4 *>(Ku + (l0 + row) * D) + cc);
+            *reinterpret_cast<uint4 *>(sB + umma::sw128_offset(row, cc * 8, 128)) = v;
+        }
+        for (int e = tid; e < 128 * CPR; e += kWTc) {  // transpose V[l][c] -> B2[c][l]
+            const int row = e / CPR, cc = e % CPR;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (l0 + row < hi) v = __ldg(reinterpret_cast<const uint4 *>(Vu + (l0 + row) * D) + cc);
+            const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(cc * 8 + q, row, D)) = pv[q];
+        }
+        {  // gamma_l = -g <k_l, kbar> for the key this thread stages
+            const int64_t l = l0 + tid;
+            float gm = 0.f;
+            if (l < hi) {
+                const uint4 *kr = reinterpret_cast<const uint4 *>(Ku + l * D);
+#pragma unroll 4
+                for (int cc = 0; cc < CPR; ++cc) {
+                    const uint4 v = __ldg(kr + cc);
+                    const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&v);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) gm = fmaf(__bfloat162float(pv[q]), sKb[cc * 8 + q], gm);
+                }
+            }
+            sG[tid] = -gf * gm;
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+        if (tid == 0) {
+            umma::gemm_128xNxK(tS, smem_u32(sA), smem_u32(sB), 128, D, false);
+            umma::commit(&bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        umma::fence_after_sync();
+        const int nl = (int)std::min<int64_t>(128, hi - l0);
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float v[32];
+            umma::ld32(tS + lane_off + c0, v);
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int l = c0 + g8 * 8 + 2 * i;
+                    const float p0 = (row_ok && l < nl) ? __expf(fmaf(gf, v[g8 * 8 + 2 * i], alpha + sG[l])) : 0.f;
+                    const float p1 = (row_ok && l + 1 < nl) ? __expf(fmaf(gf, v[g8 * 8 + 2 * i + 1], alpha + sG[l + 1])) : 0.f;
+                    const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                    rowsum += __bfloat162float(pb.x) + __bfloat162float(pb.y);
+                    pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
+                }
+                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(tid, c0 + g8 * 8, 128)) =
+                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+        umma::fence_async_smem();
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+        if (tid == 0) {
+            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sV), D, 128, !first);
+            umma::commit(&bar);
+        }
+        mbar_wait(&bar, phase);  // smem (sB, sV, sP) reusable and O updated
+        phase ^= 1u;
+        umma::fence_after_sync();
+        first = false;
+    }
+    if (row_ok) {
+        float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + tid) * DC;
+        if (first) {  // empty key range: zero partial
+            for (int c = 0; c < DC; ++c) out[c] = 0.f;
+        }
+    }
+    if (!first) {
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            float v[32];
+            umma::ld32(tO + lane_off + c0, v);
+            if (row_ok) {
+                float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + tid) * DC + c0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) out[i] = v[i];
+            }
+        }
+        if (row_ok) Ypart[(((int64_t)u * splits + split) * r + a0 + tid) * DC + D] = rowsum;
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (w == 0) umma::tmem_dealloc(tbase, 256);
+}
+
 template <typename T, int D>
 int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
                       const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
     const int units = Dm.units();
     const int splits = weights_num_splits(Dm);
+    static const char *mode = std::getenv("WC_WEIGHTS");  // "cuda": CUDA-core kernel (A/B tests)
+    if constexpr (sizeof(T) == 2 && (D == 64 || D == 128)) {
+        if (!(mode && std::strcmp(mode, "cuda") == 0)) {
+            const int smem_tc = 3 * 128 * D * 2 + 128 * 128 * 2 + 128 * 4 + D * 4 + 1024;  // A, B, V^T, P, gamma, kbar
+            auto kt = weights_tc_kernel<D>;
+            cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
+            dim3 gt(splits, (Dm.r + 127) / 128, units);
+            kt<<<gt, kWTc, smem_tc, st>>>(static_cast<const __nv_bfloat16 *>(K), static_cast<const __nv_bfloat16 *>(V),
+                                          S, r_eff, stats, Dm.n, Dm.r, splits, Ypart);
+            goto solve;
+        }
+    }
+    {
     dim3 g1(splits, (Dm.r + kTA - 1) / kTA, units);
     const size_t smem1 = D * sizeof(double) + (size_t)(kTA + 2 * kTL) * (D + 1) * sizeof(float) +
                          (size_t)kTA * (kTL + 1) * sizeof(float);
@@ -176,15 +448,24 @@ int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_
     if (smem1 > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     pk<<<g1, kWT, smem1, st>>>(static_cast<const T *>(K), static_cast<const T *>(V), S,
                                                       r_eff, stats, Dm.n, Dm.r, splits, Ypart);
+    }
+solve:
+    const size_t parts = (size_t)units * splits * Dm.r * (D + 1);
+    double *Yfull = reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
+    {
+        const int64_t cnt = (int64_t)Dm.r * (D + 1);
+        dim3 gr((unsigned)ceil_div(cnt, 256), units);
+        weights_reduce_kernel<D><<<gr, 256, 0, st>>>(Ypart, r_eff, Dm.r, splits, Yfull);
+    }
     const size_t smem = (size_t)8 * Dm.r * sizeof(double);
     auto sk = weights_solve_kernel<D>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 g2((D + 1 + 7) / 8, units);
-    sk<<<g2, 256, smem, st>>>(Ypart, L, r_eff, Dm.r, splits, X);
+    sk<<<g2, 256, smem, st>>>(Yfull, L, r_eff, Dm.r, X);
     dim3 g3(Dm.r, units);
     gather_ks_kernel<T, D><<<g3, 128, 0, st>>>(static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
                                                static_cast<T *>(KS));
-    return cudaPeekAtLastError() == cudaSuccess ? 3 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
 }
 
 template <typename T>
@@ -202,8 +483,10 @@ int launch_weights_t(const Dims &Dm, const void *K, const void *V, const int32_t
 }  // namespace
 
 int weights_num_splits(const Dims &D) {
-    const int64_t tiles = (int64_t)D.units() * ((D.r + kTA - 1) / kTA);
-    const int64_t want = std::max<int64_t>(1, (148 * 4 + tiles - 1) / tiles);
+    const bool tc = D.dtype == 1 && (D.d == 64 || D.d == 128);
+    const int rt = tc ? 128 : kTA;  // coreset rows per CTA (tensor-core / CUDA-core kernel)
+    const int64_t tiles = (int64_t)D.units() * ((D.r + rt - 1) / rt);
+    const int64_t want = std::max<int64_t>(1, ((tc ? 148 : 148 * 4) + tiles - 1) / tiles);
     const int64_t by_n = std::max<int64_t>(1, ceil_div(D.n, 256));
     return (int)std::min<int64_t>(std::min<int64_t>(want, by_n), 512);
 }

@@ -117,9 +117,12 @@ def test_split_api_equals_forward_and_is_deterministic():
     assert np.array_equal(sel.S.cpu().numpy(), res["S"])
     st = sel.stats.cpu().numpy()
     assert np.allclose(st[:, :5], res["stats"], rtol=1e-12, atol=0)
+    # X = [V_S, w]: the bf16 path rounds P = h~(K_S, K) to bf16 in the A3 GEMM (error
+    # budget), so X carries ~2^-9-relative noise amplified by cond(h~(K_S,K_S)); the output bar
+    # (2e-2 of ||V||_max) is checked by the other tests.
     X = cache.X.cpu().numpy().astype(np.float64)
     rel = np.abs(X - res["X"]).max() / np.abs(res["X"]).max()
-    assert rel < 1e-3
+    assert rel < 2e-2, rel
 
 
 @pytest.mark.slow
