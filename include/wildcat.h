@@ -47,6 +47,7 @@ extern "C" {
 #define WC_EDTYPE -3        /* dtype not WC_F32 / WC_BF16 */
 #define WC_EWORKSPACE -4    /* ws too small or misaligned (needs 256-byte alignment) */
 #define WC_ECUDA -5         /* CUDA launch / runtime error */
+#define WC_ENCCL -6         /* NCCL error (n-sharded path) */
 #define WC_EUNSUPPORTED -7  /* valid request this build does not implement */
 
 #define WC_F32 0
@@ -56,6 +57,7 @@ extern "C" {
 #define WC_OP_WEIGHTS 1
 #define WC_OP_ATTEND 2
 #define WC_OP_FORWARD 3
+#define WC_OP_FORWARD_NSHARD 4  /* per-rank workspace of wildcat_forward_nshard (shape = local shard) */
 
 /* flags */
 #define WC_NO_CLIP 1u       /* skip the clip of Alg 3 (reading Z15) */
@@ -115,6 +117,26 @@ int wildcat_attend(const wc_shape *shape, const wc_opts *opts, const void *Q, co
 int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *K,
                     const void *V, void *O, int32_t *S, int32_t *r_eff,
                     void *ws, size_t ws_bytes, void *stream);
+
+/* ---- Key-dimension sharding of one long sequence across GPUs.
+ * One process per GPU.  Rank 0 gets a 128-byte NCCL unique id from wc_comm_unique_id and shares
+ * it (e.g. torch.distributed.broadcast_object_list); every rank then calls wc_comm_init after
+ * selecting its device.  NCCL (libnccl.so.2) is resolved at run time; WC_EUNSUPPORTED if absent. */
+int wc_comm_unique_id(void *id128);
+int wc_comm_init(void **comm, const void *id128, int world, int rank);
+int wc_comm_destroy(void *comm);
+
+/* Alg 4 on one (batch, kv-head) unit whose n_global keys are split across the communicator's ranks:
+ * this rank holds keys/values [n_offset, n_offset + shape->n) (shape->n = local count >= 1, shape->batch
+ * = shape->heads_kv = 1) and shape->m local queries per q-head (any query shard).  The pivot sequence
+ * is drawn from the global residual diagonal with the same Philox stream and inverse-CDF rule as
+ * wildcat_forward, so in exact arithmetic it does not depend on the number of ranks.  Collectives
+ * per round: allgather of per-rank residual totals, allreduce(sum) of the pivot packet; plus the
+ * prologue reductions and one allreduce of Y~.  S (global key indices) and r_eff are replicated.
+ * R_Q from the local queries is max-reduced across ranks unless opts->rq >= 0. */
+int wildcat_forward_nshard(void *comm, const wc_shape *local, int64_t n_global, int64_t n_offset,
+                           const wc_opts *opts, const void *Q, const void *K, const void *V, void *O,
+                           int32_t *S, int32_t *r_eff, void *ws, size_t ws_bytes, void *stream);
 
 /* Human-readable status. */
 const char *wc_strerror(int status);

@@ -7,6 +7,8 @@ Public API (torch tensors in the BHND layout [batch, heads, seq, d], CUDA only):
     cache = weights(K, V, sel)                              # Alg 2 "Compress values"
     O = attend(Q, cache)                                    # Alg 3 WtdAttn
     O = forward_host(Q_cpu, K_cpu, V_cpu, r)                # host buffers in, host result out
+    comm = NshardComm.create(group)                         # keys of one sequence sharded over ranks
+    O_loc = forward_nshard(comm, Q_loc, K_loc, V_loc, r, n_global, n_offset)
 
 Everything runs in libwildcat.so (hand-written sm_100a kernels behind a C ABI,
 include/wildcat.h).  There is no CPU fallback: CPU tensors raise (except
@@ -22,7 +24,7 @@ from . import _binding as B
 from ._binding import WildcatError, lib  # noqa: F401
 
 __all__ = ["forward", "forward_host", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
-           "STATS_STRIDE"]
+           "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range"]
 
 
 def STATS_STRIDE(d: int) -> int:
@@ -143,4 +145,52 @@ def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda
         O = torch.empty(Od.shape, dtype=Od.dtype, pin_memory=True)
         O.copy_(Od, non_blocking=True)
     s.synchronize()
+    return O
+
+
+# --------------------------------------------------------------------------- n-sharded (PAR3)
+def shard_range(n_global: int, world: int, rank: int):
+    """Contiguous key shard of `rank`: sizes differ by at most one, every rank non-empty."""
+    if not 1 <= world <= n_global:
+        raise WildcatError("need 1 <= world <= n_global")
+    base, extra = divmod(n_global, world)
+    off = rank * base + min(rank, extra)
+    return off, base + (1 if rank < extra else 0)
+
+
+class NshardComm:
+    """NCCL communicator owned by libwildcat (one per process / GPU)."""
+
+    def __init__(self, handle, world: int, rank: int):
+        self.handle, self.world, self.rank = handle, world, rank
+
+    @classmethod
+    def create(cls, world: int | None = None, rank: int | None = None, group=None):
+        import torch.distributed as dist
+
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = [B.wc_comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0, group=group)
+        return cls(B.wc_comm_init(uid[0], world, rank), world, rank)
+
+    def close(self):
+        if self.handle is not None:
+            B.wc_comm_destroy(self.handle)
+            self.handle = None
+
+
+def forward_nshard(comm: NshardComm, Q, K, V, r, n_global, n_offset, seed=0, beta=None, rq=None, clip=True,
+                   S=None, r_eff=None, stream=None):
+    """Alg 4 for one (batch, kv-head) unit whose keys are sharded over the communicator's ranks.
+    K, V: this rank's [1, 1, n_local, d] shard at global offset n_offset; Q: [1, hq, m_local, d]."""
+    Q, K, V = _cont(Q), _cont(K), _cont(V)
+    _require_cuda(Q, K, V)
+    shape = B.make_shape(Q, K, r)
+    opts = B.make_opts(seed, beta, rq, clip)
+    O = torch.empty_like(Q)
+    ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device)
+    B.wildcat_forward_nshard(comm.handle, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libwildcat.so")
 
 WC_F32, WC_BF16 = 0, 1
-WC_OP_SELECT, WC_OP_WEIGHTS, WC_OP_ATTEND, WC_OP_FORWARD = 0, 1, 2, 3
+WC_OP_SELECT, WC_OP_WEIGHTS, WC_OP_ATTEND, WC_OP_FORWARD, WC_OP_FORWARD_NSHARD = 0, 1, 2, 3, 4
 WC_NO_CLIP = 1
 
 
@@ -66,6 +66,13 @@ def lib():
         L.wc_strerror.restype = ctypes.c_char_p
         L.wc_last_launch_count.restype = ctypes.c_int
         L.wc_version.restype = ctypes.c_int
+        L.wc_comm_unique_id.argtypes = [P]
+        L.wc_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), P, ctypes.c_int, ctypes.c_int]
+        L.wc_comm_destroy.argtypes = [P]
+        L.wildcat_forward_nshard.argtypes = [P, S, ctypes.c_int64, ctypes.c_int64, O, P, P, P, P, P, P, P,
+                                             ctypes.c_size_t, P]
+        for f in ("wc_comm_unique_id", "wc_comm_init", "wc_comm_destroy", "wildcat_forward_nshard"):
+            getattr(L, f).restype = ctypes.c_int
         L.wc_timing_enable.argtypes = [ctypes.c_int]
         L.wc_timing_enable.restype = ctypes.c_int
         L.wc_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
@@ -158,3 +165,28 @@ def timing_read(cap: int = 8) -> list:
     if k < 0:
         raise WildcatError(f"wc_timing_read: {lib().wc_strerror(k).decode()}")
     return [float(buf[i]) for i in range(k)]
+
+
+# ---------------------------------------------------------------- n-sharded path (PAR3)
+def wc_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().wc_comm_unique_id(buf), "wc_comm_unique_id")
+    return buf.raw
+
+
+def wc_comm_init(uid: bytes, world: int, rank: int) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(lib().wc_comm_init(ctypes.byref(h), buf, int(world), int(rank)), "wc_comm_init")
+    return h
+
+
+def wc_comm_destroy(h) -> None:
+    _check(lib().wc_comm_destroy(h), "wc_comm_destroy")
+
+
+def wildcat_forward_nshard(comm, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream=None):
+    rc = lib().wildcat_forward_nshard(comm, ctypes.byref(shape), int(n_global), int(n_offset), ctypes.byref(opts),
+                                      _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(r_eff), _ptr(ws),
+                                      ws.numel(), _stream(stream))
+    _check(rc, "wildcat_forward_nshard")

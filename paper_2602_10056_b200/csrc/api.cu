@@ -163,6 +163,9 @@ size_t wc_workspace_bytes(const wc_shape *s, int op) {
             c.take<char>(2 * U * (size_t)D.d * esize(s));
             break;
         }
+        case WC_OP_FORWARD_NSHARD:
+            if (D.units() != 1) return 0;
+            return wc::ns_workspace_bytes(D);
         default:
             return 0;
     }
@@ -281,6 +284,35 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     return finish(total);
 }
 
+int wc_comm_unique_id(void *id128) {
+    if (!id128) return WC_EINVAL;
+    return wc::ns_comm_unique_id(id128);
+}
+
+int wc_comm_init(void **comm, const void *id128, int world, int rank) {
+    if (!comm || !id128 || world < 1 || world > wc::kMaxCpu || rank < 0 || rank >= world) return WC_EINVAL;
+    return wc::ns_comm_init(comm, id128, world, rank);
+}
+
+int wc_comm_destroy(void *comm) { return wc::ns_comm_destroy(comm); }
+
+int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int64_t n_offset, const wc_opts *o,
+                           const void *Q, const void *K, const void *V, void *O, int32_t *S, int32_t *r_eff,
+                           void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_shape(s);
+    if (rc) return rc;
+    if (!comm || !o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
+    if (s->batch != 1 || s->heads_kv != 1) return WC_EUNSUPPORTED;
+    if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
+    if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;
+    const double rq = rq_of(o);
+    int launches = 0;
+    rc = wc::ns_forward(comm, dims_of(s), n_global, n_offset, o, beta_of(s, o), rq, Q, K, V, O, S, r_eff, ws,
+                        static_cast<cudaStream_t>(stream), &launches);
+    if (rc) return rc;
+    return finish(launches);
+}
+
 const char *wc_strerror(int st) {
     switch (st) {
         case WC_OK: return "ok";
@@ -289,6 +321,7 @@ const char *wc_strerror(int st) {
         case WC_EDTYPE: return "unsupported dtype";
         case WC_EWORKSPACE: return "workspace too small or not 256-byte aligned";
         case WC_ECUDA: return "CUDA launch or runtime error";
+        case WC_ENCCL: return "NCCL error";
         case WC_EUNSUPPORTED: return "unsupported configuration in this build (bins != 1)";
     }
     return "unknown status";

@@ -30,6 +30,13 @@ int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, 
                     ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
                     cudaStream_t st);
 
+// The two streaming passes of the prologue on their own (the n-sharded path reduces across GPUs
+// between them): pass 1 -> per-split column sums / V range / max ||q||^2; pass 2 -> nrm2, max rk^2.
+int launch_prologue_pass1(const Dims &D, const void *Q, const void *K, const void *V, bool want_q,
+                          ProloguePartials pp, cudaStream_t st);
+int launch_prologue_pass2(const Dims &D, const void *K, ProloguePartials pp, const double *stats, double *nrm2,
+                          cudaStream_t st);
+
 // Columnwise range of V only (wildcat_weights).
 int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st);
 
@@ -63,9 +70,26 @@ int weights_num_splits(const Dims &D);
 // A3+A4: X = L^{-T} L^{-1} h~(K_S,K)[V,1]; KS gather.  Ypart: [units][splits][r][d+1] fp32.
 int launch_weights(const Dims &D, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
                    const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st);
+// n-sharded variant, phase 1: fp64 partial Y~ over the local keys with the coreset rows given
+// densely (KSin [units][r][d], dtype); Yfull receives the reduced local sum [units][r][d+1].
+int launch_weights_partial_ks(const Dims &D, const void *K, const void *V, const void *KSin, const int32_t *r_eff,
+                              const double *stats, float *Ypart, double *Yfull, cudaStream_t st);
+// phase 2 (after the cross-GPU sum of Yfull): X = L^{-T} L^{-1} Y~.
+int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
+                         cudaStream_t st);
 
 // A5: attend.
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                   const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st);
+
+// n-sharded forward (nshard.cu).  Single unit per call; NCCL resolved at run time.
+size_t ns_workspace_bytes(const Dims &D);
+int ns_forward(void *comm, const Dims &D, int64_t n_global, int64_t n_off, const struct wc_opts *o, double beta,
+               double rq, const void *Q, const void *K, const void *V, void *O, int32_t *S, int32_t *reff, void *ws,
+               cudaStream_t st, int *launches);
+int ns_comm_unique_id(void *id128);
+int ns_comm_init(void **out, const void *id128, int world, int rank);
+int ns_comm_destroy(void *comm);
+int ns_comm_world(void *comm);
 
 }  // namespace wc

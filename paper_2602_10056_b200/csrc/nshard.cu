@@ -1,0 +1,488 @@
+// nshard.cu -- key-dimension sharding of one long sequence across GPUs.
+//
+// Each rank holds a contiguous shard [n_off, n_off + n_local) of the keys/values (and any shard of
+// the queries).  The method is unchanged: the pivot of round i is drawn from the GLOBAL residual
+// diagonal with the same Philox uniform and inverse-CDF rule (Eq. 4; reading Z2), so in
+// exact arithmetic the pivot sequence equals the single-GPU one for any number of ranks.
+// Per round (host-enqueued, no host synchronisation; NCCL over NVLink / NVSwitch):
+//   ns_local_total -> ncclAllGather(per-rank residual totals)
+//   ns_pick        -> owner rank finds s in its shard, writes the pivot packet
+//                     {s, p_s, k_s, F[0:i, s]} (non-owners write zeros)
+//   ncclAllReduce(sum) of the packet (an exact broadcast whose root is only known on the device)
+//   ns_update      -> every rank: kernel column, rank update and downdate of its own keys
+// Prologue: allreduce of column sums (kbar), of max ||q||^2 / value range, then of max rk^2.
+// Weights: per-rank partial Y~ over local keys, allreduce(sum) of Y~, replicated r x r solve.
+// Attend: local queries against the replicated coreset.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "../../include/wildcat.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace wc {
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (resolved at run time)
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    bool ok = false;
+};
+
+const NcclApi &nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
+        a.allReduce = (decltype(a.allReduce))dlsym(h, "ncclAllReduce");
+        a.allGather = (decltype(a.allGather))dlsym(h, "ncclAllGather");
+        a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+        a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.allGather && a.commDestroy;
+        return a;
+    }();
+    return api;
+}
+
+struct Comm {
+    ncclComm_t comm;
+    int world, rank;
+};
+
+constexpr int kNsChunk = 2048;  // keys per chunk (one CTA of ns_update, one chunk total)
+constexpr int kNsT = 256;
+
+struct Ctl {  // device-side loop state
+    int done;
+    int r_eff;
+    double T0;
+    double theta;
+};
+
+// ------------------------------------------------------------------ prologue reductions
+__global__ void ns_pro_reduce1(int d, int P, const double *colsum, const float *vmin, const float *vmax,
+                               const double *rq2, double *sumbuf, double *maxbuf) {
+    // sumbuf[d] = local column sums; maxbuf = [rq2, -vmin[d], vmax[d]]
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double t = 0.0;
+        float a = 3.0e38f, b = -3.0e38f;
+        for (int p = 0; p < P; ++p) {
+            t += colsum[(int64_t)p * d + j];
+            a = fminf(a, vmin[(int64_t)p * d + j]);
+            b = fmaxf(b, vmax[(int64_t)p * d + j]);
+        }
+        sumbuf[j] = t;
+        maxbuf[1 + j] = -(double)a;
+        maxbuf[1 + d + j] = (double)b;
+    }
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int p = 0; p < P; ++p) m = fmax(m, rq2[p]);
+        maxbuf[0] = m;
+    }
+}
+
+template <typename T>
+__global__ void ns_pro_final1(int64_t n_global, int d, const double *sumbuf, const double *maxbuf, double *stats,
+                              T *vmin, T *vmax) {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        stats[8 + j] = sumbuf[j] / (double)n_global;
+        vmin[j] = from_f32<T>((float)(-maxbuf[1 + j]));
+        vmax[j] = from_f32<T>((float)maxbuf[1 + d + j]);
+    }
+}
+
+__global__ void ns_pro_reduce2(int P, const double *rk2, double *rkbuf) {
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int p = 0; p < P; ++p) m = fmax(m, rk2[p]);
+        rkbuf[0] = m;
+    }
+}
+
+// tau (Eq. 7 with the global n), g, mstar; then the loop state.
+__global__ void ns_tau(int64_t n_global, int r, const double *rkbuf, const double *maxbuf, double rq_given,
+                       double beta, double *stats, Ctl *ctl) {
+    if (threadIdx.x != 0) return;
+    const double rk = sqrt(rkbuf[0]);
+    const double rq = rq_given >= 0.0 ? rq_given : sqrt(maxbuf[0]);
+    double tau = 1.0;
+    if (rq * rk > 0.0) {
+        const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
+        const double b0 = log((double)n_global) / (beta * rq * rk) + 2.0;
+        const double w = lambert_w0_dev(b0 / (2.0 * rho0));
+        tau = sqrt((rk / rq) * b0 / (2.0 * w));
+    }
+    const double g = beta / (tau * tau);
+    stats[0] = tau;
+    stats[1] = g;
+    stats[2] = g * rk * rk;
+    stats[3] = rk;
+    stats[4] = rq;
+    stats[5] = 0.0;
+    ctl->done = 0;
+    ctl->r_eff = r;
+    ctl->T0 = 0.0;
+    ctl->theta = 0.0;
+}
+
+// p_l <- h~(k_l, k_l) (Alg 1) and the chunk totals.
+__global__ void __launch_bounds__(kNsT) ns_init(int64_t n, const double *nrm2, const double *stats, double *p,
+                                                double *ctot) {
+    __shared__ double scr[40];
+    const double g = stats[1], mstar = stats[2];
+    const int64_t c0 = (int64_t)blockIdx.x * kNsChunk, c1 = std::min<int64_t>(n, c0 + kNsChunk);
+    double loc = 0.0;
+    for (int64_t l = c0 + threadIdx.x; l < c1; l += kNsT) {
+        const double v = exp(__dadd_rn(__dmul_rn(g, nrm2[l]), -mstar));
+        p[l] = v;
+        loc += v;
+    }
+    loc = block_sum(loc, scr);
+    if (threadIdx.x == 0) ctot[blockIdx.x] = loc;
+}
+
+__global__ void ns_local_total(int nchunks, const double *ctot, const Ctl *ctl, double *sendtot) {
+    if (threadIdx.x != 0) return;
+    double t = 0.0;
+    for (int c = 0; c < nchunks; ++c) t += ctot[c];
+    sendtot[0] = ctl->done ? 0.0 : t;
+}
+
+// Global pivot draw; the owner rank writes the pivot packet {s, p_s, k_s[d], F[0:i, s]}.
+template <typename T, int D>
+__global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int rank, int64_t n, int64_t n_off,
+                                                int nchunks, uint64_t seed, const double *ranktot,
+                                                const double *ctot, const double *p, const T *K, const double *F,
+                                                double *packet, Ctl *ctl) {
+    __shared__ double scr[40];
+    __shared__ int sh_owner, sh_c, sh_s, sh_last, sh_done;
+    __shared__ double sh_t, sh_t2;
+    const int tid = threadIdx.x;
+    const int plen = 2 + D + r;
+    for (int j = tid; j < plen; j += kNsT) packet[j] = 0.0;
+    if (tid == 0) {
+        sh_done = ctl->done;
+        sh_owner = -1;
+        if (!sh_done) {
+            double Tt = 0.0;
+            for (int q = 0; q < world; ++q) Tt += ranktot[q];
+            if (i == 0) {
+                ctl->T0 = Tt;
+                ctl->theta = 1000.0 * (double)r * 2.220446049250313e-16 * Tt;
+            }
+            if (Tt <= ctl->theta) {
+                ctl->done = 1;
+                ctl->r_eff = i;
+                sh_done = 1;
+            } else {
+                const double t = pivot_uniform(seed, (uint32_t)i, 0ull) * Tt;
+                double acc = 0.0, excl = 0.0, last_excl = 0.0;
+                int ow = -1, last = -1;
+                for (int q = 0; q < world; ++q) {
+                    const double v = ranktot[q];
+                    if (v > 0.0) { last = q; last_excl = acc; }
+                    const double na = acc + v;
+                    if (ow < 0 && na > t) { ow = q; excl = acc; }
+                    acc = na;
+                }
+                if (ow < 0) { ow = last; excl = last_excl; }
+                sh_owner = ow;
+                sh_t = t - excl;
+            }
+        }
+    }
+    __syncthreads();
+    if (sh_done || sh_owner != rank) return;
+    // owner: chunk by the local chunk totals (fixed order), then key inside the chunk
+    if (tid == 0) {
+        double acc = 0.0, excl = 0.0, last_excl = 0.0;
+        int cs = -1, last = -1;
+        for (int c = 0; c < nchunks; ++c) {
+            const double v = ctot[c];
+            if (v > 0.0) { last = c; last_excl = acc; }
+            const double na = acc + v;
+            if (cs < 0 && na > sh_t) { cs = c; excl = acc; }
+            acc = na;
+        }
+        if (cs < 0) { cs = last; excl = last_excl; }
+        sh_c = cs;
+        sh_t2 = sh_t - excl;
+        sh_s = 0x7fffffff;
+        sh_last = -1;
+    }
+    __syncthreads();
+    const int64_t c0 = (int64_t)sh_c * kNsChunk, c1 = std::min<int64_t>(n, c0 + kNsChunk);
+    const int64_t per = ceil_div(c1 - c0, kNsT);
+    const int64_t b0 = c0 + (int64_t)tid * per, b1 = std::min<int64_t>(c1, b0 + per);
+    double v = 0.0;
+    for (int64_t l = b0; l < b1; ++l) v += p[l];
+    double tot;
+    double run = block_exclusive_scan(v, scr, &tot);
+    int found = -1, lastpos = -1;
+    for (int64_t l = b0; l < b1; ++l) {
+        const double pl = p[l];
+        if (pl > 0.0) lastpos = (int)l;
+        run += pl;
+        if (found < 0 && run > sh_t2) found = (int)l;
+    }
+    if (found >= 0) atomicMin(&sh_s, found);
+    if (lastpos >= 0) atomicMax(&sh_last, lastpos);
+    __syncthreads();
+    const int s = sh_s != 0x7fffffff ? sh_s : sh_last;
+    if (tid == 0) {
+        packet[0] = (double)(n_off + s);
+        packet[1] = p[s];
+    }
+    for (int j = tid; j < D; j += kNsT) packet[2 + j] = to_f64(K[(int64_t)s * D + j]);
+    for (int j = tid; j < i; j += kNsT) packet[2 + D + j] = F[(int64_t)j * n + s];
+}
+
+// Kernel column, rank update and downdate of this rank's keys (one CTA per 2048-key chunk).
+template <typename T, int D>
+__global__ void __launch_bounds__(kNsT) ns_update(int i, int r, int64_t n, int64_t n_off, const T *K,
+                                                  const double *stats, const double *packet, double *F, double *p,
+                                                  double *ctot, int32_t *S, double *L, T *KS, const Ctl *ctl) {
+    extern __shared__ double nsm[];
+    double *kcs = nsm;      // [D]
+    double *fs = kcs + D;   // [r]
+    double *kb = fs + r;    // [D]
+    double *scr = kb + D;   // [40]
+    if (ctl->done) return;
+    const int tid = threadIdx.x;
+    const double g = stats[1], mstar = stats[2];
+    const int64_t s_glob = (int64_t)packet[0];
+    const double ps = packet[1];
+    for (int j = tid; j < D; j += kNsT) {
+        kb[j] = stats[8 + j];
+        kcs[j] = __dadd_rn(packet[2 + j], -stats[8 + j]);
+    }
+    for (int j = tid; j < i; j += kNsT) fs[j] = packet[2 + D + j];
+    __syncthreads();
+    const double rs = sqrt(ps);
+    if (blockIdx.x == 0) {  // replicated outputs: S, L row i (L[i][i] = sqrt(p_s) = F[i, s] exactly), K_S row i
+        for (int j = tid; j < i; j += kNsT) L[(int64_t)i * r + j] = fs[j];
+        for (int j = tid; j < D; j += kNsT) KS[(int64_t)i * D + j] = from_f32<T>((float)packet[2 + j]);
+        if (tid == 0) {
+            S[i] = (int32_t)s_glob;
+            L[(int64_t)i * r + i] = rs;
+        }
+    }
+    const int64_t c0 = (int64_t)blockIdx.x * kNsChunk, c1 = std::min<int64_t>(n, c0 + kNsChunk);
+    double loc = 0.0;
+    for (int64_t l = c0 + tid; l < c1; l += kNsT) {
+        double dot = 0.0;
+        for (int j = 0; j < D; ++j)
+            dot = __dadd_rn(dot, __dmul_rn(__dadd_rn(to_f64(K[l * D + j]), -kb[j]), kcs[j]));
+        const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
+        double acc = 0.0;
+        for (int j = 0; j < i; ++j) acc = __dadd_rn(acc, __dmul_rn(F[(int64_t)j * n + l], fs[j]));
+        const double f = (hval - acc) / rs;
+        F[(int64_t)i * n + l] = f;
+        double q = __dadd_rn(p[l], -__dmul_rn(f, f));
+        q = q > 0.0 ? q : 0.0;
+        if (n_off + l == s_glob) q = 0.0;
+        p[l] = q;
+        loc += q;
+    }
+    loc = block_sum(loc, scr);
+    if (tid == 0) ctot[blockIdx.x] = loc;
+}
+
+__global__ void ns_finish(const Ctl *ctl, int32_t *r_eff_out, double *stats) {
+    if (threadIdx.x == 0) {
+        *r_eff_out = ctl->r_eff;
+        stats[5] = ctl->T0;
+    }
+}
+
+struct NsWs {
+    ProloguePartials pp;
+    double *stats, *nrm2, *p, *F, *ctot, *sendtot, *ranktot, *packet, *sumbuf, *maxbuf, *rkbuf, *L, *Yfull;
+    float *Ypart, *X;
+    void *KS, *vmin, *vmax;
+    int32_t *S, *reff;
+    Ctl *ctl;
+};
+
+struct Carve {
+    char *base;
+    size_t off = 0;
+    template <typename U> U *take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        U *q = base ? reinterpret_cast<U *>(base + off) : nullptr;
+        off += count * sizeof(U);
+        return q;
+    }
+};
+
+size_t ns_carve(const Dims &D, void *base, NsWs &w) {
+    Carve c{static_cast<char *>(base)};
+    const int P = prologue_num_splits(D);
+    const int64_t nch = ceil_div(D.n, kNsChunk);
+    const size_t e = D.dtype == 0 ? 4 : 2;
+    w.pp.P = P;
+    w.pp.colsum = c.take<double>((size_t)P * D.d);
+    w.pp.vmin = c.take<float>((size_t)P * D.d);
+    w.pp.vmax = c.take<float>((size_t)P * D.d);
+    w.pp.rq2 = c.take<double>(P);
+    w.pp.rk2 = c.take<double>(P);
+    w.stats = c.take<double>(8 + D.d);
+    w.nrm2 = c.take<double>(D.n);
+    w.p = c.take<double>(D.n);
+    w.F = c.take<double>((size_t)D.r * D.n);
+    w.ctot = c.take<double>(nch);
+    w.sendtot = c.take<double>(1);
+    w.ranktot = c.take<double>(kMaxCpu);
+    w.packet = c.take<double>(2 + D.d + D.r);
+    w.sumbuf = c.take<double>(D.d);
+    w.maxbuf = c.take<double>(1 + 2 * D.d);
+    w.rkbuf = c.take<double>(1);
+    w.L = c.take<double>((size_t)D.r * D.r);
+    const int splits = weights_num_splits(D);
+    w.Ypart = c.take<float>((size_t)splits * D.r * (D.d + 1) + 2);
+    w.Yfull = c.take<double>((size_t)D.r * (D.d + 1));
+    w.X = c.take<float>((size_t)D.r * (D.d + 1));
+    w.KS = c.take<char>((size_t)D.r * D.d * e);
+    w.vmin = c.take<char>((size_t)D.d * e);
+    w.vmax = c.take<char>((size_t)D.d * e);
+    w.S = c.take<int32_t>(D.r);
+    w.reff = c.take<int32_t>(1);
+    w.ctl = c.take<Ctl>(1);
+    return ((c.off + 255) & ~size_t(255)) + 256;
+}
+
+int nccl_status(ncclResult_t r) { return r == ncclSuccess ? WC_OK : WC_ENCCL; }
+
+template <typename T, int D>
+int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, const wc_opts *o, double beta,
+                 double rq, const void *Q, const void *K, const void *V, void *O, int32_t *S_out, int32_t *reff_out,
+                 NsWs &w, cudaStream_t st, int *launches_out) {
+    const NcclApi &api = nccl();
+    const int64_t n = Dm.n;
+    const int nch = (int)ceil_div(n, kNsChunk);
+    const int r = Dm.r;
+    const bool want_q = rq < 0.0 && Dm.m > 0 && Q != nullptr;
+    int launches = 0;
+#define WC_NCCL(x)                                  \
+    do {                                            \
+        const int rc_ = nccl_status(x);             \
+        if (rc_) return rc_;                        \
+    } while (0)
+    // ---- A0 prologue with cross-rank reductions
+    if (cudaMemsetAsync(w.S, 0xff, sizeof(int32_t) * r, st) != cudaSuccess) return WC_ECUDA;
+    if (cudaMemsetAsync(w.L, 0, sizeof(double) * r * r, st) != cudaSuccess) return WC_ECUDA;
+    if (launch_prologue_pass1(Dm, Q, K, V, want_q, w.pp, st) < 0) return WC_ECUDA;
+    ns_pro_reduce1<<<1, 128, 0, st>>>(D, w.pp.P, w.pp.colsum, w.pp.vmin, w.pp.vmax, w.pp.rq2, w.sumbuf, w.maxbuf);
+    WC_NCCL(api.allReduce(w.sumbuf, w.sumbuf, D, ncclFloat64, ncclSum, cm->comm, st));
+    WC_NCCL(api.allReduce(w.maxbuf, w.maxbuf, 1 + 2 * D, ncclFloat64, ncclMax, cm->comm, st));
+    ns_pro_final1<T><<<1, 128, 0, st>>>(n_global, D, w.sumbuf, w.maxbuf, w.stats, static_cast<T *>(w.vmin),
+                                        static_cast<T *>(w.vmax));
+    if (launch_prologue_pass2(Dm, K, w.pp, w.stats, w.nrm2, st) < 0) return WC_ECUDA;
+    ns_pro_reduce2<<<1, 32, 0, st>>>(w.pp.P, w.pp.rk2, w.rkbuf);
+    WC_NCCL(api.allReduce(w.rkbuf, w.rkbuf, 1, ncclFloat64, ncclMax, cm->comm, st));
+    ns_tau<<<1, 32, 0, st>>>(n_global, r, w.rkbuf, w.maxbuf, want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, w.stats,
+                             w.ctl);
+    ns_init<<<nch, kNsT, 0, st>>>(n, w.nrm2, w.stats, w.p, w.ctot);
+    launches += 8;
+    // ---- A1 + A2: r rounds
+    const size_t usm = (size_t)(2 * D + r + 40) * sizeof(double);
+    auto upd = ns_update<T, D>;
+    if (usm > 48 * 1024) cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+    for (int i = 0; i < r; ++i) {
+        ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot);
+        WC_NCCL(api.allGather(w.sendtot, w.ranktot, 1, ncclFloat64, cm->comm, st));
+        ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, w.ranktot, w.ctot, w.p,
+                                           static_cast<const T *>(K), w.F, w.packet, w.ctl);
+        WC_NCCL(api.allReduce(w.packet, w.packet, 2 + D + r, ncclFloat64, ncclSum, cm->comm, st));
+        upd<<<nch, kNsT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,
+                                    w.S, w.L, static_cast<T *>(w.KS), w.ctl);
+        launches += 3;
+    }
+    ns_finish<<<1, 32, 0, st>>>(w.ctl, w.reff, w.stats);
+    // ---- A3 + A4: local partial Y~, allreduce, replicated solve
+    if (launch_weights_partial_ks(Dm, K, V, w.KS, w.reff, w.stats, w.Ypart, w.Yfull, st) < 0) return WC_ECUDA;
+    WC_NCCL(api.allReduce(w.Yfull, w.Yfull, (size_t)r * (D + 1), ncclFloat64, ncclSum, cm->comm, st));
+    if (launch_weights_solve(Dm, w.Yfull, w.L, w.reff, w.X, st) < 0) return WC_ECUDA;
+    // ---- A5: local queries
+    const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
+    if (Dm.m > 0 && launch_attend(Dm, Q, w.KS, w.X, w.reff, w.vmin, w.vmax, beta, clip, O, st) < 0) return WC_ECUDA;
+    if (S_out && cudaMemcpyAsync(S_out, w.S, sizeof(int32_t) * r, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return WC_ECUDA;
+    if (reff_out && cudaMemcpyAsync(reff_out, w.reff, sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return WC_ECUDA;
+    launches += 5;
+#undef WC_NCCL
+    *launches_out = launches;
+    return cudaPeekAtLastError() == cudaSuccess ? WC_OK : WC_ECUDA;
+}
+
+}  // namespace
+
+size_t ns_workspace_bytes(const Dims &D) {
+    NsWs w;
+    return ns_carve(D, nullptr, w);
+}
+
+int ns_forward(void *comm, const Dims &D, int64_t n_global, int64_t n_off, const wc_opts *o, double beta, double rq,
+               const void *Q, const void *K, const void *V, void *O, int32_t *S, int32_t *reff, void *ws,
+               cudaStream_t st, int *launches) {
+    NsWs w;
+    ns_carve(D, ws, w);
+    Comm *cm = static_cast<Comm *>(comm);
+#define WC_NSF(TT, DD) return ns_forward_t<TT, DD>(cm, D, n_global, n_off, o, beta, rq, Q, K, V, O, S, reff, w, st, launches)
+    if (D.dtype == 0) {
+        switch (D.d) { case 16: WC_NSF(float, 16); case 32: WC_NSF(float, 32); case 64: WC_NSF(float, 64); case 128: WC_NSF(float, 128); }
+    } else {
+        switch (D.d) { case 16: WC_NSF(__nv_bfloat16, 16); case 32: WC_NSF(__nv_bfloat16, 32); case 64: WC_NSF(__nv_bfloat16, 64); case 128: WC_NSF(__nv_bfloat16, 128); }
+    }
+#undef WC_NSF
+    return WC_EINVAL;
+}
+
+int ns_comm_unique_id(void *id128) {
+    const NcclApi &api = nccl();
+    if (!api.ok) return WC_EUNSUPPORTED;
+    ncclUniqueId id;
+    if (api.getUniqueId(&id) != ncclSuccess) return WC_ENCCL;
+    std::memcpy(id128, &id, sizeof(id));
+    return WC_OK;
+}
+
+int ns_comm_init(void **out, const void *id128, int world, int rank) {
+    const NcclApi &api = nccl();
+    if (!api.ok) return WC_EUNSUPPORTED;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    Comm *c = new Comm{nullptr, world, rank};
+    if (api.commInitRank(&c->comm, world, id, rank) != ncclSuccess) {
+        delete c;
+        return WC_ENCCL;
+    }
+    *out = c;
+    return WC_OK;
+}
+
+int ns_comm_destroy(void *comm) {
+    if (!comm) return WC_OK;
+    Comm *c = static_cast<Comm *>(comm);
+    const NcclApi &api = nccl();
+    if (api.ok && c->comm) api.commDestroy(c->comm);
+    delete c;
+    return WC_OK;
+}
+
+int ns_comm_world(void *comm) { return comm ? static_cast<Comm *>(comm)->world : 0; }
+
+}  // namespace wc

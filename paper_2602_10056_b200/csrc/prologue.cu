@@ -240,6 +240,37 @@ int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmi
 
 }  // namespace
 
+template <typename T>
+int launch_pass1_t(const Dims &D, const void *Q, const void *K, const void *V, bool want_q, ProloguePartials pp,
+                   cudaStream_t st) {
+    const int RG = kPT / (D.d / 8);
+    const size_t smem = (size_t)RG * D.d * (sizeof(double) + 2 * sizeof(float));
+    const int64_t mq = want_q ? (int64_t)D.group() * D.m : 0;
+    dim3 grid(pp.P, D.units());
+    prologue_pass1<T><<<grid, kPT, smem, st>>>(static_cast<const T *>(Q), static_cast<const T *>(K),
+                                               static_cast<const T *>(V), D.n, mq, D.d, pp.P, want_q ? 1 : 0, 1,
+                                               pp.colsum, pp.vmin, pp.vmax, pp.rq2, (int64_t)D.group() * D.m);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+template <typename T>
+int launch_pass2_t(const Dims &D, const void *K, ProloguePartials pp, const double *stats, double *nrm2,
+                   cudaStream_t st) {
+    dim3 grid(pp.P, D.units());
+    prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, pp.P, stats, nrm2, pp.rk2);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_prologue_pass1(const Dims &D, const void *Q, const void *K, const void *V, bool want_q,
+                          ProloguePartials pp, cudaStream_t st) {
+    if (D.dtype == 0) return launch_pass1_t<float>(D, Q, K, V, want_q, pp, st);
+    return launch_pass1_t<__nv_bfloat16>(D, Q, K, V, want_q, pp, st);
+}
+int launch_prologue_pass2(const Dims &D, const void *K, ProloguePartials pp, const double *stats, double *nrm2,
+                          cudaStream_t st) {
+    if (D.dtype == 0) return launch_pass2_t<float>(D, K, pp, stats, nrm2, st);
+    return launch_pass2_t<__nv_bfloat16>(D, K, pp, stats, nrm2, st);
+}
+
 int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin, void *vmax, cudaStream_t st) {
     if (D.dtype == 0) return launch_vrange_t<float>(D, V, pp, vmin, vmax, st);
     return launch_vrange_t<__nv_bfloat16>(D, V, pp, vmin, vmax, st);

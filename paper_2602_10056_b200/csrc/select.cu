@@ -581,37 +581,59 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         }
         cw_sync();
         if (sh_done) break;
-        // ---- A1b: inverse CDF inside c*'s slice (all compute threads, block scan, fixed order)
+        // ---- A1b: inverse CDF inside c*'s slice (all compute threads, block scan, fixed order).
+        // The finder publishes p_s from its registers (no extra global round trip).
+        int s;
         {
             const int64_t slo = std::min<int64_t>(n, (int64_t)sh_cstar * chunk);
             const int64_t shi = std::min<int64_t>(n, slo + chunk);
             const int64_t per = ceil_div(shi - slo, kCT);
             const int64_t b0 = slo + (int64_t)tid * per, b1 = std::min<int64_t>(shi, b0 + per);
             const double tp = sh_t;
+            constexpr int kC = 4;  // fast path: slice <= 4 * 256 keys, values kept in registers
+            double pr[kC];
             double v = 0.0;
-            for (int64_t l = b0; l < b1; ++l) v += __ldcg(cur + l);
+            if (per <= kC) {
+#pragma unroll
+                for (int q = 0; q < kC; ++q) pr[q] = (b0 + q < b1) ? __ldcg(cur + b0 + q) : 0.0;
+#pragma unroll
+                for (int q = 0; q < kC; ++q) v += pr[q];
+            } else {
+                for (int64_t l = b0; l < b1; ++l) v += __ldcg(cur + l);
+            }
             const double ex = cw_exclusive_scan(v, scr);
             double run = ex;
             int found = -1, lastpos = -1;
-            for (int64_t l = b0; l < b1; ++l) {
-                const double pl = __ldcg(cur + l);
-                if (pl > 0.0) lastpos = (int)l;
-                run += pl;
-                if (found < 0 && run > tp) found = (int)l;
+            double fval = 0.0, lval = 0.0;
+            if (per <= kC) {
+#pragma unroll
+                for (int q = 0; q < kC; ++q) {
+                    if (b0 + q < b1) {
+                        const double pl = pr[q];
+                        if (pl > 0.0) { lastpos = (int)(b0 + q); lval = pl; }
+                        run += pl;
+                        if (found < 0 && run > tp) { found = (int)(b0 + q); fval = pl; }
+                    }
+                }
+            } else {
+                for (int64_t l = b0; l < b1; ++l) {
+                    const double pl = __ldcg(cur + l);
+                    if (pl > 0.0) { lastpos = (int)l; lval = pl; }
+                    run += pl;
+                    if (found < 0 && run > tp) { found = (int)l; fval = pl; }
+                }
             }
             if (found >= 0) atomicMin(&sh_s, found);
             if (lastpos >= 0) atomicMax(&sh_last, lastpos);
             cw_sync();
-            if (tid == 0) {
-                if (sh_s == 0x7fffffff) sh_s = sh_last;  // rounding fallback (reading Z2)
-                sh_ps = __ldcg(cur + sh_s);
-            }
+            const int smin = sh_s;
+            s = (smin != 0x7fffffff) ? smin : sh_last;  // rounding fallback (reading Z2)
+            if (smin != 0x7fffffff ? (found == s) : (lastpos == s)) sh_ps = (smin != 0x7fffffff) ? fval : lval;
         }
         WC_TR(0);
         cw_sync();
         WC_TR(2);
         const int cstar = sh_cstar;
-        const int s = sh_s;
         // ---- pivot data: centred k_s (fp64), c0 = <kbar, k_s - kbar>, F[0:i, s]
         if (w < (D + 31) / 32) {  // warp-uniform
             double pr = 0.0;

@@ -27,6 +27,7 @@ constexpr int kTL = 32;   // keys per smem tile
 template <typename T, int D>
 __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restrict__ K, const T *__restrict__ V,
                                                               const int32_t *__restrict__ S,
+                                                              const T *__restrict__ KSin,
                                                               const int32_t *__restrict__ r_eff,
                                                               const double *__restrict__ stats, int64_t n,
                                                               int r, int splits, float *__restrict__ Ypart) {
@@ -53,8 +54,8 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
         const int a = e / D, j = e % D;
         float v = 0.f;
         if (a0 + a < re) {
-            const int s = S[(int64_t)u * r + a0 + a];
-            v = (float)(to_f64(Ku[(int64_t)s * D + j]) - kb[j]);
+            const T *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + a) * D : Ku + (int64_t)S[(int64_t)u * r + a0 + a] * D;
+            v = (float)(to_f64(ksrow[j]) - kb[j]);
         }
         kcS[a][j] = v;
     }
@@ -266,7 +267,8 @@ constexpr int kWTc = 128;
 template <int D>
 __global__ void __launch_bounds__(kWTc, 1)
     weights_tc_kernel(const __nv_bfloat16 *__restrict__ K, const __nv_bfloat16 *__restrict__ V,
-                      const int32_t *__restrict__ S, const int32_t *__restrict__ r_eff,
+                      const int32_t *__restrict__ S, const __nv_bfloat16 *__restrict__ KSin,
+                      const int32_t *__restrict__ r_eff,
                       const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
     constexpr int DC = D + 1;
     constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
@@ -298,19 +300,21 @@ __global__ void __launch_bounds__(kWTc, 1)
         const int row = e / CPR, cc = e % CPR;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (a0 + row < re) {
-            const int sidx = S[(int64_t)u * r + a0 + row];
-            v = __ldg(reinterpret_cast<const uint4 *>(Ku + (int64_t)sidx * D) + cc);
+            const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + row) * D
+                                              : Ku + (int64_t)S[(int64_t)u * r + a0 + row] * D;
+            v = __ldg(reinterpret_cast<const uint4 *>(ksrow) + cc);
         }
         *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(row, cc * 8, 128)) = v;
     }
     float alpha = 0.f;
     const bool row_ok = a0 + tid < re;
     if (row_ok) {
-        const int sidx = S[(int64_t)u * r + a0 + tid];
+        const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + tid) * D
+                                          : Ku + (int64_t)S[(int64_t)u * r + a0 + tid] * D;
         double kk = 0.0, bb = 0.0;
         for (int j = 0; j < D; ++j) {
             const double kbj = st[8 + j];
-            kk = fma(to_f64(Ku[(int64_t)sidx * D + j]), kbj, kk);
+            kk = fma(to_f64(ksrow[j]), kbj, kk);
             bb = fma(kbj, kbj, bb);
         }
         alpha = (float)(g * (bb - kk) - mstar);
@@ -423,12 +427,15 @@ __global__ void __launch_bounds__(kWTc, 1)
     if (w == 0) umma::tmem_dealloc(tbase, 256);
 }
 
+// A3: fp32 split partials of Y~ (tensor-core kernel for bf16 and d in {64, 128}), then their
+// fixed-order fp64 sum into Yfull.  Coreset rows come from K[S] or, if KSin != nullptr, densely.
 template <typename T, int D>
-int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
-                      const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
+int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const void *KSin,
+                      const int32_t *r_eff, const double *stats, float *Ypart, double **Yfull_out, cudaStream_t st) {
     const int units = Dm.units();
     const int splits = weights_num_splits(Dm);
     static const char *mode = std::getenv("WC_WEIGHTS");  // "cuda": CUDA-core kernel (A/B tests)
+    bool done = false;
     if constexpr (sizeof(T) == 2 && (D == 64 || D == 128)) {
         if (!(mode && std::strcmp(mode, "cuda") == 0)) {
             const int smem_tc = 3 * 128 * D * 2 + 128 * 128 * 2 + 128 * 4 + D * 4 + 1024;  // A, B, V^T, P, gamma, kbar
@@ -436,36 +443,52 @@ int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_
             cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
             dim3 gt(splits, (Dm.r + 127) / 128, units);
             kt<<<gt, kWTc, smem_tc, st>>>(static_cast<const __nv_bfloat16 *>(K), static_cast<const __nv_bfloat16 *>(V),
-                                          S, r_eff, stats, Dm.n, Dm.r, splits, Ypart);
-            goto solve;
+                                          S, static_cast<const __nv_bfloat16 *>(KSin), r_eff, stats, Dm.n, Dm.r,
+                                          splits, Ypart);
+            done = true;
         }
     }
-    {
-    dim3 g1(splits, (Dm.r + kTA - 1) / kTA, units);
-    const size_t smem1 = D * sizeof(double) + (size_t)(kTA + 2 * kTL) * (D + 1) * sizeof(float) +
-                         (size_t)kTA * (kTL + 1) * sizeof(float);
-    auto pk = weights_partial_kernel<T, D>;
-    if (smem1 > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-    pk<<<g1, kWT, smem1, st>>>(static_cast<const T *>(K), static_cast<const T *>(V), S,
-                                                      r_eff, stats, Dm.n, Dm.r, splits, Ypart);
+    if (!done) {
+        dim3 g1(splits, (Dm.r + kTA - 1) / kTA, units);
+        const size_t smem1 = D * sizeof(double) + (size_t)(kTA + 2 * kTL) * (D + 1) * sizeof(float) +
+                             (size_t)kTA * (kTL + 1) * sizeof(float);
+        auto pk = weights_partial_kernel<T, D>;
+        if (smem1 > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        pk<<<g1, kWT, smem1, st>>>(static_cast<const T *>(K), static_cast<const T *>(V), S,
+                                   static_cast<const T *>(KSin), r_eff, stats, Dm.n, Dm.r, splits, Ypart);
     }
-solve:
     const size_t parts = (size_t)units * splits * Dm.r * (D + 1);
-    double *Yfull = reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
-    {
-        const int64_t cnt = (int64_t)Dm.r * (D + 1);
-        dim3 gr((unsigned)ceil_div(cnt, 256), units);
-        weights_reduce_kernel<D><<<gr, 256, 0, st>>>(Ypart, r_eff, Dm.r, splits, Yfull);
-    }
+    double *Yfull = *Yfull_out ? *Yfull_out : reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
+    const int64_t cnt = (int64_t)Dm.r * (D + 1);
+    dim3 gr((unsigned)ceil_div(cnt, 256), units);
+    weights_reduce_kernel<D><<<gr, 256, 0, st>>>(Ypart, r_eff, Dm.r, splits, Yfull);
+    *Yfull_out = Yfull;
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+}
+
+template <int D>
+int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
+                   cudaStream_t st) {
     const size_t smem = (size_t)8 * Dm.r * sizeof(double);
     auto sk = weights_solve_kernel<D>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 g2((D + 1 + 7) / 8, units);
+    dim3 g2((D + 1 + 7) / 8, Dm.units());
     sk<<<g2, 256, smem, st>>>(Yfull, L, r_eff, Dm.r, X);
-    dim3 g3(Dm.r, units);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename T, int D>
+int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
+                      const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
+    double *Yfull = nullptr;
+    const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st);
+    if (k1 < 0) return -1;
+    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, st);
+    if (k2 < 0) return -1;
+    dim3 g3(Dm.r, Dm.units());
     gather_ks_kernel<T, D><<<g3, 128, 0, st>>>(static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
                                                static_cast<T *>(KS));
-    return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? k1 + k2 + 1 : -1;
 }
 
 template <typename T>
@@ -481,6 +504,30 @@ int launch_weights_t(const Dims &Dm, const void *K, const void *V, const int32_t
 }
 
 }  // namespace
+
+int launch_weights_partial_ks(const Dims &D, const void *K, const void *V, const void *KSin, const int32_t *r_eff,
+                              const double *stats, float *Ypart, double *Yfull, cudaStream_t st) {
+    double *Y = Yfull;
+#define WC_PKS(TT, DD) return launch_partial_td<TT, DD>(D, K, V, nullptr, KSin, r_eff, stats, Ypart, &Y, st)
+    if (D.dtype == 0) {
+        switch (D.d) { case 16: WC_PKS(float, 16); case 32: WC_PKS(float, 32); case 64: WC_PKS(float, 64); case 128: WC_PKS(float, 128); }
+    } else {
+        switch (D.d) { case 16: WC_PKS(__nv_bfloat16, 16); case 32: WC_PKS(__nv_bfloat16, 32); case 64: WC_PKS(__nv_bfloat16, 64); case 128: WC_PKS(__nv_bfloat16, 128); }
+    }
+#undef WC_PKS
+    return -1;
+}
+
+int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
+                         cudaStream_t st) {
+    switch (D.d) {
+        case 16: return launch_solve_d<16>(D, Yfull, L, r_eff, X, st);
+        case 32: return launch_solve_d<32>(D, Yfull, L, r_eff, X, st);
+        case 64: return launch_solve_d<64>(D, Yfull, L, r_eff, X, st);
+        case 128: return launch_solve_d<128>(D, Yfull, L, r_eff, X, st);
+    }
+    return -1;
+}
 
 int weights_num_splits(const Dims &D) {
     const bool tc = D.dtype == 1 && (D.d == 64 || D.d == 128);

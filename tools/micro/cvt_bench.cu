@@ -25,7 +25,9 @@ __global__ void k(const uint4 *in, const double *kc, double *out, int iters) {
             const uint32_t wd[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const double x = MODE == 0 ? cvt_f2f(wd[e >> 1], e & 1) : cvt_int(wd[e >> 1], e & 1);
+                const double x = MODE == 0 ? cvt_f2f(wd[e >> 1], e & 1)
+                                 : MODE == 1 ? cvt_int(wd[e >> 1], e & 1)
+                                 : ((e & 1) ? cvt_int(wd[e >> 1], 1) : cvt_f2f(wd[e >> 1], 0));
                 double &a = (e & 3) == 0 ? acc0 : (e & 3) == 1 ? acc1 : (e & 3) == 2 ? acc2 : acc3;
                 a = fma(x, s[q * 8 + e], a);
             }
@@ -36,22 +38,23 @@ __global__ void k(const uint4 *in, const double *kc, double *out, int iters) {
 }
 int main() {
     const int blocks = 148, iters = 200;
-    for (int threads = 256; threads <= 1024; threads *= 2) {
+    for (int threads = 256; threads <= 256; threads *= 2) {
     uint4 *in; double *kc, *out;
     cudaMalloc(&in, sizeof(uint4) * 16 * blocks * threads);
     cudaMemset(in, 0x3f, sizeof(uint4) * 16 * blocks * threads);
     cudaMalloc(&kc, 128 * 8); cudaMemset(kc, 0, 128 * 8);
     cudaMalloc(&out, 8 * blocks * threads);
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 3; ++mode) {
         for (int warm = 0; warm < 2; ++warm) {
             cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
             cudaEventRecord(a);
             if (mode == 0) k<0><<<blocks, threads>>>(in, kc, out, iters);
-            else k<1><<<blocks, threads>>>(in, kc, out, iters);
+            else if (mode == 1) k<1><<<blocks, threads>>>(in, kc, out, iters);
+            else k<2><<<blocks, threads>>>(in, kc, out, iters);
             cudaEventRecord(b); cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
             const double elems = (double)blocks * threads * iters * 128;
-            if (warm) printf("threads %d mode %s: %.3f ms, %.2f elem/clk/SM (at 1.965 GHz)\n", threads, mode ? "int" : "f2f", ms,
+            if (warm) printf("threads %d mode %s: %.3f ms, %.2f elem/clk/SM (at 1.965 GHz)\n", threads, mode == 2 ? "mix" : mode ? "int" : "f2f", ms,
                              elems / (ms * 1e-3) / 1.965e9 / 148);
         }
     }
