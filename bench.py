@@ -187,6 +187,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-queries", type=int, default=2048)
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--mode", default=None, choices=["replicas", "nshard"],
+                    help="replicas: each rank runs the workload on its own units (weak scaling); "
+                         "nshard: one sequence's keys sharded over the ranks (strong scaling). "
+                         "Default: nshard for the long* configs, replicas otherwise")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -211,17 +215,30 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    # replica per rank (weak scaling): same workload, rank-specific seed
-    Q, K, V = make_config(cfg, seed=cfg.seed + rank)
-    Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+    mode = args.mode or ("nshard" if cfg.name.startswith("long") else "replicas")
     units = cfg.units
     S = torch.empty(units, cfg.r, dtype=torch.int32, device=dev)
     R = torch.empty(units, dtype=torch.int32, device=dev)
     flush = torch.empty(args.flush_mb * (1 << 20), dtype=torch.uint8, device=dev)
-    seed = cfg.seed + rank
+    if mode == "nshard":
+        # one sequence, keys/values/queries sharded along the sequence over the ranks (strong scaling)
+        from paper_2602_10056_b200.inputs import make_long_shard
 
-    def step():
-        return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R)
+        Q, K, V, koff = make_long_shard(cfg, world, rank)
+        Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+        seed = cfg.seed
+        comm = wc.NshardComm.create()
+
+        def step():
+            return wc.forward_nshard(comm, Qd, Kd, Vd, cfg.r, cfg.n, koff, seed=seed, S=S[0], r_eff=R)
+    else:
+        # replica per rank (weak scaling): same workload, rank-specific seed
+        Q, K, V = make_config(cfg, seed=cfg.seed + rank)
+        Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+        seed = cfg.seed + rank
+
+        def step():
+            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R)
 
     for _ in range(args.warmup):
         step()
@@ -258,16 +275,18 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    queries_per_rank = cfg.batch * cfg.hq * cfg.m
+    queries_per_rank = cfg.batch * cfg.hq * cfg.m if mode == "replicas" else cfg.batch * cfg.hq * cfg.m / world
     value = queries_per_rank * world * args.steps / (total_ms / 1e3)
 
     # stage breakdown (ms, mean over timed steps): prologue, select, weights, attend
     st_names = ["prologue", "select", "weights", "attend"]
-    st_mean = [statistics.mean(s[i] for s in stages) for i in range(4)]
+    st_mean = ([statistics.mean(s[i] for s in stages) for i in range(4)] if all(len(s) >= 4 for s in stages)
+               else None)
     e = 2 if cfg.dtype == "bf16" else 4
     r_eff = int(R.min().item())
     alg_bytes = units * select_bytes(cfg.n, cfg.d, r_eff, e)
-    achieved = alg_bytes / (st_mean[1] / 1e3) / 1e9
+    sel_ms = st_mean[1] if st_mean else None
+    achieved = alg_bytes / (sel_ms / 1e3) / 1e9 if sel_ms else None
     peak, peak_kind = peaks()
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}.json")
@@ -280,7 +299,7 @@ def main():
 
     # end to end through the public API with host buffers (pinned), H2D + forward + D2H per step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and mode == "replicas":
         Qh, Kh, Vh = (x.pin_memory() for x in (Q, K, V))
         for _ in range(max(1, args.warmup)):
             wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev)
@@ -301,7 +320,7 @@ def main():
                "timing": "host wall clock around forward_host (H2D, wildcat_forward, D2H, sync)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.n <= 262144:
         v, secs, info = cpu_oracle_sample(cfg, Q, K, V)
         cpu = {"value": v, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                "sample": info["sample"], "cpu": cpu_model(), "seconds_extrapolated": secs,
@@ -317,16 +336,18 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "weak" if mode == "replicas" else "strong",
             "vs_baseline": None,
             "dtype": "f64-select/f32-gemm",
             "data": "synthetic",
             "config": {"workload": cfg.name, "units_per_gpu": units, "n": cfg.n, "m": cfg.m, "d": cfg.d,
                        "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
-                       "parallelism": f"replicas{world}", "l2": f"flushed ({args.flush_mb} MB write) before each step"},
-            "stages_ms": dict(zip(st_names, st_mean)),
+                       "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}"),
+                       "l2": f"flushed ({args.flush_mb} MB write) before each step"},
+            "stages_ms": dict(zip(st_names, st_mean)) if st_mean else None,
             "roofline": {"kernel": "rpc_select_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                         "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -334,6 +355,8 @@ def main():
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if mode == "nshard":
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

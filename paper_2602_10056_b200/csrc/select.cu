@@ -384,9 +384,11 @@ template <typename T, int D> struct KRow {
         for (int q = 0; q < kVec; ++q) v[q] = make_uint4(0, 0, 0, 0);
     }
     // part[e % 4] += k_j * kc_j over the row (fp64, exact widening of k)
-    __device__ __forceinline__ void dot(const double *kc, double part[4]) const {
+    __device__ __forceinline__ void dot(const double *kc, double part[4]) const { dot_range<0, kVec>(kc, part); }
+    // vectors [Q0, Q1) only (compile-time range: the row stays in registers)
+    template <int Q0, int Q1> __device__ __forceinline__ void dot_range(const double *kc, double part[4]) const {
 #pragma unroll
-        for (int q = 0; q < kVec; ++q) {
+        for (int q = Q0; q < Q1; ++q) {
             const uint32_t wd[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
             if constexpr (sizeof(T) == 2) {
 #pragma unroll

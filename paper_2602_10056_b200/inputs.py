@@ -48,7 +48,43 @@ CONFIGS = {
     "diffusion": Config("diffusion", 8, 16, 16, 4096, 4096, 64, 128, "bf16", "C"),
     "llm32k": Config("llm32k", 1, 32, 8, 32768, 32768, 128, 256, "bf16", "L"),
     "headline": Config("headline", 1, 1, 1, 65536, 65536, 128, 256, "bf16", "G"),
+    # long-sequence sweep (configs[4]): one head, keys sharded along n over the GPUs
+    "long256k": Config("long256k", 1, 1, 1, 262144, 262144, 128, 256, "bf16", "G"),
+    "long1m": Config("long1m", 1, 1, 1, 1048576, 1048576, 128, 256, "bf16", "G"),
+    "long4m": Config("long4m", 1, 1, 1, 4194304, 4194304, 128, 256, "bf16", "G"),
 }
+
+BLOCK_ROWS = 65536
+
+
+def make_rows(n_rows_total: int, row0: int, count: int, d: int, dtype="bf16", seed=0, stream=0):
+    """Rows [row0, row0 + count) of a long N(0,1) matrix generated in fixed 64K-row blocks, each from
+    its own PCG64 stream: any shard of the sequence is reproducible without generating the rest."""
+    out = np.empty((count, d))
+    b0, b1 = row0 // BLOCK_ROWS, (row0 + count - 1) // BLOCK_ROWS
+    for b in range(b0, b1 + 1):
+        rng = np.random.Generator(np.random.PCG64([seed, stream, b]))
+        blk = rng.standard_normal((min(BLOCK_ROWS, n_rows_total - b * BLOCK_ROWS), d))
+        lo = max(row0, b * BLOCK_ROWS)
+        hi = min(row0 + count, b * BLOCK_ROWS + blk.shape[0])
+        out[lo - row0:hi - row0] = blk[lo - b * BLOCK_ROWS:hi - b * BLOCK_ROWS]
+    return torch.from_numpy(out).to(DTYPES[dtype]).reshape(1, 1, count, d).contiguous()
+
+
+def make_long_shard(cfg: Config, world: int, rank: int, seed=None):
+    """(Q_shard, K_shard, V_shard, k_offset) of family-G inputs for the n-sharded path: keys/values
+    [off, off + n_local) and an even query shard; identical global data for any world size."""
+    seed = cfg.seed if seed is None else seed
+    base, extra = divmod(cfg.n, world)
+    off = rank * base + min(rank, extra)
+    nl = base + (1 if rank < extra else 0)
+    qb, qe = divmod(cfg.m, world)
+    qoff = rank * qb + min(rank, qe)
+    ml = qb + (1 if rank < qe else 0)
+    Q = make_rows(cfg.m, qoff, ml, cfg.d, cfg.dtype, seed, 0)
+    K = make_rows(cfg.n, off, nl, cfg.d, cfg.dtype, seed, 1)
+    V = make_rows(cfg.n, off, nl, cfg.d, cfg.dtype, seed, 2)
+    return Q, K, V, off
 
 
 def _draw(rng: np.random.Generator, family: str, shape_q, shape_kv, d: int, distinct: int | None):
