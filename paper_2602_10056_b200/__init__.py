@@ -183,14 +183,14 @@ class NshardComm:
 
 
 def forward_nshard(comm: NshardComm, Q, K, V, r, n_global, n_offset, seed=0, beta=None, rq=None, clip=True,
-                   S=None, r_eff=None, stream=None):
+                   S=None, r_eff=None, out=None, stream=None):
     """Alg 4 for one (batch, kv-head) unit whose keys are sharded over the communicator's ranks.
     K, V: this rank's [1, 1, n_local, d] shard at global offset n_offset; Q: [1, hq, m_local, d]."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     shape = B.make_shape(Q, K, r)
     opts = B.make_opts(seed, beta, rq, clip)
-    O = torch.empty_like(Q)
+    O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device)
     B.wildcat_forward_nshard(comm.handle, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O
