@@ -249,31 +249,38 @@ __global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int ran
     for (int j = tid; j < i; j += kNsT) packet[2 + D + j] = F[(int64_t)j * n + s];
 }
 
-// Kernel column, rank update and downdate of this rank's keys (one CTA per 2048-key chunk).
+// Kernel column, rank update and downdate of this rank's keys (one CTA of 512 threads per 2048-key
+// chunk, processed as 8 super-tiles of 256 keys).  Phase A: the 16 warps split the rows j of
+// F[0:i, tile] (each lane keeps 8 + 8 independent coalesced loads in flight); phase B: the fp64
+// kernel dot, two threads per key; phase C: fixed-order combine, F[i, :], residual, chunk sum.
+constexpr int kNuT = 512, kNuW = kNuT / 32, kNuST = 256, kNuTK = kNuST / 32;
+
 template <typename T, int D>
-__global__ void __launch_bounds__(kNsT) ns_update(int i, int r, int64_t n, int64_t n_off, const T *K,
+__global__ void __launch_bounds__(kNuT) ns_update(int i, int r, int64_t n, int64_t n_off, const T *K,
                                                   const double *stats, const double *packet, double *F, double *p,
                                                   double *ctot, int32_t *S, double *L, T *KS, const Ctl *ctl) {
     extern __shared__ double nsm[];
-    double *kcs = nsm;      // [D]
-    double *fs = kcs + D;   // [r]
-    double *kb = fs + r;    // [D]
-    double *scr = kb + D;   // [40]
+    double *kcs = nsm;               // [D]
+    double *fs = kcs + D;            // [r]
+    double *kb = fs + r;             // [D]
+    double *red = kb + D;            // [kNuW][kNuST]
+    double *kd = red + kNuW * kNuST;  // [2][kNuST]
+    double *scr = kd + 2 * kNuST;    // [40]
     if (ctl->done) return;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
     const double g = stats[1], mstar = stats[2];
     const int64_t s_glob = (int64_t)packet[0];
     const double ps = packet[1];
-    for (int j = tid; j < D; j += kNsT) {
+    for (int j = tid; j < D; j += kNuT) {
         kb[j] = stats[8 + j];
         kcs[j] = __dadd_rn(packet[2 + j], -stats[8 + j]);
     }
-    for (int j = tid; j < i; j += kNsT) fs[j] = packet[2 + D + j];
+    for (int j = tid; j < i; j += kNuT) fs[j] = packet[2 + D + j];
     __syncthreads();
     const double rs = sqrt(ps);
     if (blockIdx.x == 0) {  // replicated outputs: S, L row i (L[i][i] = sqrt(p_s) = F[i, s] exactly), K_S row i
-        for (int j = tid; j < i; j += kNsT) L[(int64_t)i * r + j] = fs[j];
-        for (int j = tid; j < D; j += kNsT) KS[(int64_t)i * D + j] = from_f32<T>((float)packet[2 + j]);
+        for (int j = tid; j < i; j += kNuT) L[(int64_t)i * r + j] = fs[j];
+        for (int j = tid; j < D; j += kNuT) KS[(int64_t)i * D + j] = from_f32<T>((float)packet[2 + j]);
         if (tid == 0) {
             S[i] = (int32_t)s_glob;
             L[(int64_t)i * r + i] = rs;
@@ -281,20 +288,73 @@ __global__ void __launch_bounds__(kNsT) ns_update(int i, int r, int64_t n, int64
     }
     const int64_t c0 = (int64_t)blockIdx.x * kNsChunk, c1 = std::min<int64_t>(n, c0 + kNsChunk);
     double loc = 0.0;
-    for (int64_t l = c0 + tid; l < c1; l += kNsT) {
-        double dot = 0.0;
-        for (int j = 0; j < D; ++j)
-            dot = __dadd_rn(dot, __dmul_rn(__dadd_rn(to_f64(K[l * D + j]), -kb[j]), kcs[j]));
-        const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
-        double acc = 0.0;
-        for (int j = 0; j < i; ++j) acc = __dadd_rn(acc, __dmul_rn(F[(int64_t)j * n + l], fs[j]));
-        const double f = (hval - acc) / rs;
-        F[(int64_t)i * n + l] = f;
-        double q = __dadd_rn(p[l], -__dmul_rn(f, f));
-        q = q > 0.0 ? q : 0.0;
-        if (n_off + l == s_glob) q = 0.0;
-        p[l] = q;
-        loc += q;
+    for (int64_t k0 = c0; k0 < c1; k0 += kNuST) {
+        {  // phase A
+            double acc[kNuTK];
+#pragma unroll
+            for (int t = 0; t < kNuTK; ++t) acc[t] = 0.0;
+            int j = w;
+            for (; j + kNuW < i; j += 2 * kNuW) {
+                const double *F0 = F + (int64_t)j * n + k0 + lane;
+                const double *F1 = F0 + (int64_t)kNuW * n;
+                double x0[kNuTK], x1[kNuTK];
+#pragma unroll
+                for (int t = 0; t < kNuTK; ++t) {
+                    const bool ok = k0 + 32 * t + lane < c1;
+                    x0[t] = ok ? __ldcg(F0 + 32 * t) : 0.0;
+                    x1[t] = ok ? __ldcg(F1 + 32 * t) : 0.0;
+                }
+                const double f0 = fs[j], f1 = fs[j + kNuW];
+#pragma unroll
+                for (int t = 0; t < kNuTK; ++t) acc[t] = fma(x1[t], f1, fma(x0[t], f0, acc[t]));
+            }
+            if (j < i) {
+                const double *F0 = F + (int64_t)j * n + k0 + lane;
+                const double f0 = fs[j];
+#pragma unroll
+                for (int t = 0; t < kNuTK; ++t) {
+                    const bool ok = k0 + 32 * t + lane < c1;
+                    acc[t] = fma(ok ? __ldcg(F0 + 32 * t) : 0.0, f0, acc[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kNuTK; ++t) red[w * kNuST + 32 * t + lane] = acc[t];
+        }
+        {  // phase B: two threads per key, D/2 elements each
+            const int kk = tid % kNuST, half = tid / kNuST;
+            const int64_t l = k0 + kk;
+            double dot = 0.0;
+            if (l < c1) {
+                constexpr int Dh = D / 2;
+                for (int jj = 0; jj < Dh; jj += 8) {
+                    double kv[8];
+                    Vec8<T>::load(K + l * D + half * Dh + jj, kv);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        dot = fma(__dadd_rn(kv[q], -kb[half * Dh + jj + q]), kcs[half * Dh + jj + q], dot);
+                }
+            }
+            kd[half * kNuST + kk] = dot;
+        }
+        __syncthreads();
+        if (tid < kNuST) {  // phase C
+            const int64_t l = k0 + tid;
+            if (l < c1) {
+                double acc = 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kNuW; ++ww) acc += red[ww * kNuST + tid];
+                const double dot = kd[tid] + kd[kNuST + tid];
+                const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
+                const double f = (hval - acc) / rs;
+                F[(int64_t)i * n + l] = f;
+                double q = __dadd_rn(p[l], -__dmul_rn(f, f));
+                q = q > 0.0 ? q : 0.0;
+                if (n_off + l == s_glob) q = 0.0;
+                p[l] = q;
+                loc += q;
+            }
+        }
+        __syncthreads();
     }
     loc = block_sum(loc, scr);
     if (tid == 0) ctot[blockIdx.x] = loc;
@@ -397,7 +457,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     ns_init<<<nch, kNsT, 0, st>>>(n, w.nrm2, w.stats, w.p, w.ctot);
     launches += 8;
     // ---- A1 + A2: r rounds
-    const size_t usm = (size_t)(2 * D + r + 40) * sizeof(double);
+    const size_t usm = (size_t)(2 * D + r + kNuW * kNuST + 2 * kNuST + 40) * sizeof(double);
     auto upd = ns_update<T, D>;
     if (usm > 48 * 1024) cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
     for (int i = 0; i < r; ++i) {
@@ -406,7 +466,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
         ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, w.ranktot, w.ctot, w.p,
                                            static_cast<const T *>(K), w.F, w.packet, w.ctl);
         WC_NCCL(api.allReduce(w.packet, w.packet, 2 + D + r, ncclFloat64, ncclSum, cm->comm, st));
-        upd<<<nch, kNsT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,
+        upd<<<nch, kNuT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,
                                     w.S, w.L, static_cast<T *>(w.KS), w.ctl);
         launches += 3;
     }
