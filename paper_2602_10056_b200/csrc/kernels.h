@@ -57,7 +57,8 @@ inline int f_tile_nst(int64_t n, int cpu) {
 int select_ctas_per_unit(const struct Dims &D);
 inline size_t f_elems_per_unit(int64_t n, int r, int cpu) {
     const size_t rowmajor = (size_t)r * f_ld(n);
-    const size_t tiles = (size_t)cpu * f_tile_nst(n, cpu) * r * 256;
+    const int64_t chunk = ((n + cpu - 1) / cpu + 31) / 32 * 32;
+    const size_t tiles = (size_t)cpu * chunk * r;  // TMA kernel: [cpu][r x chunk]
     return rowmajor > tiles ? rowmajor : tiles;
 }
 

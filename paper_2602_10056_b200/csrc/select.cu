@@ -430,9 +430,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
     const double *st = a.stats + (int64_t)u * (8 + D);
-    // tile-major F: block (c', k') = [r][kST] doubles for super-tile k' of CTA c'
-    double *Fu = a.F + (int64_t)u * a.cpu * a.nstm * a.r * kST;
-    double *Fc = Fu + (int64_t)c * a.nstm * a.r * kST;  // this CTA's blocks
+    // tile-major F: CTA c' owns [r x chunk]; its super-tile k' is the block [r][w_k'] at column
+    // offset 256 k', w_k' = min(256, chunk - 256 k') (a multiple of 32): 8 rows = one contiguous copy
+    double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
+    double *Fc = Fu + (int64_t)c * chunk * a.r;  // this CTA's blocks
+    auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(kST, chunk - (int64_t)k * kST); };
 
     if (tid == 0) {
         for (int q = 0; q < NS; ++q) {
@@ -459,16 +461,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
                 }
                 for (int k = 0; k < nst; ++k) {
                     const double *blk = Fc + (int64_t)k * a.r * kST;
+                    const int wk = tile_w(k);
                     for (int j0 = 0; j0 < rows; j0 += kRPS) {
                         const int nr = min(kRPS, rows - j0);
-                        const uint32_t bytes = (uint32_t)(nr * kST * sizeof(double));
+                        const uint32_t bytes = (uint32_t)(nr * wk * sizeof(double));
                         while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
                             if (sh_stop) goto drain;
                         }
                         if (sh_stop) goto drain;
                         mbar_arrive_expect_tx(&full[stage], bytes);
                         // one contiguous bulk copy of nr rows x 256 keys (tile-major layout)
-                        bulk_g2s_hint(ring + (size_t)stage * kRPS * kST, blk + (int64_t)j0 * kST, bytes, &full[stage],
+                        bulk_g2s_hint(ring + (size_t)stage * kRPS * kST, blk + (int64_t)j0 * wk, bytes, &full[stage],
                                       j0 < a.rkeep ? keep : stream);
                         issued |= 1u << stage;
                         par = (par & ~(1u << stage)) | (ph << stage);
@@ -649,8 +652,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         }
         {
             const int64_t cs_ = s / chunk, off = s - cs_ * chunk;
-            const double *fsrc = Fu + ((cs_ * a.nstm + off / kST) * a.r) * kST + (off % kST);
-            for (int j = tid; j < i; j += kCT) fs[j] = __ldcg(fsrc + (int64_t)j * kST);
+            const int kk_ = (int)(off / kST);
+            const int64_t wk_ = std::min<int64_t>(kST, chunk - (int64_t)kk_ * kST);
+            const double *fsrc = Fu + cs_ * chunk * a.r + (int64_t)kk_ * kST * a.r + (off % kST);
+            for (int j = tid; j < i; j += kCT) fs[j] = __ldcg(fsrc + (int64_t)j * wk_);
         }
         cw_sync();
         WC_TR(3);
@@ -670,9 +675,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         for (int k = 0; k < nst; ++k) {
             const int64_t l = lo + (int64_t)k * kST + tid;
             const bool own = l < hi;
-            double *Fk = Fc + (int64_t)k * a.r * kST + tid;  // this key's column in its block
+            const int wk = tile_w(k);
+            double *Fk = Fc + (int64_t)k * a.r * kST + tid;  // this key's column in its block (row stride wk)
             const double pcur = pcur_next;
-            const double fprev = k < 2 ? fkeep[k & 1] : ((own && i > 0) ? __ldcg(Fk + (int64_t)(i - 1) * kST) : 0.0);
+            const double fprev = k < 2 ? fkeep[k & 1] : ((own && i > 0) ? __ldcg(Fk + (int64_t)(i - 1) * wk) : 0.0);
             if (k < 2) WC_TR(4 + 3 * k);
             // phase B: kernel dot <k_l, k_s - kbar> from the prefetched K row (dot = . - c0);
             // phase A: F rows 0..i-2 from the ring, warp w takes row j0 + w of every stage
@@ -685,10 +691,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
                 const int nr = min(kRPS, rows - j0);
                 mbar_wait(&full[rstage], rph);
                 if (w < nr) {
-                    const double *src = ring + ((size_t)rstage * kRPS + w) * kST + lane;
+                    const double *src = ring + (size_t)rstage * kRPS * kST + (size_t)w * wk + lane;
                     const double fj = fs[j0 + w];
 #pragma unroll
-                    for (int t = 0; t < kTK; ++t) acc[t] = fma(src[32 * t], fj, acc[t]);
+                    for (int t = 0; t < kTK; ++t)
+                        if (32 * t < wk) acc[t] = fma(src[32 * t], fj, acc[t]);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[rstage]);
@@ -720,7 +727,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
                 accv = fma(fprev, flast, accv);
                 const double hval = exp(__dadd_rn(__dmul_rn(g, dot), -mstar));
                 const double f = (hval - accv) / rs;
-                st_f64_hint(Fk + (int64_t)i * kST, f, fpol);
+                st_f64_hint(Fk + (int64_t)i * wk, f, fpol);
                 fence_proxy_async_global();
                 double q = __dadd_rn(pcur, -__dmul_rn(f, f));
                 q = q > 0.0 ? q : 0.0;
@@ -796,7 +803,7 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         const char *env = std::getenv("WC_L2_KEEP_FRAC");
-        const double frac = env ? std::atof(env) : 0.75;
+        const double frac = env ? std::atof(env) : 0.0;  // measured best: F streamed evict-first
         const double row_bytes = (double)a.units * (double)a.ldF * sizeof(double);
         a.rkeep = (int)std::min<double>(Dm.r, std::max(0.0, frac * l2 / row_bytes));
     }
