@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      int64_t tiles_per_head, int64_t total_tiles) {
     using L = TcSmem<D, RP>;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base derived from the __shared__ array itself, so stores stay STS (not generic)
+    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char *sQ = sm + L::kOffQ, *sK = sm + L::kOffK, *sXh = sm + L::kOffXh, *sXl = sm + L::kOffXl;
     unsigned char *sP = sm + L::kOffP;
     float *sW = reinterpret_cast<float *>(sm + L::kBytes);
@@ -178,7 +179,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int cur_unit = -1, re = 0;
     const float bl2 = beta * 1.4426950408889634f;
 
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    // contiguous tile ranges per CTA: consecutive tiles share the unit, so K_S / X are staged rarely
+    const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
+    const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
+    for (int64_t tile = t_begin; tile < t_end; ++tile) {
         const int64_t head = tile / tiles_per_head;  // b * hq + h
         const int64_t q0 = (tile % tiles_per_head) * 128;
         const int b = (int)(head / hq), h = (int)(head % hq);

@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(kWTc, 1)
     constexpr int DC = D + 1;
     constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base derived from the __shared__ array itself, so stores stay STS (not generic)
+    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char *sA = sm, *sB = sm + kA, *sP = sB + kB, *sV = sP + kP;
     float *sG = reinterpret_cast<float *>(sV + kV);  // gamma_l of the slice [128]
     float *sKb = sG + 128;                             // kbar (fp32) [D]
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kWTc, 1)
     bool first = true;
     for (int64_t l0 = lo; l0 < hi; l0 += 128) {
         // keys of the slice -> B operand of GEMM1 (K-major) and V^T -> B operand of GEMM2
+        // keys of the slice -> B operand (K-major, swizzled)
         for (int e = tid; e < 128 * CPR; e += kWTc) {
             const int row = e / CPR, cc = e % CPR;
             uint4 v = make_uint4(0, 0, 0, 0);
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(kWTc, 1)
             for (int q = 0; q < 8; ++q)
                 *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(cc * 8 + q, row, D)) = pv[q];
         }
-        {  // gamma_l = -g <k_l, kbar> for the key this thread stages
+        __syncthreads();
+        {  // gamma_l = -g <k_l, kbar> for the key this thread stages (row re-read through L1/L2)
             const int64_t l = l0 + tid;
             float gm = 0.f;
             if (l < hi) {
