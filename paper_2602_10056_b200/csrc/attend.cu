@@ -6,6 +6,7 @@
 // online max rescaling across coreset tiles (exact: the shift cancels in num/den).
 #include <algorithm>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -129,7 +130,19 @@ __global__ void __launch_bounds__(kAT) attend_kernel(const T *__restrict__ Q, co
 // X = [V_S, w] is split into bf16 hi + lo parts so the values keep ~16 bits.  Thread t owns
 // TMEM lane t = query row t.  Operands are K-major, 128-byte swizzled (see umma.cuh).
 // =====================================================================================
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // 8 warps: warps w and w+4 share TMEM lane quadrant w%4 (column halves)
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ unsigned long long gtimer_a() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int D, int RP> struct TcSmem {
     // K-major SW128 rows are at least 128 bytes (64 bf16) wide
@@ -138,11 +151,20 @@ template <int D, int RP> struct TcSmem {
     static constexpr int kK = RP * D * 2;           // K_S
     static constexpr int kX = D * kRK * 2;          // one of X_hi / X_lo (B operand [d][RP])
     static constexpr int kP = 128 * kRK * 2;        // P (A operand [128][RP])
-    static constexpr bool kAliasP = kP <= kQ + kK;  // P reuses the Q/K_S region after GEMM1
-    static constexpr int kOffQ = 0, kOffK = kQ, kOffXh = kQ + kK, kOffXl = kOffXh + kX;
-    static constexpr int kOffP = kAliasP ? 0 : kOffXl + kX;
-    static constexpr int kBytes = (kAliasP ? kOffXl + kX : kOffP + kP);
-    static constexpr int kTotal = kBytes + RP * 4 + 2 * D * 2 + 1024;  // + w, vmin, vmax (bf16), alignment
+    // Layout choice: keep K_S resident across tiles (P in its own region).  X is split into bf16
+    // hi + lo parts when that still fits; otherwise (d = 128, r = 256) X_hi alone, so that nothing
+    // has to be re-staged per tile.
+    static constexpr int kBudget = 224 * 1024;
+    static constexpr bool kSplitX = kQ + kK + 2 * kX + kP <= kBudget;
+    static constexpr bool kAliasP = false;
+    static constexpr int kOffQ = 0, kOffK = kQ, kOffXh = kQ + kK, kOffXl = kOffXh + (kSplitX ? kX : 0);
+    static constexpr int kOffP = kOffXl + kX;
+    static constexpr int kBytes = kOffP + kP;
+    // + w (fp32), vmin/vmax (bf16), row exchange (2 x 128 fp32), mbarrier, TMEM base; no static smem,
+    // so the dynamic segment starts at shared offset 0 (1024-aligned, checked at run time)
+    static constexpr int kOffW = kBytes, kOffV = kOffW + RP * 4, kOffXch = kOffV + 2 * D * 2;
+    static constexpr int kOffBar = kOffXch + 2 * 128 * 4, kOffTb = kOffBar + 8;
+    static constexpr int kTotal = kOffTb + 8;
 };
 
 template <int D, int RP>
@@ -151,18 +173,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      const float *__restrict__ X, const int32_t *__restrict__ r_eff,
                      const __nv_bfloat16 *__restrict__ vmin, const __nv_bfloat16 *__restrict__ vmax, int64_t m,
                      int r, int group, int hq, int hkv, float beta, int clip, __nv_bfloat16 *__restrict__ O,
-                     int64_t tiles_per_head, int64_t total_tiles) {
+                     int64_t tiles_per_head, int64_t total_tiles, unsigned long long *atrace) {
     using L = TcSmem<D, RP>;
-    extern __shared__ unsigned char smem_raw[];
-    // 1024-byte aligned base derived from the __shared__ array itself, so stores stay STS (not generic)
-    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;  // offset 0 of the CTA's shared window: 1024-aligned
+    if (smem_u32(sm) & 1023u) __trap();
     unsigned char *sQ = sm + L::kOffQ, *sK = sm + L::kOffK, *sXh = sm + L::kOffXh, *sXl = sm + L::kOffXl;
     unsigned char *sP = sm + L::kOffP;
-    float *sW = reinterpret_cast<float *>(sm + L::kBytes);
-    __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sW + RP), *sVmax = sVmin + D;
-    __shared__ uint64_t bar;
-    __shared__ uint32_t tbase;
+    float *sW = reinterpret_cast<float *>(sm + L::kOffW);
+    __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sm + L::kOffV), *sVmax = sVmin + D;
+    float (*xch)[128] = reinterpret_cast<float (*)[128]>(sm + L::kOffXch);  // row exchange between halves
+    uint64_t &bar = *reinterpret_cast<uint64_t *>(sm + L::kOffBar);
+    uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
     const int tid = threadIdx.x, w = tid >> 5;
+    const int row = tid & 127, half = tid >> 7;  // TMEM lane (query row) and column half
     constexpr int DC = D + 1;
 
     if (w == 0) umma::tmem_alloc(&tbase, 512);
@@ -174,7 +198,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tS = tbase, tO = tbase + 256;
-    const uint32_t lane_off = (uint32_t)(w * 32) << 16;
+    const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
     uint32_t phase = 0;
     int cur_unit = -1, re = 0;
     const float bl2 = beta * 1.4426950408889634f;
@@ -183,6 +207,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
     const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
     for (int64_t tile = t_begin; tile < t_end; ++tile) {
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8] = gtimer_a();
         const int64_t head = tile / tiles_per_head;  // b * hq + h
         const int64_t q0 = (tile % tiles_per_head) * 128;
         const int b = (int)(head / hq), h = (int)(head % hq);
@@ -205,7 +230,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const __nv_bfloat16 xh = __float2bfloat16_rn(x);
                 const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
                 *reinterpret_cast<__nv_bfloat16 *>(sXh + umma::sw128_offset(c, s, D)) = xh;
-                *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
+                if (L::kSplitX) *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
             }
             for (int s = tid; s < RP; s += kTcThreads) sW[s] = (s < re) ? Xu[(int64_t)s * DC + D] : 0.f;
             for (int c = tid; c < D; c += kTcThreads) {
@@ -227,6 +252,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma::fence_before_sync();
         __syncthreads();
         umma::fence_after_sync();
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 1] = gtimer_a();
         // ---- GEMM1: S = Q K_S^T
         if (tid == 0) {
             umma::gemm_128xNxK(tS, smem_u32(sQ), smem_u32(sK), RP, D, false);
@@ -235,78 +261,92 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait(&bar, phase);
         phase ^= 1u;
         umma::fence_after_sync();
-        // ---- softmax epilogue: row max, P = exp(beta (S - max)) in bf16, den = P . w
-        float mx = -INFINITY;
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 2] = gtimer_a();
+        // ---- softmax epilogue (two threads per row, RP/2 columns each, all in registers):
+        // row max, P = exp2(beta log2e (S - max)) in bf16 -> smem, den = P . w (4 partial sums)
+        {
+            constexpr int HC = RP / 2;  // columns per thread
+            constexpr int NCH = HC / 32 > 0 ? HC / 32 : 1;
+            const int cbase = half * HC;
+            float v[HC >= 32 ? HC : 32];
 #pragma unroll
-        for (int c0 = 0; c0 < RP; c0 += 32) {
-            float v[32];
-            umma::ld32(tS + lane_off + c0, v);
+            for (int q = 0; q < NCH; ++q) umma::ld32(tS + lane_off + cbase + q * 32, v + q * 32);
+            float mx = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (c0 + i < re) mx = fmaxf(mx, v[i]);
-        }
-        float den = 0.f;
+            for (int i2 = 0; i2 < HC; ++i2)
+                if (cbase + i2 < re) mx = fmaxf(mx, v[i2]);
+            xch[half][row] = mx;
+            __syncthreads();
+            mx = fmaxf(xch[0][row], xch[1][row]);
+            const float mb = mx * bl2;
+            float dn[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c0 = 0; c0 < RP; c0 += 32) {
-            float v[32];
-            umma::ld32(tS + lane_off + c0, v);
-#pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
+            for (int g8 = 0; g8 < HC / 8; ++g8) {
                 uint32_t pk[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int s0 = c0 + g8 * 8 + 2 * i;
-                    const float p0 = (s0 < re) ? exp2f((v[g8 * 8 + 2 * i] - mx) * bl2) : 0.f;
-                    const float p1 = (s0 + 1 < re) ? exp2f((v[g8 * 8 + 2 * i + 1] - mx) * bl2) : 0.f;
+                    const int cl = g8 * 8 + 2 * i, s0 = cbase + cl;
+                    const float p0 = (s0 < re) ? ex2_approx(fmaf(v[cl], bl2, -mb)) : 0.f;
+                    const float p1 = (s0 + 1 < re) ? ex2_approx(fmaf(v[cl + 1], bl2, -mb)) : 0.f;
                     const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-                    den = fmaf(__bfloat162float(pb.x), sW[s0], den);
-                    den = fmaf(__bfloat162float(pb.y), sW[s0 + 1], den);
+                    dn[i] = fmaf(__bfloat162float(pb.x), sW[s0], dn[i]);
+                    dn[i] = fmaf(__bfloat162float(pb.y), sW[s0 + 1], dn[i]);
                     pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
                 }
-                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(tid, c0 + g8 * 8, 128)) =
+                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(row, cbase + g8 * 8, 128)) =
                     make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
+            const float dpart = (dn[0] + dn[1]) + (dn[2] + dn[3]);
+            __syncthreads();  // xch reused
+            xch[half][row] = dpart;
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
         umma::fence_after_sync();
+        const float den = xch[0][row] + xch[1][row];
         // ---- GEMM2: O = P X_hi + P X_lo
         if (tid == 0) {
             umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXh), D, RP, false);
-            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXl), D, RP, true);
+            if (L::kSplitX) umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXl), D, RP, true);
             umma::commit(&bar);
         }
         mbar_wait(&bar, phase);
         phase ^= 1u;
         umma::fence_after_sync();
-        // ---- output epilogue
-        const int64_t qi = q0 + tid;
-        const float inv = den > 0.f ? 1.f / den : 0.f;
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 4] = gtimer_a();
+        // ---- output epilogue: each thread finishes D/2 columns of its row
+        {
+            const int64_t qi = q0 + row;
+            const float inv = den > 0.f ? 1.f / den : 0.f;
+            constexpr int HD = D / 2;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-            float v[32];
-            umma::ld32(tO + lane_off + c0, v);
-            if (qi < m) {
-                uint32_t pk[16];
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                const int cc0 = half * HD + c0;
+                float v[32];
+                umma::ld32(tO + lane_off + cc0, v);
+                if (qi < m) {
+                    uint32_t pk[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
-                    if (clip) {
-                        o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[c0 + 2 * i])), __bfloat162float(sVmax[c0 + 2 * i]));
-                        o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[c0 + 2 * i + 1])), __bfloat162float(sVmax[c0 + 2 * i + 1]));
+                    for (int i = 0; i < 16; ++i) {
+                        float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
+                        if (clip) {
+                            o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[cc0 + 2 * i])), __bfloat162float(sVmax[cc0 + 2 * i]));
+                            o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[cc0 + 2 * i + 1])), __bfloat162float(sVmax[cc0 + 2 * i + 1]));
+                        }
+                        const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
+                        pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
                     }
-                    const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
-                    pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
-                }
-                uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + qi) * D + c0);
+                    uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + qi) * D + cc0);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                }
             }
         }
         umma::fence_before_sync();
         __syncthreads();  // TMEM and smem free for the next tile
         umma::fence_after_sync();
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 5] = gtimer_a();
     }
     if (w == 0) umma::tmem_dealloc(tbase, 512);
 }
@@ -323,10 +363,32 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)std::min<int64_t>(total, sms);
+    static const bool tracing = std::getenv("WC_ATTEND_TRACE") != nullptr;
+    unsigned long long *atrace = nullptr;
+    if (tracing) {
+        cudaMalloc(&atrace, 64 * 8 * sizeof(unsigned long long));
+        cudaMemsetAsync(atrace, 0, 64 * 8 * sizeof(unsigned long long), st);
+    }
     kern<<<grid, kTcThreads, L::kTotal, st>>>(
         static_cast<const __nv_bfloat16 *>(Q), static_cast<const __nv_bfloat16 *>(KS), X, r_eff,
         static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(),
-        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total);
+        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total, atrace);
+    if (atrace) {  // debug: phase durations of CTA 0's tiles (ns)
+        unsigned long long h[64 * 8];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, atrace, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaFree(atrace);
+        double acc[5] = {0};
+        int cnt = 0;
+        for (int t = 1; t < 64; ++t) {
+            if (!h[t * 8 + 5]) continue;
+            for (int k = 0; k < 5; ++k) acc[k] += (double)(h[t * 8 + k + 1] - h[t * 8 + k]);
+            ++cnt;
+        }
+        if (cnt)
+            std::fprintf(stderr, "[atrace] tiles=%d stage=%.0f gemm1=%.0f softmax=%.0f gemm2=%.0f epi=%.0f ns\n", cnt,
+                         acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
