@@ -262,7 +262,21 @@ __global__ void gather_ks_kernel(const T *__restrict__ K, const int32_t *__restr
 //   GEMM2  O[128 x d] += P . V_slice       (accumulated in TMEM across the CTA's slices)
 // and the partial Y~[a][0:d] = O, Y~[a][d] = rowsum go to Ypart (summed in fp64 by the solve).
 // =====================================================================================
-constexpr int kWTc = 128;
+constexpr int kWTc = 256;  // 8 warps: warps w and w+4 share TMEM lane quadrant w%4 (column halves)
+
+__device__ __forceinline__ float ex2_approx_w(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int D> struct WtSmem {
+    static constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
+    static constexpr int kOffA = 0, kOffB = kA, kOffP = kOffB + kB, kOffV = kOffP + kP;
+    static constexpr int kOffG = kOffV + kV, kOffKb = kOffG + 128 * 4, kOffX = kOffKb + D * 4;
+    static constexpr int kOffBar = kOffX + 2 * 128 * 4, kOffTb = kOffBar + 8;
+    static constexpr int kTotal = kOffTb + 8;
+};
 
 template <int D>
 __global__ void __launch_bounds__(kWTc, 1)
@@ -270,17 +284,18 @@ __global__ void __launch_bounds__(kWTc, 1)
                       const int32_t *__restrict__ S, const __nv_bfloat16 *__restrict__ KSin,
                       const int32_t *__restrict__ r_eff,
                       const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
+    using L = WtSmem<D>;
     constexpr int DC = D + 1;
-    constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
-    extern __shared__ unsigned char smem_raw[];
-    // 1024-byte aligned base derived from the __shared__ array itself, so stores stay STS (not generic)
-    unsigned char *sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    unsigned char *sA = sm, *sB = sm + kA, *sP = sB + kB, *sV = sP + kP;
-    float *sG = reinterpret_cast<float *>(sV + kV);  // gamma_l of the slice [128]
-    float *sKb = sG + 128;                             // kbar (fp32) [D]
-    __shared__ uint64_t bar;
-    __shared__ uint32_t tbase;
-    const int tid = threadIdx.x, w = tid >> 5;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;  // offset 0 of the CTA's shared window (no static smem): 1024-aligned
+    if (smem_u32(sm) & 1023u) __trap();
+    unsigned char *sA = sm + L::kOffA, *sB = sm + L::kOffB, *sP = sm + L::kOffP, *sV = sm + L::kOffV;
+    float *sG = reinterpret_cast<float *>(sm + L::kOffG);    // log2e * gamma_l of the slice [128]
+    float *sKb = reinterpret_cast<float *>(sm + L::kOffKb);  // kbar (fp32) [D]
+    float *xch = reinterpret_cast<float *>(sm + L::kOffX);   // [2][128] row-sum exchange
+    uint64_t &bar = *reinterpret_cast<uint64_t *>(sm + L::kOffBar);
+    uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
+    const int tid = threadIdx.x, w = tid >> 5, row = tid & 127, half = tid >> 7;
     const int split = blockIdx.x, a0 = blockIdx.y * 128, u = blockIdx.z;
     const int re = r_eff[u];
     if (a0 >= re) return;  // uniform per CTA
@@ -289,6 +304,7 @@ __global__ void __launch_bounds__(kWTc, 1)
     const double *st = stats + (int64_t)u * (8 + D);
     const double g = st[1], mstar = st[2];
     constexpr int CPR = D / 8;
+    constexpr float kLog2e = 1.4426950408889634f;
 
     if (w == 0) umma::tmem_alloc(&tbase, 256);
     if (tid == 0) {
@@ -296,57 +312,56 @@ __global__ void __launch_bounds__(kWTc, 1)
         fence_mbar_init();
     }
     for (int j = tid; j < D; j += kWTc) sKb[j] = (float)st[8 + j];
-    // coreset rows (raw keys) -> A operand; alpha_a in fp64
+    // coreset rows (raw keys) -> A operand
     for (int e = tid; e < 128 * CPR; e += kWTc) {
-        const int row = e / CPR, cc = e % CPR;
+        const int rw = e / CPR, cc = e % CPR;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (a0 + row < re) {
-            const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + row) * D
-                                              : Ku + (int64_t)S[(int64_t)u * r + a0 + row] * D;
+        if (a0 + rw < re) {
+            const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + rw) * D
+                                              : Ku + (int64_t)S[(int64_t)u * r + a0 + rw] * D;
             v = __ldg(reinterpret_cast<const uint4 *>(ksrow) + cc);
         }
-        *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(row, cc * 8, 128)) = v;
+        *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(rw, cc * 8, 128)) = v;
     }
-    float alpha = 0.f;
-    const bool row_ok = a0 + tid < re;
+    // alpha_a = g(|kbar|^2 - <k_a, kbar>) - mstar in fp64, scaled by log2(e) for ex2
+    float alpha2 = 0.f;
+    const bool row_ok = a0 + row < re;
     if (row_ok) {
-        const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + tid) * D
-                                          : Ku + (int64_t)S[(int64_t)u * r + a0 + tid] * D;
+        const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + row) * D
+                                          : Ku + (int64_t)S[(int64_t)u * r + a0 + row] * D;
         double kk = 0.0, bb = 0.0;
         for (int j = 0; j < D; ++j) {
             const double kbj = st[8 + j];
             kk = fma(to_f64(ksrow[j]), kbj, kk);
             bb = fma(kbj, kbj, bb);
         }
-        alpha = (float)(g * (bb - kk) - mstar);
+        alpha2 = (float)((g * (bb - kk) - mstar) * 1.4426950408889634);
     }
-    const float gf = (float)g;
+    const float g2 = (float)(g * 1.4426950408889634);
     const int64_t rows = ceil_div(n, splits);
     const int64_t lo = (int64_t)split * rows, hi = std::min<int64_t>(n, lo + rows);
-    const uint32_t tS = tbase, tO = tbase + 128, lane_off = (uint32_t)(w * 32) << 16;
+    const uint32_t tS = tbase, tO = tbase + 128, lane_off = (uint32_t)((w & 3) * 32) << 16;
     uint32_t phase = 0;
     float rowsum = 0.f;
     bool first = true;
     for (int64_t l0 = lo; l0 < hi; l0 += 128) {
-        // keys of the slice -> B operand of GEMM1 (K-major) and V^T -> B operand of GEMM2
-        // keys of the slice -> B operand (K-major, swizzled)
+        // keys of the slice -> B operand of GEMM1 (K-major, swizzled); V^T -> B operand of GEMM2
         for (int e = tid; e < 128 * CPR; e += kWTc) {
-            const int row = e / CPR, cc = e % CPR;
+            const int rw = e / CPR, cc = e % CPR;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (l0 + row < hi) v = __ldg(reinterpret_cast<const uint4 *>(Ku + (l0 + row) * D) + cc);
-            *reinterpret_cast<uint4 *>(sB + umma::sw128_offset(row, cc * 8, 128)) = v;
+            if (l0 + rw < hi) v = __ldg(reinterpret_cast<const uint4 *>(Ku + (l0 + rw) * D) + cc);
+            *reinterpret_cast<uint4 *>(sB + umma::sw128_offset(rw, cc * 8, 128)) = v;
         }
-        for (int e = tid; e < 128 * CPR; e += kWTc) {  // transpose V[l][c] -> B2[c][l]
-            const int row = e / CPR, cc = e % CPR;
+        for (int e = tid; e < 128 * CPR; e += kWTc) {
+            const int rw = e / CPR, cc = e % CPR;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (l0 + row < hi) v = __ldg(reinterpret_cast<const uint4 *>(Vu + (l0 + row) * D) + cc);
+            if (l0 + rw < hi) v = __ldg(reinterpret_cast<const uint4 *>(Vu + (l0 + rw) * D) + cc);
             const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&v);
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(cc * 8 + q, row, D)) = pv[q];
+                *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(cc * 8 + q, rw, D)) = pv[q];
         }
-        __syncthreads();
-        {  // gamma_l = -g <k_l, kbar> for the key this thread stages (row re-read through L1/L2)
+        if (tid < 128) {  // log2e * gamma_l = -log2e g <k_l, kbar> for key l0 + tid
             const int64_t l = l0 + tid;
             float gm = 0.f;
             if (l < hi) {
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(kWTc, 1)
                     for (int q = 0; q < 8; ++q) gm = fmaf(__bfloat162float(pv[q]), sKb[cc * 8 + q], gm);
                 }
             }
-            sG[tid] = -gf * gm;
+            sG[tid] = -g2 * gm;
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
@@ -372,26 +387,30 @@ __global__ void __launch_bounds__(kWTc, 1)
         mbar_wait(&bar, phase);
         phase ^= 1u;
         umma::fence_after_sync();
+        // P = exp2(g2 S + alpha2 + gamma2) for 64 columns per thread (its half), bf16 -> smem
         const int nl = (int)std::min<int64_t>(128, hi - l0);
+        {
+            const int cbase = half * 64;
+            float v[64];
+            umma::ld32(tS + lane_off + cbase, v);
+            umma::ld32(tS + lane_off + cbase + 32, v + 32);
+            float rs[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-            float v[32];
-            umma::ld32(tS + lane_off + c0, v);
-#pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
+            for (int g8 = 0; g8 < 8; ++g8) {
                 uint32_t pk[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int l = c0 + g8 * 8 + 2 * i;
-                    const float p0 = (row_ok && l < nl) ? __expf(fmaf(gf, v[g8 * 8 + 2 * i], alpha + sG[l])) : 0.f;
-                    const float p1 = (row_ok && l + 1 < nl) ? __expf(fmaf(gf, v[g8 * 8 + 2 * i + 1], alpha + sG[l + 1])) : 0.f;
+                    const int cl = g8 * 8 + 2 * i, l = cbase + cl;
+                    const float p0 = (row_ok && l < nl) ? ex2_approx_w(fmaf(g2, v[cl], alpha2 + sG[l])) : 0.f;
+                    const float p1 = (row_ok && l + 1 < nl) ? ex2_approx_w(fmaf(g2, v[cl + 1], alpha2 + sG[l + 1])) : 0.f;
                     const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-                    rowsum += __bfloat162float(pb.x) + __bfloat162float(pb.y);
+                    rs[i] += __bfloat162float(pb.x) + __bfloat162float(pb.y);
                     pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
                 }
-                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(tid, c0 + g8 * 8, 128)) =
+                *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(row, cbase + g8 * 8, 128)) =
                     make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
+            rowsum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
         }
         umma::fence_async_smem();
         umma::fence_before_sync();
@@ -406,24 +425,24 @@ __global__ void __launch_bounds__(kWTc, 1)
         umma::fence_after_sync();
         first = false;
     }
-    if (row_ok) {
-        float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + tid) * DC;
-        if (first) {  // empty key range: zero partial
+    xch[half * 128 + row] = rowsum;
+    __syncthreads();
+    float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + row) * DC;
+    if (first) {  // empty key range: zero partial
+        if (row_ok && half == 0)
             for (int c = 0; c < DC; ++c) out[c] = 0.f;
-        }
-    }
-    if (!first) {
+    } else {
+        constexpr int HD = D / 2;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
+        for (int c0 = 0; c0 < HD; c0 += 32) {
             float v[32];
-            umma::ld32(tO + lane_off + c0, v);
+            umma::ld32(tO + lane_off + half * HD + c0, v);
             if (row_ok) {
-                float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + tid) * DC + c0;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) out[i] = v[i];
+                for (int i = 0; i < 32; ++i) out[half * HD + c0 + i] = v[i];
             }
         }
-        if (row_ok) Ypart[(((int64_t)u * splits + split) * r + a0 + tid) * DC + D] = rowsum;
+        if (row_ok && half == 0) out[D] = xch[row] + xch[128 + row];
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -441,7 +460,7 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
     bool done = false;
     if constexpr (sizeof(T) == 2 && (D == 64 || D == 128)) {
         if (!(mode && std::strcmp(mode, "cuda") == 0)) {
-            const int smem_tc = 3 * 128 * D * 2 + 128 * 128 * 2 + 128 * 4 + D * 4 + 1024;  // A, B, V^T, P, gamma, kbar
+            const int smem_tc = WtSmem<D>::kTotal;  // A, B, V^T, P, gamma, kbar, exchange, barrier
             auto kt = weights_tc_kernel<D>;
             cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
             dim3 gt(splits, (Dm.r + 127) / 128, units);
