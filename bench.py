@@ -192,12 +192,19 @@ def main():
                     help="replicas: each rank runs the workload on its own units (weak scaling); "
                          "nshard: one sequence's keys sharded over the ranks (strong scaling). "
                          "Default: nshard for the long* configs, replicas otherwise")
+    ap.add_argument("--r", type=int, default=None, help="override the config's coreset size r")
+    ap.add_argument("--n", type=int, default=None, help="override the config's n (= m)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
     from paper_2602_10056_b200.inputs import CONFIGS, make_config
 
     cfg = CONFIGS[args.config]
+    if args.r is not None or args.n is not None:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, r=args.r or cfg.r, n=args.n or cfg.n, m=args.n or cfg.m,
+                                  name=f"{cfg.name}_n{args.n or cfg.n}_r{args.r or cfg.r}")
     if args.impl == "reference":
         run_reference(args, cfg)
         return

@@ -117,7 +117,8 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
                      seed=cache.opts.seed,
                      flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), reserved=0)
     O = torch.empty_like(Q)
-    B.wildcat_attend(shape, opts, Q, cache.KS, cache.X, cache.r_eff, cache.vmin, cache.vmax, O, None, stream)
+    ws = _workspace(shape, B.WC_OP_ATTEND, Q.device) if B.workspace_bytes(shape, B.WC_OP_ATTEND) else None
+    B.wildcat_attend(shape, opts, Q, cache.KS, cache.X, cache.r_eff, cache.vmin, cache.vmax, O, ws, stream)
     return O
 
 

@@ -148,8 +148,10 @@ size_t wc_workspace_bytes(const wc_shape *s, int op) {
                 carve_weights(c, s, &pp);
             }
             break;
-        case WC_OP_ATTEND:
-            return 0;
+        case WC_OP_ATTEND: {
+            const size_t a = wc::attend_ws_bytes(D);
+            return a ? ((a + 255) & ~size_t(255)) + 256 : 0;
+        }
         case WC_OP_FORWARD: {
             SelectWs w;
             carve_select(c, s, w);
@@ -161,6 +163,7 @@ size_t wc_workspace_bytes(const wc_shape *s, int op) {
             c.take<char>(U * (size_t)D.r * D.d * esize(s));
             c.take<float>(U * (size_t)D.r * (D.d + 1));
             c.take<char>(2 * U * (size_t)D.d * esize(s));
+            c.take<char>(wc::attend_ws_bytes(D));
             break;
         }
         case WC_OP_FORWARD_NSHARD:
@@ -227,11 +230,11 @@ int wildcat_attend(const wc_shape *s, const wc_opts *o, const void *Q, const voi
                    void *stream) {
     int rc = check_shape(s);
     if (rc) return rc;
-    (void)ws; (void)ws_bytes;
     if ((s->m > 0 && (!Q || !O)) || !KS || !X || !r_eff || !vmin || !vmax) return WC_EINVAL;
+    if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_ATTEND)))) return rc;
     const int clip = (o && (o->flags & WC_NO_CLIP)) ? 0 : 1;
     tmark(static_cast<cudaStream_t>(stream), true);
-    int n1 = wc::launch_attend(dims_of(s), Q, KS, X, r_eff, vmin, vmax, beta_of(s, o), clip, O,
+    int n1 = wc::launch_attend(dims_of(s), Q, KS, X, r_eff, vmin, vmax, beta_of(s, o), clip, O, ws,
                                static_cast<cudaStream_t>(stream));
     if (n1 < 0) return WC_ECUDA;
     tmark(static_cast<cudaStream_t>(stream));
@@ -261,6 +264,7 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     float *X = c.take<float>(U * (size_t)D.r * (D.d + 1));
     char *vr = c.take<char>(2 * U * (size_t)D.d * esize(s));
     void *vmin = vr, *vmax = vr + U * (size_t)D.d * esize(s);
+    void *aimg = c.take<char>(wc::attend_ws_bytes(D));
     if (S_out) S = S_out;
     if (reff_out) reff = reff_out;
     if (cudaMemsetAsync(S, 0xff, U * D.r * sizeof(int32_t), st) != cudaSuccess) return WC_ECUDA;
@@ -278,7 +282,7 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     total += k;
     tmark(st);
     const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
-    if ((k = wc::launch_attend(D, Q, KS, X, reff, vmin, vmax, beta, clip, O, st)) < 0) return WC_ECUDA;
+    if ((k = wc::launch_attend(D, Q, KS, X, reff, vmin, vmax, beta, clip, O, aimg, st)) < 0) return WC_ECUDA;
     total += k;
     tmark(st);
     return finish(total);

@@ -392,6 +392,291 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// =====================================================================================
+// tcgen05 path for r > 256 (bf16, d in {64, 128}): the coreset is streamed through shared memory
+// in chunks of RC = 128 rows, with the online (lazy) max rescaling of A5 (exact,
+// since the shift cancels in num/den).  A prep kernel writes, per (unit, chunk), one contiguous
+// "image" = [K_S chunk (K-major SW128) | X_hi^T chunk | X_lo^T chunk (if it fits) | w chunk fp32],
+// already in the swizzled shared-memory layout, so each chunk is ONE cp.async.bulk copy into a
+// double-buffered ring (issued as soon as the buffer's GEMM2 retires, so the next chunk lands
+// while the current one is computed).
+// Rescaling is lazy: the running max m only moves when a chunk's max exceeds it by more than
+// 2^8 (log2 domain), so P <= 2^8 and O / den stay exact ratios; when it moves, the warp rescales
+// its rows' O columns in TMEM (tcgen05.ld, multiply, tcgen05.st) and its running den.
+// =====================================================================================
+template <int D> struct TcLong {
+    static constexpr int RC = 128;
+    static constexpr int kQ = 128 * D * 2, kK = RC * D * 2, kX = D * RC * 2, kP = 128 * RC * 2;
+    static constexpr bool kSplitX = kQ + kP + 2 * (kK + 2 * kX + RC * 4 + 1024) <= 224 * 1024;
+    static constexpr int kImgK = 0, kImgXh = kK, kImgXl = kK + kX, kImgW = kK + (kSplitX ? 2 : 1) * kX;
+    static constexpr int kImg = kImgW + RC * 4;  // bytes per chunk image (multiple of 16)
+    static constexpr int kBuf = (kImg + 1023) & ~1023;
+    static constexpr int kOffQ = 0, kOffP = kQ, kOffB0 = kQ + kP;
+    static constexpr int kOffV = kOffB0 + 2 * kBuf, kOffXch = kOffV + 2 * D * 2, kOffBar = kOffXch + 2 * 128 * 4;
+    static constexpr int kOffTb = kOffBar + 3 * 8, kTotal = kOffTb + 8;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    attend_long_prep_kernel(const __nv_bfloat16 *__restrict__ KS, const float *__restrict__ X,
+                            const int32_t *__restrict__ r_eff, int r, int nch, unsigned char *__restrict__ img) {
+    using L = TcLong<D>;
+    constexpr int RC = L::RC, DC = D + 1, CPR = D / 8;
+    const int ch = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+    const int re = r_eff[u], s0 = ch * RC;
+    unsigned char *dst = img + ((int64_t)u * nch + ch) * L::kImg;
+    for (int e = tid; e < RC * CPR; e += blockDim.x) {
+        const int row = e / CPR, cc = e % CPR;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (s0 + row < re) v = __ldg(reinterpret_cast<const uint4 *>(KS + ((int64_t)u * r + s0 + row) * D) + cc);
+        *reinterpret_cast<uint4 *>(dst + L::kImgK + umma::sw128_offset(row, cc * 8, RC)) = v;
+    }
+    for (int e = tid; e < D * RC; e += blockDim.x) {
+        const int c = e / RC, sl = e % RC;
+        const float x = (s0 + sl < re) ? X[((int64_t)u * r + s0 + sl) * DC + c] : 0.f;
+        const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+        *reinterpret_cast<__nv_bfloat16 *>(dst + L::kImgXh + umma::sw128_offset(c, sl, D)) = xh;
+        if (L::kSplitX)
+            *reinterpret_cast<__nv_bfloat16 *>(dst + L::kImgXl + umma::sw128_offset(c, sl, D)) =
+                __float2bfloat16_rn(x - __bfloat162float(xh));
+    }
+    float *wd = reinterpret_cast<float *>(dst + L::kImgW);
+    for (int sl = tid; sl < RC; sl += blockDim.x) wd[sl] = (s0 + sl < re) ? X[((int64_t)u * r + s0 + sl) * DC + D] : 0.f;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attend_tc_long_kernel(const __nv_bfloat16 *__restrict__ Q, const unsigned char *__restrict__ img,
+                          const int32_t *__restrict__ r_eff, const __nv_bfloat16 *__restrict__ vmin,
+                          const __nv_bfloat16 *__restrict__ vmax, int64_t m, int nch_max, int group, int hq, int hkv,
+                          float beta, int clip, __nv_bfloat16 *__restrict__ O, int64_t tiles_per_head,
+                          int64_t total_tiles) {
+    using L = TcLong<D>;
+    constexpr int RC = L::RC;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;
+    if (smem_u32(sm) & 1023u) __trap();
+    unsigned char *sQ = sm + L::kOffQ, *sP = sm + L::kOffP;
+    __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sm + L::kOffV), *sVmax = sVmin + D;
+    float (*xch)[128] = reinterpret_cast<float (*)[128]>(sm + L::kOffXch);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::kOffBar);  // [0] MMA done, [1 + b] buffer b full
+    uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
+    const int tid = threadIdx.x, w = tid >> 5;
+    const int row = tid & 127, half = tid >> 7;
+
+    if (w == 0) umma::tmem_alloc(&tbase, 256);
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
+        fence_mbar_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tS = tbase, tO = tbase + RC;
+    const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+    const float bl2 = beta * 1.4426950408889634f;
+
+    const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
+    const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
+    auto unit_of = [&](int64_t tile) {
+        const int64_t head = tile / tiles_per_head;
+        return (int)(head / hq) * hkv + (int)(head % hq) / group;
+    };
+    // producer state (thread 0): the chunk stream is (tile, ch < nch(unit(tile))) in order
+    int64_t p_tile = t_begin;
+    int p_ch = 0, p_n = 0;
+    uint32_t issued = 0;
+    if (tid == 0 && p_tile < t_end) p_n = (int)ceil_div(r_eff[unit_of(p_tile)], RC);
+    auto issue = [&]() {
+        while (p_tile < t_end && p_ch >= p_n) {
+            ++p_tile;
+            p_ch = 0;
+            if (p_tile < t_end) p_n = (int)ceil_div(r_eff[unit_of(p_tile)], RC);
+        }
+        if (p_tile >= t_end) return;
+        const int b = issued & 1;
+        mbar_arrive_expect_tx(&bars[1 + b], L::kImg);
+        bulk_g2s(sm + L::kOffB0 + b * L::kBuf, img + ((int64_t)unit_of(p_tile) * nch_max + p_ch) * L::kImg, L::kImg,
+                 &bars[1 + b]);
+        ++issued;
+        ++p_ch;
+    };
+    if (tid == 0) {
+        issue();
+        issue();
+    }
+    uint32_t j = 0, mph = 0;
+    int cur_unit = -1;
+    for (int64_t tile = t_begin; tile < t_end; ++tile) {
+        const int64_t head = tile / tiles_per_head;
+        const int64_t q0 = (tile % tiles_per_head) * 128;
+        const int u = unit_of(tile);
+        const int re = r_eff[u];
+        const int nch = (int)ceil_div(re, RC);
+        const __nv_bfloat16 *Qh = Q + head * m * D;
+        constexpr int CPR = D / 8;
+        for (int e = tid; e < 128 * CPR; e += kTcThreads) {
+            const int rw = e / CPR, cc = e % CPR;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (q0 + rw < m) v = __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + rw) * D) + cc);
+            *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(rw, cc * 8, 128)) = v;
+        }
+        if (u != cur_unit) {
+            for (int c = tid; c < D; c += kTcThreads) {
+                sVmin[c] = vmin[(int64_t)u * D + c];
+                sVmax[c] = vmax[(int64_t)u * D + c];
+            }
+            cur_unit = u;
+        }
+        float mrun = -INFINITY, dn = 0.f;
+        for (int ch = 0; ch < nch; ++ch, ++j) {
+            const int b = j & 1;
+            const unsigned char *sB = sm + L::kOffB0 + b * L::kBuf;
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncthreads();
+            umma::fence_after_sync();
+            mbar_wait(&bars[1 + b], (j >> 1) & 1u);
+            if (tid == 0) {
+                umma::gemm_128xNxK(tS, smem_u32(sQ), smem_u32(sB + L::kImgK), RC, D, false);
+                umma::commit(&bars[0]);
+            }
+            mbar_wait(&bars[0], mph);
+            mph ^= 1u;
+            umma::fence_after_sync();
+            {
+                constexpr int HC = RC / 2;
+                const int cbase = half * HC, sg = ch * RC + cbase;
+                const float *sW = reinterpret_cast<const float *>(sB + L::kImgW);
+                float v[HC];
+#pragma unroll
+                for (int q = 0; q < HC / 32; ++q) umma::ld32(tS + lane_off + cbase + q * 32, v + q * 32);
+                float mx = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < HC; ++i)
+                    if (sg + i < re) mx = fmaxf(mx, v[i]);
+                xch[half][row] = mx;
+                __syncthreads();
+                const float mb = fmaxf(xch[0][row], xch[1][row]) * bl2;
+                bool resc = false;
+                float fac = 1.f;
+                if (ch == 0) {
+                    mrun = mb;
+                } else if (mb > mrun + 8.f) {
+                    fac = ex2_approx(mrun - mb);
+                    mrun = mb;
+                    dn *= fac;
+                    resc = true;
+                }
+                if (__any_sync(0xffffffffu, resc)) {  // warp-uniform: rescale this warp's rows of O
+                    constexpr int HD = D / 2;
+#pragma unroll
+                    for (int c0 = 0; c0 < HD; c0 += 32) {
+                        float o[32];
+                        umma::ld32(tO + lane_off + half * HD + c0, o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] *= fac;
+                        umma::st32(tO + lane_off + half * HD + c0, o);
+                    }
+                }
+                float dd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int g8 = 0; g8 < HC / 8; ++g8) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int cl = g8 * 8 + 2 * i;
+                        const float p0 = (sg + cl < re) ? ex2_approx(fmaf(v[cl], bl2, -mrun)) : 0.f;
+                        const float p1 = (sg + cl + 1 < re) ? ex2_approx(fmaf(v[cl + 1], bl2, -mrun)) : 0.f;
+                        const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                        dd[i] = fmaf(__bfloat162float(pb.x), sW[cbase + cl], dd[i]);
+                        dd[i] = fmaf(__bfloat162float(pb.y), sW[cbase + cl + 1], dd[i]);
+                        pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
+                    }
+                    *reinterpret_cast<uint4 *>(sP + umma::sw128_offset(row, cbase + g8 * 8, 128)) =
+                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                dn += (dd[0] + dd[1]) + (dd[2] + dd[3]);
+            }
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncthreads();
+            umma::fence_after_sync();
+            if (tid == 0) {
+                umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sB + L::kImgXh), D, RC, ch > 0);
+                if (L::kSplitX) umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sB + L::kImgXl), D, RC, true);
+                umma::commit(&bars[0]);
+            }
+            mbar_wait(&bars[0], mph);
+            mph ^= 1u;
+            umma::fence_after_sync();
+            if (tid == 0) issue();  // buffer b retired: prefetch the chunk after next into it
+        }
+        __syncthreads();  // xch free
+        xch[half][row] = dn;
+        __syncthreads();
+        const float den = xch[0][row] + xch[1][row];
+        {
+            const int64_t qi = q0 + row;
+            const float inv = (nch > 0 && den > 0.f) ? 1.f / den : 0.f;
+            constexpr int HD = D / 2;
+#pragma unroll
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                const int cc0 = half * HD + c0;
+                float v[32];
+                umma::ld32(tO + lane_off + cc0, v);
+                if (qi < m) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float o0 = inv != 0.f ? v[2 * i] * inv : 0.f, o1 = inv != 0.f ? v[2 * i + 1] * inv : 0.f;
+                        if (clip) {
+                            o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[cc0 + 2 * i])), __bfloat162float(sVmax[cc0 + 2 * i]));
+                            o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[cc0 + 2 * i + 1])), __bfloat162float(sVmax[cc0 + 2 * i + 1]));
+                        }
+                        const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
+                        pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
+                    }
+                    uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + qi) * D + cc0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                }
+            }
+        }
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+    }
+    if (w == 0) umma::tmem_dealloc(tbase, 256);
+}
+
+template <int D>
+int launch_attend_tc_long(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                          const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws,
+                          cudaStream_t st) {
+    using L = TcLong<D>;
+    if (!ws) return -1;
+    const int nch = (int)ceil_div(Dm.r, L::RC);
+    unsigned char *img = static_cast<unsigned char *>(ws);
+    attend_long_prep_kernel<D><<<dim3(nch, (unsigned)Dm.units()), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, nch, img);
+    auto kern = attend_tc_long_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    const int64_t tph = ceil_div(Dm.m, 128);
+    const int64_t total = tph * Dm.hq * Dm.batch;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>(total, sms);
+    kern<<<grid, kTcThreads, L::kTotal, st>>>(static_cast<const __nv_bfloat16 *>(Q), img, r_eff,
+                                              static_cast<const __nv_bfloat16 *>(vmin),
+                                              static_cast<const __nv_bfloat16 *>(vmax), Dm.m, nch, Dm.group(), Dm.hq,
+                                              Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+}
+
 template <typename T, int D>
 int launch_attend_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                      const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
@@ -400,7 +685,7 @@ int launch_attend_td(const Dims &Dm, const void *Q, const void *KS, const float 
     const size_t smem = ((size_t)kBM * (D + 1) + (size_t)kRT * (D + 1) + (size_t)kRT * (DC + 1) +
                          (size_t)kBM * (kRT + 1) + kBM) * sizeof(float);
     auto kern = attend_kernel<T, D>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)ceil_div(Dm.m, kBM), Dm.hq, Dm.batch);
     kern<<<grid, kAT, smem, st>>>(static_cast<const T *>(Q), static_cast<const T *>(KS), X, r_eff,
                                   static_cast<const T *>(vmin), static_cast<const T *>(vmax), Dm.m, Dm.r,
@@ -422,12 +707,28 @@ int launch_attend_t(const Dims &Dm, const void *Q, const void *KS, const float *
 
 }  // namespace
 
-int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                  const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
+// 0: CUDA-core kernel, 1: tcgen05 kernel with the coreset resident, 2: tcgen05 kernel streaming r > 256
+static int attend_path(const Dims &D) {
     static const char *mode = std::getenv("WC_ATTEND");  // "cuda": CUDA-core kernel (A/B tests)
-    const bool tc_ok = D.dtype == 1 && (D.d == 64 || D.d == 128) && D.r <= 256 && D.m > 0 &&
-                       !(mode && std::strcmp(mode, "cuda") == 0);
-    if (tc_ok) {
+    if (mode && std::strcmp(mode, "cuda") == 0) return 0;
+    if (!(D.dtype == 1 && (D.d == 64 || D.d == 128) && D.m > 0)) return 0;
+    return D.r <= 256 ? 1 : 2;
+}
+
+size_t attend_ws_bytes(const Dims &D) {
+    if (attend_path(D) != 2) return 0;
+    const size_t img = D.d == 64 ? TcLong<64>::kImg : TcLong<128>::kImg;
+    return D.units() * (size_t)ceil_div(D.r, 128) * img;
+}
+
+int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                  const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+    const int path = attend_path(D);
+    if (path == 2) {
+        if (D.d == 64) return launch_attend_tc_long<64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        return launch_attend_tc_long<128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    }
+    if (path == 1) {
         const int rp = D.r <= 32 ? 32 : D.r <= 64 ? 64 : D.r <= 128 ? 128 : 256;
         if (D.d == 64) {
             switch (rp) {

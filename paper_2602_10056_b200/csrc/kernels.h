@@ -81,7 +81,8 @@ int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, co
 
 // A5: attend.
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                  const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st);
+                  const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st);
+size_t attend_ws_bytes(const Dims &D);  // staging images for r > 256 (0 otherwise)
 
 // n-sharded forward (nshard.cu).  Single unit per call; NCCL resolved at run time.
 size_t ns_workspace_bytes(const Dims &D);

@@ -371,7 +371,7 @@ struct NsWs {
     ProloguePartials pp;
     double *stats, *nrm2, *p, *F, *ctot, *sendtot, *ranktot, *packet, *sumbuf, *maxbuf, *rkbuf, *L, *Yfull;
     float *Ypart, *X;
-    void *KS, *vmin, *vmax;
+    void *KS, *vmin, *vmax, *aimg;
     int32_t *S, *reff;
     Ctl *ctl;
 };
@@ -420,6 +420,7 @@ size_t ns_carve(const Dims &D, void *base, NsWs &w) {
     w.S = c.take<int32_t>(D.r);
     w.reff = c.take<int32_t>(1);
     w.ctl = c.take<Ctl>(1);
+    w.aimg = c.take<char>(attend_ws_bytes(D));
     return ((c.off + 255) & ~size_t(255)) + 256;
 }
 
@@ -459,7 +460,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     // ---- A1 + A2: r rounds
     const size_t usm = (size_t)(2 * D + r + kNuW * kNuST + 2 * kNuST + 40) * sizeof(double);
     auto upd = ns_update<T, D>;
-    if (usm > 48 * 1024) cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+    cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
     for (int i = 0; i < r; ++i) {
         ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot);
         WC_NCCL(api.allGather(w.sendtot, w.ranktot, 1, ncclFloat64, cm->comm, st));
@@ -477,7 +478,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     if (launch_weights_solve(Dm, w.Yfull, w.L, w.reff, w.X, st) < 0) return WC_ECUDA;
     // ---- A5: local queries
     const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
-    if (Dm.m > 0 && launch_attend(Dm, Q, w.KS, w.X, w.reff, w.vmin, w.vmax, beta, clip, O, st) < 0) return WC_ECUDA;
+    if (Dm.m > 0 && launch_attend(Dm, Q, w.KS, w.X, w.reff, w.vmin, w.vmax, beta, clip, O, w.aimg, st) < 0) return WC_ECUDA;
     if (S_out && cudaMemcpyAsync(S_out, w.S, sizeof(int32_t) * r, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return WC_ECUDA;
     if (reff_out && cudaMemcpyAsync(reff_out, w.reff, sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)

@@ -834,8 +834,7 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
     const int threads = (Dm.n / a.cpu >= 384) ? kSelThreads : 256;
     const size_t smem = (size_t)(2 * D + Dm.r + (threads / 32) * kST + 2 * kST + 40) * sizeof(double);
     auto kern = rpc_select_kernel<T, D>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (a.cpu > 1) {
         void *args[] = {&a};
         if (cudaLaunchCooperativeKernel((const void *)kern, grid, dim3(threads), args, smem, st) != cudaSuccess)

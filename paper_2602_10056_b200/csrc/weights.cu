@@ -475,7 +475,7 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
         const size_t smem1 = D * sizeof(double) + (size_t)(kTA + 2 * kTL) * (D + 1) * sizeof(float) +
                              (size_t)kTA * (kTL + 1) * sizeof(float);
         auto pk = weights_partial_kernel<T, D>;
-        if (smem1 > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
         pk<<<g1, kWT, smem1, st>>>(static_cast<const T *>(K), static_cast<const T *>(V), S,
                                    static_cast<const T *>(KSin), r_eff, stats, Dm.n, Dm.r, splits, Ypart);
     }
@@ -493,7 +493,8 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
                    cudaStream_t st) {
     const size_t smem = (size_t)8 * Dm.r * sizeof(double);
     auto sk = weights_solve_kernel<D>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the kernel also holds ~25 KB of static smem: always raise the dynamic limit
+    cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 g2((D + 1 + 7) / 8, Dm.units());
     sk<<<g2, 256, smem, st>>>(Yfull, L, r_eff, Dm.r, X);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;

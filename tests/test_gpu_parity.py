@@ -70,6 +70,21 @@ def test_llm_like_conditioning():
     compare(Q, K, V, 96, "bf16", seed=2)
 
 
+@pytest.mark.parametrize("d,r,family", [(128, 512, "G"), (64, 320, "L"), (128, 1024, "C")])
+def test_large_r_streamed_attend(d, r, family):
+    # r > 256: the tcgen05 attend streams the coreset in 128-row chunks with lazy max rescaling
+    # (LLM-like keys make later chunks raise the running max); r = 320 leaves a ragged last chunk
+    Q, K, V = qkv(1, 4, 2, 300, 3000, d, "bf16", family, seed=11)
+    compare(Q, K, V, r, "bf16", seed=11)
+
+
+def test_large_r_exhausted():
+    # r_eff (distinct keys) far below r: fewer chunks than r / 128, zero-padded tail
+    Q, K, V = qkv(1, 2, 1, 200, 2000, 128, "bf16", "D", seed=6, distinct=150)
+    out = compare(Q, K, V, 512, "bf16", seed=6)
+    assert out["r_eff"][0] == 150
+
+
 def test_rank_one_and_full_rank():
     Q, K, V = qkv(1, 1, 1, 40, 64, 16, "f32", "G", seed=1)
     compare(Q, K, V, 1, "f32", seed=1)
