@@ -68,7 +68,11 @@ def lib():
             L.wco_attend.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _p, _c_i32, _c_dbl, _p, _p, _c_i32, _p]
             L.wco_exact_attention.argtypes = [_c_i64, _c_i64, _c_i32, _p, _p, _p, _c_dbl, _p]
             L.wco_forward.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_dbl,
-                                      _c_dbl, _c_u64, _c_i32, _p, _p, _p, _p, _p, _p, _p, _p]
+                                      _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p, _p, _p]
+            L.wco_accept_uniform.argtypes = [_c_u64, ctypes.c_uint32, _c_u64]
+            L.wco_accept_uniform.restype = _c_dbl
+            L.wco_select_blocked.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64,
+                                             _c_u64, _p, _p, _p, _p, _p, _p, _p]
             L.wco_num_threads.restype = ctypes.c_int
             L.wco_set_num_threads.argtypes = [ctypes.c_int]
             _lib = L
@@ -147,6 +151,30 @@ def select(K, kbar, g, mstar, r, seed, unit=0):
     return dict(S=S, r_eff=re, F=F, p=p, trace=tr[: re + 1], L=L)
 
 
+def accept_uniform(seed, cand, unit=0):
+    """Acceptance uniform of blocked-RPC candidate `cand` (Philox tag 'ACPT', reading Z22)."""
+    return lib().wco_accept_uniform(int(seed), int(cand), int(unit))
+
+
+def select_blocked(K, kbar, g, mstar, r, block, seed, unit=0):
+    """Blocked (accelerated) RPCholesky, block size `block`.  Returns dict(S, r_eff, F, p, L, nblocks, ncand)."""
+    K = _f64(K)
+    n, d = K.shape
+    kbar = _f64(kbar)
+    S = np.full(r, -1, dtype=np.int32)
+    reff = np.zeros(1, dtype=np.int32)
+    F = np.zeros((r, n))
+    p = np.zeros(n)
+    L = np.zeros((r, r))
+    nb = np.zeros(1, dtype=np.int32)
+    nc = np.zeros(1, dtype=np.int32)
+    rc = lib().wco_select_blocked(n, d, r, int(block), _ptr(K), _ptr(kbar), float(g), float(mstar), int(seed),
+                                  int(unit), _ptr(S), _ptr(reff), _ptr(F), _ptr(p), _ptr(L), _ptr(nb), _ptr(nc))
+    if rc:
+        raise MemoryError("wco_select_blocked failed")
+    return dict(S=S, r_eff=int(reff[0]), F=F, p=p, L=L, nblocks=int(nb[0]), ncand=int(nc[0]))
+
+
 def select_mr(K, kbar, g, mstar, r, seed, unit=0):
     """Literal Alg 1 (M/R form).  Returns dict(S, r_eff, M, R, W, p)."""
     K = _f64(K)
@@ -205,7 +233,7 @@ def exact_attention(Q, K, V, beta=None):
     return O
 
 
-def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True):
+def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1):
     """Alg 4 over [batch, heads, seq, d] arrays (float64 copies of the inputs).
 
     Returns dict(O, S, r_eff, stats, X)."""
@@ -221,7 +249,7 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True):
     reff = np.zeros(units, dtype=np.int32)
     st = np.zeros((units, 5))
     X = np.zeros((units, r, d + 1))
-    rc = lib().wco_forward(batch, hq, hkv, m, n, d, r, beta, float(rq), int(seed), int(bool(clip)),
+    rc = lib().wco_forward(batch, hq, hkv, m, n, d, r, beta, float(rq), int(seed), int(bool(clip)), int(block),
                            _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st), _ptr(X))
     if rc:
         raise RuntimeError(f"wco_forward failed ({rc})")

@@ -184,6 +184,28 @@ static int64_t draw_pivot(int64_t n, const double *p, double T, double u)
     return -1;
 }
 
+/* One F-form round (see wco_select below) with pivot s at 0-based round i:
+ * writes F[i,:], downdates p and zeroes p_s.                                */
+static void fform_round(int64_t n, int32_t d, int32_t i, const double *K, const double *kbar,
+                        double g, double mstar, double *F, double *p, int64_t s)
+{
+    double ps = p[s];
+    double rs = sqrt(ps);
+    const double *ks = K + s * d;
+#pragma omp parallel for schedule(static)
+    for (int64_t l = 0; l < n; ++l) {
+        double c = hker(d, K + l * d, ks, kbar, g, mstar);
+        double acc = 0.0;
+        for (int32_t j = 0; j < i; ++j) acc += F[(size_t)j * n + l] * F[(size_t)j * n + s];
+        c = c - acc;
+        double f = c / rs;
+        F[(size_t)i * n + l] = f;
+        double q = p[l] - f * f;
+        p[l] = q > 0.0 ? q : 0.0;
+    }
+    p[s] = 0.0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* RPNys selection in the Cholesky-factor ("F") form, per unit.
  * Alg 1 maintains M = h(K_S,K_S)^{-1} and R = h(K_S,K); its
@@ -226,21 +248,7 @@ int wco_select(int64_t n, int32_t d, int32_t r, const double *K, const double *k
         if (T <= theta) { re = i; break; }
         double u = wco_pivot_uniform(seed, (uint32_t)i, unit);
         int64_t s = draw_pivot(n, p, T, u);
-        double ps = p[s];
-        double rs = sqrt(ps);
-        const double *ks = K + s * d;
-#pragma omp parallel for schedule(static)
-        for (int64_t l = 0; l < n; ++l) {
-            double c = hker(d, K + l * d, ks, kbar, g, mstar);
-            double acc = 0.0;
-            for (int32_t j = 0; j < i; ++j) acc += F[(size_t)j * n + l] * F[(size_t)j * n + s];
-            c = c - acc;
-            double f = c / rs;
-            F[(size_t)i * n + l] = f;
-            double q = p[l] - f * f;
-            p[l] = q > 0.0 ? q : 0.0;
-        }
-        p[s] = 0.0;
+        fform_round(n, d, i, K, kbar, g, mstar, F, p, s);
         S[i] = (int32_t)s;
     }
     if (re == r && trace) {
@@ -258,6 +266,109 @@ int wco_select(int64_t n, int32_t d, int32_t r, const double *K, const double *k
     if (p_out) memcpy(p_out, p, sizeof(double) * (size_t)n);
     free(p);
     free(F);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Blocked ("accelerated") RPCholesky -- the oversampling mechanism the paper
+ * names for future work (citing accelerated RPCholesky [epperly2024embrace]);
+ * the algorithm is that cited work's block rejection sampler, reading Z22.
+ * Per block, with i pivots accepted so far and residual diagonal p (T = sum p):
+ *   1. draw b candidates s_0..s_{b-1} i.i.d. from p / T (Eq. 4 rule, draw_pivot),
+ *      candidate c = (global candidate count) uses the pivot uniform of counter c,
+ *      so b = 1 reproduces wco_select exactly;
+ *   2. H = residual kernel on the candidates at the block start:
+ *      H[a][a] = p[s_a];  H[a][c] = h~(k_sa, k_sc) - sum_{q<i} F[q,s_a] F[q,s_c];
+ *   3. rejection, in candidate order j = 0..b-1 (stop once i + accepted = r):
+ *      accept s_j iff  v_j * p[s_j] < H[j][j]   (v_j = accept uniform of counter c),
+ *      where H[j][j] is the Schur complement after the candidates accepted before
+ *      it in this block (so P(accept) = current residual / block-start residual;
+ *      the first candidate is always accepted, a repeated candidate never);
+ *      on acceptance H[a][c] -= H[a][j] H[j][c] / H[j][j] for a, c > j;
+ *   4. the accepted pivots, in order, each run one F-form round (fform_round).
+ * The accepted sequence has the law of sequential RPCholesky (rejection sampling
+ * from the proposal p >= current residual); pivots for a given seed differ from
+ * wco_select's unless b = 1.  Exhaustion (Z3) is tested at block starts.
+ * Extra outputs: nblocks[1], ncand[1] (candidates drawn) -- may be NULL.      */
+/* ------------------------------------------------------------------------ */
+double wco_accept_uniform(uint64_t seed, uint32_t cand, uint64_t unit)
+{
+    uint32_t ctr[4] = {cand, (uint32_t)unit, (uint32_t)(unit >> 32), 0x41435054u};  /* 'ACPT' */
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t x[4];
+    wco_philox4x32_10(ctr, key, x);
+    double a = (double)(x[0] >> 5);
+    double b = (double)(x[1] >> 6);
+    return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+}
+
+int wco_select_blocked(int64_t n, int32_t d, int32_t r, int32_t b, const double *K, const double *kbar,
+                       double g, double mstar, uint64_t seed, uint64_t unit,
+                       int32_t *S, int32_t *r_eff, double *F_out, double *p_out, double *L,
+                       int32_t *nblocks, int32_t *ncand)
+{
+    if (b < 1) return -1;
+    double *p = (double *)malloc(sizeof(double) * (size_t)n);
+    double *F = (double *)calloc((size_t)r * (size_t)n, sizeof(double));
+    double *H = (double *)malloc(sizeof(double) * (size_t)b * (size_t)b);
+    int64_t *cs = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
+    int64_t *acc = (int64_t *)malloc(sizeof(int64_t) * (size_t)b);
+    if (!p || !F || !H || !cs || !acc) { free(p); free(F); free(H); free(cs); free(acc); return -1; }
+
+    for (int64_t l = 0; l < n; ++l) p[l] = hker(d, K + l * d, K + l * d, kbar, g, mstar);
+    double T0 = 0.0;
+    for (int64_t l = 0; l < n; ++l) T0 += p[l];
+    double theta = 1000.0 * (double)r * ldexp(1.0, -52) * T0;
+
+    for (int a = 0; a < r; ++a) S[a] = -1;
+    int32_t i = 0, nb = 0;
+    uint32_t c = 0;
+    while (i < r) {
+        double T = 0.0;
+        for (int64_t l = 0; l < n; ++l) T += p[l];
+        if (T <= theta) break;
+        /* 1. candidates */
+        for (int j = 0; j < b; ++j) cs[j] = draw_pivot(n, p, T, wco_pivot_uniform(seed, c + (uint32_t)j, unit));
+        /* 2. block-start residual kernel on the candidates */
+        for (int a = 0; a < b; ++a)
+            for (int e = 0; e < b; ++e) {
+                if (a == e) { H[a * b + a] = p[cs[a]]; continue; }
+                double v = hker(d, K + cs[a] * d, K + cs[e] * d, kbar, g, mstar);
+                double f = 0.0;
+                for (int32_t q = 0; q < i; ++q) f += F[(size_t)q * n + cs[a]] * F[(size_t)q * n + cs[e]];
+                H[a * b + e] = v - f;
+            }
+        /* 3. rejection */
+        int na = 0;
+        for (int j = 0; j < b && i + na < r; ++j) {
+            int dup = 0;
+            for (int a = 0; a < na; ++a) dup |= (acc[a] == cs[j]);
+            double v = wco_accept_uniform(seed, c + (uint32_t)j, unit);
+            if (dup || !(v * p[cs[j]] < H[j * b + j])) continue;
+            acc[na++] = cs[j];
+            double hjj = H[j * b + j];
+            for (int a = j + 1; a < b; ++a)
+                for (int e = j + 1; e < b; ++e) H[a * b + e] -= H[a * b + j] * H[j * b + e] / hjj;
+        }
+        c += (uint32_t)b;
+        ++nb;
+        /* 4. F-form rounds for the accepted pivots */
+        for (int a = 0; a < na; ++a) {
+            fform_round(n, d, i, K, kbar, g, mstar, F, p, acc[a]);
+            S[i++] = (int32_t)acc[a];
+        }
+    }
+    *r_eff = i;
+    if (nblocks) *nblocks = nb;
+    if (ncand) *ncand = (int32_t)c;
+    if (L) {
+        memset(L, 0, sizeof(double) * (size_t)r * (size_t)r);
+        for (int a = 0; a < i; ++a)
+            for (int e = 0; e <= a; ++e) L[a * r + e] = F[(size_t)e * n + S[a]];
+    }
+    if (F_out) memcpy(F_out, F, sizeof(double) * (size_t)r * (size_t)n);
+    if (p_out) memcpy(p_out, p, sizeof(double) * (size_t)n);
+    free(p); free(F); free(H); free(cs); free(acc);
     return 0;
 }
 
@@ -481,10 +592,11 @@ void wco_exact_attention(int64_t m, int64_t n, int32_t d, const double *Q, const
  * rq < 0 -> R_Q from the unit's query group (Alg 4).
  * Optional outputs (may be NULL): S [units][r], r_eff [units],
  * stats [units][5] = tau,g,mstar,R_K,R_Q, X [units][r][d+1].
+ * block > 1 selects with the blocked variant (wco_select_blocked, reading Z22).
  * Returns 0, or the first nonzero sub-status.                               */
 /* ------------------------------------------------------------------------ */
 int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d,
-                int32_t r, double beta, double rq, uint64_t seed, int32_t clip,
+                int32_t r, double beta, double rq, uint64_t seed, int32_t clip, int32_t block,
                 const double *Q, const double *K, const double *V, double *O,
                 int32_t *S_out, int32_t *reff_out, double *stats_out, double *X_out)
 {
@@ -518,7 +630,11 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
             double st[5];
             wco_prologue(n, d, Ku, (int64_t)group * m, Qg, rq, beta, kbar, st);
             int32_t re = 0;
-            status = wco_select(n, d, r, Ku, kbar, st[1], st[2], seed, u, S, &re, NULL, NULL, NULL, NULL);
+            if (block > 1)
+                status = wco_select_blocked(n, d, r, block, Ku, kbar, st[1], st[2], seed, u, S, &re, NULL, NULL,
+                                            NULL, NULL, NULL);
+            else
+                status = wco_select(n, d, r, Ku, kbar, st[1], st[2], seed, u, S, &re, NULL, NULL, NULL, NULL);
             if (status) break;
             status = wco_weights(n, d, r, Ku, Vu, S, re, kbar, st[1], st[2], X);
             if (status) break;
