@@ -97,13 +97,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def select_bytes(n, d, r, e):
-    """Algorithmic HBM bytes of the selection loop per unit (SURVEY.md 8(d), DESIGN.md):
+def select_bytes(n, d, r, e, nblocks=None, fread=None):
+    """Algorithmic HBM bytes of the selection loop per unit (SURVEY.md 8(d), DESIGN.md section 6):
+    per block (sequential: per round) the K rows (n d e) and the residual read + write (16 n), once
+    the new F rows (8 n r), and the F prefix re-read at every block start (8 n Fread, Fread = sum of
+    the block-start pivot counts).  Sequential RPC (nblocks = r, Fread = r (r-1) / 2) gives
     n r (d e + 24) + 4 n r (r - 1)."""
-    return n * r * (d * e + 24) + 4 * n * r * (r - 1)
+    if nblocks is None:
+        nblocks, fread = r, r * (r - 1) / 2
+    return n * (nblocks * (d * e + 16) + 8 * r + 8 * fread)
 
 
-def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048):
+def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048, block=1):
     """Time the fp64 oracle (as it stands) on a bounded sample: unit 0's full prologue + selection +
     weights over all n keys, and the attend on `max_queries` query rows; extrapolate linearly in the
     number of query rows and units to the whole workload.  Returns (queries/s, seconds, details)."""
@@ -119,7 +124,10 @@ def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048):
     beta = 1.0 / math.sqrt(d)
     t0 = time.perf_counter()
     kbar, st = oracle.prologue(K64, Qg)
-    sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
+    if block >= 2:
+        sel = oracle.select_blocked(K64, kbar, st["g"], st["mstar"], cfg.r, block, seed=cfg.seed, unit=0)
+    else:
+        sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
     t1 = time.perf_counter()
     X = oracle.weights(K64, V64, sel["S"], sel["r_eff"], kbar, st["g"], st["mstar"])
     t2 = time.perf_counter()
@@ -130,7 +138,8 @@ def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048):
     total = per_unit * cfg.units
     queries = cfg.batch * cfg.hq * cfg.m
     info = dict(select_s=t1 - t0, weights_s=t2 - t1, attend_s=t3 - t2, attend_rows=ms, threads=threads,
-                sample=(f"oracle on unit 0 of {cfg.units}: full prologue+selection+weights over n={cfg.n} keys, "
+                sample=(f"oracle on unit 0 of {cfg.units}: full prologue+selection"
+                        f"{f' (blocked, b={block})' if block >= 2 else ''}+weights over n={cfg.n} keys, "
                         f"attend on {ms} of {Qg.shape[0]} query rows; extrapolated linearly to all rows/units"))
     return queries / total, total, info
 
@@ -154,11 +163,11 @@ def run_reference(args, cfg):
 
     Q, K, V = make_config(cfg)
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries)
+        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block)
     vals, secs = [], []
     info = None
     for _ in range(args.steps):
-        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries)
+        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block)
         vals.append(v)
         secs.append(s)
     tot = sum(secs)
@@ -167,7 +176,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r,
+        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r, "block": args.block,
                    "input_dtype": cfg.dtype, "family": cfg.family},
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                          "sample": info["sample"], "cpu": cpu_model()},
@@ -194,6 +203,9 @@ def main():
                          "Default: nshard for the long* configs, replicas otherwise")
     ap.add_argument("--r", type=int, default=None, help="override the config's coreset size r")
     ap.add_argument("--n", type=int, default=None, help="override the config's n (= m)")
+    ap.add_argument("--block", type=int, default=1,
+                    help="pivot selection: 1 = sequential RPCholesky (Alg 1); b >= 2 = blocked RPCholesky "
+                         "with b candidates per block (reading Z22)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -250,7 +262,7 @@ def main():
         Obuf = torch.empty_like(Qd)  # preallocated: no allocator traffic inside the timed region
 
         def step():
-            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf)
+            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=args.block)
 
     for _ in range(args.warmup):
         step()
@@ -296,12 +308,25 @@ def main():
                else None)
     e = 2 if cfg.dtype == "bf16" else 4
     r_eff = int(R.min().item())
-    alg_bytes = units * select_bytes(cfg.n, cfg.d, r_eff, e)
+    sel_info = None
+    if mode == "replicas":
+        # selection bookkeeping of the same (deterministic) selection: blocks run, F rows re-read
+        sel = wc.select(Qd, Kd, cfg.r, seed=seed, block=args.block)
+        stt = sel.stats.double().cpu()
+        reff_u = sel.r_eff.cpu()
+        alg_bytes = sum(select_bytes(cfg.n, cfg.d, int(reff_u[u]), e, float(stt[u, 6]), float(stt[u, 8]))
+                        for u in range(units))
+        sel_info = {"block": args.block, "blocks_per_unit": float(stt[:, 6].mean()),
+                    "candidates_per_unit": float(stt[:, 7].mean()), "f_rows_reread_per_unit": float(stt[:, 8].mean())}
+        del sel
+    else:
+        alg_bytes = units * select_bytes(cfg.n, cfg.d, r_eff, e)
     sel_ms = st_mean[1] if st_mean else None
     achieved = alg_bytes / (sel_ms / 1e3) / 1e9 if sel_ms else None
     peak, peak_kind = peaks()
     traffic = None
-    tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}.json")
+    tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}" + (f"_b{args.block}" if args.block >= 2 else "")
+                      + ".json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
@@ -381,7 +406,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.n <= 262144:
-        v, secs, info = cpu_oracle_sample(cfg, Q, K, V)
+        v, secs, info = cpu_oracle_sample(cfg, Q, K, V, block=args.block)
         cpu = {"value": v, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                "sample": info["sample"], "cpu": cpu_model(), "seconds_extrapolated": secs,
                "select_s": info["select_s"], "weights_s": info["weights_s"], "attend_s": info["attend_s"]}
@@ -403,9 +428,12 @@ def main():
             "config": {"workload": cfg.name, "units_per_gpu": units, "n": cfg.n, "m": cfg.m, "d": cfg.d,
                        "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
                        "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}"),
+                       "select": "blocked" if args.block >= 2 else "sequential", "block": args.block,
                        "l2": f"flushed ({args.flush_mb} MB write) before each step"},
             "stages_ms": dict(zip(st_names, st_mean)) if st_mean else None,
-            "roofline": {"kernel": "rpc_select_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "selection": sel_info,
+            "roofline": {"kernel": "rpc_select_blocked_kernel" if args.block >= 2 else "rpc_select_tma_kernel",
+                         "bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                          "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes},

@@ -17,7 +17,11 @@
  *   r_eff  int32  [units]            number of pivots actually drawn (<= r, Z3)
  *   L      double [units][r][r]      lower-triangular Cholesky factor of h~(K_S,K_S) in pivot
  *                                    order, L[a][b] = F[b, S[a]] (b <= a), 0 elsewhere (Z6)
- *   stats  double [units][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, 0, 0, kbar[d]
+ *   stats  double [units][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, nblocks, ncand,
+ *                                    Fread, 0 (x7), kbar[d].  Selection bookkeeping: nblocks =
+ *                                    blocks (sequential: rounds) run, ncand = candidates drawn,
+ *                                    Fread = sum over blocks of the F rows re-read at the block
+ *                                    start (sequential: sum_i i) -- the F traffic is 8 n Fread bytes
  *   KS     dtype  [units][r][d]      coreset keys, uncentred (Alg 2 "K_S <- K_S + kbar")
  *   X      float  [units][r][d+1]    [V_S, w] = W [V, 1_n]  (Alg 2 "Compress values")
  *   vmin, vmax dtype [units][d]      columnwise range of V (Alg 4)
@@ -42,7 +46,7 @@ extern "C" {
 #endif
 
 #define WC_OK 0
-#define WC_EINVAL -1        /* null pointer, bad enum, unknown flag */
+#define WC_EINVAL -1        /* null pointer, bad enum, unknown flag, opts->block > WC_MAX_BLOCK */
 #define WC_ESHAPE -2        /* r < 1, r > n, bins != 1, heads_q % heads_kv != 0, d not in {16,32,64,128}, m < 0 */
 #define WC_EDTYPE -3        /* dtype not WC_F32 / WC_BF16 */
 #define WC_EWORKSPACE -4    /* ws too small or misaligned (needs 256-byte alignment) */
@@ -62,7 +66,8 @@ extern "C" {
 /* flags */
 #define WC_NO_CLIP 1u       /* skip the clip of Alg 3 (reading Z15) */
 
-#define WC_STATS_STRIDE(d) (8 + (d))
+#define WC_STATS_HEAD 16
+#define WC_STATS_STRIDE(d) (WC_STATS_HEAD + (d))
 
 typedef struct wc_shape {
     int32_t batch;     /* >= 1 */
@@ -82,8 +87,14 @@ typedef struct wc_opts {
     double rq;         /* R_Q of Alg 2; < 0 (or NaN) computes max ||q|| over the unit's query group */
     uint64_t seed;     /* Philox4x32-10 key for the pivot draws (reading Z2) */
     uint32_t flags;    /* WC_NO_CLIP */
-    uint32_t reserved;
+    uint32_t block;    /* pivot selection: 0 or 1 = sequential RPCholesky, Alg 1;
+                          2..WC_MAX_BLOCK = blocked ("accelerated") RPCholesky with b = block
+                          candidates per block (P:678 future work; reading Z22): same pivot LAW
+                          as Alg 1, a different pivot sequence for a given seed.  Blocked needs
+                          r <= 1024 (shared-memory plan), else WC_EUNSUPPORTED. */
 } wc_opts;
+
+#define WC_MAX_BLOCK 16
 
 /* Bytes of workspace the op needs for this shape (0 on invalid shape). */
 size_t wc_workspace_bytes(const wc_shape *shape, int op);
@@ -91,7 +102,8 @@ size_t wc_workspace_bytes(const wc_shape *shape, int op);
 /* Alg 2 lines "Recenter keys" .. RPNys + Alg 1:
  * per unit, recentre K, compute R_K, R_Q (from Q, or opts->rq if >= 0; Q may then be
  * NULL), tau (Eq. 7), and run r rounds of randomly pivoted Cholesky on
- * h~(a,b) = exp(beta/tau^2 <a-kbar, b-kbar> - mstar) with the Philox pivot stream.
+ * h~(a,b) = exp(beta/tau^2 <a-kbar, b-kbar> - mstar) with the Philox pivot stream
+ * (opts->block >= 2: the blocked variant, see wc_opts.block).
  * Writes S, r_eff, L, stats.  Outputs S, r_eff, L, stats are required. */
 int wildcat_select(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *K,
                    int32_t *S, int32_t *r_eff, double *L, double *stats,

@@ -27,8 +27,11 @@ __all__ = ["forward", "forward_host", "select", "weights", "attend", "Selection"
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range"]
 
 
+STATS_HEAD = 16  # tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, 0 x 7; then kbar[d]
+
+
 def STATS_STRIDE(d: int) -> int:
-    return 8 + d
+    return STATS_HEAD + d
 
 
 def _require_cuda(*ts):
@@ -46,7 +49,7 @@ class Selection:
     S: torch.Tensor       # int32 [units, r]
     r_eff: torch.Tensor   # int32 [units]
     L: torch.Tensor       # float64 [units, r, r]
-    stats: torch.Tensor   # float64 [units, 8 + d]: tau, g, mstar, R_K, R_Q, T0, -, -, kbar
+    stats: torch.Tensor   # float64 [units, 16 + d]: tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, ..., kbar
     shape: B.wc_shape
     opts: B.wc_opts
 
@@ -75,11 +78,12 @@ def _workspace(shape, op, device):
     return t
 
 
-def select(Q, K, r, seed=0, beta=None, rq=None, stream=None) -> Selection:
+def select(Q, K, r, seed=0, beta=None, rq=None, block=1, stream=None) -> Selection:
+    """RPNys selection; block >= 2 selects the blocked (accelerated) variant (reading Z22)."""
     Q, K = _cont(Q), _cont(K)
     _require_cuda(Q, K)
     shape = B.make_shape(Q, K, r)
-    opts = B.make_opts(seed, beta, rq)
+    opts = B.make_opts(seed, beta, rq, block=block)
     units = shape.batch * shape.heads_kv
     dev = K.device
     S = torch.empty(units, r, dtype=torch.int32, device=dev)
@@ -115,26 +119,28 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
                        dtype=B._dtype_code(Q), reserved=0, m=m, n=max(r, 1))
     opts = B.wc_opts(beta=cache.opts.beta if beta is None else float(beta), rq=cache.opts.rq,
                      seed=cache.opts.seed,
-                     flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), reserved=0)
+                     flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), block=0)
     O = torch.empty_like(Q)
     ws = _workspace(shape, B.WC_OP_ATTEND, Q.device) if B.workspace_bytes(shape, B.WC_OP_ATTEND) else None
     B.wildcat_attend(shape, opts, Q, cache.KS, cache.X, cache.r_eff, cache.vmin, cache.vmax, O, ws, stream)
     return O
 
 
-def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None, r_eff=None, stream=None):
-    """Alg 4 WildCat on device tensors.  Returns O (and fills S / r_eff if given)."""
+def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None, r_eff=None, block=1,
+            stream=None):
+    """Alg 4 WildCat on device tensors.  Returns O (and fills S / r_eff if given).
+    block >= 2: blocked (accelerated) RPCholesky selection with b = block (reading Z22)."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     shape = B.make_shape(Q, K, r)
-    opts = B.make_opts(seed, beta, rq, clip)
+    opts = B.make_opts(seed, beta, rq, clip, block=block)
     O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD, K.device)
     B.wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O
 
 
-def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", stream=None):
+def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, stream=None):
     """End-to-end call with host (CPU) buffers: H2D copies, the CUDA forward, D2H copy of O."""
     dev = torch.device(device)
     s = torch.cuda.current_stream(dev) if stream is None else stream
@@ -142,7 +148,7 @@ def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda
         Qd = Q.to(dev, non_blocking=True)
         Kd = K.to(dev, non_blocking=True)
         Vd = V.to(dev, non_blocking=True)
-        Od = forward(Qd, Kd, Vd, r, seed=seed, beta=beta, rq=rq, clip=clip, stream=s)
+        Od = forward(Qd, Kd, Vd, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, stream=s)
         O = torch.empty(Od.shape, dtype=Od.dtype, pin_memory=True)
         O.copy_(Od, non_blocking=True)
     s.synchronize()

@@ -33,7 +33,7 @@ class wc_shape(ctypes.Structure):
 
 class wc_opts(ctypes.Structure):
     _fields_ = [("beta", ctypes.c_double), ("rq", ctypes.c_double), ("seed", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("block", ctypes.c_uint32)]
 
 
 _lib = None
@@ -106,9 +106,9 @@ def make_shape(Q, K, r, m=None) -> wc_shape:
                     reserved=0, m=mm, n=n)
 
 
-def make_opts(seed=0, beta=None, rq=None, clip=True) -> wc_opts:
+def make_opts(seed=0, beta=None, rq=None, clip=True, block=1) -> wc_opts:
     return wc_opts(beta=-1.0 if beta is None else float(beta), rq=-1.0 if rq is None else float(rq),
-                   seed=int(seed) & 0xFFFFFFFFFFFFFFFF, flags=0 if clip else WC_NO_CLIP, reserved=0)
+                   seed=int(seed) & 0xFFFFFFFFFFFFFFFF, flags=0 if clip else WC_NO_CLIP, block=int(block))
 
 
 def _stream(stream):

@@ -9,6 +9,8 @@
 #include "../../include/wildcat.h"
 #include "kernels.h"
 
+static_assert(WC_STATS_HEAD == wc::kStatsHead, "stats layout of include/wildcat.h and the kernels differ");
+
 namespace {
 
 thread_local int g_launches = 0;
@@ -72,6 +74,24 @@ double beta_of(const wc_shape *s, const wc_opts *o) {
 double rq_of(const wc_opts *o) {
     if (!o || std::isnan(o->rq) || o->rq < 0.0) return -1.0;
     return o->rq;
+}
+
+// Selection dispatch: sequential Alg 1, or the blocked variant when opts->block >= 2.
+int run_select(const wc::Dims &D, const wc_opts *o, const void *K, double *stats, wc::SelectBufs sb, int32_t *S,
+               int32_t *r_eff, double *L, cudaStream_t st) {
+    if (o->block >= 2) {
+        const int k = wc::launch_select_blocked(D, K, stats, sb, o->seed, (int)o->block, S, r_eff, L, st);
+        return k == -2 ? WC_EUNSUPPORTED : (k < 0 ? WC_ECUDA : k);
+    }
+    const int k = wc::launch_select(D, K, stats, sb, o->seed, S, r_eff, L, st);
+    return k < 0 ? WC_ECUDA : k;
+}
+
+int check_opts(const wc_opts *o, const wc_shape *s) {
+    if (!o) return WC_EINVAL;
+    if (o->block > (uint32_t)WC_MAX_BLOCK) return WC_EINVAL;
+    if (o->block >= 2 && s->r > 1024) return WC_EUNSUPPORTED;
+    return WC_OK;
 }
 
 struct SelectWs {
@@ -180,6 +200,7 @@ int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     int rc = check_shape(s);
     if (rc) return rc;
     if (!o || !K || !S || !r_eff || !L || !stats) return WC_EINVAL;
+    if ((rc = check_opts(o, s))) return rc;
     const double rq = rq_of(o);
     if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_SELECT)))) return rc;
@@ -195,8 +216,8 @@ int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     int n1 = wc::launch_prologue(D, Q, K, nullptr, rq, beta_of(s, o), w.pp, stats, w.sb.nrm2, nullptr, nullptr, st);
     if (n1 < 0) return WC_ECUDA;
     tmark(st);
-    int n2 = wc::launch_select(D, K, stats, w.sb, o->seed, S, r_eff, L, st);
-    if (n2 < 0) return WC_ECUDA;
+    int n2 = run_select(D, o, K, stats, w.sb, S, r_eff, L, st);
+    if (n2 < 0) return n2;
     tmark(st);
     return finish(n1 + n2);
 }
@@ -246,6 +267,7 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     int rc = check_shape(s);
     if (rc) return rc;
     if (!o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
+    if ((rc = check_opts(o, s))) return rc;
     const double rq = rq_of(o);
     if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD)))) return rc;
@@ -275,7 +297,7 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     if ((k = wc::launch_prologue(D, Q, K, V, rq, beta, w.pp, stats, w.sb.nrm2, vmin, vmax, st)) < 0) return WC_ECUDA;
     total += k;
     tmark(st);
-    if ((k = wc::launch_select(D, K, stats, w.sb, o->seed, S, reff, L, st)) < 0) return WC_ECUDA;
+    if ((k = run_select(D, o, K, stats, w.sb, S, reff, L, st)) < 0) return k;
     total += k;
     tmark(st);
     if ((k = wc::launch_weights(D, K, V, S, reff, L, stats, Ypart, KS, X, st)) < 0) return WC_ECUDA;
@@ -307,6 +329,7 @@ int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int6
     if (rc) return rc;
     if (!comm || !o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
     if (s->batch != 1 || s->heads_kv != 1) return WC_EUNSUPPORTED;
+    if (o->block >= 2) return WC_EUNSUPPORTED;  // blocked selection is single-GPU in this build
     if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;
     const double rq = rq_of(o);
@@ -349,6 +372,6 @@ int wc_timing_read(float *ms, int cap) {
     return k;
 }
 
-int wc_version(void) { return 100; }
+int wc_version(void) { return 101; }
 
 }  // extern "C"

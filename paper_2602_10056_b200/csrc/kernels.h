@@ -5,6 +5,10 @@
 
 namespace wc {
 
+// Per-unit stats record: tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, 0..., kbar[d]
+// (WC_STATS_STRIDE(d) = kStatsHead + d in include/wildcat.h).
+constexpr int kStatsHead = 16;
+
 struct Dims {
     int batch, hq, hkv, d, r, dtype;
     int64_t m, n;
@@ -24,7 +28,7 @@ struct ProloguePartials {
 
 int prologue_num_splits(const Dims &D);
 
-// A0: kbar, R_K, R_Q, tau, g, mstar -> stats[u][8+d]; nrm2[u][l] = ||k_l - kbar||^2;
+// A0: kbar, R_K, R_Q, tau, g, mstar -> stats[u][kStatsHead+d]; nrm2[u][l] = ||k_l - kbar||^2;
 // vmin/vmax (dtype) when non-null.  Returns number of launches (>0) or -1 on error.
 int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
                     ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
@@ -66,6 +70,12 @@ int select_ctas_per_unit(const Dims &D);
 // A1+A2: r rounds of RP-Cholesky.  Returns launches or -1.
 int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed,
                   int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
+
+// Blocked (accelerated) RPC, 2 <= block <= select_blocked_max_block().  Returns launches, -1 on a
+// CUDA error, -2 when r does not fit the shared-memory plan.  stats[u][6..8] <- nblocks, ncand, Fread.
+int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBufs b, uint64_t seed, int block,
+                          int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
+int select_blocked_max_block();
 
 int weights_num_splits(const Dims &D);
 // A3+A4: X = L^{-T} L^{-1} h~(K_S,K)[V,1]; KS gather.  Ypart: [units][splits][r][d+1] fp32.

@@ -97,7 +97,7 @@ template <typename T>
 __global__ void ns_pro_final1(int64_t n_global, int d, const double *sumbuf, const double *maxbuf, double *stats,
                               T *vmin, T *vmax) {
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
-        stats[8 + j] = sumbuf[j] / (double)n_global;
+        stats[kStatsHead + j] = sumbuf[j] / (double)n_global;
         vmin[j] = from_f32<T>((float)(-maxbuf[1 + j]));
         vmax[j] = from_f32<T>((float)maxbuf[1 + d + j]);
     }
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(kNuT) ns_update(int i, int r, int64_t n, int64
     const int64_t s_glob = (int64_t)packet[0];
     const double ps = packet[1];
     for (int j = tid; j < D; j += kNuT) {
-        kb[j] = stats[8 + j];
-        kcs[j] = __dadd_rn(packet[2 + j], -stats[8 + j]);
+        kb[j] = stats[kStatsHead + j];
+        kcs[j] = __dadd_rn(packet[2 + j], -stats[kStatsHead + j]);
     }
     for (int j = tid; j < i; j += kNuT) fs[j] = packet[2 + D + j];
     __syncthreads();
@@ -398,7 +398,7 @@ size_t ns_carve(const Dims &D, void *base, NsWs &w) {
     w.pp.vmax = c.take<float>((size_t)P * D.d);
     w.pp.rq2 = c.take<double>(P);
     w.pp.rk2 = c.take<double>(P);
-    w.stats = c.take<double>(8 + D.d);
+    w.stats = c.take<double>(kStatsHead + D.d);
     w.nrm2 = c.take<double>(D.n);
     w.p = c.take<double>(D.n);
     w.F = c.take<double>((size_t)D.r * D.n);

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, co
             aa = fminf(aa, s_a[gg * d + j]);
             bb = fmaxf(bb, s_b[gg * d + j]);
         }
-        if (stats) stats[(int64_t)u * (8 + d) + 8 + j] = tt / (double)n;
+        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = tt / (double)n;
         if (vmin) {
             vmin[(int64_t)u * d + j] = from_f32<T>(aa);
             vmax[(int64_t)u * d + j] = from_f32<T>(bb);
@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
     const int p = blockIdx.x, u = blockIdx.y;
     const int CPR = d / 8, RG = kPT / CPR;
     const int rg = threadIdx.x / CPR, cj = threadIdx.x % CPR;
-    const double *st = stats + (int64_t)u * (8 + d);
-    for (int j = threadIdx.x; j < d; j += kPT) kb[j] = st[8 + j];
+    const double *st = stats + (int64_t)u * (kStatsHead + d);
+    for (int j = threadIdx.x; j < d; j += kPT) kb[j] = st[kStatsHead + j];
     __syncthreads();
     const int64_t rows = ceil_div(n, P);
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
@@ -189,15 +189,13 @@ __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *r
         tau = sqrt((rk / rq) * b0 / (2.0 * w));
     }
     const double g = beta / (tau * tau);
-    double *st = stats + (int64_t)u * (8 + d);
+    double *st = stats + (int64_t)u * (kStatsHead + d);
     st[0] = tau;
     st[1] = g;
     st[2] = g * rk * rk;
     st[3] = rk;
     st[4] = rq;
-    st[5] = 0.0;
-    st[6] = 0.0;
-    st[7] = 0.0;
+    for (int k = 5; k < kStatsHead; ++k) st[k] = 0.0;
 }
 
 template <typename T>

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "select_common.cuh"
 
 namespace wc {
 
@@ -63,8 +64,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && i < a.r) a.trace[i * 16 + (k)] = gtimer(); \
     } while (0)
 
-constexpr int kST = 256;  // keys per super-tile (8 warp-tiles of 32 keys)
-constexpr int kTK = kST / 32;
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
@@ -87,14 +86,14 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
-    const double *st = a.stats + (int64_t)u * (8 + D);
+    const double *st = a.stats + (int64_t)u * (kStatsHead + D);
     const double g = st[1], mstar = st[2];
     double *p0 = a.p + (int64_t)u * n;
     double *p1 = a.p + ((int64_t)a.units + u) * n;
     double *Fu = a.F + (int64_t)u * a.r * a.ldF;
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
     unsigned *bar = a.bar + u;
-    for (int j = tid; j < D; j += nt) kb[j] = st[8 + j];
+    for (int j = tid; j < D; j += nt) kb[j] = st[kStatsHead + j];
 
     // p <- kernel diagonal h~(k_l, k_l) = exp(g ||k_l - kbar||^2 - mstar)   (Alg 1)
     double loc = 0.0;
@@ -291,7 +290,11 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     }
     if (c == 0 && tid == 0) {
         a.r_eff[u] = i;
-        const_cast<double *>(st)[5] = T0;
+        double *stw = const_cast<double *>(st);
+        stw[5] = T0;
+        stw[6] = (double)i;                          // rounds run
+        stw[7] = (double)i;                          // pivots drawn
+        stw[8] = 0.5 * (double)i * (double)(i - 1);  // F rows re-read: sum over rounds q of q
     }
 }
 
@@ -305,105 +308,6 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
 // this CTA in the previous round) is read directly.  Compute warps synchronise among themselves
 // with named barrier 1 so the producer never joins a CTA-wide barrier.
 // =====================================================================================
-constexpr int kCW = 8;                // compute warps
-constexpr int kCT = kCW * 32;         // compute threads (= kST: one key per thread in phases B/C)
-constexpr int kRPS = 8;               // F rows per ring stage (one per compute warp)
-constexpr int kTmaThreads = kCT + 32; // + producer warp
-static_assert(kCT == kST, "one compute thread per super-tile key");
-
-__device__ __forceinline__ void cw_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory"); }
-
-__device__ __forceinline__ double cw_sum(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, w = warp_index();
-    v = warp_sum(v);
-    cw_sync();
-    if (lane == 0) scratch[w] = v;
-    cw_sync();
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < kCW; ++k) t += scratch[k];
-    cw_sync();
-    return t;
-}
-
-__device__ __forceinline__ double cw_exclusive_scan(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, w = warp_index();
-    double incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const double wtot = __shfl_sync(0xffffffffu, incl, 31);
-    cw_sync();
-    if (lane == 0) scratch[w] = wtot;
-    cw_sync();
-    double off = 0.0;
-    for (int k = 0; k < w; ++k) off += scratch[k];
-    const double excl = off + (incl - v);
-    cw_sync();
-    return excl;
-}
-
-// Grid-group barrier of the compute threads: bar.sync orders the CTA's writes before thread 0's
-// release-add (release is cumulative); the acquire-load orders everything after.  Thread 0 then
-// publishes `rounds` (this CTA's F rows complete) to the producer warp.
-__device__ __forceinline__ void cw_group_barrier(unsigned *ctr, unsigned count, unsigned epoch,
-                                                 volatile int *rounds_done, int rounds) {
-    cw_sync();
-    if (threadIdx.x == 0) {
-        if (count > 1) {
-            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
-            const unsigned target = epoch * count;
-            unsigned v;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-                if (v >= target) break;
-                __nanosleep(20);
-            }
-        } else {
-            __threadfence();
-        }
-        *rounds_done = rounds;
-    }
-    cw_sync();
-}
-
-// Raw K row of one key kept in registers (issued early, consumed after the pivot is known).
-template <typename T, int D> struct KRow {
-    static constexpr int kVec = D * (int)sizeof(T) / 16;  // 16-byte vectors per row
-    static constexpr int kEl = 16 / (int)sizeof(T);        // elements per vector
-    uint4 v[kVec];
-    __device__ __forceinline__ void load(const T *row) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(row);
-#pragma unroll
-        for (int q = 0; q < kVec; ++q) v[q] = __ldg(p + q);
-    }
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int q = 0; q < kVec; ++q) v[q] = make_uint4(0, 0, 0, 0);
-    }
-    // part[e % 4] += k_j * kc_j over the row (fp64, exact widening of k)
-    __device__ __forceinline__ void dot(const double *kc, double part[4]) const { dot_range<0, kVec>(kc, part); }
-    // vectors [Q0, Q1) only (compile-time range: the row stays in registers)
-    template <int Q0, int Q1> __device__ __forceinline__ void dot_range(const double *kc, double part[4]) const {
-#pragma unroll
-        for (int q = Q0; q < Q1; ++q) {
-            const uint32_t wd[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-            if constexpr (sizeof(T) == 2) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const uint32_t bits = (e & 1) ? (wd[e >> 1] & 0xffff0000u) : (wd[e >> 1] << 16);
-                    part[e & 3] = fma((double)__uint_as_float(bits), kc[q * 8 + e], part[e & 3]);
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) part[e] = fma((double)__uint_as_float(wd[e]), kc[q * 4 + e], part[e]);
-            }
-        }
-    }
-};
-
 template <typename T, int D>
 __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs a, int NS) {
     using KR = KRow<T, D>;
@@ -429,7 +333,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
     const int nst = (int)ceil_div(hi - lo, kST);
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
-    const double *st = a.stats + (int64_t)u * (8 + D);
+    const double *st = a.stats + (int64_t)u * (kStatsHead + D);
     // tile-major F: CTA c' owns [r x chunk]; its super-tile k' is the block [r][w_k'] at column
     // offset 256 k', w_k' = min(256, chunk - 256 k') (a multiple of 32): 8 rows = one contiguous copy
     double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
@@ -491,7 +395,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
     const double g = st[1], mstar = st[2];
     double *p0 = a.p + (int64_t)u * n;
     double *p1 = a.p + ((int64_t)a.units + u) * n;
-    for (int j = tid; j < D; j += kCT) kb[j] = st[8 + j];
+    for (int j = tid; j < D; j += kCT) kb[j] = st[kStatsHead + j];
 
     double loc = 0.0;
     double p_first = 0.0;  // residual of this thread's key in super-tile 0 (kept in a register)
@@ -754,7 +658,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
     if (tid == 0) sh_stop = 1;
     if (c == 0 && tid == 0) {
         a.r_eff[u] = i;
-        const_cast<double *>(st)[5] = T0;
+        double *stw = const_cast<double *>(st);
+        stw[5] = T0;
+        stw[6] = (double)i;                          // rounds run
+        stw[7] = (double)i;                          // pivots drawn
+        stw[8] = 0.5 * (double)i * (double)(i - 1);  // F rows re-read: sum over rounds q of q
     }
 }
 

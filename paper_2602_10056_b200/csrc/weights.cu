@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
     const int re = r_eff[u];
     if (a0 >= re) return;  // whole tile beyond r_eff: partials unused by the solve
     const int tid = threadIdx.x;
-    const double *st = stats + (int64_t)u * (8 + D);
+    const double *st = stats + (int64_t)u * (kStatsHead + D);
     const float g = (float)st[1], mstar = (float)st[2];
-    for (int j = tid; j < D; j += kWT) kb[j] = st[8 + j];
+    for (int j = tid; j < D; j += kWT) kb[j] = st[kStatsHead + j];
     __syncthreads();
     const T *Ku = K + (int64_t)u * n * D;
     const T *Vu = V + (int64_t)u * n * D;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kWTc, 1)
     if (a0 >= re) return;  // uniform per CTA
     const __nv_bfloat16 *Ku = K + (int64_t)u * n * D;
     const __nv_bfloat16 *Vu = V + (int64_t)u * n * D;
-    const double *st = stats + (int64_t)u * (8 + D);
+    const double *st = stats + (int64_t)u * (kStatsHead + D);
     const double g = st[1], mstar = st[2];
     constexpr int CPR = D / 8;
     constexpr float kLog2e = 1.4426950408889634f;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kWTc, 1)
         mbar_init(&bar, 1);
         fence_mbar_init();
     }
-    for (int j = tid; j < D; j += kWTc) sKb[j] = (float)st[8 + j];
+    for (int j = tid; j < D; j += kWTc) sKb[j] = (float)st[kStatsHead + j];
     // coreset rows (raw keys) -> A operand
     for (int e = tid; e < 128 * CPR; e += kWTc) {
         const int rw = e / CPR, cc = e % CPR;
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kWTc, 1)
                                           : Ku + (int64_t)S[(int64_t)u * r + a0 + row] * D;
         double kk = 0.0, bb = 0.0;
         for (int j = 0; j < D; ++j) {
-            const double kbj = st[8 + j];
+            const double kbj = st[kStatsHead + j];
             kk = fma(to_f64(ksrow[j]), kbj, kk);
             bb = fma(kbj, kbj, bb);
         }

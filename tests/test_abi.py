@@ -93,3 +93,17 @@ def test_product_package_has_no_oracle_dependency():
             if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "wildcat_oracle" not in txt, fn
+
+
+def test_block_option_validation(L):
+    from paper_2602_10056_b200 import _binding as B
+
+    assert ctypes.sizeof(B.wc_opts) == 32
+    d = ctypes.c_void_p(0x1000)
+    s = _shape()
+    o = B.make_opts(block=17)  # > WC_MAX_BLOCK
+    assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -1
+    big = _shape(n=5000, r=1025)
+    o = B.make_opts(block=8)  # blocked selection needs r <= 1024
+    assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -7
+    assert L.wc_version() >= 101
