@@ -114,6 +114,8 @@ void carve_select(Carver &c, const wc_shape *s, SelectWs &w) {
     w.sb.F = c.take<double>(U * wc::f_elems_per_unit(D.n, D.r, wc::select_ctas_per_unit(D)));
     w.sb.part = c.take<double>(U * 2 * wc::kMaxCpu);
     w.sb.bar = c.take<unsigned>(U);
+    w.sb.gsum = c.take<double>(U * 2 * (size_t)((D.n + 31) / 32));
+    w.sb.FT = c.take<double>(U * (size_t)D.n * wc::ft_ld(D.r));
 }
 
 float *carve_weights(Carver &c, const wc_shape *s, wc::ProloguePartials *pp) {

@@ -245,6 +245,12 @@ __device__ __forceinline__ void st_f64_hint(double *p, double v, uint64_t policy
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS, L1-allocating) and the wait for all of them.
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Order this thread's generic-proxy global writes before later async-proxy (TMA) reads.
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 

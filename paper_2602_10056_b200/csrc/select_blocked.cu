@@ -64,6 +64,8 @@ struct BlkArgs {
     double *F;      // per unit tile-major [cpu][nst][r][256]
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
+    double *gsum;   // [units][2][ngroups] residual sums of 32-key groups
+    double *FT;     // [units][n][ft_ld(r)] key-major F: candidate columns are contiguous rows
     int32_t *S;
     int32_t *r_eff;
     double *L;
@@ -83,59 +85,118 @@ __device__ __forceinline__ unsigned long long btimer() {
         if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + (k)] = btimer(); \
     } while (0)
 
+constexpr int kBT = 512;          // keys per super-tile of the blocked kernel (64 per compute warp)
+constexpr int kBR = 4;            // F rows per ring stage (one DMMA k-step)
+constexpr int kPitch = kBT + 8;   // ring row pitch in doubles (4160 B): odd rows sit 16 banks over
+
+// fp64 tensor-core MMA (DMMA) m8n8k4: C += A B with A 8x4 row-major (lane l holds A[l/4][l%4]),
+// B 4x8 column-major (lane l holds B[l%4][l/4]), C 8x8 (lane l holds C[l/4][2(l%4) + {0,1}]).
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+// MMA-operand layouts of the accepted (or candidate) pivot columns, 16 pivot slots p:
+//   Fcol: F[q, s_p] (candidate slot p) as 16 columns of stride ldc = 16k + 4 doubles: lane (tq, g)
+//        of the k-step at q0 reads Fcol[(8 nt + g) * ldc + q0 + tq] -- two wavefronts per warp load;
+//   kcB: centred key k_sp - kbar at dim = tq * (D/4) + t (lane tq owns a contiguous run of D/4 dims).
+template <int D> __device__ __forceinline__ int kcb(int dim, int p) {
+    constexpr int DQ = D / 4;
+    return (((dim % DQ) * 2 + (p >> 3)) * 4 + dim / DQ) * 8 + (p & 7);
+}
+
+// TC consecutive raw key elements of one row held as 32-bit words; elem() widens exactly to fp64.
+template <typename T, int TC> struct KChunk {
+    static constexpr int kWords = TC * (int)sizeof(T) / 4;
+    uint32_t w[kWords];
+    __device__ __forceinline__ void load(const T *p) {
+        if constexpr (kWords == 2) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+            w[0] = v.x; w[1] = v.y;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kWords / 4; ++q) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p) + q);
+                w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+            }
+        }
+    }
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int q = 0; q < kWords; ++q) w[q] = 0u;
+    }
+    __device__ __forceinline__ double elem(int tt) const {
+        if constexpr (sizeof(T) == 2) {
+            const uint32_t x = w[tt >> 1];
+            return (double)__uint_as_float((tt & 1) ? (x & 0xffff0000u) : (x << 16));
+        } else {
+            return (double)__uint_as_float(w[tt]);
+        }
+    }
+};
+
 template <typename T, int D>
 __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
-    using KR = KRow<T, D>;
+    constexpr int DQ = D / 4;             // dims per lane per key in the kernel-dot MMA
+    constexpr int TC = 4;                 // k-steps per register chunk of the K row (8 or 16 bytes per key)
+    using KC = KChunk<T, TC>;
     extern __shared__ __align__(128) unsigned char smraw[];
-    double *ring = reinterpret_cast<double *>(smraw);  // [NS][kRPS][kST]
-    double *FsT = ring + (size_t)NS * kRPS * kST;       // [r][kBMax]   F[q, s] of the candidates / accepted
-    double *kcT = FsT + (size_t)a.r * kBMax;            // [D][kBMax]   centred candidate keys (fp64)
-    double *Hw = kcT + D * kBMax;                        // [kBMax][kBMax] working H (Schur updates)
-    double *H0 = Hw + kBMax * kBMax;                     // [kBMax][kBMax] block-start H
-    double *Fx = H0 + kBMax * kBMax;                     // [kBMax][kBMax] Fx[x][a] = F[i+a, s_x]
-    double *cp = Fx + kBMax * kBMax;                     // [kBMax] block-start p[s_j]
-    double *c0r = cp + kBMax;                            // [kBMax] <kbar, k_sj - kbar> per candidate
-    double *c0 = c0r + kBMax;                            // [kBMax] ... per accepted pivot (0-padded)
-    double *rsp = c0 + kBMax;                            // [kBMax] sqrt(p_{s_a}) at round i+a
-    double *vac = rsp + kBMax;                           // [kBMax] accept uniforms
-    double *kb = vac + kBMax;                            // [D]
-    double *scr = kb + D;                                // [40]
-    int *cs = reinterpret_cast<int *>(scr + 40);         // [kBMax] candidates
-    int *sA = cs + kBMax;                                // [kBMax] accepted pivots (in order)
-    int *jA = sA + kBMax;                                // [kBMax] their candidate slots
-    uint64_t *full = reinterpret_cast<uint64_t *>(jA + kBMax);
+    const int ldc = ((a.r + 15) & ~15) + 4;
+    const int ftl = ft_ld(a.r);
+    double *ring = reinterpret_cast<double *>(smraw);  // [NS][kBR][kPitch]
+    double *Fcol = ring + (size_t)NS * kBR * kPitch;    // [16][ldc] candidate columns of F
+    double *kcB = Fcol + (size_t)kBMax * ldc;           // [D][16]    (MMA layout, see kcb)
+    double *H0 = kcB + D * kBMax;                       // [16][16] block-start H of the candidates
+    double *Fcand = H0 + kBMax * kBMax;                 // [16][16] Fcand[aa][x] = F[i+aa, s_x] (candidate x)
+    double *Fx = Fcand + kBMax * kBMax;                 // [16][16] Fx[aa][a2] = F[i+a2, s_aa] (accepted order)
+    double *rowj = Fx + kBMax * kBMax;                  // [2][16]  row j of the eliminated H
+    double *cp = rowj + 2 * kBMax;                      // [16] block-start p[s_j]
+    double *c0r = cp + kBMax;                           // [16] <kbar, k_sj - kbar> per candidate
+    double *c0 = c0r + kBMax;                           // [16] ... per accepted pivot (0-padded)
+    double *vac = c0 + kBMax;                           // [16] accept uniforms
+    double *rinvA = vac + kBMax;                        // [16] 1 / sqrt(p_{s_aa}) at round i+aa
+    double *kb = rinvA + kBMax;                         // [D]
+    double *scr = kb + D;                               // [40]
+    double *Hp = scr + 40;                              // [8][4][32][2] per-warp DMMA partials of H
+    double *spart = Hp + kCW * 4 * 64;                  // [cpu] per-CTA residual sums (block start)
+    double *sv = spart + a.cpu;                         // [32] lane sums of spart (warp-0 partition)
+    double *sinc = sv + 32;                             // [32] their inclusive prefix
+    long long *cfo = reinterpret_cast<long long *>(sinc + 32);  // [16] offset of F[0, s_j] in the unit's F
+    int *cs = reinterpret_cast<int *>(cfo + kBMax);     // [16] candidates
+    int *cwk = cs + kBMax;                              // [16] row stride of F at s_j
+    int *sA = cwk + kBMax;                              // [16] accepted pivots (in order)
+    int *jA = sA + kBMax;                               // [16] their candidate slots
+    int *perm = jA + kBMax;                             // [16] slot -> acceptance index (-1: rejected)
+    uint64_t *full = reinterpret_cast<uint64_t *>(perm + kBMax);
     uint64_t *empty = full + NS;
+    uint64_t *colbar = empty + NS;  // completion of the candidate-column bulk copies
     __shared__ volatile int sh_stop;
-    __shared__ volatile long long sh_req;  // (block + 1) << 32 | rows to stream
+    __shared__ volatile long long sh_req;  // request number << 32 | super-tile << 16 | F rows to stream
     __shared__ volatile int sh_dummy;
     __shared__ int sh_na;
 
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
+    const int gid = lane >> 2, tq = lane & 3;
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
     const int64_t n = a.n;
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
-    const int nst = (int)ceil_div(hi - lo, kST);
+    const int nst = (int)ceil_div(hi - lo, kBT);
     const int bsz = a.b;
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
     double *st = a.stats + (int64_t)u * (kStatsHead + D);
     double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
     double *Fc = Fu + (int64_t)c * chunk * a.r;
-    auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(kST, chunk - (int64_t)k * kST); };
-    // address of F[q, key] in the tile-major layout
-    auto fptr = [&](int q, int64_t key) -> const double * {
-        const int64_t cc = key / chunk, off = key - cc * chunk;
-        const int kk = (int)(off / kST);
-        const int64_t wk = std::min<int64_t>(kST, chunk - (int64_t)kk * kST);
-        return Fu + cc * chunk * a.r + (int64_t)kk * kST * a.r + (int64_t)q * wk + (off % kST);
-    };
+    auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(kBT, chunk - (int64_t)k * kBT); };
 
     if (tid == 0) {
         for (int q = 0; q < NS; ++q) {
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], kCW);
         }
+        mbar_init(colbar, 1);
         sh_stop = 0;
         sh_req = 0;
         fence_mbar_init();
@@ -143,30 +204,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     __syncthreads();  // the only CTA-wide barrier: everything after is role-specific
 
     if (w == kCW) {
-        // ================= producer warp: streams F[0:i, own slice] once per block =================
+        // ============ producer warp: streams F[0:i, own slice] once per block (one bulk copy per row) ============
         if (lane == 0) {
             int stage = 0;
             uint32_t ph = 0, issued = 0, par = 0;
             long long seen = 0;
+            const uint64_t pol = policy_evict_first();
             while (true) {
                 long long req;
                 while (((req = sh_req) >> 32) == seen) {
                     if (sh_stop) goto drain;
-                    __nanosleep(32);
+                    __nanosleep(64);
                 }
                 seen = req >> 32;
-                const int rows = (int)(req & 0xffffffffLL);
-                for (int k = 0; k < nst; ++k) {
-                    const double *blk = Fc + (int64_t)k * a.r * kST;
+                const int rows = (int)(req & 0xffffLL), k = (int)((req >> 16) & 0xffffLL);
+                {
+                    const double *blk = Fc + (int64_t)k * a.r * kBT;
                     const int wk = tile_w(k);
-                    for (int j0 = 0; j0 < rows; j0 += kRPS) {
-                        const int nr = min(kRPS, rows - j0);
-                        const uint32_t bytes = (uint32_t)(nr * wk * sizeof(double));
+                    const uint32_t rb = (uint32_t)(wk * sizeof(double));
+                    for (int j0 = 0; j0 < rows; j0 += kBR) {
+                        const int nr = min(kBR, rows - j0);
                         while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
                             if (sh_stop) goto drain;
+                            __nanosleep(128);  // ring full: do not steal issue slots from warp 0 (same SMSP)
                         }
-                        mbar_arrive_expect_tx(&full[stage], bytes);
-                        bulk_g2s(ring + (size_t)stage * kRPS * kST, blk + (int64_t)j0 * wk, bytes, &full[stage]);
+                        mbar_arrive_expect_tx(&full[stage], rb * (uint32_t)nr);
+                        double *dst = ring + (size_t)stage * kBR * kPitch;
+                        for (int rr = 0; rr < nr; ++rr)  // F streams through L2 evict-first (K, p stay)
+                            bulk_g2s_hint(dst + rr * kPitch, blk + (int64_t)(j0 + rr) * wk, rb, &full[stage], pol);
                         issued |= 1u << stage;
                         par = (par & ~(1u << stage)) | (ph << stage);
                         if (++stage == NS) { stage = 0; ph ^= 1u; }
@@ -187,12 +252,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
     for (int j = tid; j < D; j += kCT) kb[j] = st[kStatsHead + j];
 
-    // p <- kernel diagonal h~(k_l, k_l) (Alg 1)
+    // p <- kernel diagonal h~(k_l, k_l) (Alg 1); 32-key group sums (one warp per group)
     double loc = 0.0;
-    for (int64_t l = lo + tid; l < hi; l += kCT) {
-        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
-        p0[l] = v;
-        loc += v;
+    {
+        const int ngr0 = (int)((n + 31) / 32);
+        double *g0s = a.gsum + (int64_t)u * 2 * ngr0;
+        for (int64_t gb = lo + 32 * w; gb < hi; gb += kCT) {
+            const int64_t l = gb + lane;
+            double v = 0.0;
+            if (l < hi) {
+                v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
+                p0[l] = v;
+            }
+            v = warp_sum(v);
+            if (lane == 0) g0s[gb / 32] = v;
+            loc += lane == 0 ? v : 0.0;
+        }
     }
     loc = cw_sum(loc, scr);
     if (tid == 0) partu[c] = loc;
@@ -205,324 +280,392 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     int i = 0, blk = 0;
     uint32_t cbase = 0;
     double fread = 0.0;
+    long long nreq = 0;  // requests published to the producer (thread 0)
+    int ncol = 0;        // candidate-column copy rounds (parity of colbar)
     while (i < a.r) {
         double *cur = (blk & 1) ? p1 : p0;
         double *nxt = (blk & 1) ? p0 : p1;
         const double *pc = partu + (blk & 1) * kMaxCpu;
         double *pn = partu + ((blk + 1) & 1) * kMaxCpu;
         WC_BTR(0);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + 12] = clock64();
 
-        // ---- 1a: total residual T over the per-CTA sums (every warp, identical fixed order)
+        // ---- 1a (warp 0): per-CTA residual sums -> shared memory (one L2 read per CTA), lane
+        // partition sums and their inclusive prefix, total T (fixed order)
+        const int ngr = (int)((n + 31) / 32);
+        const double *gcur = a.gsum + ((int64_t)u * 2 + (blk & 1)) * ngr;
+        double *gnxt = a.gsum + ((int64_t)u * 2 + ((blk + 1) & 1)) * ngr;
         const int per = (a.cpu + 31) / 32;
-        const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
-        constexpr int kPer = 8;  // fast path (cpu <= 256): the lane's CTA sums kept in registers
-        double pv[kPer];
-        double v = 0.0;
-        if (per <= kPer) {
+        if (w == 0) {
+            const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
+            double v = 0.0;
+            for (int cc = b0; cc < b1; ++cc) {
+                const double x = __ldcg(pc + cc);
+                spart[cc] = x;
+                v += x;
+            }
+            double incl = v;
 #pragma unroll
-            for (int q = 0; q < kPer; ++q) pv[q] = (b0 + q < b1) ? __ldcg(pc + b0 + q) : 0.0;
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) v += pv[q];
-        } else {
-            for (int cc = b0; cc < b1; ++cc) v += __ldcg(pc + cc);
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            sv[lane] = v;
+            sinc[lane] = incl;
         }
-        double incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const double Ttot = __shfl_sync(0xffffffffu, incl, 31);
+        cw_sync();
+        const double Ttot = sinc[31];
         if (blk == 0) {
             T0 = Ttot;
             theta = 1000.0 * (double)a.r * 2.220446049250313e-16 * T0;
         }
         if (Ttot <= theta) break;  // exhausted (reading Z3), tested at block starts
-        if (tid == 0) sh_req = ((long long)(blk + 1) << 32) | (long long)i;  // producer: stream F[0:i]
+        if (tid == 0) sh_req = ((long long)(++nreq) << 32) | (long long)i;  // producer: F[0:i] of super-tile 0
+        WC_BTR(10);
 
-        // ---- 1b: candidates, warp w draws j = w, w + 8 (Eq. 4 inverse CDF, strict '>')
-        for (int j = w; j < bsz; j += kCW) {
-            const double t = pivot_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u) * Ttot;
-            const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
-            const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
-            const int Ln = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
-            int cstar = 0;
-            double tp = 0.0;
-            if (lane == Ln) {
-                double acc = incl - v;
-                int csel = -1, last = -1;
-                double excl = 0.0, last_excl = 0.0;
-                for (int cc = b0; cc < b1; ++cc) {
-                    double pvv = 0.0;
-                    if (per <= kPer) {
-#pragma unroll
-                        for (int q = 0; q < kPer; ++q) pvv = (q == cc - b0) ? pv[q] : pvv;
-                    } else {
-                        pvv = __ldcg(pc + cc);
+        // ---- 1b: candidates, warp w draws j = w, w + 8 by the Eq. 4 inverse CDF with strict '>',
+        // hierarchically: owning CTA (prefix of CTA sums) -> 32-key group (prefix of the group sums
+        // of that CTA's slice) -> key (warp scan of the group's 32 residuals).  Each level falls back
+        // to its last positive entry if rounding leaves no crossing (reading Z2).
+        {
+            const double v = sv[lane], incl = sinc[lane];
+            const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
+            for (int j = w; j < bsz; j += kCW) {
+                const double t = pivot_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u) * Ttot;
+                // level 1: CTA
+                const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
+                const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
+                const int Ln = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
+                int cstar = 0;
+                double tp = 0.0;
+                if (lane == Ln) {
+                    double acc = incl - v;
+                    int csel = -1, last = -1;
+                    double excl = 0.0, last_excl = 0.0;
+                    for (int cc = b0; cc < b1; ++cc) {
+                        const double pvv = spart[cc];
+                        if (pvv > 0.0) { last = cc; last_excl = acc; }
+                        const double nacc = acc + pvv;
+                        if (csel < 0 && hit && nacc > t) { csel = cc; excl = acc; }
+                        acc = nacc;
                     }
-                    if (pvv > 0.0) { last = cc; last_excl = acc; }
-                    const double nacc = acc + pvv;
-                    if (csel < 0 && hit && nacc > t) { csel = cc; excl = acc; }
-                    acc = nacc;
+                    if (csel < 0) { csel = last; excl = last_excl; }
+                    cstar = csel;
+                    tp = t - excl;
                 }
-                if (csel < 0) { csel = last; excl = last_excl; }  // rounding fallback (reading Z2)
-                cstar = csel;
-                tp = t - excl;
-            }
-            cstar = __shfl_sync(0xffffffffu, cstar, Ln);
-            tp = __shfl_sync(0xffffffffu, tp, Ln);
-            // warp inverse CDF over c*'s slice of the block-start residual
-            const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
-            const int64_t shi = std::min<int64_t>(n, slo + chunk);
-            const int64_t per2 = ceil_div(shi - slo, 32);
-            const int64_t q0 = slo + (int64_t)lane * per2, q1 = std::min<int64_t>(shi, q0 + per2);
-            constexpr int kSl = 16;  // fast path (slice <= 512 keys): the lane's residuals in registers
-            double pr[kSl];
-            double v2 = 0.0;
-            if (per2 <= kSl) {
+                cstar = __shfl_sync(0xffffffffu, cstar, Ln);
+                tp = __shfl_sync(0xffffffffu, tp, Ln);
+                // level 2: 32-key group inside c*'s slice
+                const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
+                const int64_t shi = std::min<int64_t>(n, slo + chunk);
+                const int g0 = (int)(slo / 32), gn = (int)((shi - slo + 31) / 32);
+                const int gper = (gn + 31) / 32;
+                const int q0 = g0 + lane * gper, q1 = min(g0 + gn, q0 + gper);
+                constexpr int kG = 4;  // fast path: <= 128 groups per slice, kept in registers
+                double gv[kG];
+                double v2 = 0.0;
+                if (gper <= kG) {
 #pragma unroll
-                for (int q = 0; q < kSl; ++q) pr[q] = (q0 + q < q1) ? __ldcg(cur + q0 + q) : 0.0;
+                    for (int q = 0; q < kG; ++q) gv[q] = (q0 + q < q1) ? __ldcg(gcur + q0 + q) : 0.0;
 #pragma unroll
-                for (int q = 0; q < kSl; ++q) v2 += pr[q];
-            } else {
-                for (int64_t l = q0; l < q1; ++l) v2 += __ldcg(cur + l);
-            }
-            double inc2 = v2;
+                    for (int q = 0; q < kG; ++q) v2 += gv[q];
+                } else {
+                    for (int q = q0; q < q1; ++q) v2 += __ldcg(gcur + q);
+                }
+                double inc2 = v2;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, inc2, o);
-                if (lane >= o) inc2 += y;
-            }
-            double run = inc2 - v2;
-            int found = INT_MAX, lastpos = -1;
-            double fval = 0.0, lval = 0.0;
-            if (per2 <= kSl) {
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, inc2, o);
+                    if (lane >= o) inc2 += y;
+                }
+                const unsigned hit2 = __ballot_sync(0xffffffffu, q1 > q0 && inc2 > tp);
+                const unsigned pos2 = __ballot_sync(0xffffffffu, q1 > q0 && v2 > 0.0);
+                const int L2 = hit2 ? __ffs(hit2) - 1 : 31 - __clz(pos2);
+                int gstar = 0;
+                double tq2 = 0.0;
+                if (lane == L2) {
+                    double acc = inc2 - v2;
+                    int gsel = -1, last = -1;
+                    double excl = 0.0, last_excl = 0.0;
+                    for (int q = q0; q < q1; ++q) {
+                        double gg = 0.0;
+                        if (gper <= kG) {
 #pragma unroll
-                for (int q = 0; q < kSl; ++q) {
-                    if (q0 + q < q1) {
-                        const double pl = pr[q];
-                        if (pl > 0.0) { lastpos = (int)(q0 + q); lval = pl; }
-                        run += pl;
-                        if (found == INT_MAX && run > tp) { found = (int)(q0 + q); fval = pl; }
+                            for (int z = 0; z < kG; ++z) gg = (z == q - q0) ? gv[z] : gg;
+                        } else {
+                            gg = __ldcg(gcur + q);
+                        }
+                        if (gg > 0.0) { last = q; last_excl = acc; }
+                        const double nacc = acc + gg;
+                        if (gsel < 0 && hit2 && nacc > tp) { gsel = q; excl = acc; }
+                        acc = nacc;
                     }
+                    if (gsel < 0) { gsel = last; excl = last_excl; }
+                    gstar = gsel;
+                    tq2 = tp - excl;
                 }
-            } else {
-                for (int64_t l = q0; l < q1; ++l) {
-                    const double pl = __ldcg(cur + l);
-                    if (pl > 0.0) { lastpos = (int)l; lval = pl; }
-                    run += pl;
-                    if (found == INT_MAX && run > tp) { found = (int)l; fval = pl; }
+                gstar = __shfl_sync(0xffffffffu, gstar, L2);
+                tq2 = __shfl_sync(0xffffffffu, tq2, L2);
+                // level 3: key inside the group
+                const int64_t key = (int64_t)gstar * 32 + lane;
+                const double pl = key < shi ? __ldcg(cur + key) : 0.0;
+                double inc3 = pl;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, inc3, o);
+                    if (lane >= o) inc3 += y;
                 }
-            }
-            const int smin = __reduce_min_sync(0xffffffffu, found);
-            int s;
-            double psv;
-            if (smin != INT_MAX) {
-                s = smin;
-                const int src = __ffs(__ballot_sync(0xffffffffu, found == smin)) - 1;
-                psv = __shfl_sync(0xffffffffu, fval, src);
-            } else {  // rounding fallback (reading Z2): last key with positive residual
-                s = __reduce_max_sync(0xffffffffu, lastpos);
-                const int src = __ffs(__ballot_sync(0xffffffffu, lastpos == s)) - 1;
-                psv = __shfl_sync(0xffffffffu, lval, src);
-            }
-            if (lane == 0) {
-                cs[j] = s;
-                cp[j] = psv;
-                vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u);
+                const unsigned hit3 = __ballot_sync(0xffffffffu, inc3 > tq2);
+                const unsigned pos3 = __ballot_sync(0xffffffffu, pl > 0.0);
+                const int L3 = hit3 ? __ffs(hit3) - 1 : 31 - __clz(pos3);
+                const double psv = __shfl_sync(0xffffffffu, pl, L3);
+                if (lane == 0) {
+                    const int s = (int)(gstar * 32 + L3);
+                    cs[j] = s;
+                    cp[j] = psv;
+                    vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u);
+                    const int64_t cc = s / chunk, off = s - cc * chunk;
+                    const int kk = (int)(off / kBT);
+                    cfo[j] = cc * chunk * a.r + (int64_t)kk * kBT * a.r + (off % kBT);
+                    cwk[j] = (int)std::min<int64_t>(kBT, chunk - (int64_t)kk * kBT);
+                }
+                if (blk == 0 && j == 0) WC_BTR(11);
             }
         }
         cw_sync();
         WC_BTR(1);
 
-        // ---- 2: candidate data: centred keys (fp64), F[0:i, s_j] (gathered from L2)
+        // ---- 2: candidate data: the columns F[0:i, s_j] arrive as one bulk copy each from the
+        // key-major copy FT (written by the owner thread of each key in earlier blocks), overlapped
+        // with the centred candidate keys (fp64, MMA layout), their kernel dots on the tensor cores
+        // (warps 4-7) and c0; rows [i, i4) and unused slots of Fcol are zeroed.
+        const int i4 = (i + 3) & ~3;
+        if (tid == 0 && i > 0) {  // one bulk copy per candidate: its key-major F row FT[s_j][0:i4]
+            const double *FTu = a.FT + (int64_t)u * n * ftl;
+            mbar_arrive_expect_tx(colbar, (uint32_t)(bsz * i4 * sizeof(double)));
+            for (int j = 0; j < bsz; ++j)
+                bulk_g2s(Fcol + (size_t)j * ldc, FTu + (int64_t)cs[j] * ftl, (uint32_t)(i4 * sizeof(double)), colbar);
+        }
         for (int idx = tid; idx < bsz * D; idx += kCT) {
             const int j = idx / D, e = idx - j * D;
-            kcT[e * kBMax + j] = __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]);
+            kcB[kcb<D>(e, j)] = __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]);
         }
-#pragma unroll 4
-        for (int idx = tid; idx < bsz * i; idx += kCT) {
-            const int q = idx / bsz, j = idx - q * bsz;
-            FsT[q * kBMax + j] = __ldcg(fptr(q, cs[j]));
+        cw_sync();
+        // H = h~(K_C, K_C) - F[0:i, C]^T F[0:i, C] on the fp64 tensor cores: warps 4-7 split the
+        // kernel-dot k-steps (now), warps 0-3 the F k-steps (once the gather has landed); the
+        // per-warp partials are summed in fixed warp order
+        double Hc[2][2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) Hc[mt][nt][0] = Hc[mt][nt][1] = 0.0;
+        if (w >= 4) {
+            for (int t = w - 4; t < DQ; t += 4) {
+                const double *base = kcB + (size_t)t * 64;
+                const double k0 = base[(0 * 4 + tq) * 8 + gid], k1 = base[(1 * 4 + tq) * 8 + gid];
+                dmma(Hc[0][0][0], Hc[0][0][1], k0, k0);
+                dmma(Hc[0][1][0], Hc[0][1][1], k0, k1);
+                dmma(Hc[1][0][0], Hc[1][0][1], k1, k0);
+                dmma(Hc[1][1][0], Hc[1][1][1], k1, k1);
+            }
+        }
+        // c0[j] = <kbar, k_sj - kbar>: warp w for j = w, w + 8
+        for (int j = w; j < bsz; j += kCW) {
+            double s0 = 0.0;
+            for (int e = lane; e < D; e += 32) s0 = fma(kb[e], kcB[kcb<D>(e, j)], s0);
+            s0 = warp_sum(s0);
+            if (lane == 0) c0r[j] = s0;
+        }
+        if (i > 0) {
+            mbar_wait(colbar, (uint32_t)(ncol & 1));
+            ++ncol;
+        }
+        // rows [i, i4) of the copies are stale, slots >= bsz unused: zero them
+        for (int idx = tid; i4 > 0 && idx < kBMax * i4; idx += kCT) {
+            const int j = idx / i4, q = idx - j * i4;
+            if (j >= bsz || q >= i) Fcol[(size_t)j * ldc + q] = 0.0;
         }
         cw_sync();
         WC_BTR(2);
-        // H off-diagonal: two threads per pair (a < e), halves combined in fixed order
+        if (w < 4) {
+            for (int kq = w; kq < i4 / 4; kq += 4) {
+                const double f0 = Fcol[(size_t)gid * ldc + 4 * kq + tq];
+                const double f1 = Fcol[(size_t)(8 + gid) * ldc + 4 * kq + tq];
+                dmma(Hc[0][0][0], Hc[0][0][1], f0, f0);
+                dmma(Hc[0][1][0], Hc[0][1][1], f0, f1);
+                dmma(Hc[1][0][0], Hc[1][0][1], f1, f0);
+                dmma(Hc[1][1][0], Hc[1][1][1], f1, f1);
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) Hp[((w * 4 + mt * 2 + nt) * 32 + lane) * 2 + hh] = Hc[mt][nt][hh];
+        cw_sync();
         {
-            const int npairs = bsz * (bsz - 1) / 2;
-            const int pidx = tid >> 1, half = tid & 1;
-            double kd = 0.0, fd = 0.0;
-            int pa = 0, pe = 0;
-            if (pidx < npairs) {
-                int rem = pidx;
-                while (rem >= bsz - 1 - pa) { rem -= bsz - 1 - pa; ++pa; }
-                pe = pa + 1 + rem;
-                double kd2 = 0.0, fd2 = 0.0;  // two chains per half (fixed order)
-#pragma unroll 4
-                for (int e = 2 * half; e < D; e += 4) {
-                    kd = fma(kcT[e * kBMax + pa], kcT[e * kBMax + pe], kd);
-                    kd2 = fma(kcT[(e + 1) * kBMax + pa], kcT[(e + 1) * kBMax + pe], kd2);
-                }
-                int q = 2 * half;
-#pragma unroll 4
-                for (; q + 1 < i; q += 4) {
-                    fd = fma(FsT[q * kBMax + pa], FsT[q * kBMax + pe], fd);
-                    fd2 = fma(FsT[(q + 1) * kBMax + pa], FsT[(q + 1) * kBMax + pe], fd2);
-                }
-                if (q < i) fd = fma(FsT[q * kBMax + pa], FsT[q * kBMax + pe], fd);
-                kd += kd2;
-                fd += fd2;
-            }
-            const double kd1 = __shfl_xor_sync(0xffffffffu, kd, 1);
-            const double fd1 = __shfl_xor_sync(0xffffffffu, fd, 1);
-            if (pidx < npairs && half == 0) {
-                const double h = exp(__dadd_rn(__dmul_rn(g, kd + kd1), -mstar)) - (fd + fd1);
-                H0[pa * kBMax + pe] = h;
-                H0[pe * kBMax + pa] = h;
-                Hw[pa * kBMax + pe] = h;
-                Hw[pe * kBMax + pa] = h;
-            }
-            if (tid < bsz) {
-                H0[tid * kBMax + tid] = cp[tid];
-                Hw[tid * kBMax + tid] = cp[tid];
-                double s0 = 0.0;
-                for (int e = 0; e < D; ++e) s0 = fma(kb[e], kcT[e * kBMax + tid], s0);
-                c0r[tid] = s0;
-            }
+            const int x = tid >> 4, e = tid & 15;
+            const int mt = x >> 3, nt = e >> 3, ln = ((x & 7) << 2) | ((e & 7) >> 1), hh = e & 1;
+            const int off = ((mt * 2 + nt) * 32 + ln) * 2 + hh;
+            double fs = 0.0, ks = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < 4; ++ww) fs += Hp[ww * 256 + off];
+#pragma unroll
+            for (int ww = 4; ww < 8; ++ww) ks += Hp[ww * 256 + off];
+            H0[x * kBMax + e] = (x == e) ? cp[x < bsz ? x : 0] : exp(__dadd_rn(__dmul_rn(g, ks), -mstar)) - fs;
         }
         cw_sync();
         WC_BTR(3);
 
-        // ---- 3: rejection in candidate order (warp 0; lane e owns column e of H)
+        // ---- 3: rejection in candidate order as a parallel symmetric elimination: thread (x, e)
+        // owns H[x][e]; accepting j subtracts F_x F_e with F_x = H[x][j] / sqrt(H[j][j]), which is
+        // also F[i+aa, s_x] for the later candidates x (the coefficients of the per-key triangle).
+        // (warp 0, lane e = column e of the symmetric H in registers; column j is fetched from lane j
+        // by shuffles -- H[x][j] is lane j's entry x).  Every thread learns na from shared memory.
         if (w == 0) {
-            int na = 0;
-            for (int j = 0; j < bsz; ++j) {
-                if (i + na >= a.r) break;
-                const int sj = cs[j];
-                bool dup = false;
-                for (int x = 0; x < na; ++x) dup |= (sA[x] == sj);
-                const double hjj = Hw[j * kBMax + j];
-                const bool acc = !dup && (__dmul_rn(vac[j], cp[j]) < hjj);
-                if (acc) {
-                    if (lane > j && lane < bsz) {
-                        const double hje = Hw[j * kBMax + lane];
-                        for (int x = j + 1; x < bsz; ++x)
-                            Hw[x * kBMax + lane] =
-                                __dsub_rn(Hw[x * kBMax + lane], __ddiv_rn(__dmul_rn(Hw[x * kBMax + j], hje), hjj));
+            const int e = lane;
+            double hc[kBMax];
+#pragma unroll
+            for (int x = 0; x < kBMax; ++x) hc[x] = (e < bsz && x < bsz) ? H0[x * kBMax + e] : 0.0;
+            const int my_cs = e < bsz ? cs[e] : -1;
+            const double my_vp = e < bsz ? __dmul_rn(vac[e], cp[e]) : 0.0;  // v_e p[s_e]
+            bool my_acc = false;
+            int nacc = 0;
+#pragma unroll 1
+            for (int j = 0; j < bsz && i + nacc < a.r; ++j) {
+                double hej = 0.0;  // H[j][e] (own column, row j) -- compile-time register indices
+#pragma unroll
+                for (int x = 0; x < kBMax; ++x) hej = (x == j) ? hc[x] : hej;
+                const double hjj = __shfl_sync(0xffffffffu, hej, j);
+                const int sj = __shfl_sync(0xffffffffu, my_cs, j);
+                const double vp = __shfl_sync(0xffffffffu, my_vp, j);
+                const bool dup = __any_sync(0xffffffffu, my_acc && my_cs == sj);
+                if (!dup && vp < hjj) {
+                    const double rinv = rsqrt(hjj);
+                    const double fe = hej * rinv;  // F[i+nacc, s_e] = H[j][e] / sqrt(H[j][j])
+                    if (e < kBMax) Fcand[nacc * kBMax + e] = (e > j && e < bsz) ? fe : 0.0;
+#pragma unroll
+                    for (int x = 0; x < kBMax; ++x) {
+                        const double fx = __shfl_sync(0xffffffffu, hc[x], j) * rinv;  // H[x][j] / sqrt
+                        if (e > j && x > j) hc[x] = fma(-fx, fe, hc[x]);
                     }
                     if (lane == 0) {
-                        sA[na] = sj;
-                        jA[na] = j;
+                        sA[nacc] = sj;
+                        jA[nacc] = j;
+                        rinvA[nacc] = rinv;
                     }
-                    ++na;
+                    my_acc |= (lane == j);
+                    ++nacc;
                 }
-                __syncwarp();
             }
-            // pre-phase: the triangular recursion on the accepted pivots themselves (lane x = pivot
-            // s_x) gives Fx[x][a] = F[i+a, s_x] and sqrt(p_{s_a}) just before round i+a
-            const int x = lane;
-            double px = (x < na) ? cp[jA[x]] : 0.0;
-            for (int aa = 0; aa < na; ++aa) {
-                const double rs = sqrt(__shfl_sync(0xffffffffu, px, aa));
-                if (x < na) {
-                    double cv = H0[jA[x] * kBMax + jA[aa]];
-                    for (int a2 = 0; a2 < aa; ++a2) cv = fma(-Fx[x * kBMax + a2], Fx[aa * kBMax + a2], cv);
-                    const double f = cv / rs;
-                    Fx[x * kBMax + aa] = f;
-                    const double q = __dadd_rn(px, -__dmul_rn(f, f));
-                    px = (x == aa || !(q > 0.0)) ? 0.0 : q;
-                }
-                if (lane == 0) rsp[aa] = rs;
-                __syncwarp();
+            if (lane == 0) sh_na = nacc;
+            WC_BTR(14);
+        }
+        cw_sync();  // Fcand, sA, jA, rinvA, sh_na visible
+        const int na = sh_na;
+        {
+            const int aa = tid >> 4, a2 = tid & 15;
+            Fx[aa * kBMax + a2] = (aa < na && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
+            if (tid < kBMax) {
+                int pa = -1;
+                for (int x = 0; x < na; ++x) pa = (jA[x] == tid) ? x : pa;
+                perm[tid] = pa;
             }
-            if (lane < kBMax) c0[lane] = lane < na ? c0r[jA[lane]] : 0.0;
-            if (lane == 0) sh_na = na;
         }
         cw_sync();
         WC_BTR(4);
-        const int na = sh_na;
-        // compact the candidate columns of FsT / kcT to accepted order, zero padding
-        for (int row = tid; row < i + D; row += kCT) {
-            double *R = row < i ? FsT + (size_t)row * kBMax : kcT + (size_t)(row - i) * kBMax;
-            double tmp[kBMax];
-#pragma unroll
-            for (int x = 0; x < kBMax; ++x) tmp[x] = x < na ? R[jA[x]] : 0.0;
-#pragma unroll
-            for (int x = 0; x < kBMax; ++x) R[x] = tmp[x];
-        }
-        cw_sync();
         // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
         for (int x = 0; x < na; ++x) {
             const int s = sA[x];
             if (s >= lo && s < hi) {
-                for (int q = tid; q < i; q += kCT) a.L[((int64_t)u * a.r + i + x) * a.r + q] = FsT[(size_t)q * kBMax + x];
+                const int sl = jA[x];
+                for (int q = tid; q < i; q += kCT) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
                 if (tid == 0) a.S[(int64_t)u * a.r + i + x] = s;
             }
         }
-
         WC_BTR(5);
-        // ---- 4: na F-form rounds over this CTA's keys, one key per thread per super-tile
+
+        // ---- 4: na F-form rounds over this CTA's keys.  Per 512-key super-tile, warp w owns keys
+        // [64w, 64w+64) as 8 MMA row-tiles of 8; over the 16 candidate slots,
+        //   G = h~(K_tile, K_C) - F[0:i, tile]^T F[0:i, C]
+        // is accumulated on the fp64 tensor cores (kernel dot, exp in registers, then the F prefix
+        // with negated ring operands); the quad of lanes sharing a key then runs the triangle over
+        // the accepted slots in acceptance order, right-looking, with shuffles.
         loc = 0.0;
         for (int k = 0; k < nst; ++k) {
-            const int64_t l = lo + (int64_t)k * kST + tid;
-            const bool own = l < hi;
+            const int64_t t0 = lo + (int64_t)k * kBT;
             const int wk = tile_w(k);
-            double *Fk = Fc + (int64_t)k * a.r * kST + tid;
-            const double pcur = own ? __ldcg(cur + l) : 0.0;
-            // kernel dots <k_l, k_sa - kbar> against the accepted centred keys; the raw K row is
-            // read in chunks of <= 16 16-byte vectors (register budget: 9 warps => <= 168 regs)
-            double hv[kBMax];
+            double *Fk = Fc + (int64_t)k * a.r * kBT;
+            const int kw = 64 * w;
+            const bool wact = t0 + kw < hi;
+            double C[8][2][2];
 #pragma unroll
-            for (int x = 0; x < kBMax; ++x) hv[x] = 0.0;
-            constexpr int kVec = KR::kVec, kEl = KR::kEl, kChunk = kVec < 16 ? kVec : 16;
+            for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-            for (int q0 = 0; q0 < kVec; q0 += kChunk) {
-                uint4 kv[kChunk];
-                const uint4 *kp = reinterpret_cast<const uint4 *>(Ku + (own ? l : lo) * D) + q0;
+                for (int nt = 0; nt < 2; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
+            int pm[4];  // acceptance index of this lane's 4 C columns (slots 8 nt + 2 tq + hh), -1: rejected
 #pragma unroll
-                for (int q = 0; q < kChunk; ++q) kv[q] = own ? __ldg(kp + q) : make_uint4(0, 0, 0, 0);
+            for (int z = 0; z < 4; ++z) pm[z] = perm[8 * (z >> 1) + 2 * tq + (z & 1)];
+            if (wact) {
+                KC kc[2][8];  // double-buffered K chunks: chunk c + 1 is in flight while c feeds the MMAs
 #pragma unroll
-                for (int q = 0; q < kChunk; ++q) {
-                    const uint32_t wd[4] = {kv[q].x, kv[q].y, kv[q].z, kv[q].w};
+                for (int mt = 0; mt < 8; ++mt) {
+                    const int64_t key = t0 + kw + 8 * mt + gid;
+                    if (key < hi) kc[0][mt].load(Ku + key * D + tq * DQ);
+                    else kc[0][mt].zero();
+                }
 #pragma unroll
-                    for (int e = 0; e < kEl; ++e) {
-                        double xe;
-                        if constexpr (sizeof(T) == 2) {
-                            const uint32_t bits = (e & 1) ? (wd[e >> 1] & 0xffff0000u) : (wd[e >> 1] << 16);
-                            xe = (double)__uint_as_float(bits);
-                        } else {
-                            xe = (double)__uint_as_float(wd[e]);
+                for (int t0c = 0; t0c < DQ; t0c += TC) {
+                    const int cb = (t0c / TC) & 1;
+                    if (t0c + TC < DQ) {
+#pragma unroll
+                        for (int mt = 0; mt < 8; ++mt) {
+                            const int64_t key = t0 + kw + 8 * mt + gid;
+                            if (key < hi) kc[cb ^ 1][mt].load(Ku + key * D + tq * DQ + t0c + TC);
+                            else kc[cb ^ 1][mt].zero();
                         }
-                        const double2 *kr = reinterpret_cast<const double2 *>(kcT + ((q0 + q) * kEl + e) * kBMax);
+                    }
 #pragma unroll
-                        for (int x2 = 0; x2 < kBMax / 2; ++x2) {
-                            const double2 kk = kr[x2];
-                            hv[2 * x2] = fma(xe, kk.x, hv[2 * x2]);
-                            hv[2 * x2 + 1] = fma(xe, kk.y, hv[2 * x2 + 1]);
+                    for (int tt = 0; tt < TC; ++tt) {
+                        const int t = t0c + tt;
+                        const double bk0 = kcB[((t * 2 + 0) * 4 + tq) * 8 + gid];
+                        const double bk1 = kcB[((t * 2 + 1) * 4 + tq) * 8 + gid];
+#pragma unroll
+                        for (int mt = 0; mt < 8; ++mt) {
+                            const double av = kc[cb][mt].elem(tt);
+                            dmma(C[mt][0][0], C[mt][0][1], av, bk0);
+                            dmma(C[mt][1][0], C[mt][1][1], av, bk1);
                         }
                     }
                 }
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int sl = 8 * nt + 2 * tq + hh;
+                        const double cz = c0r[sl];
+                        if (pm[nt * 2 + hh] >= 0) {
+#pragma unroll
+                            for (int mt = 0; mt < 8; ++mt)
+                                C[mt][nt][hh] = exp(__dadd_rn(__dmul_rn(g, C[mt][nt][hh] - cz), -mstar));
+                        }
+                    }
             }
-#pragma unroll
-            for (int x = 0; x < kBMax; ++x)
-                if (x < na) hv[x] = exp(__dadd_rn(__dmul_rn(g, hv[x] - c0[x]), -mstar));
             if (k == 0) WC_BTR(6);
-            // F-prefix dots: rows 0..i-1 of this super-tile from the ring
-            double acc[kBMax];
-#pragma unroll
-            for (int x = 0; x < kBMax; ++x) acc[x] = 0.0;
-            for (int j0 = 0; j0 < i; j0 += kRPS) {
-                const int nr = min(kRPS, i - j0);
+            // F-prefix dots: rows 0..i-1 of this super-tile from the ring (one k-step per stage)
+            for (int j0 = 0; j0 < i; j0 += kBR) {
                 mbar_wait(&full[rstage], rph);
-                const double *src = ring + (size_t)rstage * kRPS * kST + tid;
-                for (int rr = 0; rr < nr; ++rr) {
-                    const double xv = tid < wk ? src[rr * wk] : 0.0;
-                    const double2 *fr = reinterpret_cast<const double2 *>(FsT + (size_t)(j0 + rr) * kBMax);
+                if (wact) {
+                    const double *sb = ring + (size_t)rstage * kBR * kPitch;
+                    const bool rowok = j0 + tq < i;
+                    const double bf0 = Fcol[(size_t)gid * ldc + j0 + tq];
+                    const double bf1 = Fcol[(size_t)(8 + gid) * ldc + j0 + tq];
 #pragma unroll
-                    for (int x2 = 0; x2 < kBMax / 2; ++x2) {
-                        const double2 ff = fr[x2];
-                        acc[2 * x2] = fma(xv, ff.x, acc[2 * x2]);
-                        acc[2 * x2 + 1] = fma(xv, ff.y, acc[2 * x2 + 1]);
+                    for (int mt = 0; mt < 8; ++mt) {
+                        const double av = rowok ? -sb[tq * kPitch + kw + 8 * mt + gid] : 0.0;
+                        dmma(C[mt][0][0], C[mt][0][1], av, bf0);
+                        dmma(C[mt][1][0], C[mt][1][1], av, bf1);
                     }
                 }
                 __syncwarp();
@@ -533,35 +676,75 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                 }
             }
             if (k == 0) WC_BTR(7);
-            // per-key triangle over the block's rounds, F row writes, downdate
-            if (own) {
-                double f[kBMax];
-                double pl = pcur;
+            cw_sync();  // every warp is done with the ring before it is reused as staging
+            // per-key triangle over the accepted pivots in acceptance order: G is transposed through
+            // the ring (idle until the next block's request) so that lane k owns key 32 h + k of its
+            // warp with all its G values in registers; left-looking:
+            //   F[i+aa, l] = (G[l, aa] - sum_{a2<aa} F[i+a2, l] F[i+a2, s_aa]) / sqrt(p_{s_aa})
+            // then the F row writes (coalesced), the downdate with the clamp (Z4), p_s <- 0, the L
+            // entries of pivot keys, and the 32-key group sums.
+            if (wact) {
+                double *stg = ring + (size_t)w * 32 * 17;  // [32 keys][17] per warp
 #pragma unroll
-                for (int aa = 0; aa < kBMax; ++aa) {
-                    f[aa] = 0.0;
-                    if (aa < na) {
-                        double cv = hv[aa] - acc[aa];
+                for (int h = 0; h < 2; ++h) {
 #pragma unroll
-                        for (int a2 = 0; a2 < aa; ++a2) cv = fma(-f[a2], Fx[aa * kBMax + a2], cv);
-                        const double fv = cv / rsp[aa];
-                        f[aa] = fv;
-                        Fk[(int64_t)(i + aa) * wk] = fv;
-                        const double q = __dadd_rn(pl, -__dmul_rn(fv, fv));
-                        pl = q > 0.0 ? q : 0.0;
-                        if (l == sA[aa]) pl = 0.0;
+                    for (int m4 = 0; m4 < 4; ++m4)
+#pragma unroll
+                        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const int ai = pm[nt * 2 + hh];
+                                if (ai >= 0) stg[(8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
+                            }
+                    __syncwarp();
+                    const int64_t key = t0 + kw + 32 * h + lane;
+                    double gk[kBMax];
+#pragma unroll
+                    for (int aa = 0; aa < kBMax; ++aa) gk[aa] = aa < na ? stg[lane * 17 + aa] : 0.0;
+                    __syncwarp();
+                    double pl = key < hi ? __ldcg(cur + key) : 0.0;
+                    double* frow = Fk + (int64_t)i * wk + kw + 32 * h + lane;
+                    double f[kBMax];
+#pragma unroll
+                    for (int aa = 0; aa < kBMax; ++aa) {
+                        f[aa] = 0.0;
+                        if (aa < na) {
+                            double cv = gk[aa];
+                            const double *fx = Fx + aa * kBMax;
+#pragma unroll
+                            for (int a2 = 0; a2 < aa; ++a2) cv = fma(-f[a2], fx[a2], cv);
+                            const double fv = cv * rinvA[aa];
+                            f[aa] = fv;
+                            if (key < hi) frow[(int64_t)aa * wk] = fv;
+                            const double q = __dadd_rn(pl, -__dmul_rn(fv, fv));
+                            pl = (q > 0.0 && key != sA[aa]) ? q : 0.0;
+                        }
+                    }
+                    if (key < hi) {
+                        nxt[key] = pl;
+                        double *ftr = a.FT + ((int64_t)u * n + key) * ftl + i;  // key-major copy of the new rows
+#pragma unroll
+                        for (int aa = 0; aa < kBMax; ++aa)
+                            if (aa < na) ftr[aa] = f[aa];
+                        for (int x = 0; x < na; ++x) {
+                            if (sA[x] == key) {  // L[i+x][i..i+x] = F[i..i+x, s_x]
+                                double *Lr = a.L + ((int64_t)u * a.r + i + x) * a.r + i;
+#pragma unroll
+                                for (int a2 = 0; a2 < kBMax; ++a2)
+                                    if (a2 <= x) Lr[a2] = f[a2];
+                            }
+                        }
+                    }
+                    const double gs = warp_sum(key < hi ? pl : 0.0);  // one 32-key group (fixed order)
+                    if (lane == 0 && t0 + kw + 32 * h < hi) {
+                        gnxt[(t0 + kw) / 32 + h] = gs;
+                        loc += gs;
                     }
                 }
-                nxt[l] = pl;
-                loc += pl;
-                for (int aa = 0; aa < na; ++aa) {
-                    if (l == sA[aa]) {
-                        double *Lrow = a.L + ((int64_t)u * a.r + i + aa) * a.r + i;
-#pragma unroll
-                        for (int a2 = 0; a2 < kBMax; ++a2)
-                            if (a2 <= aa) Lrow[a2] = f[a2];
-                    }
-                }
+            }
+            if (k + 1 < nst) {  // the ring (used as staging above) is free: stream the next super-tile
+                cw_sync();
+                if (tid == 0) sh_req = ((long long)(++nreq) << 32) | ((long long)(k + 1) << 16) | (long long)i;
             }
         }
         WC_BTR(8);
@@ -569,6 +752,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         loc = cw_sum(loc, scr);
         if (tid == 0) pn[c] = loc;
         WC_BTR(9);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + 13] = clock64();
         fread += (double)i;
         i += na;
         cbase += (uint32_t)bsz;
@@ -591,7 +775,7 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), dtrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(dtrace);
-    const char *names[] = {"cand", "gather", "H", "accept", "compact", "t0_kdot", "t0_fdot", "tiles", "sum",
+    const char *names[] = {"cand", "gather", "H", "elim+compact", "Lrows", "t0_kdot", "t0_fdot", "tiles", "sum",
                            "gbar"};
     for (int b = 0; b < r; ++b) {
         const unsigned long long *t = &h[(size_t)b * 16];
@@ -604,6 +788,9 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
             std::fprintf(stderr, " %s=%llu", names[k - 1], v - last);
             last = v;
         }
+        if (b == 0 && t[10] && t[11]) std::fprintf(stderr, " [1a=%llu cand0=%llu]", t[10] - t[0], t[11] - t[10]);
+        if (t[14] > t[3]) std::fprintf(stderr, " [elim=%llu]", t[14] - t[3]);
+        if (t[13] > t[12] && t[9] > t[0]) std::fprintf(stderr, " MHz=%.0f", 1e3 * (double)(t[13] - t[12]) / (double)(t[9] - t[0]));
         std::fprintf(stderr, "\n");
     }
 }
@@ -613,16 +800,21 @@ int launch_blocked_td(const Dims &Dm, const void *K, double *stats, SelectBufs b
                       int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     BlkArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
+    a.gsum = b.gsum;
+    a.FT = b.FT;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
     a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.trace = nullptr;
     static const bool tracing = std::getenv("WC_SELECT_TRACE") != nullptr;
     if (tracing && cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * Dm.r) == cudaSuccess)
         cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 16 * Dm.r, st);
-    const size_t fixed = ((size_t)Dm.r * kBMax + (size_t)D * kBMax + 3 * kBMax * kBMax + 5 * kBMax + D + 40) *
-                             sizeof(double) + 3 * kBMax * sizeof(int) + 64;
-    const size_t stage_bytes = (size_t)kRPS * kST * sizeof(double);
-    if (fixed + 2 * stage_bytes + 2 * 16 > 220 * 1024) return -2;  // r too large for the shared-memory plan
-    int NS = (int)std::min<size_t>(12, (220 * 1024 - fixed) / (stage_bytes + 16));
+    const size_t ldc = (size_t)((Dm.r + 15) & ~15) + 4;
+    const size_t fixed = (ldc * kBMax + (size_t)D * kBMax + 3 * kBMax * kBMax + 7 * kBMax + D + 40 + kCW * 4 * 64 +
+                          a.cpu + 64) * sizeof(double) +
+                         kBMax * sizeof(long long) + 5 * kBMax * sizeof(int) + 64;
+    const size_t stage_bytes = (size_t)kBR * kPitch * sizeof(double);
+    // >= 3 stages: the triangle stages G (8 warps x 32 keys x 17 doubles) through the idle ring
+    if (fixed + 3 * (stage_bytes + 16) > 220 * 1024) return -2;  // r too large for the shared-memory plan
+    int NS = (int)std::min<size_t>(12, (220 * 1024 - fixed - 16) / (stage_bytes + 16));
     const size_t smem = fixed + (size_t)NS * (stage_bytes + 16);
     auto kt = rpc_select_blocked_kernel<T, D>;
     cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
