@@ -34,6 +34,11 @@ def _env_int(k, d):
         return d
 
 
+# fp64 tensor-core (DMMA m8n8k4) throughput measured on this pool's B200 by tools/micro/fp64_bench.cu
+# (profiles/r1_fp64_microbench.txt): there is no fp64 entry in MEASURED_PEAKS.json.
+FP64_TENSOR_TFLOPS = 36.5
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -203,9 +208,11 @@ def main():
                          "Default: nshard for the long* configs, replicas otherwise")
     ap.add_argument("--r", type=int, default=None, help="override the config's coreset size r")
     ap.add_argument("--n", type=int, default=None, help="override the config's n (= m)")
-    ap.add_argument("--block", type=int, default=1,
+    ap.add_argument("--block", type=int, default=16,
                     help="pivot selection: 1 = sequential RPCholesky (Alg 1); b >= 2 = blocked RPCholesky "
-                         "with b candidates per block (reading Z22)")
+                         "with b candidates per block (reading Z22; default 16)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip timing the other selection variant (sequential when --block >= 2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -316,14 +323,51 @@ def main():
         reff_u = sel.r_eff.cpu()
         alg_bytes = sum(select_bytes(cfg.n, cfg.d, int(reff_u[u]), e, float(stt[u, 6]), float(stt[u, 8]))
                         for u in range(units))
+        # algorithmic fp64 flops of the round updates: kernel dots 2 n d r_eff + F-prefix dots 2 n Fdot
+        alg_flops = sum(2.0 * cfg.n * (cfg.d * int(reff_u[u]) + float(stt[u, 9])) for u in range(units))
         sel_info = {"block": args.block, "blocks_per_unit": float(stt[:, 6].mean()),
-                    "candidates_per_unit": float(stt[:, 7].mean()), "f_rows_reread_per_unit": float(stt[:, 8].mean())}
+                    "candidates_per_unit": float(stt[:, 7].mean()), "f_rows_reread_per_unit": float(stt[:, 8].mean()),
+                    "alg_fp64_flops": alg_flops}
         del sel
     else:
         alg_bytes = units * select_bytes(cfg.n, cfg.d, r_eff, e)
     sel_ms = st_mean[1] if st_mean else None
     achieved = alg_bytes / (sel_ms / 1e3) / 1e9 if sel_ms else None
     peak, peak_kind = peaks()
+    roof64 = None
+    if sel_info and sel_ms:
+        a64 = sel_info["alg_fp64_flops"] / (sel_ms / 1e3) / 1e12
+        roof64 = {"kernel": "rpc_select_blocked_kernel" if args.block >= 2 else "rpc_select_tma_kernel",
+                  "bound": "fp64", "achieved": a64, "peak": FP64_TENSOR_TFLOPS, "peak_kind":
+                  "measured DMMA microbenchmark (tools/micro/fp64_bench.cu)", "unit": "TFLOP/s",
+                  "frac": a64 / FP64_TENSOR_TFLOPS}
+
+    # the other selection variant on the same inputs (context: sequential Alg 1 vs blocked)
+    variants = None
+    if not args.no_variants and mode == "replicas" and args.block >= 2:
+        nvs = max(2, min(5, args.steps))
+        forward_seq = lambda: wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=1)
+        forward_seq()
+        torch.cuda.synchronize()
+        B.timing_enable(True)
+        vt, vst = [], []
+        for _ in range(nvs):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            forward_seq()
+            e1.record(stream)
+            e1.synchronize()
+            vt.append(e0.elapsed_time(e1))
+            vst.append(B.timing_read())
+        B.timing_enable(False)
+        vsel = statistics.mean(x[1] for x in vst)
+        vbytes = units * select_bytes(cfg.n, cfg.d, int(R.min().item()), e)
+        variants = {"sequential": {"block": 1, "steps": nvs, "ms_per_step": statistics.mean(vt),
+                                   "queries_per_s": queries_per_rank * world / (statistics.mean(vt) / 1e3),
+                                   "select_ms": vsel, "select_hbm_gbs": vbytes / (vsel / 1e3) / 1e9,
+                                   "select_hbm_frac": vbytes / (vsel / 1e3) / 1e9 / peak}}
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}" + (f"_b{args.block}" if args.block >= 2 else "")
                       + ".json")
@@ -432,6 +476,8 @@ def main():
                        "l2": f"flushed ({args.flush_mb} MB write) before each step"},
             "stages_ms": dict(zip(st_names, st_mean)) if st_mean else None,
             "selection": sel_info,
+            "roofline_fp64": roof64,
+            "variants": variants,
             "roofline": {"kernel": "rpc_select_blocked_kernel" if args.block >= 2 else "rpc_select_tma_kernel",
                          "bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if achieved else None,

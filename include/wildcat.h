@@ -18,10 +18,11 @@
  *   L      double [units][r][r]      lower-triangular Cholesky factor of h~(K_S,K_S) in pivot
  *                                    order, L[a][b] = F[b, S[a]] (b <= a), 0 elsewhere (Z6)
  *   stats  double [units][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, nblocks, ncand,
- *                                    Fread, 0 (x7), kbar[d].  Selection bookkeeping: nblocks =
+ *                                    Fread, Fdot, 0 (x6), kbar[d].  Selection bookkeeping: nblocks =
  *                                    blocks (sequential: rounds) run, ncand = candidates drawn,
  *                                    Fread = sum over blocks of the F rows re-read at the block
- *                                    start (sequential: sum_i i) -- the F traffic is 8 n Fread bytes
+ *                                    start (sequential: sum_i i) -- the F traffic is 8 n Fread bytes;
+ *                                    Fdot = sum over blocks of (rows re-read x pivots accepted)
  *   KS     dtype  [units][r][d]      coreset keys, uncentred (Alg 2 "K_S <- K_S + kbar")
  *   X      float  [units][r][d+1]    [V_S, w] = W [V, 1_n]  (Alg 2 "Compress values")
  *   vmin, vmax dtype [units][d]      columnwise range of V (Alg 4)

@@ -27,7 +27,7 @@ __all__ = ["forward", "forward_host", "select", "weights", "attend", "Selection"
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range"]
 
 
-STATS_HEAD = 16  # tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, 0 x 7; then kbar[d]
+STATS_HEAD = 16  # tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, Fdot, 0 x 6; then kbar[d]
 
 
 def STATS_STRIDE(d: int) -> int:

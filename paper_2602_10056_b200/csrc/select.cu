@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
         stw[6] = (double)i;                          // rounds run
         stw[7] = (double)i;                          // pivots drawn
         stw[8] = 0.5 * (double)i * (double)(i - 1);  // F rows re-read: sum over rounds q of q
+        stw[9] = stw[8];                             // F-prefix dot work (one pivot per round)
     }
 }
 
@@ -663,6 +664,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         stw[6] = (double)i;                          // rounds run
         stw[7] = (double)i;                          // pivots drawn
         stw[8] = 0.5 * (double)i * (double)(i - 1);  // F rows re-read: sum over rounds q of q
+        stw[9] = stw[8];                             // F-prefix dot work (one pivot per round)
     }
 }
 

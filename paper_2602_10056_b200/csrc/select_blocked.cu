@@ -87,7 +87,8 @@ __device__ __forceinline__ unsigned long long btimer() {
 
 constexpr int kBT = 512;          // keys per super-tile of the blocked kernel (64 per compute warp)
 constexpr int kBR = 4;            // F rows per ring stage (one DMMA k-step)
-constexpr int kPitch = kBT + 8;   // ring row pitch in doubles (4160 B): odd rows sit 16 banks over
+constexpr int kPitch = kBT + 4;   // ring row pitch in doubles (4128 B): the 4 rows of a k-step sit 8 banks
+                                  // apart, so each half-warp of an A-fragment load is conflict-free
 
 // fp64 tensor-core MMA (DMMA) m8n8k4: C += A B with A 8x4 row-major (lane l holds A[l/4][l%4]),
 // B 4x8 column-major (lane l holds B[l%4][l/4]), C 8x8 (lane l holds C[l/4][2(l%4) + {0,1}]).
@@ -100,10 +101,12 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 // MMA-operand layouts of the accepted (or candidate) pivot columns, 16 pivot slots p:
 //   Fcol: F[q, s_p] (candidate slot p) as 16 columns of stride ldc = 16k + 4 doubles: lane (tq, g)
 //        of the k-step at q0 reads Fcol[(8 nt + g) * ldc + q0 + tq] -- two wavefronts per warp load;
-//   kcB: centred key k_sp - kbar at dim = tq * (D/4) + t (lane tq owns a contiguous run of D/4 dims).
+//   kcB: centred key k_sp - kbar at dim = tq * (D/4) + t (lane tq owns a contiguous run of D/4 dims),
+//        stored at ((t * 2 + p/8) * 8 + p%8) * 4 + tq: a half-warp of 64-bit loads hits 16 distinct
+//        consecutive doubles.
 template <int D> __device__ __forceinline__ int kcb(int dim, int p) {
     constexpr int DQ = D / 4;
-    return (((dim % DQ) * 2 + (p >> 3)) * 4 + dim / DQ) * 8 + (p & 7);
+    return (((dim % DQ) * 2 + (p >> 3)) * 8 + (p & 7)) * 4 + dim / DQ;
 }
 
 // TC consecutive raw key elements of one row held as 32-bit words; elem() widens exactly to fp64.
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     double T0 = 0.0, theta = 0.0;
     int i = 0, blk = 0;
     uint32_t cbase = 0;
-    double fread = 0.0;
+    double fread = 0.0, fdot = 0.0;
     long long nreq = 0;  // requests published to the producer (thread 0)
     int ncol = 0;        // candidate-column copy rounds (parity of colbar)
     while (i < a.r) {
@@ -446,14 +449,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             for (int j = 0; j < bsz; ++j)
                 bulk_g2s(Fcol + (size_t)j * ldc, FTu + (int64_t)cs[j] * ftl, (uint32_t)(i4 * sizeof(double)), colbar);
         }
-        for (int idx = tid; idx < bsz * D; idx += kCT) {
-            const int j = idx / D, e = idx - j * D;
-            kcB[kcb<D>(e, j)] = __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]);
+        {
+            // thread (e-part, j): j = tid & 15 is fixed per thread; also its part of c0[j] = <kbar, k_sj - kbar>
+            const int j = tid & 15;
+            double s0 = 0.0;
+            for (int e = tid >> 4; e < D; e += kCT / 16) {
+                const double kc = j < bsz ? __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]) : 0.0;
+                kcB[kcb<D>(e, j)] = kc;
+                s0 = fma(kb[e], kc, s0);
+            }
+            Hp[tid] = s0;  // Hp is free until the H partials below
         }
         cw_sync();
         // H = h~(K_C, K_C) - F[0:i, C]^T F[0:i, C] on the fp64 tensor cores: warps 4-7 split the
         // kernel-dot k-steps (now), warps 0-3 the F k-steps (once the gather has landed); the
         // per-warp partials are summed in fixed warp order
+        if (tid < kBMax) {  // c0[j]: the 16 e-parts of slot j in fixed order
+            double s0 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kCT / 16; ++q) s0 += Hp[q * 16 + tid];
+            c0r[tid] = s0;
+        }
         double Hc[2][2][2];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
@@ -462,19 +478,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         if (w >= 4) {
             for (int t = w - 4; t < DQ; t += 4) {
                 const double *base = kcB + (size_t)t * 64;
-                const double k0 = base[(0 * 4 + tq) * 8 + gid], k1 = base[(1 * 4 + tq) * 8 + gid];
+                const double k0 = base[(0 * 8 + gid) * 4 + tq], k1 = base[(1 * 8 + gid) * 4 + tq];
                 dmma(Hc[0][0][0], Hc[0][0][1], k0, k0);
                 dmma(Hc[0][1][0], Hc[0][1][1], k0, k1);
                 dmma(Hc[1][0][0], Hc[1][0][1], k1, k0);
                 dmma(Hc[1][1][0], Hc[1][1][1], k1, k1);
             }
-        }
-        // c0[j] = <kbar, k_sj - kbar>: warp w for j = w, w + 8
-        for (int j = w; j < bsz; j += kCW) {
-            double s0 = 0.0;
-            for (int e = lane; e < D; e += 32) s0 = fma(kb[e], kcB[kcb<D>(e, j)], s0);
-            s0 = warp_sum(s0);
-            if (lane == 0) c0r[j] = s0;
         }
         if (i > 0) {
             mbar_wait(colbar, (uint32_t)(ncol & 1));
@@ -629,8 +638,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
 #pragma unroll
                     for (int tt = 0; tt < TC; ++tt) {
                         const int t = t0c + tt;
-                        const double bk0 = kcB[((t * 2 + 0) * 4 + tq) * 8 + gid];
-                        const double bk1 = kcB[((t * 2 + 1) * 4 + tq) * 8 + gid];
+                        const double bk0 = kcB[((t * 2 + 0) * 8 + gid) * 4 + tq];
+                        const double bk1 = kcB[((t * 2 + 1) * 8 + gid) * 4 + tq];
 #pragma unroll
                         for (int mt = 0; mt < 8; ++mt) {
                             const double av = kc[cb][mt].elem(tt);
@@ -754,6 +763,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         WC_BTR(9);
         if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + 13] = clock64();
         fread += (double)i;
+        fdot += (double)i * (double)na;
         i += na;
         cbase += (uint32_t)bsz;
         ++blk;
@@ -766,6 +776,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         st[6] = (double)blk;    // blocks run
         st[7] = (double)cbase;  // candidates drawn
         st[8] = fread;          // F rows re-read: sum over blocks of the block-start i
+        st[9] = fdot;           // F-prefix dot work: sum over blocks of i * (pivots accepted)
     }
 }
 
