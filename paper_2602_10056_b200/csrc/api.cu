@@ -132,7 +132,8 @@ float *carve_weights(Carver &c, const wc_shape *s, wc::ProloguePartials *pp) {
     }
     // fp32 split partials of Y~, followed by the fp64 reduced Y~ (8-byte aligned: the float count is even)
     const size_t parts = U * wc::weights_num_splits(D) * (size_t)D.r * (D.d + 1);
-    return c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1));
+    // + the fp64 Y~, + the inverted diagonal blocks of L (solve scratch)
+    return c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1) + 2 * U * wc::dinv_elems(D.r));
 }
 
 int finish(int launches) {

@@ -215,22 +215,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const __nv_bfloat16 *Qh = Q + head * m * D;
         // ---- stage operands in shared memory (16-byte chunks -> 128B-swizzled K-major layout)
         constexpr int CPR = D / 8;  // 16-byte chunks per row
-        for (int e = tid; e < 128 * CPR; e += kTcThreads) {
-            const int row = e / CPR, cc = e % CPR;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (q0 + row < m) v = __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc);
-            *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = v;
+        {
+            constexpr int NQ = 128 * CPR / kTcThreads;  // chunks per thread, all loads in flight
+            uint4 qv[NQ];
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+                const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+                qv[k] = (q0 + row < m) ? __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc)
+                                       : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+                const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+                *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = qv[k];
+            }
         }
         if (u != cur_unit) {
             re = r_eff[u];
             const float *Xu = X + (int64_t)u * r * DC;
-            for (int e = tid; e < D * RP; e += kTcThreads) {  // X^T split into bf16 hi + lo
-                const int c = e / RP, s = e % RP;
-                const float x = (s < re) ? Xu[(int64_t)s * DC + c] : 0.f;
-                const __nv_bfloat16 xh = __float2bfloat16_rn(x);
-                const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
-                *reinterpret_cast<__nv_bfloat16 *>(sXh + umma::sw128_offset(c, s, D)) = xh;
-                if (L::kSplitX) *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
+            // X^T split into bf16 hi + lo; batches of 8 independent loads per thread in flight
+            static_assert((D * RP) % (8 * kTcThreads) == 0, "X staging batch");
+            for (int e0 = tid; e0 < D * RP; e0 += 8 * kTcThreads) {
+                float xv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int e = e0 + k * kTcThreads, c = e / RP, s = e % RP;
+                    xv[k] = (s < re) ? __ldg(Xu + (int64_t)s * DC + c) : 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int e = e0 + k * kTcThreads, c = e / RP, s = e % RP;
+                    const __nv_bfloat16 xh = __float2bfloat16_rn(xv[k]);
+                    const __nv_bfloat16 xl = __float2bfloat16_rn(xv[k] - __bfloat162float(xh));
+                    *reinterpret_cast<__nv_bfloat16 *>(sXh + umma::sw128_offset(c, s, D)) = xh;
+                    if (L::kSplitX) *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
+                }
             }
             for (int s = tid; s < RP; s += kTcThreads) sW[s] = (s < re) ? Xu[(int64_t)s * DC + D] : 0.f;
             for (int c = tid; c < D; c += kTcThreads) {
@@ -240,6 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         if (u != cur_unit || L::kAliasP) {  // K_S (reloaded each tile when P aliases it)
             const __nv_bfloat16 *KSu = KS + (int64_t)u * r * D;
+#pragma unroll 8
             for (int e = tid; e < RP * CPR; e += kTcThreads) {
                 const int row = e / CPR, cc = e % CPR;
                 uint4 v = make_uint4(0, 0, 0, 0);

@@ -41,6 +41,30 @@ template <> struct Vec8<float> {
     }
 };
 
+// 8 consecutive raw elements kept as 16-byte vectors (bf16: one, fp32: two) until they are used;
+// at(k) widens element k exactly to fp64.
+template <typename T> struct Raw8;
+template <> struct Raw8<__nv_bfloat16> {
+    uint4 v;
+    __device__ __forceinline__ void load(const __nv_bfloat16 *p) { v = __ldg(reinterpret_cast<const uint4 *>(p)); }
+    __device__ __forceinline__ double at(int k) const {
+        const uint32_t wd = k < 2 ? v.x : k < 4 ? v.y : k < 6 ? v.z : v.w;
+        return (double)__uint_as_float((k & 1) ? (wd & 0xffff0000u) : (wd << 16));
+    }
+};
+template <> struct Raw8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void load(const float *p) {
+        a = __ldg(reinterpret_cast<const float4 *>(p));
+        b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    }
+    __device__ __forceinline__ double at(int k) const {
+        const float4 &q = k < 4 ? a : b;
+        const int kk = k & 3;
+        return (double)(kk == 0 ? q.x : kk == 1 ? q.y : kk == 2 ? q.z : q.w);
+    }
+};
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based generator of Salmon et al. (SC'11).  The pivot uniform of round i of
 // unit u is built from Philox4x32-10(key = seed, ctr = (i, u_lo, u_hi, 'PIVT')) with

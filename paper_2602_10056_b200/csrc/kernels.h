@@ -91,9 +91,11 @@ int launch_weights(const Dims &D, const void *K, const void *V, const int32_t *S
 // densely (KSin [units][r][d], dtype); Yfull receives the reduced local sum [units][r][d+1].
 int launch_weights_partial_ks(const Dims &D, const void *K, const void *V, const void *KSin, const int32_t *r_eff,
                               const double *stats, float *Ypart, double *Yfull, cudaStream_t st);
-// phase 2 (after the cross-GPU sum of Yfull): X = L^{-T} L^{-1} Y~.
+// phase 2 (after the cross-GPU sum of Yfull): X = L^{-T} L^{-1} Y~.  Dinv: scratch of
+// units * dinv_elems(r) doubles for the inverted 32 x 32 diagonal blocks of L.
 int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
-                         cudaStream_t st);
+                         double *Dinv, cudaStream_t st);
+inline size_t dinv_elems(int r) { return (size_t)((r + 31) / 32) * 32 * 32; }
 
 // A5: attend.
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,

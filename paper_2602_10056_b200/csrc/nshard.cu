@@ -369,7 +369,7 @@ __global__ void ns_finish(const Ctl *ctl, int32_t *r_eff_out, double *stats) {
 
 struct NsWs {
     ProloguePartials pp;
-    double *stats, *nrm2, *p, *F, *ctot, *sendtot, *ranktot, *packet, *sumbuf, *maxbuf, *rkbuf, *L, *Yfull;
+    double *stats, *nrm2, *p, *F, *ctot, *sendtot, *ranktot, *packet, *sumbuf, *maxbuf, *rkbuf, *L, *Yfull, *Dinv;
     float *Ypart, *X;
     void *KS, *vmin, *vmax, *aimg;
     int32_t *S, *reff;
@@ -413,6 +413,7 @@ size_t ns_carve(const Dims &D, void *base, NsWs &w) {
     const int splits = weights_num_splits(D);
     w.Ypart = c.take<float>((size_t)splits * D.r * (D.d + 1) + 2);
     w.Yfull = c.take<double>((size_t)D.r * (D.d + 1));
+    w.Dinv = c.take<double>(dinv_elems(D.r));
     w.X = c.take<float>((size_t)D.r * (D.d + 1));
     w.KS = c.take<char>((size_t)D.r * D.d * e);
     w.vmin = c.take<char>((size_t)D.d * e);
@@ -475,7 +476,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     // ---- A3 + A4: local partial Y~, allreduce, replicated solve
     if (launch_weights_partial_ks(Dm, K, V, w.KS, w.reff, w.stats, w.Ypart, w.Yfull, st) < 0) return WC_ECUDA;
     WC_NCCL(api.allReduce(w.Yfull, w.Yfull, (size_t)r * (D + 1), ncclFloat64, ncclSum, cm->comm, st));
-    if (launch_weights_solve(Dm, w.Yfull, w.L, w.reff, w.X, st) < 0) return WC_ECUDA;
+    if (launch_weights_solve(Dm, w.Yfull, w.L, w.reff, w.X, w.Dinv, st) < 0) return WC_ECUDA;
     // ---- A5: local queries
     const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
     if (Dm.m > 0 && launch_attend(Dm, Q, w.KS, w.X, w.reff, w.vmin, w.vmax, beta, clip, O, w.aimg, st) < 0) return WC_ECUDA;

@@ -35,15 +35,30 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
     float mn[8], mx[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) { cs[k] = 0.0; mn[k] = 3.0e38f; mx[k] = -3.0e38f; }
-    for (int64_t l = lo + rg; l < hi; l += RG) {
-        double x[8];
-        Vec8<T>::load(Ku + l * d + 8 * cj, x);
+    constexpr int U4 = 4;  // rows per thread in flight
+    for (int64_t l0 = lo + rg; l0 < hi; l0 += (int64_t)U4 * RG) {
+        Raw8<T> xk[U4], xv[U4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) cs[k] += x[k];
-        if (want_v) {
-            Vec8<T>::load(Vu + l * d + 8 * cj, x);
+        for (int q = 0; q < U4; ++q) {
+            const int64_t l = l0 + (int64_t)q * RG;
+            if (l < hi) {
+                xk[q].load(Ku + l * d + 8 * cj);
+                if (want_v) xv[q].load(Vu + l * d + 8 * cj);
+            }
+        }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) { mn[k] = fminf(mn[k], (float)x[k]); mx[k] = fmaxf(mx[k], (float)x[k]); }
+        for (int q = 0; q < U4; ++q) {
+            if (l0 + (int64_t)q * RG < hi) {  // rows in ascending order: fixed summation order
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cs[k] += xk[q].at(k);
+                if (want_v) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        mn[k] = fminf(mn[k], (float)xv[q].at(k));
+                        mx[k] = fmaxf(mx[k], (float)xv[q].at(k));
+                    }
+                }
+            }
         }
     }
     double *s_cs = sm1;                                    // [RG][d]
@@ -74,17 +89,24 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
         const int64_t qlo = (int64_t)p * qrows, qhi = min(mq, qlo + qrows);
         const T *Qu = Q + (int64_t)u * q_unit_stride_rows * d;
         double best = 0.0;
-        for (int64_t i0 = qlo; i0 < qhi; i0 += RG) {
-            const int64_t i = i0 + rg;
-            double sq = 0.0;
-            if (i < qhi) {
-                double x[8];
-                Vec8<T>::load(Qu + i * d + 8 * cj, x);
+        for (int64_t i0 = qlo; i0 < qhi; i0 += (int64_t)U4 * RG) {
+            Raw8<T> xq[U4];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) sq += x[k] * x[k];
+            for (int q = 0; q < U4; ++q) {
+                const int64_t i = i0 + (int64_t)q * RG + rg;
+                if (i < qhi) xq[q].load(Qu + i * d + 8 * cj);
             }
-            for (int o = 1; o < CPR; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            best = fmax(best, sq);
+#pragma unroll
+            for (int q = 0; q < U4; ++q) {
+                const int64_t i = i0 + (int64_t)q * RG + rg;
+                double sq = 0.0;
+                if (i < qhi) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) sq += xq[q].at(k) * xq[q].at(k);
+                }
+                for (int o = 1; o < CPR; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                best = fmax(best, sq);
+            }
         }
         __shared__ double scr[40];
         best = block_max(best, scr);
@@ -92,34 +114,37 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
     }
 }
 
-// Finalise kbar (fixed-order sum over splits) and the value range.  G groups of d threads.
+// Finalise kbar (fixed-order sum over splits) and the value range.  Block (u, column chunk of 32):
+// 8 groups of 32 threads; group g sums splits p = g, g + 8, ... (unrolled), combined in group order.
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
                                                      T *vmin, T *vmax) {
     __shared__ double s_t[kPT];
     __shared__ float s_a[kPT], s_b[kPT];
-    const int u = blockIdx.x, G = kPT / d, g = threadIdx.x / d, j = threadIdx.x % d;
+    const int u = blockIdx.x, g = threadIdx.x >> 5, j = blockIdx.y * 32 + (threadIdx.x & 31);
     double t = 0.0;
     float a = 3.0e38f, b = -3.0e38f;
+    if (j < d) {
 #pragma unroll 8
-    for (int p = g; p < P; p += G) {
-        const int64_t o = ((int64_t)u * P + p) * d + j;
-        t += colsum[o];
-        a = fminf(a, vmin_p[o]);
-        b = fmaxf(b, vmax_p[o]);
+        for (int p = g; p < P; p += 8) {
+            const int64_t o = ((int64_t)u * P + p) * d + j;
+            t += colsum[o];
+            a = fminf(a, vmin_p[o]);
+            b = fmaxf(b, vmax_p[o]);
+        }
     }
     s_t[threadIdx.x] = t;
     s_a[threadIdx.x] = a;
     s_b[threadIdx.x] = b;
     __syncthreads();
-    if (threadIdx.x < d) {
+    if (threadIdx.x < 32 && j < d) {
         double tt = 0.0;
         float aa = 3.0e38f, bb = -3.0e38f;
-        for (int gg = 0; gg < G; ++gg) {
-            tt += s_t[gg * d + j];
-            aa = fminf(aa, s_a[gg * d + j]);
-            bb = fmaxf(bb, s_b[gg * d + j]);
+        for (int gg = 0; gg < 8; ++gg) {
+            tt += s_t[gg * 32 + threadIdx.x];
+            aa = fminf(aa, s_a[gg * 32 + threadIdx.x]);
+            bb = fmaxf(bb, s_b[gg * 32 + threadIdx.x]);
         }
         if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = tt / (double)n;
         if (vmin) {
@@ -145,21 +170,29 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
     const T *Ku = K + (int64_t)u * n * d;
     double best = 0.0;
-    for (int64_t l0 = lo; l0 < hi; l0 += RG) {
-        const int64_t l = l0 + rg;
-        double sq = 0.0;
-        if (l < hi) {
-            double x[8];
-            Vec8<T>::load(Ku + l * d + 8 * cj, x);
+    constexpr int U4 = 4;  // rows per thread in flight
+    for (int64_t l0 = lo; l0 < hi; l0 += (int64_t)U4 * RG) {
+        Raw8<T> xk[U4];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const double c = __dadd_rn(x[k], -kb[8 * cj + k]);
-                sq = __dadd_rn(sq, __dmul_rn(c, c));
-            }
+        for (int q = 0; q < U4; ++q) {
+            const int64_t l = l0 + (int64_t)q * RG + rg;
+            if (l < hi) xk[q].load(Ku + l * d + 8 * cj);
         }
-        for (int o = 1; o < CPR; o <<= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
-        if (l < hi && cj == 0) nrm2[(int64_t)u * n + l] = sq;
-        best = fmax(best, sq);
+#pragma unroll
+        for (int q = 0; q < U4; ++q) {
+            const int64_t l = l0 + (int64_t)q * RG + rg;
+            double sq = 0.0;
+            if (l < hi) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double c = __dadd_rn(xk[q].at(k), -kb[8 * cj + k]);
+                    sq = __dadd_rn(sq, __dmul_rn(c, c));
+                }
+            }
+            for (int o = 1; o < CPR; o <<= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+            if (l < hi && cj == 0) nrm2[(int64_t)u * n + l] = sq;
+            best = fmax(best, sq);
+        }
     }
     best = block_max(best, scr);
     if (threadIdx.x == 0) rk2[(int64_t)u * P + p] = best;
@@ -214,7 +247,7 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                                                static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
                                                (int64_t)D.group() * D.m);
-    prologue_kbar<T><<<units, kPT, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
+    prologue_kbar<T><<<dim3(units, (D.d + 31) / 32), kPT, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
                                             want_v ? static_cast<T *>(vmin) : nullptr,
                                             want_v ? static_cast<T *>(vmax) : nullptr);
     prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, P, stats, nrm2, pp.rk2);
@@ -231,7 +264,7 @@ int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmi
     dim3 grid(pp.P, units);
     prologue_pass1<T><<<grid, kPT, smem, st>>>(nullptr, static_cast<const T *>(V), static_cast<const T *>(V), D.n,
                                                0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0);
-    prologue_kbar<T><<<units, kPT, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
+    prologue_kbar<T><<<dim3(units, (D.d + 31) / 32), kPT, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
                                             static_cast<T *>(vmin), static_cast<T *>(vmax));
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }

@@ -114,11 +114,6 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
     }
 }
 
-// Reduce split partials (fixed order, fp64) and solve L L^T X = Y~ for 8 RHS columns per CTA
-// (256 threads: thread t owns panel row t/8 and column t%8).  Blocked in 32-row panels so the
-// sequential part only touches a 32 x 32 diagonal block held in shared memory:
-//   forward  (L Z = Y):   z_P -= L[P, 0:p0] z_{0:p0}  (parallel), then solve the panel's block
-//   backward (L^T X = Z): x_P -= L[pe:q, P]^T x_{pe:q} (parallel, reads rows of L), then the block
 // Y~ = sum over n-splits of the fp32 partials, in fixed split order, in fp64.
 template <int D>
 __global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__restrict__ Ypart,
@@ -132,107 +127,156 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__rest
     double y = 0.0;
     if (a < r_eff[u]) {
         const float *src = Ypart + (int64_t)u * splits * r * DC + e;
-#pragma unroll 8
-        for (int sp = 0; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
+        int sp = 0;
+        for (; sp + 16 <= splits; sp += 16) {  // 16 independent loads in flight, summed in split order
+            float t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) y += (double)t[k];
+        }
+        for (; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
     }
     Y[(int64_t)u * r * DC + e] = y;
 }
 
+// A4: X = L^{-T} (L^{-1} Y~), blocked in 32-row panels.  weights_dinv_kernel inverts the 32 x 32
+// diagonal blocks of L once per unit (one warp per block; lane c owns column c of the inverse, a
+// sequential substitution with broadcast reads of the block), so that the panel solves are plain
+// 32 x 32 products; the sequential part of the solve is only the panel order.
+constexpr int kPB = 32;   // panel size
+constexpr int kCBs = 128; // L columns (forward) / rows (backward) fetched per round trip
+
+__global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restrict__ L, const int32_t *__restrict__ r_eff,
+                                                          int r, double *__restrict__ Dinv) {
+    __shared__ double Lb[kPB][kPB + 1];
+    const int blk = blockIdx.x, u = blockIdx.y, lane = threadIdx.x;
+    const int q = r_eff[u], p0 = blk * kPB;
+    if (p0 >= q) return;
+    const int nb = min(kPB, q - p0);
+    const double *Lu = L + (int64_t)u * r * r;
+#pragma unroll 8
+    for (int i = 0; i < kPB; ++i) Lb[i][lane] = (i < nb && lane <= i) ? __ldg(Lu + (int64_t)(p0 + i) * r + p0 + lane) : 0.0;
+    __syncwarp();
+    // column c = lane of inv(Lb): x_i = (delta_ic - sum_{j<i} L_ij x_j) / L_ii, i = c .. nb-1
+    double x[kPB];
+#pragma unroll
+    for (int i = 0; i < kPB; ++i) {
+        double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < i; ++j) acc = fma(-Lb[i][j], x[j], acc);
+        x[i] = (i < nb && i >= lane) ? acc / Lb[i][i] : 0.0;
+    }
+    double *Du = Dinv + ((int64_t)u * ((r + kPB - 1) / kPB) + blk) * kPB * kPB;
+#pragma unroll
+    for (int i = 0; i < kPB; ++i) Du[i * kPB + lane] = x[i];  // row-major inverse, lower triangular
+}
+
+// 8 RHS columns per CTA, 256 threads: thread t owns panel row t/8, column t%8.
 template <int D>
 __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__restrict__ Y,
                                                             const double *__restrict__ L,
+                                                            const double *__restrict__ Dinv,
                                                             const int32_t *__restrict__ r_eff, int r,
                                                             float *__restrict__ X) {
     constexpr int DC = D + 1;
-    constexpr int PB = 32;
-    constexpr int CB = 64;          // L columns (forward) / rows (backward) staged per block
-    extern __shared__ double zs[];  // z[r][8]
-    __shared__ double Ld[PB][PB + 1];
-    __shared__ double Lb[PB][CB + 1];  // staged block of L
+    constexpr int NL = kPB * kCBs / 256;  // L elements per thread per round trip
+    extern __shared__ double zs[];          // z[r][8]
+    __shared__ double Lb[kPB][kCBs + 1];    // a fetched chunk of L (row-major panel rows / transposed)
+    __shared__ double Di[kPB][kPB + 1];     // inverse of the panel's diagonal block
+    __shared__ double tP[kPB][8];
     const int u = blockIdx.y, tid = threadIdx.x;
-    const int w = warp_index(), lane = tid & 31;
     const int cbase = blockIdx.x * 8;
     const int q = r_eff[u];
+    const int nbl = (r + kPB - 1) / kPB;
     const double *Lu = L + (int64_t)u * r * r;
+    const double *Du = Dinv + (int64_t)u * nbl * kPB * kPB;
     float *Xu = X + (int64_t)u * r * DC;
+#pragma unroll 8
     for (int e = tid; e < q * 8; e += 256) {
         const int a = e / 8, cc = e % 8, col = cbase + cc;
-        zs[a * 8 + cc] = col < DC ? Y[((int64_t)u * r + a) * DC + col] : 0.0;
+        zs[a * 8 + cc] = col < DC ? __ldg(Y + ((int64_t)u * r + a) * DC + col) : 0.0;
     }
     __syncthreads();
-    const int pr = tid / 8, pc = tid % 8;  // panel row, column
-    // ---- forward substitution
-    for (int p0 = 0; p0 < q; p0 += PB) {
-        const int nb = min(PB, q - p0);
+    const int pr = tid / 8, pc = tid % 8;
+    auto load_dinv = [&](int blk, bool trans) {
+        const double *src = Du + (int64_t)blk * kPB * kPB;
+        double t[kPB * kPB / 256];
+#pragma unroll
+        for (int k = 0; k < kPB * kPB / 256; ++k) t[k] = __ldg(src + tid + 256 * k);
+#pragma unroll
+        for (int k = 0; k < kPB * kPB / 256; ++k) {
+            const int e = tid + 256 * k;
+            if (trans) Di[e % kPB][e / kPB] = t[k];
+            else Di[e / kPB][e % kPB] = t[k];
+        }
+    };
+    // ---- forward: z_P = Dinv_PP (y_P - L[P, 0:p0] z[0:p0])
+    for (int p0 = 0; p0 < q; p0 += kPB) {
+        const int nb = min(kPB, q - p0);
         double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
-        for (int b0 = 0; b0 < p0; b0 += CB) {  // z_P -= L[P, b0:b0+CB] z[b0:b0+CB], block staged in smem
-            const int nbk = min(CB, p0 - b0);
+        for (int b0 = 0; b0 < p0; b0 += kCBs) {
+            const int nbk = min(kCBs, p0 - b0);
+            double t[NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                const int e = tid + 256 * k, rr = e / kCBs, c2 = e % kCBs;
+                t[k] = (rr < nb && c2 < nbk) ? __ldg(Lu + (int64_t)(p0 + rr) * r + b0 + c2) : 0.0;
+            }
             __syncthreads();
-            for (int e = tid; e < nb * CB; e += 256) {
-                const int rr = e / CB, cc2 = e % CB;
-                Lb[rr][cc2] = cc2 < nbk ? Lu[(int64_t)(p0 + rr) * r + b0 + cc2] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                const int e = tid + 256 * k;
+                Lb[e / kCBs][e % kCBs] = t[k];
             }
             __syncthreads();
             if (pr < nb)
 #pragma unroll 8
-                for (int b = 0; b < nbk; ++b) acc = fma(-Lb[pr][b], zs[(b0 + b) * 8 + pc], acc);
+                for (int bb = 0; bb < nbk; ++bb) acc = fma(-Lb[pr][bb], zs[(b0 + bb) * 8 + pc], acc);
         }
-        if (pr < nb) zs[(p0 + pr) * 8 + pc] = acc;
-        for (int e = tid; e < nb * nb; e += 256) Ld[e / nb][e % nb] = Lu[(int64_t)(p0 + e / nb) * r + p0 + e % nb];
+        load_dinv(p0 / kPB, false);
+        tP[pr][pc] = acc;
         __syncthreads();
-        if (w < 8) {  // warp w solves column w of the panel block; lane i owns row p0 + i
-            double zi = lane < nb ? zs[(p0 + lane) * 8 + w] : 0.0;
-            double lrow[PB];  // this lane's row of the diagonal block, in registers
-#pragma unroll
-            for (int j = 0; j < PB; ++j) lrow[j] = (lane < nb && j < nb) ? Ld[lane][j] : 0.0;
-            const double inv = lane < nb ? 1.0 / Ld[lane][lane] : 0.0;
-#pragma unroll
-            for (int j = 0; j < PB; ++j) {
-                if (j < nb) {
-                    const double zj = __shfl_sync(0xffffffffu, zi * inv, j);
-                    if (lane == j) zi = zj;
-                    else if (lane > j) zi = fma(-lrow[j], zj, zi);
-                }
-            }
-            if (lane < nb) zs[(p0 + lane) * 8 + w] = zi;
+        if (pr < nb) {
+            double z = 0.0;
+#pragma unroll 8
+            for (int j = 0; j <= pr; ++j) z = fma(Di[pr][j], tP[j][pc], z);
+            zs[(p0 + pr) * 8 + pc] = z;
         }
         __syncthreads();
     }
-    // ---- backward substitution (upper-triangular L^T)
-    const int npan = (q + PB - 1) / PB;
+    // ---- backward (L^T upper): x_P = Dinv_PP^T (z_P - L[pe:q, P]^T x[pe:q])
+    const int npan = (q + kPB - 1) / kPB;
     for (int pi = npan - 1; pi >= 0; --pi) {
-        const int p0 = pi * PB, nb = min(PB, q - p0), pe = p0 + nb;
+        const int p0 = pi * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
         double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
-        for (int b0 = pe; b0 < q; b0 += CB) {  // x_P -= L[b0:b0+CB, P]^T x[b0:b0+CB], staged transposed
-            const int nbk = min(CB, q - b0);
+        for (int b0 = pe; b0 < q; b0 += kCBs) {
+            const int nbk = min(kCBs, q - b0);
+            double t[NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {  // row b0 + bb, column p0 + c2 (coalesced), staged transposed
+                const int e = tid + 256 * k, bb = e / kPB, c2 = e % kPB;
+                t[k] = (bb < nbk && c2 < nb) ? __ldg(Lu + (int64_t)(b0 + bb) * r + p0 + c2) : 0.0;
+            }
             __syncthreads();
-            for (int e = tid; e < CB * PB; e += 256) {
-                const int bb = e / PB, cc2 = e % PB;  // row b0 + bb, column p0 + cc2 (coalesced)
-                Lb[cc2][bb] = (bb < nbk && cc2 < nb) ? Lu[(int64_t)(b0 + bb) * r + p0 + cc2] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                const int e = tid + 256 * k;
+                Lb[e % kPB][e / kPB] = t[k];
             }
             __syncthreads();
             if (pr < nb)
 #pragma unroll 8
-                for (int b = 0; b < nbk; ++b) acc = fma(-Lb[pr][b], zs[(b0 + b) * 8 + pc], acc);
+                for (int bb = 0; bb < nbk; ++bb) acc = fma(-Lb[pr][bb], zs[(b0 + bb) * 8 + pc], acc);
         }
-        if (pr < nb) zs[(p0 + pr) * 8 + pc] = acc;
-        for (int e = tid; e < nb * nb; e += 256) Ld[e / nb][e % nb] = Lu[(int64_t)(p0 + e / nb) * r + p0 + e % nb];
+        load_dinv(pi, true);  // Di = Dinv_PP^T (upper triangular)
+        tP[pr][pc] = acc;
         __syncthreads();
-        if (w < 8) {
-            double zi = lane < nb ? zs[(p0 + lane) * 8 + w] : 0.0;
-            double lcol[PB];  // column `lane` of the diagonal block (row j, col lane), in registers
-#pragma unroll
-            for (int j = 0; j < PB; ++j) lcol[j] = (lane < nb && j < nb) ? Ld[j][lane] : 0.0;
-            const double inv = lane < nb ? 1.0 / Ld[lane][lane] : 0.0;
-#pragma unroll
-            for (int j = PB - 1; j >= 0; --j) {
-                if (j < nb) {
-                    const double xj = __shfl_sync(0xffffffffu, zi * inv, j);
-                    if (lane == j) zi = xj;
-                    else if (lane < j) zi = fma(-lcol[j], xj, zi);
-                }
-            }
-            if (lane < nb) zs[(p0 + lane) * 8 + w] = zi;
+        if (pr < nb) {
+            double x = 0.0;
+#pragma unroll 8
+            for (int j = pr; j < nb; ++j) x = fma(Di[pr][j], tP[j][pc], x);
+            zs[(p0 + pr) * 8 + pc] = x;
         }
         __syncthreads();
     }
@@ -272,12 +316,16 @@ __device__ __forceinline__ float ex2_approx_w(float x) {
 
 template <int D> struct WtSmem {
     static constexpr int kA = 128 * D * 2, kB = 128 * D * 2, kP = 128 * 128 * 2, kV = D * 128 * 2;
-    static constexpr int kOffA = 0, kOffB = kA, kOffP = kOffB + kB, kOffV = kOffP + kP;
-    static constexpr int kOffG = kOffV + kV, kOffKb = kOffG + 128 * 4, kOffX = kOffKb + D * 4;
-    static constexpr int kOffBar = kOffX + 2 * 128 * 4, kOffTb = kOffBar + 8;
+    static constexpr int kOffA = 0, kOffB = kA, kOffP = kOffB + 2 * kB, kOffV = kOffP + kP;  // B, V double-buffered
+    static constexpr int kOffG = kOffV + 2 * kV, kOffKb = kOffG + 2 * 128 * 4, kOffX = kOffKb + D * 4;
+    static constexpr int kOffBar = kOffX + 2 * 128 * 4, kOffTb = kOffBar + 16;
     static constexpr int kTotal = kOffTb + 8;
 };
 
+// Software pipeline over the CTA's 128-key slices: the next slice's K and V rows are loaded into
+// registers while the tensor cores run GEMM1 / GEMM2 of the current one, then written (swizzled;
+// V transposed) into the other B / V buffer; gamma_l = -g <k_l, kbar> comes from the same registers.
+// tcgen05.commit on bar1 after GEMM1(s) also retires GEMM2(s-1), which frees P and the old buffers.
 template <int D>
 __global__ void __launch_bounds__(kWTc, 1)
     weights_tc_kernel(const __nv_bfloat16 *__restrict__ K, const __nv_bfloat16 *__restrict__ V,
@@ -286,14 +334,18 @@ __global__ void __launch_bounds__(kWTc, 1)
                       const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
     using L = WtSmem<D>;
     constexpr int DC = D + 1;
+    constexpr int CPR = D / 8;          // 16-byte chunks per row
+    constexpr int NCH = 128 * CPR / kWTc;  // chunks per thread per slice (K: same chunk column, rows tid/CPR + k*RPS;
+                                           // V: row tid % 128, chunk columns tid/128 + 2k)
+    constexpr int RPS = kWTc / CPR;     // rows per pass
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw;  // offset 0 of the CTA's shared window (no static smem): 1024-aligned
     if (smem_u32(sm) & 1023u) __trap();
-    unsigned char *sA = sm + L::kOffA, *sB = sm + L::kOffB, *sP = sm + L::kOffP, *sV = sm + L::kOffV;
-    float *sG = reinterpret_cast<float *>(sm + L::kOffG);    // log2e * gamma_l of the slice [128]
+    unsigned char *sA = sm + L::kOffA, *sP = sm + L::kOffP;
+    float *sG = reinterpret_cast<float *>(sm + L::kOffG);    // [2][128] log2e * gamma_l of the slice
     float *sKb = reinterpret_cast<float *>(sm + L::kOffKb);  // kbar (fp32) [D]
     float *xch = reinterpret_cast<float *>(sm + L::kOffX);   // [2][128] row-sum exchange
-    uint64_t &bar = *reinterpret_cast<uint64_t *>(sm + L::kOffBar);
+    uint64_t *bar1 = reinterpret_cast<uint64_t *>(sm + L::kOffBar), *bar2 = bar1 + 1;
     uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
     const int tid = threadIdx.x, w = tid >> 5, row = tid & 127, half = tid >> 7;
     const int split = blockIdx.x, a0 = blockIdx.y * 128, u = blockIdx.z;
@@ -303,93 +355,121 @@ __global__ void __launch_bounds__(kWTc, 1)
     const __nv_bfloat16 *Vu = V + (int64_t)u * n * D;
     const double *st = stats + (int64_t)u * (kStatsHead + D);
     const double g = st[1], mstar = st[2];
-    constexpr int CPR = D / 8;
-    constexpr float kLog2e = 1.4426950408889634f;
 
     if (w == 0) umma::tmem_alloc(&tbase, 256);
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(bar1, 1);
+        mbar_init(bar2, 1);
         fence_mbar_init();
     }
     for (int j = tid; j < D; j += kWTc) sKb[j] = (float)st[kStatsHead + j];
-    // coreset rows (raw keys) -> A operand
-    for (int e = tid; e < 128 * CPR; e += kWTc) {
-        const int rw = e / CPR, cc = e % CPR;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (a0 + rw < re) {
-            const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + rw) * D
-                                              : Ku + (int64_t)S[(int64_t)u * r + a0 + rw] * D;
-            v = __ldg(reinterpret_cast<const uint4 *>(ksrow) + cc);
+    // coreset rows (raw keys) -> A operand (all of the thread's loads in flight)
+    {
+        uint4 av[NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int e = tid + k * kWTc, rw = e / CPR, cc = e % CPR;
+            av[k] = make_uint4(0, 0, 0, 0);
+            if (a0 + rw < re) {
+                const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + rw) * D
+                                                  : Ku + (int64_t)S[(int64_t)u * r + a0 + rw] * D;
+                av[k] = __ldg(reinterpret_cast<const uint4 *>(ksrow) + cc);
+            }
         }
-        *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(rw, cc * 8, 128)) = v;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int e = tid + k * kWTc, rw = e / CPR, cc = e % CPR;
+            *reinterpret_cast<uint4 *>(sA + umma::sw128_offset(rw, cc * 8, 128)) = av[k];
+        }
     }
-    // alpha_a = g(|kbar|^2 - <k_a, kbar>) - mstar in fp64, scaled by log2(e) for ex2
-    float alpha2 = 0.f;
+    // alpha_a = g(|kbar|^2 - <k_a, kbar>) - mstar in fp64, scaled by log2(e) for ex2: from shared
+    // memory (the staged A rows and an fp64 copy of kbar), the two halves of a row on its two threads
+    double *sKbd = reinterpret_cast<double *>(sP);  // sP is unused until the first exp epilogue
+    for (int j = tid; j < D; j += kWTc) sKbd[j] = st[kStatsHead + j];
+    __syncthreads();
     const bool row_ok = a0 + row < re;
-    if (row_ok) {
-        const __nv_bfloat16 *ksrow = KSin ? KSin + ((int64_t)u * r + a0 + row) * D
-                                          : Ku + (int64_t)S[(int64_t)u * r + a0 + row] * D;
-        double kk = 0.0, bb = 0.0;
-        for (int j = 0; j < D; ++j) {
-            const double kbj = st[kStatsHead + j];
-            kk = fma(to_f64(ksrow[j]), kbj, kk);
-            bb = fma(kbj, kbj, bb);
-        }
-        alpha2 = (float)((g * (bb - kk) - mstar) * 1.4426950408889634);
+    double kk = 0.0, bb = 0.0;
+#pragma unroll 8
+    for (int j = half * (D / 2); j < (half + 1) * (D / 2); ++j) {
+        const double kbj = sKbd[j];
+        const __nv_bfloat16 kv = *reinterpret_cast<const __nv_bfloat16 *>(sA + umma::sw128_offset(row, j, 128));
+        kk = fma(to_f64(kv), kbj, kk);
+        bb = fma(kbj, kbj, bb);
     }
+    double *xd = reinterpret_cast<double *>(sP) + D;  // [2][128] half-row partials
+    xd[half * 256 + row] = kk;
+    xd[half * 256 + 128 + row] = bb;
+    __syncthreads();
+    float alpha2 = 0.f;
+    if (row_ok) {
+        const double kks = xd[row] + xd[256 + row], bbs = xd[128 + row] + xd[256 + 128 + row];
+        alpha2 = (float)((g * (bbs - kks) - mstar) * 1.4426950408889634);
+    }
+    __syncthreads();  // sP is reused below
     const float g2 = (float)(g * 1.4426950408889634);
     const int64_t rows = ceil_div(n, splits);
     const int64_t lo = (int64_t)split * rows, hi = std::min<int64_t>(n, lo + rows);
+    const int nsl = (int)ceil_div(std::max<int64_t>(0, hi - lo), 128);
     const uint32_t tS = tbase, tO = tbase + 128, lane_off = (uint32_t)((w & 3) * 32) << 16;
-    uint32_t phase = 0;
-    float rowsum = 0.f;
-    bool first = true;
-    for (int64_t l0 = lo; l0 < hi; l0 += 128) {
-        // keys of the slice -> B operand of GEMM1 (K-major, swizzled); V^T -> B operand of GEMM2
-        for (int e = tid; e < 128 * CPR; e += kWTc) {
-            const int rw = e / CPR, cc = e % CPR;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (l0 + rw < hi) v = __ldg(reinterpret_cast<const uint4 *>(Ku + (l0 + rw) * D) + cc);
-            *reinterpret_cast<uint4 *>(sB + umma::sw128_offset(rw, cc * 8, 128)) = v;
+    const int cc_t = tid % CPR, r_t = tid / CPR;  // this thread's chunk column and first row
+
+    uint4 kreg[NCH], vreg[NCH];
+    auto prefetch = [&](int64_t l0) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int64_t l = l0 + r_t + k * RPS;
+            kreg[k] = l < hi ? __ldg(reinterpret_cast<const uint4 *>(Ku + l * D) + cc_t) : make_uint4(0, 0, 0, 0);
+            // V: lane <-> key row, so that the transposed 2-byte stores below are bank-conflict free
+            const int64_t lv = l0 + (tid & 127);
+            const int ccv = (tid >> 7) + 2 * k;
+            vreg[k] = lv < hi ? __ldg(reinterpret_cast<const uint4 *>(Vu + lv * D) + ccv) : make_uint4(0, 0, 0, 0);
         }
-        for (int e = tid; e < 128 * CPR; e += kWTc) {
-            const int rw = e / CPR, cc = e % CPR;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (l0 + rw < hi) v = __ldg(reinterpret_cast<const uint4 *>(Vu + (l0 + rw) * D) + cc);
-            const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&v);
+    };
+    auto stage = [&](int buf) {
+        unsigned char *sB = sm + L::kOffB + buf * L::kB, *sV = sm + L::kOffV + buf * L::kV;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int rw = r_t + k * RPS;
+            *reinterpret_cast<uint4 *>(sB + umma::sw128_offset(rw, cc_t * 8, 128)) = kreg[k];
+            const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&vreg[k]);
+            const int lvr = tid & 127, ccv = (tid >> 7) + 2 * k;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(cc * 8 + q, rw, D)) = pv[q];
-        }
-        if (tid < 128) {  // log2e * gamma_l = -log2e g <k_l, kbar> for key l0 + tid
-            const int64_t l = l0 + tid;
+                *reinterpret_cast<__nv_bfloat16 *>(sV + umma::sw128_offset(ccv * 8 + q, lvr, D)) = pv[q];
+            // gamma: partial <k_l, kbar> over this chunk, reduced over the CPR lanes of the row
+            const __nv_bfloat16 *pk = reinterpret_cast<const __nv_bfloat16 *>(&kreg[k]);
             float gm = 0.f;
-            if (l < hi) {
-                const uint4 *kr = reinterpret_cast<const uint4 *>(Ku + l * D);
-#pragma unroll 4
-                for (int cc = 0; cc < CPR; ++cc) {
-                    const uint4 v = __ldg(kr + cc);
-                    const __nv_bfloat16 *pv = reinterpret_cast<const __nv_bfloat16 *>(&v);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) gm = fmaf(__bfloat162float(pv[q]), sKb[cc * 8 + q], gm);
-                }
-            }
-            sG[tid] = -g2 * gm;
+            for (int q = 0; q < 8; ++q) gm = fmaf(__bfloat162float(pk[q]), sKb[cc_t * 8 + q], gm);
+#pragma unroll
+            for (int o = 1; o < CPR; o <<= 1) gm += __shfl_xor_sync(0xffffffffu, gm, o);
+            if (cc_t == 0) sG[buf * 128 + rw] = -g2 * gm;
         }
-        umma::fence_async_smem();
-        umma::fence_before_sync();
-        __syncthreads();
-        umma::fence_after_sync();
+    };
+
+    float rowsum = 0.f;
+    if (nsl > 0) {
+        prefetch(lo);
+        stage(0);
+    }
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    for (int s = 0; s < nsl; ++s) {
+        const int buf = s & 1;
+        const int64_t l0 = lo + (int64_t)s * 128;
         if (tid == 0) {
-            umma::gemm_128xNxK(tS, smem_u32(sA), smem_u32(sB), 128, D, false);
-            umma::commit(&bar);
+            umma::gemm_128xNxK(tS, smem_u32(sA), smem_u32(sm + L::kOffB + buf * L::kB), 128, D, false);
+            umma::commit(bar1);  // also retires GEMM2(s-1)
         }
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
+        if (s + 1 < nsl) prefetch(l0 + 128);  // global loads in flight during GEMM1 / exp
+        mbar_wait(bar1, (uint32_t)(s & 1));
         umma::fence_after_sync();
         // P = exp2(g2 S + alpha2 + gamma2) for 64 columns per thread (its half), bf16 -> smem
         const int nl = (int)std::min<int64_t>(128, hi - l0);
         {
+            const float *gmb = sG + buf * 128;
             const int cbase = half * 64;
             float v[64];
             umma::ld32(tS + lane_off + cbase, v);
@@ -401,8 +481,8 @@ __global__ void __launch_bounds__(kWTc, 1)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int cl = g8 * 8 + 2 * i, l = cbase + cl;
-                    const float p0 = (row_ok && l < nl) ? ex2_approx_w(fmaf(g2, v[cl], alpha2 + sG[l])) : 0.f;
-                    const float p1 = (row_ok && l + 1 < nl) ? ex2_approx_w(fmaf(g2, v[cl + 1], alpha2 + sG[l + 1])) : 0.f;
+                    const float p0 = (row_ok && l < nl) ? ex2_approx_w(fmaf(g2, v[cl], alpha2 + gmb[l])) : 0.f;
+                    const float p1 = (row_ok && l + 1 < nl) ? ex2_approx_w(fmaf(g2, v[cl + 1], alpha2 + gmb[l + 1])) : 0.f;
                     const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
                     rs[i] += __bfloat162float(pb.x) + __bfloat162float(pb.y);
                     pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
@@ -417,18 +497,25 @@ __global__ void __launch_bounds__(kWTc, 1)
         __syncthreads();
         umma::fence_after_sync();
         if (tid == 0) {
-            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sV), D, 128, !first);
-            umma::commit(&bar);
+            umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sm + L::kOffV + buf * L::kV), D, 128, s > 0);
+            umma::commit(bar2);
         }
-        mbar_wait(&bar, phase);  // smem (sB, sV, sP) reusable and O updated
-        phase ^= 1u;
+        if (s + 1 < nsl) {
+            stage(buf ^ 1);  // B/V buffers of slice s-1: retired by the bar1 wait above
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncthreads();
+            umma::fence_after_sync();
+        }
+    }
+    if (nsl > 0) {
+        mbar_wait(bar2, (uint32_t)((nsl - 1) & 1));
         umma::fence_after_sync();
-        first = false;
     }
     xch[half * 128 + row] = rowsum;
     __syncthreads();
     float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + row) * DC;
-    if (first) {  // empty key range: zero partial
+    if (nsl == 0) {  // empty key range: zero partial
         if (row_ok && half == 0)
             for (int c = 0; c < DC; ++c) out[c] = 0.f;
     } else {
@@ -490,14 +577,16 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
 
 template <int D>
 int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
-                   cudaStream_t st) {
+                   double *Dinv, cudaStream_t st) {
+    const int nbl = (Dm.r + kPB - 1) / kPB;
+    weights_dinv_kernel<<<dim3(nbl, Dm.units()), 32, 0, st>>>(L, r_eff, Dm.r, Dinv);
     const size_t smem = (size_t)8 * Dm.r * sizeof(double);
     auto sk = weights_solve_kernel<D>;
-    // the kernel also holds ~25 KB of static smem: always raise the dynamic limit
+    // the kernel also holds ~45 KB of static smem: always raise the dynamic limit
     cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 g2((D + 1 + 7) / 8, Dm.units());
-    sk<<<g2, 256, smem, st>>>(Yfull, L, r_eff, Dm.r, X);
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    sk<<<g2, 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 template <typename T, int D>
@@ -506,7 +595,9 @@ int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_
     double *Yfull = nullptr;
     const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st);
     if (k1 < 0) return -1;
-    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, st);
+    // scratch for the diagonal-block inverses: after Y~ in the weights workspace (carve_weights)
+    double *Dinv = Yfull + (size_t)Dm.units() * Dm.r * (D + 1);
+    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st);
     if (k2 < 0) return -1;
     dim3 g3(Dm.r, Dm.units());
     gather_ks_kernel<T, D><<<g3, 128, 0, st>>>(static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
@@ -542,12 +633,12 @@ int launch_weights_partial_ks(const Dims &D, const void *K, const void *V, const
 }
 
 int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
-                         cudaStream_t st) {
+                         double *Dinv, cudaStream_t st) {
     switch (D.d) {
-        case 16: return launch_solve_d<16>(D, Yfull, L, r_eff, X, st);
-        case 32: return launch_solve_d<32>(D, Yfull, L, r_eff, X, st);
-        case 64: return launch_solve_d<64>(D, Yfull, L, r_eff, X, st);
-        case 128: return launch_solve_d<128>(D, Yfull, L, r_eff, X, st);
+        case 16: return launch_solve_d<16>(D, Yfull, L, r_eff, X, Dinv, st);
+        case 32: return launch_solve_d<32>(D, Yfull, L, r_eff, X, Dinv, st);
+        case 64: return launch_solve_d<64>(D, Yfull, L, r_eff, X, Dinv, st);
+        case 128: return launch_solve_d<128>(D, Yfull, L, r_eff, X, Dinv, st);
     }
     return -1;
 }
