@@ -383,13 +383,13 @@ def main():
     if not args.no_e2e and mode == "replicas":
         Qh, Kh, Vh = (x.pin_memory() for x in (Q, K, V))
         for _ in range(max(1, args.warmup)):
-            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev)
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block)
         tt = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev)
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block)
             tt.append(time.perf_counter() - t0)
         te = torch.tensor([sum(tt)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -398,7 +398,8 @@ def main():
         d2h = O.numel() * O.element_size()
         e2e = {"value": queries_per_rank * world * args.steps / float(te.item()), "unit": "queries/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "timing": "host wall clock around forward_host (H2D, wildcat_forward, D2H, sync)"}
+               "timing": ("host wall clock around forward_host: H2D of K, Q; wildcat_select (H2D of V overlapped "
+                          "on a side stream); wildcat_weights; wildcat_attend; D2H of O; sync")}
 
     # accuracy vs exact attention (the metric's third part) on 4096 seeded query rows, fp64 on the
     # GPU (torch matmul; a measurement helper outside the timed region), and the exact bf16 SDPA

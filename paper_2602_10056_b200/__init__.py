@@ -23,7 +23,7 @@ import torch
 from . import _binding as B
 from ._binding import WildcatError, lib  # noqa: F401
 
-__all__ = ["forward", "forward_host", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
+__all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range"]
 
 
@@ -140,19 +140,75 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None,
     return O
 
 
+class HostForward:
+    """End-to-end WildCat on host (CPU) buffers with persistent device buffers.
+
+    Per call: H2D of K and Q, wildcat_select, then wildcat_weights once the H2D of V (issued on a
+    side stream after K and Q, so it overlaps the selection) has landed, wildcat_attend, D2H of O
+    into a pinned buffer, synchronise.  Every step is a C-ABI call (include/wildcat.h)."""
+
+    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, device="cuda"):
+        dev = torch.device(device)
+        self.dev, self.r = dev, int(r)
+        self.Qd = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
+        self.Kd = torch.empty(K.shape, dtype=K.dtype, device=dev)
+        self.Vd = torch.empty(K.shape, dtype=K.dtype, device=dev)
+        self.Od = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
+        self.Oh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+        self.shape = B.make_shape(self.Qd, self.Kd, r)
+        self.opts = B.make_opts(seed, beta, rq, clip, block=block)
+        units, d = self.shape.batch * self.shape.heads_kv, self.shape.d
+        self.S = torch.empty(units, r, dtype=torch.int32, device=dev)
+        self.reff = torch.empty(units, dtype=torch.int32, device=dev)
+        self.L = torch.empty(units, r, r, dtype=torch.float64, device=dev)
+        self.stats = torch.empty(units, STATS_STRIDE(d), dtype=torch.float64, device=dev)
+        self.KS = torch.empty(units, r, d, dtype=K.dtype, device=dev)
+        self.X = torch.empty(units, r, d + 1, dtype=torch.float32, device=dev)
+        self.vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
+        self.vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
+        self.ws_s = B.alloc_workspace(self.shape, B.WC_OP_SELECT, dev)
+        self.ws_w = B.alloc_workspace(self.shape, B.WC_OP_WEIGHTS, dev)
+        na = B.workspace_bytes(self.shape, B.WC_OP_ATTEND)
+        self.ws_a = B.alloc_workspace(self.shape, B.WC_OP_ATTEND, dev) if na else None
+        self.s_main = torch.cuda.Stream(dev)
+        self.s_v = torch.cuda.Stream(dev)
+        self.ev_kq = torch.cuda.Event()
+        self.ev_v = torch.cuda.Event()
+
+    def __call__(self, Qh, Kh, Vh):
+        sm, sv = self.s_main, self.s_v
+        with torch.cuda.stream(sm):
+            self.Kd.copy_(Kh, non_blocking=True)
+            self.Qd.copy_(Qh, non_blocking=True)
+            self.ev_kq.record(sm)
+        with torch.cuda.stream(sv):
+            sv.wait_event(self.ev_kq)  # V after K and Q on the link, overlapping the selection
+            self.Vd.copy_(Vh, non_blocking=True)
+            self.ev_v.record(sv)
+        B.wildcat_select(self.shape, self.opts, self.Qd, self.Kd, self.S, self.reff, self.L, self.stats, self.ws_s, sm)
+        sm.wait_event(self.ev_v)
+        B.wildcat_weights(self.shape, self.opts, self.Kd, self.Vd, self.S, self.reff, self.L, self.stats, self.KS,
+                          self.X, self.vmin, self.vmax, self.ws_w, sm)
+        B.wildcat_attend(self.shape, self.opts, self.Qd, self.KS, self.X, self.reff, self.vmin, self.vmax, self.Od,
+                         self.ws_a, sm)
+        with torch.cuda.stream(sm):
+            self.Oh.copy_(self.Od, non_blocking=True)
+        sm.synchronize()
+        return self.Oh
+
+
+_host_cache: dict = {}
+
+
 def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, stream=None):
-    """End-to-end call with host (CPU) buffers: H2D copies, the CUDA forward, D2H copy of O."""
-    dev = torch.device(device)
-    s = torch.cuda.current_stream(dev) if stream is None else stream
-    with torch.cuda.stream(s):
-        Qd = Q.to(dev, non_blocking=True)
-        Kd = K.to(dev, non_blocking=True)
-        Vd = V.to(dev, non_blocking=True)
-        Od = forward(Qd, Kd, Vd, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, stream=s)
-        O = torch.empty(Od.shape, dtype=Od.dtype, pin_memory=True)
-        O.copy_(Od, non_blocking=True)
-    s.synchronize()
-    return O
+    """End-to-end call with host (CPU) buffers: H2D copies, the CUDA path, D2H copy of O (pinned).
+    Device buffers persist per (shapes, options); see HostForward."""
+    key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), str(device))
+    hf = _host_cache.get(key)
+    if hf is None:
+        hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, device=device)
+        _host_cache[key] = hf
+    return hf(Q, K, V)
 
 
 # --------------------------------------------------------------------------- n-sharded (PAR3)

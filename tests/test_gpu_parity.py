@@ -162,3 +162,18 @@ def test_headline_full_size_pivots_and_sampled_outputs():
     Oo = oracle.attend(Q64[rows], K64[sel["S"]], X, sel["r_eff"], 1 / math.sqrt(128), V64.min(0), V64.max(0))
     err = np.abs(O[0, 0][rows] - Oo).max() / np.abs(V64).max()
     assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("block", [1, 16])
+def test_forward_host_matches_device_forward(block):
+    # the end-to-end host-buffer path (split C-ABI calls, V copied on a side stream) == wildcat_forward
+    import paper_2602_10056_b200 as wc
+
+    Q, K, V = qkv(2, 4, 2, 300, 3000, 64, "bf16", "C", seed=12)
+    dev = torch.device("cuda:0")
+    Od = wc.forward(Q.to(dev), K.to(dev), V.to(dev), 64, seed=12, block=block)
+    torch.cuda.synchronize()
+    Qh, Kh, Vh = (x.pin_memory() for x in (Q, K, V))
+    for _ in range(2):  # second call reuses the cached device buffers
+        Oh = wc.forward_host(Qh, Kh, Vh, 64, seed=12, block=block)
+        assert torch.equal(Oh, Od.cpu())
