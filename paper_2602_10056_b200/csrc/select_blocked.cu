@@ -56,6 +56,16 @@ __device__ __forceinline__ double accept_uniform(uint64_t seed, uint32_t cand, u
     return (x * 67108864.0 + y) * (1.0 / 9007199254740992.0);
 }
 
+// 1/sqrt(h) in fp64: MUFU rsqrt of the float value, then two Newton steps (2^-23 -> 2^-46 -> fp64
+// rounding); the library rsqrt(double) carries a much longer dependent chain.
+__device__ __forceinline__ double rsqrt_nr(double h) {
+    if (!(h > 1e-30 && h < 1e30)) return 1.0 / sqrt(h);
+    double y = (double)rsqrtf((float)h);
+    y = y * fma(-0.5 * h * y, y, 1.5);
+    y = y * fma(-0.5 * h * y, y, 1.5);
+    return y;
+}
+
 struct BlkArgs {
     const void *K;
     double *stats;
@@ -551,7 +561,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                 const double vp = __shfl_sync(0xffffffffu, my_vp, j);
                 const bool dup = __any_sync(0xffffffffu, my_acc && my_cs == sj);
                 if (!dup && vp < hjj) {
-                    const double rinv = rsqrt(hjj);
+                    const double rinv = rsqrt_nr(hjj);
                     const double fe = hej * rinv;  // F[i+nacc, s_e] = H[j][e] / sqrt(H[j][j])
                     if (e < kBMax) Fcand[nacc * kBMax + e] = (e > j && e < bsz) ? fe : 0.0;
 #pragma unroll
@@ -732,9 +742,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     if (key < hi) {
                         nxt[key] = pl;
                         double *ftr = a.FT + ((int64_t)u * n + key) * ftl + i;  // key-major copy of the new rows
+                        if (i & 1) {  // 16-byte stores from the first even index (FT rows are 32-byte aligned)
+                            if (na > 0) ftr[0] = f[0];
 #pragma unroll
-                        for (int aa = 0; aa < kBMax; ++aa)
-                            if (aa < na) ftr[aa] = f[aa];
+                            for (int aa = 1; aa < kBMax - 1; aa += 2) {
+                                if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
+                                else if (aa < na) ftr[aa] = f[aa];
+                            }
+                            if (kBMax - 1 < na) ftr[kBMax - 1] = f[kBMax - 1];
+                        } else {
+#pragma unroll
+                            for (int aa = 0; aa < kBMax; aa += 2) {
+                                if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
+                                else if (aa < na) ftr[aa] = f[aa];
+                            }
+                        }
                         for (int x = 0; x < na; ++x) {
                             if (sA[x] == key) {  // L[i+x][i..i+x] = F[i..i+x, s_x]
                                 double *Lr = a.L + ((int64_t)u * a.r + i + x) * a.r + i;
