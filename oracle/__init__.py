@@ -69,6 +69,9 @@ def lib():
             L.wco_exact_attention.argtypes = [_c_i64, _c_i64, _c_i32, _p, _p, _p, _c_dbl, _p]
             L.wco_forward.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_dbl,
                                       _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p, _p, _p]
+            L.wco_forward_binned.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32,
+                                             _c_dbl, _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p,
+                                             _p, _p]
             L.wco_accept_uniform.argtypes = [_c_u64, ctypes.c_uint32, _c_u64]
             L.wco_accept_uniform.restype = _c_dbl
             L.wco_select_blocked.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64,
@@ -233,10 +236,13 @@ def exact_attention(Q, K, V, beta=None):
     return O
 
 
-def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1):
+def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1, bins=1):
     """Alg 4 over [batch, heads, seq, d] arrays (float64 copies of the inputs).
+    bins > 1: Alg 2 with B contiguous bins (wco_forward_binned; stats are then per bin).
 
     Returns dict(O, S, r_eff, stats, X)."""
+    if bins > 1:
+        return forward_binned(Q, K, V, r, bins, seed=seed, beta=beta, rq=rq, clip=clip, block=block)
     Q = _f64(Q)
     K = _f64(K)
     V = _f64(V)
@@ -253,6 +259,36 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1):
                            _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st), _ptr(X))
     if rc:
         raise RuntimeError(f"wco_forward failed ({rc})")
+    return dict(O=O, S=S, r_eff=reff, stats=st, X=X)
+
+
+def bin_rank(n, r, bins):
+    """Per-bin rank rb = min(ceil(r / B), n / B) (reading Z13) and the coreset slots B * rb."""
+    rb = min(-(-r // bins), n // bins)
+    return rb, bins * rb
+
+
+def forward_binned(Q, K, V, r, bins, seed=0, beta=None, rq=-1.0, clip=True, block=1):
+    """Alg 4 with Alg 2 binning (wco_forward_binned).  Returns dict(O, S, r_eff, stats, X) with
+    S [units][B*rb], stats [units][B][5] (tau_b, g_b, mstar_b, R_K^b, R_Q), X [units][B*rb][d+1]."""
+    Q = _f64(Q)
+    K = _f64(K)
+    V = _f64(V)
+    batch, hq, m, d = Q.shape
+    _, hkv, n, _ = K.shape
+    beta = 1.0 / np.sqrt(d) if beta is None else float(beta)
+    units = batch * hkv
+    _, R = bin_rank(n, r, bins)
+    O = np.zeros_like(Q)
+    S = np.full((units, R), -1, dtype=np.int32)
+    reff = np.zeros(units, dtype=np.int32)
+    st = np.zeros((units, bins, 5))
+    X = np.zeros((units, R, d + 1))
+    rc = lib().wco_forward_binned(batch, hq, hkv, m, n, d, r, bins, beta, float(rq), int(seed), int(bool(clip)),
+                                  int(block), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st),
+                                  _ptr(X))
+    if rc:
+        raise RuntimeError(f"wco_forward_binned failed ({rc})")
     return dict(O=O, S=S, r_eff=reff, stats=st, X=X)
 
 

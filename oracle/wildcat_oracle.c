@@ -654,6 +654,116 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
     return status;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Algorithm 4 WildCat with B > 1 bins (Alg 2 CompressKV).
+ * Readings (Z12, Z13, Z23):
+ *   - kbar is the row mean over ALL n keys of the unit and the recentring is global;
+ *     R_Q and the value range are over the unit's full query group / full V;
+ *   - bins are contiguous: bin b = rows [b nb, (b+1) nb), nb = n / B; this build requires
+ *     B | n (the paper's "evenly divide (or reshape)");
+ *   - per bin: R_K^b = max ||k_l - kbar|| over the bin, tau_b = Eq. 7 with n_b = nb
+ *     (Z12), RPNys on the bin's centred keys at rank rb = min(ceil(r/B), nb) (Z13), with the
+ *     Philox stream of unit id u*B + b (Z23), sequential or blocked (block > 1);
+ *   - the bin coresets are concatenated in bin order with their valid rows only, so
+ *     the unit's coreset is r_eff = sum_b r_eff_b rows; V_S, w from each bin's own Nystrom
+ *     weights over its own keys (W block diagonal); then Alg 3 over the whole coreset.
+ * Outputs (may be NULL): S [units][B*rb] unit-level key indices, -1 past r_eff;
+ * r_eff [units]; binstats [units][B][5] = tau_b, g_b, mstar_b, R_K^b, R_Q;
+ * X [units][B*rb][d+1] (rows past r_eff zero).  Returns -2 if B does not divide n.   */
+/* ------------------------------------------------------------------------ */
+int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d,
+                       int32_t r, int32_t bins, double beta, double rq, uint64_t seed, int32_t clip,
+                       int32_t block, const double *Q, const double *K, const double *V, double *O,
+                       int32_t *S_out, int32_t *reff_out, double *binstats_out, double *X_out)
+{
+    if (bins < 1 || n % bins != 0 || bins > r) return -2;
+    const int64_t nb = n / bins;
+    int32_t rb = (r + bins - 1) / bins;
+    if (rb > nb) rb = (int32_t)nb;
+    const int32_t R = bins * rb, dc = d + 1, group = hq / hkv;
+    double *kbar = (double *)malloc(sizeof(double) * d);
+    double *Xb = (double *)malloc(sizeof(double) * (size_t)rb * dc);
+    double *X = (double *)malloc(sizeof(double) * (size_t)R * dc);
+    double *KS = (double *)malloc(sizeof(double) * (size_t)R * d);
+    double *vmin = (double *)malloc(sizeof(double) * d);
+    double *vmax = (double *)malloc(sizeof(double) * d);
+    int32_t *Sb = (int32_t *)malloc(sizeof(int32_t) * rb);
+    int32_t *S = (int32_t *)malloc(sizeof(int32_t) * R);
+    if (!kbar || !Xb || !X || !KS || !vmin || !vmax || !Sb || !S) return -1;
+    int status = 0;
+    for (int32_t bt = 0; bt < batch && status == 0; ++bt) {
+        for (int32_t h = 0; h < hkv && status == 0; ++h) {
+            uint64_t u = (uint64_t)bt * hkv + h;
+            const double *Ku = K + (size_t)u * n * d;
+            const double *Vu = V + (size_t)u * n * d;
+            const double *Qg = Q + ((size_t)bt * hq + (size_t)h * group) * m * d;
+            for (int c = 0; c < d; ++c) {  /* value range over the full V */
+                double lo = Vu[c], hi = Vu[c];
+                for (int64_t l = 1; l < n; ++l) {
+                    double v = Vu[l * d + c];
+                    if (v < lo) lo = v;
+                    if (v > hi) hi = v;
+                }
+                vmin[c] = lo;
+                vmax[c] = hi;
+            }
+            double st[5];
+            wco_prologue(n, d, Ku, (int64_t)group * m, Qg, rq, beta, kbar, st);  /* global kbar, R_Q */
+            const double rqu = st[4];
+            memset(X, 0, sizeof(double) * (size_t)R * dc);
+            memset(KS, 0, sizeof(double) * (size_t)R * d);
+            for (int a = 0; a < R; ++a) S[a] = -1;
+            int32_t tot = 0;
+            for (int32_t b = 0; b < bins && status == 0; ++b) {
+                const double *Kb = Ku + (size_t)b * nb * d;
+                const double *Vb = Vu + (size_t)b * nb * d;
+                double rk2 = 0.0;  /* R_K^b over the bin's centred keys */
+                for (int64_t l = 0; l < nb; ++l) {
+                    double s2 = 0.0;
+                    for (int j = 0; j < d; ++j) {
+                        double c = Kb[l * d + j] - kbar[j];
+                        s2 += c * c;
+                    }
+                    if (s2 > rk2) rk2 = s2;
+                }
+                const double rk = sqrt(rk2);
+                const double tau = wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
+                const double g = beta / (tau * tau), mstar = g * rk * rk;
+                int32_t re = 0;
+                const uint64_t ub = u * (uint64_t)bins + (uint64_t)b;  /* Z23 */
+                if (block > 1)
+                    status = wco_select_blocked(nb, d, rb, block, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL,
+                                                NULL, NULL, NULL);
+                else
+                    status = wco_select(nb, d, rb, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL, NULL, NULL);
+                if (status) break;
+                status = wco_weights(nb, d, rb, Kb, Vb, Sb, re, kbar, g, mstar, Xb);
+                if (status) break;
+                for (int a = 0; a < re; ++a) {  /* concatenate the bin's valid rows */
+                    S[tot + a] = (int32_t)(b * nb + Sb[a]);
+                    memcpy(KS + (size_t)(tot + a) * d, Kb + (size_t)Sb[a] * d, sizeof(double) * d);
+                    memcpy(X + (size_t)(tot + a) * dc, Xb + (size_t)a * dc, sizeof(double) * dc);
+                }
+                tot += re;
+                if (binstats_out) {
+                    double *bs = binstats_out + ((size_t)u * bins + b) * 5;
+                    bs[0] = tau; bs[1] = g; bs[2] = mstar; bs[3] = rk; bs[4] = rqu;
+                }
+            }
+            if (status) break;
+            for (int32_t hh = 0; hh < group; ++hh) {
+                size_t qoff = ((size_t)bt * hq + (size_t)h * group + hh) * m * d;
+                wco_attend(m, d, R, Q + qoff, KS, X, tot, beta, vmin, vmax, clip, O + qoff);
+            }
+            if (S_out) memcpy(S_out + (size_t)u * R, S, sizeof(int32_t) * R);
+            if (reff_out) reff_out[u] = tot;
+            if (X_out) memcpy(X_out + (size_t)u * R * dc, X, sizeof(double) * (size_t)R * dc);
+        }
+    }
+    free(kbar); free(Xb); free(X); free(KS); free(vmin); free(vmax); free(Sb); free(S);
+    return status;
+}
+
 int wco_num_threads(void)
 {
 #ifdef _OPENMP

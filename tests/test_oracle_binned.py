@@ -1,0 +1,85 @@
+"""Pins for the binned oracle (Alg 2 CompressKV with B bins; readings Z12, Z13, Z23).
+
+Checked against things other than the binned code itself:
+  * B = 1 is the unbinned Alg 4 oracle bit for bit;
+  * full-rank bins (r_b = n_b) make every bin's Nystrom weights exact, so WildCat reproduces exact
+    softmax attention over ALL keys (Prop.) -- this pins the global recentring, the
+    concatenation of the bin coresets and the per-bin value compression at once;
+  * bins whose keys repeat m distinct vectors exhaust at r_eff_b = m and are again exact;
+  * structural consistency (SPEC "binning consistency"): each bin's pivots are the single-bin RPNys
+    on the bin slice with the global kbar, tau_b from the bin's radius and n_b, and stream u*B + b;
+  * tau_b from the bin's own radius R_K^b (numpy max norm) and n_b.
+"""
+import numpy as np
+import pytest
+
+from paper_2602_10056_b200.inputs import make_qkv
+
+
+def _qkv(batch, hq, hkv, m, n, d, family="G", seed=0, distinct=None):
+    Q, K, V = make_qkv(batch, hq, hkv, m, n, d, "f32", family, seed, distinct)
+    return Q.double().numpy(), K.double().numpy(), V.double().numpy()
+
+
+@pytest.mark.parametrize("block", [1, 8])
+def test_one_bin_is_unbinned(orc, block):
+    Q, K, V = _qkv(2, 4, 2, 40, 120, 16, "C", seed=3)
+    a = orc.forward(Q, K, V, 20, seed=3, block=block)
+    b = orc.forward_binned(Q, K, V, 20, 1, seed=3, block=block)
+    assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["r_eff"], b["r_eff"])
+    assert np.array_equal(a["O"], b["O"]) and np.array_equal(a["X"], b["X"])
+    assert np.allclose(b["stats"][:, 0, :], a["stats"], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("bins", [2, 4, 8])
+def test_full_rank_bins_are_exact_attention(orc, bins):
+    Q, K, V = _qkv(1, 2, 1, 30, 64, 8, "G", seed=5)
+    res = orc.forward_binned(Q, K, V, 64, bins, seed=5, clip=False)
+    assert res["r_eff"][0] == 64
+    ex = np.stack([orc.exact_attention(Q[0, h], K[0, 0], V[0, 0]) for h in range(2)])
+    err = np.abs(res["O"][0] - ex).max() / np.abs(V).max()
+    assert err < 1e-8, err
+
+
+def test_distinct_key_bins_exhaust_and_are_exact(orc):
+    # every bin repeats 5 distinct key vectors: r_eff_b = 5 per bin, exact attention overall
+    bins, nb, d = 4, 40, 8
+    rng = np.random.Generator(np.random.PCG64(11))
+    K = np.concatenate([rng.standard_normal((5, d))[rng.integers(0, 5, nb)] for _ in range(bins)])[None, None]
+    V = rng.standard_normal((1, 1, bins * nb, d))
+    Q = rng.standard_normal((1, 1, 25, d))
+    res = orc.forward_binned(Q, K, V, 40, bins, seed=11, clip=False)
+    assert res["r_eff"][0] == 5 * bins
+    ex = orc.exact_attention(Q[0, 0], K[0, 0], V[0, 0])
+    assert np.abs(res["O"][0, 0] - ex).max() / np.abs(V).max() < 1e-8
+
+
+@pytest.mark.parametrize("block", [1, 4])
+def test_bin_pivots_are_single_bin_rpnys(orc, block):
+    Q, K, V = _qkv(1, 2, 1, 50, 240, 16, "L", seed=7)
+    bins, r = 4, 30
+    res = orc.forward_binned(Q, K, V, r, bins, seed=7, block=block)
+    rb, R = orc.bin_rank(240, r, bins)
+    K64 = K[0, 0]
+    kbar, st = orc.prologue(K64, Q[0].reshape(-1, 16))
+    tot = 0
+    for b in range(bins):
+        Kb = K64[b * 60:(b + 1) * 60]
+        rk = np.sqrt(((Kb - kbar) ** 2).sum(1).max())
+        tau = orc.temperature(1 / np.sqrt(16), st["rq"], rk, 60)
+        g = (1 / np.sqrt(16)) / tau ** 2
+        assert np.isclose(res["stats"][0, b, 3], rk, rtol=1e-13) and np.isclose(res["stats"][0, b, 0], tau, rtol=1e-13)
+        if block > 1:
+            sel = orc.select_blocked(Kb, kbar, g, g * rk * rk, rb, block, seed=7, unit=b)
+        else:
+            sel = orc.select(Kb, kbar, g, g * rk * rk, rb, seed=7, unit=b)
+        re = sel["r_eff"]
+        assert np.array_equal(res["S"][0, tot:tot + re], sel["S"][:re] + b * 60)
+        tot += re
+    assert res["r_eff"][0] == tot and np.all(res["S"][0, tot:] == -1)
+
+
+def test_bins_must_divide_n(orc):
+    Q, K, V = _qkv(1, 1, 1, 10, 50, 8, seed=1)
+    with pytest.raises(RuntimeError):
+        orc.forward_binned(Q, K, V, 12, 3, seed=1)
