@@ -8,23 +8,33 @@
  * Problem (Alg 4): queries Q, keys K, values V, scale beta, rank r
  *   -> O^ = WtdAttn(Q, CompressKV(K, V, R_Q, beta, r)),
  * computed independently for every "unit" u = b*heads_kv + h (one (batch,
- * kv-head) pair; bins B = 1).  Query head hq uses unit (b, hq / (heads_q/heads_kv)).
+ * kv-head) pair).  Query head hq uses unit (b, hq / (heads_q/heads_kv)).
+ *
+ * Binning (shape.bins = B > 1; Alg 2; readings Z12, Z13, Z23 of DESIGN.md):
+ * the keys of a unit are recentred with the unit's kbar, then split into B contiguous bins of
+ * nb = n/B keys (B must divide n: WC_EUNSUPPORTED otherwise); bin b gets its own R_K^b, tau_b
+ * (Eq. 7 with n_b) and RPNys at rank rb = min(ceil(r/B), nb) with the Philox stream of
+ * sub-unit u*B + b; the bin coresets are concatenated.  Sizes below use R = B*rb (= r when B = 1).
  *
  * Layouts (row-major, contiguous, device memory unless stated):
  *   Q, O   [batch][heads_q ][m][d]   dtype
  *   K, V   [batch][heads_kv][n][d]   dtype
- *   S      int32  [units][r]         global key index (0..n-1) of the i-th pivot, -1 past r_eff
- *   r_eff  int32  [units]            number of pivots actually drawn (<= r, Z3)
- *   L      double [units][r][r]      lower-triangular Cholesky factor of h~(K_S,K_S) in pivot
- *                                    order, L[a][b] = F[b, S[a]] (b <= a), 0 elsewhere (Z6)
- *   stats  double [units][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, nblocks, ncand,
+ *   S      int32  [units][R]         key index (0..n-1) of the i-th pivot, -1 past r_eff; with
+ *                                    bins, the bins' valid pivots concatenated in bin order
+ *   r_eff  int32  [units]            number of pivots actually drawn (<= R, Z3; sum over bins)
+ *   L      double [units][B][rb][rb] lower-triangular Cholesky factor of h~(K_S,K_S) in pivot
+ *                                    order, L[a][b] = F[b, S[a]] (b <= a), 0 elsewhere (Z6);
+ *                                    one factor per bin (row/column index bin-local)
+ *   stats  double [units][B][WC_STATS_STRIDE(d)] = tau, g, mstar, R_K, R_Q, T0, nblocks, ncand,
  *                                    Fread, Fdot, 0 (x6), kbar[d].  Selection bookkeeping: nblocks =
  *                                    blocks (sequential: rounds) run, ncand = candidates drawn,
  *                                    Fread = sum over blocks of the F rows re-read at the block
  *                                    start (sequential: sum_i i) -- the F traffic is 8 n Fread bytes;
  *                                    Fdot = sum over blocks of (rows re-read x pivots accepted)
- *   KS     dtype  [units][r][d]      coreset keys, uncentred (Alg 2 "K_S <- K_S + kbar")
- *   X      float  [units][r][d+1]    [V_S, w] = W [V, 1_n]  (Alg 2 "Compress values")
+ *   KS     dtype  [units][R][d]      coreset keys, uncentred (Alg 2 "K_S <- K_S + kbar"), rows
+ *                                    in the order of S, zero past r_eff
+ *   X      float  [units][R][d+1]    [V_S, w] = W [V, 1_n]  (Alg 2 "Compress values"); with
+ *                                    bins W is block diagonal (each bin's weights over its keys)
  *   vmin, vmax dtype [units][d]      columnwise range of V (Alg 4)
  *
  * Conventions:
@@ -48,7 +58,7 @@ extern "C" {
 
 #define WC_OK 0
 #define WC_EINVAL -1        /* null pointer, bad enum, unknown flag, opts->block > WC_MAX_BLOCK */
-#define WC_ESHAPE -2        /* r < 1, r > n, bins != 1, heads_q % heads_kv != 0, d not in {16,32,64,128}, m < 0 */
+#define WC_ESHAPE -2        /* r < 1, r > n, bins < 1 or > r, heads_q % heads_kv != 0, d not in {16,32,64,128}, m < 0 */
 #define WC_EDTYPE -3        /* dtype not WC_F32 / WC_BF16 */
 #define WC_EWORKSPACE -4    /* ws too small or misaligned (needs 256-byte alignment) */
 #define WC_ECUDA -5         /* CUDA launch / runtime error */
@@ -76,7 +86,7 @@ typedef struct wc_shape {
     int32_t heads_kv;  /* >= 1 */
     int32_t d;         /* head dim: 16, 32, 64 or 128 */
     int32_t r;         /* coreset size, 1 <= r <= n ("rank r") */
-    int32_t bins;      /* B of Alg 2; must be 1 in this build */
+    int32_t bins;      /* B of Alg 2: 1 <= B <= r, B must divide n */
     int32_t dtype;     /* WC_F32 or WC_BF16 (element type of Q, K, V, O, KS, vmin, vmax) */
     int32_t reserved;
     int64_t m;         /* queries per q-head, >= 0 */

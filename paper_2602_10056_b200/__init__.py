@@ -63,6 +63,7 @@ class Cache:
     r_eff: torch.Tensor
     heads_kv: int
     opts: B.wc_opts
+    shape: B.wc_shape = None  # the selection's shape (n, r, bins)
 
 
 _ws_cache: dict = {}
@@ -78,18 +79,20 @@ def _workspace(shape, op, device):
     return t
 
 
-def select(Q, K, r, seed=0, beta=None, rq=None, block=1, stream=None) -> Selection:
-    """RPNys selection; block >= 2 selects the blocked (accelerated) variant (reading Z22)."""
+def select(Q, K, r, seed=0, beta=None, rq=None, block=1, bins=1, stream=None) -> Selection:
+    """RPNys selection; block >= 2 selects the blocked (accelerated) variant (reading Z22); bins > 1
+    runs Alg 2 binning (S [units][R] concatenated over bins, L [units*B][rb][rb], stats per bin)."""
     Q, K = _cont(Q), _cont(K)
     _require_cuda(Q, K)
-    shape = B.make_shape(Q, K, r)
+    shape = B.make_shape(Q, K, r, bins=bins)
     opts = B.make_opts(seed, beta, rq, block=block)
     units = shape.batch * shape.heads_kv
+    rb, R = B.coreset_rows(shape.n, r, bins)
     dev = K.device
-    S = torch.empty(units, r, dtype=torch.int32, device=dev)
+    S = torch.empty(units, R, dtype=torch.int32, device=dev)
     reff = torch.empty(units, dtype=torch.int32, device=dev)
-    L = torch.empty(units, r, r, dtype=torch.float64, device=dev)
-    stats = torch.empty(units, STATS_STRIDE(shape.d), dtype=torch.float64, device=dev)
+    L = torch.empty(units * bins, rb, rb, dtype=torch.float64, device=dev)
+    stats = torch.empty(units * bins, STATS_STRIDE(shape.d), dtype=torch.float64, device=dev)
     ws = _workspace(shape, B.WC_OP_SELECT, dev)
     B.wildcat_select(shape, opts, Q, K, S, reff, L, stats, ws, stream)
     return Selection(S, reff, L, stats, shape, opts)
@@ -99,15 +102,16 @@ def weights(K, V, sel: Selection, stream=None) -> Cache:
     K, V = _cont(K), _cont(V)
     _require_cuda(K, V)
     shape = sel.shape
-    units, r, d = shape.batch * shape.heads_kv, shape.r, shape.d
+    units, d = shape.batch * shape.heads_kv, shape.d
+    _, R = B.coreset_rows(shape.n, shape.r, shape.bins)
     dev = K.device
-    KS = torch.empty(units, r, d, dtype=K.dtype, device=dev)
-    X = torch.empty(units, r, d + 1, dtype=torch.float32, device=dev)
+    KS = torch.empty(units, R, d, dtype=K.dtype, device=dev)
+    X = torch.empty(units, R, d + 1, dtype=torch.float32, device=dev)
     vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
     vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
     ws = _workspace(shape, B.WC_OP_WEIGHTS, dev)
     B.wildcat_weights(shape, sel.opts, K, V, sel.S, sel.r_eff, sel.L, sel.stats, KS, X, vmin, vmax, ws, stream)
-    return Cache(KS, X, vmin, vmax, sel.r_eff, shape.heads_kv, sel.opts)
+    return Cache(KS, X, vmin, vmax, sel.r_eff, shape.heads_kv, sel.opts, shape)
 
 
 def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
@@ -115,8 +119,13 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
     _require_cuda(Q)
     b, hq, m, d = Q.shape
     units, r, _ = cache.KS.shape
-    shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=r, bins=1,
-                       dtype=B._dtype_code(Q), reserved=0, m=m, n=max(r, 1))
+    if cache.shape is not None:  # the selection's (n, r, bins) define the coreset layout
+        cs = cache.shape
+        shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=cs.r, bins=cs.bins,
+                           dtype=B._dtype_code(Q), reserved=0, m=m, n=cs.n)
+    else:
+        shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=r, bins=1,
+                           dtype=B._dtype_code(Q), reserved=0, m=m, n=max(r, 1))
     opts = B.wc_opts(beta=cache.opts.beta if beta is None else float(beta), rq=cache.opts.rq,
                      seed=cache.opts.seed,
                      flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), block=0)
@@ -127,12 +136,13 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
 
 
 def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None, r_eff=None, block=1,
-            stream=None):
-    """Alg 4 WildCat on device tensors.  Returns O (and fills S / r_eff if given).
-    block >= 2: blocked (accelerated) RPCholesky selection with b = block (reading Z22)."""
+            bins=1, stream=None):
+    """Alg 4 WildCat on device tensors.  Returns O (and fills S [units][R] / r_eff if given).
+    block >= 2: blocked (accelerated) RPCholesky selection with b = block (reading Z22).
+    bins > 1: Alg 2 binning with B = bins (R = B * min(ceil(r/B), n/B) coreset rows per unit)."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
-    shape = B.make_shape(Q, K, r)
+    shape = B.make_shape(Q, K, r, bins=bins)
     opts = B.make_opts(seed, beta, rq, clip, block=block)
     O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD, K.device)
@@ -147,7 +157,7 @@ class HostForward:
     side stream after K and Q, so it overlaps the selection) has landed, wildcat_attend, D2H of O
     into a pinned buffer, synchronise.  Every step is a C-ABI call (include/wildcat.h)."""
 
-    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, device="cuda"):
+    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, bins=1, device="cuda"):
         dev = torch.device(device)
         self.dev, self.r = dev, int(r)
         self.Qd = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
@@ -155,15 +165,16 @@ class HostForward:
         self.Vd = torch.empty(K.shape, dtype=K.dtype, device=dev)
         self.Od = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
         self.Oh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
-        self.shape = B.make_shape(self.Qd, self.Kd, r)
+        self.shape = B.make_shape(self.Qd, self.Kd, r, bins=bins)
         self.opts = B.make_opts(seed, beta, rq, clip, block=block)
         units, d = self.shape.batch * self.shape.heads_kv, self.shape.d
-        self.S = torch.empty(units, r, dtype=torch.int32, device=dev)
+        rb, R = B.coreset_rows(self.shape.n, r, bins)
+        self.S = torch.empty(units, R, dtype=torch.int32, device=dev)
         self.reff = torch.empty(units, dtype=torch.int32, device=dev)
-        self.L = torch.empty(units, r, r, dtype=torch.float64, device=dev)
-        self.stats = torch.empty(units, STATS_STRIDE(d), dtype=torch.float64, device=dev)
-        self.KS = torch.empty(units, r, d, dtype=K.dtype, device=dev)
-        self.X = torch.empty(units, r, d + 1, dtype=torch.float32, device=dev)
+        self.L = torch.empty(units * bins, rb, rb, dtype=torch.float64, device=dev)
+        self.stats = torch.empty(units * bins, STATS_STRIDE(d), dtype=torch.float64, device=dev)
+        self.KS = torch.empty(units, R, d, dtype=K.dtype, device=dev)
+        self.X = torch.empty(units, R, d + 1, dtype=torch.float32, device=dev)
         self.vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
         self.vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
         self.ws_s = B.alloc_workspace(self.shape, B.WC_OP_SELECT, dev)
@@ -200,13 +211,13 @@ class HostForward:
 _host_cache: dict = {}
 
 
-def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, stream=None):
+def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, bins=1, stream=None):
     """End-to-end call with host (CPU) buffers: H2D copies, the CUDA path, D2H copy of O (pinned).
     Device buffers persist per (shapes, options); see HostForward."""
-    key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), str(device))
+    key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), int(bins), str(device))
     hf = _host_cache.get(key)
     if hf is None:
-        hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, device=device)
+        hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, bins=bins, device=device)
         _host_cache[key] = hf
     return hf(Q, K, V)
 

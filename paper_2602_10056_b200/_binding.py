@@ -98,12 +98,18 @@ def _dtype_code(t: torch.Tensor) -> int:
     raise WildcatError(f"unsupported dtype {t.dtype}")
 
 
-def make_shape(Q, K, r, m=None) -> wc_shape:
+def make_shape(Q, K, r, m=None, bins=1) -> wc_shape:
     b, hkv, n, d = K.shape
     hq = Q.shape[1] if Q is not None else hkv
     mm = (Q.shape[2] if Q is not None else 0) if m is None else m
-    return wc_shape(batch=b, heads_q=hq, heads_kv=hkv, d=d, r=int(r), bins=1, dtype=_dtype_code(K),
+    return wc_shape(batch=b, heads_q=hq, heads_kv=hkv, d=d, r=int(r), bins=int(bins), dtype=_dtype_code(K),
                     reserved=0, m=mm, n=n)
+
+
+def coreset_rows(n: int, r: int, bins: int = 1):
+    """(rb, R): per-bin rank min(ceil(r/B), n/B) and coreset rows B*rb per unit (Z13; R = r if B = 1)."""
+    rb = min(-(-int(r) // int(bins)), int(n) // int(bins))
+    return rb, int(bins) * rb
 
 
 def make_opts(seed=0, beta=None, rq=None, clip=True, block=1) -> wc_opts:

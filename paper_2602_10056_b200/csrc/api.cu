@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libwildcat.so (declared in include/wildcat.h).
 // Argument validation, workspace carving and kernel sequencing only; every arithmetic step
 // of the method runs in the sm_100a kernels of prologue.cu / select.cu / weights.cu / attend.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -55,7 +56,8 @@ int check_shape(const wc_shape *s) {
     if (s->batch < 1 || s->heads_q < 1 || s->heads_kv < 1 || s->heads_q % s->heads_kv) return WC_ESHAPE;
     if (!(s->d == 16 || s->d == 32 || s->d == 64 || s->d == 128)) return WC_ESHAPE;
     if (s->n < 1 || s->n > (int64_t)0x7fffffff || s->m < 0 || s->r < 1 || s->r > s->n) return WC_ESHAPE;
-    if (s->bins != 1) return WC_EUNSUPPORTED;
+    if (s->bins < 1 || s->bins > s->r) return WC_ESHAPE;
+    if (s->n % s->bins) return WC_EUNSUPPORTED;  // bins must divide n in this build (Alg 2 "evenly divide")
     return WC_OK;
 }
 
@@ -64,6 +66,31 @@ wc::Dims dims_of(const wc_shape *s) {
     D.batch = s->batch; D.hq = s->heads_q; D.hkv = s->heads_kv; D.d = s->d; D.r = s->r; D.dtype = s->dtype;
     D.m = s->m; D.n = s->n;
     return D;
+}
+
+// Binning plan (Alg 2; readings Z12, Z13, Z23).  D: the unit-level problem (prologue,
+// value range, attend with R coreset rows); Ds: the sub-unit problem of the selection and weights
+// kernels -- unit u, bin b -> sub-unit u*B + b with nb = n/B keys and rank rb = min(ceil(r/B), nb).
+// With B = 1, Ds = D and R = r.
+struct Plan {
+    wc::Dims D, Ds, Da;  // unit level, sub-unit level, attend (unit level with r = R)
+    int B, rb, R;
+};
+Plan plan_of(const wc_shape *s) {
+    Plan p;
+    p.D = dims_of(s);
+    p.B = s->bins;
+    const int64_t nb = s->n / p.B;
+    p.rb = (int)std::min<int64_t>((s->r + p.B - 1) / p.B, nb);
+    p.R = p.B * p.rb;
+    p.Ds = p.D;
+    p.Ds.hkv = p.D.hkv * p.B;
+    p.Ds.hq = p.D.hq * p.B;  // keeps group() = hq/hkv; the sub-unit dims never touch Q
+    p.Ds.n = nb;
+    p.Ds.r = p.rb;
+    p.Da = p.D;
+    p.Da.r = p.R;
+    return p;
 }
 
 size_t esize(const wc_shape *s) { return s->dtype == WC_F32 ? 4 : 2; }
@@ -90,25 +117,33 @@ int run_select(const wc::Dims &D, const wc_opts *o, const void *K, double *stats
 int check_opts(const wc_opts *o, const wc_shape *s) {
     if (!o) return WC_EINVAL;
     if (o->block > (uint32_t)WC_MAX_BLOCK) return WC_EINVAL;
-    if (o->block >= 2 && s->r > 1024) return WC_EUNSUPPORTED;
+    if (o->block >= 2 && plan_of(s).rb > 1024) return WC_EUNSUPPORTED;
     return WC_OK;
 }
 
+void carve_prologue(Carver &c, const wc::Dims &D, wc::ProloguePartials &pp) {
+    const size_t U = D.units();
+    const int P = wc::prologue_num_splits(D);
+    pp.P = P;
+    pp.colsum = c.take<double>(U * P * D.d);
+    pp.vmin = c.take<float>(U * P * D.d);
+    pp.vmax = c.take<float>(U * P * D.d);
+    pp.rq2 = c.take<double>(U * P);
+    pp.rk2 = c.take<double>(U * P);
+}
+
+// Selection workspace: unit-level prologue partials and nrm2 ([units][n] == [units*B][nb]), the
+// selection state at the sub-unit level, and (B > 1) the unit-level stats and sub-unit S / r_eff.
 struct SelectWs {
     wc::ProloguePartials pp;
     wc::SelectBufs sb;
+    double *stats_u = nullptr;
+    int32_t *Ssub = nullptr, *reff_sub = nullptr;
 };
-
-void carve_select(Carver &c, const wc_shape *s, SelectWs &w) {
-    const wc::Dims D = dims_of(s);
+void carve_select(Carver &c, const Plan &p, SelectWs &w) {
+    carve_prologue(c, p.D, w.pp);
+    const wc::Dims &D = p.Ds;
     const size_t U = D.units();
-    const int P = wc::prologue_num_splits(D);
-    w.pp.P = P;
-    w.pp.colsum = c.take<double>(U * P * D.d);
-    w.pp.vmin = c.take<float>(U * P * D.d);
-    w.pp.vmax = c.take<float>(U * P * D.d);
-    w.pp.rq2 = c.take<double>(U * P);
-    w.pp.rk2 = c.take<double>(U * P);
     w.sb.nrm2 = c.take<double>(U * D.n);
     w.sb.p = c.take<double>(2 * U * D.n);
     w.sb.F = c.take<double>(U * wc::f_elems_per_unit(D.n, D.r, wc::select_ctas_per_unit(D)));
@@ -116,24 +151,58 @@ void carve_select(Carver &c, const wc_shape *s, SelectWs &w) {
     w.sb.bar = c.take<unsigned>(U);
     w.sb.gsum = c.take<double>(U * 2 * (size_t)((D.n + 31) / 32));
     w.sb.FT = c.take<double>(U * (size_t)D.n * wc::ft_ld(D.r));
+    if (p.B > 1) {
+        w.stats_u = c.take<double>((size_t)p.D.units() * WC_STATS_STRIDE(D.d));
+        w.Ssub = c.take<int32_t>(U * D.r);
+        w.reff_sub = c.take<int32_t>(U);
+    }
 }
 
-float *carve_weights(Carver &c, const wc_shape *s, wc::ProloguePartials *pp) {
-    const wc::Dims D = dims_of(s);
+// Weights workspace at the sub-unit level: fp32 split partials of Y~, the fp64 Y~, the inverted
+// diagonal blocks of L; (B > 1) sub-unit S / r_eff and the unpacked KS / X.
+struct WeightsWs {
+    float *Ypart = nullptr;
+    int32_t *Ssub = nullptr, *reff_sub = nullptr;
+    void *KSsub = nullptr;
+    float *Xsub = nullptr;
+};
+void carve_weights(Carver &c, const wc_shape *s, const Plan &p, WeightsWs &w) {
+    const wc::Dims &D = p.Ds;
     const size_t U = D.units();
-    if (pp) {
-        const int P = wc::prologue_num_splits(D);
-        pp->P = P;
-        pp->colsum = c.take<double>(U * P * D.d);
-        pp->vmin = c.take<float>(U * P * D.d);
-        pp->vmax = c.take<float>(U * P * D.d);
-        pp->rq2 = c.take<double>(U * P);
-        pp->rk2 = c.take<double>(U * P);
-    }
-    // fp32 split partials of Y~, followed by the fp64 reduced Y~ (8-byte aligned: the float count is even)
     const size_t parts = U * wc::weights_num_splits(D) * (size_t)D.r * (D.d + 1);
-    // + the fp64 Y~, + the inverted diagonal blocks of L (solve scratch)
-    return c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1) + 2 * U * wc::dinv_elems(D.r));
+    w.Ypart = c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1) + 2 * U * wc::dinv_elems(D.r));
+    if (p.B > 1) {
+        w.Ssub = c.take<int32_t>(U * D.r);
+        w.reff_sub = c.take<int32_t>(U);
+        w.KSsub = c.take<char>(U * (size_t)D.r * D.d * esize(s));
+        w.Xsub = c.take<float>(U * (size_t)D.r * (D.d + 1));
+    }
+}
+
+// wildcat_forward workspace: selection + weights + the forward's own buffers.
+struct ForwardWs {
+    SelectWs sel;
+    WeightsWs wts;
+    double *stats = nullptr;  // [units*B][stride] (sub-unit stats; == unit stats when B = 1)
+    int32_t *S = nullptr, *reff = nullptr;
+    double *L = nullptr;
+    void *KS = nullptr, *vmin = nullptr, *vmax = nullptr, *aimg = nullptr;
+    float *X = nullptr;
+};
+void carve_forward(Carver &c, const wc_shape *s, const Plan &p, ForwardWs &w) {
+    carve_select(c, p, w.sel);
+    const size_t U = p.D.units(), Us = p.Ds.units();
+    w.stats = c.take<double>(Us * WC_STATS_STRIDE(p.D.d));
+    w.S = c.take<int32_t>(U * p.R);
+    w.reff = c.take<int32_t>(U);
+    w.L = c.take<double>(Us * (size_t)p.rb * p.rb);
+    carve_weights(c, s, p, w.wts);
+    w.KS = c.take<char>(U * (size_t)p.R * p.D.d * esize(s));
+    w.X = c.take<float>(U * (size_t)p.R * (p.D.d + 1));
+    char *vr = c.take<char>(2 * U * (size_t)p.D.d * esize(s));
+    w.vmin = vr;
+    w.vmax = vr ? vr + U * (size_t)p.D.d * esize(s) : nullptr;
+    w.aimg = c.take<char>(wc::attend_ws_bytes(p.Da));
 }
 
 int finish(int launches) {
@@ -149,6 +218,60 @@ int ws_ok(void *ws, size_t have, size_t need) {
     return WC_OK;
 }
 
+size_t rounded(const Carver &c) { return ((c.off + 255) & ~size_t(255)) + 256; }
+
+// A0 + A1/A2 for a plan.  B = 1: prologue into `stats`, selection into S / r_eff / L.
+// B > 1: unit prologue into w.stats_u, per-bin stats into `stats` ([units*B]), selection at the
+// sub-unit level into w.Ssub / w.reff_sub and L ([units][B][rb][rb]); then S / r_eff packed.
+int select_stage(const Plan &p, const wc_opts *o, double beta, double rq, const void *Q, const void *K, const void *V,
+                 SelectWs &w, double *stats, int32_t *S, int32_t *r_eff, double *L, void *vmin, void *vmax,
+                 cudaStream_t st, int *launches) {
+    const size_t Us = p.Ds.units();
+    int32_t *Ssel = p.B > 1 ? w.Ssub : S;
+    int32_t *Rsel = p.B > 1 ? w.reff_sub : r_eff;
+    if (cudaMemsetAsync(Ssel, 0xff, Us * p.rb * sizeof(int32_t), st) != cudaSuccess) return WC_ECUDA;
+    if (cudaMemsetAsync(L, 0, Us * (size_t)p.rb * p.rb * sizeof(double), st) != cudaSuccess) return WC_ECUDA;
+    int k = wc::launch_prologue(p.D, Q, K, V, rq, beta, w.pp, p.B > 1 ? w.stats_u : stats, w.sb.nrm2, vmin, vmax, st);
+    if (k < 0) return WC_ECUDA;
+    *launches += k;
+    if (p.B > 1) {
+        if ((k = wc::launch_bins_stats(p.D, p.B, beta, w.stats_u, w.sb.nrm2, stats, st)) < 0) return WC_ECUDA;
+        *launches += k;
+    }
+    tmark(st);
+    if ((k = run_select(p.Ds, o, K, stats, w.sb, Ssel, Rsel, L, st)) < 0) return k;
+    *launches += k;
+    if (p.B > 1) {
+        if ((k = wc::launch_bins_pack(p.D, p.B, p.rb, w.Ssub, w.reff_sub, nullptr, nullptr, S, r_eff, nullptr, nullptr,
+                                      st)) < 0)
+            return WC_ECUDA;
+        *launches += k;
+    }
+    return WC_OK;
+}
+
+// A3 + A4 for a plan (S / r_eff packed at the unit level when B > 1; unpacked here).
+int weights_stage(const Plan &p, const void *K, const void *V, const int32_t *S, const int32_t *r_eff, const double *L,
+                  const double *stats, WeightsWs &w, bool have_sub, void *KS, float *X, cudaStream_t st, int *launches) {
+    int k;
+    if (p.B == 1) {
+        if ((k = wc::launch_weights(p.D, K, V, S, r_eff, L, stats, w.Ypart, KS, X, st)) < 0) return WC_ECUDA;
+        *launches += k;
+        return WC_OK;
+    }
+    if (!have_sub) {
+        if ((k = wc::launch_bins_unpack(p.D, p.B, p.rb, S, w.Ssub, w.reff_sub, st)) < 0) return WC_ECUDA;
+        *launches += k;
+    }
+    if ((k = wc::launch_weights(p.Ds, K, V, w.Ssub, w.reff_sub, L, stats, w.Ypart, w.KSsub, w.Xsub, st)) < 0)
+        return WC_ECUDA;
+    *launches += k;
+    if ((k = wc::launch_bins_pack(p.D, p.B, p.rb, w.Ssub, w.reff_sub, w.KSsub, w.Xsub, nullptr, nullptr, KS, X, st)) < 0)
+        return WC_ECUDA;
+    *launches += k;
+    return WC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -156,46 +279,36 @@ extern "C" {
 size_t wc_workspace_bytes(const wc_shape *s, int op) {
     if (check_shape(s) != WC_OK) return 0;
     Carver c(nullptr);
-    const wc::Dims D = dims_of(s);
-    const size_t U = D.units();
+    const Plan p = plan_of(s);
     switch (op) {
         case WC_OP_SELECT: {
             SelectWs w;
-            carve_select(c, s, w);
+            carve_select(c, p, w);
             break;
         }
-        case WC_OP_WEIGHTS:
-            carve_weights(c, s, nullptr);
-            {
-                wc::ProloguePartials pp;
-                carve_weights(c, s, &pp);
-            }
+        case WC_OP_WEIGHTS: {
+            WeightsWs w;
+            carve_weights(c, s, p, w);
+            wc::ProloguePartials pp;
+            carve_prologue(c, p.D, pp);
             break;
+        }
         case WC_OP_ATTEND: {
-            const size_t a = wc::attend_ws_bytes(D);
+            const size_t a = wc::attend_ws_bytes(p.Da);
             return a ? ((a + 255) & ~size_t(255)) + 256 : 0;
         }
         case WC_OP_FORWARD: {
-            SelectWs w;
-            carve_select(c, s, w);
-            c.take<double>(U * WC_STATS_STRIDE(D.d));
-            c.take<int32_t>(U * D.r);
-            c.take<int32_t>(U);
-            c.take<double>(U * (size_t)D.r * D.r);
-            carve_weights(c, s, nullptr);
-            c.take<char>(U * (size_t)D.r * D.d * esize(s));
-            c.take<float>(U * (size_t)D.r * (D.d + 1));
-            c.take<char>(2 * U * (size_t)D.d * esize(s));
-            c.take<char>(wc::attend_ws_bytes(D));
+            ForwardWs w;
+            carve_forward(c, s, p, w);
             break;
         }
         case WC_OP_FORWARD_NSHARD:
-            if (D.units() != 1) return 0;
-            return wc::ns_workspace_bytes(D);
+            if (p.D.units() != 1 || p.B != 1) return 0;
+            return wc::ns_workspace_bytes(p.D);
         default:
             return 0;
     }
-    return ((c.off + 255) & ~size_t(255)) + 256;
+    return rounded(c);
 }
 
 int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const void *K, int32_t *S,
@@ -208,21 +321,17 @@ int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_SELECT)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const wc::Dims D = dims_of(s);
+    const Plan p = plan_of(s);
     Carver c(ws);
     SelectWs w;
-    carve_select(c, s, w);
-    const size_t U = D.units();
-    if (cudaMemsetAsync(S, 0xff, U * D.r * sizeof(int32_t), st) != cudaSuccess) return WC_ECUDA;
-    if (cudaMemsetAsync(L, 0, U * (size_t)D.r * D.r * sizeof(double), st) != cudaSuccess) return WC_ECUDA;
+    carve_select(c, p, w);
     tmark(st, true);
-    int n1 = wc::launch_prologue(D, Q, K, nullptr, rq, beta_of(s, o), w.pp, stats, w.sb.nrm2, nullptr, nullptr, st);
-    if (n1 < 0) return WC_ECUDA;
+    int launches = 0;
+    if ((rc = select_stage(p, o, beta_of(s, o), rq, Q, K, nullptr, w, stats, S, r_eff, L, nullptr, nullptr, st,
+                           &launches)))
+        return rc;
     tmark(st);
-    int n2 = run_select(D, o, K, stats, w.sb, S, r_eff, L, st);
-    if (n2 < 0) return n2;
-    tmark(st);
-    return finish(n1 + n2);
+    return finish(launches);
 }
 
 int wildcat_weights(const wc_shape *s, const wc_opts *o, const void *K, const void *V, const int32_t *S,
@@ -234,19 +343,19 @@ int wildcat_weights(const wc_shape *s, const wc_opts *o, const void *K, const vo
     if (!K || !V || !S || !r_eff || !L || !stats || !KS || !X || !vmin || !vmax) return WC_EINVAL;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_WEIGHTS)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const wc::Dims D = dims_of(s);
+    const Plan p = plan_of(s);
     Carver c(ws);
-    float *Ypart = carve_weights(c, s, nullptr);
+    WeightsWs w;
+    carve_weights(c, s, p, w);
     wc::ProloguePartials pp;
-    carve_weights(c, s, &pp);
+    carve_prologue(c, p.D, pp);
     tmark(st, true);
-    int n1 = wc::launch_vrange(D, V, pp, vmin, vmax, st);
-    if (n1 < 0) return WC_ECUDA;
+    int launches = wc::launch_vrange(p.D, V, pp, vmin, vmax, st);
+    if (launches < 0) return WC_ECUDA;
     tmark(st);
-    int n2 = wc::launch_weights(D, K, V, S, r_eff, L, stats, Ypart, KS, X, st);
-    if (n2 < 0) return WC_ECUDA;
+    if ((rc = weights_stage(p, K, V, S, r_eff, L, stats, w, false, KS, X, st, &launches))) return rc;
     tmark(st);
-    return finish(n1 + n2);
+    return finish(launches);
 }
 
 int wildcat_attend(const wc_shape *s, const wc_opts *o, const void *Q, const void *KS, const float *X,
@@ -258,7 +367,7 @@ int wildcat_attend(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_ATTEND)))) return rc;
     const int clip = (o && (o->flags & WC_NO_CLIP)) ? 0 : 1;
     tmark(static_cast<cudaStream_t>(stream), true);
-    int n1 = wc::launch_attend(dims_of(s), Q, KS, X, r_eff, vmin, vmax, beta_of(s, o), clip, O, ws,
+    int n1 = wc::launch_attend(plan_of(s).Da, Q, KS, X, r_eff, vmin, vmax, beta_of(s, o), clip, O, ws,
                                static_cast<cudaStream_t>(stream));
     if (n1 < 0) return WC_ECUDA;
     tmark(static_cast<cudaStream_t>(stream));
@@ -275,42 +384,32 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     if (rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;  // m = 0: R_Q = max over no queries = 0
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const wc::Dims D = dims_of(s);
-    const size_t U = D.units();
+    const Plan p = plan_of(s);
     Carver c(ws);
-    SelectWs w;
-    carve_select(c, s, w);
-    double *stats = c.take<double>(U * WC_STATS_STRIDE(D.d));
-    int32_t *S = c.take<int32_t>(U * D.r);
-    int32_t *reff = c.take<int32_t>(U);
-    double *L = c.take<double>(U * (size_t)D.r * D.r);
-    float *Ypart = carve_weights(c, s, nullptr);
-    void *KS = c.take<char>(U * (size_t)D.r * D.d * esize(s));
-    float *X = c.take<float>(U * (size_t)D.r * (D.d + 1));
-    char *vr = c.take<char>(2 * U * (size_t)D.d * esize(s));
-    void *vmin = vr, *vmax = vr + U * (size_t)D.d * esize(s);
-    void *aimg = c.take<char>(wc::attend_ws_bytes(D));
-    if (S_out) S = S_out;
-    if (reff_out) reff = reff_out;
-    if (cudaMemsetAsync(S, 0xff, U * D.r * sizeof(int32_t), st) != cudaSuccess) return WC_ECUDA;
-    if (cudaMemsetAsync(L, 0, U * (size_t)D.r * D.r * sizeof(double), st) != cudaSuccess) return WC_ECUDA;
+    ForwardWs w;
+    carve_forward(c, s, p, w);
+    int32_t *S = S_out ? S_out : w.S;
+    int32_t *reff = reff_out ? reff_out : w.reff;
     const double beta = beta_of(s, o);
-    int total = 0, k;
+    int launches = 0;
     tmark(st, true);
-    if ((k = wc::launch_prologue(D, Q, K, V, rq, beta, w.pp, stats, w.sb.nrm2, vmin, vmax, st)) < 0) return WC_ECUDA;
-    total += k;
+    if ((rc = select_stage(p, o, beta, rq, Q, K, V, w.sel, w.stats, S, reff, w.L, w.vmin, w.vmax, st, &launches)))
+        return rc;
     tmark(st);
-    if ((k = run_select(D, o, K, stats, w.sb, S, reff, L, st)) < 0) return k;
-    total += k;
-    tmark(st);
-    if ((k = wc::launch_weights(D, K, V, S, reff, L, stats, Ypart, KS, X, st)) < 0) return WC_ECUDA;
-    total += k;
+    // B > 1: the sub-unit S / r_eff of the selection are still in w.sel
+    if (p.B > 1) {
+        w.wts.Ssub = w.sel.Ssub;
+        w.wts.reff_sub = w.sel.reff_sub;
+    }
+    if ((rc = weights_stage(p, K, V, S, reff, w.L, w.stats, w.wts, true, w.KS, w.X, st, &launches))) return rc;
     tmark(st);
     const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
-    if ((k = wc::launch_attend(D, Q, KS, X, reff, vmin, vmax, beta, clip, O, aimg, st)) < 0) return WC_ECUDA;
-    total += k;
+    int k;
+    if ((k = wc::launch_attend(p.Da, Q, w.KS, w.X, reff, w.vmin, w.vmax, beta, clip, O, w.aimg, st)) < 0)
+        return WC_ECUDA;
+    launches += k;
     tmark(st);
-    return finish(total);
+    return finish(launches);
 }
 
 int wc_comm_unique_id(void *id128) {
@@ -332,7 +431,7 @@ int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int6
     if (rc) return rc;
     if (!comm || !o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
     if (s->batch != 1 || s->heads_kv != 1) return WC_EUNSUPPORTED;
-    if (o->block >= 2) return WC_EUNSUPPORTED;  // blocked selection is single-GPU in this build
+    if (o->block >= 2 || s->bins != 1) return WC_EUNSUPPORTED;  // blocked / binned selection is single-GPU  // blocked selection is single-GPU in this build
     if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;
     const double rq = rq_of(o);
@@ -352,7 +451,7 @@ const char *wc_strerror(int st) {
         case WC_EWORKSPACE: return "workspace too small or not 256-byte aligned";
         case WC_ECUDA: return "CUDA launch or runtime error";
         case WC_ENCCL: return "NCCL error";
-        case WC_EUNSUPPORTED: return "unsupported configuration in this build (bins != 1)";
+        case WC_EUNSUPPORTED: return "unsupported configuration in this build (bins not dividing n, n-sharded bins/blocks, r too large for blocked selection)";
     }
     return "unknown status";
 }
@@ -375,6 +474,6 @@ int wc_timing_read(float *ms, int cap) {
     return k;
 }
 
-int wc_version(void) { return 101; }
+int wc_version(void) { return 102; }
 
 }  // extern "C"

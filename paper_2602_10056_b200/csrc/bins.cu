@@ -1,0 +1,124 @@
+// bins.cu -- Alg 2 binning on top of the per-unit kernels: every (unit u,
+// bin b) pair is a sub-unit su = u*B + b of the selection and weights kernels (contiguous bins of
+// nb = n/B keys; the K/V reshape [units][n] -> [units*B][nb] is free).  Readings Z12 (tau_b uses
+// n_b), Z13 (r_b = min(ceil(r/B), n_b)), Z23 (Philox stream of sub-unit u*B + b).
+//   bins_stats_kernel: per sub-unit R_K^b = max ||k_l - kbar|| over the bin (global kbar, from
+//     the unit prologue's nrm2), tau_b (Eq. 7 with n_b), g_b, mstar_b; R_Q and kbar of the unit.
+//   bins_pack_kernel:  concatenate the bins' valid coreset rows into the unit layout (S with
+//     unit-level key indices, KS, X, r_eff = sum of the bins' r_eff), rows past r_eff zero / -1.
+//   bins_unpack_kernel: the inverse for S (split API: wildcat_weights after wildcat_select).
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace wc {
+
+namespace {
+
+constexpr int kBT = 256;
+
+__global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restrict__ stats_u, const double *__restrict__ nrm2,
+                                                         int64_t nb, int d, int bins, double beta, double *__restrict__ stats_b) {
+    __shared__ double scr[40];
+    const int su = blockIdx.x, u = su / bins;
+    const double *nr = nrm2 + (int64_t)su * nb;  // nrm2 [units][n] == [units*B][nb]
+    double mx = 0.0;
+    for (int64_t l = threadIdx.x; l < nb; l += kBT) mx = fmax(mx, __ldg(nr + l));
+    mx = block_max(mx, scr);
+    const double *su_u = stats_u + (int64_t)u * (kStatsHead + d);
+    double *sb = stats_b + (int64_t)su * (kStatsHead + d);
+    for (int j = threadIdx.x; j < d; j += kBT) sb[kStatsHead + j] = su_u[kStatsHead + j];  // global kbar
+    if (threadIdx.x == 0) {
+        const double rk = sqrt(mx), rq = su_u[4];
+        double tau = 1.0;
+        if (rq * rk > 0.0) {  // Eq. 7 with n_b (Z12)
+            const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
+            const double b0 = log((double)nb) / (beta * rq * rk) + 2.0;
+            const double w = lambert_w0_dev(b0 / (2.0 * rho0));
+            tau = sqrt((rk / rq) * b0 / (2.0 * w));
+        }
+        const double g = beta / (tau * tau);
+        sb[0] = tau;
+        sb[1] = g;
+        sb[2] = g * rk * rk;
+        sb[3] = rk;
+        sb[4] = rq;
+        for (int k = 5; k < kStatsHead; ++k) sb[k] = 0.0;
+    }
+}
+
+// Block (row a, unit u) of the packed layout: row a comes from bin b, local row a - off_b, where
+// off_b = sum_{b' < b} r_eff_{b'}.  Ssub holds bin-local key indices.
+template <typename T>
+__global__ void bins_pack_kernel(const int32_t *__restrict__ Ssub, const int32_t *__restrict__ reff_sub, int bins,
+                                 int rb, int64_t nb, int d, const T *__restrict__ KSsub, const float *__restrict__ Xsub,
+                                 int32_t *__restrict__ S, int32_t *__restrict__ reff, T *__restrict__ KS,
+                                 float *__restrict__ X) {
+    const int a = blockIdx.x, u = blockIdx.y, R = bins * rb, dc = d + 1;
+    int off = 0, b = -1, loc = 0;
+    for (int bb = 0; bb < bins; ++bb) {
+        const int re = reff_sub[u * bins + bb];
+        if (b < 0 && a < off + re) { b = bb; loc = a - off; }
+        off += re;
+    }
+    if (a == 0 && threadIdx.x == 0 && reff) reff[u] = off;
+    const int64_t src = ((int64_t)u * bins + (b < 0 ? 0 : b)) * rb + loc;
+    if (threadIdx.x == 0 && S) S[(int64_t)u * R + a] = b < 0 ? -1 : (int32_t)(b * nb + Ssub[src]);
+    if (KS)
+        for (int j = threadIdx.x; j < d; j += blockDim.x)
+            KS[((int64_t)u * R + a) * d + j] = b < 0 ? from_f32<T>(0.f) : KSsub[src * d + j];
+    if (X)
+        for (int j = threadIdx.x; j < dc; j += blockDim.x) X[((int64_t)u * R + a) * dc + j] = b < 0 ? 0.f : Xsub[src * dc + j];
+}
+
+// One warp per unit: split the packed S (bin order) back into bin-local indices per sub-unit.
+__global__ void bins_unpack_kernel(const int32_t *__restrict__ S, int units, int bins, int rb, int64_t nb,
+                                   int32_t *__restrict__ Ssub, int32_t *__restrict__ reff_sub) {
+    const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (u >= units) return;
+    const int R = bins * rb;
+    for (int b = lane; b < bins; b += 32) reff_sub[u * bins + b] = 0;
+    __syncwarp();
+    if (lane == 0) {
+        int cnt = 0, cur = -1;
+        for (int a = 0; a < R; ++a) {
+            const int s = S[(int64_t)u * R + a];
+            if (s < 0) break;
+            const int b = (int)(s / nb);
+            if (b != cur) { cur = b; cnt = 0; }
+            Ssub[((int64_t)u * bins + b) * rb + cnt] = (int32_t)(s - b * nb);
+            reff_sub[u * bins + b] = ++cnt;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
+                      cudaStream_t st) {
+    bins_stats_kernel<<<D.units() * bins, kBT, 0, st>>>(stats_u, nrm2, D.n / bins, D.d, bins, beta, stats_b);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_bins_pack(const Dims &D, int bins, int rb, const int32_t *Ssub, const int32_t *reff_sub, const void *KSsub,
+                     const float *Xsub, int32_t *S, int32_t *reff, void *KS, float *X, cudaStream_t st) {
+    dim3 g(bins * rb, D.units());
+    if (D.dtype == 0)
+        bins_pack_kernel<float><<<g, 64, 0, st>>>(Ssub, reff_sub, bins, rb, D.n / bins, D.d,
+                                                  static_cast<const float *>(KSsub), Xsub, S, reff,
+                                                  static_cast<float *>(KS), X);
+    else
+        bins_pack_kernel<__nv_bfloat16><<<g, 64, 0, st>>>(Ssub, reff_sub, bins, rb, D.n / bins, D.d,
+                                                          static_cast<const __nv_bfloat16 *>(KSsub), Xsub, S, reff,
+                                                          static_cast<__nv_bfloat16 *>(KS), X);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_bins_unpack(const Dims &D, int bins, int rb, const int32_t *S, int32_t *Ssub, int32_t *reff_sub,
+                       cudaStream_t st) {
+    bins_unpack_kernel<<<(D.units() + 3) / 4, 128, 0, st>>>(S, D.units(), bins, rb, D.n / bins, Ssub, reff_sub);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace wc

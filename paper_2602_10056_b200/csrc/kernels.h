@@ -83,6 +83,14 @@ int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBuf
                           int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
 int select_blocked_max_block();
 
+// Alg 2 binning (bins.cu): per-bin stats, pack (sub-unit -> unit layout), unpack (S only).
+int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
+                      cudaStream_t st);
+int launch_bins_pack(const Dims &D, int bins, int rb, const int32_t *Ssub, const int32_t *reff_sub, const void *KSsub,
+                     const float *Xsub, int32_t *S, int32_t *reff, void *KS, float *X, cudaStream_t st);
+int launch_bins_unpack(const Dims &D, int bins, int rb, const int32_t *S, int32_t *Ssub, int32_t *reff_sub,
+                       cudaStream_t st);
+
 int weights_num_splits(const Dims &D);
 // A3+A4: X = L^{-T} L^{-1} h~(K_S,K)[V,1]; KS gather.  Ypart: [units][splits][r][d+1] fp32.
 int launch_weights(const Dims &D, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,

@@ -47,7 +47,8 @@ def _shape(**kw):
 
 @pytest.mark.parametrize("kw,code", [
     (dict(r=0), -2), (dict(r=101), -2), (dict(d=48), -2), (dict(heads_q=3, heads_kv=2), -2),
-    (dict(dtype=7), -3), (dict(bins=2), -7), (dict(m=-1), -2), (dict(n=0), -2),
+    (dict(dtype=7), -3), (dict(bins=3), -7), (dict(bins=9), -2), (dict(bins=0), -2), (dict(m=-1), -2),
+    (dict(n=0), -2),
 ])
 def test_validation_before_launch(L, kw, code):
     from paper_2602_10056_b200 import _binding as B
@@ -107,3 +108,18 @@ def test_block_option_validation(L):
     o = B.make_opts(block=8)  # blocked selection needs r <= 1024
     assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -7
     assert L.wc_version() >= 101
+
+
+def test_binned_workspace_and_layout(L):
+    from paper_2602_10056_b200 import _binding as B
+
+    # R = B * min(ceil(r/B), n/B) coreset rows per unit (reading Z13)
+    assert B.coreset_rows(4096, 128, 8) == (16, 128)
+    assert B.coreset_rows(1200, 50, 3) == (17, 51)
+    assert B.coreset_rows(64, 64, 8) == (8, 64)
+    s1 = _shape(n=4096, r=128, bins=1)
+    s8 = _shape(n=4096, r=128, bins=8)
+    for op in (0, 1, 3):
+        assert L.wc_workspace_bytes(ctypes.byref(s8), op) > 0
+    # bins shrink the per-unit F state (n r fp64 -> n r / B)
+    assert L.wc_workspace_bytes(ctypes.byref(s8), 0) < L.wc_workspace_bytes(ctypes.byref(s1), 0)
