@@ -113,7 +113,7 @@ def select_bytes(n, d, r, e, nblocks=None, fread=None):
     return n * (nblocks * (d * e + 16) + 8 * r + 8 * fread)
 
 
-def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048, block=1):
+def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048, block=1, bins=1):
     """Time the fp64 oracle (as it stands) on a bounded sample: unit 0's full prologue + selection +
     weights over all n keys, and the attend on `max_queries` query rows; extrapolate linearly in the
     number of query rows and units to the whole workload.  Returns (queries/s, seconds, details)."""
@@ -127,26 +127,65 @@ def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048, block=1):
     V64 = V[0, 0].double().numpy()
     Qg = Q[0, :group].double().numpy().reshape(-1, d)
     beta = 1.0 / math.sqrt(d)
-    t0 = time.perf_counter()
-    kbar, st = oracle.prologue(K64, Qg)
-    if block >= 2:
-        sel = oracle.select_blocked(K64, kbar, st["g"], st["mstar"], cfg.r, block, seed=cfg.seed, unit=0)
-    else:
-        sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
-    t1 = time.perf_counter()
-    X = oracle.weights(K64, V64, sel["S"], sel["r_eff"], kbar, st["g"], st["mstar"])
-    t2 = time.perf_counter()
     ms = min(max_queries, Qg.shape[0])
-    oracle.attend(Qg[:ms], K64[sel["S"]], X, sel["r_eff"], beta, V64.min(0), V64.max(0))
-    t3 = time.perf_counter()
-    per_unit = (t1 - t0) + (t2 - t1) + (t3 - t2) * (Qg.shape[0] / ms)
+    if bins > 1:  # Alg 2 binned oracle on unit 0 with the query sample, attend part timed separately
+        t0 = time.perf_counter()
+        res = oracle.forward_binned(Qg[None, None, :ms], K64[None, None], V64[None, None], cfg.r, bins,
+                                    seed=cfg.seed, block=block)
+        t1 = time.perf_counter()
+        re = int(res["r_eff"][0])
+        oracle.attend(Qg[:ms], K64[res["S"][0, :re]], res["X"][0], re, beta, V64.min(0), V64.max(0))
+        t2 = time.perf_counter()
+        sel_w = (t1 - t0) - (t2 - t1)
+        per_unit = sel_w + (t2 - t1) * (Qg.shape[0] / ms)
+        info = dict(select_s=sel_w, weights_s=0.0, attend_s=t2 - t1)
+        what = f"prologue+binned selection (B={bins}{f', blocked b={block}' if block >= 2 else ''})+weights"
+    else:
+        t0 = time.perf_counter()
+        kbar, st = oracle.prologue(K64, Qg)
+        if block >= 2:
+            sel = oracle.select_blocked(K64, kbar, st["g"], st["mstar"], cfg.r, block, seed=cfg.seed, unit=0)
+        else:
+            sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
+        t1 = time.perf_counter()
+        X = oracle.weights(K64, V64, sel["S"], sel["r_eff"], kbar, st["g"], st["mstar"])
+        t2 = time.perf_counter()
+        oracle.attend(Qg[:ms], K64[sel["S"]], X, sel["r_eff"], beta, V64.min(0), V64.max(0))
+        t3 = time.perf_counter()
+        per_unit = (t1 - t0) + (t2 - t1) + (t3 - t2) * (Qg.shape[0] / ms)
+        info = dict(select_s=t1 - t0, weights_s=t2 - t1, attend_s=t3 - t2)
+        what = f"prologue+selection{f' (blocked, b={block})' if block >= 2 else ''}+weights"
     total = per_unit * cfg.units
     queries = cfg.batch * cfg.hq * cfg.m
-    info = dict(select_s=t1 - t0, weights_s=t2 - t1, attend_s=t3 - t2, attend_rows=ms, threads=threads,
-                sample=(f"oracle on unit 0 of {cfg.units}: full prologue+selection"
-                        f"{f' (blocked, b={block})' if block >= 2 else ''}+weights over n={cfg.n} keys, "
+    info.update(attend_rows=ms, threads=threads,
+                sample=(f"oracle on unit 0 of {cfg.units}: full {what} over n={cfg.n} keys, "
                         f"attend on {ms} of {Qg.shape[0]} query rows; extrapolated linearly to all rows/units"))
     return queries / total, total, info
+
+
+def exact_errors(cfg, Qd, Kd, Vd, O):
+    """max |O^ - O| / max |V| against fp64 exact attention (torch on the GPU, outside the timed region)
+    on seeded query rows of up to 32 heads (P:144 normalisation)."""
+    import torch
+
+    from paper_2602_10056_b200.inputs import query_sample
+
+    errs = []
+    beta = 1.0 / math.sqrt(cfg.d)
+    dev = Qd.device
+    for b in range(cfg.batch):
+        for h in range(cfg.hq):
+            rows = torch.from_numpy(query_sample(cfg.m, 4096 // max(1, cfg.batch * cfg.hq) + 1, seed=b * 131 + h))
+            q = Qd[b, h, rows.to(dev)].double()
+            kk = Kd[b, h // (cfg.hq // cfg.hkv)].double()
+            vv = Vd[b, h // (cfg.hq // cfg.hkv)].double()
+            ex = torch.softmax(beta * (q @ kk.T), dim=-1) @ vv
+            errs.append(float((O[b, h, rows.to(dev)].double() - ex).abs().max() / vv.abs().max()))
+            if b * cfg.hq + h >= 31:
+                break
+        if len(errs) >= 32:
+            break
+    return errs
 
 
 def cpu_model():
@@ -168,11 +207,11 @@ def run_reference(args, cfg):
 
     Q, K, V = make_config(cfg)
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block)
+        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block, args.bins)
     vals, secs = [], []
     info = None
     for _ in range(args.steps):
-        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block)
+        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block, args.bins)
         vals.append(v)
         secs.append(s)
     tot = sum(secs)
@@ -181,7 +220,8 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r, "block": args.block,
+        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r,
+                   "block": args.block, "bins": args.bins,
                    "input_dtype": cfg.dtype, "family": cfg.family},
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                          "sample": info["sample"], "cpu": cpu_model()},
@@ -211,6 +251,8 @@ def main():
     ap.add_argument("--block", type=int, default=16,
                     help="pivot selection: 1 = sequential RPCholesky (Alg 1); b >= 2 = blocked RPCholesky "
                          "with b candidates per block (reading Z22; default 16)")
+    ap.add_argument("--bins", type=int, default=1,
+                    help="Alg 2 bins B (must divide n; default 1 = the north star's per-(batch, head) RPNys)")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip timing the other selection variant (sequential when --block >= 2)")
     args = ap.parse_args()
@@ -244,7 +286,10 @@ def main():
 
     mode = args.mode or ("nshard" if cfg.name.startswith("long") else "replicas")
     units = cfg.units
-    S = torch.empty(units, cfg.r, dtype=torch.int32, device=dev)
+    from paper_2602_10056_b200 import _binding as B0
+
+    rb_main, R_main = B0.coreset_rows(cfg.n, cfg.r, max(1, args.bins))
+    S = torch.empty(units, max(cfg.r, R_main), dtype=torch.int32, device=dev)
     R = torch.empty(units, dtype=torch.int32, device=dev)
     flush = torch.empty(args.flush_mb * (1 << 20), dtype=torch.uint8, device=dev)
     if mode == "nshard":
@@ -269,7 +314,7 @@ def main():
         Obuf = torch.empty_like(Qd)  # preallocated: no allocator traffic inside the timed region
 
         def step():
-            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=args.block)
+            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=args.block, bins=args.bins)
 
     for _ in range(args.warmup):
         step()
@@ -318,14 +363,17 @@ def main():
     sel_info = None
     if mode == "replicas":
         # selection bookkeeping of the same (deterministic) selection: blocks run, F rows re-read
-        sel = wc.select(Qd, Kd, cfg.r, seed=seed, block=args.block)
-        stt = sel.stats.double().cpu()
-        reff_u = sel.r_eff.cpu()
-        alg_bytes = sum(select_bytes(cfg.n, cfg.d, int(reff_u[u]), e, float(stt[u, 6]), float(stt[u, 8]))
-                        for u in range(units))
+        sel = wc.select(Qd, Kd, cfg.r, seed=seed, block=args.block, bins=args.bins)
+        stt = sel.stats.double().cpu()  # per (unit, bin) sub-unit
+        nb = cfg.n // args.bins
+        Sh = sel.S.cpu().numpy()
+        reff_b = [int(((Sh[su // args.bins] >= 0) & (Sh[su // args.bins] // nb == su % args.bins)).sum())
+                  for su in range(units * args.bins)]
+        alg_bytes = sum(select_bytes(nb, cfg.d, reff_b[su], e, float(stt[su, 6]), float(stt[su, 8]))
+                        for su in range(units * args.bins))
         # algorithmic fp64 flops of the round updates: kernel dots 2 n d r_eff + F-prefix dots 2 n Fdot
-        alg_flops = sum(2.0 * cfg.n * (cfg.d * int(reff_u[u]) + float(stt[u, 9])) for u in range(units))
-        sel_info = {"block": args.block, "blocks_per_unit": float(stt[:, 6].mean()),
+        alg_flops = sum(2.0 * nb * (cfg.d * reff_b[su] + float(stt[su, 9])) for su in range(units * args.bins))
+        sel_info = {"block": args.block, "bins": args.bins, "blocks_per_unit": float(stt[:, 6].mean()),
                     "candidates_per_unit": float(stt[:, 7].mean()), "f_rows_reread_per_unit": float(stt[:, 8].mean()),
                     "alg_fp64_flops": alg_flops}
         del sel
@@ -364,10 +412,41 @@ def main():
         B.timing_enable(False)
         vsel = statistics.mean(x[1] for x in vst)
         vbytes = units * select_bytes(cfg.n, cfg.d, int(R.min().item()), e)
-        variants = {"sequential": {"block": 1, "steps": nvs, "ms_per_step": statistics.mean(vt),
+        variants = {"sequential": {"block": 1, "bins": args.bins, "steps": nvs, "ms_per_step": statistics.mean(vt),
                                    "queries_per_s": queries_per_rank * world / (statistics.mean(vt) / 1e3),
                                    "select_ms": vsel, "select_hbm_gbs": vbytes / (vsel / 1e3) / 1e9,
                                    "select_hbm_frac": vbytes / (vsel / 1e3) / 1e9 / peak}}
+    # Alg 2 binning with the paper's KV-cache setting B ~ r/12: the largest power of two
+    # <= r/12 that divides n (so B = 16 at the headline), blocked selection, same inputs
+    if not args.no_variants and mode == "replicas" and args.bins == 1:
+        bv = 1
+        while bv * 2 <= max(1, cfg.r // 12) and cfg.n % (bv * 2) == 0:
+            bv *= 2
+        if bv > 1:
+            _, Rv = B0.coreset_rows(cfg.n, cfg.r, bv)
+            Sv = torch.empty(units, Rv, dtype=torch.int32, device=dev)
+            fwd_b = lambda: wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=Sv, r_eff=R, out=Obuf, block=max(2, args.block),
+                                       bins=bv)
+            fwd_b()
+            torch.cuda.synchronize()
+            vt = []
+            for _ in range(max(2, min(5, args.steps))):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fwd_b()
+                e1.record(stream)
+                e1.synchronize()
+                vt.append(e0.elapsed_time(e1))
+            Ob = fwd_b()
+            torch.cuda.synchronize()
+            berr = max(exact_errors(cfg, Qd, Kd, Vd, Ob)) if (rank == 0 and not args.no_exact) else None
+            variants = variants or {}
+            variants["binned"] = {"bins": bv, "block": max(2, args.block), "r_per_bin": Rv // bv,
+                                  "ms_per_step": statistics.mean(vt),
+                                  "queries_per_s": queries_per_rank * world / (statistics.mean(vt) / 1e3),
+                                  "max_rel_err_vs_exact": berr}
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}" + (f"_b{args.block}" if args.block >= 2 else "")
                       + ".json")
@@ -412,22 +491,7 @@ def main():
 
         O_ref = step()
         torch.cuda.synchronize()
-        errs = []
-        beta = 1.0 / math.sqrt(cfg.d)
-        for b in range(cfg.batch):
-            for h in range(cfg.hq):
-                u = b * cfg.hkv + h // (cfg.hq // cfg.hkv)
-                rows = torch.from_numpy(query_sample(cfg.m, 4096 // max(1, cfg.batch * cfg.hq) + 1, seed=b * 131 + h))
-                q = Qd[b, h, rows.to(dev)].double()
-                kk = Kd[b, h // (cfg.hq // cfg.hkv)].double()
-                vv = Vd[b, h // (cfg.hq // cfg.hkv)].double()
-                a = torch.softmax(beta * (q @ kk.T), dim=-1)
-                ex = a @ vv
-                errs.append(float((O_ref[b, h, rows.to(dev)].double() - ex).abs().max() / vv.abs().max()))
-                if b * cfg.hq + h >= 31:
-                    break
-            if len(errs) >= 32:
-                break
+        errs = exact_errors(cfg, Qd, Kd, Vd, O_ref)
         err = {"max_rel_err_vs_exact": max(errs), "rows_per_head": 4096 // max(1, cfg.batch * cfg.hq) + 1,
                "heads_checked": len(errs), "norm": "max|O^ - O| / max|V| (P:144)"}
         try:
@@ -451,7 +515,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.n <= 262144:
-        v, secs, info = cpu_oracle_sample(cfg, Q, K, V, block=args.block)
+        v, secs, info = cpu_oracle_sample(cfg, Q, K, V, block=args.block, bins=args.bins)
         cpu = {"value": v, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                "sample": info["sample"], "cpu": cpu_model(), "seconds_extrapolated": secs,
                "select_s": info["select_s"], "weights_s": info["weights_s"], "attend_s": info["attend_s"]}
@@ -474,6 +538,7 @@ def main():
                        "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
                        "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}"),
                        "select": "blocked" if args.block >= 2 else "sequential", "block": args.block,
+                       "bins": args.bins,
                        "l2": f"flushed ({args.flush_mb} MB write) before each step"},
             "stages_ms": dict(zip(st_names, st_mean)) if st_mean else None,
             "selection": sel_info,
