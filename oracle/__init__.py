@@ -72,6 +72,9 @@ def lib():
             L.wco_forward_binned.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32,
                                              _c_dbl, _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p,
                                              _p, _p]
+            L.wco_compress_kv.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32,
+                                          _c_i32, _c_i32, _c_dbl, _c_dbl, _c_u64, _p, _p, _p, _p, _p, _p, _p, _p,
+                                          _p]
             L.wco_accept_uniform.argtypes = [_c_u64, ctypes.c_uint32, _c_u64]
             L.wco_accept_uniform.restype = _c_dbl
             L.wco_select_blocked.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64,
@@ -290,6 +293,56 @@ def forward_binned(Q, K, V, r, bins, seed=0, beta=None, rq=-1.0, clip=True, bloc
     if rc:
         raise RuntimeError(f"wco_forward_binned failed ({rc})")
     return dict(O=O, S=S, r_eff=reff, stats=st, X=X)
+
+
+def kv_capacity(n, r, keep_first, keep_last, bins=1):
+    """Cache rows per unit C = keep_first + keep_last + R (R = B*rb over the n_mid middle tokens)."""
+    nmid = n - keep_first - keep_last
+    R = bin_rank(nmid, r, bins)[1] if nmid > 0 else 0
+    return keep_first + keep_last + R, R
+
+
+def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=-1.0, block=1):
+    """KV-cache compression (wco_compress_kv, reading Z24) over
+    [batch, heads, seq, d] arrays.  Returns dict(KC [units][C][d], XC [units][C][d+1], c_eff [units],
+    vmin, vmax [units][d], S [units][R] global token indices of the coreset)."""
+    Q = _f64(Q)
+    K = _f64(K)
+    V = _f64(V)
+    batch, hq, m, d = Q.shape
+    _, hkv, n, _ = K.shape
+    beta = 1.0 / np.sqrt(d) if beta is None else float(beta)
+    units = batch * hkv
+    C, R = kv_capacity(n, r, keep_first, keep_last, bins)
+    KC = np.zeros((units, C, d))
+    XC = np.zeros((units, C, d + 1))
+    ceff = np.zeros(units, dtype=np.int32)
+    vmin = np.zeros((units, d))
+    vmax = np.zeros((units, d))
+    S = np.full((units, max(R, 1)), -1, dtype=np.int32)
+    rc = lib().wco_compress_kv(batch, hq, hkv, m, n, d, r, bins, int(block), int(keep_first), int(keep_last), beta,
+                               float(rq), int(seed), _ptr(Q), _ptr(K), _ptr(V), _ptr(KC), _ptr(XC), _ptr(ceff),
+                               _ptr(vmin), _ptr(vmax), _ptr(S))
+    if rc == -2:
+        raise ValueError("invalid KV split (keep_first/keep_last/bins)")
+    if rc:
+        raise RuntimeError(f"wco_compress_kv failed ({rc})")
+    return dict(KC=KC, XC=XC, c_eff=ceff, vmin=vmin, vmax=vmax, S=S[:, :R])
+
+
+def cache_attend(Q, KC, XC, c_eff, vmin, vmax, hkv, beta=None, clip=True):
+    """Alg 3 WtdAttn (wco_attend) of queries Q [batch, hq, m, d] over a compressed cache
+    (KC, XC, c_eff, vmin, vmax per unit, units = batch*hkv); query head h uses unit h // (hq/hkv)."""
+    Q = _f64(Q)
+    batch, hq, m, d = Q.shape
+    beta = 1.0 / np.sqrt(d) if beta is None else float(beta)
+    group = hq // hkv
+    O = np.zeros_like(Q)
+    for b in range(batch):
+        for h in range(hq):
+            u = b * hkv + h // group
+            O[b, h] = attend(Q[b, h], KC[u], XC[u], int(c_eff[u]), beta, vmin[u], vmax[u], clip=clip)
+    return O
 
 
 # --------------------------------------------------------------------------- checkers

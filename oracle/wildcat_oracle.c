@@ -671,6 +671,91 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
  * r_eff [units]; binstats [units][B][5] = tau_b, g_b, mstar_b, R_K^b, R_Q;
  * X [units][B*rb][d+1] (rows past r_eff zero).  Returns -2 if B does not divide n.   */
 /* ------------------------------------------------------------------------ */
+/* CompressKV (Alg 2) of ONE unit with B >= 1 contiguous bins: the per-unit body of
+ * wco_forward_binned, shared with wco_compress_kv.  Ku, Vu [n][d]; Qg [mq][d] the unit's query rows
+ * (for R_Q; unused when rq >= 0).  Outputs: S [B*rb] unit-level key indices (-1 past tot),
+ * KS [B*rb][d], X [B*rb][d+1] (rows past tot zero), *tot = r_eff, binstats [B][5] (may be NULL).
+ * Requires B | n (checked by the callers).                                                      */
+static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t block, double beta,
+                         double rq, uint64_t seed, uint64_t u, const double *Ku, const double *Vu,
+                         int64_t mq, const double *Qg, int32_t *S, double *KS, double *X,
+                         int32_t *tot_out, double *binstats)
+{
+    const int64_t nb = n / bins;
+    int32_t rb = (r + bins - 1) / bins;
+    if (rb > nb) rb = (int32_t)nb;
+    const int32_t R = bins * rb, dc = d + 1;
+    double *kbar = (double *)malloc(sizeof(double) * d);
+    double *Xb = (double *)malloc(sizeof(double) * (size_t)rb * dc);
+    int32_t *Sb = (int32_t *)malloc(sizeof(int32_t) * rb);
+    if (!kbar || !Xb || !Sb) {
+        free(kbar); free(Xb); free(Sb);
+        return -1;
+    }
+    int status = 0;
+    double st[5];
+    wco_prologue(n, d, Ku, mq, Qg, rq, beta, kbar, st);  /* global kbar, R_Q */
+    const double rqu = st[4];
+    memset(X, 0, sizeof(double) * (size_t)R * dc);
+    memset(KS, 0, sizeof(double) * (size_t)R * d);
+    for (int a = 0; a < R; ++a) S[a] = -1;
+    int32_t tot = 0;
+    for (int32_t b = 0; b < bins && status == 0; ++b) {
+        const double *Kb = Ku + (size_t)b * nb * d;
+        const double *Vb = Vu + (size_t)b * nb * d;
+        double rk2 = 0.0;  /* R_K^b over the bin's centred keys */
+        for (int64_t l = 0; l < nb; ++l) {
+            double s2 = 0.0;
+            for (int j = 0; j < d; ++j) {
+                double c = Kb[l * d + j] - kbar[j];
+                s2 += c * c;
+            }
+            if (s2 > rk2) rk2 = s2;
+        }
+        const double rk = sqrt(rk2);
+        const double tau = wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
+        const double g = beta / (tau * tau), mstar = g * rk * rk;
+        int32_t re = 0;
+        const uint64_t ub = u * (uint64_t)bins + (uint64_t)b;  /* Z23 */
+        if (block > 1)
+            status = wco_select_blocked(nb, d, rb, block, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL,
+                                        NULL, NULL, NULL);
+        else
+            status = wco_select(nb, d, rb, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL, NULL, NULL);
+        if (status) break;
+        status = wco_weights(nb, d, rb, Kb, Vb, Sb, re, kbar, g, mstar, Xb);
+        if (status) break;
+        for (int a = 0; a < re; ++a) {  /* concatenate the bin's valid rows */
+            S[tot + a] = (int32_t)(b * nb + Sb[a]);
+            memcpy(KS + (size_t)(tot + a) * d, Kb + (size_t)Sb[a] * d, sizeof(double) * d);
+            memcpy(X + (size_t)(tot + a) * dc, Xb + (size_t)a * dc, sizeof(double) * dc);
+        }
+        tot += re;
+        if (binstats) {
+            double *bs = binstats + (size_t)b * 5;
+            bs[0] = tau; bs[1] = g; bs[2] = mstar; bs[3] = rk; bs[4] = rqu;
+        }
+    }
+    *tot_out = tot;
+    free(kbar); free(Xb); free(Sb);
+    return status;
+}
+
+/* Columnwise range of V over rows [0, n) (Alg 4). */
+static void value_range(int64_t n, int32_t d, const double *Vu, double *vmin, double *vmax)
+{
+    for (int c = 0; c < d; ++c) {
+        double lo = Vu[c], hi = Vu[c];
+        for (int64_t l = 1; l < n; ++l) {
+            double v = Vu[l * d + c];
+            if (v < lo) lo = v;
+            if (v > hi) hi = v;
+        }
+        vmin[c] = lo;
+        vmax[c] = hi;
+    }
+}
+
 int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d,
                        int32_t r, int32_t bins, double beta, double rq, uint64_t seed, int32_t clip,
                        int32_t block, const double *Q, const double *K, const double *V, double *O,
@@ -681,15 +766,12 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
     int32_t rb = (r + bins - 1) / bins;
     if (rb > nb) rb = (int32_t)nb;
     const int32_t R = bins * rb, dc = d + 1, group = hq / hkv;
-    double *kbar = (double *)malloc(sizeof(double) * d);
-    double *Xb = (double *)malloc(sizeof(double) * (size_t)rb * dc);
     double *X = (double *)malloc(sizeof(double) * (size_t)R * dc);
     double *KS = (double *)malloc(sizeof(double) * (size_t)R * d);
     double *vmin = (double *)malloc(sizeof(double) * d);
     double *vmax = (double *)malloc(sizeof(double) * d);
-    int32_t *Sb = (int32_t *)malloc(sizeof(int32_t) * rb);
     int32_t *S = (int32_t *)malloc(sizeof(int32_t) * R);
-    if (!kbar || !Xb || !X || !KS || !vmin || !vmax || !Sb || !S) return -1;
+    if (!X || !KS || !vmin || !vmax || !S) return -1;
     int status = 0;
     for (int32_t bt = 0; bt < batch && status == 0; ++bt) {
         for (int32_t h = 0; h < hkv && status == 0; ++h) {
@@ -697,59 +779,10 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
             const double *Ku = K + (size_t)u * n * d;
             const double *Vu = V + (size_t)u * n * d;
             const double *Qg = Q + ((size_t)bt * hq + (size_t)h * group) * m * d;
-            for (int c = 0; c < d; ++c) {  /* value range over the full V */
-                double lo = Vu[c], hi = Vu[c];
-                for (int64_t l = 1; l < n; ++l) {
-                    double v = Vu[l * d + c];
-                    if (v < lo) lo = v;
-                    if (v > hi) hi = v;
-                }
-                vmin[c] = lo;
-                vmax[c] = hi;
-            }
-            double st[5];
-            wco_prologue(n, d, Ku, (int64_t)group * m, Qg, rq, beta, kbar, st);  /* global kbar, R_Q */
-            const double rqu = st[4];
-            memset(X, 0, sizeof(double) * (size_t)R * dc);
-            memset(KS, 0, sizeof(double) * (size_t)R * d);
-            for (int a = 0; a < R; ++a) S[a] = -1;
+            value_range(n, d, Vu, vmin, vmax);  /* value range over the full V */
             int32_t tot = 0;
-            for (int32_t b = 0; b < bins && status == 0; ++b) {
-                const double *Kb = Ku + (size_t)b * nb * d;
-                const double *Vb = Vu + (size_t)b * nb * d;
-                double rk2 = 0.0;  /* R_K^b over the bin's centred keys */
-                for (int64_t l = 0; l < nb; ++l) {
-                    double s2 = 0.0;
-                    for (int j = 0; j < d; ++j) {
-                        double c = Kb[l * d + j] - kbar[j];
-                        s2 += c * c;
-                    }
-                    if (s2 > rk2) rk2 = s2;
-                }
-                const double rk = sqrt(rk2);
-                const double tau = wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
-                const double g = beta / (tau * tau), mstar = g * rk * rk;
-                int32_t re = 0;
-                const uint64_t ub = u * (uint64_t)bins + (uint64_t)b;  /* Z23 */
-                if (block > 1)
-                    status = wco_select_blocked(nb, d, rb, block, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL,
-                                                NULL, NULL, NULL);
-                else
-                    status = wco_select(nb, d, rb, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL, NULL, NULL);
-                if (status) break;
-                status = wco_weights(nb, d, rb, Kb, Vb, Sb, re, kbar, g, mstar, Xb);
-                if (status) break;
-                for (int a = 0; a < re; ++a) {  /* concatenate the bin's valid rows */
-                    S[tot + a] = (int32_t)(b * nb + Sb[a]);
-                    memcpy(KS + (size_t)(tot + a) * d, Kb + (size_t)Sb[a] * d, sizeof(double) * d);
-                    memcpy(X + (size_t)(tot + a) * dc, Xb + (size_t)a * dc, sizeof(double) * dc);
-                }
-                tot += re;
-                if (binstats_out) {
-                    double *bs = binstats_out + ((size_t)u * bins + b) * 5;
-                    bs[0] = tau; bs[1] = g; bs[2] = mstar; bs[3] = rk; bs[4] = rqu;
-                }
-            }
+            status = compress_unit(n, d, r, bins, block, beta, rq, seed, u, Ku, Vu, (int64_t)group * m, Qg, S,
+                                   KS, X, &tot, binstats_out ? binstats_out + (size_t)u * bins * 5 : NULL);
             if (status) break;
             for (int32_t hh = 0; hh < group; ++hh) {
                 size_t qoff = ((size_t)bt * hq + (size_t)h * group + hh) * m * d;
@@ -760,7 +793,84 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
             if (X_out) memcpy(X_out + (size_t)u * R * dc, X, sizeof(double) * (size_t)R * dc);
         }
     }
-    free(kbar); free(Xb); free(X); free(KS); free(vmin); free(vmax); free(Sb); free(S);
+    free(X); free(KS); free(vmin); free(vmax); free(S);
+    return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* KV-cache compression ("prefill phase"; E3 protocol P:667-669).
+ * Per unit u = b*hkv + h with keys/values K, V [n][d]:
+ *   - the first keep_first and the last keep_last tokens are retained exactly ("retain the first
+ *     and last 32 context tokens and compress the remaining tokens");
+ *   - the middle n_mid = n - keep_first - keep_last tokens are compressed by CompressKV (Alg 2,
+ *     P:297-313) with rank r and B bins (B | n_mid), exactly as wco_forward_binned does for a
+ *     unit whose keys are the middle slice (its own kbar and R_K; R_Q from the unit's query rows
+ *     Q [m per q-head] of the prompt, or rq >= 0; Philox unit id u, sub-unit u*B + b);
+ *   - reading Z24: the cache is the union of exact and compressed entries, each entry a key row
+ *     and an [value | weight] row: a retained token l contributes (k_l, [v_l, 1]), a coreset key
+ *     s contributes (k_s, [V_S, w]_s) -- so WtdAttn (Alg 3) over the cache sums the
+ *     exact terms of the retained tokens and the Nystrom estimate of the middle's terms under one
+ *     softmax shift (the estimate is of the unnormalised sums, so the two add);
+ *   - the clip range (vmin, vmax) is over all n values ("full V").
+ * Cache rows per unit, capacity C = keep_first + keep_last + R (R = B*rb, rb = min(ceil(r/B),
+ * n_mid/B); R = 0 when n_mid = 0): [first keep_first tokens | last keep_last tokens | r_eff
+ * coreset rows in the order of Alg 2], zero rows after; c_eff = keep_first + keep_last + r_eff.
+ * Outputs: KC [units][C][d], XC [units][C][d+1], c_eff [units], vmin/vmax [units][d],
+ * S [units][R] (global token indices of the coreset, -1 past r_eff; may be NULL).
+ * Returns -2 on an invalid split (keep_* < 0, n_mid < 0, n_mid > 0 with B not dividing n_mid
+ * or B > r).                                                                */
+/* ------------------------------------------------------------------------ */
+int wco_compress_kv(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d, int32_t r,
+                    int32_t bins, int32_t block, int32_t keep_first, int32_t keep_last, double beta, double rq,
+                    uint64_t seed, const double *Q, const double *K, const double *V, double *KC, double *XC,
+                    int32_t *c_eff, double *vmin_out, double *vmax_out, int32_t *S_out)
+{
+    const int64_t nmid = n - keep_first - keep_last;
+    if (keep_first < 0 || keep_last < 0 || nmid < 0) return -2;
+    if (nmid > 0 && (bins < 1 || nmid % bins != 0 || bins > r || r < 1)) return -2;
+    int32_t R = 0;
+    if (nmid > 0) {
+        int32_t rb = (r + bins - 1) / bins;
+        if (rb > nmid / bins) rb = (int32_t)(nmid / bins);
+        R = bins * rb;
+    }
+    const int32_t kept = keep_first + keep_last, C = kept + R, dc = d + 1, group = hq / hkv;
+    double *X = (double *)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1) * dc);
+    double *KS = (double *)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1) * d);
+    int32_t *S = (int32_t *)malloc(sizeof(int32_t) * (size_t)(R > 0 ? R : 1));
+    if (!X || !KS || !S) return -1;
+    int status = 0;
+    for (int32_t bt = 0; bt < batch && status == 0; ++bt) {
+        for (int32_t h = 0; h < hkv && status == 0; ++h) {
+            const uint64_t u = (uint64_t)bt * hkv + h;
+            const double *Ku = K + (size_t)u * n * d;
+            const double *Vu = V + (size_t)u * n * d;
+            const double *Qg = Q + ((size_t)bt * hq + (size_t)h * group) * m * d;
+            double *KCu = KC + (size_t)u * C * d;
+            double *XCu = XC + (size_t)u * C * dc;
+            value_range(n, d, Vu, vmin_out + (size_t)u * d, vmax_out + (size_t)u * d);
+            memset(KCu, 0, sizeof(double) * (size_t)C * d);
+            memset(XCu, 0, sizeof(double) * (size_t)C * dc);
+            for (int32_t a = 0; a < kept; ++a) {  /* retained tokens: (k_l, [v_l, 1]) */
+                const int64_t l = a < keep_first ? a : n - keep_last + (a - keep_first);
+                memcpy(KCu + (size_t)a * d, Ku + (size_t)l * d, sizeof(double) * d);
+                memcpy(XCu + (size_t)a * dc, Vu + (size_t)l * d, sizeof(double) * d);
+                XCu[(size_t)a * dc + d] = 1.0;
+            }
+            int32_t tot = 0;
+            if (nmid > 0) {
+                status = compress_unit(nmid, d, r, bins, block, beta, rq, seed, u, Ku + (size_t)keep_first * d,
+                                       Vu + (size_t)keep_first * d, (int64_t)group * m, Qg, S, KS, X, &tot, NULL);
+                if (status) break;
+                memcpy(KCu + (size_t)kept * d, KS, sizeof(double) * (size_t)tot * d);
+                memcpy(XCu + (size_t)kept * dc, X, sizeof(double) * (size_t)tot * dc);
+            }
+            c_eff[u] = kept + tot;
+            if (S_out)
+                for (int32_t a = 0; a < R; ++a) S_out[(size_t)u * R + a] = a < tot ? S[a] + keep_first : -1;
+        }
+    }
+    free(X); free(KS); free(S);
     return status;
 }
 
