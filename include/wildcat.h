@@ -130,7 +130,7 @@ int wildcat_weights(const wc_shape *shape, const wc_opts *opts, const void *K, c
 
 /* Alg 3 WtdAttn: O = clip( diag(A^ w)^{-1} A^ V_S where A^ w > 0 else 0, vmin, vmax ),
  * A^ = exp(beta Q K_S^T) over the first r_eff coreset rows.  `m` of the shape is the
- * number of queries per q-head (e.g. 1 for decode). */
+ * number of queries per q-head (e.g. 1 for decode; 0 < m <= 16 selects the split-cache decode kernel). */
 int wildcat_attend(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *KS,
                    const float *X, const int32_t *r_eff, const void *vmin, const void *vmax,
                    void *O, void *ws, size_t ws_bytes, void *stream);
@@ -140,6 +140,35 @@ int wildcat_attend(const wc_shape *shape, const wc_opts *opts, const void *Q, co
 int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *K,
                     const void *V, void *O, int32_t *S, int32_t *r_eff,
                     void *ws, size_t ws_bytes, void *stream);
+
+/* ---- KV-cache compression (prefill) and decode.
+ * The E3 protocol retains the first and last tokens of the context exactly and
+ * compresses the rest: per unit, the first keep_first and last keep_last of the n tokens are kept,
+ * and the n_mid = n - keep_first - keep_last middle tokens go through CompressKV (Alg 2,
+ * P:297-313) at rank shape->r with shape->bins bins (B | n_mid; r <= n_mid; recentring, R_K and tau
+ * over the middle only; R_Q from Q's m prompt rows per q-head, or opts->rq >= 0, Q then nullable;
+ * Philox unit ids as wildcat_forward; opts->block as wildcat_select).  Reading Z24:
+ * the cache is the union of exact and compressed entries, so WtdAttn over it adds the retained
+ * tokens' exact terms to the Nystrom estimate of the middle's unnormalised sums:
+ *   KC  dtype [units][C][d]    rows: first keep_first tokens | last keep_last tokens | the middle's
+ *                              r_eff coreset keys (Alg 2 order) | zero rows
+ *   XC  float [units][C][d+1]  matching [value | weight] rows: [v_l, 1] for retained tokens,
+ *                              [V_S, w] for coreset rows, zero after
+ *   c_eff int32 [units]        keep_first + keep_last + r_eff (valid rows of the cache)
+ *   vmin, vmax dtype [units][d] range of ALL n values
+ *   S   int32 [units][R]       global token index of each coreset row, -1 past r_eff (nullable)
+ * C = wc_kv_capacity(shape, keep_first, keep_last) = keep_first + keep_last + R, with R = B*rb of
+ * the middle (R = 0 when n_mid = 0; then nothing is compressed and r, bins are not checked).
+ * Decode (WtdAttn, Alg 3) over the cache is wildcat_attend with shape.r = C,
+ * shape.bins = 1, shape.m = new queries per q-head, KS = KC, X = XC, r_eff = c_eff; for
+ * m <= 16 it runs a decode kernel that splits the cache over CTAs (fp32 scores and sums).
+ * Errors: WC_ESHAPE for keep_* < 0 or n_mid < 0 and the wildcat_select shape rules applied to the
+ * middle; WC_EUNSUPPORTED when B does not divide n_mid. */
+size_t wc_kv_capacity(const wc_shape *shape, int32_t keep_first, int32_t keep_last);       /* 0 if invalid */
+size_t wc_kv_workspace_bytes(const wc_shape *shape, int32_t keep_first, int32_t keep_last); /* 0 if invalid */
+int wildcat_compress_kv(const wc_shape *shape, const wc_opts *opts, int32_t keep_first, int32_t keep_last,
+                        const void *Q, const void *K, const void *V, void *KC, float *XC, int32_t *c_eff,
+                        void *vmin, void *vmax, int32_t *S, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- Key-dimension sharding of one long sequence across GPUs.
  * One process per GPU.  Rank 0 gets a 128-byte NCCL unique id from wc_comm_unique_id and shares

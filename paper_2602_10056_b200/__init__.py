@@ -7,6 +7,8 @@ Public API (torch tensors in the BHND layout [batch, heads, seq, d], CUDA only):
     cache = weights(K, V, sel)                              # Alg 2 "Compress values"
     O = attend(Q, cache)                                    # Alg 3 WtdAttn
     O = forward_host(Q_cpu, K_cpu, V_cpu, r)                # host buffers in, host result out
+    cache = compress_kv(Q, K, V, r, keep_first=32, keep_last=32)  # KV-cache compression (prefill)
+    O_new = attend(Q_new, cache)                            # decode over the compressed cache
     comm = NshardComm.create(group)                         # keys of one sequence sharded over ranks
     O_loc = forward_nshard(comm, Q_loc, K_loc, V_loc, r, n_global, n_offset)
 
@@ -24,7 +26,7 @@ from . import _binding as B
 from ._binding import WildcatError, lib  # noqa: F401
 
 __all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
-           "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range"]
+           "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range", "compress_kv", "kv_capacity"]
 
 
 STATS_HEAD = 16  # tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, Fdot, 0 x 6; then kbar[d]
@@ -148,6 +150,48 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None,
     ws = _workspace(shape, B.WC_OP_FORWARD, K.device)
     B.wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O
+
+
+def kv_capacity(n, r, keep_first=0, keep_last=0, bins=1) -> int:
+    """Cache rows per unit of compress_kv: keep_first + keep_last + B * min(ceil(r/B), n_mid/B)."""
+    nmid = int(n) - int(keep_first) - int(keep_last)
+    return int(keep_first) + int(keep_last) + (B.coreset_rows(nmid, r, bins)[1] if nmid > 0 else 0)
+
+
+def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=None, block=1, S=None,
+                stream=None) -> Cache:
+    """KV-cache compression (E3 protocol P:667-669; reading Z24): the first keep_first and
+    last keep_last tokens of every (batch, kv-head) are kept exactly, the middle goes through
+    CompressKV (Alg 2) at rank r with `bins` bins.  Q holds the prompt's queries (for R_Q) or may be
+    None when rq is given.  Returns a Cache whose rows are [retained | coreset | zero] (r_eff = c_eff),
+    ready for attend(Q_new, cache) -- the decode step.  S (int32 [units][R]), if given, receives the
+    global token index of each coreset row."""
+    Q, K, V = _cont(Q), _cont(K), _cont(V)
+    _require_cuda(Q, K, V)
+    if Q is None and rq is None:
+        raise WildcatError("compress_kv needs the prompt queries Q or rq")
+    b, hkv, n, d = K.shape
+    shape = B.make_shape(Q, K, r, bins=bins)
+    opts = B.make_opts(seed, beta, rq, block=block)
+    C = B.kv_capacity(shape, keep_first, keep_last)
+    if C == 0:
+        raise WildcatError("compress_kv: invalid split (keep_first/keep_last/r/bins)")
+    units, dev = b * hkv, K.device
+    KC = torch.empty(units, C, d, dtype=K.dtype, device=dev)
+    XC = torch.empty(units, C, d + 1, dtype=torch.float32, device=dev)
+    ceff = torch.empty(units, dtype=torch.int32, device=dev)
+    vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
+    vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
+    nb = B.kv_workspace_bytes(shape, keep_first, keep_last)
+    key = (dev, "kv")
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+        _ws_cache[key] = ws
+    B.wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, ceff, vmin, vmax, S, ws, stream)
+    cshape = B.wc_shape(batch=b, heads_q=shape.heads_q, heads_kv=hkv, d=d, r=C, bins=1, dtype=shape.dtype,
+                        reserved=0, m=0, n=n)
+    return Cache(KC, XC, vmin, vmax, ceff, hkv, opts, cshape)
 
 
 class HostForward:

@@ -73,6 +73,13 @@ def lib():
                                              ctypes.c_size_t, P]
         for f in ("wc_comm_unique_id", "wc_comm_init", "wc_comm_destroy", "wildcat_forward_nshard"):
             getattr(L, f).restype = ctypes.c_int
+        L.wc_kv_capacity.argtypes = [S, ctypes.c_int32, ctypes.c_int32]
+        L.wc_kv_capacity.restype = ctypes.c_size_t
+        L.wc_kv_workspace_bytes.argtypes = [S, ctypes.c_int32, ctypes.c_int32]
+        L.wc_kv_workspace_bytes.restype = ctypes.c_size_t
+        L.wildcat_compress_kv.argtypes = [S, O, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, P, P,
+                                          ctypes.c_size_t, P]
+        L.wildcat_compress_kv.restype = ctypes.c_int
         L.wc_timing_enable.argtypes = [ctypes.c_int]
         L.wc_timing_enable.restype = ctypes.c_int
         L.wc_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
@@ -155,6 +162,21 @@ def wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream=None):
     rc = lib().wildcat_forward(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
                                _ptr(S), _ptr(r_eff), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "wildcat_forward")
+
+
+def kv_capacity(shape, keep_first, keep_last) -> int:
+    return int(lib().wc_kv_capacity(ctypes.byref(shape), int(keep_first), int(keep_last)))
+
+
+def kv_workspace_bytes(shape, keep_first, keep_last) -> int:
+    return int(lib().wc_kv_workspace_bytes(ctypes.byref(shape), int(keep_first), int(keep_last)))
+
+
+def wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, c_eff, vmin, vmax, S, ws, stream=None):
+    rc = lib().wildcat_compress_kv(ctypes.byref(shape), ctypes.byref(opts), int(keep_first), int(keep_last), _ptr(Q),
+                                   _ptr(K), _ptr(V), _ptr(KC), _ptr(XC), _ptr(c_eff), _ptr(vmin), _ptr(vmax),
+                                   _ptr(S), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "wildcat_compress_kv")
 
 
 def last_launch_count() -> int:

@@ -272,6 +272,62 @@ int weights_stage(const Plan &p, const void *K, const void *V, const int32_t *S,
     return WC_OK;
 }
 
+// ---- KV-cache compression (reading Z24): full-context shape -> the middle's shape.
+struct KvPlan {
+    wc_shape full, mid;
+    int64_t nmid = 0;
+    int kf = 0, kl = 0, R = 0;
+    bool has_mid = false;
+};
+int kv_plan(const wc_shape *s, int32_t kf, int32_t kl, KvPlan &kp) {
+    if (!s) return WC_EINVAL;
+    if (kf < 0 || kl < 0) return WC_ESHAPE;
+    kp.full = *s;
+    kp.full.r = 1;
+    kp.full.bins = 1;
+    int rc = check_shape(&kp.full);
+    if (rc) return rc;
+    kp.kf = kf;
+    kp.kl = kl;
+    kp.nmid = s->n - (int64_t)kf - (int64_t)kl;
+    if (kp.nmid < 0) return WC_ESHAPE;
+    kp.has_mid = kp.nmid > 0;
+    if (kp.has_mid) {
+        kp.mid = *s;
+        kp.mid.n = kp.nmid;
+        if ((rc = check_shape(&kp.mid))) return rc;
+        kp.R = plan_of(&kp.mid).R;
+    }
+    return WC_OK;
+}
+
+struct KvWs {
+    wc::ProloguePartials ppf;  // value range over the full V
+    void *Kmid = nullptr, *Vmid = nullptr;
+    SelectWs sel;
+    WeightsWs wts;
+    double *stats = nullptr, *L = nullptr;
+    int32_t *S = nullptr, *reff = nullptr;
+    void *KS = nullptr;
+    float *X = nullptr;
+};
+void carve_kv(Carver &c, const KvPlan &kp, KvWs &w) {
+    carve_prologue(c, dims_of(&kp.full), w.ppf);
+    if (!kp.has_mid) return;
+    const Plan p = plan_of(&kp.mid);
+    const size_t U = p.D.units(), Us = p.Ds.units(), e = esize(&kp.mid);
+    w.Kmid = c.take<char>(U * (size_t)kp.nmid * p.D.d * e);
+    w.Vmid = c.take<char>(U * (size_t)kp.nmid * p.D.d * e);
+    carve_select(c, p, w.sel);
+    carve_weights(c, &kp.mid, p, w.wts);
+    w.stats = c.take<double>(Us * WC_STATS_STRIDE(p.D.d));
+    w.S = c.take<int32_t>(U * p.R);
+    w.reff = c.take<int32_t>(U);
+    w.L = c.take<double>(Us * (size_t)p.rb * p.rb);
+    w.KS = c.take<char>(U * (size_t)p.R * p.D.d * e);
+    w.X = c.take<float>(U * (size_t)p.R * (p.D.d + 1));
+}
+
 }  // namespace
 
 extern "C" {
@@ -412,6 +468,72 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     return finish(launches);
 }
 
+size_t wc_kv_capacity(const wc_shape *s, int32_t keep_first, int32_t keep_last) {
+    KvPlan kp;
+    if (kv_plan(s, keep_first, keep_last, kp) != WC_OK) return 0;
+    return (size_t)keep_first + (size_t)keep_last + (size_t)kp.R;
+}
+
+size_t wc_kv_workspace_bytes(const wc_shape *s, int32_t keep_first, int32_t keep_last) {
+    KvPlan kp;
+    if (kv_plan(s, keep_first, keep_last, kp) != WC_OK) return 0;
+    Carver c(nullptr);
+    KvWs w;
+    carve_kv(c, kp, w);
+    return rounded(c);
+}
+
+int wildcat_compress_kv(const wc_shape *s, const wc_opts *o, int32_t keep_first, int32_t keep_last, const void *Q,
+                        const void *K, const void *V, void *KC, float *XC, int32_t *c_eff, void *vmin, void *vmax,
+                        int32_t *S_out, void *ws, size_t ws_bytes, void *stream) {
+    KvPlan kp;
+    int rc = kv_plan(s, keep_first, keep_last, kp);
+    if (rc) return rc;
+    if (!o || !K || !V || !KC || !XC || !c_eff || !vmin || !vmax) return WC_EINVAL;
+    if (kp.has_mid && (rc = check_opts(o, &kp.mid))) return rc;
+    const double rq = rq_of(o);
+    if (kp.has_mid && rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;
+    if ((rc = ws_ok(ws, ws_bytes, wc_kv_workspace_bytes(s, keep_first, keep_last)))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Carver c(ws);
+    KvWs w;
+    carve_kv(c, kp, w);
+    const wc::Dims Df = dims_of(&kp.full);
+    int launches = 0, k;
+    tmark(st, true);
+    if ((k = wc::launch_vrange(Df, V, w.ppf, vmin, vmax, st)) < 0) return WC_ECUDA;  // full V
+    launches += k;
+    if (kp.has_mid) {
+        const Plan p = plan_of(&kp.mid);
+        const size_t e = esize(s), row = (size_t)s->d * e;
+        // the middle tokens of every unit, packed [units][nmid][d] for the per-unit kernels
+        for (int t = 0; t < 2; ++t) {
+            if (cudaMemcpy2DAsync(t ? w.Vmid : w.Kmid, kp.nmid * row,
+                                  static_cast<const char *>(t ? V : K) + (size_t)keep_first * row, s->n * row,
+                                  kp.nmid * row, Df.units(), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return WC_ECUDA;
+        }
+        tmark(st);
+        if ((rc = select_stage(p, o, beta_of(s, o), rq, Q, w.Kmid, nullptr, w.sel, w.stats, w.S, w.reff, w.L, nullptr,
+                               nullptr, st, &launches)))
+            return rc;
+        tmark(st);
+        if (p.B > 1) {
+            w.wts.Ssub = w.sel.Ssub;
+            w.wts.reff_sub = w.sel.reff_sub;
+        }
+        if ((rc = weights_stage(p, w.Kmid, w.Vmid, w.S, w.reff, w.L, w.stats, w.wts, true, w.KS, w.X, st, &launches)))
+            return rc;
+    }
+    tmark(st);
+    if ((k = wc::launch_kv_assemble(Df, K, V, keep_first, keep_last, kp.R, w.KS, w.X, w.S, w.reff, KC, XC, c_eff,
+                                    S_out, st)) < 0)
+        return WC_ECUDA;
+    launches += k;
+    tmark(st);
+    return finish(launches);
+}
+
 int wc_comm_unique_id(void *id128) {
     if (!id128) return WC_EINVAL;
     return wc::ns_comm_unique_id(id128);
@@ -474,6 +596,6 @@ int wc_timing_read(float *ms, int cap) {
     return k;
 }
 
-int wc_version(void) { return 102; }
+int wc_version(void) { return 103; }
 
 }  // extern "C"

@@ -727,15 +727,18 @@ int launch_attend_t(const Dims &Dm, const void *Q, const void *KS, const float *
 
 }  // namespace
 
-// 0: CUDA-core kernel, 1: tcgen05 kernel with the coreset resident, 2: tcgen05 kernel streaming r > 256
+// 0: CUDA-core kernel, 1: tcgen05 kernel with the coreset resident, 2: tcgen05 kernel streaming r > 256,
+// 3: decode kernel (kvcache.cu) for m <= kDecodeMaxM queries per q-head
 static int attend_path(const Dims &D) {
     static const char *mode = std::getenv("WC_ATTEND");  // "cuda": CUDA-core kernel (A/B tests)
     if (mode && std::strcmp(mode, "cuda") == 0) return 0;
+    if (D.m > 0 && D.m <= kDecodeMaxM) return 3;
     if (!(D.dtype == 1 && (D.d == 64 || D.d == 128) && D.m > 0)) return 0;
     return D.r <= 256 ? 1 : 2;
 }
 
 size_t attend_ws_bytes(const Dims &D) {
+    if (attend_path(D) == 3) return attend_decode_ws_bytes(D);
     if (attend_path(D) != 2) return 0;
     const size_t img = D.d == 64 ? TcLong<64>::kImg : TcLong<128>::kImg;
     return D.units() * (size_t)ceil_div(D.r, 128) * img;
@@ -744,6 +747,7 @@ size_t attend_ws_bytes(const Dims &D) {
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                   const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
     const int path = attend_path(D);
+    if (path == 3) return launch_attend_decode(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
     if (path == 2) {
         if (D.d == 64) return launch_attend_tc_long<64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
         return launch_attend_tc_long<128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);

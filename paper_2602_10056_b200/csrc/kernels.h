@@ -108,7 +108,20 @@ inline size_t dinv_elems(int r) { return (size_t)((r + 31) / 32) * 32 * 32; }
 // A5: attend.
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
                   const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st);
-size_t attend_ws_bytes(const Dims &D);  // staging images for r > 256 (0 otherwise)
+size_t attend_ws_bytes(const Dims &D);  // staging images for r > 256, decode partials (0 otherwise)
+
+// Decode-shaped A5 (kvcache.cu), used by launch_attend when 0 < m <= kDecodeMaxM.
+constexpr int kDecodeMaxM = 16;
+size_t attend_decode_ws_bytes(const Dims &D);
+int launch_attend_decode(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                         const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws,
+                         cudaStream_t st);
+// KV-cache assembly (reading Z24): KC / XC rows [first kf | last kl | middle coreset], c_eff, S (global).
+// D: the full-context unit dims (n = all tokens).  Smid / reff_mid / KS / X of the middle may be null
+// when R = 0.
+int launch_kv_assemble(const Dims &D, const void *K, const void *V, int kf, int kl, int R, const void *KS,
+                       const float *X, const int32_t *Smid, const int32_t *reff_mid, void *KC, float *XC,
+                       int32_t *c_eff, int32_t *S_out, cudaStream_t st);
 
 // n-sharded forward (nshard.cu).  Single unit per call; NCCL resolved at run time.
 size_t ns_workspace_bytes(const Dims &D);

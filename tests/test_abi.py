@@ -83,7 +83,35 @@ def test_workspace_sizes_scale(L):
     s1 = _shape(n=1000, r=10)
     s2 = _shape(n=2000, r=20)
     assert L.wc_workspace_bytes(ctypes.byref(s2), 0) > 3 * L.wc_workspace_bytes(ctypes.byref(s1), 0)
-    assert L.wc_workspace_bytes(ctypes.byref(s1), 2) == 0
+    big_m = _shape(n=1000, r=10, m=500)
+    assert L.wc_workspace_bytes(ctypes.byref(big_m), 2) == 0  # resident-coreset attend needs none
+    assert L.wc_workspace_bytes(ctypes.byref(_shape(n=1000, r=10, m=16)), 2) > 0  # decode kernel partials
+
+
+def test_kv_cache_abi(L):
+    from paper_2602_10056_b200 import _binding as B
+
+    # capacity C = keep_first + keep_last + B * min(ceil(r/B), n_mid/B) (reading Z24)
+    s = _shape(n=1000, r=64)
+    assert B.kv_capacity(s, 32, 32) == 64 + 64
+    assert B.kv_capacity(s, 500, 500) == 1000  # nothing compressed
+    assert B.kv_capacity(_shape(n=1000, r=64, bins=4), 20, 20) == 40 + 64
+    assert B.kv_capacity(_shape(n=1000, r=64, bins=5), 32, 32) == 0  # 5 divides n = 1000 but not n_mid = 936
+    assert B.kv_capacity(s, 600, 500) == 0 and B.kv_capacity(s, -1, 0) == 0
+    assert B.kv_workspace_bytes(s, 32, 32) > 0
+    o = B.make_opts()
+    d = ctypes.c_void_p(0x1000)
+    f = ctypes.c_void_p(0x1000)
+    # invalid split -> WC_ESHAPE; null cache output -> WC_EINVAL; small workspace -> WC_EWORKSPACE
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 600, 500, d, d, d, d, f, d, d, d, None, d,
+                                 1 << 40, None) == -2
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, None, f, d, d, d, None, d,
+                                 1 << 40, None) == -1
+    need = B.kv_workspace_bytes(s, 32, 32)
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, d, f, d, d, d, None, d,
+                                 need - 1, None) == -4
+    assert L.wildcat_compress_kv(ctypes.byref(_shape(n=1000, r=64, bins=5)), ctypes.byref(o), 32, 32, d, d, d, d, f,
+                                 d, d, d, None, d, 1 << 40, None) == -7
 
 
 def test_product_package_has_no_oracle_dependency():
