@@ -188,6 +188,98 @@ def exact_errors(cfg, Qd, Kd, Vd, O):
     return errs
 
 
+def kv_divisor_bins(nmid, target_rows, rb=12):
+    """Bins B for the E3 setting B = r/12: the divisor of n_mid (contiguous bins must divide
+    it, reading Z13) whose B * rb coreset rows come closest to `target_rows`."""
+    best = 1
+    for b in range(1, nmid // rb + 1):
+        if nmid % b == 0 and abs(b * rb - target_rows) < abs(best * rb - target_rows):
+            best = b
+    return best
+
+
+def kv_variant(dev, flush, block, steps, with_exact=True):
+    """KV-cache workload (E3 protocol P:667-669, reading Z24) at the llm32k
+    shapes (GQA 32/8, n = 32768, d = 128, bf16, L family): prefill compression keeping the first and
+    last 32 tokens and compressing the rest to ~25 % of the context with B = r/12 bins (rb = 12), then
+    one decode step (m = 1 new query per q-head) over the compressed cache vs exact decode attention
+    over the full cache.  L2 flushed before every timed call."""
+    import torch
+    import torch.nn.functional as Fnn
+
+    import paper_2602_10056_b200 as wc
+    from paper_2602_10056_b200.inputs import CONFIGS, make_config, make_qkv
+
+    cfg = CONFIGS["llm32k"]
+    kf = kl = 32
+    nmid = cfg.n - kf - kl
+    bins = kv_divisor_bins(nmid, cfg.n // 4 - kf - kl)
+    r = 12 * bins
+    Q, K, V = make_config(cfg)
+    Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+    del Q
+    Qdec = make_qkv(cfg.batch, cfg.hq, cfg.hkv, 1, 16, cfg.d, cfg.dtype, cfg.family, seed=777)[0].to(dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, k):
+        # a GPU-side sleep queued ahead of e0 keeps the device busy while the host enqueues fn, so
+        # e0 -> e1 is device time (host launch latency excluded; a decode loop would be graph-captured)
+        out, ts = None, []
+        for _ in range(k):
+            flush.zero_()
+            torch.cuda._sleep(200000)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return out, ts
+
+    comp = lambda: wc.compress_kv(Qd, Kd, Vd, r, keep_first=kf, keep_last=kl, bins=bins, block=block)
+    comp()
+    torch.cuda.synchronize()
+    cache, tc = timed(comp, max(3, min(steps, 5)))
+    dec = lambda: wc.attend(Qdec, cache)
+    dec()
+    Od, td = timed(dec, 30)
+    exact = lambda: Fnn.scaled_dot_product_attention(Qdec, Kd, Vd, enable_gqa=True)
+    exact()
+    Oe, te = timed(exact, 30)
+    C = cache.KS.shape[1]
+    units = cfg.units
+    cache_bytes = units * C * (cfg.d * 2 + (cfg.d + 1) * 4) + 2 * units * cfg.d * 2
+    kv_bytes = units * cfg.n * 2 * cfg.d * 2
+    dec_us = statistics.median(td) * 1e3
+    res = {"workload": "llm32k", "keep_first": kf, "keep_last": kl, "r": r, "bins": bins, "r_per_bin": 12,
+           "block": block, "cache_rows_per_head": C, "c_eff_min": int(cache.r_eff.min().item()),
+           "cache_bytes": cache_bytes, "kv_bytes": kv_bytes, "cache_fraction_of_kv_bytes": cache_bytes / kv_bytes,
+           "compress_ms": statistics.median(tc), "decode_us": dec_us,
+           "decode_steps_per_s": 1e6 / dec_us,
+           "decode_cache_gbs": cache_bytes / (dec_us / 1e6) / 1e9,
+           "exact_decode_sdpa_us": statistics.median(te) * 1e3,
+           "timing": "CUDA events per call (device time: a queued GPU sleep hides host launch latency), L2 flushed before each; decode = one wildcat_attend (m = 1 per q-head, "
+                     "all 32 q-heads) over the compressed cache; exact = torch SDPA over the full K, V"}
+    if with_exact:
+        beta = 1.0 / math.sqrt(cfg.d)
+        errs = []
+        g = cfg.hq // cfg.hkv
+        for h in range(cfg.hq):
+            q = Qdec[0, h].double()
+            kk, vv = Kd[0, h // g].double(), Vd[0, h // g].double()
+            ex = torch.softmax(beta * (q @ kk.T), dim=-1) @ vv
+            errs.append(float((Od[0, h].double() - ex).abs().max() / vv.abs().max()))
+        res["max_rel_err_vs_exact"] = max(errs)
+        res["exact_sdpa_bf16_rel_err"] = max(
+            float((Oe[0, h].double() - torch.softmax(1.0 / math.sqrt(cfg.d) * (Qdec[0, h].double()
+                  @ Kd[0, h // g].double().T), -1) @ Vd[0, h // g].double()).abs().max() / Vd[0, h // g].double().abs().max())
+            for h in range(cfg.hq))
+    del cache, Qd, Kd, Vd
+    torch.cuda.empty_cache()
+    return res
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -447,6 +539,10 @@ def main():
                                   "ms_per_step": statistics.mean(vt),
                                   "queries_per_s": queries_per_rank * world / (statistics.mean(vt) / 1e3),
                                   "max_rel_err_vs_exact": berr}
+    # KV-cache workload (prefill compression + decode) at the LLM shapes, rank 0, single GPU
+    if not args.no_variants and mode == "replicas" and rank == 0 and world == 1 and args.config == "headline":
+        variants = variants or {}
+        variants["kvcache"] = kv_variant(dev, flush, max(2, args.block), args.steps, with_exact=not args.no_exact)
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}" + (f"_b{args.block}" if args.block >= 2 else "")
                       + ".json")

@@ -61,172 +61,318 @@ __global__ void kv_assemble_kernel(const T *__restrict__ K, const T *__restrict_
     for (int j = lane; j < dc; j += 32) xc[j] = ok ? X[((int64_t)u * R + j0) * dc + j] : 0.f;
 }
 
-constexpr int kDecQ = 16;   // query rows per CTA
-constexpr int kDecC = 64;   // cache rows per CTA
-constexpr int kDecT = 256;  // threads
+constexpr int kDecC = 64;   // cache rows per tile
+constexpr int kDecT = 256;  // threads: QR query rows x (256 / QR) threads
+constexpr int kDecQmax = 16;
 
-template <int D> struct DecSmem {
-    static constexpr int kQ = 0;                                // [kDecQ][D]    fp32, scaled by beta*log2(e)
-    static constexpr int kK = kQ + kDecQ * D;                   // [kDecC][D+1]  fp32
-    static constexpr int kX = kK + kDecC * (D + 1);             // [kDecC][D+1]  fp32 ([V_S, w] rows)
-    static constexpr int kS = kX + kDecC * (D + 1);             // [kDecQ][kDecC] scores -> P
-    static constexpr int kM = kS + kDecQ * kDecC;               // [kDecQ] chunk max
-    static constexpr int kFloats = kM + kDecQ + 1;
+template <int D, int QR> struct DecSmem {
+    static constexpr int kQ = 0;                                // [QR][D]       fp32, scaled by beta*log2(e)
+    static constexpr int kKW = D + 1;                           // K row stride in 32-bit words (raw elements;
+    static constexpr int kK = kQ + QR * D;                      //  bf16 rows use (D/2 + 1) of them)
+    static constexpr int kX = kK + kDecC * kKW;                 // [kDecC][D+1]  fp32 ([V_S, w] rows)
+    static constexpr int kS = kX + kDecC * (D + 1);             // [kDecC][QR]   P (row-major over cache rows)
+    static constexpr int kF = kS + QR * kDecC;                  // [QR] this tile's rescale factors
+    static constexpr int kDen = kF + QR;                        // [QR] running denominators
+    static constexpr int kRed = kDen + QR;                      // [2][8] cross-warp max / den partials
+    static constexpr int kR = kRed + 16;                        // [256/D][QR][D] row-group partial sums
+    static constexpr int kFloats = kR + kDecT * QR;
     static constexpr size_t kBytes = (size_t)kFloats * 4;
 };
 
-// part: [units][qz][splits][kDecQ][D + 2] = (max, num[0..D-1], den) per (chunk, row), log2 domain.
-template <typename T, int D>
+// One cache tile (kDecC rows of KS and X) held in registers between its global load and its
+// shared-memory store, so the next tile's loads are in flight while the current one is computed.
+template <typename T, int D> struct DecTile {
+    static constexpr int kKTot = kDecC * D * (int)sizeof(T) / 16;       // 16-byte K vectors per tile
+    static constexpr int kKVec = (kKTot + kDecT - 1) / kDecT;             // ... per thread
+    static constexpr int kXF = kDecC * (D + 1) / kDecT;                   // X floats per thread (exact)
+    static constexpr int kXRem = kDecC * (D + 1) - kXF * kDecT;
+    uint4 k[kKVec];
+    float x[kXF + 1];
+    __device__ __forceinline__ void load(const T *KSu, const float *Xu, int c0, int nc, int tid) {
+        const uint4 *kv = reinterpret_cast<const uint4 *>(KSu + (int64_t)c0 * D);
+        constexpr int kPerRow = D * (int)sizeof(T) / 16;
+#pragma unroll
+        for (int i = 0; i < kKVec; ++i) {
+            const int e = tid + i * kDecT;
+            k[i] = (e < kKTot && e / kPerRow < nc) ? __ldg(kv + e) : make_uint4(0, 0, 0, 0);
+        }
+        const float *xr = Xu + (int64_t)c0 * (D + 1);
+        const int lim = nc * (D + 1);
+#pragma unroll
+        for (int i = 0; i < kXF; ++i) {
+            const int e = tid + i * kDecT;
+            x[i] = e < lim ? __ldg(xr + e) : 0.f;
+        }
+        if (kXRem) x[kXF] = (tid < kXRem && kXF * kDecT + tid < lim) ? __ldg(xr + kXF * kDecT + tid) : 0.f;
+    }
+    // K rows stay raw (bf16 pairs / fp32) in shared memory, row stride kW = D*sizeof(T)/4 + 1 words
+    // (odd: the score loop's row-per-lane reads are conflict-free); 4 word stores per vector.
+    static constexpr int kW = D * (int)sizeof(T) / 4 + 1;
+    __device__ __forceinline__ void store(uint32_t *ks, float *xs, int tid) const {
+        constexpr int kPerRow = D * (int)sizeof(T) / 16;
+#pragma unroll
+        for (int i = 0; i < kKVec; ++i) {
+            const int e = tid + i * kDecT, row = e / kPerRow, c = e % kPerRow;
+            if (kKTot % kDecT && e >= kKTot) break;
+            uint32_t *dst = ks + row * kW + 4 * c;
+            dst[0] = k[i].x; dst[1] = k[i].y; dst[2] = k[i].z; dst[3] = k[i].w;
+        }
+#pragma unroll
+        for (int i = 0; i < kXF; ++i) xs[tid + i * kDecT] = x[i];
+        if (kXRem && tid < kXRem) xs[kXF * kDecT + tid] = x[kXF];
+    }
+};
+
+// Grid (splits, units, qz).  CTA (split, u, z) runs query rows [QR z, QR z + QR) of unit u over the
+// cache tiles split, split + splits, ... (kDecC rows each) with an online max.
+//   scores: thread (q = tid / TPR, g = tid % TPR), TPR = 256 / QR, computes query row q's scores of
+//           cache rows g + TPR k, the tile max, P = 2^(s - max) and P . w (the weight column, reduced
+//           over the row's TPR threads into the running denominator);
+//   P . V_S: thread (col = tid % D, rg = tid / D) owns value column col for ALL QR query rows over the
+//           cache rows of row group rg (rows rg, rg + RS, ...; RS = 256 / D), so each X element is read
+//           once from shared memory and P arrives as one vector load per cache row.
+// QR = 4 serves one decode token of a 4-query-head group.
+// part: [units][qz][splits][QR][D + 2] = (max, num[0..D-1], den) per CTA and row (log2 domain).
+template <typename T, int D, int QR>
 __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
     const T *__restrict__ Q, const T *__restrict__ KS, const float *__restrict__ X, const int32_t *__restrict__ r_eff,
     const T *__restrict__ vmin, const T *__restrict__ vmax, int64_t m, int r, int group, int hq, int hkv, float sl2,
     int clip, T *__restrict__ O, float *__restrict__ part, unsigned *__restrict__ tickets) {
     extern __shared__ float sm[];
-    using L = DecSmem<D>;
-    float *qs = sm + L::kQ, *ks = sm + L::kK, *xs = sm + L::kX, *ss = sm + L::kS, *mx = sm + L::kM;
-    constexpr int DC = D + 1, PW = D + 2;
+    using L = DecSmem<D, QR>;
+    float *qs = sm + L::kQ, *xs = sm + L::kX, *ps = sm + L::kS, *fs = sm + L::kF, *dens = sm + L::kDen;
+    float *red = sm + L::kRed;
+    uint32_t *ks = reinterpret_cast<uint32_t *>(sm + L::kK);
+    constexpr int KW = DecTile<T, D>::kW;
+    constexpr int TPR = kDecT / QR, DC = D + 1, PW = D + 2, NS = kDecC / TPR;
+    constexpr int WPR = TPR > 32 ? TPR / 32 : 1;  // warps per query row (score phase)
+    constexpr int RS = kDecT / D;                 // row groups of the P . V_S phase
     const int split = blockIdx.x, u = blockIdx.y, z = blockIdx.z, splits = gridDim.x, qz = gridDim.z;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, q = tid / TPR, g = tid % TPR, col = tid % D, rg = tid / D;
     const int b = u / hkv, h = u % hkv;
     const int64_t rows = (int64_t)group * m;  // the unit's query rows are contiguous
     const int64_t qoff = ((int64_t)b * hq + (int64_t)h * group) * m;
-    const int64_t t0 = (int64_t)z * kDecQ;
-    const int nq = (int)(rows - t0 < kDecQ ? rows - t0 : kDecQ);
+    const int64_t t0 = (int64_t)z * QR;
+    const int nq = (int)(rows - t0 < QR ? rows - t0 : QR);
     const int re = r_eff[u];
-    const int c0 = split * kDecC, nc = max(0, min(kDecC, re - c0));
-    float *pp = part + ((((int64_t)u * qz + z) * splits + split) * kDecQ) * PW;
+    const int ntiles = (re + kDecC - 1) / kDecC;
+    const T *KSu = KS + (int64_t)u * r * D;
+    const float *Xu = X + (int64_t)u * r * DC;
 
-    if (nc > 0) {
-        for (int e = tid; e < kDecQ * D; e += kDecT) {
-            const int q = e / D, j = e % D;
-            qs[e] = q < nq ? to_f32(Q[(qoff + t0 + q) * D + j]) * sl2 : 0.f;
-        }
-        const T *kr = KS + ((int64_t)u * r + c0) * D;
-        for (int e = tid; e < nc * D; e += kDecT) ks[(e / D) * DC + e % D] = to_f32(kr[e]);
-        const float *xr = X + ((int64_t)u * r + c0) * DC;
-        for (int e = tid; e < nc * DC; e += kDecT) xs[e] = xr[e];
-        __syncthreads();
-        // scores: thread -> row q = tid / 16, cache rows c = tid % 16 + 16 k
-        {
-            const int q = tid >> 4, cl = tid & 15;
-            float acc[kDecC / 16];
+    for (int e = tid; e < QR * D; e += kDecT) {
+        const int qq = e / D, j = e % D;
+        qs[e] = qq < nq ? to_f32(Q[(qoff + t0 + qq) * D + j]) * sl2 : 0.f;
+    }
+    if (tid < QR) dens[tid] = 0.f;
+    float acc[QR];
 #pragma unroll
-            for (int k = 0; k < kDecC / 16; ++k) acc[k] = 0.f;
+    for (int k = 0; k < QR; ++k) acc[k] = 0.f;
+    float mrun = -INFINITY;  // of query row q (score-phase mapping)
+    DecTile<T, D> tile;
+    int tcur = split;
+    if (tcur < ntiles) tile.load(KSu, Xu, tcur * kDecC, min(kDecC, re - tcur * kDecC), tid);
+    while (tcur < ntiles) {
+        const int nc = min(kDecC, re - tcur * kDecC);
+        __syncthreads();  // previous tile's readers are done with ks / xs / ps / red
+        tile.store(ks, xs, tid);
+        const int tnext = tcur + splits;
+        if (tnext < ntiles) tile.load(KSu, Xu, tnext * kDecC, min(kDecC, re - tnext * kDecC), tid);
+        __syncthreads();
+        // ---- scores of query row q against cache rows g + TPR k
+        float sc[NS], sc2[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) sc[k] = sc2[k] = 0.f;
+        if constexpr (sizeof(T) == 2) {
 #pragma unroll 8
-            for (int j = 0; j < D; ++j) {
-                const float qv = qs[q * D + j];
+            for (int j2 = 0; j2 < D / 2; ++j2) {
+                const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + 2 * j2);
 #pragma unroll
-                for (int k = 0; k < kDecC / 16; ++k) acc[k] = fmaf(qv, ks[(cl + 16 * k) * DC + j], acc[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < kDecC / 16; ++k) ss[q * kDecC + cl + 16 * k] = cl + 16 * k < nc ? acc[k] : -INFINITY;
-        }
-        __syncthreads();
-        // per row: chunk max, P = 2^(s - max); warp w owns rows 2w, 2w + 1
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int q = 2 * warp + rr;
-            float a0 = ss[q * kDecC + lane], a1 = ss[q * kDecC + lane + 32];
-            float mm = fmaxf(a0, a1);
-#pragma unroll
-            for (int o = 16; o; o >>= 1) mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
-            ss[q * kDecC + lane] = lane < nc ? exp2f(a0 - mm) : 0.f;
-            ss[q * kDecC + lane + 32] = lane + 32 < nc ? exp2f(a1 - mm) : 0.f;
-            if (lane == 0) mx[q] = mm;
-        }
-        __syncthreads();
-        // partial [num | den] = P . [V_S, w]: warp w rows 2w, 2w + 1, lane -> columns lane + 32 k
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int q = 2 * warp + rr;
-            float acc[(DC + 31) / 32];
-#pragma unroll
-            for (int k = 0; k < (DC + 31) / 32; ++k) acc[k] = 0.f;
-            for (int c = 0; c < nc; ++c) {
-                const float p = ss[q * kDecC + c];
-#pragma unroll
-                for (int k = 0; k < (DC + 31) / 32; ++k) {
-                    const int col = lane + 32 * k;
-                    if (col < DC) acc[k] = fmaf(p, xs[c * DC + col], acc[k]);
+                for (int k = 0; k < NS; ++k) {
+                    const uint32_t w = ks[(g + TPR * k) * KW + j2];
+                    sc[k] = fmaf(qv.x, __uint_as_float(w << 16), sc[k]);
+                    sc2[k] = fmaf(qv.y, __uint_as_float(w & 0xffff0000u), sc2[k]);
                 }
             }
-            float *o = pp + (int64_t)q * PW;
-            if (lane == 0) o[0] = mx[q];
+        } else {
+#pragma unroll 8
+            for (int j = 0; j < D; j += 2) {
+                const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + j);
 #pragma unroll
-            for (int k = 0; k < (DC + 31) / 32; ++k) {
-                const int col = lane + 32 * k;
-                if (col < DC) o[1 + col] = acc[k];
+                for (int k = 0; k < NS; ++k) {
+                    sc[k] = fmaf(qv.x, __uint_as_float(ks[(g + TPR * k) * KW + j]), sc[k]);
+                    sc2[k] = fmaf(qv.y, __uint_as_float(ks[(g + TPR * k) * KW + j + 1]), sc2[k]);
+                }
             }
         }
-    } else {
-        for (int e = tid; e < kDecQ * PW; e += kDecT) pp[e] = (e % PW) == 0 ? -INFINITY : 0.f;
+        float tm = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            sc[k] = g + TPR * k < nc ? sc[k] + sc2[k] : -INFINITY;
+            tm = fmaxf(tm, sc[k]);
+        }
+#pragma unroll
+        for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+        if constexpr (WPR > 1) {
+            if ((tid & 31) == 0) red[tid >> 5] = tm;
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) tm = fmaxf(tm, red[q * WPR + w]);
+        }
+        const float mnew = fmaxf(mrun, tm);  // nc >= 1, so finite
+        const float f = exp2f(mrun - mnew);  // 0 on the first tile
+        mrun = mnew;
+        float dp = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int c = g + TPR * k;
+            const float pv = exp2f(sc[k] - mnew);  // 0 for rows past nc
+            ps[c * QR + q] = pv;
+            if (c < nc) dp = fmaf(pv, xs[c * DC + D], dp);
+        }
+#pragma unroll
+        for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+        if constexpr (WPR > 1) {
+            if ((tid & 31) == 0) red[8 + (tid >> 5)] = dp;
+            __syncthreads();
+            if (g == 0) {
+                dp = 0.f;
+#pragma unroll
+                for (int w = 0; w < WPR; ++w) dp += red[8 + q * WPR + w];
+            }
+        }
+        if (g == 0) {
+            dens[q] = dens[q] * f + dp;
+            fs[q] = f;
+        }
+        __syncthreads();
+        // ---- P . V_S: column col for all QR query rows over the row group's cache rows
+#pragma unroll
+        for (int k = 0; k < QR; ++k) acc[k] *= fs[k];
+#pragma unroll 4
+        for (int c = rg; c < nc; c += RS) {
+            const float x = xs[c * DC + col];
+#pragma unroll
+            for (int k4 = 0; k4 < QR; k4 += 4) {
+                const float4 p4 = *reinterpret_cast<const float4 *>(ps + c * QR + k4);
+                acc[k4] = fmaf(p4.x, x, acc[k4]);
+                acc[k4 + 1] = fmaf(p4.y, x, acc[k4 + 1]);
+                acc[k4 + 2] = fmaf(p4.z, x, acc[k4 + 2]);
+                acc[k4 + 3] = fmaf(p4.w, x, acc[k4 + 3]);
+            }
+        }
+        tcur = tnext;
     }
-    // the last CTA of (unit, query chunk) merges the chunk partials
+    // ---- this CTA's partial (max, num, den) per query row; num summed over the RS row groups
+    static_assert(RS > 1, "D <= 128");
+    float *rsum = sm + L::kR;
+#pragma unroll
+    for (int k = 0; k < QR; ++k) rsum[(rg * QR + k) * D + col] = acc[k];
+    __syncthreads();
+    float *pbase = part + (((int64_t)u * qz + z) * splits + split) * QR * PW;
+    if (g == 0) pbase[q * PW] = mrun;
+    if (tid < QR) pbase[tid * PW + 1 + D] = dens[tid];
+    for (int e = tid; e < QR * D; e += kDecT) {
+        const int qq = e / D, cc = e % D;
+        float v = 0.f;
+#pragma unroll
+        for (int k = 0; k < RS; ++k) v += rsum[(k * QR + qq) * D + cc];
+        pbase[qq * PW + 1 + cc] = v;
+    }
+    // merge: the last CTA of (unit, query chunk) combines the partials (also when splits = 1)
     __shared__ unsigned s_last;
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const unsigned t = atomicAdd(tickets + (int64_t)u * qz + z, 1u);
+        const unsigned t = splits > 1 ? atomicAdd(tickets + (int64_t)u * qz + z, 1u) : 0u;
         s_last = (t == (unsigned)splits - 1) ? 1u : 0u;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const float *pu = part + (((int64_t)u * qz + z) * splits) * kDecQ * PW;
-    for (int q = warp; q < nq; q += kDecT / 32) {
-        float M = -INFINITY;
-        for (int s = lane; s < splits; s += 32) M = fmaxf(M, __ldcg(pu + ((int64_t)s * kDecQ + q) * PW));
+    constexpr int NCOL = (DC + TPR - 1) / TPR;
+    const float *pu = part + (((int64_t)u * qz + z) * splits) * QR * PW;
+    float M = -INFINITY;
+    for (int s2 = g; s2 < splits; s2 += TPR) M = fmaxf(M, __ldcg(pu + ((int64_t)s2 * QR + q) * PW));
 #pragma unroll
-        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        float acc[(DC + 31) / 32];
+    for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if constexpr (WPR > 1) {
+        if ((tid & 31) == 0) red[tid >> 5] = M;
+        __syncthreads();
 #pragma unroll
-        for (int k = 0; k < (DC + 31) / 32; ++k) acc[k] = 0.f;
-        if (M > -INFINITY) {
-            for (int s = 0; s < splits; ++s) {
-                const float *ps = pu + ((int64_t)s * kDecQ + q) * PW;
-                const float ms = __ldcg(ps);
-                if (!(ms > -INFINITY)) continue;
-                const float f = exp2f(ms - M);
+        for (int w = 0; w < WPR; ++w) M = fmaxf(M, red[q * WPR + w]);
+    }
+    float o_[NCOL];
 #pragma unroll
-                for (int k = 0; k < (DC + 31) / 32; ++k) {
-                    const int col = lane + 32 * k;
-                    if (col < DC) acc[k] = fmaf(f, __ldcg(ps + 1 + col), acc[k]);
-                }
-            }
-        }
-        // den = column D: lane D % 32 of chunk k = D / 32
-        const float den = __shfl_sync(0xffffffffu, acc[D / 32], D % 32);
-        T *orow = O + (qoff + t0 + q) * D;
+    for (int k = 0; k < NCOL; ++k) o_[k] = 0.f;
+    if (M > -INFINITY) {
+#pragma unroll 4
+        for (int s2 = 0; s2 < splits; ++s2) {
+            const float *pp = pu + ((int64_t)s2 * QR + q) * PW;
+            const float ms = __ldcg(pp);
+            const float f = ms > -INFINITY ? exp2f(ms - M) : 0.f;
 #pragma unroll
-        for (int k = 0; k < (DC + 31) / 32; ++k) {
-            const int col = lane + 32 * k;
-            if (col < D) {
-                float o = den > 0.f ? acc[k] / den : 0.f;
-                if (clip) o = fminf(fmaxf(o, to_f32(vmin[(int64_t)u * D + col])), to_f32(vmax[(int64_t)u * D + col]));
-                orow[col] = from_f32<T>(o);
+            for (int k = 0; k < NCOL; ++k) {
+                const int cc = g + TPR * k;
+                if (cc < DC) o_[k] = fmaf(f, __ldcg(pp + 1 + cc), o_[k]);
             }
         }
     }
-    if (tid == 0) tickets[(int64_t)u * qz + z] = 0u;  // reusable without a reset launch
+    if (splits > 1 && tid == 0) tickets[(int64_t)u * qz + z] = 0u;  // reusable without a reset launch
+    // den = column D, owned by thread g = D % TPR as o_[D / TPR]
+    __syncthreads();
+    if (g == D % TPR) dens[q] = o_[D / TPR];
+    __syncthreads();
+    if (q >= nq) return;
+    const float den = dens[q];
+    T *orow = O + (qoff + t0 + q) * D;
+#pragma unroll
+    for (int k = 0; k < NCOL; ++k) {
+        const int cc = g + TPR * k;
+        if (cc < D) {
+            float o = den > 0.f ? o_[k] / den : 0.f;
+            if (clip) o = fminf(fmaxf(o, to_f32(vmin[(int64_t)u * D + cc])), to_f32(vmax[(int64_t)u * D + cc]));
+            orow[cc] = from_f32<T>(o);
+        }
+    }
 }
 
-template <typename T, int D>
-int launch_decode_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                     const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
-    using L = DecSmem<D>;
-    const int splits = (int)std::max<int64_t>(1, (Dm.r + kDecC - 1) / kDecC);
-    const int qz = (int)(((int64_t)Dm.group() * Dm.m + kDecQ - 1) / kDecQ);
+// Query rows per CTA: 4 when one CTA covers the unit's whole query group (a decode token of a
+// 4-head GQA group), else 16.
+inline int decode_qr(const Dims &D) { return (int64_t)D.group() * D.m <= 4 ? 4 : kDecQmax; }
+
+// CTAs per (unit, query chunk): about two per SM over the whole grid, at most one per tile.
+int decode_splits(const Dims &D) {
+    const int64_t ntiles = std::max<int64_t>(1, (D.r + kDecC - 1) / kDecC);
+    const int64_t qz = ((int64_t)D.group() * D.m + decode_qr(D) - 1) / decode_qr(D);
+    const int64_t want = (2 * 148 + D.units() * qz - 1) / (D.units() * qz);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, want));
+}
+
+template <typename T, int D, int QR>
+int launch_decode_tdq(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                      const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+    using L = DecSmem<D, QR>;
+    const int splits = decode_splits(Dm);
+    const int qz = (int)(((int64_t)Dm.group() * Dm.m + QR - 1) / QR);
     float *part = static_cast<float *>(ws);
     unsigned *tickets = reinterpret_cast<unsigned *>(
-        static_cast<char *>(ws) + (size_t)Dm.units() * qz * splits * kDecQ * (D + 2) * sizeof(float));
-    if (cudaMemsetAsync(tickets, 0, (size_t)Dm.units() * qz * sizeof(unsigned), st) != cudaSuccess) return -1;
-    auto kern = attend_decode_kernel<T, D>;
+        static_cast<char *>(ws) + (size_t)Dm.units() * qz * splits * QR * (D + 2) * sizeof(float));
+    if (splits > 1 && cudaMemsetAsync(tickets, 0, (size_t)Dm.units() * qz * sizeof(unsigned), st) != cudaSuccess)
+        return -1;
+    auto kern = attend_decode_kernel<T, D, QR>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
     kern<<<dim3(splits, Dm.units(), qz), kDecT, L::kBytes, st>>>(
         static_cast<const T *>(Q), static_cast<const T *>(KS), X, r_eff, static_cast<const T *>(vmin),
         static_cast<const T *>(vmax), Dm.m, Dm.r, Dm.group(), Dm.hq, Dm.hkv, (float)(beta * 1.4426950408889634), clip,
         static_cast<T *>(O), part, tickets);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename T, int D>
+int launch_decode_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                     const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+    if (decode_qr(Dm) == 4) return launch_decode_tdq<T, D, 4>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    return launch_decode_tdq<T, D, kDecQmax>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
 }
 
 template <typename T>
@@ -244,9 +390,9 @@ int launch_decode_t(const Dims &Dm, const void *Q, const void *KS, const float *
 }  // namespace
 
 size_t attend_decode_ws_bytes(const Dims &D) {
-    const int64_t splits = std::max<int64_t>(1, (D.r + kDecC - 1) / kDecC);
-    const int64_t qz = ((int64_t)D.group() * D.m + kDecQ - 1) / kDecQ;
-    return (size_t)D.units() * qz * splits * kDecQ * (D.d + 2) * sizeof(float) + (size_t)D.units() * qz * 4 + 256;
+    const int64_t splits = decode_splits(D), QR = decode_qr(D);
+    const int64_t qz = ((int64_t)D.group() * D.m + QR - 1) / QR;
+    return (size_t)D.units() * qz * splits * QR * (D.d + 2) * sizeof(float) + (size_t)D.units() * qz * 4 + 256;
 }
 
 int launch_attend_decode(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
