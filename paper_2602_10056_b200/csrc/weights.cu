@@ -173,6 +173,26 @@ __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restri
 }
 
 // 8 RHS columns per CTA, 256 threads: thread t owns panel row t/8, column t%8.
+// The solve is a chain of steps: per panel P (kPB rows), CHUNK steps (acc -= L-block . z over kCBs
+// already-solved rows) and one DIAG step (z_P = Dinv_PP . acc); forward over P = 0.., then backward
+// (L^T) over P = npan-1..0.  No L or Dinv load depends on z, so the operands of the next kSolveNS-1
+// steps are in flight (cp.async, zero-filled out of range, transposes done by the copy placement)
+// while the current step computes: the chain carries shared-memory latency only.
+constexpr int kSolveNS = 4;                              // operand ring stages
+constexpr int kSolveBuf = kPB * (kCBs + 1);              // doubles per stage (>= kPB * (kPB + 1))
+constexpr int kSolveMaxSteps = 2 * (1024 / kPB) * (1024 / kCBs + 1);
+
+// 8-byte async copy, zero-filled (no global read) when !ok; `safe` is any valid global address
+__device__ __forceinline__ void cp_async8_zfill(double *dst, const double *src, bool ok, const double *safe) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(ok ? src : safe),
+                 "r"(ok ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__restrict__ Y,
                                                             const double *__restrict__ L,
@@ -180,11 +200,10 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
                                                             const int32_t *__restrict__ r_eff, int r,
                                                             float *__restrict__ X) {
     constexpr int DC = D + 1;
-    constexpr int NL = kPB * kCBs / 256;  // L elements per thread per round trip
-    extern __shared__ double zs[];          // z[r][8]
-    __shared__ double Lb[kPB][kCBs + 1];    // a fetched chunk of L (row-major panel rows / transposed)
-    __shared__ double Di[kPB][kPB + 1];     // inverse of the panel's diagonal block
+    extern __shared__ double zs[];  // z[r][8], then the operand ring [kSolveNS][kSolveBuf]
     __shared__ double tP[kPB][8];
+    __shared__ int steps[kSolveMaxSteps];
+    __shared__ int nsteps;
     const int u = blockIdx.y, tid = threadIdx.x;
     const int cbase = blockIdx.x * 8;
     const int q = r_eff[u];
@@ -192,94 +211,107 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
     const double *Lu = L + (int64_t)u * r * r;
     const double *Du = Dinv + (int64_t)u * nbl * kPB * kPB;
     float *Xu = X + (int64_t)u * r * DC;
+    double *ring = zs + (size_t)r * 8;
+    const int npan = (q + kPB - 1) / kPB;
+    auto nch = [&](int dir, int P) {
+        const int p0 = P * kPB, pe = min(p0 + kPB, q);
+        return dir == 0 ? (p0 + kCBs - 1) / kCBs : (q - pe + kCBs - 1) / kCBs;
+    };
+    if (tid == 0) {  // step list: dir << 24 | P << 12 | (chunk + 1), chunk -1 = DIAG
+        int k = 0;
+        for (int P = 0; P < npan; ++P) {
+            for (int c = 0; c < nch(0, P); ++c) steps[k++] = (P << 12) | (c + 1);
+            steps[k++] = P << 12;
+        }
+        for (int P = npan - 1; P >= 0; --P) {
+            for (int c = 0; c < nch(1, P); ++c) steps[k++] = (1 << 24) | (P << 12) | (c + 1);
+            steps[k++] = (1 << 24) | (P << 12);
+        }
+        nsteps = k;
+    }
 #pragma unroll 8
     for (int e = tid; e < q * 8; e += 256) {
         const int a = e / 8, cc = e % 8, col = cbase + cc;
         zs[a * 8 + cc] = col < DC ? __ldg(Y + ((int64_t)u * r + a) * DC + col) : 0.0;
     }
     __syncthreads();
-    const int pr = tid / 8, pc = tid % 8;
-    auto load_dinv = [&](int blk, bool trans) {
-        const double *src = Du + (int64_t)blk * kPB * kPB;
-        double t[kPB * kPB / 256];
+    const int ns = nsteps;
+    // issue the operand copies of step k into ring stage k % kSolveNS (one commit group per step)
+    auto issue = [&](int k) {
+        if (k < ns) {
+            const int code = steps[k], dir = code >> 24, P = (code >> 12) & 0xfff, c = (code & 0xfff) - 1;
+            const int p0 = P * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
+            double *buf = ring + (size_t)(k % kSolveNS) * kSolveBuf;
+            if (c < 0) {  // Di (forward: row-major lower; backward: transposed)
+                const double *src = Du + (int64_t)P * kPB * kPB;
 #pragma unroll
-        for (int k = 0; k < kPB * kPB / 256; ++k) t[k] = __ldg(src + tid + 256 * k);
+                for (int kk = 0; kk < kPB * kPB / 256; ++kk) {
+                    const int e = tid + 256 * kk;
+                    double *dst = dir ? buf + (e % kPB) * (kPB + 1) + e / kPB : buf + (e / kPB) * (kPB + 1) + e % kPB;
+                    cp_async8_zfill(dst, src + e, true, Lu);
+                }
+            } else if (dir == 0) {  // Lb[rr][c2] = L[p0 + rr][b0 + c2]
+                const int b0 = c * kCBs, nbk = min(kCBs, p0 - b0);
 #pragma unroll
-        for (int k = 0; k < kPB * kPB / 256; ++k) {
-            const int e = tid + 256 * k;
-            if (trans) Di[e % kPB][e / kPB] = t[k];
-            else Di[e / kPB][e % kPB] = t[k];
+                for (int kk = 0; kk < kPB * kCBs / 256; ++kk) {
+                    const int e = tid + 256 * kk, rr = e / kCBs, c2 = e % kCBs;
+                    cp_async8_zfill(buf + rr * (kCBs + 1) + c2, Lu + (int64_t)(p0 + rr) * r + b0 + c2, rr < nb && c2 < nbk,
+                                    Lu);
+                }
+            } else {  // Lb[c2][bb] = L[b0 + bb][p0 + c2]  (coalesced rows of L, transposed placement)
+                const int b0 = pe + c * kCBs, nbk = min(kCBs, q - b0);
+#pragma unroll
+                for (int kk = 0; kk < kPB * kCBs / 256; ++kk) {
+                    const int e = tid + 256 * kk, bb = e / kPB, c2 = e % kPB;
+                    cp_async8_zfill(buf + c2 * (kCBs + 1) + bb, Lu + (int64_t)(b0 + bb) * r + p0 + c2, bb < nbk && c2 < nb,
+                                    Lu);
+                }
+            }
         }
+        cp_async_commit();
     };
-    // ---- forward: z_P = Dinv_PP (y_P - L[P, 0:p0] z[0:p0])
-    for (int p0 = 0; p0 < q; p0 += kPB) {
-        const int nb = min(kPB, q - p0);
-        double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
-        for (int b0 = 0; b0 < p0; b0 += kCBs) {
-            const int nbk = min(kCBs, p0 - b0);
-            double t[NL];
 #pragma unroll
-            for (int k = 0; k < NL; ++k) {
-                const int e = tid + 256 * k, rr = e / kCBs, c2 = e % kCBs;
-                t[k] = (rr < nb && c2 < nbk) ? __ldg(Lu + (int64_t)(p0 + rr) * r + b0 + c2) : 0.0;
+    for (int k = 0; k < kSolveNS - 1; ++k) issue(k);
+    const int pr = tid / 8, pc = tid % 8;
+    double acc = 0.0;
+    bool panel_start = true;
+    for (int k = 0; k < ns; ++k) {
+        const int code = steps[k], dir = code >> 24, P = (code >> 12) & 0xfff, c = (code & 0xfff) - 1;
+        const int p0 = P * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
+        const double *buf = ring + (size_t)(k % kSolveNS) * kSolveBuf;
+        if (panel_start) acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
+        cp_async_wait<kSolveNS - 2>();  // this thread's copies of step k landed
+        if (c < 0) tP[pr][pc] = acc;
+        __syncthreads();                // everyone's copies (and tP) visible
+        if (c < 0) {
+            if (pr < nb) {  // Di is triangular with explicit zeros: full-length dot, two partial sums
+                double z0 = 0.0, z1 = 0.0;
+#pragma unroll 8
+                for (int j = 0; j < kPB; j += 2) {
+                    z0 = fma(buf[pr * (kPB + 1) + j], tP[j][pc], z0);
+                    z1 = fma(buf[pr * (kPB + 1) + j + 1], tP[j + 1][pc], z1);
+                }
+                zs[(p0 + pr) * 8 + pc] = z0 + z1;
             }
-            __syncthreads();
+        } else if (pr < nb) {
+            const int b0 = dir == 0 ? c * kCBs : pe + c * kCBs;
+            const int nbk = dir == 0 ? min(kCBs, p0 - b0) : min(kCBs, q - b0);
+            const double *lr = buf + pr * (kCBs + 1);
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+            int bb = 0;
+#pragma unroll 4
+            for (; bb + 4 <= nbk; bb += 4) {
 #pragma unroll
-            for (int k = 0; k < NL; ++k) {
-                const int e = tid + 256 * k;
-                Lb[e / kCBs][e % kCBs] = t[k];
+                for (int kk = 0; kk < 4; ++kk) a4[kk] = fma(-lr[bb + kk], zs[(b0 + bb + kk) * 8 + pc], a4[kk]);
             }
-            __syncthreads();
-            if (pr < nb)
-#pragma unroll 8
-                for (int bb = 0; bb < nbk; ++bb) acc = fma(-Lb[pr][bb], zs[(b0 + bb) * 8 + pc], acc);
+            for (; bb < nbk; ++bb) a4[0] = fma(-lr[bb], zs[(b0 + bb) * 8 + pc], a4[0]);
+            acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
         }
-        load_dinv(p0 / kPB, false);
-        tP[pr][pc] = acc;
-        __syncthreads();
-        if (pr < nb) {
-            double z = 0.0;
-#pragma unroll 8
-            for (int j = 0; j <= pr; ++j) z = fma(Di[pr][j], tP[j][pc], z);
-            zs[(p0 + pr) * 8 + pc] = z;
-        }
-        __syncthreads();
+        __syncthreads();  // stage k % NS and tP free; z of a DIAG step visible
+        issue(k + kSolveNS - 1);
+        panel_start = (c < 0);
     }
-    // ---- backward (L^T upper): x_P = Dinv_PP^T (z_P - L[pe:q, P]^T x[pe:q])
-    const int npan = (q + kPB - 1) / kPB;
-    for (int pi = npan - 1; pi >= 0; --pi) {
-        const int p0 = pi * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
-        double acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
-        for (int b0 = pe; b0 < q; b0 += kCBs) {
-            const int nbk = min(kCBs, q - b0);
-            double t[NL];
-#pragma unroll
-            for (int k = 0; k < NL; ++k) {  // row b0 + bb, column p0 + c2 (coalesced), staged transposed
-                const int e = tid + 256 * k, bb = e / kPB, c2 = e % kPB;
-                t[k] = (bb < nbk && c2 < nb) ? __ldg(Lu + (int64_t)(b0 + bb) * r + p0 + c2) : 0.0;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < NL; ++k) {
-                const int e = tid + 256 * k;
-                Lb[e % kPB][e / kPB] = t[k];
-            }
-            __syncthreads();
-            if (pr < nb)
-#pragma unroll 8
-                for (int bb = 0; bb < nbk; ++bb) acc = fma(-Lb[pr][bb], zs[(b0 + bb) * 8 + pc], acc);
-        }
-        load_dinv(pi, true);  // Di = Dinv_PP^T (upper triangular)
-        tP[pr][pc] = acc;
-        __syncthreads();
-        if (pr < nb) {
-            double x = 0.0;
-#pragma unroll 8
-            for (int j = pr; j < nb; ++j) x = fma(Di[pr][j], tP[j][pc], x);
-            zs[(p0 + pr) * 8 + pc] = x;
-        }
-        __syncthreads();
-    }
+    cp_async_wait<0>();
     for (int e = tid; e < r * 8; e += 256) {
         const int a = e / 8, cc = e % 8, col = cbase + cc;
         if (col < DC) Xu[(int64_t)a * DC + col] = a < q ? (float)zs[a * 8 + cc] : 0.f;
@@ -580,9 +612,9 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
                    double *Dinv, cudaStream_t st) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
     weights_dinv_kernel<<<dim3(nbl, Dm.units()), 32, 0, st>>>(L, r_eff, Dm.r, Dinv);
-    const size_t smem = (size_t)8 * Dm.r * sizeof(double);
+    const size_t smem = ((size_t)8 * Dm.r + (size_t)kSolveNS * kSolveBuf) * sizeof(double);
     auto sk = weights_solve_kernel<D>;
-    // the kernel also holds ~45 KB of static smem: always raise the dynamic limit
+    // z plus the operand ring is dynamic (up to ~197 KB at r = 1024): always raise the limit
     cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 g2((D + 1 + 7) / 8, Dm.units());
     sk<<<g2, 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
