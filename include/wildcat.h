@@ -178,6 +178,23 @@ int wc_comm_unique_id(void *id128);
 int wc_comm_init(void **comm, const void *id128, int world, int rank);
 int wc_comm_destroy(void *comm);
 
+/* Device-initiated transport for the same n-sharded forward: no NCCL call per
+ * round.  Each rank allocates a mailbox of 2 x world x capacity doubles (+ flags) in its own HBM
+ * (the library's only allocation besides the comm) and exports it with CUDA IPC:
+ *   wc_p2p_comm_create(&comm, world, rank, capacity, handle64)  -> this rank's 64-byte IPC handle
+ *   (the caller all-gathers the handles, e.g. torch.distributed.all_gather_object, in rank order)
+ *   wc_p2p_comm_connect(comm, handles)                          -> maps every peer's mailbox
+ * Every exchange of wildcat_forward_nshard (prologue reductions, the per-round residual totals and
+ * pivot packet, Y~) is then one kernel that stores this rank's vector into slot `rank` of every
+ * peer's mailbox over NVLink (peer stores, system-scope release of a per-slot epoch flag) and one
+ * kernel that acquires the world flags of the local mailbox and reduces the slots in rank order
+ * (deterministic and identical on every rank).  capacity >= r (d + 1) doubles (the Y~ exchange);
+ * smaller -> WC_EUNSUPPORTED at the forward.  world <= 8; world = 1 needs no connect.  A peer that
+ * never posts makes the waiting kernel trap after 20 s (WC_ECUDA) instead of hanging the GPU.
+ * wc_comm_destroy releases either kind of communicator. */
+int wc_p2p_comm_create(void **comm, int world, int rank, size_t capacity, void *handle64);
+int wc_p2p_comm_connect(void *comm, const void *handles);
+
 /* Alg 4 on one (batch, kv-head) unit whose n_global keys are split across the communicator's ranks:
  * this rank holds keys/values [n_offset, n_offset + shape->n) (shape->n = local count >= 1, shape->batch
  * = shape->heads_kv = 1) and shape->m local queries per q-head (any query shard).  The pivot sequence

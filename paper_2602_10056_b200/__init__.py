@@ -283,12 +283,24 @@ class NshardComm:
         self.handle, self.world, self.rank = handle, world, rank
 
     @classmethod
-    def create(cls, world: int | None = None, rank: int | None = None, group=None):
+    def create(cls, world: int | None = None, rank: int | None = None, group=None, transport: str = "nccl",
+               capacity: int = 1 << 18):
+        """transport "nccl": NCCL collectives per exchange; "p2p": device-initiated peer-memory
+        mailboxes (CUDA IPC; handles exchanged over `group`, which may be a gloo group)."""
         import torch.distributed as dist
 
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
             rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if transport == "p2p":
+            h, mine = B.wc_p2p_comm_create(world, rank, capacity)
+            if world > 1:
+                allh = [None] * world
+                dist.all_gather_object(allh, mine, group=group)
+                B.wc_p2p_comm_connect(h, allh)
+            return cls(h, world, rank)
+        if transport != "nccl":
+            raise WildcatError(f"unknown transport {transport!r}")
         uid = [B.wc_comm_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(uid, src=0, group=group)

@@ -71,7 +71,10 @@ def lib():
         L.wc_comm_destroy.argtypes = [P]
         L.wildcat_forward_nshard.argtypes = [P, S, ctypes.c_int64, ctypes.c_int64, O, P, P, P, P, P, P, P,
                                              ctypes.c_size_t, P]
-        for f in ("wc_comm_unique_id", "wc_comm_init", "wc_comm_destroy", "wildcat_forward_nshard"):
+        L.wc_p2p_comm_create.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_size_t, P]
+        L.wc_p2p_comm_connect.argtypes = [P, P]
+        for f in ("wc_comm_unique_id", "wc_comm_init", "wc_comm_destroy", "wildcat_forward_nshard",
+                  "wc_p2p_comm_create", "wc_p2p_comm_connect"):
             getattr(L, f).restype = ctypes.c_int
         L.wc_kv_capacity.argtypes = [S, ctypes.c_int32, ctypes.c_int32]
         L.wc_kv_capacity.restype = ctypes.c_size_t
@@ -207,6 +210,19 @@ def wc_comm_init(uid: bytes, world: int, rank: int) -> ctypes.c_void_p:
     buf = ctypes.create_string_buffer(uid, 128)
     _check(lib().wc_comm_init(ctypes.byref(h), buf, int(world), int(rank)), "wc_comm_init")
     return h
+
+
+def wc_p2p_comm_create(world: int, rank: int, capacity: int):
+    """Device-initiated (peer-memory) transport: returns (handle, this rank's 64-byte IPC handle)."""
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().wc_p2p_comm_create(ctypes.byref(h), int(world), int(rank), int(capacity), buf), "wc_p2p_comm_create")
+    return h, buf.raw
+
+
+def wc_p2p_comm_connect(h, handles: list) -> None:
+    blob = ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
+    _check(lib().wc_p2p_comm_connect(h, blob), "wc_p2p_comm_connect")
 
 
 def wc_comm_destroy(h) -> None:

@@ -546,6 +546,13 @@ int wc_comm_init(void **comm, const void *id128, int world, int rank) {
 
 int wc_comm_destroy(void *comm) { return wc::ns_comm_destroy(comm); }
 
+int wc_p2p_comm_create(void **comm, int world, int rank, size_t capacity, void *handle64) {
+    if (!comm || !handle64) return WC_EINVAL;
+    return wc::ns_p2p_create(comm, world, rank, capacity, handle64);
+}
+
+int wc_p2p_comm_connect(void *comm, const void *handles) { return wc::ns_p2p_connect(comm, handles); }
+
 int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int64_t n_offset, const wc_opts *o,
                            const void *Q, const void *K, const void *V, void *O, int32_t *S, int32_t *r_eff,
                            void *ws, size_t ws_bytes, void *stream) {

@@ -131,6 +131,8 @@ int ns_forward(void *comm, const Dims &D, int64_t n_global, int64_t n_off, const
 int ns_comm_unique_id(void *id128);
 int ns_comm_init(void **out, const void *id128, int world, int rank);
 int ns_comm_destroy(void *comm);
+int ns_p2p_create(void **out, int world, int rank, size_t cap, void *handle64);
+int ns_p2p_connect(void *comm, const void *handles);
 int ns_comm_world(void *comm);
 
 }  // namespace wc

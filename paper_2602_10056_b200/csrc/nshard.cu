@@ -13,6 +13,17 @@
 // Prologue: allreduce of column sums (kbar), of max ||q||^2 / value range, then of max rk^2.
 // Weights: per-rank partial Y~ over local keys, allreduce(sum) of Y~, replicated r x r solve.
 // Attend: local queries against the replicated coreset.
+//
+// Transport: NCCL, or device-initiated peer-memory exchange ("p2p").  In p2p
+// mode every rank owns a mailbox [2 parities][world slots][cap] doubles + flags [2][world] in its
+// own HBM, CUDA-IPC-mapped into every peer; an exchange is one single-CTA kernel that stores the
+// rank's vector straight into slot `rank` of every peer's mailbox (NVLink P2P stores), fences at
+// system scope and releases a flag = epoch per peer, and one single-CTA kernel that acquires the
+// world flags of its own mailbox and reduces the slots in rank order (sum / max / gather) -- the
+// same result on every rank, with no host round trip and no NCCL call per round.  Epochs are
+// host-counted per exchange (all ranks run the same sequence); the parity double buffer is enough
+// because a rank can only post exchange e+1 after every rank has posted e, i.e. finished e-1.
+// Spins are bounded (globaltimer, 20 s) and trap instead of hanging the GPU.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -55,10 +66,88 @@ const NcclApi &nccl() {
     return api;
 }
 
-struct Comm {
-    ncclComm_t comm;
-    int world, rank;
+constexpr int kP2PMaxWorld = 8;
+
+struct PeerPtrs {
+    double *mbox[kP2PMaxWorld];
+    unsigned long long *flags[kP2PMaxWorld];
 };
+
+struct Comm {
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+    int p2p = 0;                          // 1: device-initiated peer-memory transport
+    size_t cap = 0;                       // doubles per mailbox slot
+    char *base = nullptr;                 // local mailbox allocation (cudaMalloc, IPC-exported)
+    PeerPtrs peers{};                     // mapped mailboxes of every rank (own rank: local)
+    char *opened[kP2PMaxWorld] = {};      // IPC-opened peer bases (to close)
+    unsigned long long epoch = 0;         // exchanges issued
+};
+
+size_t p2p_bytes(int world, size_t cap) {
+    return ((2 * (size_t)world * cap * sizeof(double) + 255) & ~size_t(255)) + 2 * (size_t)world * 8;
+}
+void p2p_set_peer(Comm *c, int q, char *b) {
+    c->peers.mbox[q] = reinterpret_cast<double *>(b);
+    c->peers.flags[q] = reinterpret_cast<unsigned long long *>(
+        b + ((2 * (size_t)c->world * c->cap * sizeof(double) + 255) & ~size_t(255)));
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtime_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Store src[0:count] into slot `rank` (parity `par`) of every rank's mailbox, then release the flags.
+__global__ void __launch_bounds__(256) p2p_post(PeerPtrs pp, int world, int rank, size_t cap, const double *src,
+                                                int count, int par, unsigned long long epoch) {
+    for (int q = 0; q < world; ++q) {
+        double *dst = pp.mbox[q] + ((size_t)par * world + rank) * cap;
+        for (int e = threadIdx.x; e < count; e += blockDim.x) dst[e] = src[e];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < world) st_release_sys(pp.flags[threadIdx.x] + (size_t)par * world + rank, epoch);
+}
+
+// Acquire the world flags of the local mailbox (parity `par`), then reduce the slots in rank order:
+// op 0 = sum, 1 = max, 2 = gather (dst[q * count + e] = slot_q[e]).
+__global__ void __launch_bounds__(256) p2p_reduce(const double *mbox, const unsigned long long *flags, int world,
+                                                  size_t cap, int count, int par, unsigned long long epoch, int op,
+                                                  double *dst) {
+    if (threadIdx.x < world) {
+        const unsigned long long *f = flags + (size_t)par * world + threadIdx.x;
+        const unsigned long long t0 = gtime_ns();
+        while (ld_acquire_sys(f) < epoch) {
+            if (gtime_ns() - t0 > 20000000000ull) __trap();  // a peer never posted: fail, do not hang
+            __nanosleep(200);
+        }
+    }
+    __syncthreads();
+    __threadfence_system();
+    const double *slot = mbox + (size_t)par * world * cap;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        if (op == 2) {
+            for (int q = 0; q < world; ++q) dst[(size_t)q * count + e] = __ldcv(slot + (size_t)q * cap + e);
+        } else {
+            double v = __ldcv(slot + e);
+            for (int q = 1; q < world; ++q) {
+                const double x = __ldcv(slot + (size_t)q * cap + e);
+                v = op == 0 ? v + x : fmax(v, x);
+            }
+            dst[e] = v;
+        }
+    }
+}
 
 constexpr int kNsChunk = 2048;  // keys per chunk (one CTA of ns_update, one chunk total)
 constexpr int kNsT = 256;
@@ -437,9 +526,24 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     const int r = Dm.r;
     const bool want_q = rq < 0.0 && Dm.m > 0 && Q != nullptr;
     int launches = 0;
+    // one collective on either transport: op 0 = sum, 1 = max, 2 = allgather of `count` per rank
+    auto coll = [&](const double *src, double *dst, size_t count, int op) -> int {
+        if (!cm->p2p) {
+            if (op == 2) return nccl_status(api.allGather(src, dst, count, ncclFloat64, cm->comm, st));
+            return nccl_status(api.allReduce(src, dst, count, ncclFloat64, op == 0 ? ncclSum : ncclMax, cm->comm, st));
+        }
+        if (count > cm->cap) return WC_EUNSUPPORTED;
+        const unsigned long long ep = ++cm->epoch;
+        const int par = (int)(ep & 1);
+        p2p_post<<<1, 256, 0, st>>>(cm->peers, cm->world, cm->rank, cm->cap, src, (int)count, par, ep);
+        p2p_reduce<<<1, 256, 0, st>>>(cm->peers.mbox[cm->rank], cm->peers.flags[cm->rank], cm->world, cm->cap,
+                                      (int)count, par, ep, op, dst);
+        launches += 2;
+        return cudaPeekAtLastError() == cudaSuccess ? WC_OK : WC_ECUDA;
+    };
 #define WC_NCCL(x)                                  \
     do {                                            \
-        const int rc_ = nccl_status(x);             \
+        const int rc_ = (x);                        \
         if (rc_) return rc_;                        \
     } while (0)
     // ---- A0 prologue with cross-rank reductions
@@ -447,13 +551,13 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     if (cudaMemsetAsync(w.L, 0, sizeof(double) * r * r, st) != cudaSuccess) return WC_ECUDA;
     if (launch_prologue_pass1(Dm, Q, K, V, want_q, w.pp, st) < 0) return WC_ECUDA;
     ns_pro_reduce1<<<1, 128, 0, st>>>(D, w.pp.P, w.pp.colsum, w.pp.vmin, w.pp.vmax, w.pp.rq2, w.sumbuf, w.maxbuf);
-    WC_NCCL(api.allReduce(w.sumbuf, w.sumbuf, D, ncclFloat64, ncclSum, cm->comm, st));
-    WC_NCCL(api.allReduce(w.maxbuf, w.maxbuf, 1 + 2 * D, ncclFloat64, ncclMax, cm->comm, st));
+    WC_NCCL(coll(w.sumbuf, w.sumbuf, D, 0));
+    WC_NCCL(coll(w.maxbuf, w.maxbuf, 1 + 2 * D, 1));
     ns_pro_final1<T><<<1, 128, 0, st>>>(n_global, D, w.sumbuf, w.maxbuf, w.stats, static_cast<T *>(w.vmin),
                                         static_cast<T *>(w.vmax));
     if (launch_prologue_pass2(Dm, K, w.pp, w.stats, w.nrm2, st) < 0) return WC_ECUDA;
     ns_pro_reduce2<<<1, 32, 0, st>>>(w.pp.P, w.pp.rk2, w.rkbuf);
-    WC_NCCL(api.allReduce(w.rkbuf, w.rkbuf, 1, ncclFloat64, ncclMax, cm->comm, st));
+    WC_NCCL(coll(w.rkbuf, w.rkbuf, 1, 1));
     ns_tau<<<1, 32, 0, st>>>(n_global, r, w.rkbuf, w.maxbuf, want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, w.stats,
                              w.ctl);
     ns_init<<<nch, kNsT, 0, st>>>(n, w.nrm2, w.stats, w.p, w.ctot);
@@ -464,10 +568,10 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
     for (int i = 0; i < r; ++i) {
         ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot);
-        WC_NCCL(api.allGather(w.sendtot, w.ranktot, 1, ncclFloat64, cm->comm, st));
+        WC_NCCL(coll(w.sendtot, w.ranktot, 1, 2));
         ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, w.ranktot, w.ctot, w.p,
                                            static_cast<const T *>(K), w.F, w.packet, w.ctl);
-        WC_NCCL(api.allReduce(w.packet, w.packet, 2 + D + r, ncclFloat64, ncclSum, cm->comm, st));
+        WC_NCCL(coll(w.packet, w.packet, 2 + D + r, 0));
         upd<<<nch, kNuT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,
                                     w.S, w.L, static_cast<T *>(w.KS), w.ctl);
         launches += 3;
@@ -475,7 +579,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     ns_finish<<<1, 32, 0, st>>>(w.ctl, w.reff, w.stats);
     // ---- A3 + A4: local partial Y~, allreduce, replicated solve
     if (launch_weights_partial_ks(Dm, K, V, w.KS, w.reff, w.stats, w.Ypart, w.Yfull, st) < 0) return WC_ECUDA;
-    WC_NCCL(api.allReduce(w.Yfull, w.Yfull, (size_t)r * (D + 1), ncclFloat64, ncclSum, cm->comm, st));
+    WC_NCCL(coll(w.Yfull, w.Yfull, (size_t)r * (D + 1), 0));
     if (launch_weights_solve(Dm, w.Yfull, w.L, w.reff, w.X, w.Dinv, st) < 0) return WC_ECUDA;
     // ---- A5: local queries
     const int clip = (o->flags & WC_NO_CLIP) ? 0 : 1;
@@ -527,7 +631,9 @@ int ns_comm_init(void **out, const void *id128, int world, int rank) {
     if (!api.ok) return WC_EUNSUPPORTED;
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
-    Comm *c = new Comm{nullptr, world, rank};
+    Comm *c = new Comm;
+    c->world = world;
+    c->rank = rank;
     if (api.commInitRank(&c->comm, world, id, rank) != ncclSuccess) {
         delete c;
         return WC_ENCCL;
@@ -536,11 +642,61 @@ int ns_comm_init(void **out, const void *id128, int world, int rank) {
     return WC_OK;
 }
 
+int ns_p2p_create(void **out, int world, int rank, size_t cap, void *handle64) {
+    if (world < 1 || world > kP2PMaxWorld || rank < 0 || rank >= world || cap < 1) return WC_EINVAL;
+    Comm *c = new Comm;
+    c->world = world;
+    c->rank = rank;
+    c->p2p = 1;
+    c->cap = cap;
+    const size_t bytes = p2p_bytes(world, cap);
+    if (cudaMalloc(&c->base, bytes) != cudaSuccess || cudaMemset(c->base, 0, bytes) != cudaSuccess) {
+        delete c;
+        return WC_ECUDA;
+    }
+    p2p_set_peer(c, rank, c->base);
+    std::memset(handle64, 0, 64);
+    if (world > 1) {
+        cudaIpcMemHandle_t h;
+        static_assert(sizeof(h) == 64, "IPC handle size");
+        if (cudaIpcGetMemHandle(&h, c->base) != cudaSuccess) {
+            cudaFree(c->base);
+            delete c;
+            return WC_ECUDA;
+        }
+        std::memcpy(handle64, &h, 64);
+    }
+    *out = c;
+    return WC_OK;
+}
+
+int ns_p2p_connect(void *comm, const void *handles) {
+    Comm *c = static_cast<Comm *>(comm);
+    if (!c || !c->p2p || !handles) return WC_EINVAL;
+    for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char *>(handles) + 64 * (size_t)q, 64);
+        void *ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return WC_ECUDA;
+        c->opened[q] = static_cast<char *>(ptr);
+        p2p_set_peer(c, q, c->opened[q]);
+    }
+    return WC_OK;
+}
+
 int ns_comm_destroy(void *comm) {
     if (!comm) return WC_OK;
     Comm *c = static_cast<Comm *>(comm);
-    const NcclApi &api = nccl();
-    if (api.ok && c->comm) api.commDestroy(c->comm);
+    if (c->p2p) {
+        cudaDeviceSynchronize();
+        for (int q = 0; q < kP2PMaxWorld; ++q)
+            if (c->opened[q]) cudaIpcCloseMemHandle(c->opened[q]);
+        if (c->base) cudaFree(c->base);
+    } else {
+        const NcclApi &api = nccl();
+        if (api.ok && c->comm) api.commDestroy(c->comm);
+    }
     delete c;
     return WC_OK;
 }
