@@ -338,6 +338,8 @@ def main():
                     help="replicas: each rank runs the workload on its own units (weak scaling); "
                          "nshard: one sequence's keys sharded over the ranks (strong scaling). "
                          "Default: nshard for the long* configs, replicas otherwise")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="nshard mode: NCCL collectives, or device-initiated peer-memory mailboxes (8(f)-3)")
     ap.add_argument("--r", type=int, default=None, help="override the config's coreset size r")
     ap.add_argument("--n", type=int, default=None, help="override the config's n (= m)")
     ap.add_argument("--block", type=int, default=16,
@@ -391,7 +393,7 @@ def main():
         Q, K, V, koff = make_long_shard(cfg, world, rank)
         Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
         seed = cfg.seed
-        comm = wc.NshardComm.create()
+        comm = wc.NshardComm.create(transport=args.transport, capacity=cfg.r * (cfg.d + 1) + 64)
 
         Obuf = torch.empty_like(Qd)
 
@@ -632,7 +634,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": cfg.name, "units_per_gpu": units, "n": cfg.n, "m": cfg.m, "d": cfg.d,
                        "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
-                       "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}"),
+                       "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}-{args.transport}"),
                        "select": "blocked" if args.block >= 2 else "sequential", "block": args.block,
                        "bins": args.bins,
                        "l2": f"flushed ({args.flush_mb} MB write) before each step"},

@@ -159,6 +159,47 @@ struct Ctl {  // device-side loop state
     double theta;
 };
 
+// Per-round exchanges fused into the round kernels (p2p transport): the producer kernel stores its
+// vector into every peer's mailbox and releases the flags; the consumer kernel acquires them.
+struct P2PRound {
+    int on, world, rank;
+    size_t cap;
+    PeerPtrs pp;
+    unsigned long long ep;  // epoch of this exchange (parity = ep & 1)
+};
+// all threads of the block: post src[0:count] (already written, visible after __syncthreads)
+__device__ __forceinline__ void p2p_post_block(const P2PRound &a, const double *src, int count) {
+    const int par = (int)(a.ep & 1);
+    for (int q = 0; q < a.world; ++q) {
+        double *dst = a.pp.mbox[q] + ((size_t)par * a.world + a.rank) * a.cap;
+        for (int e = threadIdx.x; e < count; e += blockDim.x) dst[e] = src[e];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if ((int)threadIdx.x < a.world) st_release_sys(a.pp.flags[threadIdx.x] + (size_t)par * a.world + a.rank, a.ep);
+}
+// all threads of the block: wait until every rank posted exchange a.ep into the local mailbox
+__device__ __forceinline__ void p2p_wait_block(const P2PRound &a) {
+    const int par = (int)(a.ep & 1);
+    if ((int)threadIdx.x < a.world) {
+        const unsigned long long *f = a.pp.flags[a.rank] + (size_t)par * a.world + threadIdx.x;
+        const unsigned long long t0 = gtime_ns();
+        while (ld_acquire_sys(f) < a.ep) {
+            if (gtime_ns() - t0 > 20000000000ull) __trap();
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    __threadfence_system();
+}
+// element e of the rank-ordered sum of the posted vectors (after p2p_wait_block)
+__device__ __forceinline__ double p2p_sum(const P2PRound &a, int e) {
+    const double *slot = a.pp.mbox[a.rank] + (size_t)(a.ep & 1) * a.world * a.cap;
+    double v = __ldcv(slot + e);
+    for (int q = 1; q < a.world; ++q) v += __ldcv(slot + (size_t)q * a.cap + e);
+    return v;
+}
+
 // ------------------------------------------------------------------ prologue reductions
 __global__ void ns_pro_reduce1(int d, int P, const double *colsum, const float *vmin, const float *vmax,
                                const double *rq2, double *sumbuf, double *maxbuf) {
@@ -242,25 +283,40 @@ __global__ void __launch_bounds__(kNsT) ns_init(int64_t n, const double *nrm2, c
     if (threadIdx.x == 0) ctot[blockIdx.x] = loc;
 }
 
-__global__ void ns_local_total(int nchunks, const double *ctot, const Ctl *ctl, double *sendtot) {
-    if (threadIdx.x != 0) return;
-    double t = 0.0;
-    for (int c = 0; c < nchunks; ++c) t += ctot[c];
-    sendtot[0] = ctl->done ? 0.0 : t;
+__global__ void ns_local_total(int nchunks, const double *ctot, const Ctl *ctl, double *sendtot, P2PRound px) {
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int c = 0; c < nchunks; ++c) t += ctot[c];
+        sendtot[0] = ctl->done ? 0.0 : t;
+    }
+    __syncthreads();
+    if (px.on) p2p_post_block(px, sendtot, 1);  // this rank's total -> slot `rank` of every mailbox
 }
+
+template <typename T, int D>
+__device__ __forceinline__ void ns_pick_owner(int i, int64_t n, int64_t n_off, int nchunks, const double *ctot,
+                                              const double *p, const T *K, const double *F, double *packet,
+                                              double *scr, int &sh_c, int &sh_s, int &sh_last, double &sh_t,
+                                              double &sh_t2);
 
 // Global pivot draw; the owner rank writes the pivot packet {s, p_s, k_s[d], F[0:i, s]}.
 template <typename T, int D>
 __global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int rank, int64_t n, int64_t n_off,
                                                 int nchunks, uint64_t seed, const double *ranktot,
                                                 const double *ctot, const double *p, const T *K, const double *F,
-                                                double *packet, Ctl *ctl) {
+                                                double *packet, Ctl *ctl, P2PRound pw, P2PRound px) {
     __shared__ double scr[40];
     __shared__ int sh_owner, sh_c, sh_s, sh_last, sh_done;
     __shared__ double sh_t, sh_t2;
     const int tid = threadIdx.x;
     const int plen = 2 + D + r;
+    if (pw.on) {  // the rank totals of this round, gathered from the local mailbox
+        p2p_wait_block(pw);
+        if (tid < world) const_cast<double *>(ranktot)[tid] =
+            __ldcv(pw.pp.mbox[pw.rank] + ((size_t)(pw.ep & 1) * world + tid) * pw.cap);
+    }
     for (int j = tid; j < plen; j += kNsT) packet[j] = 0.0;
+    __syncthreads();
     if (tid == 0) {
         sh_done = ctl->done;
         sh_owner = -1;
@@ -293,8 +349,21 @@ __global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int ran
         }
     }
     __syncthreads();
-    if (sh_done || sh_owner != rank) return;
-    // owner: chunk by the local chunk totals (fixed order), then key inside the chunk
+    if (!(sh_done || sh_owner != rank)) ns_pick_owner<T, D>(i, n, n_off, nchunks, ctot, p, K, F, packet, scr, sh_c,
+                                                            sh_s, sh_last, sh_t, sh_t2);
+    if (px.on) {  // every rank posts its packet (non-owners: zeros); consumers sum in rank order
+        __syncthreads();
+        p2p_post_block(px, packet, plen);
+    }
+}
+
+// owner rank of ns_pick: chunk by the local chunk totals (fixed order), then key inside the chunk
+template <typename T, int D>
+__device__ __forceinline__ void ns_pick_owner(int i, int64_t n, int64_t n_off, int nchunks, const double *ctot,
+                                              const double *p, const T *K, const double *F, double *packet,
+                                              double *scr, int &sh_c, int &sh_s, int &sh_last, double &sh_t,
+                                              double &sh_t2) {
+    const int tid = threadIdx.x;
     if (tid == 0) {
         double acc = 0.0, excl = 0.0, last_excl = 0.0;
         int cs = -1, last = -1;
@@ -347,7 +416,8 @@ constexpr int kNuT = 512, kNuW = kNuT / 32, kNuST = 256, kNuTK = kNuST / 32;
 template <typename T, int D>
 __global__ void __launch_bounds__(kNuT) ns_update(int i, int r, int64_t n, int64_t n_off, const T *K,
                                                   const double *stats, const double *packet, double *F, double *p,
-                                                  double *ctot, int32_t *S, double *L, T *KS, const Ctl *ctl) {
+                                                  double *ctot, int32_t *S, double *L, T *KS, const Ctl *ctl,
+                                                  P2PRound pw) {
     extern __shared__ double nsm[];
     double *kcs = nsm;               // [D]
     double *fs = kcs + D;            // [r]
@@ -358,18 +428,21 @@ __global__ void __launch_bounds__(kNuT) ns_update(int i, int r, int64_t n, int64
     if (ctl->done) return;
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
     const double g = stats[1], mstar = stats[2];
-    const int64_t s_glob = (int64_t)packet[0];
-    const double ps = packet[1];
+    // the pivot packet: the NCCL-reduced buffer, or (p2p) the rank-ordered sum of the posted packets
+    if (pw.on) p2p_wait_block(pw);
+    auto pk = [&](int e) { return pw.on ? p2p_sum(pw, e) : packet[e]; };
+    const int64_t s_glob = (int64_t)pk(0);
+    const double ps = pk(1);
     for (int j = tid; j < D; j += kNuT) {
         kb[j] = stats[kStatsHead + j];
-        kcs[j] = __dadd_rn(packet[2 + j], -stats[kStatsHead + j]);
+        kcs[j] = __dadd_rn(pk(2 + j), -stats[kStatsHead + j]);
     }
-    for (int j = tid; j < i; j += kNuT) fs[j] = packet[2 + D + j];
+    for (int j = tid; j < i; j += kNuT) fs[j] = pk(2 + D + j);
     __syncthreads();
     const double rs = sqrt(ps);
     if (blockIdx.x == 0) {  // replicated outputs: S, L row i (L[i][i] = sqrt(p_s) = F[i, s] exactly), K_S row i
         for (int j = tid; j < i; j += kNuT) L[(int64_t)i * r + j] = fs[j];
-        for (int j = tid; j < D; j += kNuT) KS[(int64_t)i * D + j] = from_f32<T>((float)packet[2 + j]);
+        for (int j = tid; j < D; j += kNuT) KS[(int64_t)i * D + j] = from_f32<T>((float)pk(2 + j));
         if (tid == 0) {
             S[i] = (int32_t)s_glob;
             L[(int64_t)i * r + i] = rs;
@@ -566,14 +639,22 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     const size_t usm = (size_t)(2 * D + r + kNuW * kNuST + 2 * kNuST + 40) * sizeof(double);
     auto upd = ns_update<T, D>;
     cudaFuncSetAttribute(upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+    // p2p: the two per-round exchanges are fused into the round kernels (no extra launches)
+    P2PRound off{};
+    if (cm->p2p && (size_t)(2 + D + r) > cm->cap) return WC_EUNSUPPORTED;
     for (int i = 0; i < r; ++i) {
-        ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot);
-        WC_NCCL(coll(w.sendtot, w.ranktot, 1, 2));
+        P2PRound ptot = off, ppk = off;
+        if (cm->p2p) {
+            ptot = P2PRound{1, cm->world, cm->rank, cm->cap, cm->peers, ++cm->epoch};
+            ppk = P2PRound{1, cm->world, cm->rank, cm->cap, cm->peers, ++cm->epoch};
+        }
+        ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot, ptot);
+        if (!cm->p2p) WC_NCCL(coll(w.sendtot, w.ranktot, 1, 2));
         ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, w.ranktot, w.ctot, w.p,
-                                           static_cast<const T *>(K), w.F, w.packet, w.ctl);
-        WC_NCCL(coll(w.packet, w.packet, 2 + D + r, 0));
+                                           static_cast<const T *>(K), w.F, w.packet, w.ctl, ptot, ppk);
+        if (!cm->p2p) WC_NCCL(coll(w.packet, w.packet, 2 + D + r, 0));
         upd<<<nch, kNuT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,
-                                    w.S, w.L, static_cast<T *>(w.KS), w.ctl);
+                                    w.S, w.L, static_cast<T *>(w.KS), w.ctl, ppk);
         launches += 3;
     }
     ns_finish<<<1, 32, 0, st>>>(w.ctl, w.reff, w.stats);
