@@ -163,9 +163,49 @@ template <int D, int RP> struct TcSmem {
     // + w (fp32), vmin/vmax (bf16), row exchange (2 x 128 fp32), mbarrier, TMEM base; no static smem,
     // so the dynamic segment starts at shared offset 0 (1024-aligned, checked at run time)
     static constexpr int kOffW = kBytes, kOffV = kOffW + RP * 4, kOffXch = kOffV + 2 * D * 2;
-    static constexpr int kOffBar = kOffXch + 2 * 128 * 4, kOffTb = kOffBar + 8;
-    static constexpr int kTotal = kOffTb + 8;
+    static constexpr int kOffBar = kOffXch + 2 * 128 * 4, kOffTb = kOffBar + 8, kOffBarI = kOffTb + 8;
+    static constexpr int kTotal = kOffBarI + 8;
+    // per-unit staging image in global memory (attend_img_prep_kernel): [K_S | X_hi^T | X_lo^T] in
+    // the shared-memory layout from kOffK on (one bulk copy), then w (fp32)
+    static constexpr int kImgKX = kOffP - kOffK;
+    static constexpr int kImgStride = (kImgKX + RP * 4 + 1023) & ~1023;
 };
+
+// Per unit: the swizzled K_S / X_hi^T / X_lo^T operand image and w, built once for all CTAs (each
+// CTA then stages a unit with one bulk copy instead of re-converting X from fp32).
+template <int D, int RP>
+__global__ void __launch_bounds__(256) attend_img_prep_kernel(const __nv_bfloat16 *__restrict__ KS,
+                                                              const float *__restrict__ X,
+                                                              const int32_t *__restrict__ r_eff, int r,
+                                                              unsigned char *__restrict__ img) {
+    using L = TcSmem<D, RP>;
+    constexpr int DC = D + 1, CPR = D / 8;
+    const int u = blockIdx.y, re = r_eff[u];
+    unsigned char *dst = img + (int64_t)u * L::kImgStride;
+    const int nth = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int e = t0; e < RP * CPR; e += nth) {
+        const int row = e / CPR, cc = e % CPR;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < re) v = __ldg(reinterpret_cast<const uint4 *>(KS + ((int64_t)u * r + row) * D) + cc);
+        *reinterpret_cast<uint4 *>(dst + umma::sw128_offset(row, cc * 8, RP)) = v;
+    }
+    // X read row-major (coalesced), written transposed into the swizzled images; column D is w
+    float *wd = reinterpret_cast<float *>(dst + L::kImgKX);
+    const float *Xu = X + (int64_t)u * r * DC;
+    for (int e = t0; e < RP * DC; e += nth) {
+        const int s2 = e / DC, c = e % DC;
+        const float x = (s2 < re) ? __ldg(Xu + e) : 0.f;
+        if (c == D) {
+            wd[s2] = x;
+            continue;
+        }
+        const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+        *reinterpret_cast<__nv_bfloat16 *>(dst + (L::kOffXh - L::kOffK) + umma::sw128_offset(c, s2, D)) = xh;
+        if (L::kSplitX)
+            *reinterpret_cast<__nv_bfloat16 *>(dst + (L::kOffXl - L::kOffK) + umma::sw128_offset(c, s2, D)) =
+                __float2bfloat16_rn(x - __bfloat162float(xh));
+    }
+}
 
 template <int D, int RP>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -173,7 +213,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      const float *__restrict__ X, const int32_t *__restrict__ r_eff,
                      const __nv_bfloat16 *__restrict__ vmin, const __nv_bfloat16 *__restrict__ vmax, int64_t m,
                      int r, int group, int hq, int hkv, float beta, int clip, __nv_bfloat16 *__restrict__ O,
-                     int64_t tiles_per_head, int64_t total_tiles, unsigned long long *atrace) {
+                     int64_t tiles_per_head, int64_t total_tiles, const unsigned char *__restrict__ img,
+                     unsigned long long *atrace) {
     using L = TcSmem<D, RP>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw;  // offset 0 of the CTA's shared window: 1024-aligned
@@ -184,14 +225,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sm + L::kOffV), *sVmax = sVmin + D;
     float (*xch)[128] = reinterpret_cast<float (*)[128]>(sm + L::kOffXch);  // row exchange between halves
     uint64_t &bar = *reinterpret_cast<uint64_t *>(sm + L::kOffBar);
+    uint64_t &ibar = *reinterpret_cast<uint64_t *>(sm + L::kOffBarI);
     uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
     const int tid = threadIdx.x, w = tid >> 5;
     const int row = tid & 127, half = tid >> 7;  // TMEM lane (query row) and column half
     constexpr int DC = D + 1;
+    uint32_t iphase = 0;
 
     if (w == 0) umma::tmem_alloc(&tbase, 512);
     if (tid == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&ibar, 1);
         fence_mbar_init();
     }
     umma::fence_before_sync();
@@ -203,81 +247,80 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int cur_unit = -1, re = 0;
     const float bl2 = beta * 1.4426950408889634f;
 
-    // contiguous tile ranges per CTA: consecutive tiles share the unit, so K_S / X are staged rarely
+    // contiguous tile ranges per CTA: consecutive tiles share the unit, so K_S / X are staged rarely.
+    // Pipeline per tile t (one TMEM S accumulator, one O accumulator, one mbarrier, commits waited
+    // in issue order): GEMM1(t) -> softmax(t) -> GEMM2(t) [Q(t+1) loads in flight] -> Q(t+1) into
+    // sQ (free since GEMM1(t) retired) -> GEMM1(t+1) issued -> epilogue(t) from O while GEMM1(t+1)
+    // runs (S and O are disjoint TMEM columns; sP is next written by softmax(t+1), after GEMM2(t)).
     const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
     const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
-    for (int64_t tile = t_begin; tile < t_end; ++tile) {
-        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8] = gtimer_a();
-        const int64_t head = tile / tiles_per_head;  // b * hq + h
-        const int64_t q0 = (tile % tiles_per_head) * 128;
-        const int b = (int)(head / hq), h = (int)(head % hq);
-        const int u = b * hkv + h / group;
+    constexpr int CPR = D / 8;                   // 16-byte chunks per row
+    constexpr int NQ = 128 * CPR / kTcThreads;   // Q chunks per thread
+    auto unit_of = [&](int64_t tile) {
+        const int64_t head = tile / tiles_per_head;
+        return (int)(head / hq) * hkv + (int)(head % hq) / group;
+    };
+    auto load_q = [&](int64_t tile, uint4 (&qv)[NQ]) {
+        const int64_t head = tile / tiles_per_head, q0 = (tile % tiles_per_head) * 128;
         const __nv_bfloat16 *Qh = Q + head * m * D;
-        // ---- stage operands in shared memory (16-byte chunks -> 128B-swizzled K-major layout)
-        constexpr int CPR = D / 8;  // 16-byte chunks per row
-        {
-            constexpr int NQ = 128 * CPR / kTcThreads;  // chunks per thread, all loads in flight
-            uint4 qv[NQ];
 #pragma unroll
-            for (int k = 0; k < NQ; ++k) {
-                const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
-                qv[k] = (q0 + row < m) ? __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc)
-                                       : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int k = 0; k < NQ; ++k) {
-                const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
-                *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = qv[k];
-            }
+        for (int k = 0; k < NQ; ++k) {
+            const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+            qv[k] = (q0 + row < m) ? __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc)
+                                   : make_uint4(0, 0, 0, 0);
         }
-        if (u != cur_unit) {
-            re = r_eff[u];
-            const float *Xu = X + (int64_t)u * r * DC;
-            // X^T split into bf16 hi + lo; batches of 8 independent loads per thread in flight
-            static_assert((D * RP) % (8 * kTcThreads) == 0, "X staging batch");
-            for (int e0 = tid; e0 < D * RP; e0 += 8 * kTcThreads) {
-                float xv[8];
+    };
+    auto store_q = [&](const uint4 (&qv)[NQ]) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int e = e0 + k * kTcThreads, c = e / RP, s = e % RP;
-                    xv[k] = (s < re) ? __ldg(Xu + (int64_t)s * DC + c) : 0.f;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int e = e0 + k * kTcThreads, c = e / RP, s = e % RP;
-                    const __nv_bfloat16 xh = __float2bfloat16_rn(xv[k]);
-                    const __nv_bfloat16 xl = __float2bfloat16_rn(xv[k] - __bfloat162float(xh));
-                    *reinterpret_cast<__nv_bfloat16 *>(sXh + umma::sw128_offset(c, s, D)) = xh;
-                    if (L::kSplitX) *reinterpret_cast<__nv_bfloat16 *>(sXl + umma::sw128_offset(c, s, D)) = xl;
-                }
-            }
-            for (int s = tid; s < RP; s += kTcThreads) sW[s] = (s < re) ? Xu[(int64_t)s * DC + D] : 0.f;
-            for (int c = tid; c < D; c += kTcThreads) {
-                sVmin[c] = vmin[(int64_t)u * D + c];
-                sVmax[c] = vmax[(int64_t)u * D + c];
-            }
+        for (int k = 0; k < NQ; ++k) {
+            const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+            *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = qv[k];
         }
-        if (u != cur_unit || L::kAliasP) {  // K_S (reloaded each tile when P aliases it)
-            const __nv_bfloat16 *KSu = KS + (int64_t)u * r * D;
-#pragma unroll 8
-            for (int e = tid; e < RP * CPR; e += kTcThreads) {
-                const int row = e / CPR, cc = e % CPR;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (row < re) v = __ldg(reinterpret_cast<const uint4 *>(KSu + (int64_t)row * D) + cc);
-                *reinterpret_cast<uint4 *>(sK + umma::sw128_offset(row, cc * 8, RP)) = v;
-            }
+    };
+    // K_S, X (hi / lo) of unit u: one bulk copy of its prepared image; w and the value range
+    auto stage_unit = [&](int u) {
+        re = r_eff[u];
+        const unsigned char *iu = img + (int64_t)u * L::kImgStride;
+        if (tid == 0) {
+            mbar_arrive_expect_tx(&ibar, (uint32_t)L::kImgKX);
+            bulk_g2s(sK, iu, (uint32_t)L::kImgKX, &ibar);
         }
+        const float *wu = reinterpret_cast<const float *>(iu + L::kImgKX);
+        for (int s2 = tid; s2 < RP; s2 += kTcThreads) sW[s2] = __ldg(wu + s2);
+        for (int c = tid; c < D; c += kTcThreads) {
+            sVmin[c] = vmin[(int64_t)u * D + c];
+            sVmax[c] = vmax[(int64_t)u * D + c];
+        }
+        mbar_wait(&ibar, iphase);
+        iphase ^= 1u;
         cur_unit = u;
+    };
+    auto sync_for_mma = [&]() {
         umma::fence_async_smem();
         umma::fence_before_sync();
         __syncthreads();
         umma::fence_after_sync();
-        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 1] = gtimer_a();
-        // ---- GEMM1: S = Q K_S^T
+    };
+    auto issue_gemm1 = [&]() {
         if (tid == 0) {
             umma::gemm_128xNxK(tS, smem_u32(sQ), smem_u32(sK), RP, D, false);
             umma::commit(&bar);
         }
+    };
+    if (t_begin < t_end) {
+        uint4 qv[NQ];
+        load_q(t_begin, qv);
+        store_q(qv);
+        stage_unit(unit_of(t_begin));
+        sync_for_mma();
+        issue_gemm1();
+    }
+    for (int64_t tile = t_begin; tile < t_end; ++tile) {
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64)
+            atrace[(tile - t_begin) * 8] = atrace[(tile - t_begin) * 8 + 1] = gtimer_a();
+        const int64_t head = tile / tiles_per_head;  // b * hq + h
+        const int64_t q0 = (tile % tiles_per_head) * 128;
+        // ---- S = Q K_S^T (issued at the end of the previous tile, or above)
         mbar_wait(&bar, phase);
         phase ^= 1u;
         umma::fence_after_sync();
@@ -320,21 +363,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncthreads();  // xch reused
             xch[half][row] = dpart;
         }
-        umma::fence_async_smem();
-        umma::fence_before_sync();
-        __syncthreads();
-        umma::fence_after_sync();
+        sync_for_mma();
+        if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 3] = gtimer_a();
         const float den = xch[0][row] + xch[1][row];
-        // ---- GEMM2: O = P X_hi + P X_lo
+        // ---- O = P X_hi (+ P X_lo); the next tile's Q loads fly meanwhile
         if (tid == 0) {
             umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXh), D, RP, false);
             if (L::kSplitX) umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXl), D, RP, true);
             umma::commit(&bar);
         }
+        const bool has_next = tile + 1 < t_end;
+        const bool same_unit = has_next && unit_of(tile + 1) == cur_unit;
+        uint4 qv[NQ];
+        if (has_next) load_q(tile + 1, qv);
         mbar_wait(&bar, phase);
         phase ^= 1u;
         umma::fence_after_sync();
         if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 4] = gtimer_a();
+        if (same_unit) {  // S(t+1) overlaps this tile's output epilogue
+            store_q(qv);
+            sync_for_mma();
+            issue_gemm1();
+        }
         // ---- output epilogue: each thread finishes D/2 columns of its row
         {
             const int64_t qi = q0 + row;
@@ -364,8 +414,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
         umma::fence_before_sync();
-        __syncthreads();  // TMEM and smem free for the next tile
+        __syncthreads();  // O (TMEM) and the unit's smem free
         umma::fence_after_sync();
+        if (has_next && !same_unit) {  // new unit: restage K_S / X, then S(t+1)
+            store_q(qv);
+            stage_unit(unit_of(tile + 1));
+            sync_for_mma();
+            issue_gemm1();
+        }
         if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 5] = gtimer_a();
     }
     if (w == 0) umma::tmem_dealloc(tbase, 512);
@@ -373,8 +429,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 template <int D, int RP>
 int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                     const void *vmin, const void *vmax, double beta, int clip, void *O, cudaStream_t st) {
+                     const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
     using L = TcSmem<D, RP>;
+    if (!ws) return -1;
+    unsigned char *img = static_cast<unsigned char *>(ws);
+    attend_img_prep_kernel<D, RP><<<dim3(RP / 4, (unsigned)Dm.units()), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, img);
     auto kern = attend_tc_kernel<D, RP>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     const int64_t tph = ceil_div(Dm.m, 128);
@@ -392,7 +452,7 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
     kern<<<grid, kTcThreads, L::kTotal, st>>>(
         static_cast<const __nv_bfloat16 *>(Q), static_cast<const __nv_bfloat16 *>(KS), X, r_eff,
         static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(),
-        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total, atrace);
+        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total, img, atrace);
     if (atrace) {  // debug: phase durations of CTA 0's tiles (ns)
         unsigned long long h[64 * 8];
         cudaStreamSynchronize(st);
@@ -409,7 +469,7 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
             std::fprintf(stderr, "[atrace] tiles=%d stage=%.0f gemm1=%.0f softmax=%.0f gemm2=%.0f epi=%.0f ns\n", cnt,
                          acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
     }
-    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 // =====================================================================================
@@ -737,8 +797,23 @@ static int attend_path(const Dims &D) {
     return D.r <= 256 ? 1 : 2;
 }
 
+static int attend_rp(const Dims &D) { return D.r <= 32 ? 32 : D.r <= 64 ? 64 : D.r <= 128 ? 128 : 256; }
+template <int D> static int img_stride(int rp) {
+    switch (rp) {
+        case 32: return TcSmem<D, 32>::kImgStride;
+        case 64: return TcSmem<D, 64>::kImgStride;
+        case 128: return TcSmem<D, 128>::kImgStride;
+        default: return TcSmem<D, 256>::kImgStride;
+    }
+}
+
 size_t attend_ws_bytes(const Dims &D) {
     if (attend_path(D) == 3) return attend_decode_ws_bytes(D);
+    if (attend_path(D) == 1) {
+        const int rp = attend_rp(D);
+        const int stride = D.d == 64 ? img_stride<64>(rp) : img_stride<128>(rp);
+        return (size_t)D.units() * stride;
+    }
     if (attend_path(D) != 2) return 0;
     const size_t img = D.d == 64 ? TcLong<64>::kImg : TcLong<128>::kImg;
     return D.units() * (size_t)ceil_div(D.r, 128) * img;
@@ -753,20 +828,20 @@ int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, 
         return launch_attend_tc_long<128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
     }
     if (path == 1) {
-        const int rp = D.r <= 32 ? 32 : D.r <= 64 ? 64 : D.r <= 128 ? 128 : 256;
+        const int rp = attend_rp(D);
         if (D.d == 64) {
             switch (rp) {
-                case 32: return launch_attend_tc<64, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-                case 64: return launch_attend_tc<64, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-                case 128: return launch_attend_tc<64, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-                default: return launch_attend_tc<64, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+                case 32: return launch_attend_tc<64, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+                case 64: return launch_attend_tc<64, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+                case 128: return launch_attend_tc<64, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+                default: return launch_attend_tc<64, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
             }
         }
         switch (rp) {
-            case 32: return launch_attend_tc<128, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-            case 64: return launch_attend_tc<128, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-            case 128: return launch_attend_tc<128, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
-            default: return launch_attend_tc<128, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
+            case 32: return launch_attend_tc<128, 32>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+            case 64: return launch_attend_tc<128, 64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+            case 128: return launch_attend_tc<128, 128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+            default: return launch_attend_tc<128, 256>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
         }
     }
     if (D.dtype == 0) return launch_attend_t<float>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, st);
