@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restri
     for (int i = 0; i < kPB; ++i) Du[i * kPB + lane] = x[i];  // row-major inverse, lower triangular
 }
 
-// 8 RHS columns per CTA, 256 threads: thread t owns panel row t/8, column t%8.
 // The solve is a chain of steps: per panel P (kPB rows), CHUNK steps (acc -= L-block . z over kCBs
 // already-solved rows) and one DIAG step (z_P = Dinv_PP . acc); forward over P = 0.., then backward
 // (L^T) over P = npan-1..0.  No L or Dinv load depends on z, so the operands of the next kSolveNS-1
@@ -193,25 +192,28 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// kSolveC RHS columns per CTA (65 CTAs per unit at d = 128), 256 threads: thread t owns panel row
+// t / 8, column (t / 4) % 2 and a quarter of every dot (part t % 4, combined by two shuffles).
+constexpr int kSolveC = 2;
 template <int D>
 __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__restrict__ Y,
                                                             const double *__restrict__ L,
                                                             const double *__restrict__ Dinv,
                                                             const int32_t *__restrict__ r_eff, int r,
                                                             float *__restrict__ X) {
-    constexpr int DC = D + 1;
-    extern __shared__ double zs[];  // z[r][8], then the operand ring [kSolveNS][kSolveBuf]
-    __shared__ double tP[kPB][8];
+    constexpr int DC = D + 1, C = kSolveC;
+    extern __shared__ double zs[];  // z[r][C], then the operand ring [kSolveNS][kSolveBuf]
+    __shared__ double tP[kPB][C];
     __shared__ int steps[kSolveMaxSteps];
     __shared__ int nsteps;
     const int u = blockIdx.y, tid = threadIdx.x;
-    const int cbase = blockIdx.x * 8;
+    const int cbase = blockIdx.x * C;
     const int q = r_eff[u];
     const int nbl = (r + kPB - 1) / kPB;
     const double *Lu = L + (int64_t)u * r * r;
     const double *Du = Dinv + (int64_t)u * nbl * kPB * kPB;
     float *Xu = X + (int64_t)u * r * DC;
-    double *ring = zs + (size_t)r * 8;
+    double *ring = zs + (size_t)r * C;
     const int npan = (q + kPB - 1) / kPB;
     auto nch = [&](int dir, int P) {
         const int p0 = P * kPB, pe = min(p0 + kPB, q);
@@ -229,10 +231,9 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
         }
         nsteps = k;
     }
-#pragma unroll 8
-    for (int e = tid; e < q * 8; e += 256) {
-        const int a = e / 8, cc = e % 8, col = cbase + cc;
-        zs[a * 8 + cc] = col < DC ? __ldg(Y + ((int64_t)u * r + a) * DC + col) : 0.0;
+    for (int e = tid; e < q * C; e += 256) {
+        const int a = e / C, cc = e % C, col = cbase + cc;
+        zs[a * C + cc] = col < DC ? __ldg(Y + ((int64_t)u * r + a) * DC + col) : 0.0;
     }
     __syncthreads();
     const int ns = nsteps;
@@ -272,49 +273,56 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
     };
 #pragma unroll
     for (int k = 0; k < kSolveNS - 1; ++k) issue(k);
-    const int pr = tid / 8, pc = tid % 8;
-    double acc = 0.0;
+    const int pr = tid >> 3, pc = (tid >> 2) & 1, part = tid & 3;
+    double acc = 0.0;  // this thread's quarter of the panel row's running right-hand side
     bool panel_start = true;
     for (int k = 0; k < ns; ++k) {
         const int code = steps[k], dir = code >> 24, P = (code >> 12) & 0xfff, c = (code & 0xfff) - 1;
         const int p0 = P * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
         const double *buf = ring + (size_t)(k % kSolveNS) * kSolveBuf;
-        if (panel_start) acc = (pr < nb) ? zs[(p0 + pr) * 8 + pc] : 0.0;
+        if (panel_start) acc = (pr < nb && part == 0) ? zs[(p0 + pr) * C + pc] : 0.0;
         cp_async_wait<kSolveNS - 2>();  // this thread's copies of step k landed
-        if (c < 0) tP[pr][pc] = acc;
-        __syncthreads();                // everyone's copies (and tP) visible
+        if (c < 0) {                    // combine the four parts of the row's right-hand side
+            double t = acc;
+            t += __shfl_xor_sync(0xffffffffu, t, 1);
+            t += __shfl_xor_sync(0xffffffffu, t, 2);
+            if (part == 0) tP[pr][pc] = t;
+        }
+        __syncthreads();  // everyone's copies (and tP) visible
         if (c < 0) {
-            if (pr < nb) {  // Di is triangular with explicit zeros: full-length dot, two partial sums
-                double z0 = 0.0, z1 = 0.0;
-#pragma unroll 8
-                for (int j = 0; j < kPB; j += 2) {
-                    z0 = fma(buf[pr * (kPB + 1) + j], tP[j][pc], z0);
-                    z1 = fma(buf[pr * (kPB + 1) + j + 1], tP[j + 1][pc], z1);
-                }
-                zs[(p0 + pr) * 8 + pc] = z0 + z1;
+            // Di is triangular with explicit zeros: full-length dot, split over the four parts
+            double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+            for (int j = part; j < kPB; j += 8) {
+                z0 = fma(buf[pr * (kPB + 1) + j], tP[j][pc], z0);
+                z1 = fma(buf[pr * (kPB + 1) + j + 4], tP[j + 4][pc], z1);
             }
+            double z = z0 + z1;
+            z += __shfl_xor_sync(0xffffffffu, z, 1);
+            z += __shfl_xor_sync(0xffffffffu, z, 2);
+            if (pr < nb && part == 0) zs[(p0 + pr) * C + pc] = z;
         } else if (pr < nb) {
             const int b0 = dir == 0 ? c * kCBs : pe + c * kCBs;
             const int nbk = dir == 0 ? min(kCBs, p0 - b0) : min(kCBs, q - b0);
             const double *lr = buf + pr * (kCBs + 1);
-            double a4[4] = {0.0, 0.0, 0.0, 0.0};
-            int bb = 0;
+            double a0 = 0.0, a1 = 0.0;
+            int bb = part;
 #pragma unroll 4
-            for (; bb + 4 <= nbk; bb += 4) {
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) a4[kk] = fma(-lr[bb + kk], zs[(b0 + bb + kk) * 8 + pc], a4[kk]);
+            for (; bb + 4 < nbk; bb += 8) {
+                a0 = fma(-lr[bb], zs[(b0 + bb) * C + pc], a0);
+                a1 = fma(-lr[bb + 4], zs[(b0 + bb + 4) * C + pc], a1);
             }
-            for (; bb < nbk; ++bb) a4[0] = fma(-lr[bb], zs[(b0 + bb) * 8 + pc], a4[0]);
-            acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
+            if (bb < nbk) a0 = fma(-lr[bb], zs[(b0 + bb) * C + pc], a0);
+            acc += a0 + a1;
         }
         __syncthreads();  // stage k % NS and tP free; z of a DIAG step visible
         issue(k + kSolveNS - 1);
         panel_start = (c < 0);
     }
     cp_async_wait<0>();
-    for (int e = tid; e < r * 8; e += 256) {
-        const int a = e / 8, cc = e % 8, col = cbase + cc;
-        if (col < DC) Xu[(int64_t)a * DC + col] = a < q ? (float)zs[a * 8 + cc] : 0.f;
+    for (int e = tid; e < r * C; e += 256) {
+        const int a = e / C, cc = e % C, col = cbase + cc;
+        if (col < DC) Xu[(int64_t)a * DC + col] = a < q ? (float)zs[a * C + cc] : 0.f;
     }
 }
 
@@ -612,11 +620,11 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
                    double *Dinv, cudaStream_t st) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
     weights_dinv_kernel<<<dim3(nbl, Dm.units()), 32, 0, st>>>(L, r_eff, Dm.r, Dinv);
-    const size_t smem = ((size_t)8 * Dm.r + (size_t)kSolveNS * kSolveBuf) * sizeof(double);
+    const size_t smem = ((size_t)kSolveC * Dm.r + (size_t)kSolveNS * kSolveBuf) * sizeof(double);
     auto sk = weights_solve_kernel<D>;
     // z plus the operand ring is dynamic (up to ~197 KB at r = 1024): always raise the limit
     cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 g2((D + 1 + 7) / 8, Dm.units());
+    dim3 g2((D + 1 + kSolveC - 1) / kSolveC, Dm.units());
     sk<<<g2, 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
