@@ -84,7 +84,8 @@ def test_workspace_sizes_scale(L):
     s2 = _shape(n=2000, r=20)
     assert L.wc_workspace_bytes(ctypes.byref(s2), 0) > 3 * L.wc_workspace_bytes(ctypes.byref(s1), 0)
     big_m = _shape(n=1000, r=10, m=500)
-    assert L.wc_workspace_bytes(ctypes.byref(big_m), 2) == 0  # resident-coreset attend needs none
+    assert L.wc_workspace_bytes(ctypes.byref(big_m), 2) > 0  # tcgen05 attend: per-unit operand image
+    assert L.wc_workspace_bytes(ctypes.byref(_shape(n=1000, r=10, m=500, dtype=0)), 2) == 0  # fp32: none
     assert L.wc_workspace_bytes(ctypes.byref(_shape(n=1000, r=10, m=16)), 2) > 0  # decode kernel partials
 
 
