@@ -178,7 +178,6 @@ __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restri
 // steps are in flight (cp.async, zero-filled out of range, transposes done by the copy placement)
 // while the current step computes: the chain carries shared-memory latency only.
 constexpr int kSolveNS = 4;                              // operand ring stages
-constexpr int kSolveBuf = kPB * (kCBs + 1);              // doubles per stage (>= kPB * (kPB + 1))
 constexpr int kSolveMaxSteps = 2 * (1024 / kPB) * (1024 / kCBs + 1);
 
 // 8-byte async copy, zero-filled (no global read) when !ok; `safe` is any valid global address
@@ -192,17 +191,19 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// kSolveC RHS columns per CTA (65 CTAs per unit at d = 128), 256 threads: thread t owns panel row
-// t / 8, column (t / 4) % 2 and a quarter of every dot (part t % 4, combined by two shuffles).
-constexpr int kSolveC = 2;
-template <int D>
+// C RHS columns per CTA, 256 threads: thread t owns panel row t / 8, column (t / PARTS) % C and the
+// part t % PARTS of every dot (PARTS = 8 / C, combined by shuffles).  C = 2 (65 CTAs per unit at
+// d = 128) when there are few units, C = 8 when there are many (binned sub-units).  The operand ring
+// stage holds kPB rows of lb = min(kCBs, r) + 1 doubles (>= kPB + 1 for the Dinv blocks).
+template <int D, int C>
 __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__restrict__ Y,
                                                             const double *__restrict__ L,
                                                             const double *__restrict__ Dinv,
                                                             const int32_t *__restrict__ r_eff, int r,
                                                             float *__restrict__ X) {
-    constexpr int DC = D + 1, C = kSolveC;
-    extern __shared__ double zs[];  // z[r][C], then the operand ring [kSolveNS][kSolveBuf]
+    constexpr int DC = D + 1, PARTS = 8 / C;
+    const int lb = min(kCBs, r) + 1, sbuf = kPB * max(lb, kPB + 1);
+    extern __shared__ double zs[];  // z[r][C], then the operand ring [kSolveNS][sbuf]
     __shared__ double tP[kPB][C];
     __shared__ int steps[kSolveMaxSteps];
     __shared__ int nsteps;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
         if (k < ns) {
             const int code = steps[k], dir = code >> 24, P = (code >> 12) & 0xfff, c = (code & 0xfff) - 1;
             const int p0 = P * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
-            double *buf = ring + (size_t)(k % kSolveNS) * kSolveBuf;
+            double *buf = ring + (size_t)(k % kSolveNS) * sbuf;
             if (c < 0) {  // Di (forward: row-major lower; backward: transposed)
                 const double *src = Du + (int64_t)P * kPB * kPB;
 #pragma unroll
@@ -256,16 +257,16 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
 #pragma unroll
                 for (int kk = 0; kk < kPB * kCBs / 256; ++kk) {
                     const int e = tid + 256 * kk, rr = e / kCBs, c2 = e % kCBs;
-                    cp_async8_zfill(buf + rr * (kCBs + 1) + c2, Lu + (int64_t)(p0 + rr) * r + b0 + c2, rr < nb && c2 < nbk,
-                                    Lu);
+                    if (c2 < lb - 1)
+                        cp_async8_zfill(buf + rr * lb + c2, Lu + (int64_t)(p0 + rr) * r + b0 + c2, rr < nb && c2 < nbk, Lu);
                 }
             } else {  // Lb[c2][bb] = L[b0 + bb][p0 + c2]  (coalesced rows of L, transposed placement)
                 const int b0 = pe + c * kCBs, nbk = min(kCBs, q - b0);
 #pragma unroll
                 for (int kk = 0; kk < kPB * kCBs / 256; ++kk) {
                     const int e = tid + 256 * kk, bb = e / kPB, c2 = e % kPB;
-                    cp_async8_zfill(buf + c2 * (kCBs + 1) + bb, Lu + (int64_t)(b0 + bb) * r + p0 + c2, bb < nbk && c2 < nb,
-                                    Lu);
+                    if (bb < lb - 1)
+                        cp_async8_zfill(buf + c2 * lb + bb, Lu + (int64_t)(b0 + bb) * r + p0 + c2, bb < nbk && c2 < nb, Lu);
                 }
             }
         }
@@ -273,19 +274,19 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
     };
 #pragma unroll
     for (int k = 0; k < kSolveNS - 1; ++k) issue(k);
-    const int pr = tid >> 3, pc = (tid >> 2) & 1, part = tid & 3;
+    const int pr = tid >> 3, pc = (tid / PARTS) % C, part = tid % PARTS;
     double acc = 0.0;  // this thread's quarter of the panel row's running right-hand side
     bool panel_start = true;
     for (int k = 0; k < ns; ++k) {
         const int code = steps[k], dir = code >> 24, P = (code >> 12) & 0xfff, c = (code & 0xfff) - 1;
         const int p0 = P * kPB, nb = min(kPB, q - p0), pe = p0 + nb;
-        const double *buf = ring + (size_t)(k % kSolveNS) * kSolveBuf;
+        const double *buf = ring + (size_t)(k % kSolveNS) * sbuf;
         if (panel_start) acc = (pr < nb && part == 0) ? zs[(p0 + pr) * C + pc] : 0.0;
         cp_async_wait<kSolveNS - 2>();  // this thread's copies of step k landed
         if (c < 0) {                    // combine the four parts of the row's right-hand side
             double t = acc;
-            t += __shfl_xor_sync(0xffffffffu, t, 1);
-            t += __shfl_xor_sync(0xffffffffu, t, 2);
+#pragma unroll
+            for (int o = 1; o < PARTS; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
             if (part == 0) tP[pr][pc] = t;
         }
         __syncthreads();  // everyone's copies (and tP) visible
@@ -293,24 +294,24 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
             // Di is triangular with explicit zeros: full-length dot, split over the four parts
             double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-            for (int j = part; j < kPB; j += 8) {
+            for (int j = part; j < kPB; j += 2 * PARTS) {
                 z0 = fma(buf[pr * (kPB + 1) + j], tP[j][pc], z0);
-                z1 = fma(buf[pr * (kPB + 1) + j + 4], tP[j + 4][pc], z1);
+                z1 = fma(buf[pr * (kPB + 1) + j + PARTS], tP[j + PARTS][pc], z1);
             }
             double z = z0 + z1;
-            z += __shfl_xor_sync(0xffffffffu, z, 1);
-            z += __shfl_xor_sync(0xffffffffu, z, 2);
+#pragma unroll
+            for (int o = 1; o < PARTS; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
             if (pr < nb && part == 0) zs[(p0 + pr) * C + pc] = z;
         } else if (pr < nb) {
             const int b0 = dir == 0 ? c * kCBs : pe + c * kCBs;
             const int nbk = dir == 0 ? min(kCBs, p0 - b0) : min(kCBs, q - b0);
-            const double *lr = buf + pr * (kCBs + 1);
+            const double *lr = buf + pr * lb;
             double a0 = 0.0, a1 = 0.0;
             int bb = part;
 #pragma unroll 4
-            for (; bb + 4 < nbk; bb += 8) {
+            for (; bb + PARTS < nbk; bb += 2 * PARTS) {
                 a0 = fma(-lr[bb], zs[(b0 + bb) * C + pc], a0);
-                a1 = fma(-lr[bb + 4], zs[(b0 + bb + 4) * C + pc], a1);
+                a1 = fma(-lr[bb + PARTS], zs[(b0 + bb + PARTS) * C + pc], a1);
             }
             if (bb < nbk) a0 = fma(-lr[bb], zs[(b0 + bb) * C + pc], a0);
             acc += a0 + a1;
@@ -620,12 +621,21 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
                    double *Dinv, cudaStream_t st) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
     weights_dinv_kernel<<<dim3(nbl, Dm.units()), 32, 0, st>>>(L, r_eff, Dm.r, Dinv);
-    const size_t smem = ((size_t)kSolveC * Dm.r + (size_t)kSolveNS * kSolveBuf) * sizeof(double);
-    auto sk = weights_solve_kernel<D>;
-    // z plus the operand ring is dynamic (up to ~197 KB at r = 1024): always raise the limit
-    cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 g2((D + 1 + kSolveC - 1) / kSolveC, Dm.units());
-    sk<<<g2, 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+    // few units: 2 columns per CTA (more CTAs on the panel chain); many units: 8 per CTA
+    const bool wide = (int64_t)Dm.units() * ((D + 1 + 1) / 2) <= 4 * 148;
+    const int lb = std::min(kCBs, Dm.r) + 1;
+    const size_t ring = (size_t)kSolveNS * kPB * std::max(lb, kPB + 1);
+    if (wide) {
+        const size_t smem = ((size_t)2 * Dm.r + ring) * sizeof(double);
+        auto sk = weights_solve_kernel<D, 2>;
+        cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sk<<<dim3((D + 1 + 1) / 2, Dm.units()), 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+    } else {
+        const size_t smem = ((size_t)8 * Dm.r + ring) * sizeof(double);
+        auto sk = weights_solve_kernel<D, 8>;
+        cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sk<<<dim3((D + 1 + 7) / 8, Dm.units()), 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
