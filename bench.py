@@ -545,6 +545,25 @@ def main():
     if not args.no_variants and mode == "replicas" and rank == 0 and world == 1 and args.config == "headline":
         variants = variants or {}
         variants["kvcache"] = kv_variant(dev, flush, max(2, args.block), args.steps, with_exact=not args.no_exact)
+    # A5 against its own roofline (HBM-bound for r < 258 at bf16; intensity ~ r flop/byte):
+    # algorithmic bytes 2 m d e + r d e + 4 r (d + 1) per head and flops 4 m r d, over the attend stage
+    attend_roof = None
+    if st_mean and mode == "replicas":
+        at_ms = st_mean[3]
+        heads = cfg.batch * cfg.hq
+        a_bytes = heads * 2 * cfg.m * cfg.d * e + units * (R_main * cfg.d * e + 4 * R_main * (cfg.d + 1))
+        a_flops = heads * 4.0 * cfg.m * R_main * cfg.d
+        tp = None
+        tpf = os.path.join(ROOT, "profiles", "r1_ncu_attend_full_summary.txt")
+        if cfg.name == "headline" and os.path.exists(tpf):
+            for ln in open(tpf):
+                if ln.startswith("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"):
+                    tp = float(ln.split()[1]) / 100.0
+        attend_roof = {"kernel": "attend_tc_kernel (+ attend_img_prep_kernel)", "bound": "hbm",
+                       "achieved": a_bytes / (at_ms / 1e3) / 1e9, "peak": peaks()[0], "unit": "GB/s",
+                       "frac": a_bytes / (at_ms / 1e3) / 1e9 / peaks()[0],
+                       "tflops": a_flops / (at_ms / 1e3) / 1e12, "tensor_peak_tflops": 1685.2,
+                       "tensor_pipe_active_ncu": tp}
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"select_traffic_{cfg.name}" + (f"_b{args.block}" if args.block >= 2 else "")
                       + ".json")
@@ -647,6 +666,7 @@ def main():
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if achieved else None,
                          "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes},
+            "roofline_attend": attend_roof,
             "accuracy": err,
             "exact_sdpa_bf16_ms": sdpa_ms,
             "cpu_baseline": cpu,
