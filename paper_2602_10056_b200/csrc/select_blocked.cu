@@ -553,10 +553,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             int nacc = 0;
 #pragma unroll 1
             for (int j = 0; j < bsz && i + nacc < a.r; ++j) {
-                double hej = 0.0;  // H[j][e] (own column, row j) -- compile-time register indices
+                // lane j publishes its column H[:, j] through shared memory (double-buffered by step
+                // parity: the previous user of this buffer finished before the last __syncwarp);
+                // H stays bitwise symmetric (symmetric DMMA sums, commuted fma products), so
+                // H[j][e] = H[e][j] = col[e] and no register-indexed select chain is needed
+                double *col = rowj + (j & 1) * kBMax;
+                if (lane == j) {
 #pragma unroll
-                for (int x = 0; x < kBMax; ++x) hej = (x == j) ? hc[x] : hej;
-                const double hjj = __shfl_sync(0xffffffffu, hej, j);
+                    for (int x = 0; x < kBMax; ++x) col[x] = hc[x];
+                }
+                __syncwarp();
+                const double hjj = col[j];
+                const double hej = e < kBMax ? col[e] : 0.0;  // H[j][e] (lanes >= kBMax own no column)
                 const int sj = __shfl_sync(0xffffffffu, my_cs, j);
                 const double vp = __shfl_sync(0xffffffffu, my_vp, j);
                 const bool dup = __any_sync(0xffffffffu, my_acc && my_cs == sj);
@@ -566,7 +574,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     if (e < kBMax) Fcand[nacc * kBMax + e] = (e > j && e < bsz) ? fe : 0.0;
 #pragma unroll
                     for (int x = 0; x < kBMax; ++x) {
-                        const double fx = __shfl_sync(0xffffffffu, hc[x], j) * rinv;  // H[x][j] / sqrt
+                        const double fx = col[x] * rinv;  // H[x][j] / sqrt(H[j][j])
                         if (e > j && x > j) hc[x] = fma(-fx, fe, hc[x]);
                     }
                     if (lane == 0) {
