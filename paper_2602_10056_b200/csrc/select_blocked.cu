@@ -312,10 +312,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         if (w == 0) {
             const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
             double v = 0.0;
-            for (int cc = b0; cc < b1; ++cc) {
-                const double x = __ldcg(pc + cc);
-                spart[cc] = x;
-                v += x;
+            if (per <= 8) {  // all of the lane's loads in flight, then the fixed-order sum
+                double xs[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) xs[q] = (b0 + q < b1) ? __ldcg(pc + b0 + q) : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (b0 + q < b1) {
+                        spart[b0 + q] = xs[q];
+                        v += xs[q];
+                    }
+                }
+            } else {
+                for (int cc = b0; cc < b1; ++cc) {
+                    const double x = __ldcg(pc + cc);
+                    spart[cc] = x;
+                    v += x;
+                }
             }
             double incl = v;
 #pragma unroll
