@@ -725,6 +725,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             // entries of pivot keys, and the 32-key group sums.
             if (wact) {
                 double *stg = ring + (size_t)w * 32 * 17;  // [32 keys][17] per warp
+                double plh[2];  // the residuals of the lane's two keys, loaded before the staging
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t key = t0 + kw + 32 * h + lane;
+                    plh[h] = key < hi ? __ldcg(cur + key) : 0.0;
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
 #pragma unroll
                     for (int aa = 0; aa < kBMax; ++aa) gk[aa] = aa < na ? stg[lane * 17 + aa] : 0.0;
                     __syncwarp();
-                    double pl = key < hi ? __ldcg(cur + key) : 0.0;
+                    double pl = plh[h];
                     double* frow = Fk + (int64_t)i * wk + kw + 32 * h + lane;
                     double f[kBMax];
 #pragma unroll
@@ -778,13 +784,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                                 else if (aa < na) ftr[aa] = f[aa];
                             }
                         }
-                        for (int x = 0; x < na; ++x) {
-                            if (sA[x] == key) {  // L[i+x][i..i+x] = F[i..i+x, s_x]
-                                double *Lr = a.L + ((int64_t)u * a.r + i + x) * a.r + i;
+                        int xm = -1;  // acceptance index if this key is an accepted pivot (branch-free search)
 #pragma unroll
-                                for (int a2 = 0; a2 < kBMax; ++a2)
-                                    if (a2 <= x) Lr[a2] = f[a2];
-                            }
+                        for (int x = 0; x < kBMax; ++x) xm = (x < na && sA[x] == key) ? x : xm;
+                        if (xm >= 0) {  // L[i+x][i..i+x] = F[i..i+x, s_x]
+                            double *Lr = a.L + ((int64_t)u * a.r + i + xm) * a.r + i;
+#pragma unroll
+                            for (int a2 = 0; a2 < kBMax; ++a2)
+                                if (a2 <= xm) Lr[a2] = f[a2];
                         }
                     }
                     const double gs = warp_sum(key < hi ? pl : 0.0);  // one 32-key group (fixed order)
