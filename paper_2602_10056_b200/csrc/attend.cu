@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(256) attend_img_prep_kernel(const __nv_bfloat1
     }
 }
 
-template <int D, int RP>
-__global__ void __launch_bounds__(kTcThreads, 1)
+// NT threads: NT / 128 threads per query row (TMEM lane), each owning 1 / (NT / 128) of the S and O
+// columns; NT = 512 for d = 128, r > 64 (shorter softmax / epilogue per thread), else 256.
+template <int D, int RP, int NT>
+__global__ void __launch_bounds__(NT, 1)
     attend_tc_kernel(const __nv_bfloat16 *__restrict__ Q, const __nv_bfloat16 *__restrict__ KS,
                      const float *__restrict__ X, const int32_t *__restrict__ r_eff,
                      const __nv_bfloat16 *__restrict__ vmin, const __nv_bfloat16 *__restrict__ vmax, int64_t m,
@@ -223,12 +225,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     unsigned char *sP = sm + L::kOffP;
     float *sW = reinterpret_cast<float *>(sm + L::kOffW);
     __nv_bfloat16 *sVmin = reinterpret_cast<__nv_bfloat16 *>(sm + L::kOffV), *sVmax = sVmin + D;
-    float (*xch)[128] = reinterpret_cast<float (*)[128]>(sm + L::kOffXch);  // row exchange between halves
+    // row exchange between the NSPLIT column parts; aliases the Q tile, which is idle from the
+    // retirement of GEMM1 until the next tile's Q is stored (after a barrier)
+    float (*xch)[128] = reinterpret_cast<float (*)[128]>(sQ);
     uint64_t &bar = *reinterpret_cast<uint64_t *>(sm + L::kOffBar);
     uint64_t &ibar = *reinterpret_cast<uint64_t *>(sm + L::kOffBarI);
     uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + L::kOffTb);
     const int tid = threadIdx.x, w = tid >> 5;
-    const int row = tid & 127, half = tid >> 7;  // TMEM lane (query row) and column half
+    constexpr int NSPLIT = NT / 128;
+    const int row = tid & 127, half = tid >> 7;  // TMEM lane (query row) and column part
     constexpr int DC = D + 1;
     uint32_t iphase = 0;
 
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
     const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
     constexpr int CPR = D / 8;                   // 16-byte chunks per row
-    constexpr int NQ = 128 * CPR / kTcThreads;   // Q chunks per thread
+    constexpr int NQ = 128 * CPR / NT;           // Q chunks per thread
     auto unit_of = [&](int64_t tile) {
         const int64_t head = tile / tiles_per_head;
         return (int)(head / hq) * hkv + (int)(head % hq) / group;
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const __nv_bfloat16 *Qh = Q + head * m * D;
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
-            const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+            const int e = tid + k * NT, row = e / CPR, cc = e % CPR;
             qv[k] = (q0 + row < m) ? __ldg(reinterpret_cast<const uint4 *>(Qh + (q0 + row) * D) + cc)
                                    : make_uint4(0, 0, 0, 0);
         }
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     auto store_q = [&](const uint4 (&qv)[NQ]) {
 #pragma unroll
         for (int k = 0; k < NQ; ++k) {
-            const int e = tid + k * kTcThreads, row = e / CPR, cc = e % CPR;
+            const int e = tid + k * NT, row = e / CPR, cc = e % CPR;
             *reinterpret_cast<uint4 *>(sQ + umma::sw128_offset(row, cc * 8, 128)) = qv[k];
         }
     };
@@ -286,8 +291,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             bulk_g2s(sK, iu, (uint32_t)L::kImgKX, &ibar);
         }
         const float *wu = reinterpret_cast<const float *>(iu + L::kImgKX);
-        for (int s2 = tid; s2 < RP; s2 += kTcThreads) sW[s2] = __ldg(wu + s2);
-        for (int c = tid; c < D; c += kTcThreads) {
+        for (int s2 = tid; s2 < RP; s2 += NT) sW[s2] = __ldg(wu + s2);
+        for (int c = tid; c < D; c += NT) {
             sVmin[c] = vmin[(int64_t)u * D + c];
             sVmax[c] = vmax[(int64_t)u * D + c];
         }
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ---- softmax epilogue (two threads per row, RP/2 columns each, all in registers):
         // row max, P = exp2(beta log2e (S - max)) in bf16 -> smem, den = P . w (4 partial sums)
         {
-            constexpr int HC = RP / 2;  // columns per thread
+            constexpr int HC = RP / NSPLIT;  // columns per thread
             constexpr int NCH = HC / 32 > 0 ? HC / 32 : 1;
             const int cbase = half * HC;
             float v[HC >= 32 ? HC : 32];
@@ -340,7 +345,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (cbase + i2 < re) mx = fmaxf(mx, v[i2]);
             xch[half][row] = mx;
             __syncthreads();
-            mx = fmaxf(xch[0][row], xch[1][row]);
+#pragma unroll
+            for (int q2 = 0; q2 < NSPLIT; ++q2) mx = fmaxf(mx, xch[q2][row]);
             const float mb = mx * bl2;
             float dn[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -365,7 +371,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         sync_for_mma();
         if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 3] = gtimer_a();
-        const float den = xch[0][row] + xch[1][row];
+        float den = 0.f;
+#pragma unroll
+        for (int q2 = 0; q2 < NSPLIT; ++q2) den += xch[q2][row];
         // ---- O = P X_hi (+ P X_lo); the next tile's Q loads fly meanwhile
         if (tid == 0) {
             umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sXh), D, RP, false);
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma::fence_after_sync();
         if (atrace && blockIdx.x == 0 && threadIdx.x == 0 && tile - t_begin < 64) atrace[(tile - t_begin) * 8 + 4] = gtimer_a();
         if (same_unit) {  // S(t+1) overlaps this tile's output epilogue
+            __syncthreads();  // every thread has read den from xch (the Q tile) before it is refilled
             store_q(qv);
             sync_for_mma();
             issue_gemm1();
@@ -389,7 +398,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         {
             const int64_t qi = q0 + row;
             const float inv = den > 0.f ? 1.f / den : 0.f;
-            constexpr int HD = D / 2;
+            constexpr int HD = D / NSPLIT;
 #pragma unroll
             for (int c0 = 0; c0 < HD; c0 += 32) {
                 const int cc0 = half * HD + c0;
@@ -435,7 +444,8 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
     unsigned char *img = static_cast<unsigned char *>(ws);
     attend_img_prep_kernel<D, RP><<<dim3(RP / 4, (unsigned)Dm.units()), 256, 0, st>>>(
         static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, img);
-    auto kern = attend_tc_kernel<D, RP>;
+    constexpr int NT = (D == 128 && RP >= 128) ? 512 : kTcThreads;
+    auto kern = attend_tc_kernel<D, RP, NT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     const int64_t tph = ceil_div(Dm.m, 128);
     const int64_t total = tph * Dm.hq * Dm.batch;
@@ -449,7 +459,7 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
         cudaMalloc(&atrace, 64 * 8 * sizeof(unsigned long long));
         cudaMemsetAsync(atrace, 0, 64 * 8 * sizeof(unsigned long long), st);
     }
-    kern<<<grid, kTcThreads, L::kTotal, st>>>(
+    kern<<<grid, NT, L::kTotal, st>>>(
         static_cast<const __nv_bfloat16 *>(Q), static_cast<const __nv_bfloat16 *>(KS), X, r_eff,
         static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(),
         Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total, img, atrace);
