@@ -48,6 +48,7 @@ namespace wc {
 namespace {
 
 constexpr int kBMax = 16;  // largest supported block size b
+constexpr int kElimW = 7;  // compute warp that runs the rejection (kCW - 1)
 
 __device__ __forceinline__ double accept_uniform(uint64_t seed, uint32_t cand, uint64_t unit) {
     uint32_t c[4] = {cand, (uint32_t)unit, (uint32_t)(unit >> 32), 0x41435054u};  // 'ACPT'
@@ -555,7 +556,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         // also F[i+aa, s_x] for the later candidates x (the coefficients of the per-key triangle).
         // (warp 0, lane e = column e of the symmetric H in registers; column j is fetched from lane j
         // by shuffles -- H[x][j] is lane j's entry x).  Every thread learns na from shared memory.
-        if (w == 0) {
+        // The elimination runs on the LAST compute warp while the others start the round-update
+        // GEMMs (kernel dots and F prefix over all candidate slots do not depend on acceptance); at
+        // the headline that warp owns no keys of the CTA's slice, so the elimination is hidden.
+        if (w == kElimW) {
             const int e = lane;
             double hc[kBMax];
 #pragma unroll
@@ -602,29 +606,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             if (lane == 0) sh_na = nacc;
             WC_BTR(14);
         }
-        cw_sync();  // Fcand, sA, jA, rinvA, sh_na visible
-        const int na = sh_na;
-        {
-            const int aa = tid >> 4, a2 = tid & 15;
-            Fx[aa * kBMax + a2] = (aa < na && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
-            if (tid < kBMax) {
-                int pa = -1;
-                for (int x = 0; x < na; ++x) pa = (jA[x] == tid) ? x : pa;
-                perm[tid] = pa;
+        // na, Fx, perm and the owners' L rows / S: after the first super-tile's GEMM phase (below),
+        // once the elimination warp has joined the compute-warp barrier
+        int na = 0;
+        auto finish_elim = [&]() {
+            na = sh_na;
+            {
+                const int aa = tid >> 4, a2 = tid & 15;
+                Fx[aa * kBMax + a2] = (aa < na && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
+                if (tid < kBMax) {
+                    int pa = -1;
+                    for (int x = 0; x < na; ++x) pa = (jA[x] == tid) ? x : pa;
+                    perm[tid] = pa;
+                }
             }
-        }
-        cw_sync();
-        WC_BTR(4);
-        // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
-        for (int x = 0; x < na; ++x) {
-            const int s = sA[x];
-            if (s >= lo && s < hi) {
-                const int sl = jA[x];
-                for (int q = tid; q < i; q += kCT) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
-                if (tid == 0) a.S[(int64_t)u * a.r + i + x] = s;
+            cw_sync();
+            WC_BTR(4);
+            // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
+            for (int x = 0; x < na; ++x) {
+                const int s = sA[x];
+                if (s >= lo && s < hi) {
+                    const int sl = jA[x];
+                    for (int q = tid; q < i; q += kCT) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
+                    if (tid == 0) a.S[(int64_t)u * a.r + i + x] = s;
+                }
             }
-        }
-        WC_BTR(5);
+            WC_BTR(5);
+        };
 
         // ---- 4: na F-form rounds over this CTA's keys.  Per 512-key super-tile, warp w owns keys
         // [64w, 64w+64) as 8 MMA row-tiles of 8; over the 16 candidate slots,
@@ -644,9 +652,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
-            int pm[4];  // acceptance index of this lane's 4 C columns (slots 8 nt + 2 tq + hh), -1: rejected
-#pragma unroll
-            for (int z = 0; z < 4; ++z) pm[z] = perm[8 * (z >> 1) + 2 * tq + (z & 1)];
             if (wact) {
                 KC kc[2][8];  // double-buffered K chunks: chunk c + 1 is in flight while c feeds the MMAs
 #pragma unroll
@@ -685,7 +690,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     for (int hh = 0; hh < 2; ++hh) {
                         const int sl = 8 * nt + 2 * tq + hh;
                         const double cz = c0r[sl];
-                        if (pm[nt * 2 + hh] >= 0) {
+                        if (sl < bsz) {  // every drawn candidate (acceptance is not known yet)
 #pragma unroll
                             for (int mt = 0; mt < 8; ++mt)
                                 C[mt][nt][hh] = exp(__dadd_rn(__dmul_rn(g, C[mt][nt][hh] - cz), -mstar));
@@ -717,6 +722,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             }
             if (k == 0) WC_BTR(7);
             cw_sync();  // every warp is done with the ring before it is reused as staging
+            if (k == 0) finish_elim();  // (the elimination warp has arrived: its results are visible)
+            int pm[4];  // acceptance index of this lane's 4 C columns (slots 8 nt + 2 tq + hh), -1: rejected
+#pragma unroll
+            for (int z = 0; z < 4; ++z) pm[z] = perm[8 * (z >> 1) + 2 * tq + (z & 1)];
             // per-key triangle over the accepted pivots in acceptance order: G is transposed through
             // the ring (idle until the next block's request) so that lane k owns key 32 h + k of its
             // warp with all its G values in registers; left-looking:
@@ -805,6 +814,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                 cw_sync();
                 if (tid == 0) sh_req = ((long long)(++nreq) << 32) | ((long long)(k + 1) << 16) | (long long)i;
             }
+        }
+        if (nst == 0) {  // a CTA without keys still needs the accepted count
+            cw_sync();
+            finish_elim();
         }
         WC_BTR(8);
         fence_proxy_async_global();  // this block's F rows are read by later TMA copies
