@@ -849,17 +849,21 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), dtrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(dtrace);
-    const char *names[] = {"cand", "gather", "H", "elim+compact", "Lrows", "t0_kdot", "t0_fdot", "tiles", "sum",
+    // stamps in program order: 0 start, 1 candidates, 2 gather, 3 H, 6 kernel dots of super-tile 0
+    // (the rejection runs meanwhile on the last compute warp), 7 F prefix, 4 na / Fx / perm,
+    // 5 owners' L rows, 8 per-key triangle + writes, 9 sum, then the grid barrier (next block's 0)
+    const int order[] = {1, 2, 3, 6, 7, 4, 5, 8, 9, 16};
+    const char *names[] = {"cand", "gather", "H", "t0_kdot(+elim)", "t0_fdot", "na/Fx", "Lrows", "tiles", "sum",
                            "gbar"};
     for (int b = 0; b < r; ++b) {
         const unsigned long long *t = &h[(size_t)b * 16];
         if (!t[0] || !t[9]) break;
         std::fprintf(stderr, "[btrace] block %3d:", b);
         unsigned long long last = t[0];
-        for (int k = 1; k <= 10; ++k) {
-            const unsigned long long v = (k == 10) ? (b + 1 < r ? h[(size_t)(b + 1) * 16] : 0) : t[k];
+        for (int k = 0; k < 10; ++k) {
+            const unsigned long long v = order[k] == 16 ? (b + 1 < r ? h[(size_t)(b + 1) * 16] : 0) : t[order[k]];
             if (!v) continue;
-            std::fprintf(stderr, " %s=%llu", names[k - 1], v - last);
+            std::fprintf(stderr, " %s=%llu", names[k], v - last);
             last = v;
         }
         if (b == 0 && t[10] && t[11]) std::fprintf(stderr, " [1a=%llu cand0=%llu]", t[10] - t[0], t[11] - t[10]);
