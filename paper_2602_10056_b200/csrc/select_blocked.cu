@@ -603,34 +603,35 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     ++nacc;
                 }
             }
+            // the bookkeeping of the accepted pivots, still on this warp while the others run GEMMs:
+            // Fx[aa][a2] = F[i+a2, s_aa], perm (slot -> acceptance index), the owners' L rows and S
+            __syncwarp();  // Fcand, sA, jA written by lane 0 / the column lanes
+            for (int idx = lane; idx < kBMax * kBMax; idx += 32) {
+                const int aa = idx >> 4, a2 = idx & 15;
+                Fx[aa * kBMax + a2] = (aa < nacc && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
+            }
+            if (lane < kBMax) {
+                int pa = -1;
+                for (int x = 0; x < nacc; ++x) pa = (jA[x] == lane) ? x : pa;
+                perm[lane] = pa;
+            }
+            for (int x = 0; x < nacc; ++x) {  // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
+                const int s = sA[x];
+                if (s >= lo && s < hi) {
+                    const int sl = jA[x];
+                    for (int q = lane; q < i; q += 32) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
+                    if (lane == 0) a.S[(int64_t)u * a.r + i + x] = s;
+                }
+            }
             if (lane == 0) sh_na = nacc;
             WC_BTR(14);
         }
         // na, Fx, perm and the owners' L rows / S: after the first super-tile's GEMM phase (below),
         // once the elimination warp has joined the compute-warp barrier
         int na = 0;
-        auto finish_elim = [&]() {
+        auto finish_elim = [&]() {  // after a compute-warp barrier that follows the elimination
             na = sh_na;
-            {
-                const int aa = tid >> 4, a2 = tid & 15;
-                Fx[aa * kBMax + a2] = (aa < na && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
-                if (tid < kBMax) {
-                    int pa = -1;
-                    for (int x = 0; x < na; ++x) pa = (jA[x] == tid) ? x : pa;
-                    perm[tid] = pa;
-                }
-            }
-            cw_sync();
             WC_BTR(4);
-            // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
-            for (int x = 0; x < na; ++x) {
-                const int s = sA[x];
-                if (s >= lo && s < hi) {
-                    const int sl = jA[x];
-                    for (int q = tid; q < i; q += kCT) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
-                    if (tid == 0) a.S[(int64_t)u * a.r + i + x] = s;
-                }
-            }
             WC_BTR(5);
         };
 
