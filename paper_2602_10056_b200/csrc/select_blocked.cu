@@ -197,6 +197,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
     const int nst = (int)ceil_div(hi - lo, kBT);
+    // the per-key triangle stages both of a lane's keys at once when the ring holds [64][17] per warp
+    const bool two_keys = (size_t)NS * kBR * kPitch >= (size_t)kCW * 64 * 17;
     const int bsz = a.b;
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
@@ -734,48 +736,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             // then the F row writes (coalesced), the downdate with the clamp (Z4), p_s <- 0, the L
             // entries of pivot keys, and the 32-key group sums.
             if (wact) {
-                double *stg = ring + (size_t)w * 32 * 17;  // [32 keys][17] per warp
                 double plh[2];  // the residuals of the lane's two keys, loaded before the staging
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int64_t key = t0 + kw + 32 * h + lane;
                     plh[h] = key < hi ? __ldcg(cur + key) : 0.0;
                 }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                    for (int m4 = 0; m4 < 4; ++m4)
-#pragma unroll
-                        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const int ai = pm[nt * 2 + hh];
-                                if (ai >= 0) stg[(8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
-                            }
-                    __syncwarp();
+                // per key (lane, half h) after its triangle: residual, key-major FT row, L rows of an
+                // accepted pivot, and the 32-key group sum
+                auto key_epilogue = [&](int h, const double (&f)[kBMax], double pl) {
                     const int64_t key = t0 + kw + 32 * h + lane;
-                    double gk[kBMax];
-#pragma unroll
-                    for (int aa = 0; aa < kBMax; ++aa) gk[aa] = aa < na ? stg[lane * 17 + aa] : 0.0;
-                    __syncwarp();
-                    double pl = plh[h];
-                    double* frow = Fk + (int64_t)i * wk + kw + 32 * h + lane;
-                    double f[kBMax];
-#pragma unroll
-                    for (int aa = 0; aa < kBMax; ++aa) {
-                        f[aa] = 0.0;
-                        if (aa < na) {
-                            double cv = gk[aa];
-                            const double *fx = Fx + aa * kBMax;
-#pragma unroll
-                            for (int a2 = 0; a2 < aa; ++a2) cv = fma(-f[a2], fx[a2], cv);
-                            const double fv = cv * rinvA[aa];
-                            f[aa] = fv;
-                            if (key < hi) frow[(int64_t)aa * wk] = fv;
-                            const double q = __dadd_rn(pl, -__dmul_rn(fv, fv));
-                            pl = (q > 0.0 && key != sA[aa]) ? q : 0.0;
-                        }
-                    }
                     if (key < hi) {
                         nxt[key] = pl;
                         double *ftr = a.FT + ((int64_t)u * n + key) * ftl + i;  // key-major copy of the new rows
@@ -808,6 +778,96 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     if (lane == 0 && t0 + kw + 32 * h < hi) {
                         gnxt[(t0 + kw) / 32 + h] = gs;
                         loc += gs;
+                    }
+                };
+                if (two_keys) {
+                    // both of the lane's keys staged at once and their triangles interleaved (two
+                    // independent fp64 chains; per key the same operations in the same order)
+                    double *stg = ring + (size_t)w * 64 * 17;  // [64 keys][17] per warp
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int m4 = 0; m4 < 4; ++m4)
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    const int ai = pm[nt * 2 + hh];
+                                    if (ai >= 0) stg[(32 * h + 8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
+                                }
+                    __syncwarp();
+                    const int64_t key0 = t0 + kw + lane, key1 = key0 + 32;
+                    const double *g0 = stg + lane * 17, *g1 = g0 + 32 * 17;
+                    double *frow0 = Fk + (int64_t)i * wk + kw + lane, *frow1 = frow0 + 32;
+                    double f0[kBMax], f1[kBMax];
+                    double pl0 = plh[0], pl1 = plh[1];
+#pragma unroll
+                    for (int aa = 0; aa < kBMax; ++aa) {
+                        f0[aa] = 0.0;
+                        f1[aa] = 0.0;
+                        if (aa < na) {
+                            double c0v = g0[aa], c1v = g1[aa];
+                            const double *fx = Fx + aa * kBMax;
+#pragma unroll
+                            for (int a2 = 0; a2 < aa; ++a2) {
+                                const double x = fx[a2];
+                                c0v = fma(-f0[a2], x, c0v);
+                                c1v = fma(-f1[a2], x, c1v);
+                            }
+                            const double ra = rinvA[aa];
+                            const double fv0 = c0v * ra, fv1 = c1v * ra;
+                            f0[aa] = fv0;
+                            f1[aa] = fv1;
+                            if (key0 < hi) frow0[(int64_t)aa * wk] = fv0;
+                            if (key1 < hi) frow1[(int64_t)aa * wk] = fv1;
+                            const int sa = sA[aa];
+                            const double q0 = __dadd_rn(pl0, -__dmul_rn(fv0, fv0));
+                            const double q1 = __dadd_rn(pl1, -__dmul_rn(fv1, fv1));
+                            pl0 = (q0 > 0.0 && key0 != sa) ? q0 : 0.0;
+                            pl1 = (q1 > 0.0 && key1 != sa) ? q1 : 0.0;
+                        }
+                    }
+                    __syncwarp();
+                    key_epilogue(0, f0, pl0);
+                    key_epilogue(1, f1, pl1);
+                } else {
+                    double *stg = ring + (size_t)w * 32 * 17;  // [32 keys][17] per warp
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int m4 = 0; m4 < 4; ++m4)
+#pragma unroll
+                            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    const int ai = pm[nt * 2 + hh];
+                                    if (ai >= 0) stg[(8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
+                                }
+                        __syncwarp();
+                        const int64_t key = t0 + kw + 32 * h + lane;
+                        double gk[kBMax];
+#pragma unroll
+                        for (int aa = 0; aa < kBMax; ++aa) gk[aa] = aa < na ? stg[lane * 17 + aa] : 0.0;
+                        __syncwarp();
+                        double pl = plh[h];
+                        double *frow = Fk + (int64_t)i * wk + kw + 32 * h + lane;
+                        double f[kBMax];
+#pragma unroll
+                        for (int aa = 0; aa < kBMax; ++aa) {
+                            f[aa] = 0.0;
+                            if (aa < na) {
+                                double cv = gk[aa];
+                                const double *fx = Fx + aa * kBMax;
+#pragma unroll
+                                for (int a2 = 0; a2 < aa; ++a2) cv = fma(-f[a2], fx[a2], cv);
+                                const double fv = cv * rinvA[aa];
+                                f[aa] = fv;
+                                if (key < hi) frow[(int64_t)aa * wk] = fv;
+                                const double q = __dadd_rn(pl, -__dmul_rn(fv, fv));
+                                pl = (q > 0.0 && key != sA[aa]) ? q : 0.0;
+                            }
+                        }
+                        key_epilogue(h, f, pl);
                     }
                 }
             }
