@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
     float mn[8], mx[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) { cs[k] = 0.0; mn[k] = 3.0e38f; mx[k] = -3.0e38f; }
-    constexpr int U4 = 4;  // rows per thread in flight
+    constexpr int U4 = 8;  // rows per thread in flight
     for (int64_t l0 = lo + rg; l0 < hi; l0 += (int64_t)U4 * RG) {
         Raw8<T> xk[U4], xv[U4];
 #pragma unroll
@@ -114,10 +114,49 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
     }
 }
 
-// Finalise kbar (fixed-order sum over splits) and the value range.  Block (u, column chunk of 32):
-// 8 groups of 32 threads; group g sums splits p = g, g + 8, ... (unrolled), combined in group order.
+// Finalise kbar (fixed-order sum over splits) and the value range.  One block per (unit, column j):
+// thread t sums splits t, t + 256, ... (in order), then a fixed-shape shared-memory tree combines
+// the 256 partials -- every column is reduced by its own block, with all its loads in flight.
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, const double *colsum,
+                                                     const float *vmin_p, const float *vmax_p, double *stats,
+                                                     T *vmin, T *vmax) {
+    __shared__ double s_t[kPT];
+    __shared__ float s_a[kPT], s_b[kPT];
+    const int u = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+    double t = 0.0;
+    float a = 3.0e38f, b = -3.0e38f;
+    for (int p = tid; p < P; p += nt) {
+        const int64_t o = ((int64_t)u * P + p) * d + j;
+        t += colsum[o];
+        a = fminf(a, vmin_p[o]);
+        b = fmaxf(b, vmax_p[o]);
+    }
+    s_t[tid] = t;
+    s_a[tid] = a;
+    s_b[tid] = b;
+    __syncthreads();
+    for (int h = nt / 2; h > 0; h >>= 1) {  // nt is a power of two
+        if (tid < h) {
+            s_t[tid] += s_t[tid + h];
+            s_a[tid] = fminf(s_a[tid], s_a[tid + h]);
+            s_b[tid] = fmaxf(s_b[tid], s_b[tid + h]);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = s_t[0] / (double)n;
+        if (vmin) {
+            vmin[(int64_t)u * d + j] = from_f32<T>(s_a[0]);
+            vmax[(int64_t)u * d + j] = from_f32<T>(s_b[0]);
+        }
+    }
+}
+
+// Few splits (many units): finalise kbar and the value range for 32 columns per block.  Block (u, column chunk of 32):
+// 8 groups of 32 threads; group g sums splits p = g, g + 8, ... (unrolled), combined in group order.
+template <typename T>
+__global__ void __launch_bounds__(kPT) prologue_kbar_small(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
                                                      T *vmin, T *vmax) {
     __shared__ double s_t[kPT];
@@ -154,6 +193,26 @@ __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, co
     }
 }
 
+// threads of a kbar block: a power of two in [32, kPT] covering the split count
+inline int kbar_threads(int P) {
+    int t = 32;
+    while (t < P && t < kPT) t <<= 1;
+    return t;
+}
+
+// kbar / value-range finalisation: one block per column for many splits, 32 columns per block else
+template <typename T>
+void launch_kbar(const Dims &D, int P, const ProloguePartials &pp, double *stats, void *vmin, void *vmax,
+                 cudaStream_t st) {
+    if (P >= 64)
+        prologue_kbar<T><<<dim3(D.units(), D.d), kbar_threads(P), 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax,
+                                                                          stats, static_cast<T *>(vmin),
+                                                                          static_cast<T *>(vmax));
+    else
+        prologue_kbar_small<T><<<dim3(D.units(), (D.d + 31) / 32), kPT, 0, st>>>(
+            D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats, static_cast<T *>(vmin), static_cast<T *>(vmax));
+}
+
 // Pass 2: nrm2_l = ||k_l - kbar||^2 (fp64) and the split max.  CPR threads per key.
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, int64_t n, int d, int P,
@@ -170,7 +229,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
     const T *Ku = K + (int64_t)u * n * d;
     double best = 0.0;
-    constexpr int U4 = 4;  // rows per thread in flight
+    constexpr int U4 = 8;  // rows per thread in flight
     for (int64_t l0 = lo; l0 < hi; l0 += (int64_t)U4 * RG) {
         Raw8<T> xk[U4];
 #pragma unroll
@@ -247,9 +306,7 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                                                static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
                                                (int64_t)D.group() * D.m);
-    prologue_kbar<T><<<dim3(units, (D.d + 31) / 32), kPT, 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats,
-                                            want_v ? static_cast<T *>(vmin) : nullptr,
-                                            want_v ? static_cast<T *>(vmax) : nullptr);
+    launch_kbar<T>(D, P, pp, stats, want_v ? vmin : nullptr, want_v ? vmax : nullptr, st);
     prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, P, stats, nrm2, pp.rk2);
     prologue_tau<<<ceil_div(units, 4), 128, 0, st>>>(units, D.n, D.d, P, pp.rk2, pp.rq2,
                                                       want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats);
@@ -264,8 +321,7 @@ int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmi
     dim3 grid(pp.P, units);
     prologue_pass1<T><<<grid, kPT, smem, st>>>(nullptr, static_cast<const T *>(V), static_cast<const T *>(V), D.n,
                                                0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0);
-    prologue_kbar<T><<<dim3(units, (D.d + 31) / 32), kPT, 0, st>>>(D.n, D.d, pp.P, pp.colsum, pp.vmin, pp.vmax, nullptr,
-                                            static_cast<T *>(vmin), static_cast<T *>(vmax));
+    launch_kbar<T>(D, pp.P, pp, nullptr, vmin, vmax, st);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
