@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
     const int64_t rows = ceil_div(n, P);
     const int64_t lo = (int64_t)p * rows, hi = min(n, lo + rows);
     const T *Ku = K + (int64_t)u * n * d;
+    double kbr[8];  // this thread's 8 columns of kbar, kept in registers across its rows
+#pragma unroll
+    for (int k = 0; k < 8; ++k) kbr[k] = kb[8 * cj + k];
     double best = 0.0;
     constexpr int U4 = 8;  // rows per thread in flight
     for (int64_t l0 = lo; l0 < hi; l0 += (int64_t)U4 * RG) {
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
             if (l < hi) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const double c = __dadd_rn(xk[q].at(k), -kb[8 * cj + k]);
+                    const double c = __dadd_rn(xk[q].at(k), -kbr[k]);
                     sq = __dadd_rn(sq, __dmul_rn(c, c));
                 }
             }
