@@ -357,109 +357,134 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         // of that CTA's slice) -> key (warp scan of the group's 32 residuals).  Each level falls back
         // to its last positive entry if rounding leaves no crossing (reading Z2).
         {
-            const double v = sv[lane], incl = sinc[lane];
-            const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
-            for (int j = w; j < bsz; j += kCW) {
-                const double t = pivot_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u) * Ttot;
-                // level 1: CTA
-                const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
-                const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
-                const int Ln = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
-                int cstar = 0;
-                double tp = 0.0;
-                if (lane == Ln) {
-                    double acc = incl - v;
-                    int csel = -1, last = -1;
-                    double excl = 0.0, last_excl = 0.0;
-                    for (int cc = b0; cc < b1; ++cc) {
-                        const double pvv = spart[cc];
-                        if (pvv > 0.0) { last = cc; last_excl = acc; }
-                        const double nacc = acc + pvv;
-                        if (csel < 0 && hit && nacc > t) { csel = cc; excl = acc; }
-                        acc = nacc;
-                    }
-                    if (csel < 0) { csel = last; excl = last_excl; }
-                    cstar = csel;
-                    tp = t - excl;
-                }
-                cstar = __shfl_sync(0xffffffffu, cstar, Ln);
-                tp = __shfl_sync(0xffffffffu, tp, Ln);
-                // level 2: 32-key group inside c*'s slice
-                const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
-                const int64_t shi = std::min<int64_t>(n, slo + chunk);
-                const int g0 = (int)(slo / 32), gn = (int)((shi - slo + 31) / 32);
-                const int gper = (gn + 31) / 32;
-                const int q0 = g0 + lane * gper, q1 = min(g0 + gn, q0 + gper);
-                constexpr int kG = 4;  // fast path: <= 128 groups per slice, kept in registers
-                double gv[kG];
-                double v2 = 0.0;
-                if (gper <= kG) {
+            // each half-warp draws one candidate (j = w and j = w + 8 at the same time): 16 lanes per
+            // level of the hierarchy, so a warp's two draws share one chain of L2 round trips
+            const int h16 = lane >> 4, l16 = lane & 15;
+            const unsigned hm = 0xFFFFu << (16 * h16);
+            const int j = w + kCW * h16;
+            const bool jok = j < bsz;
+            const int per16 = (a.cpu + 15) / 16;
+            const int b0 = l16 * per16, b1 = min(a.cpu, b0 + per16);
+            double v = 0.0;
+            for (int cc = b0; cc < b1; ++cc) v += spart[cc];
+            double incl = v;
 #pragma unroll
-                    for (int q = 0; q < kG; ++q) gv[q] = (q0 + q < q1) ? __ldcg(gcur + q0 + q) : 0.0;
-#pragma unroll
-                    for (int q = 0; q < kG; ++q) v2 += gv[q];
-                } else {
-                    for (int q = q0; q < q1; ++q) v2 += __ldcg(gcur + q);
-                }
-                double inc2 = v2;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, inc2, o);
-                    if (lane >= o) inc2 += y;
-                }
-                const unsigned hit2 = __ballot_sync(0xffffffffu, q1 > q0 && inc2 > tp);
-                const unsigned pos2 = __ballot_sync(0xffffffffu, q1 > q0 && v2 > 0.0);
-                const int L2 = hit2 ? __ffs(hit2) - 1 : 31 - __clz(pos2);
-                int gstar = 0;
-                double tq2 = 0.0;
-                if (lane == L2) {
-                    double acc = inc2 - v2;
-                    int gsel = -1, last = -1;
-                    double excl = 0.0, last_excl = 0.0;
-                    for (int q = q0; q < q1; ++q) {
-                        double gg = 0.0;
-                        if (gper <= kG) {
-#pragma unroll
-                            for (int z = 0; z < kG; ++z) gg = (z == q - q0) ? gv[z] : gg;
-                        } else {
-                            gg = __ldcg(gcur + q);
-                        }
-                        if (gg > 0.0) { last = q; last_excl = acc; }
-                        const double nacc = acc + gg;
-                        if (gsel < 0 && hit2 && nacc > tp) { gsel = q; excl = acc; }
-                        acc = nacc;
-                    }
-                    if (gsel < 0) { gsel = last; excl = last_excl; }
-                    gstar = gsel;
-                    tq2 = tp - excl;
-                }
-                gstar = __shfl_sync(0xffffffffu, gstar, L2);
-                tq2 = __shfl_sync(0xffffffffu, tq2, L2);
-                // level 3: key inside the group
-                const int64_t key = (int64_t)gstar * 32 + lane;
-                const double pl = key < shi ? __ldcg(cur + key) : 0.0;
-                double inc3 = pl;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, inc3, o);
-                    if (lane >= o) inc3 += y;
-                }
-                const unsigned hit3 = __ballot_sync(0xffffffffu, inc3 > tq2);
-                const unsigned pos3 = __ballot_sync(0xffffffffu, pl > 0.0);
-                const int L3 = hit3 ? __ffs(hit3) - 1 : 31 - __clz(pos3);
-                const double psv = __shfl_sync(0xffffffffu, pl, L3);
-                if (lane == 0) {
-                    const int s = (int)(gstar * 32 + L3);
-                    cs[j] = s;
-                    cp[j] = psv;
-                    vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u);
-                    const int64_t cc = s / chunk, off = s - cc * chunk;
-                    const int kk = (int)(off / kBT);
-                    cfo[j] = cc * chunk * a.r + (int64_t)kk * kBT * a.r + (off % kBT);
-                    cwk[j] = (int)std::min<int64_t>(kBT, chunk - (int64_t)kk * kBT);
-                }
-                if (blk == 0 && j == 0) WC_BTR(11);
+            for (int o = 1; o < 16; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, o, 16);
+                if (l16 >= o) incl += y;
             }
+            const double Tw = __shfl_sync(0xffffffffu, incl, 15, 16);  // the total in this order
+            const double t = jok ? pivot_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u) * Tw : 0.0;
+            // level 1: CTA
+            const unsigned hit = (__ballot_sync(0xffffffffu, b1 > b0 && incl > t) & hm) >> (16 * h16);
+            const unsigned pos = (__ballot_sync(0xffffffffu, b1 > b0 && v > 0.0) & hm) >> (16 * h16);
+            const int Ln = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
+            int cstar = 0;
+            double tp = 0.0;
+            if (l16 == Ln) {
+                double acc = incl - v;
+                int csel = -1, last = -1;
+                double excl = 0.0, last_excl = 0.0;
+                for (int cc = b0; cc < b1; ++cc) {
+                    const double pvv = spart[cc];
+                    if (pvv > 0.0) { last = cc; last_excl = acc; }
+                    const double nacc = acc + pvv;
+                    if (csel < 0 && hit && nacc > t) { csel = cc; excl = acc; }
+                    acc = nacc;
+                }
+                if (csel < 0) { csel = last; excl = last_excl; }
+                cstar = csel;
+                tp = t - excl;
+            }
+            cstar = __shfl_sync(0xffffffffu, cstar, Ln, 16);
+            tp = __shfl_sync(0xffffffffu, tp, Ln, 16);
+            // level 2: 32-key group inside c*'s slice
+            const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
+            const int64_t shi = std::min<int64_t>(n, slo + chunk);
+            const int g0 = (int)(slo / 32), gn = (int)((shi - slo + 31) / 32);
+            const int gper = (gn + 15) / 16;
+            const int q0 = g0 + l16 * gper, q1 = min(g0 + gn, q0 + gper);
+            constexpr int kG = 8;  // fast path: <= 128 groups per slice, kept in registers
+            double gv[kG];
+            double v2 = 0.0;
+            if (gper <= kG) {
+#pragma unroll
+                for (int q = 0; q < kG; ++q) gv[q] = (q0 + q < q1) ? __ldcg(gcur + q0 + q) : 0.0;
+#pragma unroll
+                for (int q = 0; q < kG; ++q) v2 += gv[q];
+            } else {
+                for (int q = q0; q < q1; ++q) v2 += __ldcg(gcur + q);
+            }
+            double inc2 = v2;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, inc2, o, 16);
+                if (l16 >= o) inc2 += y;
+            }
+            const unsigned hit2 = (__ballot_sync(0xffffffffu, q1 > q0 && inc2 > tp) & hm) >> (16 * h16);
+            const unsigned pos2 = (__ballot_sync(0xffffffffu, q1 > q0 && v2 > 0.0) & hm) >> (16 * h16);
+            const int L2 = hit2 ? __ffs(hit2) - 1 : 31 - __clz(pos2);
+            int gstar = 0;
+            double tq2 = 0.0;
+            if (l16 == L2) {
+                double acc = inc2 - v2;
+                int gsel = -1, last = -1;
+                double excl = 0.0, last_excl = 0.0;
+                for (int q = q0; q < q1; ++q) {
+                    double gg = 0.0;
+                    if (gper <= kG) {
+#pragma unroll
+                        for (int z = 0; z < kG; ++z) gg = (z == q - q0) ? gv[z] : gg;
+                    } else {
+                        gg = __ldcg(gcur + q);
+                    }
+                    if (gg > 0.0) { last = q; last_excl = acc; }
+                    const double nacc = acc + gg;
+                    if (gsel < 0 && hit2 && nacc > tp) { gsel = q; excl = acc; }
+                    acc = nacc;
+                }
+                if (gsel < 0) { gsel = last; excl = last_excl; }
+                gstar = gsel;
+                tq2 = tp - excl;
+            }
+            gstar = __shfl_sync(0xffffffffu, gstar, L2, 16);
+            tq2 = __shfl_sync(0xffffffffu, tq2, L2, 16);
+            // level 3: key inside the group, two keys per lane (in key order)
+            const int64_t k0 = (int64_t)gstar * 32 + 2 * l16;
+            const double pa = k0 < shi ? __ldcg(cur + k0) : 0.0;
+            const double pb = k0 + 1 < shi ? __ldcg(cur + k0 + 1) : 0.0;
+            const double v3 = pa + pb;
+            double inc3 = v3;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, inc3, o, 16);
+                if (l16 >= o) inc3 += y;
+            }
+            const unsigned hit3 = (__ballot_sync(0xffffffffu, inc3 > tq2) & hm) >> (16 * h16);
+            const unsigned pos3 = (__ballot_sync(0xffffffffu, v3 > 0.0) & hm) >> (16 * h16);
+            const int L3 = hit3 ? __ffs(hit3) - 1 : 31 - __clz(pos3);
+            int s3 = 0;
+            double psv = 0.0;
+            if (l16 == L3) {  // which of the lane's two keys: strict '>' in key order, fallback to the last positive
+                const double ex = inc3 - v3;
+                if (hit3 && ex + pa > tq2) { s3 = 0; psv = pa; }
+                else if (hit3) { s3 = 1; psv = pb; }
+                else if (pb > 0.0) { s3 = 1; psv = pb; }
+                else { s3 = 0; psv = pa; }
+            }
+            s3 = __shfl_sync(0xffffffffu, s3, L3, 16);
+            psv = __shfl_sync(0xffffffffu, psv, L3, 16);
+            if (l16 == 0 && jok) {
+                const int s = (int)(gstar * 32 + 2 * L3 + s3);
+                cs[j] = s;
+                cp[j] = psv;
+                vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u);
+                const int64_t cc = s / chunk, off = s - cc * chunk;
+                const int kk = (int)(off / kBT);
+                cfo[j] = cc * chunk * a.r + (int64_t)kk * kBT * a.r + (off % kBT);
+                cwk[j] = (int)std::min<int64_t>(kBT, chunk - (int64_t)kk * kBT);
+            }
+            if (blk == 0 && j == 0) WC_BTR(11);
         }
         cw_sync();
         WC_BTR(1);
