@@ -555,22 +555,30 @@ __global__ void __launch_bounds__(kWTc, 1)
     }
     xch[half * 128 + row] = rowsum;
     __syncthreads();
-    float *out = Ypart + (((int64_t)u * splits + split) * r + a0 + row) * DC;
-    if (nsl == 0) {  // empty key range: zero partial
-        if (row_ok && half == 0)
-            for (int c = 0; c < DC; ++c) out[c] = 0.f;
-    } else {
+    // the [128][d+1] partial tile is staged in the idle B / P / V buffers (all MMAs have retired) and
+    // written as one contiguous run (its rows are consecutive rows of Ypart): coalesced stores
+    float *ytile = reinterpret_cast<float *>(sm + L::kOffB);
+    static_assert(128 * (D + 1) * 4 <= L::kOffG - L::kOffB, "partial tile fits the idle operand buffers");
+    {
         constexpr int HD = D / 2;
+        if (nsl == 0) {  // empty key range: zero partial
+            for (int c = half * HD; c < half * HD + HD; ++c) ytile[row * DC + c] = 0.f;
+        } else {
 #pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-            float v[32];
-            umma::ld32(tO + lane_off + half * HD + c0, v);
-            if (row_ok) {
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                float v[32];
+                umma::ld32(tO + lane_off + half * HD + c0, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) out[half * HD + c0 + i] = v[i];
+                for (int i = 0; i < 32; ++i) ytile[row * DC + half * HD + c0 + i] = v[i];
             }
         }
-        if (row_ok && half == 0) out[D] = xch[row] + xch[128 + row];
+        if (half == 0) ytile[row * DC + D] = nsl == 0 ? 0.f : xch[row] + xch[128 + row];
+    }
+    __syncthreads();
+    {
+        const int nrows = min(128, re - a0);  // rows past r_eff are not written
+        float *dst = Ypart + (((int64_t)u * splits + split) * r + a0) * DC;
+        for (int e = tid; e < nrows * DC; e += kWTc) dst[e] = ytile[e];
     }
     umma::fence_before_sync();
     __syncthreads();
