@@ -394,8 +394,13 @@ __global__ void __launch_bounds__(NT, 1)
             sync_for_mma();
             issue_gemm1();
         }
-        // ---- output epilogue: each thread finishes D/2 columns of its row
+        // ---- output epilogue: each thread finishes D/NSPLIT columns of its row.  When the bf16 tile
+        // fits the (idle) P buffer it is assembled there (16-byte chunks XOR-swizzled by row, so
+        // both the row writes and the chunk reads are bank-conflict free) and, its rows being
+        // consecutive rows of O, leaves as one contiguous run of 16-byte stores.
         {
+            constexpr bool kStaged = 128 * D * 2 <= L::kP;
+            constexpr int RB = D * 2;  // output row bytes
             const int64_t qi = q0 + row;
             const float inv = den > 0.f ? 1.f / den : 0.f;
             constexpr int HD = D / NSPLIT;
@@ -404,27 +409,41 @@ __global__ void __launch_bounds__(NT, 1)
                 const int cc0 = half * HD + c0;
                 float v[32];
                 umma::ld32(tO + lane_off + cc0, v);
-                if (qi < m) {
-                    uint32_t pk[16];
+                uint32_t pk[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
-                        if (clip) {
-                            o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[cc0 + 2 * i])), __bfloat162float(sVmax[cc0 + 2 * i]));
-                            o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[cc0 + 2 * i + 1])), __bfloat162float(sVmax[cc0 + 2 * i + 1]));
-                        }
-                        const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
-                        pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
+                for (int i = 0; i < 16; ++i) {
+                    float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
+                    if (clip) {
+                        o0 = fminf(fmaxf(o0, __bfloat162float(sVmin[cc0 + 2 * i])), __bfloat162float(sVmax[cc0 + 2 * i]));
+                        o1 = fminf(fmaxf(o1, __bfloat162float(sVmin[cc0 + 2 * i + 1])), __bfloat162float(sVmax[cc0 + 2 * i + 1]));
                     }
+                    const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
+                    pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
+                }
+                if constexpr (kStaged) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int ch = cc0 / 8 + i;  // 16-byte chunk of the row
+                        *reinterpret_cast<uint4 *>(sP + row * RB + ((ch ^ (row & 7)) * 16)) =
+                            make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                    }
+                } else if (qi < m) {
                     uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + qi) * D + cc0);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
                 }
             }
+            if constexpr (kStaged) {
+                __syncthreads();
+                constexpr int CPRO = RB / 16;  // 16-byte chunks per output row (>= 8)
+                const int nrows = (int)std::min<int64_t>(128, m - q0);
+                uint4 *dst = reinterpret_cast<uint4 *>(O + (head * m + q0) * D);
+                for (int e = tid; e < nrows * CPRO; e += NT) {
+                    const int rr = e / CPRO, ch = e % CPRO;
+                    dst[e] = *reinterpret_cast<const uint4 *>(sP + rr * RB + ((ch ^ (rr & 7)) * 16));
+                }
+            }
         }
-        umma::fence_before_sync();
-        __syncthreads();  // O (TMEM) and the unit's smem free
-        umma::fence_after_sync();
         if (has_next && !same_unit) {  // new unit: restage K_S / X, then S(t+1)
             store_q(qv);
             stage_unit(unit_of(tile + 1));
