@@ -130,7 +130,9 @@ int wildcat_weights(const wc_shape *shape, const wc_opts *opts, const void *K, c
 
 /* Alg 3 WtdAttn: O = clip( diag(A^ w)^{-1} A^ V_S where A^ w > 0 else 0, vmin, vmax ),
  * A^ = exp(beta Q K_S^T) over the first r_eff coreset rows.  `m` of the shape is the
- * number of queries per q-head (e.g. 1 for decode; 0 < m <= 16 selects the split-cache decode kernel). */
+ * number of queries per q-head (e.g. 1 for decode; 0 < m <= 16 selects the split-cache decode kernel).
+ * Workspace: wc_workspace_bytes(shape, WC_OP_ATTEND) -- the per-unit operand image of the tcgen05
+ * path (bf16, d in {64, 128}) or the decode kernel's split partials; 0 (ws may be NULL) otherwise. */
 int wildcat_attend(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *KS,
                    const float *X, const int32_t *r_eff, const void *vmin, const void *vmax,
                    void *O, void *ws, size_t ws_bytes, void *stream);
