@@ -74,7 +74,8 @@ template <int D, int QR> struct DecSmem {
     static constexpr int kF = kS + QR * kDecC;                  // [QR] this tile's rescale factors
     static constexpr int kDen = kF + QR;                        // [QR] running denominators
     static constexpr int kRed = kDen + QR;                      // [2][8] cross-warp max / den partials
-    static constexpr int kR = kRed + 16;                        // [256/D][QR][D] row-group partial sums
+                                                                //  (MMA scores: [2][8 warps][4] + run / new max)
+    static constexpr int kR = kRed + 80;                        // [256/D][QR][D] row-group partial sums
     static constexpr int kFloats = kR + kDecT * QR;
     static constexpr size_t kBytes = (size_t)kFloats * 4;
 };
@@ -123,6 +124,14 @@ template <typename T, int D> struct DecTile {
     }
 };
 
+// bf16 tensor-core MMA m16n8k16 (fp32 accumulate): D = A B + C, A 16x16 row-major, B 16x8 column-major.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 // Grid (splits, units, qz).  CTA (split, u, z) runs query rows [QR z, QR z + QR) of unit u over the
 // cache tiles split, split + splits, ... (kDecC rows each) with an online max.
 //   scores: thread (q = tid / TPR, g = tid % TPR), TPR = 256 / QR, computes query row q's scores of
@@ -168,6 +177,24 @@ __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
 #pragma unroll
     for (int k = 0; k < QR; ++k) acc[k] = 0.f;
     float mrun = -INFINITY;  // of query row q (score-phase mapping)
+    // QR = 4, bf16: the scores run on the tensor cores (m16n8k16, the 4 query rows padded to 16): warp
+    // w forms S[0:4, 8w:8w+8] of the 64-row tile over D/16 k-steps; A fragments (raw bf16 Q) stay in
+    // registers for the whole CTA, B fragments are the raw key words in shared memory.  Products of
+    // bf16 are exact in fp32; the beta*log2(e) scale is applied to the fp32 result.
+    constexpr bool kMma = (QR == 4) && (sizeof(T) == 2);
+    const int lane = tid & 31, wq = tid >> 5, gid = lane >> 2, tq = lane & 3;
+    uint32_t aq[kMma ? D / 16 : 1][2];
+    float *mrun_s = red + 64, *mnew_s = red + 68;
+    if constexpr (kMma) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+            const bool okq = gid < nq;
+            const uint32_t *qr = reinterpret_cast<const uint32_t *>(Q + (qoff + t0 + (okq ? gid : 0)) * D);
+            aq[kk][0] = okq ? __ldg(qr + kk * 8 + tq) : 0u;
+            aq[kk][1] = okq ? __ldg(qr + kk * 8 + 4 + tq) : 0u;
+        }
+        if (tid < 4) mrun_s[tid] = -INFINITY;
+    }
     DecTile<T, D> tile;
     int tcur = split;
     if (tcur < ntiles) tile.load(KSu, Xu, tcur * kDecC, min(kDecC, re - tcur * kDecC), tid);
@@ -178,73 +205,122 @@ __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
         const int tnext = tcur + splits;
         if (tnext < ntiles) tile.load(KSu, Xu, tnext * kDecC, min(kDecC, re - tnext * kDecC), tid);
         __syncthreads();
-        // ---- scores of query row q against cache rows g + TPR k
-        float sc[NS], sc2[NS];
+        if constexpr (kMma) {
+            float c4[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint32_t *kr = ks + (8 * wq + gid) * KW;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) sc[k] = sc2[k] = 0.f;
-        if constexpr (sizeof(T) == 2) {
-#pragma unroll 8
-            for (int j2 = 0; j2 < D / 2; ++j2) {
-                const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + 2 * j2);
-#pragma unroll
-                for (int k = 0; k < NS; ++k) {
-                    const uint32_t w = ks[(g + TPR * k) * KW + j2];
-                    sc[k] = fmaf(qv.x, __uint_as_float(w << 16), sc[k]);
-                    sc2[k] = fmaf(qv.y, __uint_as_float(w & 0xffff0000u), sc2[k]);
-                }
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t a4[4] = {aq[kk][0], 0u, aq[kk][1], 0u};
+                mma_bf16_16816(c4, a4, kr[kk * 8 + tq], kr[kk * 8 + 4 + tq]);
             }
+            // lane (gid, tq): query gid, cache rows 8 wq + 2 tq + {0, 1}
+            const int c0 = 8 * wq + 2 * tq;
+            const float s0 = c0 < nc ? c4[0] * sl2 : -INFINITY, s1 = c0 + 1 < nc ? c4[1] * sl2 : -INFINITY;
+            float tm = fmaxf(s0, s1);
+            tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 1));
+            tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 2));
+            if (tq == 0 && gid < 4) red[wq * 4 + gid] = tm;
+            __syncthreads();
+            if (tid < 4) {  // per query: tile max over the 8 warps, running max, rescale factor
+                float m8 = red[tid];
+#pragma unroll
+                for (int w8 = 1; w8 < 8; ++w8) m8 = fmaxf(m8, red[w8 * 4 + tid]);
+                const float mo = mrun_s[tid], mn = fmaxf(mo, m8);  // nc >= 1, so finite
+                fs[tid] = exp2f(mo - mn);  // 0 on the first tile
+                mrun_s[tid] = mn;
+                mnew_s[tid] = mn;
+            }
+            __syncthreads();
+            float dp = 0.f;
+            if (gid < 4) {
+                const float mn = mnew_s[gid];
+                const float p0 = exp2f(s0 - mn), p1 = exp2f(s1 - mn);  // 0 for rows past nc
+                ps[c0 * QR + gid] = p0;
+                ps[(c0 + 1) * QR + gid] = p1;
+                if (c0 < nc) dp = fmaf(p0, xs[c0 * DC + D], dp);
+                if (c0 + 1 < nc) dp = fmaf(p1, xs[(c0 + 1) * DC + D], dp);
+            }
+            dp += __shfl_xor_sync(0xffffffffu, dp, 1);
+            dp += __shfl_xor_sync(0xffffffffu, dp, 2);
+            if (tq == 0 && gid < 4) red[32 + wq * 4 + gid] = dp;
+            __syncthreads();
+            if (tid < 4) {
+                float d8 = 0.f;
+#pragma unroll
+                for (int w8 = 0; w8 < 8; ++w8) d8 += red[32 + w8 * 4 + tid];
+                dens[tid] = dens[tid] * fs[tid] + d8;
+            }
+            mrun = mrun_s[q];
+            __syncthreads();
         } else {
-#pragma unroll 8
-            for (int j = 0; j < D; j += 2) {
-                const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + j);
-#pragma unroll
-                for (int k = 0; k < NS; ++k) {
-                    sc[k] = fmaf(qv.x, __uint_as_float(ks[(g + TPR * k) * KW + j]), sc[k]);
-                    sc2[k] = fmaf(qv.y, __uint_as_float(ks[(g + TPR * k) * KW + j + 1]), sc2[k]);
+        // ---- scores of query row q against cache rows g + TPR k
+            float sc[NS], sc2[NS];
+    #pragma unroll
+            for (int k = 0; k < NS; ++k) sc[k] = sc2[k] = 0.f;
+            if constexpr (sizeof(T) == 2) {
+    #pragma unroll 8
+                for (int j2 = 0; j2 < D / 2; ++j2) {
+                    const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + 2 * j2);
+    #pragma unroll
+                    for (int k = 0; k < NS; ++k) {
+                        const uint32_t w = ks[(g + TPR * k) * KW + j2];
+                        sc[k] = fmaf(qv.x, __uint_as_float(w << 16), sc[k]);
+                        sc2[k] = fmaf(qv.y, __uint_as_float(w & 0xffff0000u), sc2[k]);
+                    }
+                }
+            } else {
+    #pragma unroll 8
+                for (int j = 0; j < D; j += 2) {
+                    const float2 qv = *reinterpret_cast<const float2 *>(qs + q * D + j);
+    #pragma unroll
+                    for (int k = 0; k < NS; ++k) {
+                        sc[k] = fmaf(qv.x, __uint_as_float(ks[(g + TPR * k) * KW + j]), sc[k]);
+                        sc2[k] = fmaf(qv.y, __uint_as_float(ks[(g + TPR * k) * KW + j + 1]), sc2[k]);
+                    }
                 }
             }
-        }
-        float tm = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            sc[k] = g + TPR * k < nc ? sc[k] + sc2[k] : -INFINITY;
-            tm = fmaxf(tm, sc[k]);
-        }
-#pragma unroll
-        for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-        if constexpr (WPR > 1) {
-            if ((tid & 31) == 0) red[tid >> 5] = tm;
-            __syncthreads();
-#pragma unroll
-            for (int w = 0; w < WPR; ++w) tm = fmaxf(tm, red[q * WPR + w]);
-        }
-        const float mnew = fmaxf(mrun, tm);  // nc >= 1, so finite
-        const float f = exp2f(mrun - mnew);  // 0 on the first tile
-        mrun = mnew;
-        float dp = 0.f;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const int c = g + TPR * k;
-            const float pv = exp2f(sc[k] - mnew);  // 0 for rows past nc
-            ps[c * QR + q] = pv;
-            if (c < nc) dp = fmaf(pv, xs[c * DC + D], dp);
-        }
-#pragma unroll
-        for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
-        if constexpr (WPR > 1) {
-            if ((tid & 31) == 0) red[8 + (tid >> 5)] = dp;
-            __syncthreads();
-            if (g == 0) {
-                dp = 0.f;
-#pragma unroll
-                for (int w = 0; w < WPR; ++w) dp += red[8 + q * WPR + w];
+            float tm = -INFINITY;
+    #pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                sc[k] = g + TPR * k < nc ? sc[k] + sc2[k] : -INFINITY;
+                tm = fmaxf(tm, sc[k]);
             }
+    #pragma unroll
+            for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+            if constexpr (WPR > 1) {
+                if ((tid & 31) == 0) red[tid >> 5] = tm;
+                __syncthreads();
+    #pragma unroll
+                for (int w = 0; w < WPR; ++w) tm = fmaxf(tm, red[q * WPR + w]);
+            }
+            const float mnew = fmaxf(mrun, tm);  // nc >= 1, so finite
+            const float f = exp2f(mrun - mnew);  // 0 on the first tile
+            mrun = mnew;
+            float dp = 0.f;
+    #pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const int c = g + TPR * k;
+                const float pv = exp2f(sc[k] - mnew);  // 0 for rows past nc
+                ps[c * QR + q] = pv;
+                if (c < nc) dp = fmaf(pv, xs[c * DC + D], dp);
+            }
+    #pragma unroll
+            for (int o = (TPR < 32 ? TPR : 32) / 2; o; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+            if constexpr (WPR > 1) {
+                if ((tid & 31) == 0) red[8 + (tid >> 5)] = dp;
+                __syncthreads();
+                if (g == 0) {
+                    dp = 0.f;
+    #pragma unroll
+                    for (int w = 0; w < WPR; ++w) dp += red[8 + q * WPR + w];
+                }
+            }
+            if (g == 0) {
+                dens[q] = dens[q] * f + dp;
+                fs[q] = f;
+            }
+            __syncthreads();
         }
-        if (g == 0) {
-            dens[q] = dens[q] * f + dp;
-            fs[q] = f;
-        }
-        __syncthreads();
         // ---- P . V_S: column col for all QR query rows over the row group's cache rows
 #pragma unroll
         for (int k = 0; k < QR; ++k) acc[k] *= fs[k];
