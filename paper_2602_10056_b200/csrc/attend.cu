@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(256) attend_img_prep_kernel(const __nv_bfloat1
                                                               const float *__restrict__ X,
                                                               const int32_t *__restrict__ r_eff, int r,
                                                               unsigned char *__restrict__ img) {
+    pdl_wait();
     using L = TcSmem<D, RP>;
     constexpr int DC = D + 1, CPR = D / 8;
     const int u = blockIdx.y, re = r_eff[u];
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(NT, 1)
                      int r, int group, int hq, int hkv, float beta, int clip, __nv_bfloat16 *__restrict__ O,
                      int64_t tiles_per_head, int64_t total_tiles, const unsigned char *__restrict__ img,
                      unsigned long long *atrace) {
+    pdl_wait();
     using L = TcSmem<D, RP>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw;  // offset 0 of the CTA's shared window: 1024-aligned
@@ -461,8 +463,8 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
     using L = TcSmem<D, RP>;
     if (!ws) return -1;
     unsigned char *img = static_cast<unsigned char *>(ws);
-    attend_img_prep_kernel<D, RP><<<dim3(RP / 4, (unsigned)Dm.units()), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, img);
+    launch_pdl(attend_img_prep_kernel<D, RP>, dim3(RP / 4, (unsigned)Dm.units()), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, img);
     constexpr int NT = (D == 128 && RP >= 128) ? 512 : kTcThreads;
     auto kern = attend_tc_kernel<D, RP, NT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
@@ -478,10 +480,10 @@ int launch_attend_tc(const Dims &Dm, const void *Q, const void *KS, const float 
         cudaMalloc(&atrace, 64 * 8 * sizeof(unsigned long long));
         cudaMemsetAsync(atrace, 0, 64 * 8 * sizeof(unsigned long long), st);
     }
-    kern<<<grid, NT, L::kTotal, st>>>(
-        static_cast<const __nv_bfloat16 *>(Q), static_cast<const __nv_bfloat16 *>(KS), X, r_eff,
-        static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(),
-        Dm.hq, Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total, img, atrace);
+    launch_pdl(kern, dim3(grid), dim3(NT), (size_t)L::kTotal, st, static_cast<const __nv_bfloat16 *>(Q),
+               static_cast<const __nv_bfloat16 *>(KS), X, r_eff, static_cast<const __nv_bfloat16 *>(vmin),
+               static_cast<const __nv_bfloat16 *>(vmax), Dm.m, Dm.r, Dm.group(), Dm.hq, Dm.hkv, (float)beta, clip,
+               static_cast<__nv_bfloat16 *>(O), tph, total, (const unsigned char *)img, atrace);
     if (atrace) {  // debug: phase durations of CTA 0's tiles (ns)
         unsigned long long h[64 * 8];
         cudaStreamSynchronize(st);

@@ -119,6 +119,7 @@ template <int D>
 __global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__restrict__ Ypart,
                                                              const int32_t *__restrict__ r_eff, int r, int splits,
                                                              double *__restrict__ Y) {
+    pdl_wait();
     constexpr int DC = D + 1;
     const int u = blockIdx.y;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (a, c) flattened
@@ -149,6 +150,7 @@ constexpr int kCBs = 128; // L columns (forward) / rows (backward) fetched per r
 
 __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restrict__ L, const int32_t *__restrict__ r_eff,
                                                           int r, double *__restrict__ Dinv) {
+    pdl_wait();
     __shared__ double Lb[kPB][kPB + 1];
     const int blk = blockIdx.x, u = blockIdx.y, lane = threadIdx.x;
     const int q = r_eff[u], p0 = blk * kPB;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
                                                             const double *__restrict__ Dinv,
                                                             const int32_t *__restrict__ r_eff, int r,
                                                             float *__restrict__ X) {
+    pdl_wait();
     constexpr int DC = D + 1, PARTS = 8 / C;
     const int lb = min(kCBs, r) + 1, sbuf = kPB * max(lb, kPB + 1);
     extern __shared__ double zs[];  // z[r][C], then the operand ring [kSolveNS][sbuf]
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
 template <typename T, int D>
 __global__ void gather_ks_kernel(const T *__restrict__ K, const int32_t *__restrict__ S,
                                  const int32_t *__restrict__ r_eff, int64_t n, int r, T *__restrict__ KS) {
+    pdl_wait();
     const int u = blockIdx.y, a = blockIdx.x;
     const int q = r_eff[u];
     const int s = a < q ? S[(int64_t)u * r + a] : -1;
@@ -373,6 +377,7 @@ __global__ void __launch_bounds__(kWTc, 1)
                       const int32_t *__restrict__ S, const __nv_bfloat16 *__restrict__ KSin,
                       const int32_t *__restrict__ r_eff,
                       const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
+    pdl_wait();
     using L = WtSmem<D>;
     constexpr int DC = D + 1;
     constexpr int CPR = D / 8;          // 16-byte chunks per row
@@ -600,9 +605,9 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
             auto kt = weights_tc_kernel<D>;
             cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc);
             dim3 gt(splits, (Dm.r + 127) / 128, units);
-            kt<<<gt, kWTc, smem_tc, st>>>(static_cast<const __nv_bfloat16 *>(K), static_cast<const __nv_bfloat16 *>(V),
-                                          S, static_cast<const __nv_bfloat16 *>(KSin), r_eff, stats, Dm.n, Dm.r,
-                                          splits, Ypart);
+            launch_pdl(kt, gt, dim3(kWTc), smem_tc, st, static_cast<const __nv_bfloat16 *>(K),
+                       static_cast<const __nv_bfloat16 *>(V), S, static_cast<const __nv_bfloat16 *>(KSin), r_eff,
+                       stats, Dm.n, Dm.r, splits, Ypart);
             done = true;
         }
     }
@@ -619,7 +624,7 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
     double *Yfull = *Yfull_out ? *Yfull_out : reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
     const int64_t cnt = (int64_t)Dm.r * (D + 1);
     dim3 gr((unsigned)ceil_div(cnt, 256), units);
-    weights_reduce_kernel<D><<<gr, 256, 0, st>>>(Ypart, r_eff, Dm.r, splits, Yfull);
+    launch_pdl(weights_reduce_kernel<D>, gr, dim3(256), 0, st, (const float *)Ypart, r_eff, Dm.r, splits, Yfull);
     *Yfull_out = Yfull;
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
@@ -628,7 +633,7 @@ template <int D>
 int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
                    double *Dinv, cudaStream_t st) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
-    weights_dinv_kernel<<<dim3(nbl, Dm.units()), 32, 0, st>>>(L, r_eff, Dm.r, Dinv);
+    launch_pdl(weights_dinv_kernel, dim3(nbl, Dm.units()), dim3(32), 0, st, L, r_eff, Dm.r, Dinv);
     // few units: 2 columns per CTA (more CTAs on the panel chain); many units: 8 per CTA
     const bool wide = (int64_t)Dm.units() * ((D + 1 + 1) / 2) <= 4 * 148;
     const int lb = std::min(kCBs, Dm.r) + 1;
@@ -637,12 +642,14 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
         const size_t smem = ((size_t)2 * Dm.r + ring) * sizeof(double);
         auto sk = weights_solve_kernel<D, 2>;
         cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sk<<<dim3((D + 1 + 1) / 2, Dm.units()), 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+        launch_pdl(sk, dim3((D + 1 + 1) / 2, Dm.units()), dim3(256), smem, st, Yfull, L, (const double *)Dinv, r_eff,
+                   Dm.r, X);
     } else {
         const size_t smem = ((size_t)8 * Dm.r + ring) * sizeof(double);
         auto sk = weights_solve_kernel<D, 8>;
         cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sk<<<dim3((D + 1 + 7) / 8, Dm.units()), 256, smem, st>>>(Yfull, L, Dinv, r_eff, Dm.r, X);
+        launch_pdl(sk, dim3((D + 1 + 7) / 8, Dm.units()), dim3(256), smem, st, Yfull, L, (const double *)Dinv, r_eff,
+                   Dm.r, X);
     }
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
@@ -658,8 +665,8 @@ int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_
     const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st);
     if (k2 < 0) return -1;
     dim3 g3(Dm.r, Dm.units());
-    gather_ks_kernel<T, D><<<g3, 128, 0, st>>>(static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
-                                               static_cast<T *>(KS));
+    launch_pdl(gather_ks_kernel<T, D>, g3, dim3(128), 0, st, static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
+               static_cast<T *>(KS));
     return cudaPeekAtLastError() == cudaSuccess ? k1 + k2 + 1 : -1;
 }
 
