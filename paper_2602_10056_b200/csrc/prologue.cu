@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
                                                       int P, int want_q, int want_v, double *colsum,
                                                       float *vmin, float *vmax, double *rq2,
                                                       int64_t q_unit_stride_rows) {
+    pdl_wait();
     extern __shared__ double sm1[];
     const int p = blockIdx.x, u = blockIdx.y;
     const int CPR = d / 8, RG = kPT / CPR;
@@ -121,6 +122,7 @@ template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
                                                      T *vmin, T *vmax) {
+    pdl_wait();
     __shared__ double s_t[kPT];
     __shared__ float s_a[kPT], s_b[kPT];
     const int u = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
@@ -159,6 +161,7 @@ template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar_small(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
                                                      T *vmin, T *vmax) {
+    pdl_wait();
     __shared__ double s_t[kPT];
     __shared__ float s_a[kPT], s_b[kPT];
     const int u = blockIdx.x, g = threadIdx.x >> 5, j = blockIdx.y * 32 + (threadIdx.x & 31);
@@ -205,9 +208,9 @@ template <typename T>
 void launch_kbar(const Dims &D, int P, const ProloguePartials &pp, double *stats, void *vmin, void *vmax,
                  cudaStream_t st) {
     if (P >= 64)
-        prologue_kbar<T><<<dim3(D.units(), D.d), kbar_threads(P), 0, st>>>(D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax,
-                                                                          stats, static_cast<T *>(vmin),
-                                                                          static_cast<T *>(vmax));
+        launch_pdl(prologue_kbar<T>, dim3(D.units(), D.d), dim3(kbar_threads(P)), 0, st, D.n, D.d, P,
+                   (const double *)pp.colsum, (const float *)pp.vmin, (const float *)pp.vmax, stats,
+                   static_cast<T *>(vmin), static_cast<T *>(vmax));
     else
         prologue_kbar_small<T><<<dim3(D.units(), (D.d + 31) / 32), kPT, 0, st>>>(
             D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats, static_cast<T *>(vmin), static_cast<T *>(vmax));
@@ -217,6 +220,7 @@ void launch_kbar(const Dims &D, int P, const ProloguePartials &pp, double *stats
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, int64_t n, int d, int P,
                                                       const double *stats, double *nrm2, double *rk2) {
+    pdl_wait();
     __shared__ double kb[128];
     __shared__ double scr[40];
     const int p = blockIdx.x, u = blockIdx.y;
@@ -264,6 +268,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
 // One warp per unit: maxima over the P splits, then lane 0 evaluates Eq. 7.
 __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *rk2, const double *rq2,
                              double rq_given, double beta, double *stats) {
+    pdl_wait();
     const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (u >= units) return;
     double mk = 0.0, mq = 0.0;
@@ -310,8 +315,10 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
                                                (int64_t)D.group() * D.m);
     launch_kbar<T>(D, P, pp, stats, want_v ? vmin : nullptr, want_v ? vmax : nullptr, st);
-    prologue_pass2<T><<<grid, kPT, 0, st>>>(static_cast<const T *>(K), D.n, D.d, P, stats, nrm2, pp.rk2);
-    prologue_tau<<<ceil_div(units, 4), 128, 0, st>>>(units, D.n, D.d, P, pp.rk2, pp.rq2,
+    launch_pdl(prologue_pass2<T>, grid, dim3(kPT), 0, st, static_cast<const T *>(K), D.n, D.d, P,
+               (const double *)stats, nrm2, pp.rk2);
+    launch_pdl(prologue_tau, dim3((unsigned)ceil_div(units, 4)), dim3(128), 0, st, units, D.n, D.d, P,
+               (const double *)pp.rk2, (const double *)pp.rq2,
                                                       want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats);
     return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
 }
