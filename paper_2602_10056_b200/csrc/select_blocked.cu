@@ -152,6 +152,7 @@ template <typename T, int TC> struct KChunk {
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
+    pdl_wait();  // the prologue's stats / nrm2 (programmatic dependent launch)
     constexpr int DQ = D / 4;             // dims per lane per key in the kernel-dot MMA
     constexpr int TC = 4;                 // k-steps per register chunk of the K row (8 or 16 bytes per key)
     using KC = KChunk<T, TC>;
@@ -987,10 +988,23 @@ int launch_blocked_td(const Dims &Dm, const void *K, double *stats, SelectBufs b
     const dim3 grid(a.units * a.cpu);
     if (a.cpu > 1) {
         void *args[] = {&a, (void *)&NS};
-        if (cudaLaunchCooperativeKernel((const void *)kt, grid, dim3(kTmaThreads), args, smem, st) != cudaSuccess)
-            return -1;
+        // cooperative (co-resident CTAs for the grid barrier) + programmatic stream serialisation
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kTmaThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        if (cudaLaunchKernelEx(&cfg, kt, a, NS) != cudaSuccess) return -1;
+        (void)args;
     } else {
-        kt<<<grid, kTmaThreads, smem, st>>>(a, NS);
+        launch_pdl(kt, grid, dim3(kTmaThreads), smem, st, a, NS);
     }
     if (a.trace) dump_block_trace(a.trace, Dm.r, st);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
