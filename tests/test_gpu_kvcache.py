@@ -138,3 +138,11 @@ def test_kv_llm32k_full_size():
     Oo = oracle.cache_attend(_np(Qdec[:, :4]), orc["KC"], orc["XC"], orc["c_eff"], orc["vmin"], orc["vmax"], 1)
     err = float(np.abs(_np(Od[:, :4]) - Oo).max()) / float(np.abs(_np(V[:, :1])).max())
     assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("d,g,m_dec", [(16, 4, 1), (32, 2, 2), (64, 1, 3), (128, 4, 1)])
+def test_decode_token_tensor_core_scores(d, g, m_dec):
+    # group * m <= 4: one decode token of a GQA group -> tensor-core scores (QR = 4) for every d
+    Q, K, V = qkv(1, 2 * g, 2, 64, 700, d, "bf16", "G", seed=21)
+    Qdec = qkv(1, 2 * g, 2, m_dec, 16, d, "bf16", "G", seed=22)[0]
+    _kv_case(Q, K, V, 96, 8, 8, "bf16", block=8, seed=21, Qdec=Qdec)
