@@ -148,11 +148,11 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__rest
 constexpr int kPB = 32;   // panel size
 constexpr int kCBs = 128; // L columns (forward) / rows (backward) fetched per round trip
 
-__global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restrict__ L, const int32_t *__restrict__ r_eff,
-                                                          int r, double *__restrict__ Dinv) {
-    pdl_wait();
-    __shared__ double Lb[kPB][kPB + 1];
-    const int blk = blockIdx.x, u = blockIdx.y, lane = threadIdx.x;
+// Inverse of the 32 x 32 diagonal block blk of unit u's L (one warp; lane c owns column c of the
+// inverse, a sequential substitution with broadcast reads of the block).
+__device__ __forceinline__ void dinv_block(const double *__restrict__ L, const int32_t *__restrict__ r_eff, int r,
+                                           double *__restrict__ Dinv, int blk, int u, int lane,
+                                           double (*Lb)[kPB + 1]) {
     const int q = r_eff[u], p0 = blk * kPB;
     if (p0 >= q) return;
     const int nb = min(kPB, q - p0);
@@ -172,6 +172,48 @@ __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restri
     double *Du = Dinv + ((int64_t)u * ((r + kPB - 1) / kPB) + blk) * kPB * kPB;
 #pragma unroll
     for (int i = 0; i < kPB; ++i) Du[i * kPB + lane] = x[i];  // row-major inverse, lower triangular
+}
+
+__global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restrict__ L, const int32_t *__restrict__ r_eff,
+                                                          int r, double *__restrict__ Dinv) {
+    pdl_wait();
+    __shared__ double Lb[kPB][kPB + 1];
+    dinv_block(L, r_eff, r, Dinv, blockIdx.x, blockIdx.y, threadIdx.x, Lb);
+}
+
+// weights_reduce_kernel + the diagonal-block inverses in one launch (single-GPU path): blocks
+// [0, nred) reduce the split partials, blocks [nred, nred + r/32) invert one diagonal block each
+// (both depend only on earlier kernels, so they run side by side).
+template <int D>
+__global__ void __launch_bounds__(256) weights_reduce_dinv_kernel(const float *__restrict__ Ypart,
+                                                                  const int32_t *__restrict__ r_eff, int r, int splits,
+                                                                  double *__restrict__ Y, const double *__restrict__ L,
+                                                                  double *__restrict__ Dinv, int nred) {
+    pdl_wait();
+    __shared__ double Lb[kPB][kPB + 1];
+    constexpr int DC = D + 1;
+    const int u = blockIdx.y;
+    if ((int)blockIdx.x >= nred) {
+        if (threadIdx.x < 32) dinv_block(L, r_eff, r, Dinv, blockIdx.x - nred, u, threadIdx.x, Lb);
+        return;
+    }
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (a, c) flattened
+    if (e >= (int64_t)r * DC) return;
+    const int a = (int)(e / DC);
+    double y = 0.0;
+    if (a < r_eff[u]) {
+        const float *src = Ypart + (int64_t)u * splits * r * DC + e;
+        int sp = 0;
+        for (; sp + 16 <= splits; sp += 16) {  // 16 independent loads in flight, summed in split order
+            float t[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) y += (double)t[k];
+        }
+        for (; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
+    }
+    Y[(int64_t)u * r * DC + e] = y;
 }
 
 // The solve is a chain of steps: per panel P (kPB rows), CHUNK steps (acc -= L-block . z over kCBs
@@ -594,7 +636,8 @@ __global__ void __launch_bounds__(kWTc, 1)
 // fixed-order fp64 sum into Yfull.  Coreset rows come from K[S] or, if KSin != nullptr, densely.
 template <typename T, int D>
 int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const void *KSin,
-                      const int32_t *r_eff, const double *stats, float *Ypart, double **Yfull_out, cudaStream_t st) {
+                      const int32_t *r_eff, const double *stats, float *Ypart, double **Yfull_out, cudaStream_t st,
+                      const double *L_dinv = nullptr) {
     const int units = Dm.units();
     const int splits = weights_num_splits(Dm);
     static const char *mode = std::getenv("WC_WEIGHTS");  // "cuda": CUDA-core kernel (A/B tests)
@@ -624,16 +667,23 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
     double *Yfull = *Yfull_out ? *Yfull_out : reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
     const int64_t cnt = (int64_t)Dm.r * (D + 1);
     dim3 gr((unsigned)ceil_div(cnt, 256), units);
-    launch_pdl(weights_reduce_kernel<D>, gr, dim3(256), 0, st, (const float *)Ypart, r_eff, Dm.r, splits, Yfull);
+    if (L_dinv) {  // single-GPU path: the diagonal-block inverses of L ride along (Dinv follows Y~)
+        const int nbl = (Dm.r + kPB - 1) / kPB;
+        double *Dinv = Yfull + (size_t)units * Dm.r * (D + 1);
+        launch_pdl(weights_reduce_dinv_kernel<D>, dim3(gr.x + nbl, units), dim3(256), 0, st, (const float *)Ypart,
+                   r_eff, Dm.r, splits, Yfull, L_dinv, Dinv, (int)gr.x);
+    } else {
+        launch_pdl(weights_reduce_kernel<D>, gr, dim3(256), 0, st, (const float *)Ypart, r_eff, Dm.r, splits, Yfull);
+    }
     *Yfull_out = Yfull;
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 template <int D>
 int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
-                   double *Dinv, cudaStream_t st) {
+                   double *Dinv, cudaStream_t st, bool dinv_done = false) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
-    launch_pdl(weights_dinv_kernel, dim3(nbl, Dm.units()), dim3(32), 0, st, L, r_eff, Dm.r, Dinv);
+    if (!dinv_done) launch_pdl(weights_dinv_kernel, dim3(nbl, Dm.units()), dim3(32), 0, st, L, r_eff, Dm.r, Dinv);
     // few units: 2 columns per CTA (more CTAs on the panel chain); many units: 8 per CTA
     const bool wide = (int64_t)Dm.units() * ((D + 1 + 1) / 2) <= 4 * 148;
     const int lb = std::min(kCBs, Dm.r) + 1;
@@ -651,18 +701,18 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
         launch_pdl(sk, dim3((D + 1 + 7) / 8, Dm.units()), dim3(256), smem, st, Yfull, L, (const double *)Dinv, r_eff,
                    Dm.r, X);
     }
-    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
 }
 
 template <typename T, int D>
 int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
                       const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
     double *Yfull = nullptr;
-    const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st);
+    const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st, L);
     if (k1 < 0) return -1;
     // scratch for the diagonal-block inverses: after Y~ in the weights workspace (carve_weights)
     double *Dinv = Yfull + (size_t)Dm.units() * Dm.r * (D + 1);
-    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st);
+    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st, true);
     if (k2 < 0) return -1;
     dim3 g3(Dm.r, Dm.units());
     launch_pdl(gather_ks_kernel<T, D>, g3, dim3(128), 0, st, static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
