@@ -20,6 +20,7 @@ constexpr int kBT = 256;
 
 __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restrict__ stats_u, const double *__restrict__ nrm2,
                                                          int64_t nb, int d, int bins, double beta, double *__restrict__ stats_b) {
+    pdl_wait();
     __shared__ double scr[40];
     const int su = blockIdx.x, u = su / bins;
     const double *nr = nrm2 + (int64_t)su * nb;  // nrm2 [units][n] == [units*B][nb]
@@ -55,6 +56,7 @@ __global__ void bins_pack_kernel(const int32_t *__restrict__ Ssub, const int32_t
                                  int rb, int64_t nb, int d, const T *__restrict__ KSsub, const float *__restrict__ Xsub,
                                  int32_t *__restrict__ S, int32_t *__restrict__ reff, T *__restrict__ KS,
                                  float *__restrict__ X) {
+    pdl_wait();
     const int a = blockIdx.x, u = blockIdx.y, R = bins * rb, dc = d + 1;
     int off = 0, b = -1, loc = 0;
     for (int bb = 0; bb < bins; ++bb) {
@@ -97,7 +99,8 @@ __global__ void bins_unpack_kernel(const int32_t *__restrict__ S, int units, int
 
 int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
                       cudaStream_t st) {
-    bins_stats_kernel<<<D.units() * bins, kBT, 0, st>>>(stats_u, nrm2, D.n / bins, D.d, bins, beta, stats_b);
+    launch_pdl(bins_stats_kernel, dim3(D.units() * bins), dim3(kBT), 0, st, stats_u, nrm2, D.n / bins, D.d, bins, beta,
+               stats_b);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -105,13 +108,11 @@ int launch_bins_pack(const Dims &D, int bins, int rb, const int32_t *Ssub, const
                      const float *Xsub, int32_t *S, int32_t *reff, void *KS, float *X, cudaStream_t st) {
     dim3 g(bins * rb, D.units());
     if (D.dtype == 0)
-        bins_pack_kernel<float><<<g, 64, 0, st>>>(Ssub, reff_sub, bins, rb, D.n / bins, D.d,
-                                                  static_cast<const float *>(KSsub), Xsub, S, reff,
-                                                  static_cast<float *>(KS), X);
+        launch_pdl(bins_pack_kernel<float>, g, dim3(64), 0, st, Ssub, reff_sub, bins, rb, D.n / bins, D.d,
+                   static_cast<const float *>(KSsub), Xsub, S, reff, static_cast<float *>(KS), X);
     else
-        bins_pack_kernel<__nv_bfloat16><<<g, 64, 0, st>>>(Ssub, reff_sub, bins, rb, D.n / bins, D.d,
-                                                          static_cast<const __nv_bfloat16 *>(KSsub), Xsub, S, reff,
-                                                          static_cast<__nv_bfloat16 *>(KS), X);
+        launch_pdl(bins_pack_kernel<__nv_bfloat16>, g, dim3(64), 0, st, Ssub, reff_sub, bins, rb, D.n / bins, D.d,
+                   static_cast<const __nv_bfloat16 *>(KSsub), Xsub, S, reff, static_cast<__nv_bfloat16 *>(KS), X);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
