@@ -229,9 +229,12 @@ int select_stage(const Plan &p, const wc_opts *o, double beta, double rq, const 
     const size_t Us = p.Ds.units();
     int32_t *Ssel = p.B > 1 ? w.Ssub : S;
     int32_t *Rsel = p.B > 1 ? w.reff_sub : r_eff;
-    if (cudaMemsetAsync(Ssel, 0xff, Us * p.rb * sizeof(int32_t), st) != cudaSuccess) return WC_ECUDA;
-    if (cudaMemsetAsync(L, 0, Us * (size_t)p.rb * p.rb * sizeof(double), st) != cudaSuccess) return WC_ECUDA;
-    int k = wc::launch_prologue(p.D, Q, K, V, rq, beta, w.pp, p.B > 1 ? w.stats_u : stats, w.sb.nrm2, vmin, vmax, st);
+    wc::ProloguePartials pp = w.pp;  // pass 1 also initialises S (-1) and L (0)
+    pp.fill_S = Ssel;
+    pp.nS = (int64_t)Us * p.rb;
+    pp.zero_L = L;
+    pp.nL = (int64_t)Us * p.rb * p.rb;
+    int k = wc::launch_prologue(p.D, Q, K, V, rq, beta, pp, p.B > 1 ? w.stats_u : stats, w.sb.nrm2, vmin, vmax, st);
     if (k < 0) return WC_ECUDA;
     *launches += k;
     if (p.B > 1) {

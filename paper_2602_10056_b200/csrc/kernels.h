@@ -24,6 +24,11 @@ struct ProloguePartials {
     double *rq2;     // [units][P]
     double *rk2;     // [units][P]
     int P;
+    // optional output initialisation folded into pass 1 (instead of two memsets): S <- -1, L <- 0
+    int32_t *fill_S = nullptr;
+    int64_t nS = 0;
+    double *zero_L = nullptr;
+    int64_t nL = 0;
 };
 
 int prologue_num_splits(const Dims &D);

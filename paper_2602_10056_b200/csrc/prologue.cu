@@ -22,8 +22,15 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
                                                       const T *__restrict__ V, int64_t n, int64_t mq, int d,
                                                       int P, int want_q, int want_v, double *colsum,
                                                       float *vmin, float *vmax, double *rq2,
-                                                      int64_t q_unit_stride_rows) {
+                                                      int64_t q_unit_stride_rows, int32_t *fill_S, int64_t nS,
+                                                      double *zero_L, int64_t nL) {
     pdl_wait();
+    if (nS > 0 || nL > 0) {  // the selection's outputs: S <- -1, L <- 0 (grid-stride, all blocks)
+        const int64_t nth = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+        const int64_t g0 = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+        for (int64_t e = g0; e < nS; e += nth) fill_S[e] = -1;
+        for (int64_t e = g0; e < nL; e += nth) zero_L[e] = 0.0;
+    }
     extern __shared__ double sm1[];
     const int p = blockIdx.x, u = blockIdx.y;
     const int CPR = d / 8, RG = kPT / CPR;
@@ -313,7 +320,7 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
     prologue_pass1<T><<<grid, kPT, smem, st>>>(static_cast<const T *>(Q), static_cast<const T *>(K),
                                                static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
-                                               (int64_t)D.group() * D.m);
+                                               (int64_t)D.group() * D.m, pp.fill_S, pp.nS, pp.zero_L, pp.nL);
     launch_kbar<T>(D, P, pp, stats, want_v ? vmin : nullptr, want_v ? vmax : nullptr, st);
     launch_pdl(prologue_pass2<T>, grid, dim3(kPT), 0, st, static_cast<const T *>(K), D.n, D.d, P,
                (const double *)stats, nrm2, pp.rk2);
@@ -330,7 +337,8 @@ int launch_vrange_t(const Dims &D, const void *V, ProloguePartials pp, void *vmi
     const size_t smem = (size_t)RG * D.d * (sizeof(double) + 2 * sizeof(float));
     dim3 grid(pp.P, units);
     prologue_pass1<T><<<grid, kPT, smem, st>>>(nullptr, static_cast<const T *>(V), static_cast<const T *>(V), D.n,
-                                               0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0);
+                                               0, D.d, pp.P, 0, 1, pp.colsum, pp.vmin, pp.vmax, pp.rq2, 0, nullptr, 0,
+                                               nullptr, 0);
     launch_kbar<T>(D, pp.P, pp, nullptr, vmin, vmax, st);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
@@ -346,7 +354,8 @@ int launch_pass1_t(const Dims &D, const void *Q, const void *K, const void *V, b
     dim3 grid(pp.P, D.units());
     prologue_pass1<T><<<grid, kPT, smem, st>>>(static_cast<const T *>(Q), static_cast<const T *>(K),
                                                static_cast<const T *>(V), D.n, mq, D.d, pp.P, want_q ? 1 : 0, 1,
-                                               pp.colsum, pp.vmin, pp.vmax, pp.rq2, (int64_t)D.group() * D.m);
+                                               pp.colsum, pp.vmin, pp.vmax, pp.rq2, (int64_t)D.group() * D.m, nullptr, 0,
+                                               nullptr, 0);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 template <typename T>
