@@ -49,29 +49,63 @@ __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restric
     }
 }
 
-// Block (row a, unit u) of the packed layout: row a comes from bin b, local row a - off_b, where
-// off_b = sum_{b' < b} r_eff_{b'}.  Ssub holds bin-local key indices.
+// Packed layout: row a of unit u comes from bin b, local row a - off_b, off_b = sum_{b' < b} r_eff_b'.
+// Block (row tile of kPackRows, unit u): the block first forms off_b for all bins of the unit (a
+// 128-thread exclusive scan in shared memory), then each warp places its rows by a binary search over
+// the offsets and copies them with its lanes.  Ssub holds bin-local key indices.
+constexpr int kPackRows = 32, kPackT = 128;
 template <typename T>
-__global__ void bins_pack_kernel(const int32_t *__restrict__ Ssub, const int32_t *__restrict__ reff_sub, int bins,
+__global__ void __launch_bounds__(kPackT) bins_pack_kernel(const int32_t *__restrict__ Ssub, const int32_t *__restrict__ reff_sub, int bins,
                                  int rb, int64_t nb, int d, const T *__restrict__ KSsub, const float *__restrict__ Xsub,
                                  int32_t *__restrict__ S, int32_t *__restrict__ reff, T *__restrict__ KS,
                                  float *__restrict__ X) {
     pdl_wait();
-    const int a = blockIdx.x, u = blockIdx.y, R = bins * rb, dc = d + 1;
-    int off = 0, b = -1, loc = 0;
-    for (int bb = 0; bb < bins; ++bb) {
-        const int re = reff_sub[u * bins + bb];
-        if (b < 0 && a < off + re) { b = bb; loc = a - off; }
-        off += re;
+    extern __shared__ int offs[];  // [bins + 1]: exclusive prefix of the bins' r_eff, offs[bins] = total
+    __shared__ int wsum[kPackT / 32];
+    const int u = blockIdx.y, R = bins * rb, dc = d + 1, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int per = (bins + kPackT - 1) / kPackT, b0 = tid * per, b1 = min(bins, b0 + per);
+    int v = 0;
+    for (int bb = b0; bb < b1; ++bb) v += reff_sub[u * bins + bb];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    if (a == 0 && threadIdx.x == 0 && reff) reff[u] = off;
-    const int64_t src = ((int64_t)u * bins + (b < 0 ? 0 : b)) * rb + loc;
-    if (threadIdx.x == 0 && S) S[(int64_t)u * R + a] = b < 0 ? -1 : (int32_t)(b * nb + Ssub[src]);
-    if (KS)
-        for (int j = threadIdx.x; j < d; j += blockDim.x)
-            KS[((int64_t)u * R + a) * d + j] = b < 0 ? from_f32<T>(0.f) : KSsub[src * d + j];
-    if (X)
-        for (int j = threadIdx.x; j < dc; j += blockDim.x) X[((int64_t)u * R + a) * dc + j] = b < 0 ? 0.f : Xsub[src * dc + j];
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int k = 0; k < w; ++k) base += wsum[k];
+    int run = base + incl - v;  // exclusive prefix at b0
+    for (int bb = b0; bb < b1; ++bb) {
+        offs[bb] = run;
+        run += reff_sub[u * bins + bb];
+    }
+    if (tid == kPackT - 1) offs[bins] = base + incl;
+    __syncthreads();
+    const int total = offs[bins];
+    if (blockIdx.x == 0 && tid == 0 && reff) reff[u] = total;
+    for (int rr = w; rr < kPackRows; rr += kPackT / 32) {
+        const int a = blockIdx.x * kPackRows + rr;
+        if (a >= R) break;
+        int b = -1, loc = 0;
+        if (a < total) {  // last bin with offs[bin] <= a (bins with r_eff = 0 share offsets: take the last)
+            int lo = 0, hi = bins - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (offs[mid] <= a) lo = mid; else hi = mid - 1;
+            }
+            b = lo;
+            loc = a - offs[b];
+        }
+        const int64_t src = ((int64_t)u * bins + (b < 0 ? 0 : b)) * rb + loc;
+        if (lane == 0 && S) S[(int64_t)u * R + a] = b < 0 ? -1 : (int32_t)(b * nb + Ssub[src]);
+        if (KS)
+            for (int j = lane; j < d; j += 32)
+                KS[((int64_t)u * R + a) * d + j] = b < 0 ? from_f32<T>(0.f) : KSsub[src * d + j];
+        if (X)
+            for (int j = lane; j < dc; j += 32) X[((int64_t)u * R + a) * dc + j] = b < 0 ? 0.f : Xsub[src * dc + j];
+    }
 }
 
 // One warp per unit: split the packed S (bin order) back into bin-local indices per sub-unit.
@@ -106,13 +140,14 @@ int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_
 
 int launch_bins_pack(const Dims &D, int bins, int rb, const int32_t *Ssub, const int32_t *reff_sub, const void *KSsub,
                      const float *Xsub, int32_t *S, int32_t *reff, void *KS, float *X, cudaStream_t st) {
-    dim3 g(bins * rb, D.units());
+    dim3 g((bins * rb + kPackRows - 1) / kPackRows, D.units());
+    const size_t smem = (size_t)(bins + 1) * sizeof(int);
     if (D.dtype == 0)
-        launch_pdl(bins_pack_kernel<float>, g, dim3(64), 0, st, Ssub, reff_sub, bins, rb, D.n / bins, D.d,
+        launch_pdl(bins_pack_kernel<float>, g, dim3(kPackT), smem, st, Ssub, reff_sub, bins, rb, D.n / bins, D.d,
                    static_cast<const float *>(KSsub), Xsub, S, reff, static_cast<float *>(KS), X);
     else
-        launch_pdl(bins_pack_kernel<__nv_bfloat16>, g, dim3(64), 0, st, Ssub, reff_sub, bins, rb, D.n / bins, D.d,
-                   static_cast<const __nv_bfloat16 *>(KSsub), Xsub, S, reff, static_cast<__nv_bfloat16 *>(KS), X);
+        launch_pdl(bins_pack_kernel<__nv_bfloat16>, g, dim3(kPackT), smem, st, Ssub, reff_sub, bins, rb, D.n / bins,
+                   D.d, static_cast<const __nv_bfloat16 *>(KSsub), Xsub, S, reff, static_cast<__nv_bfloat16 *>(KS), X);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
