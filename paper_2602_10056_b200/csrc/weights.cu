@@ -679,11 +679,63 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
+// r <= 32 (e.g. binned sub-units): the whole solve is one diagonal block, X = Dinv^T (Dinv Y); one
+// CTA per unit does both 32 x 32 products for all d + 1 columns out of shared memory.
+template <int D>
+__global__ void __launch_bounds__(256) weights_solve_small_kernel(const double *__restrict__ Y,
+                                                                  const double *__restrict__ Dinv,
+                                                                  const int32_t *__restrict__ r_eff, int r,
+                                                                  float *__restrict__ X) {
+    pdl_wait();
+    constexpr int DC = D + 1;
+    __shared__ double Di[kPB][kPB + 1];
+    __shared__ double Z[kPB][DC];
+    const int u = blockIdx.x, tid = threadIdx.x;
+    const int q = r_eff[u];
+    const double *Du = Dinv + (int64_t)u * kPB * kPB;  // one block per unit (r <= 32)
+    for (int e = tid; e < kPB * kPB; e += 256) Di[e / kPB][e % kPB] = q > 0 ? Du[e] : 0.0;
+    for (int e = tid; e < kPB * DC; e += 256) {
+        const int a = e / DC, c = e % DC;
+        Z[a][c] = a < q ? Y[((int64_t)u * r + a) * DC + c] : 0.0;
+    }
+    __syncthreads();
+    double t[(kPB * DC + 255) / 256];
+#pragma unroll
+    for (int k = 0; k < (kPB * DC + 255) / 256; ++k) {  // z = Dinv y (lower triangular)
+        const int e = tid + 256 * k;
+        double acc = 0.0;
+        if (e < kPB * DC) {
+            const int a = e / DC, c = e % DC;
+            for (int j = 0; j <= a; ++j) acc = fma(Di[a][j], Z[j][c], acc);
+        }
+        t[k] = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < (kPB * DC + 255) / 256; ++k) {
+        const int e = tid + 256 * k;
+        if (e < kPB * DC) Z[e / DC][e % DC] = t[k];
+    }
+    __syncthreads();
+    float *Xu = X + (int64_t)u * r * DC;
+    for (int e = tid; e < r * DC; e += 256) {  // x = Dinv^T z (upper triangular)
+        const int a = e / DC, c = e % DC;
+        double acc = 0.0;
+        for (int j = a; j < kPB; ++j) acc = fma(Di[j][a], Z[j][c], acc);
+        Xu[e] = a < q ? (float)acc : 0.f;
+    }
+}
+
 template <int D>
 int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
                    double *Dinv, cudaStream_t st, bool dinv_done = false) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
     if (!dinv_done) launch_pdl(weights_dinv_kernel, dim3(nbl, Dm.units()), dim3(32), 0, st, L, r_eff, Dm.r, Dinv);
+    if (Dm.r <= kPB) {  // one diagonal block: both triangular products in one CTA per unit
+        launch_pdl(weights_solve_small_kernel<D>, dim3(Dm.units()), dim3(256), 0, st, Yfull, (const double *)Dinv,
+                   r_eff, Dm.r, X);
+        return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
+    }
     // few units: 2 columns per CTA (more CTAs on the panel chain); many units: 8 per CTA
     const bool wide = (int64_t)Dm.units() * ((D + 1 + 1) / 2) <= 4 * 148;
     const int lb = std::min(kCBs, Dm.r) + 1;
