@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restric
 // Block (row tile of kPackRows, unit u): the block first forms off_b for all bins of the unit (a
 // 128-thread exclusive scan in shared memory), then each warp places its rows by a binary search over
 // the offsets and copies them with its lanes.  Ssub holds bin-local key indices.
-constexpr int kPackRows = 32, kPackT = 128;
+constexpr int kPackRows = 8, kPackT = 128;
 template <typename T>
 __global__ void __launch_bounds__(kPackT) bins_pack_kernel(const int32_t *__restrict__ Ssub, const int32_t *__restrict__ reff_sub, int bins,
                                  int rb, int64_t nb, int d, const T *__restrict__ KSsub, const float *__restrict__ Xsub,

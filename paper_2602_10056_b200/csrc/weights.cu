@@ -731,7 +731,7 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
                    double *Dinv, cudaStream_t st, bool dinv_done = false) {
     const int nbl = (Dm.r + kPB - 1) / kPB;
     if (!dinv_done) launch_pdl(weights_dinv_kernel, dim3(nbl, Dm.units()), dim3(32), 0, st, L, r_eff, Dm.r, Dinv);
-    if (Dm.r <= kPB) {  // one diagonal block: both triangular products in one CTA per unit
+    if (Dm.r <= kPB && Dm.units() >= 148) {  // many small units: both products in one CTA per unit
         launch_pdl(weights_solve_small_kernel<D>, dim3(Dm.units()), dim3(256), 0, st, Yfull, (const double *)Dinv,
                    r_eff, Dm.r, X);
         return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
