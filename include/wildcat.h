@@ -101,11 +101,16 @@ typedef struct wc_opts {
     uint32_t block;    /* pivot selection: 0 or 1 = sequential RPCholesky, Alg 1;
                           2..WC_MAX_BLOCK = blocked ("accelerated") RPCholesky with b = block
                           candidates per block (P:678 future work; reading Z22): same pivot LAW
-                          as Alg 1, a different pivot sequence for a given seed.  Blocked needs
-                          r <= 1024 (shared-memory plan), else WC_EUNSUPPORTED. */
+                          as Alg 1, a different pivot sequence for a given seed. */
 } wc_opts;
 
 #define WC_MAX_BLOCK 16
+
+/* Largest coreset size per selection problem (r, or rb = ceil(r/B) per bin) for wildcat_select /
+ * wildcat_weights / wildcat_forward / wildcat_compress_kv / wildcat_forward_nshard: the r x r solve
+ * and the blocked selection are planned for at most this many pivots; larger -> WC_EUNSUPPORTED
+ * (before any launch).  wildcat_attend itself streams any number of coreset rows (decode caches). */
+#define WC_MAX_R 1024
 
 /* Bytes of workspace the op needs for this shape (0 on invalid shape). */
 size_t wc_workspace_bytes(const wc_shape *shape, int op);

@@ -71,14 +71,33 @@ class Cache:
 _ws_cache: dict = {}
 
 
-def _workspace(shape, op, device):
-    nb = B.workspace_bytes(shape, op)
-    key = (device, op)
+def _stream_of(stream):
+    return torch.cuda.current_stream() if stream is None else stream
+
+
+def _workspace(shape, op, device, stream=None, nbytes=None):
+    """Scratch for one call, cached per (device, op, stream): calls on one stream are serialised by
+    the stream, so they may share it; another stream gets its own buffer.  A buffer allocated while a
+    different stream is current is tied to the launching stream with record_stream, so the caching
+    allocator never hands its memory out while the library's kernels still use it."""
+    nb = B.workspace_bytes(shape, op) if nbytes is None else nbytes
+    st = _stream_of(stream)
+    key = (device, op, st.cuda_stream)
     t = _ws_cache.get(key)
     if t is None or t.numel() < nb:
         t = torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
         _ws_cache[key] = t
+        _on_stream(st, t)
     return t
+
+
+def _on_stream(stream, *ts):
+    """Outputs allocated on the current stream but written on `stream`: record the use."""
+    if stream is None or stream == torch.cuda.current_stream():
+        return
+    for t in ts:
+        if t is not None:
+            t.record_stream(stream)
 
 
 def select(Q, K, r, seed=0, beta=None, rq=None, block=1, bins=1, stream=None) -> Selection:
@@ -95,7 +114,8 @@ def select(Q, K, r, seed=0, beta=None, rq=None, block=1, bins=1, stream=None) ->
     reff = torch.empty(units, dtype=torch.int32, device=dev)
     L = torch.empty(units * bins, rb, rb, dtype=torch.float64, device=dev)
     stats = torch.empty(units * bins, STATS_STRIDE(shape.d), dtype=torch.float64, device=dev)
-    ws = _workspace(shape, B.WC_OP_SELECT, dev)
+    ws = _workspace(shape, B.WC_OP_SELECT, dev, stream)
+    _on_stream(stream, S, reff, L, stats)
     B.wildcat_select(shape, opts, Q, K, S, reff, L, stats, ws, stream)
     return Selection(S, reff, L, stats, shape, opts)
 
@@ -111,7 +131,8 @@ def weights(K, V, sel: Selection, stream=None) -> Cache:
     X = torch.empty(units, R, d + 1, dtype=torch.float32, device=dev)
     vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
     vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
-    ws = _workspace(shape, B.WC_OP_WEIGHTS, dev)
+    ws = _workspace(shape, B.WC_OP_WEIGHTS, dev, stream)
+    _on_stream(stream, KS, X, vmin, vmax)
     B.wildcat_weights(shape, sel.opts, K, V, sel.S, sel.r_eff, sel.L, sel.stats, KS, X, vmin, vmax, ws, stream)
     return Cache(KS, X, vmin, vmax, sel.r_eff, shape.heads_kv, sel.opts, shape)
 
@@ -132,7 +153,8 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
                      seed=cache.opts.seed,
                      flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), block=0)
     O = torch.empty_like(Q)
-    ws = _workspace(shape, B.WC_OP_ATTEND, Q.device) if B.workspace_bytes(shape, B.WC_OP_ATTEND) else None
+    ws = _workspace(shape, B.WC_OP_ATTEND, Q.device, stream) if B.workspace_bytes(shape, B.WC_OP_ATTEND) else None
+    _on_stream(stream, O)
     B.wildcat_attend(shape, opts, Q, cache.KS, cache.X, cache.r_eff, cache.vmin, cache.vmax, O, ws, stream)
     return O
 
@@ -147,7 +169,9 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None,
     shape = B.make_shape(Q, K, r, bins=bins)
     opts = B.make_opts(seed, beta, rq, clip, block=block)
     O = torch.empty_like(Q) if out is None else out
-    ws = _workspace(shape, B.WC_OP_FORWARD, K.device)
+    ws = _workspace(shape, B.WC_OP_FORWARD, K.device, stream)
+    if out is None:
+        _on_stream(stream, O)
     B.wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O
 
@@ -182,12 +206,8 @@ def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None
     ceff = torch.empty(units, dtype=torch.int32, device=dev)
     vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
     vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
-    nb = B.kv_workspace_bytes(shape, keep_first, keep_last)
-    key = (dev, "kv")
-    ws = _ws_cache.get(key)
-    if ws is None or ws.numel() < nb:
-        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
-        _ws_cache[key] = ws
+    ws = _workspace(shape, "kv", dev, stream, nbytes=B.kv_workspace_bytes(shape, keep_first, keep_last))
+    _on_stream(stream, KC, XC, ceff, vmin, vmax)
     B.wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, ceff, vmin, vmax, S, ws, stream)
     cshape = B.wc_shape(batch=b, heads_q=shape.heads_q, heads_kv=hkv, d=d, r=C, bins=1, dtype=shape.dtype,
                         reserved=0, m=0, n=n)
@@ -230,7 +250,12 @@ class HostForward:
         self.ev_kq = torch.cuda.Event()
         self.ev_v = torch.cuda.Event()
 
-    def __call__(self, Qh, Kh, Vh):
+    def __call__(self, Qh, Kh, Vh, out=None):
+        """Returns O on the host.  With out=None a fresh tensor (a copy of the persistent pinned
+        buffer, so earlier results are never overwritten); with out= (a host tensor of Q's shape and
+        dtype, ideally pinned) O is written there directly and `out` is returned."""
+        if out is not None and (out.shape != self.Oh.shape or out.dtype != self.Oh.dtype or out.is_cuda):
+            raise WildcatError("forward_host: out must be a host tensor of Q's shape and dtype")
         sm, sv = self.s_main, self.s_v
         with torch.cuda.stream(sm):
             self.Kd.copy_(Kh, non_blocking=True)
@@ -246,24 +271,26 @@ class HostForward:
                           self.X, self.vmin, self.vmax, self.ws_w, sm)
         B.wildcat_attend(self.shape, self.opts, self.Qd, self.KS, self.X, self.reff, self.vmin, self.vmax, self.Od,
                          self.ws_a, sm)
+        dst = self.Oh if out is None else out
         with torch.cuda.stream(sm):
-            self.Oh.copy_(self.Od, non_blocking=True)
+            dst.copy_(self.Od, non_blocking=True)
         sm.synchronize()
-        return self.Oh
+        return self.Oh.clone() if out is None else out
 
 
 _host_cache: dict = {}
 
 
-def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, bins=1, stream=None):
-    """End-to-end call with host (CPU) buffers: H2D copies, the CUDA path, D2H copy of O (pinned).
-    Device buffers persist per (shapes, options); see HostForward."""
+def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, bins=1, out=None):
+    """End-to-end call with host (CPU) buffers: H2D copies, the CUDA path, D2H copy of O (into `out`
+    if given, else into a new host tensor).  Device buffers persist per (shapes, options); see
+    HostForward.  Calls with the same key share those device buffers: serialise them."""
     key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), int(bins), str(device))
     hf = _host_cache.get(key)
     if hf is None:
         hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, bins=bins, device=device)
         _host_cache[key] = hf
-    return hf(Q, K, V)
+    return hf(Q, K, V, out=out)
 
 
 # --------------------------------------------------------------------------- n-sharded (PAR3)
@@ -321,6 +348,8 @@ def forward_nshard(comm: NshardComm, Q, K, V, r, n_global, n_offset, seed=0, bet
     shape = B.make_shape(Q, K, r)
     opts = B.make_opts(seed, beta, rq, clip)
     O = torch.empty_like(Q) if out is None else out
-    ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device)
+    ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device, stream)
+    if out is None:
+        _on_stream(stream, O)
     B.wildcat_forward_nshard(comm.handle, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream)
     return O

@@ -141,13 +141,80 @@ def alloc_workspace(shape: wc_shape, op: int, device) -> torch.Tensor:
     return torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
 
 
+# ---- argument checks (before any ctypes call): the C ABI takes raw pointers, so a tensor that
+# disagrees with the shape would be read or written out of bounds.  Every wrapper checks dtype,
+# device, contiguity and size of each tensor against the wc_shape it passes.
+_TDT = {WC_F32: torch.float32, WC_BF16: torch.bfloat16}
+
+
+def _need(t, name, dtype, numel, device=None, exact=False, optional=False):
+    if t is None:
+        if optional:
+            return None
+        raise WildcatError(f"{name}: tensor required")
+    if not isinstance(t, torch.Tensor):
+        raise WildcatError(f"{name}: expected a torch.Tensor")
+    if not t.is_cuda:
+        raise WildcatError(f"{name}: must be a CUDA tensor (no CPU fallback)")
+    if device is not None and t.device != device:
+        raise WildcatError(f"{name}: on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise WildcatError(f"{name}: must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise WildcatError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if (t.numel() != numel) if exact else (t.numel() < numel):
+        raise WildcatError(f"{name}: {t.numel()} elements, expected {'' if exact else '>= '}{numel}")
+    return t.device
+
+
+def _dims(shape):
+    units = shape.batch * shape.heads_kv
+    rb, R = coreset_rows(shape.n, shape.r, shape.bins)
+    return units, rb, R, shape.d, _TDT.get(shape.dtype)
+
+
+def _check_sel_out(shape, dev, S, r_eff, L, stats, optional_S=False):
+    units, rb, R, d, _ = _dims(shape)
+    _need(S, "S", torch.int32, units * R, dev, optional=optional_S)
+    _need(r_eff, "r_eff", torch.int32, units, dev, optional=optional_S)
+    if L is not None or stats is not None:
+        _need(L, "L", torch.float64, units * shape.bins * rb * rb, dev)
+        _need(stats, "stats", torch.float64, units * shape.bins * (16 + d), dev)
+
+
+def _check_qkv(shape, Q, K, V=None, O=None, q_optional=False):
+    units, _, _, d, tdt = _dims(shape)
+    dev = _need(K, "K", tdt, units * shape.n * d, exact=True)
+    _need(V, "V", tdt, units * shape.n * d, dev, exact=True, optional=V is None)
+    nq = shape.batch * shape.heads_q * shape.m * d
+    _need(Q, "Q", tdt, nq, dev, exact=True, optional=q_optional or nq == 0)
+    _need(O, "O", tdt, nq, dev, exact=True, optional=nq == 0)
+    return dev
+
+
+def _check_ws(ws, dev, op_bytes):
+    if op_bytes:
+        _need(ws, "workspace", torch.uint8, op_bytes, dev)
+
+
 def wildcat_select(shape, opts, Q, K, S, r_eff, L, stats, ws, stream=None):
+    dev = _check_qkv(shape, Q, K, q_optional=opts.rq >= 0)
+    _check_sel_out(shape, dev, S, r_eff, L, stats)
+    _check_ws(ws, dev, workspace_bytes(shape, WC_OP_SELECT))
     rc = lib().wildcat_select(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(S), _ptr(r_eff),
                               _ptr(L), _ptr(stats), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "wildcat_select")
 
 
 def wildcat_weights(shape, opts, K, V, S, r_eff, L, stats, KS, X, vmin, vmax, ws, stream=None):
+    units, rb, R, d, tdt = _dims(shape)
+    dev = _check_qkv(shape, None, K, V, q_optional=True)
+    _check_sel_out(shape, dev, S, r_eff, L, stats)
+    _need(KS, "KS", tdt, units * R * d, dev)
+    _need(X, "X", torch.float32, units * R * (d + 1), dev)
+    _need(vmin, "vmin", tdt, units * d, dev)
+    _need(vmax, "vmax", tdt, units * d, dev)
+    _check_ws(ws, dev, workspace_bytes(shape, WC_OP_WEIGHTS))
     rc = lib().wildcat_weights(ctypes.byref(shape), ctypes.byref(opts), _ptr(K), _ptr(V), _ptr(S), _ptr(r_eff),
                                _ptr(L), _ptr(stats), _ptr(KS), _ptr(X), _ptr(vmin), _ptr(vmax), _ptr(ws),
                                ws.numel(), _stream(stream))
@@ -155,6 +222,16 @@ def wildcat_weights(shape, opts, K, V, S, r_eff, L, stats, KS, X, vmin, vmax, ws
 
 
 def wildcat_attend(shape, opts, Q, KS, X, r_eff, vmin, vmax, O, ws=None, stream=None):
+    units, _, R, d, tdt = _dims(shape)
+    nq = shape.batch * shape.heads_q * shape.m * d
+    dev = _need(KS, "KS", tdt, units * R * d)
+    _need(Q, "Q", tdt, nq, dev, exact=True, optional=nq == 0)
+    _need(O, "O", tdt, nq, dev, exact=True, optional=nq == 0)
+    _need(X, "X", torch.float32, units * R * (d + 1), dev)
+    _need(r_eff, "r_eff", torch.int32, units, dev)
+    _need(vmin, "vmin", tdt, units * d, dev)
+    _need(vmax, "vmax", tdt, units * d, dev)
+    _check_ws(ws, dev, workspace_bytes(shape, WC_OP_ATTEND))
     rc = lib().wildcat_attend(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(KS), _ptr(X), _ptr(r_eff),
                               _ptr(vmin), _ptr(vmax), _ptr(O), _ptr(ws), 0 if ws is None else ws.numel(),
                               _stream(stream))
@@ -162,6 +239,9 @@ def wildcat_attend(shape, opts, Q, KS, X, r_eff, vmin, vmax, O, ws=None, stream=
 
 
 def wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream=None):
+    dev = _check_qkv(shape, Q, K, V, O)
+    _check_sel_out(shape, dev, S, r_eff, None, None, optional_S=True)
+    _check_ws(ws, dev, workspace_bytes(shape, WC_OP_FORWARD))
     rc = lib().wildcat_forward(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
                                _ptr(S), _ptr(r_eff), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "wildcat_forward")
@@ -176,6 +256,18 @@ def kv_workspace_bytes(shape, keep_first, keep_last) -> int:
 
 
 def wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, c_eff, vmin, vmax, S, ws, stream=None):
+    units, _, _, d, tdt = _dims(shape)
+    C = kv_capacity(shape, keep_first, keep_last)
+    if C == 0:
+        raise WildcatError("wildcat_compress_kv: invalid split (keep_first / keep_last / r / bins)")
+    dev = _check_qkv(shape, Q, K, V, q_optional=True)
+    _need(KC, "KC", tdt, units * C * d, dev)
+    _need(XC, "XC", torch.float32, units * C * (d + 1), dev)
+    _need(c_eff, "c_eff", torch.int32, units, dev)
+    _need(vmin, "vmin", tdt, units * d, dev)
+    _need(vmax, "vmax", tdt, units * d, dev)
+    _need(S, "S", torch.int32, units * (C - int(keep_first) - int(keep_last)), dev, optional=True)
+    _check_ws(ws, dev, kv_workspace_bytes(shape, keep_first, keep_last))
     rc = lib().wildcat_compress_kv(ctypes.byref(shape), ctypes.byref(opts), int(keep_first), int(keep_last), _ptr(Q),
                                    _ptr(K), _ptr(V), _ptr(KC), _ptr(XC), _ptr(c_eff), _ptr(vmin), _ptr(vmax),
                                    _ptr(S), _ptr(ws), ws.numel(), _stream(stream))
@@ -230,6 +322,10 @@ def wc_comm_destroy(h) -> None:
 
 
 def wildcat_forward_nshard(comm, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream=None):
+    dev = _check_qkv(shape, Q, K, V, O)
+    _need(S, "S", torch.int32, shape.r, dev, optional=True)
+    _need(r_eff, "r_eff", torch.int32, 1, dev, optional=True)
+    _check_ws(ws, dev, workspace_bytes(shape, WC_OP_FORWARD_NSHARD))
     rc = lib().wildcat_forward_nshard(comm, ctypes.byref(shape), int(n_global), int(n_offset), ctypes.byref(opts),
                                       _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(r_eff), _ptr(ws),
                                       ws.numel(), _stream(stream))

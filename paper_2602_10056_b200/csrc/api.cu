@@ -11,6 +11,7 @@
 #include "kernels.h"
 
 static_assert(WC_STATS_HEAD == wc::kStatsHead, "stats layout of include/wildcat.h and the kernels differ");
+static_assert(WC_MAX_R == wc::kMaxR, "WC_MAX_R of include/wildcat.h and the kernels' plan differ");
 
 namespace {
 
@@ -117,7 +118,7 @@ int run_select(const wc::Dims &D, const wc_opts *o, const void *K, double *stats
 int check_opts(const wc_opts *o, const wc_shape *s) {
     if (!o) return WC_EINVAL;
     if (o->block > (uint32_t)WC_MAX_BLOCK) return WC_EINVAL;
-    if (o->block >= 2 && plan_of(s).rb > 1024) return WC_EUNSUPPORTED;
+    if (plan_of(s).rb > WC_MAX_R) return WC_EUNSUPPORTED;  // solve / blocked plan (every selection path)
     return WC_OK;
 }
 
@@ -400,6 +401,7 @@ int wildcat_weights(const wc_shape *s, const wc_opts *o, const void *K, const vo
     if (rc) return rc;
     (void)o;
     if (!K || !V || !S || !r_eff || !L || !stats || !KS || !X || !vmin || !vmax) return WC_EINVAL;
+    if (plan_of(s).rb > WC_MAX_R) return WC_EUNSUPPORTED;  // the solve's plan
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_WEIGHTS)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Plan p = plan_of(s);
@@ -563,7 +565,8 @@ int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int6
     if (rc) return rc;
     if (!comm || !o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
     if (s->batch != 1 || s->heads_kv != 1) return WC_EUNSUPPORTED;
-    if (o->block >= 2 || s->bins != 1) return WC_EUNSUPPORTED;  // blocked / binned selection is single-GPU  // blocked selection is single-GPU in this build
+    if (o->block >= 2 || s->bins != 1) return WC_EUNSUPPORTED;  // blocked / binned selection is single-GPU
+    if (s->r > WC_MAX_R) return WC_EUNSUPPORTED;                  // the solve's plan
     if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;
     const double rq = rq_of(o);

@@ -8,6 +8,7 @@ namespace wc {
 // Per-unit stats record: tau, g, mstar, R_K, R_Q, T0, nblocks, ncand, Fread, 0..., kbar[d]
 // (WC_STATS_STRIDE(d) = kStatsHead + d in include/wildcat.h).
 constexpr int kStatsHead = 16;
+constexpr int kMaxR = 1024;  // largest r (or rb per bin) of a selection problem: the solve / blocked plans (WC_MAX_R)
 
 struct Dims {
     int batch, hq, hkv, d, r, dtype;

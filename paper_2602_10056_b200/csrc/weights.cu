@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) weights_reduce_dinv_kernel(const float *_
 // steps are in flight (cp.async, zero-filled out of range, transposes done by the copy placement)
 // while the current step computes: the chain carries shared-memory latency only.
 constexpr int kSolveNS = 4;                              // operand ring stages
-constexpr int kSolveMaxSteps = 2 * (1024 / kPB) * (1024 / kCBs + 1);
+constexpr int kSolveMaxSteps = 2 * (kMaxR / kPB) * (kMaxR / kCBs + 1);  // r <= kMaxR is checked at the ABI
 
 // 8-byte async copy, zero-filled (no global read) when !ok; `safe` is any valid global address
 __device__ __forceinline__ void cp_async8_zfill(double *dst, const double *src, bool ok, const double *safe) {

@@ -133,22 +133,44 @@ def test_block_option_validation(L):
     s = _shape()
     o = B.make_opts(block=17)  # > WC_MAX_BLOCK
     assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -1
-    big = _shape(n=5000, r=1025)
-    o = B.make_opts(block=8)  # blocked selection needs r <= 1024
-    assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -7
     assert L.wc_version() >= 101
 
 
-def test_binned_workspace_and_layout(L):
+@pytest.mark.parametrize("block", [1, 8])
+def test_r_above_max_r_is_unsupported_on_every_path(L, block):
+    # WC_MAX_R = 1024: the r x r solve and the blocked plan are sized for it; larger r (or rb per bin)
+    # must be refused before any launch on every selection path, sequential included
     from paper_2602_10056_b200 import _binding as B
 
-    # R = B * min(ceil(r/B), n/B) coreset rows per unit (reading Z13)
-    assert B.coreset_rows(4096, 128, 8) == (16, 128)
-    assert B.coreset_rows(1200, 50, 3) == (17, 51)
-    assert B.coreset_rows(64, 64, 8) == (8, 64)
-    s1 = _shape(n=4096, r=128, bins=1)
-    s8 = _shape(n=4096, r=128, bins=8)
-    for op in (0, 1, 3):
-        assert L.wc_workspace_bytes(ctypes.byref(s8), op) > 0
-    # bins shrink the per-unit F state (n r fp64 -> n r / B)
-    assert L.wc_workspace_bytes(ctypes.byref(s8), 0) < L.wc_workspace_bytes(ctypes.byref(s1), 0)
+    d = ctypes.c_void_p(0x1000)
+    o = B.make_opts(block=block)
+    for r in (1025, 2048):
+        big = _shape(n=5000, r=r)
+        assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -7
+        assert L.wildcat_select(ctypes.byref(big), ctypes.byref(o), d, d, d, d, d, d, d, 1 << 40, None) == -7
+        assert L.wildcat_weights(ctypes.byref(big), ctypes.byref(o), d, d, d, d, d, d, d, d, d, d, d, 1 << 40,
+                                 None) == -7
+        assert L.wildcat_compress_kv(ctypes.byref(big), ctypes.byref(o), 32, 32, d, d, d, d, d, d, d, d, None, d,
+                                     1 << 40, None) == -7
+        assert L.wildcat_forward_nshard(d, ctypes.byref(big), 5000, 0, ctypes.byref(o), d, d, d, d, None, None, d,
+                                        1 << 40, None) == -7
+    # with bins, the limit applies per bin: r = 2048 over 2 bins is rb = 1024 (accepted by the check)
+    ok = _shape(n=5000, r=2048, bins=2)
+    assert L.wc_workspace_bytes(ctypes.byref(ok), 3) > 0
+
+
+def test_binding_refuses_cpu_tensors():
+    # the ctypes wrappers refuse tensors that are not CUDA before any C call (no CPU fallback);
+    # the shape / dtype / size rules are exercised on the GPU in tests/test_gpu_parity.py
+    import torch
+
+    from paper_2602_10056_b200 import _binding as B
+
+    s = _shape(n=100, r=8, m=16)
+    K = torch.zeros(1, 1, 100, 64, dtype=torch.bfloat16)
+    with pytest.raises(B.WildcatError, match="CUDA"):
+        B._check_qkv(s, K, K)
+    with pytest.raises(B.WildcatError, match="torch.Tensor"):
+        B._need(object(), "X", torch.float32, 1)
+    with pytest.raises(B.WildcatError, match="required"):
+        B._need(None, "X", torch.float32, 1)

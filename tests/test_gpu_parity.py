@@ -177,3 +177,33 @@ def test_forward_host_matches_device_forward(block):
     for _ in range(2):  # second call reuses the cached device buffers
         Oh = wc.forward_host(Qh, Kh, Vh, 64, seed=12, block=block)
         assert torch.equal(Oh, Od.cpu())
+
+
+@pytest.mark.gpu
+def test_binding_rejects_mismatched_tensors():
+    import paper_2602_10056_b200 as wc
+    # the C ABI takes raw pointers, so the wrappers must refuse tensors that disagree
+    # with the shape (dtype, batch / d, sizes of S / r_eff / out) before any launch
+    dev = torch.device("cuda:0")
+    Q, K, V = (x.to(dev) for x in qkv(1, 2, 1, 64, 128, 64, "bf16"))
+    with pytest.raises(wc.WildcatError, match="dtype"):
+        wc.forward(Q.float(), K, V, 8)
+    with pytest.raises(wc.WildcatError, match="elements"):
+        wc.forward(torch.cat([Q, Q]), K, V, 8)  # Q batch larger than K's
+    with pytest.raises(wc.WildcatError, match="elements"):
+        wc.forward(Q, K, V[:, :, :100].contiguous(), 8)
+    with pytest.raises(wc.WildcatError, match="S"):
+        wc.forward(Q, K, V, 8, S=torch.empty(1, 4, dtype=torch.int32, device=dev))
+    with pytest.raises(wc.WildcatError, match="contiguous"):
+        B = wc._binding
+        sh = B.make_shape(Q, K, 8)
+        B.wildcat_forward(sh, B.make_opts(), Q, K, V, torch.empty_like(Q).transpose(2, 3), None, None,
+                          wc._workspace(sh, B.WC_OP_FORWARD, dev))
+    sel = wc.select(Q, K, 8)
+    cache = wc.weights(K, V, sel)
+    with pytest.raises(wc.WildcatError, match="dtype"):
+        wc.attend(Q.float(), cache)
+    # a correct call still runs
+    O = wc.forward(Q, K, V, 8)
+    torch.cuda.synchronize()
+    assert torch.isfinite(O.float()).all()

@@ -162,3 +162,23 @@ def test_recentring_invariance_of_selection(orc):
     b = orc.select(K + 0.75, k2, s2["g"], s2["mstar"], r, seed=3)
     assert s1["rk"] == pytest.approx(s2["rk"], rel=1e-12)
     assert np.array_equal(a["S"], b["S"])
+
+
+def test_kbar_is_the_row_mean(orc):
+    # Alg 2 "Recenter keys": kbar = (1/n) sum_l k_l, pinned directly (not only through
+    # shift invariance): dyadic keys with n a power of two make the mean exact in fp64, so any other
+    # centre (median, midrange, a dropped row, a 1/(n-1) scale) fails bit for bit.
+    rng = np.random.default_rng(5)
+    n, d = 256, 16
+    K = rng.integers(-64, 64, size=(n, d)).astype(np.float64) / 8.0
+    K[7] += 40.0  # an outlier row moves the mean but not the median
+    kbar, st = orc.prologue(K, K[:10])
+    assert np.array_equal(kbar, K.sum(0) / n)
+    # R_K = max_l ||k_l - kbar||, R_Q = max_i ||q_i||, against numpy on the same data
+    assert st["rk"] == pytest.approx(np.sqrt(((K - K.mean(0)) ** 2).sum(1)).max(), rel=1e-14)
+    assert st["rq"] == pytest.approx(np.sqrt((K[:10] ** 2).sum(1)).max(), rel=1e-14)
+    # Gaussian keys: within a few ulps of the compensated mean
+    G = rng.standard_normal((1000, 8))
+    kg, _ = orc.prologue(G, G[:5])
+    exact = np.array([math.fsum(G[:, j]) / 1000 for j in range(8)])
+    assert np.abs(kg - exact).max() <= 1e-15 * np.abs(G).max()
