@@ -182,13 +182,13 @@ def _check_sel_out(shape, dev, S, r_eff, L, stats, optional_S=False):
         _need(stats, "stats", torch.float64, units * shape.bins * (16 + d), dev)
 
 
-def _check_qkv(shape, Q, K, V=None, O=None, q_optional=False):
+def _check_qkv(shape, Q, K, V=None, O=None, q_optional=False, need_v=False, need_o=False):
     units, _, _, d, tdt = _dims(shape)
     dev = _need(K, "K", tdt, units * shape.n * d, exact=True)
-    _need(V, "V", tdt, units * shape.n * d, dev, exact=True, optional=V is None)
+    _need(V, "V", tdt, units * shape.n * d, dev, exact=True, optional=not need_v)
     nq = shape.batch * shape.heads_q * shape.m * d
     _need(Q, "Q", tdt, nq, dev, exact=True, optional=q_optional or nq == 0)
-    _need(O, "O", tdt, nq, dev, exact=True, optional=nq == 0)
+    _need(O, "O", tdt, nq, dev, exact=True, optional=not need_o or nq == 0)
     return dev
 
 
@@ -208,7 +208,7 @@ def wildcat_select(shape, opts, Q, K, S, r_eff, L, stats, ws, stream=None):
 
 def wildcat_weights(shape, opts, K, V, S, r_eff, L, stats, KS, X, vmin, vmax, ws, stream=None):
     units, rb, R, d, tdt = _dims(shape)
-    dev = _check_qkv(shape, None, K, V, q_optional=True)
+    dev = _check_qkv(shape, None, K, V, q_optional=True, need_v=True)
     _check_sel_out(shape, dev, S, r_eff, L, stats)
     _need(KS, "KS", tdt, units * R * d, dev)
     _need(X, "X", torch.float32, units * R * (d + 1), dev)
@@ -239,7 +239,7 @@ def wildcat_attend(shape, opts, Q, KS, X, r_eff, vmin, vmax, O, ws=None, stream=
 
 
 def wildcat_forward(shape, opts, Q, K, V, O, S, r_eff, ws, stream=None):
-    dev = _check_qkv(shape, Q, K, V, O)
+    dev = _check_qkv(shape, Q, K, V, O, need_v=True, need_o=True)
     _check_sel_out(shape, dev, S, r_eff, None, None, optional_S=True)
     _check_ws(ws, dev, workspace_bytes(shape, WC_OP_FORWARD))
     rc = lib().wildcat_forward(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(K), _ptr(V), _ptr(O),
@@ -260,7 +260,7 @@ def wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, c_e
     C = kv_capacity(shape, keep_first, keep_last)
     if C == 0:
         raise WildcatError("wildcat_compress_kv: invalid split (keep_first / keep_last / r / bins)")
-    dev = _check_qkv(shape, Q, K, V, q_optional=True)
+    dev = _check_qkv(shape, Q, K, V, q_optional=True, need_v=True)
     _need(KC, "KC", tdt, units * C * d, dev)
     _need(XC, "XC", torch.float32, units * C * (d + 1), dev)
     _need(c_eff, "c_eff", torch.int32, units, dev)
@@ -322,7 +322,7 @@ def wc_comm_destroy(h) -> None:
 
 
 def wildcat_forward_nshard(comm, shape, n_global, n_offset, opts, Q, K, V, O, S, r_eff, ws, stream=None):
-    dev = _check_qkv(shape, Q, K, V, O)
+    dev = _check_qkv(shape, Q, K, V, O, need_v=True, need_o=True)
     _need(S, "S", torch.int32, shape.r, dev, optional=True)
     _need(r_eff, "r_eff", torch.int32, 1, dev, optional=True)
     _check_ws(ws, dev, workspace_bytes(shape, WC_OP_FORWARD_NSHARD))
