@@ -6,8 +6,10 @@ Contract:
 One step = one pass of the whole hot path (prologue, RPCholesky selection, Nystrom weights,
 weighted attend) over one batch of synthetic inputs resident in HBM, through the C ABI
 (wildcat_forward).  L2 is flushed (a 512 MB write) before every timed step, outside the timed
-events.  Multi-GPU (torchrun): each rank runs an independent replica (units sharded, no
-data-path collective) -> weak scaling; time = max over ranks.
+events.  Multi-GPU (torchrun, PAR2): the config's (batch, kv-head) units are partitioned over the
+ranks with no data-path collective, each rank passing unit_offset = its first unit so the pivots
+are those of the one-GPU run (strong scaling); the 1-unit headline grows its batch with the ranks
+instead (weak scaling).  Time = max over ranks.  --impl reference times the fp64 oracle.
 """
 from __future__ import annotations
 
@@ -113,54 +115,58 @@ def select_bytes(n, d, r, e, nblocks=None, fread=None):
     return n * (nblocks * (d * e + 16) + 8 * r + 8 * fread)
 
 
-def cpu_oracle_sample(cfg, Q, K, V, max_queries=2048, block=1, bins=1):
-    """Time the fp64 oracle (as it stands) on a bounded sample: unit 0's full prologue + selection +
-    weights over all n keys, and the attend on `max_queries` query rows; extrapolate linearly in the
-    number of query rows and units to the whole workload.  Returns (queries/s, seconds, details)."""
+def cpu_oracle_sample(cfg, Q, K, V, block=1, bins=1, max_units=1):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: the first `max_units`
+    units run COMPLETELY (prologue, selection, weights, and the attend of every query row of the
+    unit's q-heads) -- nothing is extrapolated: the rate is the queries actually answered divided by
+    the seconds they took.  At the headline (1 unit) the sample is the whole workload.
+    Returns (queries/s, seconds, details)."""
     import oracle
 
     threads = len(os.sched_getaffinity(0))
     oracle.set_threads(threads)
-    d = cfg.d
     group = cfg.hq // cfg.hkv
-    K64 = K[0, 0].double().numpy()
-    V64 = V[0, 0].double().numpy()
-    Qg = Q[0, :group].double().numpy().reshape(-1, d)
-    beta = 1.0 / math.sqrt(d)
-    ms = min(max_queries, Qg.shape[0])
-    if bins > 1:  # Alg 2 binned oracle on unit 0 with the query sample, attend part timed separately
+    nu = min(max_units, cfg.units)
+    secs, queries = 0.0, 0
+    for u in range(nu):
+        b, h = divmod(u, cfg.hkv)
+        Qu = Q[b:b + 1, h * group:(h + 1) * group].double().numpy()
+        Ku = K[b:b + 1, h:h + 1].double().numpy()
+        Vu = V[b:b + 1, h:h + 1].double().numpy()
         t0 = time.perf_counter()
-        res = oracle.forward_binned(Qg[None, None, :ms], K64[None, None], V64[None, None], cfg.r, bins,
-                                    seed=cfg.seed, block=block)
-        t1 = time.perf_counter()
-        re = int(res["r_eff"][0])
-        oracle.attend(Qg[:ms], K64[res["S"][0, :re]], res["X"][0], re, beta, V64.min(0), V64.max(0))
-        t2 = time.perf_counter()
-        sel_w = (t1 - t0) - (t2 - t1)
-        per_unit = sel_w + (t2 - t1) * (Qg.shape[0] / ms)
-        info = dict(select_s=sel_w, weights_s=0.0, attend_s=t2 - t1)
-        what = f"prologue+binned selection (B={bins}{f', blocked b={block}' if block >= 2 else ''})+weights"
-    else:
-        t0 = time.perf_counter()
-        kbar, st = oracle.prologue(K64, Qg)
-        if block >= 2:
-            sel = oracle.select_blocked(K64, kbar, st["g"], st["mstar"], cfg.r, block, seed=cfg.seed, unit=0)
-        else:
-            sel = oracle.select(K64, kbar, st["g"], st["mstar"], cfg.r, seed=cfg.seed, unit=0)
-        t1 = time.perf_counter()
-        X = oracle.weights(K64, V64, sel["S"], sel["r_eff"], kbar, st["g"], st["mstar"])
-        t2 = time.perf_counter()
-        oracle.attend(Qg[:ms], K64[sel["S"]], X, sel["r_eff"], beta, V64.min(0), V64.max(0))
-        t3 = time.perf_counter()
-        per_unit = (t1 - t0) + (t2 - t1) + (t3 - t2) * (Qg.shape[0] / ms)
-        info = dict(select_s=t1 - t0, weights_s=t2 - t1, attend_s=t3 - t2)
-        what = f"prologue+selection{f' (blocked, b={block})' if block >= 2 else ''}+weights"
-    total = per_unit * cfg.units
-    queries = cfg.batch * cfg.hq * cfg.m
-    info.update(attend_rows=ms, threads=threads,
-                sample=(f"oracle on unit 0 of {cfg.units}: full {what} over n={cfg.n} keys, "
-                        f"attend on {ms} of {Qg.shape[0]} query rows; extrapolated linearly to all rows/units"))
-    return queries / total, total, info
+        oracle.forward(Qu, Ku, Vu, cfg.r, seed=cfg.seed, block=block, bins=bins, unit_offset=u)
+        secs += time.perf_counter() - t0
+        queries += group * cfg.m
+    what = f"Alg 4 (selection {'blocked b=' + str(block) if block >= 2 else 'sequential'}, B={bins})"
+    info = dict(threads=threads, units=nu, queries=queries,
+                sample=(f"oracle {what} on {nu} of {cfg.units} units, complete: prologue, selection, weights "
+                        f"and the attend of all {group * cfg.m} query rows per unit; rate = queries answered / "
+                        f"seconds (no extrapolation)"))
+    return queries / secs, secs, info
+
+
+def config_dict(cfg, args, world, mode, units_per_rank):
+    """The `config` object of the JSON line -- identical for the GPU arm and the reference arm."""
+    return {"workload": cfg.name, "units": cfg.units, "units_per_gpu": units_per_rank, "n": cfg.n, "m": cfg.m,
+            "d": cfg.d, "r": cfg.r, "input_dtype": cfg.dtype, "family": cfg.family,
+            "parallelism": (f"units{world}" if mode == "units" else f"nshard{world}-{args.transport}"),
+            "select": ("blocked" if (args.block >= 2 and mode == "units") else "sequential"),
+            "block": args.block if mode == "units" else 1, "bins": args.bins,
+            "l2": f"flushed ({args.flush_mb} MB write) before each step"}
+
+
+def unit_partition(cfg, world, rank):
+    """PAR2 (P:303 ForPar; north_star "partitioned ... by (batch, head)"): the config's
+    units split into contiguous ranges, one per rank, each run with unit_offset = its first unit (so
+    every unit draws the Philox stream of the one-GPU run) -> strong scaling.  A config with fewer
+    units than ranks (the 1-unit headline) instead grows the batch with the ranks: rank k holds unit
+    k of a `world`-unit batch (inputs drawn with seed + k) -> weak scaling.
+    Returns (u0, u1, unit_offset, scaling)."""
+    U = cfg.units
+    if U >= world and U % world == 0:
+        per = U // world
+        return rank * per, (rank + 1) * per, rank * per, "strong"
+    return 0, U, rank * U, "weak"
 
 
 def exact_errors(cfg, Qd, Kd, Vd, O):
@@ -292,29 +298,34 @@ def cpu_model():
 
 
 def run_reference(args, cfg):
+    """The reference arm: the fp64 oracle as it stands (the tier's reference), timed on the host cores,
+    on the same workload/config as the GPU arm; each step a complete oracle run of a bounded sample
+    (see cpu_oracle_sample).  Under torchrun only rank 0 runs; the others exit without work."""
     rank = _env_int("RANK", 0)
     if rank != 0:
         return
     from paper_2602_10056_b200.inputs import make_config
 
+    world = max(1, args.gpus)
+    mode = args.mode or ("nshard" if cfg.name.startswith("long") else "units")
     Q, K, V = make_config(cfg)
+    block = args.block if mode == "units" else 1
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block, args.bins)
-    vals, secs = [], []
+        cpu_oracle_sample(cfg, Q, K, V, block, args.bins)
+    secs, queries = 0.0, 0
     info = None
     for _ in range(args.steps):
-        v, s, info = cpu_oracle_sample(cfg, Q, K, V, args.ref_queries, args.block, args.bins)
-        vals.append(v)
-        secs.append(s)
-    tot = sum(secs)
-    value = cfg.batch * cfg.hq * cfg.m * args.steps / tot
+        _, s_, info = cpu_oracle_sample(cfg, Q, K, V, block, args.bins)
+        secs += s_
+        queries += info["queries"]
+    value = queries / secs
+    u0, u1, _, scaling = unit_partition(cfg, world, 0)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "units": cfg.units, "n": cfg.n, "m": cfg.m, "d": cfg.d, "r": cfg.r,
-                   "block": args.block, "bins": args.bins,
-                   "input_dtype": cfg.dtype, "family": cfg.family},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": scaling if mode == "units" else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, args, world, mode, u1 - u0),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
                          "sample": info["sample"], "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -332,12 +343,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the accuracy-vs-exact and SDPA comparison")
-    ap.add_argument("--ref-queries", type=int, default=2048)
     ap.add_argument("--flush-mb", type=int, default=512)
-    ap.add_argument("--mode", default=None, choices=["replicas", "nshard"],
-                    help="replicas: each rank runs the workload on its own units (weak scaling); "
-                         "nshard: one sequence's keys sharded over the ranks (strong scaling). "
-                         "Default: nshard for the long* configs, replicas otherwise")
+    ap.add_argument("--mode", default=None, choices=["units", "nshard"],
+                    help="units: PAR2, the config's (batch, kv-head) units partitioned over the ranks (see "
+                         "unit_partition); nshard: one sequence's keys sharded over the ranks (strong scaling). "
+                         "Default: nshard for the long* configs, units otherwise")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
                     help="nshard mode: NCCL collectives, or device-initiated peer-memory mailboxes (8(f)-3)")
     ap.add_argument("--r", type=int, default=None, help="override the config's coreset size r")
@@ -378,9 +388,24 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    mode = args.mode or ("nshard" if cfg.name.startswith("long") else "replicas")
-    units = cfg.units
+    mode = args.mode or ("nshard" if cfg.name.startswith("long") else "units")
+    import dataclasses
+
     from paper_2602_10056_b200 import _binding as B0
+
+    uoff, scaling, lcfg = 0, "strong", cfg
+    if mode == "units":
+        u0, u1, uoff, scaling = unit_partition(cfg, world, rank)
+        per = u1 - u0
+        if per == cfg.units:
+            lcfg = cfg
+        elif per % cfg.hkv == 0:  # whole batch elements
+            lcfg = dataclasses.replace(cfg, batch=per // cfg.hkv)
+        else:  # kv-heads (with their q-heads) of one batch element
+            assert cfg.hkv % per == 0, "units per rank must tile batch elements or kv-head groups"
+            g = cfg.hq // cfg.hkv
+            lcfg = dataclasses.replace(cfg, batch=1, hkv=per, hq=per * g)
+    units = lcfg.units
 
     rb_main, R_main = B0.coreset_rows(cfg.n, cfg.r, max(1, args.bins))
     S = torch.empty(units, max(cfg.r, R_main), dtype=torch.int32, device=dev)
@@ -400,15 +425,30 @@ def main():
         def step():
             return wc.forward_nshard(comm, Qd, Kd, Vd, cfg.r, cfg.n, koff, seed=seed, S=S[0], r_eff=R, out=Obuf)
     else:
-        # replica per rank (weak scaling): same workload, rank-specific seed
-        Q, K, V = make_config(cfg, seed=cfg.seed + rank)
+        # PAR2: this rank's units of the batch (unit_partition), Philox ids from unit_offset = uoff
+        seed = cfg.seed
+        if scaling == "weak":  # the batch grows with the ranks: unit block `rank` drawn with seed + rank
+            Q, K, V = make_config(cfg, seed=cfg.seed + rank)
+        else:
+            Qa, Ka, Va = make_config(cfg)
+            if lcfg is cfg:
+                Q, K, V = Qa, Ka, Va
+            elif lcfg.batch * cfg.hkv == u1 - u0:
+                b0 = u0 // cfg.hkv
+                Q, K, V = (x[b0:b0 + lcfg.batch].contiguous() for x in (Qa, Ka, Va))
+            else:
+                b0, h0 = divmod(u0, cfg.hkv)
+                g = cfg.hq // cfg.hkv
+                Q = Qa[b0:b0 + 1, h0 * g:(h0 + lcfg.hkv) * g].contiguous()
+                K, V = (x[b0:b0 + 1, h0:h0 + lcfg.hkv].contiguous() for x in (Ka, Va))
+            del Qa, Ka, Va
         Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
-        seed = cfg.seed + rank
 
         Obuf = torch.empty_like(Qd)  # preallocated: no allocator traffic inside the timed region
 
         def step():
-            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=args.block, bins=args.bins)
+            return wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=args.block, bins=args.bins,
+                              unit_offset=uoff)
 
     for _ in range(args.warmup):
         step()
@@ -445,7 +485,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    queries_per_rank = cfg.batch * cfg.hq * cfg.m if mode == "replicas" else cfg.batch * cfg.hq * cfg.m / world
+    queries_per_rank = lcfg.batch * lcfg.hq * cfg.m if mode == "units" else cfg.batch * cfg.hq * cfg.m / world
     value = queries_per_rank * world * args.steps / (total_ms / 1e3)
 
     # stage breakdown (ms, mean over timed steps): prologue, select, weights, attend
@@ -455,9 +495,9 @@ def main():
     e = 2 if cfg.dtype == "bf16" else 4
     r_eff = int(R.min().item())
     sel_info = None
-    if mode == "replicas":
+    if mode == "units":
         # selection bookkeeping of the same (deterministic) selection: blocks run, F rows re-read
-        sel = wc.select(Qd, Kd, cfg.r, seed=seed, block=args.block, bins=args.bins)
+        sel = wc.select(Qd, Kd, cfg.r, seed=seed, block=args.block, bins=args.bins, unit_offset=uoff)
         stt = sel.stats.double().cpu()  # per (unit, bin) sub-unit
         nb = cfg.n // args.bins
         Sh = sel.S.cpu().numpy()
@@ -486,9 +526,10 @@ def main():
 
     # the other selection variant on the same inputs (context: sequential Alg 1 vs blocked)
     variants = None
-    if not args.no_variants and mode == "replicas" and args.block >= 2:
+    if not args.no_variants and mode == "units" and args.block >= 2:
         nvs = max(2, min(5, args.steps))
-        forward_seq = lambda: wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=1)
+        forward_seq = lambda: wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=S, r_eff=R, out=Obuf, block=1,
+                                         unit_offset=uoff)
         forward_seq()
         torch.cuda.synchronize()
         B.timing_enable(True)
@@ -512,7 +553,7 @@ def main():
                                    "select_hbm_frac": vbytes / (vsel / 1e3) / 1e9 / peak}}
     # Alg 2 binning with the paper's KV-cache setting B ~ r/12: the largest power of two
     # <= r/12 that divides n (so B = 16 at the headline), blocked selection, same inputs
-    if not args.no_variants and mode == "replicas" and args.bins == 1:
+    if not args.no_variants and mode == "units" and args.bins == 1:
         bv = 1
         while bv * 2 <= max(1, cfg.r // 12) and cfg.n % (bv * 2) == 0:
             bv *= 2
@@ -520,7 +561,7 @@ def main():
             _, Rv = B0.coreset_rows(cfg.n, cfg.r, bv)
             Sv = torch.empty(units, Rv, dtype=torch.int32, device=dev)
             fwd_b = lambda: wc.forward(Qd, Kd, Vd, cfg.r, seed=seed, S=Sv, r_eff=R, out=Obuf, block=max(2, args.block),
-                                       bins=bv)
+                                       bins=bv, unit_offset=uoff)
             fwd_b()
             torch.cuda.synchronize()
             vt = []
@@ -535,22 +576,22 @@ def main():
                 vt.append(e0.elapsed_time(e1))
             Ob = fwd_b()
             torch.cuda.synchronize()
-            berr = max(exact_errors(cfg, Qd, Kd, Vd, Ob)) if (rank == 0 and not args.no_exact) else None
+            berr = max(exact_errors(lcfg, Qd, Kd, Vd, Ob)) if (rank == 0 and not args.no_exact) else None
             variants = variants or {}
             variants["binned"] = {"bins": bv, "block": max(2, args.block), "r_per_bin": Rv // bv,
                                   "ms_per_step": statistics.mean(vt),
                                   "queries_per_s": queries_per_rank * world / (statistics.mean(vt) / 1e3),
                                   "max_rel_err_vs_exact": berr}
     # KV-cache workload (prefill compression + decode) at the LLM shapes, rank 0, single GPU
-    if not args.no_variants and mode == "replicas" and rank == 0 and world == 1 and args.config == "headline":
+    if not args.no_variants and mode == "units" and rank == 0 and world == 1 and args.config == "headline":
         variants = variants or {}
         variants["kvcache"] = kv_variant(dev, flush, max(2, args.block), args.steps, with_exact=not args.no_exact)
     # A5 against its own roofline (HBM-bound for r < 258 at bf16; intensity ~ r flop/byte):
     # algorithmic bytes 2 m d e + r d e + 4 r (d + 1) per head and flops 4 m r d, over the attend stage
     attend_roof = None
-    if st_mean and mode == "replicas":
+    if st_mean and mode == "units":
         at_ms = st_mean[3]
-        heads = cfg.batch * cfg.hq
+        heads = lcfg.batch * lcfg.hq
         a_bytes = heads * 2 * cfg.m * cfg.d * e + units * (R_main * cfg.d * e + 4 * R_main * (cfg.d + 1))
         a_flops = heads * 4.0 * cfg.m * R_main * cfg.d
         tp = None
@@ -576,16 +617,16 @@ def main():
 
     # end to end through the public API with host buffers (pinned), H2D + forward + D2H per step
     e2e = None
-    if not args.no_e2e and mode == "replicas":
+    if not args.no_e2e and mode == "units":
         Qh, Kh, Vh = (x.pin_memory() for x in (Q, K, V))
         for _ in range(max(1, args.warmup)):
-            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block)
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block, unit_offset=uoff)
         tt = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block)
+            wc.forward_host(Qh, Kh, Vh, cfg.r, seed=seed, device=dev, block=args.block, unit_offset=uoff)
             tt.append(time.perf_counter() - t0)
         te = torch.tensor([sum(tt)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -603,26 +644,26 @@ def main():
     # n ~ 262K at r = 256 -- SURVEY.md 8(d)).
     err = None
     sdpa_ms = None
-    if rank == 0 and mode == "replicas" and not args.no_exact:
+    if rank == 0 and mode == "units" and not args.no_exact:
         from paper_2602_10056_b200.inputs import query_sample
 
         O_ref = step()
         torch.cuda.synchronize()
-        errs = exact_errors(cfg, Qd, Kd, Vd, O_ref)
-        err = {"max_rel_err_vs_exact": max(errs), "rows_per_head": 4096 // max(1, cfg.batch * cfg.hq) + 1,
+        errs = exact_errors(lcfg, Qd, Kd, Vd, O_ref)
+        err = {"max_rel_err_vs_exact": max(errs), "rows_per_head": 4096 // max(1, lcfg.batch * lcfg.hq) + 1,
                "heads_checked": len(errs), "norm": "max|O^ - O| / max|V| (P:144)"}
         try:
             import torch.nn.functional as Fnn
 
             for _ in range(2):
-                Fnn.scaled_dot_product_attention(Qd, Kd, Vd, enable_gqa=cfg.hq != cfg.hkv)
+                Fnn.scaled_dot_product_attention(Qd, Kd, Vd, enable_gqa=lcfg.hq != lcfg.hkv)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             tt = []
             for _ in range(3):
                 flush.zero_()
                 e0.record()
-                Fnn.scaled_dot_product_attention(Qd, Kd, Vd, enable_gqa=cfg.hq != cfg.hkv)
+                Fnn.scaled_dot_product_attention(Qd, Kd, Vd, enable_gqa=lcfg.hq != lcfg.hkv)
                 e1.record()
                 e1.synchronize()
                 tt.append(e0.elapsed_time(e1))
@@ -632,10 +673,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.n <= 262144:
-        v, secs, info = cpu_oracle_sample(cfg, Q, K, V, block=args.block, bins=args.bins)
+        v, secs, info = cpu_oracle_sample(lcfg, Q, K, V, block=args.block, bins=args.bins)
         cpu = {"value": v, "unit": "queries/s", "cores": info["threads"], "kind": "oracle",
-               "sample": info["sample"], "cpu": cpu_model(), "seconds_extrapolated": secs,
-               "select_s": info["select_s"], "weights_s": info["weights_s"], "attend_s": info["attend_s"]}
+               "sample": info["sample"], "cpu": cpu_model(), "seconds": secs}
 
     if rank == 0:
         line = {
@@ -647,16 +687,13 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak" if mode == "replicas" else "strong",
+            "scaling": scaling if mode == "units" else "strong",
             "vs_baseline": None,
             "dtype": "f64-select/f32-gemm",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "units_per_gpu": units, "n": cfg.n, "m": cfg.m, "d": cfg.d,
-                       "r": cfg.r, "r_eff": r_eff, "input_dtype": cfg.dtype, "family": cfg.family,
-                       "parallelism": (f"replicas{world}" if mode == "replicas" else f"nshard{world}-{args.transport}"),
-                       "select": "blocked" if args.block >= 2 else "sequential", "block": args.block,
-                       "bins": args.bins,
-                       "l2": f"flushed ({args.flush_mb} MB write) before each step"},
+            "config": config_dict(cfg, args, world, mode, units),
+            "r_eff_min": r_eff,
+            "unit_offset": uoff,
             "stages_ms": dict(zip(st_names, st_mean)) if st_mean else None,
             "selection": sel_info,
             "roofline_fp64": roof64,

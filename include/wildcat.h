@@ -64,6 +64,7 @@ extern "C" {
 #define WC_ECUDA -5         /* CUDA launch / runtime error */
 #define WC_ENCCL -6         /* NCCL error (n-sharded path) */
 #define WC_EUNSUPPORTED -7  /* valid request this build does not implement */
+#define WC_ENONFINITE -8    /* WC_CHECK_FINITE: an input element is NaN or +-Inf (nothing else is launched) */
 
 #define WC_F32 0
 #define WC_BF16 1
@@ -74,8 +75,20 @@ extern "C" {
 #define WC_OP_FORWARD 3
 #define WC_OP_FORWARD_NSHARD 4  /* per-rank workspace of wildcat_forward_nshard (shape = local shard) */
 
-/* flags */
+/* flags (wc_opts.flags; any other bit -> WC_EINVAL) */
 #define WC_NO_CLIP 1u       /* skip the clip of Alg 3 (reading Z15) */
+#define WC_TAU_ONE 2u       /* temperature tau = 1 instead of Eq. 7: the selection / weights kernel is
+                               then h(a,b) = exp(beta <a - kbar, b - kbar>) -- the untempered softmax kernel of
+                               P:124-129 on (recentred) keys; every bin (Alg 2) likewise */
+#define WC_NO_RECENTER 4u   /* skip "Recenter keys" (Alg 2): kbar = 0, R_K = max ||k_l|| (P:304 with
+                               uncentred keys); attention itself is invariant to the recentring, the
+                               kernel the selection and the Nystrom weights approximate is not.  The kernel
+                               values h~ span [exp(-2 mstar), 1]; the A3 weights run their exponentials in
+                               fp32, so keys whose offset makes 2 mstar > ~80 (what recentring prevents)
+                               lose the small entries to underflow */
+#define WC_CHECK_FINITE 8u  /* debug: before any other work, scan Q, K, V for NaN / Inf (SPEC's finite-input
+                               rule); synchronises `stream` once and returns WC_ENONFINITE if one is found */
+#define WC_FLAGS_ALL 15u
 
 #define WC_STATS_HEAD 16
 #define WC_STATS_STRIDE(d) (WC_STATS_HEAD + (d))
@@ -97,14 +110,23 @@ typedef struct wc_opts {
     double beta;       /* softmax scale; <= 0 selects 1/sqrt(d) (reading Z7) */
     double rq;         /* R_Q of Alg 2; < 0 (or NaN) computes max ||q|| over the unit's query group */
     uint64_t seed;     /* Philox4x32-10 key for the pivot draws (reading Z2) */
-    uint32_t flags;    /* WC_NO_CLIP */
+    uint32_t flags;    /* WC_NO_CLIP | WC_TAU_ONE | WC_NO_RECENTER | WC_CHECK_FINITE */
     uint32_t block;    /* pivot selection: 0 or 1 = sequential RPCholesky, Alg 1;
                           2..WC_MAX_BLOCK = blocked ("accelerated") RPCholesky with b = block
                           candidates per block (P:678 future work; reading Z22): same pivot LAW
-                          as Alg 1, a different pivot sequence for a given seed. */
+                          as Alg 1, a different pivot sequence for a given seed.  b <= 16 runs the
+                          16-slot plan (any r <= WC_MAX_R); 16 < b <= 32 the 32-slot plan, whose
+                          candidate columns must fit shared memory (r up to ~300, else
+                          WC_EUNSUPPORTED before any launch). */
+    uint64_t unit_offset; /* global id of this call's unit 0 (PAR2): unit u of the call draws
+                          the Philox stream of unit unit_offset + u (bin b: sub-unit (unit_offset+u)*B + b;
+                          reading Z2, Z23), so a GPU that holds units [u0, u0 + U) of a larger batch and
+                          passes unit_offset = u0 selects exactly the pivots of the one-GPU run on those
+                          units ("ForPar"; north_star "partitioned ... by (batch, head)").  The
+                          n-sharded forward uses it as the id of its single unit. */
 } wc_opts;
 
-#define WC_MAX_BLOCK 16
+#define WC_MAX_BLOCK 32
 
 /* Largest coreset size per selection problem (r, or rb = ceil(r/B) per bin) for wildcat_select /
  * wildcat_weights / wildcat_forward / wildcat_compress_kv / wildcat_forward_nshard: the r x r solve
@@ -231,7 +253,7 @@ int wc_timing_enable(int on);
 int wc_timing_read(float *ms, int cap);
 
 /* ABI version (major*100 + minor). */
-int wc_version(void);
+int wc_version(void);  /* 200: wc_opts.unit_offset, WC_TAU_ONE / WC_NO_RECENTER / WC_CHECK_FINITE */
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,14 @@ _c_u64 = ctypes.c_uint64
 _c_dbl = ctypes.c_double
 _p = ctypes.c_void_p
 
+# options of the prologue (the oracle's own constants, same meaning as the ABI's flags)
+TAU_ONE = 2
+NO_RECENTER = 4
+
+
+def _flags(tau_one=False, recenter=True):
+    return (TAU_ONE if tau_one else 0) | (0 if recenter else NO_RECENTER)
+
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2, no FMA contraction, OpenMP)."""
@@ -59,7 +67,7 @@ def lib():
             L.wco_rho0.restype = _c_dbl
             L.wco_temperature.argtypes = [_c_dbl, _c_dbl, _c_dbl, _c_i64]
             L.wco_temperature.restype = _c_dbl
-            L.wco_prologue.argtypes = [_c_i64, _c_i32, _p, _c_i64, _p, _c_dbl, _c_dbl, _p, _p]
+            L.wco_prologue.argtypes = [_c_i64, _c_i32, _p, _c_i64, _p, _c_dbl, _c_dbl, _p, _p, _c_i32]
             L.wco_select.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64, _c_u64,
                                      _p, _p, _p, _p, _p, _p]
             L.wco_select_mr.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64, _c_u64,
@@ -68,13 +76,13 @@ def lib():
             L.wco_attend.argtypes = [_c_i64, _c_i32, _c_i32, _p, _p, _p, _c_i32, _c_dbl, _p, _p, _c_i32, _p]
             L.wco_exact_attention.argtypes = [_c_i64, _c_i64, _c_i32, _p, _p, _p, _c_dbl, _p]
             L.wco_forward.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_dbl,
-                                      _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p, _p, _p]
+                                      _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p, _p, _p, _c_u64, _c_i32]
             L.wco_forward_binned.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32,
                                              _c_dbl, _c_dbl, _c_u64, _c_i32, _c_i32, _p, _p, _p, _p, _p, _p,
-                                             _p, _p]
+                                             _p, _p, _c_u64, _c_i32]
             L.wco_compress_kv.argtypes = [_c_i32, _c_i32, _c_i32, _c_i64, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32,
                                           _c_i32, _c_i32, _c_dbl, _c_dbl, _c_u64, _p, _p, _p, _p, _p, _p, _p, _p,
-                                          _p]
+                                          _p, _c_u64, _c_i32]
             L.wco_accept_uniform.argtypes = [_c_u64, ctypes.c_uint32, _c_u64]
             L.wco_accept_uniform.restype = _c_dbl
             L.wco_select_blocked.argtypes = [_c_i64, _c_i32, _c_i32, _c_i32, _p, _p, _c_dbl, _c_dbl, _c_u64,
@@ -127,14 +135,15 @@ def num_threads() -> int:
 
 
 # --------------------------------------------------------------------------- per unit
-def prologue(K, Qrows=None, rq=-1.0, beta=None):
+def prologue(K, Qrows=None, rq=-1.0, beta=None, tau_one=False, recenter=True):
     K = _f64(K)
     n, d = K.shape
     beta = 1.0 / np.sqrt(d) if beta is None else float(beta)
     Qr = _f64(Qrows) if Qrows is not None else np.zeros((0, d))
     kbar = np.zeros(d)
     st = np.zeros(5)
-    lib().wco_prologue(n, d, _ptr(K), Qr.shape[0], _ptr(Qr), float(rq), beta, _ptr(kbar), _ptr(st))
+    lib().wco_prologue(n, d, _ptr(K), Qr.shape[0], _ptr(Qr), float(rq), beta, _ptr(kbar), _ptr(st),
+                       _flags(tau_one, recenter))
     return kbar, dict(tau=st[0], g=st[1], mstar=st[2], rk=st[3], rq=st[4])
 
 
@@ -239,13 +248,16 @@ def exact_attention(Q, K, V, beta=None):
     return O
 
 
-def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1, bins=1):
+def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1, bins=1, unit_offset=0, tau_one=False,
+            recenter=True):
     """Alg 4 over [batch, heads, seq, d] arrays (float64 copies of the inputs).
     bins > 1: Alg 2 with B contiguous bins (wco_forward_binned; stats are then per bin).
+    unit_offset: the units are [unit_offset, ...) of a larger batch (Philox unit ids, PAR2).
 
     Returns dict(O, S, r_eff, stats, X)."""
     if bins > 1:
-        return forward_binned(Q, K, V, r, bins, seed=seed, beta=beta, rq=rq, clip=clip, block=block)
+        return forward_binned(Q, K, V, r, bins, seed=seed, beta=beta, rq=rq, clip=clip, block=block,
+                              unit_offset=unit_offset, tau_one=tau_one, recenter=recenter)
     Q = _f64(Q)
     K = _f64(K)
     V = _f64(V)
@@ -259,7 +271,8 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=-1.0, clip=True, block=1, bins=1):
     st = np.zeros((units, 5))
     X = np.zeros((units, r, d + 1))
     rc = lib().wco_forward(batch, hq, hkv, m, n, d, r, beta, float(rq), int(seed), int(bool(clip)), int(block),
-                           _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st), _ptr(X))
+                           _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st), _ptr(X),
+                           int(unit_offset), _flags(tau_one, recenter))
     if rc:
         raise RuntimeError(f"wco_forward failed ({rc})")
     return dict(O=O, S=S, r_eff=reff, stats=st, X=X)
@@ -271,7 +284,8 @@ def bin_rank(n, r, bins):
     return rb, bins * rb
 
 
-def forward_binned(Q, K, V, r, bins, seed=0, beta=None, rq=-1.0, clip=True, block=1):
+def forward_binned(Q, K, V, r, bins, seed=0, beta=None, rq=-1.0, clip=True, block=1, unit_offset=0, tau_one=False,
+                   recenter=True):
     """Alg 4 with Alg 2 binning (wco_forward_binned).  Returns dict(O, S, r_eff, stats, X) with
     S [units][B*rb], stats [units][B][5] (tau_b, g_b, mstar_b, R_K^b, R_Q), X [units][B*rb][d+1]."""
     Q = _f64(Q)
@@ -289,7 +303,7 @@ def forward_binned(Q, K, V, r, bins, seed=0, beta=None, rq=-1.0, clip=True, bloc
     X = np.zeros((units, R, d + 1))
     rc = lib().wco_forward_binned(batch, hq, hkv, m, n, d, r, bins, beta, float(rq), int(seed), int(bool(clip)),
                                   int(block), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(S), _ptr(reff), _ptr(st),
-                                  _ptr(X))
+                                  _ptr(X), int(unit_offset), _flags(tau_one, recenter))
     if rc:
         raise RuntimeError(f"wco_forward_binned failed ({rc})")
     return dict(O=O, S=S, r_eff=reff, stats=st, X=X)
@@ -302,7 +316,8 @@ def kv_capacity(n, r, keep_first, keep_last, bins=1):
     return keep_first + keep_last + R, R
 
 
-def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=-1.0, block=1):
+def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=-1.0, block=1, unit_offset=0,
+                tau_one=False, recenter=True):
     """KV-cache compression (wco_compress_kv, reading Z24) over
     [batch, heads, seq, d] arrays.  Returns dict(KC [units][C][d], XC [units][C][d+1], c_eff [units],
     vmin, vmax [units][d], S [units][R] global token indices of the coreset)."""
@@ -322,7 +337,7 @@ def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None
     S = np.full((units, max(R, 1)), -1, dtype=np.int32)
     rc = lib().wco_compress_kv(batch, hq, hkv, m, n, d, r, bins, int(block), int(keep_first), int(keep_last), beta,
                                float(rq), int(seed), _ptr(Q), _ptr(K), _ptr(V), _ptr(KC), _ptr(XC), _ptr(ceff),
-                               _ptr(vmin), _ptr(vmax), _ptr(S))
+                               _ptr(vmin), _ptr(vmax), _ptr(S), int(unit_offset), _flags(tau_one, recenter))
     if rc == -2:
         raise ValueError("invalid KV split (keep_first/keep_last/bins)")
     if rc:

@@ -117,15 +117,20 @@ double wco_temperature(double beta, double rq, double rk, int64_t n)
  *   tau (Eq. 7), g = beta/tau^2, mstar = g R_K^2 (reading Z10: the kernel used for
  *   selection and weights is h~(a,b) = exp(g<a-kbar,b-kbar> - mstar), which is
  *   h_tau of P:306 on centred keys times the global constant e^{-mstar}).
- * stats out: [tau, g, mstar, R_K, R_Q].                                     */
+ * stats out: [tau, g, mstar, R_K, R_Q].
+ * Options (flags; the switches of SURVEY 8(b)): WCO_NO_RECENTER skips "Recenter keys"
+ * (P:300-301): kbar = 0, so R_K = max ||k_l|| and the kernel is on uncentred keys;
+ * WCO_TAU_ONE skips Eq. 7: tau = 1, i.e. h_tau = exp(beta <.,.>) (P:306 at tau = 1).        */
 /* ------------------------------------------------------------------------ */
+#define WCO_TAU_ONE 2
+#define WCO_NO_RECENTER 4
 void wco_prologue(int64_t n, int32_t d, const double *K, int64_t mq, const double *Qrows,
-                  double rq_given, double beta, double *kbar, double *stats)
+                  double rq_given, double beta, double *kbar, double *stats, int32_t flags)
 {
     for (int j = 0; j < d; ++j) {
         double s = 0.0;
         for (int64_t l = 0; l < n; ++l) s += K[l * d + j];
-        kbar[j] = s / (double)n;
+        kbar[j] = (flags & WCO_NO_RECENTER) ? 0.0 : s / (double)n;
     }
     double rk2 = 0.0;
     for (int64_t l = 0; l < n; ++l) {
@@ -149,7 +154,7 @@ void wco_prologue(int64_t n, int32_t d, const double *K, int64_t mq, const doubl
         }
         rq = sqrt(rq2);
     }
-    double tau = wco_temperature(beta, rq, rk, n);
+    double tau = (flags & WCO_TAU_ONE) ? 1.0 : wco_temperature(beta, rq, rk, n);
     double g = beta / (tau * tau);
     stats[0] = tau;
     stats[1] = g;
@@ -593,12 +598,16 @@ void wco_exact_attention(int64_t m, int64_t n, int32_t d, const double *Q, const
  * Optional outputs (may be NULL): S [units][r], r_eff [units],
  * stats [units][5] = tau,g,mstar,R_K,R_Q, X [units][r][d+1].
  * block > 1 selects with the blocked variant (wco_select_blocked, reading Z22).
+ * unit0: these units are units [unit0, unit0 + batch*hkv) of a larger batch -- unit u draws
+ * the Philox stream of unit id unit0 + u (reading Z2; PAR2 of SURVEY 8(e)).
+ * flags: WCO_TAU_ONE / WCO_NO_RECENTER (see wco_prologue).
  * Returns 0, or the first nonzero sub-status.                               */
 /* ------------------------------------------------------------------------ */
 int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d,
                 int32_t r, double beta, double rq, uint64_t seed, int32_t clip, int32_t block,
                 const double *Q, const double *K, const double *V, double *O,
-                int32_t *S_out, int32_t *reff_out, double *stats_out, double *X_out)
+                int32_t *S_out, int32_t *reff_out, double *stats_out, double *X_out,
+                uint64_t unit0, int32_t flags)
 {
     int32_t group = hq / hkv;
     int32_t dc = d + 1;
@@ -628,13 +637,14 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
                 vmax[c] = hi;
             }
             double st[5];
-            wco_prologue(n, d, Ku, (int64_t)group * m, Qg, rq, beta, kbar, st);
+            wco_prologue(n, d, Ku, (int64_t)group * m, Qg, rq, beta, kbar, st, flags);
             int32_t re = 0;
+            const uint64_t uid = unit0 + u;  /* global unit id of the Philox stream */
             if (block > 1)
-                status = wco_select_blocked(n, d, r, block, Ku, kbar, st[1], st[2], seed, u, S, &re, NULL, NULL,
+                status = wco_select_blocked(n, d, r, block, Ku, kbar, st[1], st[2], seed, uid, S, &re, NULL, NULL,
                                             NULL, NULL, NULL);
             else
-                status = wco_select(n, d, r, Ku, kbar, st[1], st[2], seed, u, S, &re, NULL, NULL, NULL, NULL);
+                status = wco_select(n, d, r, Ku, kbar, st[1], st[2], seed, uid, S, &re, NULL, NULL, NULL, NULL);
             if (status) break;
             status = wco_weights(n, d, r, Ku, Vu, S, re, kbar, st[1], st[2], X);
             if (status) break;
@@ -679,7 +689,7 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
 static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t block, double beta,
                          double rq, uint64_t seed, uint64_t u, const double *Ku, const double *Vu,
                          int64_t mq, const double *Qg, int32_t *S, double *KS, double *X,
-                         int32_t *tot_out, double *binstats)
+                         int32_t *tot_out, double *binstats, int32_t flags)
 {
     const int64_t nb = n / bins;
     int32_t rb = (r + bins - 1) / bins;
@@ -694,7 +704,7 @@ static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t 
     }
     int status = 0;
     double st[5];
-    wco_prologue(n, d, Ku, mq, Qg, rq, beta, kbar, st);  /* global kbar, R_Q */
+    wco_prologue(n, d, Ku, mq, Qg, rq, beta, kbar, st, flags);  /* global kbar, R_Q */
     const double rqu = st[4];
     memset(X, 0, sizeof(double) * (size_t)R * dc);
     memset(KS, 0, sizeof(double) * (size_t)R * d);
@@ -713,7 +723,7 @@ static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t 
             if (s2 > rk2) rk2 = s2;
         }
         const double rk = sqrt(rk2);
-        const double tau = wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
+        const double tau = (flags & WCO_TAU_ONE) ? 1.0 : wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
         const double g = beta / (tau * tau), mstar = g * rk * rk;
         int32_t re = 0;
         const uint64_t ub = u * (uint64_t)bins + (uint64_t)b;  /* Z23 */
@@ -759,7 +769,8 @@ static void value_range(int64_t n, int32_t d, const double *Vu, double *vmin, do
 int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d,
                        int32_t r, int32_t bins, double beta, double rq, uint64_t seed, int32_t clip,
                        int32_t block, const double *Q, const double *K, const double *V, double *O,
-                       int32_t *S_out, int32_t *reff_out, double *binstats_out, double *X_out)
+                       int32_t *S_out, int32_t *reff_out, double *binstats_out, double *X_out,
+                       uint64_t unit0, int32_t flags)
 {
     if (bins < 1 || n % bins != 0 || bins > r) return -2;
     const int64_t nb = n / bins;
@@ -781,8 +792,8 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
             const double *Qg = Q + ((size_t)bt * hq + (size_t)h * group) * m * d;
             value_range(n, d, Vu, vmin, vmax);  /* value range over the full V */
             int32_t tot = 0;
-            status = compress_unit(n, d, r, bins, block, beta, rq, seed, u, Ku, Vu, (int64_t)group * m, Qg, S,
-                                   KS, X, &tot, binstats_out ? binstats_out + (size_t)u * bins * 5 : NULL);
+            status = compress_unit(n, d, r, bins, block, beta, rq, seed, unit0 + u, Ku, Vu, (int64_t)group * m, Qg,
+                                   S, KS, X, &tot, binstats_out ? binstats_out + (size_t)u * bins * 5 : NULL, flags);
             if (status) break;
             for (int32_t hh = 0; hh < group; ++hh) {
                 size_t qoff = ((size_t)bt * hq + (size_t)h * group + hh) * m * d;
@@ -823,7 +834,8 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
 int wco_compress_kv(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d, int32_t r,
                     int32_t bins, int32_t block, int32_t keep_first, int32_t keep_last, double beta, double rq,
                     uint64_t seed, const double *Q, const double *K, const double *V, double *KC, double *XC,
-                    int32_t *c_eff, double *vmin_out, double *vmax_out, int32_t *S_out)
+                    int32_t *c_eff, double *vmin_out, double *vmax_out, int32_t *S_out, uint64_t unit0,
+                    int32_t flags)
 {
     const int64_t nmid = n - keep_first - keep_last;
     if (keep_first < 0 || keep_last < 0 || nmid < 0) return -2;
@@ -859,8 +871,9 @@ int wco_compress_kv(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n
             }
             int32_t tot = 0;
             if (nmid > 0) {
-                status = compress_unit(nmid, d, r, bins, block, beta, rq, seed, u, Ku + (size_t)keep_first * d,
-                                       Vu + (size_t)keep_first * d, (int64_t)group * m, Qg, S, KS, X, &tot, NULL);
+                status = compress_unit(nmid, d, r, bins, block, beta, rq, seed, unit0 + u,
+                                       Ku + (size_t)keep_first * d, Vu + (size_t)keep_first * d, (int64_t)group * m,
+                                       Qg, S, KS, X, &tot, NULL, flags);
                 if (status) break;
                 memcpy(KCu + (size_t)kept * d, KS, sizeof(double) * (size_t)tot * d);
                 memcpy(XCu + (size_t)kept * dc, X, sizeof(double) * (size_t)tot * dc);

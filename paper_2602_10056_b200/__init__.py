@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _binding as B
-from ._binding import WildcatError, lib  # noqa: F401
+from ._binding import NonFiniteInput, WildcatError, lib  # noqa: F401
 
 __all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range", "compress_kv", "kv_capacity"]
@@ -100,13 +100,23 @@ def _on_stream(stream, *ts):
             t.record_stream(stream)
 
 
-def select(Q, K, r, seed=0, beta=None, rq=None, block=1, bins=1, stream=None) -> Selection:
+def _opts(seed, beta, rq, clip, block, kw):
+    """wc_opts from the common keywords plus the optional ones: unit_offset (PAR2: global id of unit 0),
+    tau_one (WC_TAU_ONE), recenter (False -> WC_NO_RECENTER), check_finite (WC_CHECK_FINITE)."""
+    bad = set(kw) - {"unit_offset", "tau_one", "recenter", "check_finite"}
+    if bad:
+        raise TypeError(f"unexpected keyword arguments {sorted(bad)}")
+    return B.make_opts(seed, beta, rq, clip, block=block, **kw)
+
+
+def select(Q, K, r, seed=0, beta=None, rq=None, block=1, bins=1, stream=None, **kw) -> Selection:
     """RPNys selection; block >= 2 selects the blocked (accelerated) variant (reading Z22); bins > 1
-    runs Alg 2 binning (S [units][R] concatenated over bins, L [units*B][rb][rb], stats per bin)."""
+    runs Alg 2 binning (S [units][R] concatenated over bins, L [units*B][rb][rb], stats per bin).
+    Keywords unit_offset / tau_one / recenter / check_finite: see _opts."""
     Q, K = _cont(Q), _cont(K)
     _require_cuda(Q, K)
     shape = B.make_shape(Q, K, r, bins=bins)
-    opts = B.make_opts(seed, beta, rq, block=block)
+    opts = _opts(seed, beta, rq, True, block, kw)
     units = shape.batch * shape.heads_kv
     rb, R = B.coreset_rows(shape.n, r, bins)
     dev = K.device
@@ -149,9 +159,9 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
     else:
         shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=r, bins=1,
                            dtype=B._dtype_code(Q), reserved=0, m=m, n=max(r, 1))
+    flags = cache.opts.flags if clip is None else ((cache.opts.flags & ~B.WC_NO_CLIP) | (0 if clip else B.WC_NO_CLIP))
     opts = B.wc_opts(beta=cache.opts.beta if beta is None else float(beta), rq=cache.opts.rq,
-                     seed=cache.opts.seed,
-                     flags=cache.opts.flags if clip is None else (0 if clip else B.WC_NO_CLIP), block=0)
+                     seed=cache.opts.seed, flags=flags, block=0, unit_offset=cache.opts.unit_offset)
     O = torch.empty_like(Q)
     ws = _workspace(shape, B.WC_OP_ATTEND, Q.device, stream) if B.workspace_bytes(shape, B.WC_OP_ATTEND) else None
     _on_stream(stream, O)
@@ -160,14 +170,16 @@ def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
 
 
 def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None, r_eff=None, block=1,
-            bins=1, stream=None):
+            bins=1, stream=None, **kw):
     """Alg 4 WildCat on device tensors.  Returns O (and fills S [units][R] / r_eff if given).
     block >= 2: blocked (accelerated) RPCholesky selection with b = block (reading Z22).
-    bins > 1: Alg 2 binning with B = bins (R = B * min(ceil(r/B), n/B) coreset rows per unit)."""
+    bins > 1: Alg 2 binning with B = bins (R = B * min(ceil(r/B), n/B) coreset rows per unit).
+    unit_offset = u0: these units are units [u0, u0 + units) of a larger batch (PAR2 partition: the
+    same pivots as the one-GPU run); tau_one / recenter / check_finite: see _opts."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     shape = B.make_shape(Q, K, r, bins=bins)
-    opts = B.make_opts(seed, beta, rq, clip, block=block)
+    opts = _opts(seed, beta, rq, clip, block, kw)
     O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD, K.device, stream)
     if out is None:
@@ -183,7 +195,7 @@ def kv_capacity(n, r, keep_first=0, keep_last=0, bins=1) -> int:
 
 
 def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=None, block=1, S=None,
-                stream=None) -> Cache:
+                stream=None, **kw) -> Cache:
     """KV-cache compression (E3 protocol P:667-669; reading Z24): the first keep_first and
     last keep_last tokens of every (batch, kv-head) are kept exactly, the middle goes through
     CompressKV (Alg 2) at rank r with `bins` bins.  Q holds the prompt's queries (for R_Q) or may be
@@ -196,7 +208,7 @@ def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None
         raise WildcatError("compress_kv needs the prompt queries Q or rq")
     b, hkv, n, d = K.shape
     shape = B.make_shape(Q, K, r, bins=bins)
-    opts = B.make_opts(seed, beta, rq, block=block)
+    opts = _opts(seed, beta, rq, True, block, kw)
     C = B.kv_capacity(shape, keep_first, keep_last)
     if C == 0:
         raise WildcatError("compress_kv: invalid split (keep_first/keep_last/r/bins)")
@@ -221,7 +233,7 @@ class HostForward:
     side stream after K and Q, so it overlaps the selection) has landed, wildcat_attend, D2H of O
     into a pinned buffer, synchronise.  Every step is a C-ABI call (include/wildcat.h)."""
 
-    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, bins=1, device="cuda"):
+    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, bins=1, device="cuda", **kw):
         dev = torch.device(device)
         self.dev, self.r = dev, int(r)
         self.Qd = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
@@ -230,7 +242,7 @@ class HostForward:
         self.Od = torch.empty(Q.shape, dtype=Q.dtype, device=dev)
         self.Oh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
         self.shape = B.make_shape(self.Qd, self.Kd, r, bins=bins)
-        self.opts = B.make_opts(seed, beta, rq, clip, block=block)
+        self.opts = _opts(seed, beta, rq, clip, block, kw)
         units, d = self.shape.batch * self.shape.heads_kv, self.shape.d
         rb, R = B.coreset_rows(self.shape.n, r, bins)
         self.S = torch.empty(units, R, dtype=torch.int32, device=dev)
@@ -281,14 +293,15 @@ class HostForward:
 _host_cache: dict = {}
 
 
-def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, bins=1, out=None):
+def forward_host(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, device="cuda", block=1, bins=1, out=None, **kw):
     """End-to-end call with host (CPU) buffers: H2D copies, the CUDA path, D2H copy of O (into `out`
     if given, else into a new host tensor).  Device buffers persist per (shapes, options); see
     HostForward.  Calls with the same key share those device buffers: serialise them."""
-    key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), int(bins), str(device))
+    key = (tuple(Q.shape), tuple(K.shape), Q.dtype, int(r), seed, beta, rq, clip, int(block), int(bins), str(device),
+           tuple(sorted(kw.items())))
     hf = _host_cache.get(key)
     if hf is None:
-        hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, bins=bins, device=device)
+        hf = HostForward(Q, K, r, seed=seed, beta=beta, rq=rq, clip=clip, block=block, bins=bins, device=device, **kw)
         _host_cache[key] = hf
     return hf(Q, K, V, out=out)
 
@@ -340,13 +353,13 @@ class NshardComm:
 
 
 def forward_nshard(comm: NshardComm, Q, K, V, r, n_global, n_offset, seed=0, beta=None, rq=None, clip=True,
-                   S=None, r_eff=None, out=None, stream=None):
+                   S=None, r_eff=None, out=None, stream=None, **kw):
     """Alg 4 for one (batch, kv-head) unit whose keys are sharded over the communicator's ranks.
     K, V: this rank's [1, 1, n_local, d] shard at global offset n_offset; Q: [1, hq, m_local, d]."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     shape = B.make_shape(Q, K, r)
-    opts = B.make_opts(seed, beta, rq, clip)
+    opts = _opts(seed, beta, rq, clip, 1, kw)
     O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device, stream)
     if out is None:

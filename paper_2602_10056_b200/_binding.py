@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(_HERE, "libwildcat.so")
 
 WC_F32, WC_BF16 = 0, 1
 WC_OP_SELECT, WC_OP_WEIGHTS, WC_OP_ATTEND, WC_OP_FORWARD, WC_OP_FORWARD_NSHARD = 0, 1, 2, 3, 4
-WC_NO_CLIP = 1
+WC_NO_CLIP, WC_TAU_ONE, WC_NO_RECENTER, WC_CHECK_FINITE = 1, 2, 4, 8
+WC_ENONFINITE = -8
 
 
 class WildcatError(RuntimeError):
@@ -33,7 +34,7 @@ class wc_shape(ctypes.Structure):
 
 class wc_opts(ctypes.Structure):
     _fields_ = [("beta", ctypes.c_double), ("rq", ctypes.c_double), ("seed", ctypes.c_uint64),
-                ("flags", ctypes.c_uint32), ("block", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("block", ctypes.c_uint32), ("unit_offset", ctypes.c_uint64)]
 
 
 _lib = None
@@ -91,7 +92,13 @@ def lib():
     return _lib
 
 
+class NonFiniteInput(WildcatError):
+    """WC_CHECK_FINITE found a NaN or Inf in an input."""
+
+
 def _check(rc: int, what: str) -> None:
+    if rc == WC_ENONFINITE:
+        raise NonFiniteInput(f"{what}: {lib().wc_strerror(rc).decode()} ({rc})")
     if rc != 0:
         raise WildcatError(f"{what}: {lib().wc_strerror(rc).decode()} ({rc})")
 
@@ -122,9 +129,15 @@ def coreset_rows(n: int, r: int, bins: int = 1):
     return rb, int(bins) * rb
 
 
-def make_opts(seed=0, beta=None, rq=None, clip=True, block=1) -> wc_opts:
+def make_opts(seed=0, beta=None, rq=None, clip=True, block=1, unit_offset=0, tau_one=False, recenter=True,
+              check_finite=False) -> wc_opts:
+    """wc_opts: unit_offset = global id of the call's unit 0 (PAR2 partitions); tau_one -> WC_TAU_ONE;
+    recenter=False -> WC_NO_RECENTER; check_finite -> WC_CHECK_FINITE (include/wildcat.h)."""
+    flags = ((0 if clip else WC_NO_CLIP) | (WC_TAU_ONE if tau_one else 0) | (0 if recenter else WC_NO_RECENTER)
+             | (WC_CHECK_FINITE if check_finite else 0))
     return wc_opts(beta=-1.0 if beta is None else float(beta), rq=-1.0 if rq is None else float(rq),
-                   seed=int(seed) & 0xFFFFFFFFFFFFFFFF, flags=0 if clip else WC_NO_CLIP, block=int(block))
+                   seed=int(seed) & 0xFFFFFFFFFFFFFFFF, flags=flags, block=int(block),
+                   unit_offset=int(unit_offset))
 
 
 def _stream(stream):

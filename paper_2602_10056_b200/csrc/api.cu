@@ -3,6 +3,7 @@
 // of the method runs in the sm_100a kernels of prologue.cu / select.cu / weights.cu / attend.cu.
 #include <algorithm>
 #include <cmath>
+#include <initializer_list>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -104,21 +105,59 @@ double rq_of(const wc_opts *o) {
     return o->rq;
 }
 
-// Selection dispatch: sequential Alg 1, or the blocked variant when opts->block >= 2.
-int run_select(const wc::Dims &D, const wc_opts *o, const void *K, double *stats, wc::SelectBufs sb, int32_t *S,
-               int32_t *r_eff, double *L, cudaStream_t st) {
+// Selection dispatch: sequential Alg 1, or the blocked variant when opts->block >= 2.  unit0 = the
+// Philox id of the call's first sub-unit: opts->unit_offset * B (PAR2; readings Z2, Z23).
+int run_select(const wc::Dims &D, const wc_opts *o, uint64_t unit0, const void *K, double *stats, wc::SelectBufs sb,
+               int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     if (o->block >= 2) {
-        const int k = wc::launch_select_blocked(D, K, stats, sb, o->seed, (int)o->block, S, r_eff, L, st);
+        const int k = wc::launch_select_blocked(D, K, stats, sb, o->seed, unit0, (int)o->block, S, r_eff, L, st);
         return k == -2 ? WC_EUNSUPPORTED : (k < 0 ? WC_ECUDA : k);
     }
-    const int k = wc::launch_select(D, K, stats, sb, o->seed, S, r_eff, L, st);
+    const int k = wc::launch_select(D, K, stats, sb, o->seed, unit0, S, r_eff, L, st);
     return k < 0 ? WC_ECUDA : k;
 }
 
+int pflags_of(const wc_opts *o) {
+    int f = 0;
+    if (o && (o->flags & WC_TAU_ONE)) f |= wc::kPfTauOne;
+    if (o && (o->flags & WC_NO_RECENTER)) f |= wc::kPfNoRecenter;
+    return f;
+}
+
+// WC_CHECK_FINITE (debug): scan the inputs before anything else is launched, synchronise the stream
+// once, and report WC_ENONFINITE if one holds a NaN / Inf.  `scratch` (4 device bytes the call may
+// overwrite: its workspace or an output) receives the flag.
+struct Arr {
+    const void *p;
+    int64_t count;
+};
+int check_finite(const wc_opts *o, int dtype, void *scratch, std::initializer_list<Arr> arrs, cudaStream_t st,
+                 int *launches) {
+    if (!o || !(o->flags & WC_CHECK_FINITE)) return WC_OK;
+    if (!scratch) return WC_OK;  // nothing to scan (no inputs with elements)
+    int *flag = static_cast<int *>(scratch);
+    if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess) return WC_ECUDA;
+    for (const Arr &a : arrs) {
+        const int k = wc::launch_check_finite(a.p, a.count, dtype, flag, st);
+        if (k < 0) return WC_ECUDA;
+        *launches += k;
+    }
+    int h = 0;
+    if (cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return WC_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return WC_ECUDA;
+    return h ? WC_ENONFINITE : WC_OK;
+}
+
+int64_t q_elems(const wc_shape *s) { return (int64_t)s->batch * s->heads_q * s->m * s->d; }
+int64_t kv_elems(const wc_shape *s) { return (int64_t)s->batch * s->heads_kv * s->n * s->d; }
+
 int check_opts(const wc_opts *o, const wc_shape *s) {
     if (!o) return WC_EINVAL;
+    if (o->flags & ~WC_FLAGS_ALL) return WC_EINVAL;
     if (o->block > (uint32_t)WC_MAX_BLOCK) return WC_EINVAL;
-    if (plan_of(s).rb > WC_MAX_R) return WC_EUNSUPPORTED;  // solve / blocked plan (every selection path)
+    const Plan p = plan_of(s);
+    if (p.rb > WC_MAX_R) return WC_EUNSUPPORTED;  // solve / blocked plan (every selection path)
+    if (o->block >= 2 && !wc::select_blocked_plan_ok(p.Ds, (int)o->block)) return WC_EUNSUPPORTED;
     return WC_OK;
 }
 
@@ -235,15 +274,17 @@ int select_stage(const Plan &p, const wc_opts *o, double beta, double rq, const 
     pp.nS = (int64_t)Us * p.rb;
     pp.zero_L = L;
     pp.nL = (int64_t)Us * p.rb * p.rb;
-    int k = wc::launch_prologue(p.D, Q, K, V, rq, beta, pp, p.B > 1 ? w.stats_u : stats, w.sb.nrm2, vmin, vmax, st);
+    const int pf = pflags_of(o);
+    int k = wc::launch_prologue(p.D, Q, K, V, rq, beta, pp, p.B > 1 ? w.stats_u : stats, w.sb.nrm2, vmin, vmax, pf,
+                                st);
     if (k < 0) return WC_ECUDA;
     *launches += k;
     if (p.B > 1) {
-        if ((k = wc::launch_bins_stats(p.D, p.B, beta, w.stats_u, w.sb.nrm2, stats, st)) < 0) return WC_ECUDA;
+        if ((k = wc::launch_bins_stats(p.D, p.B, beta, w.stats_u, w.sb.nrm2, stats, pf, st)) < 0) return WC_ECUDA;
         *launches += k;
     }
     tmark(st);
-    if ((k = run_select(p.Ds, o, K, stats, w.sb, Ssel, Rsel, L, st)) < 0) return k;
+    if ((k = run_select(p.Ds, o, o->unit_offset * (uint64_t)p.B, K, stats, w.sb, Ssel, Rsel, L, st)) < 0) return k;
     *launches += k;
     if (p.B > 1) {
         if ((k = wc::launch_bins_pack(p.D, p.B, p.rb, w.Ssub, w.reff_sub, nullptr, nullptr, S, r_eff, nullptr, nullptr,
@@ -382,11 +423,13 @@ int wildcat_select(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_SELECT)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Plan p = plan_of(s);
+    int launches = 0;
+    if ((rc = check_finite(o, s->dtype, ws, {{Q, rq < 0.0 ? q_elems(s) : 0}, {K, kv_elems(s)}}, st, &launches)))
+        return rc;
     Carver c(ws);
     SelectWs w;
     carve_select(c, p, w);
     tmark(st, true);
-    int launches = 0;
     if ((rc = select_stage(p, o, beta_of(s, o), rq, Q, K, nullptr, w, stats, S, r_eff, L, nullptr, nullptr, st,
                            &launches)))
         return rc;
@@ -399,8 +442,8 @@ int wildcat_weights(const wc_shape *s, const wc_opts *o, const void *K, const vo
                     void *vmax, void *ws, size_t ws_bytes, void *stream) {
     int rc = check_shape(s);
     if (rc) return rc;
-    (void)o;
     if (!K || !V || !S || !r_eff || !L || !stats || !KS || !X || !vmin || !vmax) return WC_EINVAL;
+    if (o && (o->flags & ~WC_FLAGS_ALL)) return WC_EINVAL;
     if (plan_of(s).rb > WC_MAX_R) return WC_EUNSUPPORTED;  // the solve's plan
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_WEIGHTS)))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -410,9 +453,12 @@ int wildcat_weights(const wc_shape *s, const wc_opts *o, const void *K, const vo
     carve_weights(c, s, p, w);
     wc::ProloguePartials pp;
     carve_prologue(c, p.D, pp);
+    int launches = 0;
+    if ((rc = check_finite(o, s->dtype, ws, {{K, kv_elems(s)}, {V, kv_elems(s)}}, st, &launches))) return rc;
     tmark(st, true);
-    int launches = wc::launch_vrange(p.D, V, pp, vmin, vmax, st);
-    if (launches < 0) return WC_ECUDA;
+    const int kv = wc::launch_vrange(p.D, V, pp, vmin, vmax, st);
+    if (kv < 0) return WC_ECUDA;
+    launches += kv;
     tmark(st);
     if ((rc = weights_stage(p, K, V, S, r_eff, L, stats, w, false, KS, X, st, &launches))) return rc;
     tmark(st);
@@ -426,13 +472,18 @@ int wildcat_attend(const wc_shape *s, const wc_opts *o, const void *Q, const voi
     if (rc) return rc;
     if ((s->m > 0 && (!Q || !O)) || !KS || !X || !r_eff || !vmin || !vmax) return WC_EINVAL;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_ATTEND)))) return rc;
+    if (o && (o->flags & ~WC_FLAGS_ALL)) return WC_EINVAL;
     const int clip = (o && (o->flags & WC_NO_CLIP)) ? 0 : 1;
+    int nf = 0;  // the queries are the attend's only caller-provided input (O is scratch for the flag)
+    if ((rc = check_finite(o, s->dtype, s->m > 0 ? O : nullptr, {{Q, q_elems(s)}}, static_cast<cudaStream_t>(stream),
+                           &nf)))
+        return rc;
     tmark(static_cast<cudaStream_t>(stream), true);
     int n1 = wc::launch_attend(plan_of(s).Da, Q, KS, X, r_eff, vmin, vmax, beta_of(s, o), clip, O, ws,
                                static_cast<cudaStream_t>(stream));
     if (n1 < 0) return WC_ECUDA;
     tmark(static_cast<cudaStream_t>(stream));
-    return finish(n1);
+    return finish(n1 + nf);
 }
 
 int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const void *K, const void *V, void *O,
@@ -453,6 +504,8 @@ int wildcat_forward(const wc_shape *s, const wc_opts *o, const void *Q, const vo
     int32_t *reff = reff_out ? reff_out : w.reff;
     const double beta = beta_of(s, o);
     int launches = 0;
+    if ((rc = check_finite(o, s->dtype, ws, {{Q, q_elems(s)}, {K, kv_elems(s)}, {V, kv_elems(s)}}, st, &launches)))
+        return rc;
     tmark(st, true);
     if ((rc = select_stage(p, o, beta, rq, Q, K, V, w.sel, w.stats, S, reff, w.L, w.vmin, w.vmax, st, &launches)))
         return rc;
@@ -505,6 +558,9 @@ int wildcat_compress_kv(const wc_shape *s, const wc_opts *o, int32_t keep_first,
     carve_kv(c, kp, w);
     const wc::Dims Df = dims_of(&kp.full);
     int launches = 0, k;
+    if ((rc = check_finite(o, s->dtype, ws, {{Q, rq < 0.0 ? q_elems(s) : 0}, {K, kv_elems(s)}, {V, kv_elems(s)}}, st,
+                           &launches)))
+        return rc;
     tmark(st, true);
     if ((k = wc::launch_vrange(Df, V, w.ppf, vmin, vmax, st)) < 0) return WC_ECUDA;  // full V
     launches += k;
@@ -569,12 +625,17 @@ int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int6
     if (s->r > WC_MAX_R) return WC_EUNSUPPORTED;                  // the solve's plan
     if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;
+    if (o->flags & ~WC_FLAGS_ALL) return WC_EINVAL;
     const double rq = rq_of(o);
     int launches = 0;
+    if ((rc = check_finite(o, s->dtype, ws, {{Q, q_elems(s)}, {K, kv_elems(s)}, {V, kv_elems(s)}},
+                           static_cast<cudaStream_t>(stream), &launches)))
+        return rc;
+    int nf = launches;
     rc = wc::ns_forward(comm, dims_of(s), n_global, n_offset, o, beta_of(s, o), rq, Q, K, V, O, S, r_eff, ws,
                         static_cast<cudaStream_t>(stream), &launches);
     if (rc) return rc;
-    return finish(launches);
+    return finish(launches + nf);
 }
 
 const char *wc_strerror(int st) {
@@ -587,6 +648,7 @@ const char *wc_strerror(int st) {
         case WC_ECUDA: return "CUDA launch or runtime error";
         case WC_ENCCL: return "NCCL error";
         case WC_EUNSUPPORTED: return "unsupported configuration in this build (bins not dividing n, n-sharded bins/blocks, r too large for blocked selection)";
+        case WC_ENONFINITE: return "non-finite input (NaN or Inf) found by WC_CHECK_FINITE";
     }
     return "unknown status";
 }
@@ -609,6 +671,6 @@ int wc_timing_read(float *ms, int cap) {
     return k;
 }
 
-int wc_version(void) { return 103; }
+int wc_version(void) { return 200; }
 
 }  // extern "C"

@@ -19,7 +19,8 @@ namespace {
 constexpr int kBT = 256;
 
 __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restrict__ stats_u, const double *__restrict__ nrm2,
-                                                         int64_t nb, int d, int bins, double beta, double *__restrict__ stats_b) {
+                                                         int64_t nb, int d, int bins, double beta, double *__restrict__ stats_b,
+                                                         int tau_one) {
     pdl_wait();
     __shared__ double scr[40];
     const int su = blockIdx.x, u = su / bins;
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restric
     if (threadIdx.x == 0) {
         const double rk = sqrt(mx), rq = su_u[4];
         double tau = 1.0;
-        if (rq * rk > 0.0) {  // Eq. 7 with n_b (Z12)
+        if (!tau_one && rq * rk > 0.0) {  // Eq. 7 with n_b (Z12); WC_TAU_ONE: tau = 1
             const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
             const double b0 = log((double)nb) / (beta * rq * rk) + 2.0;
             const double w = lambert_w0_dev(b0 / (2.0 * rho0));
@@ -132,9 +133,9 @@ __global__ void bins_unpack_kernel(const int32_t *__restrict__ S, int units, int
 }  // namespace
 
 int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
-                      cudaStream_t st) {
+                      int pflags, cudaStream_t st) {
     launch_pdl(bins_stats_kernel, dim3(D.units() * bins), dim3(kBT), 0, st, stats_u, nrm2, D.n / bins, D.d, bins, beta,
-               stats_b);
+               stats_b, (pflags & kPfTauOne) ? 1 : 0);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

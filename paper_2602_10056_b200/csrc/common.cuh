@@ -292,6 +292,10 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32
 __device__ __forceinline__ void st_f64_hint(double *p, double v, uint64_t policy) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
+__device__ __forceinline__ void st_f64x2_hint(double *p, double a, double b, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(policy)
+                 : "memory");
+}
 
 // 8-byte asynchronous global -> shared copy (LDGSTS, L1-allocating) and the wait for all of them.
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
@@ -301,6 +305,19 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Order this thread's generic-proxy global writes before later async-proxy (TMA) reads.
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// generic-proxy shared-memory accesses of this thread ordered before later async-proxy (bulk copy) writes
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Flags shared by a producer warp and the compute warps, which share no barrier: every access is a
+// shared-memory atomic, so it is one coherent operation (and not a data race for compute-sanitizer).
+__device__ __forceinline__ int flag_ld(volatile int *p) { return atomicAdd(const_cast<int *>(p), 0); }
+__device__ __forceinline__ void flag_st(volatile int *p, int v) { atomicExch(const_cast<int *>(p), v); }
+__device__ __forceinline__ long long flag_ld64(volatile long long *p) {
+    return (long long)atomicAdd(reinterpret_cast<unsigned long long *>(const_cast<long long *>(p)), 0ull);
+}
+__device__ __forceinline__ void flag_st64(volatile long long *p, long long v) {
+    atomicExch(reinterpret_cast<unsigned long long *>(const_cast<long long *>(p)), (unsigned long long)v);
+}
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

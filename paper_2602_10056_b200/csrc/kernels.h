@@ -34,10 +34,16 @@ struct ProloguePartials {
 
 int prologue_num_splits(const Dims &D);
 
+// Prologue options (wc_opts.flags): kPfTauOne -> tau = 1 (WC_TAU_ONE); kPfNoRecenter -> kbar = 0 (WC_NO_RECENTER).
+constexpr int kPfTauOne = 1;
+// WC_CHECK_FINITE: *flag |= 1 if x[0, count) (dtype 0 fp32, 1 bf16) holds a NaN / Inf.  Returns launches or -1.
+int launch_check_finite(const void *x, int64_t count, int dtype, int *flag, cudaStream_t st);
+constexpr int kPfNoRecenter = 2;
+
 // A0: kbar, R_K, R_Q, tau, g, mstar -> stats[u][kStatsHead+d]; nrm2[u][l] = ||k_l - kbar||^2;
 // vmin/vmax (dtype) when non-null.  Returns number of launches (>0) or -1 on error.
 int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
-                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax, int pflags,
                     cudaStream_t st);
 
 // The two streaming passes of the prologue on their own (the n-sharded path reduces across GPUs
@@ -80,18 +86,21 @@ inline size_t f_elems_per_unit(int64_t n, int r, int cpu) {
 
 int select_ctas_per_unit(const Dims &D);
 // A1+A2: r rounds of RP-Cholesky.  Returns launches or -1.
-int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed,
+// unit0: Philox id of the call's sub-unit 0 (wc_opts.unit_offset, times B with bins).
+int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
                   int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
 
 // Blocked (accelerated) RPC, 2 <= block <= select_blocked_max_block().  Returns launches, -1 on a
 // CUDA error, -2 when r does not fit the shared-memory plan.  stats[u][6..8] <- nblocks, ncand, Fread.
-int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBufs b, uint64_t seed, int block,
-                          int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
+int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
+                          int block, int32_t *S, int32_t *r_eff, double *L, cudaStream_t st);
 int select_blocked_max_block();
+// Whether the blocked kernel's shared-memory plan holds this r at this block size (host check, no launch).
+bool select_blocked_plan_ok(const Dims &D, int block);
 
 // Alg 2 binning (bins.cu): per-bin stats, pack (sub-unit -> unit layout), unpack (S only).
 int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
-                      cudaStream_t st);
+                      int pflags, cudaStream_t st);
 int launch_bins_pack(const Dims &D, int bins, int rb, const int32_t *Ssub, const int32_t *reff_sub, const void *KSsub,
                      const float *Xsub, int32_t *S, int32_t *reff, void *KS, float *X, cudaStream_t st);
 int launch_bins_unpack(const Dims &D, int bins, int rb, const int32_t *S, int32_t *Ssub, int32_t *reff_sub,

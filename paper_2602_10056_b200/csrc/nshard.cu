@@ -225,9 +225,9 @@ __global__ void ns_pro_reduce1(int d, int P, const double *colsum, const float *
 
 template <typename T>
 __global__ void ns_pro_final1(int64_t n_global, int d, const double *sumbuf, const double *maxbuf, double *stats,
-                              T *vmin, T *vmax) {
+                              T *vmin, T *vmax, int no_recenter) {
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
-        stats[kStatsHead + j] = sumbuf[j] / (double)n_global;
+        stats[kStatsHead + j] = no_recenter ? 0.0 : sumbuf[j] / (double)n_global;  // WC_NO_RECENTER: kbar = 0
         vmin[j] = from_f32<T>((float)(-maxbuf[1 + j]));
         vmax[j] = from_f32<T>((float)maxbuf[1 + d + j]);
     }
@@ -243,12 +243,12 @@ __global__ void ns_pro_reduce2(int P, const double *rk2, double *rkbuf) {
 
 // tau (Eq. 7 with the global n), g, mstar; then the loop state.
 __global__ void ns_tau(int64_t n_global, int r, const double *rkbuf, const double *maxbuf, double rq_given,
-                       double beta, double *stats, Ctl *ctl) {
+                       double beta, double *stats, Ctl *ctl, int tau_one) {
     if (threadIdx.x != 0) return;
     const double rk = sqrt(rkbuf[0]);
     const double rq = rq_given >= 0.0 ? rq_given : sqrt(maxbuf[0]);
     double tau = 1.0;
-    if (rq * rk > 0.0) {
+    if (!tau_one && rq * rk > 0.0) {
         const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
         const double b0 = log((double)n_global) / (beta * rq * rk) + 2.0;
         const double w = lambert_w0_dev(b0 / (2.0 * rho0));
@@ -302,7 +302,7 @@ __device__ __forceinline__ void ns_pick_owner(int i, int64_t n, int64_t n_off, i
 // Global pivot draw; the owner rank writes the pivot packet {s, p_s, k_s[d], F[0:i, s]}.
 template <typename T, int D>
 __global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int rank, int64_t n, int64_t n_off,
-                                                int nchunks, uint64_t seed, const double *ranktot,
+                                                int nchunks, uint64_t seed, uint64_t unit_id, const double *ranktot,
                                                 const double *ctot, const double *p, const T *K, const double *F,
                                                 double *packet, Ctl *ctl, P2PRound pw, P2PRound px) {
     __shared__ double scr[40];
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kNsT) ns_pick(int i, int r, int world, int ran
                 ctl->r_eff = i;
                 sh_done = 1;
             } else {
-                const double t = pivot_uniform(seed, (uint32_t)i, 0ull) * Tt;
+                const double t = pivot_uniform(seed, (uint32_t)i, unit_id) * Tt;
                 double acc = 0.0, excl = 0.0, last_excl = 0.0;
                 int ow = -1, last = -1;
                 for (int q = 0; q < world; ++q) {
@@ -627,12 +627,12 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
     WC_NCCL(coll(w.sumbuf, w.sumbuf, D, 0));
     WC_NCCL(coll(w.maxbuf, w.maxbuf, 1 + 2 * D, 1));
     ns_pro_final1<T><<<1, 128, 0, st>>>(n_global, D, w.sumbuf, w.maxbuf, w.stats, static_cast<T *>(w.vmin),
-                                        static_cast<T *>(w.vmax));
+                                        static_cast<T *>(w.vmax), (o->flags & WC_NO_RECENTER) ? 1 : 0);
     if (launch_prologue_pass2(Dm, K, w.pp, w.stats, w.nrm2, st) < 0) return WC_ECUDA;
     ns_pro_reduce2<<<1, 32, 0, st>>>(w.pp.P, w.pp.rk2, w.rkbuf);
     WC_NCCL(coll(w.rkbuf, w.rkbuf, 1, 1));
     ns_tau<<<1, 32, 0, st>>>(n_global, r, w.rkbuf, w.maxbuf, want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, w.stats,
-                             w.ctl);
+                             w.ctl, (o->flags & WC_TAU_ONE) ? 1 : 0);
     ns_init<<<nch, kNsT, 0, st>>>(n, w.nrm2, w.stats, w.p, w.ctot);
     launches += 8;
     // ---- A1 + A2: r rounds
@@ -650,7 +650,7 @@ int ns_forward_t(Comm *cm, const Dims &Dm, int64_t n_global, int64_t n_off, cons
         }
         ns_local_total<<<1, 32, 0, st>>>(nch, w.ctot, w.ctl, w.sendtot, ptot);
         if (!cm->p2p) WC_NCCL(coll(w.sendtot, w.ranktot, 1, 2));
-        ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, w.ranktot, w.ctot, w.p,
+        ns_pick<T, D><<<1, kNsT, 0, st>>>(i, r, cm->world, cm->rank, n, n_off, nch, o->seed, o->unit_offset, w.ranktot, w.ctot, w.p,
                                            static_cast<const T *>(K), w.F, w.packet, w.ctl, ptot, ppk);
         if (!cm->p2p) WC_NCCL(coll(w.packet, w.packet, 2 + D + r, 0));
         upd<<<nch, kNuT, usm, st>>>(i, r, n, n_off, static_cast<const T *>(K), w.stats, w.packet, w.F, w.p, w.ctot,

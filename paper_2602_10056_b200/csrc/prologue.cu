@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass1(const T *__restrict__ Q, c
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
-                                                     T *vmin, T *vmax) {
+                                                     T *vmin, T *vmax, int no_recenter) {
     pdl_wait();
     __shared__ double s_t[kPT];
     __shared__ float s_a[kPT], s_b[kPT];
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, co
         __syncthreads();
     }
     if (tid == 0) {
-        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = s_t[0] / (double)n;
+        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = no_recenter ? 0.0 : s_t[0] / (double)n;
         if (vmin) {
             vmin[(int64_t)u * d + j] = from_f32<T>(s_a[0]);
             vmax[(int64_t)u * d + j] = from_f32<T>(s_b[0]);
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kPT) prologue_kbar(int64_t n, int d, int P, co
 template <typename T>
 __global__ void __launch_bounds__(kPT) prologue_kbar_small(int64_t n, int d, int P, const double *colsum,
                                                      const float *vmin_p, const float *vmax_p, double *stats,
-                                                     T *vmin, T *vmax) {
+                                                     T *vmin, T *vmax, int no_recenter) {
     pdl_wait();
     __shared__ double s_t[kPT];
     __shared__ float s_a[kPT], s_b[kPT];
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kPT) prologue_kbar_small(int64_t n, int d, int
             aa = fminf(aa, s_a[gg * 32 + threadIdx.x]);
             bb = fmaxf(bb, s_b[gg * 32 + threadIdx.x]);
         }
-        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = tt / (double)n;
+        if (stats) stats[(int64_t)u * (kStatsHead + d) + kStatsHead + j] = no_recenter ? 0.0 : tt / (double)n;
         if (vmin) {
             vmin[(int64_t)u * d + j] = from_f32<T>(aa);
             vmax[(int64_t)u * d + j] = from_f32<T>(bb);
@@ -213,14 +213,15 @@ inline int kbar_threads(int P) {
 // kbar / value-range finalisation: one block per column for many splits, 32 columns per block else
 template <typename T>
 void launch_kbar(const Dims &D, int P, const ProloguePartials &pp, double *stats, void *vmin, void *vmax,
-                 cudaStream_t st) {
+                 cudaStream_t st, int no_recenter = 0) {
     if (P >= 64)
         launch_pdl(prologue_kbar<T>, dim3(D.units(), D.d), dim3(kbar_threads(P)), 0, st, D.n, D.d, P,
                    (const double *)pp.colsum, (const float *)pp.vmin, (const float *)pp.vmax, stats,
-                   static_cast<T *>(vmin), static_cast<T *>(vmax));
+                   static_cast<T *>(vmin), static_cast<T *>(vmax), no_recenter);
     else
         prologue_kbar_small<T><<<dim3(D.units(), (D.d + 31) / 32), kPT, 0, st>>>(
-            D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats, static_cast<T *>(vmin), static_cast<T *>(vmax));
+            D.n, D.d, P, pp.colsum, pp.vmin, pp.vmax, stats, static_cast<T *>(vmin), static_cast<T *>(vmax),
+            no_recenter);
 }
 
 // Pass 2: nrm2_l = ||k_l - kbar||^2 (fp64) and the split max.  CPR threads per key.
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kPT) prologue_pass2(const T *__restrict__ K, i
 // tau (Eq. 7), g, mstar.  One thread per unit.
 // One warp per unit: maxima over the P splits, then lane 0 evaluates Eq. 7.
 __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *rk2, const double *rq2,
-                             double rq_given, double beta, double *stats) {
+                             double rq_given, double beta, double *stats, int tau_one) {
     pdl_wait();
     const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (u >= units) return;
@@ -288,8 +289,8 @@ __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *r
     if (lane != 0) return;
     const double rk = sqrt(mk);
     const double rq = rq_given >= 0.0 ? rq_given : sqrt(mq);
-    double tau = 1.0;
-    if (rq * rk > 0.0) {
+    double tau = 1.0;  // WC_TAU_ONE, or the R_Q R_K = 0 fallback (reading Z20)
+    if (!tau_one && rq * rk > 0.0) {
         const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
         const double b0 = log((double)n) / (beta * rq * rk) + 2.0;
         const double w = lambert_w0_dev(b0 / (2.0 * rho0));
@@ -307,7 +308,7 @@ __global__ void prologue_tau(int units, int64_t n, int d, int P, const double *r
 
 template <typename T>
 int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
-                      ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                      ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax, int pflags,
                       cudaStream_t st) {
     const int units = D.units();
     const int P = pp.P;
@@ -321,12 +322,13 @@ int launch_prologue_t(const Dims &D, const void *Q, const void *K, const void *V
                                                static_cast<const T *>(V ? V : K), D.n, mq, D.d, P, want_q,
                                                want_v, pp.colsum, pp.vmin, pp.vmax, pp.rq2,
                                                (int64_t)D.group() * D.m, pp.fill_S, pp.nS, pp.zero_L, pp.nL);
-    launch_kbar<T>(D, P, pp, stats, want_v ? vmin : nullptr, want_v ? vmax : nullptr, st);
+    launch_kbar<T>(D, P, pp, stats, want_v ? vmin : nullptr, want_v ? vmax : nullptr, st,
+                   (pflags & kPfNoRecenter) ? 1 : 0);
     launch_pdl(prologue_pass2<T>, grid, dim3(kPT), 0, st, static_cast<const T *>(K), D.n, D.d, P,
                (const double *)stats, nrm2, pp.rk2);
     launch_pdl(prologue_tau, dim3((unsigned)ceil_div(units, 4)), dim3(128), 0, st, units, D.n, D.d, P,
                (const double *)pp.rk2, (const double *)pp.rq2,
-                                                      want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats);
+               want_q ? -1.0 : (rq < 0.0 ? 0.0 : rq), beta, stats, (pflags & kPfTauOne) ? 1 : 0);
     return cudaPeekAtLastError() == cudaSuccess ? 4 : -1;
 }
 
@@ -382,6 +384,40 @@ int launch_vrange(const Dims &D, const void *V, ProloguePartials pp, void *vmin,
     return launch_vrange_t<__nv_bfloat16>(D, V, pp, vmin, vmax, st);
 }
 
+// WC_CHECK_FINITE: flag |= 1 if any element of x[0, count) is NaN or +-Inf (exponent field all ones).
+// bf16 and fp32 are tested on their bit patterns, 16 bytes per thread per step.
+__global__ void __launch_bounds__(256) check_finite_kernel(const uint4 *x, int64_t nvec, const unsigned char *tail,
+                                                            int64_t ntail, int esz, int *flag) {
+    const uint32_t m32 = 0x7f800000u;
+    bool bad = false;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+        const uint4 q = __ldg(x + v);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (esz == 4) bad |= (w[k] & m32) == m32;
+            else bad |= ((w[k] & 0x7f80u) == 0x7f80u) || (((w[k] >> 16) & 0x7f80u) == 0x7f80u);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < ntail) {  // the < 16 trailing bytes, one element per thread
+        if (esz == 4) bad |= (reinterpret_cast<const uint32_t *>(tail)[threadIdx.x] & m32) == m32;
+        else bad |= (reinterpret_cast<const uint16_t *>(tail)[threadIdx.x] & 0x7f80u) == 0x7f80u;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+int launch_check_finite(const void *x, int64_t count, int dtype, int *flag, cudaStream_t st) {
+    if (!x || count <= 0) return 0;
+    const int esz = dtype == 0 ? 4 : 2;
+    const int64_t bytes = count * esz, nvec = bytes / 16;
+    const int64_t ntail = (bytes - nvec * 16) / esz;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(nvec, 256)));
+    check_finite_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4 *>(x), nvec,
+                                                static_cast<const unsigned char *>(x) + nvec * 16, ntail, esz, flag);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 int prologue_num_splits(const Dims &D) {
     const int64_t by_rows = ceil_div(std::max<int64_t>(D.n, (int64_t)D.group() * D.m), 256);
     const int64_t cap = std::max<int64_t>(1, 1184 / D.units());
@@ -389,10 +425,10 @@ int prologue_num_splits(const Dims &D) {
 }
 
 int launch_prologue(const Dims &D, const void *Q, const void *K, const void *V, double rq, double beta,
-                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax,
+                    ProloguePartials pp, double *stats, double *nrm2, void *vmin, void *vmax, int pflags,
                     cudaStream_t st) {
-    if (D.dtype == 0) return launch_prologue_t<float>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, st);
-    return launch_prologue_t<__nv_bfloat16>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, st);
+    if (D.dtype == 0) return launch_prologue_t<float>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, pflags, st);
+    return launch_prologue_t<__nv_bfloat16>(D, Q, K, V, rq, beta, pp, stats, nrm2, vmin, vmax, pflags, st);
 }
 
 }  // namespace wc

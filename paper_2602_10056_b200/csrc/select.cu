@@ -49,6 +49,7 @@ struct SelArgs {
     int64_t ldF;  // row stride of F (n rounded up to 32: every row segment is 256-byte aligned)
     int units, r, cpu;
     uint64_t seed;
+    uint64_t unit0;  // Philox id of sub-unit 0 (wc_opts.unit_offset [x B]); unit u draws stream unit0 + u
     unsigned long long *trace;  // debug (WC_SELECT_TRACE): [r][16] globaltimer stamps of CTA 0
     int rkeep;                  // F rows [0, rkeep) are kept L2-resident (evict_last); later rows evict_first
     int nstm;                   // TMA kernel: super-tiles per CTA slice (tile-major F: [cpu][nstm][r][256])
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
             }
             const bool done = Ttot <= theta;
             if (!done) {
-                const double t = pivot_uniform(a.seed, (uint32_t)i, (uint64_t)u) * Ttot;
+                const double t = pivot_uniform(a.seed, (uint32_t)i, a.unit0 + (uint64_t)u) * Ttot;
                 const unsigned hit = __ballot_sync(0xffffffffu, b1 > b0 && incl > t);
                 const unsigned pos = __ballot_sync(0xffffffffu, b1 > b0 && v > 0.0);
                 const int L = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
@@ -346,8 +347,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], kCW);
         }
-        sh_stop = 0;
-        sh_rounds_done = 0;
+        flag_st(&sh_stop, 0);
+        flag_st(&sh_rounds_done, 0);
         fence_mbar_init();
     }
     __syncthreads();  // the only CTA-wide barrier: everything after is role-specific
@@ -360,8 +361,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
             uint32_t ph = 0, issued = 0, par = 0;
             for (int i = 2; i < a.r; ++i) {
                 const int rows = i - 1;  // TMA rows 0..i-2; row i-1 is read directly
-                while (sh_rounds_done < i - 1) {  // rows 0..i-2 of this CTA written and visible
-                    if (sh_stop) goto drain;
+                while (flag_ld(&sh_rounds_done) < i - 1) {  // rows 0..i-2 of this CTA written and visible
+                    if (flag_ld(&sh_stop)) goto drain;
                     __nanosleep(32);
                 }
                 for (int k = 0; k < nst; ++k) {
@@ -371,9 +372,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
                         const int nr = min(kRPS, rows - j0);
                         const uint32_t bytes = (uint32_t)(nr * wk * sizeof(double));
                         while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
-                            if (sh_stop) goto drain;
+                            if (flag_ld(&sh_stop)) goto drain;
                         }
-                        if (sh_stop) goto drain;
+                        if (flag_ld(&sh_stop)) goto drain;
                         mbar_arrive_expect_tx(&full[stage], bytes);
                         // one contiguous bulk copy of nr rows x 256 keys (tile-major layout)
                         bulk_g2s_hint(ring + (size_t)stage * kRPS * kST, blk + (int64_t)j0 * wk, bytes, &full[stage],
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         // ---- A1a (warp 0): totals over the per-CTA residual sums (one L2 round trip, cached in
         // registers), exhaustion test, Philox uniform, owning CTA c*.  Fixed order.
         if (w == 0) {
-            const double uni = pivot_uniform(a.seed, (uint32_t)i, (uint64_t)u);
+            const double uni = pivot_uniform(a.seed, (uint32_t)i, a.unit0 + (uint64_t)u);
             const double *pc = a.part + (int64_t)u * 2 * kMaxCpu + (i & 1) * kMaxCpu;
             const int per = (a.cpu + 31) / 32;
             const int b0 = lane * per, b1 = min(a.cpu, b0 + per);
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
         cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_rounds_done, i + 1);
         WC_TR(11);
     }
-    if (tid == 0) sh_stop = 1;
+    if (tid == 0) flag_st(&sh_stop, 1);
     if (c == 0 && tid == 0) {
         a.r_eff[u] = i;
         double *stw = const_cast<double *>(st);
@@ -700,13 +701,13 @@ void dump_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
 }
 
 template <typename T, int D>
-int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectBufs b, uint64_t seed,
+int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
                      int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     SelArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.ldF = f_ld(Dm.n); a.units = Dm.units(); a.r = Dm.r;
     a.nstm = f_tile_nst(Dm.n, select_ctas_per_unit(Dm));
-    a.cpu = select_ctas_per_unit(Dm); a.seed = seed; a.trace = nullptr;
+    a.cpu = select_ctas_per_unit(Dm); a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
     {
         // keep the first F rows L2-resident: ~3/4 of L2 for F (the rest holds K, p and streams)
         int dev = 0, l2 = 0;
@@ -756,13 +757,13 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
 }
 
 template <typename T>
-int launch_select_t(const Dims &Dm, const void *K, const double *stats, SelectBufs b, uint64_t seed,
+int launch_select_t(const Dims &Dm, const void *K, const double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
                     int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     switch (Dm.d) {
-        case 16: return launch_select_td<T, 16>(Dm, K, stats, b, seed, S, r_eff, L, st);
-        case 32: return launch_select_td<T, 32>(Dm, K, stats, b, seed, S, r_eff, L, st);
-        case 64: return launch_select_td<T, 64>(Dm, K, stats, b, seed, S, r_eff, L, st);
-        case 128: return launch_select_td<T, 128>(Dm, K, stats, b, seed, S, r_eff, L, st);
+        case 16: return launch_select_td<T, 16>(Dm, K, stats, b, seed, unit0, S, r_eff, L, st);
+        case 32: return launch_select_td<T, 32>(Dm, K, stats, b, seed, unit0, S, r_eff, L, st);
+        case 64: return launch_select_td<T, 64>(Dm, K, stats, b, seed, unit0, S, r_eff, L, st);
+        case 128: return launch_select_td<T, 128>(Dm, K, stats, b, seed, unit0, S, r_eff, L, st);
     }
     return -1;
 }
@@ -779,10 +780,10 @@ int select_ctas_per_unit(const Dims &D) {
     return (int)std::min<int64_t>(std::min<int64_t>(per_unit, by_n), kMaxCpu);
 }
 
-int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed,
+int launch_select(const Dims &D, const void *K, const double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
                   int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
-    if (D.dtype == 0) return launch_select_t<float>(D, K, stats, b, seed, S, r_eff, L, st);
-    return launch_select_t<__nv_bfloat16>(D, K, stats, b, seed, S, r_eff, L, st);
+    if (D.dtype == 0) return launch_select_t<float>(D, K, stats, b, seed, unit0, S, r_eff, L, st);
+    return launch_select_t<__nv_bfloat16>(D, K, stats, b, seed, unit0, S, r_eff, L, st);
 }
 
 }  // namespace wc

@@ -47,8 +47,17 @@ namespace wc {
 
 namespace {
 
-constexpr int kBMax = 16;  // largest supported block size b
-constexpr int kElimW = 7;  // compute warp that runs the rejection (kCW - 1)
+constexpr int kBMax = 32;  // largest supported block size b (candidate slots of the NSL = 32 plan)
+
+// Warp roles: compute warps 0..kCW-1, the TMA producer warp kWP, the rejection warp kWE.  The
+// rejection warp is warp 11, on SM sub-partition 3 (warps 9 and 10 leave at once): sub-partition 3
+// hosts compute warps 3 and 7, the last warps of a super-tile, which are the ones idle in a partial
+// tile, so the sequential rejection chain is not starved of issue slots by two DMMA streams.  12 warps
+// cost no registers over 10 (the register file is allocated in 4-warp units: 168 per thread either way).
+constexpr int kWP = kCW, kWE = kCW + 3;
+constexpr int kBThreads = kCT + 128;
+// named barrier 2: the compute warps and the rejection warp (hand-over of H and of the accepted pivots)
+__device__ __forceinline__ void ce_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kCT + 32) : "memory"); }
 
 __device__ __forceinline__ double accept_uniform(uint64_t seed, uint32_t cand, uint64_t unit) {
     uint32_t c[4] = {cand, (uint32_t)unit, (uint32_t)(unit >> 32), 0x41435054u};  // 'ACPT'
@@ -72,7 +81,7 @@ struct BlkArgs {
     double *stats;
     const double *nrm2;
     double *p;      // [2][units][n]
-    double *F;      // per unit tile-major [cpu][nst][r][256]
+    double *F;      // per unit tile-major [cpu][nst][r][BT]
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ngroups] residual sums of 32-key groups
@@ -83,6 +92,7 @@ struct BlkArgs {
     int64_t n;
     int units, r, cpu, b;
     uint64_t seed;
+    uint64_t unit0;  // Philox id of sub-unit 0 (wc_opts.unit_offset [x B]); unit u draws stream unit0 + u
     unsigned long long *trace;  // debug (WC_SELECT_TRACE): [r][16] globaltimer stamps of CTA 0 per block
 };
 
@@ -95,11 +105,26 @@ __device__ __forceinline__ unsigned long long btimer() {
     do {                                                                                            \
         if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + (k)] = btimer(); \
     } while (0)
+#define WC_BTRE(k)                                                                                  \
+    do {                                                                                            \
+        if (a.trace && blockIdx.x == 0 && lane == 0 && blk < a.r) a.trace[blk * 16 + (k)] = btimer(); \
+    } while (0)
 
-constexpr int kBT = 512;          // keys per super-tile of the blocked kernel (64 per compute warp)
-constexpr int kBR = 4;            // F rows per ring stage (one DMMA k-step)
-constexpr int kPitch = kBT + 4;   // ring row pitch in doubles (4128 B): the 4 rows of a k-step sit 8 banks
-                                  // apart, so each half-warp of an A-fragment load is conflict-free
+constexpr int kBR = 4;  // F rows per ring stage (one DMMA k-step)
+
+// Plan of the candidate-slot count NSL (16 or 32): NT 8-column MMA n-tiles of slots, MT 8-key MMA
+// row tiles per compute warp (MT * NT * 2 = 32 fp64 accumulators per thread either way), BT keys per
+// super-tile (the tile-major F width), ring row pitch BT + 4 doubles (the 4 rows of a k-step sit 8
+// banks apart, so each half-warp of an A-fragment load is conflict-free).
+template <int NSL> struct BPlan {
+    static constexpr int NT = NSL / 8;
+    static constexpr int MT = 128 / NSL;
+    static constexpr int KPW = 8 * MT;    // keys per compute warp per super-tile
+    static constexpr int KPL = KPW / 32;  // keys per lane in the per-key triangle
+    static constexpr int BT = kCW * KPW;  // keys per super-tile (512 for NSL = 16, 256 for NSL = 32)
+    static constexpr int PITCH = BT + 4;
+    static constexpr int SPITCH = NSL + 1;  // staging row pitch (doubles) of the per-key triangle
+};
 
 // fp64 tensor-core MMA (DMMA) m8n8k4: C += A B with A 8x4 row-major (lane l holds A[l/4][l%4]),
 // B 4x8 column-major (lane l holds B[l%4][l/4]), C 8x8 (lane l holds C[l/4][2(l%4) + {0,1}]).
@@ -109,15 +134,15 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
         : "d"(a), "d"(b));
 }
 
-// MMA-operand layouts of the accepted (or candidate) pivot columns, 16 pivot slots p:
-//   Fcol: F[q, s_p] (candidate slot p) as 16 columns of stride ldc = 16k + 4 doubles: lane (tq, g)
-//        of the k-step at q0 reads Fcol[(8 nt + g) * ldc + q0 + tq] -- two wavefronts per warp load;
+// MMA-operand layouts of the candidate pivot columns (NSL slots p):
+//   Fcol: F[q, s_p] as NSL rows of stride ldc = 16k + 4 doubles: lane (tq, g) of the k-step at q0
+//        reads Fcol[(8 nt + g) * ldc + q0 + tq];
 //   kcB: centred key k_sp - kbar at dim = tq * (D/4) + t (lane tq owns a contiguous run of D/4 dims),
-//        stored at ((t * 2 + p/8) * 8 + p%8) * 4 + tq: a half-warp of 64-bit loads hits 16 distinct
+//        stored at ((t * NT + p/8) * 8 + p%8) * 4 + tq: a half-warp of 64-bit loads hits 16 distinct
 //        consecutive doubles.
-template <int D> __device__ __forceinline__ int kcb(int dim, int p) {
+template <int D, int NSL> __device__ __forceinline__ int kcb(int dim, int p) {
     constexpr int DQ = D / 4;
-    return (((dim % DQ) * 2 + (p >> 3)) * 8 + (p & 7)) * 4 + dim / DQ;
+    return (((dim % DQ) * (NSL / 8) + (p >> 3)) * 8 + (p & 7)) * 4 + dim / DQ;
 }
 
 // TC consecutive raw key elements of one row held as 32-bit words; elem() widens exactly to fp64.
@@ -150,46 +175,115 @@ template <typename T, int TC> struct KChunk {
     }
 };
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
+// Per-key triangle of KSN keys per lane at once (independent fp64 chains interleaved):
+//   F[i+aa, l] = (G[l, aa] - sum_{a2<aa} F[i+a2, l] F[i+a2, s_aa]) * (1 / sqrt(p_{s_aa}))
+// for the accepted slots aa < na in acceptance order; F rows written to frow[h] + aa * wk (key < hi),
+// residual downdate with the clamp (Z4) and p_s <- 0.  stg: the staged G rows [32 KSN keys][NSL + 1].
+template <int NSL, int KSN>
+__device__ __forceinline__ void key_triangle(const double *stg, int lane, const double *Fx, const double *rinvA,
+                                             const int *sA, int na, const int64_t (&key)[KSN], int64_t hi,
+                                             double *const (&frow)[KSN], int wk, double (&f)[KSN][NSL],
+                                             double (&pl)[KSN]) {
+    constexpr int SP = NSL + 1;
+#pragma unroll
+    for (int aa = 0; aa < NSL; ++aa) {
+#pragma unroll
+        for (int h = 0; h < KSN; ++h) f[h][aa] = 0.0;
+        if (aa < na) {
+            const double *fx = Fx + aa * NSL;
+            double c0v[KSN], c1v[KSN];  // two partial sums per key shorten the dependent chain
+#pragma unroll
+            for (int h = 0; h < KSN; ++h) {
+                c0v[h] = stg[(32 * h + lane) * SP + aa];
+                c1v[h] = 0.0;
+            }
+#pragma unroll
+            for (int a2 = 0; a2 < aa; ++a2) {
+                const double x = fx[a2];
+#pragma unroll
+                for (int h = 0; h < KSN; ++h) {
+                    if (a2 & 1) c1v[h] = fma(-f[h][a2], x, c1v[h]);
+                    else c0v[h] = fma(-f[h][a2], x, c0v[h]);
+                }
+            }
+            const double ra = rinvA[aa];
+            const int sa = sA[aa];
+#pragma unroll
+            for (int h = 0; h < KSN; ++h) {
+                const double fv = (c0v[h] + c1v[h]) * ra;
+                f[h][aa] = fv;
+                if (key[h] < hi) frow[h][(int64_t)aa * wk] = fv;
+                const double qd = __dadd_rn(pl[h], -__dmul_rn(fv, fv));
+                pl[h] = (qd > 0.0 && key[h] != sa) ? qd : 0.0;
+            }
+        }
+    }
+}
+
+// Shared-memory carve of the kernel (the launcher sizes it with the same function).
+template <int D, int NSL> struct BSmem {
+    double *ring, *Fcol, *kcB, *H0, *Fcand, *Fx, *colbuf, *cp, *c0r, *vac, *rinvA, *kb, *scr, *c0p, *spart, *sv, *sinc;
+    int *cs, *sA, *jA, *perm;
+    uint64_t *full, *empty, *colbar;
+    size_t bytes;
+    __host__ __device__ BSmem(unsigned char *base, int NS, int ldc, int cpu) {
+        using PL = BPlan<NSL>;
+        size_t o = 0;
+        // (base == nullptr: only the size is wanted)
+        auto at = [&](size_t bytes) { unsigned char *q = base ? base + o : nullptr; o += bytes; return q; };
+        auto td = [&](size_t cnt) { return reinterpret_cast<double *>(at(cnt * sizeof(double))); };
+        ring = td((size_t)NS * kBR * PL::PITCH);
+        Fcol = td((size_t)NSL * ldc);
+        kcB = td((size_t)D * NSL);
+        H0 = td(NSL * NSL);
+        Fcand = td(NSL * NSL);
+        Fx = td(NSL * NSL);
+        colbuf = td(2 * NSL);
+        cp = td(NSL);
+        c0r = td(NSL);
+        vac = td(NSL);
+        rinvA = td(NSL);
+        kb = td(D);
+        scr = td(40);
+        c0p = td(kCT);
+        spart = td(cpu);
+        sv = td(32);
+        sinc = td(32);
+        cs = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        sA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        jA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        perm = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        o = (o + 15) & ~size_t(15);
+        full = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
+        empty = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
+        colbar = reinterpret_cast<uint64_t *>(at(sizeof(uint64_t)));
+        bytes = o;
+    }
+};
+
+template <typename T, int D, int NSL>
+__global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
     pdl_wait();  // the prologue's stats / nrm2 (programmatic dependent launch)
+    using PL = BPlan<NSL>;
+    constexpr int NT = PL::NT, MT = PL::MT, KPW = PL::KPW, KPL = PL::KPL, BT = PL::BT, PITCH = PL::PITCH;
+    static_assert(MT == 4 * KPL, "row tiles 4h .. 4h + 3 hold the keys 32h .. 32h + 31 of a warp");
+    constexpr int SP = PL::SPITCH;
     constexpr int DQ = D / 4;             // dims per lane per key in the kernel-dot MMA
     constexpr int TC = 4;                 // k-steps per register chunk of the K row (8 or 16 bytes per key)
     using KC = KChunk<T, TC>;
     extern __shared__ __align__(128) unsigned char smraw[];
     const int ldc = ((a.r + 15) & ~15) + 4;
     const int ftl = ft_ld(a.r);
-    double *ring = reinterpret_cast<double *>(smraw);  // [NS][kBR][kPitch]
-    double *Fcol = ring + (size_t)NS * kBR * kPitch;    // [16][ldc] candidate columns of F
-    double *kcB = Fcol + (size_t)kBMax * ldc;           // [D][16]    (MMA layout, see kcb)
-    double *H0 = kcB + D * kBMax;                       // [16][16] block-start H of the candidates
-    double *Fcand = H0 + kBMax * kBMax;                 // [16][16] Fcand[aa][x] = F[i+aa, s_x] (candidate x)
-    double *Fx = Fcand + kBMax * kBMax;                 // [16][16] Fx[aa][a2] = F[i+a2, s_aa] (accepted order)
-    double *rowj = Fx + kBMax * kBMax;                  // [2][16]  row j of the eliminated H
-    double *cp = rowj + 2 * kBMax;                      // [16] block-start p[s_j]
-    double *c0r = cp + kBMax;                           // [16] <kbar, k_sj - kbar> per candidate
-    double *c0 = c0r + kBMax;                           // [16] ... per accepted pivot (0-padded)
-    double *vac = c0 + kBMax;                           // [16] accept uniforms
-    double *rinvA = vac + kBMax;                        // [16] 1 / sqrt(p_{s_aa}) at round i+aa
-    double *kb = rinvA + kBMax;                         // [D]
-    double *scr = kb + D;                               // [40]
-    double *Hp = scr + 40;                              // [8][4][32][2] per-warp DMMA partials of H
-    double *spart = Hp + kCW * 4 * 64;                  // [cpu] per-CTA residual sums (block start)
-    double *sv = spart + a.cpu;                         // [32] lane sums of spart (warp-0 partition)
-    double *sinc = sv + 32;                             // [32] their inclusive prefix
-    long long *cfo = reinterpret_cast<long long *>(sinc + 32);  // [16] offset of F[0, s_j] in the unit's F
-    int *cs = reinterpret_cast<int *>(cfo + kBMax);     // [16] candidates
-    int *cwk = cs + kBMax;                              // [16] row stride of F at s_j
-    int *sA = cwk + kBMax;                              // [16] accepted pivots (in order)
-    int *jA = sA + kBMax;                               // [16] their candidate slots
-    int *perm = jA + kBMax;                             // [16] slot -> acceptance index (-1: rejected)
-    uint64_t *full = reinterpret_cast<uint64_t *>(perm + kBMax);
-    uint64_t *empty = full + NS;
-    uint64_t *colbar = empty + NS;  // completion of the candidate-column bulk copies
+    BSmem<D, NSL> sm(smraw, NS, ldc, a.cpu);
+    double *ring = sm.ring, *Fcol = sm.Fcol, *kcB = sm.kcB, *H0 = sm.H0, *Fcand = sm.Fcand, *Fx = sm.Fx;
+    double *colbuf = sm.colbuf, *cp = sm.cp, *c0r = sm.c0r, *vac = sm.vac, *rinvA = sm.rinvA, *kb = sm.kb;
+    double *scr = sm.scr, *spart = sm.spart, *sv = sm.sv, *sinc = sm.sinc;
+    int *cs = sm.cs, *sA = sm.sA, *jA = sm.jA, *perm = sm.perm;
+    uint64_t *full = sm.full, *empty = sm.empty, *colbar = sm.colbar;
     __shared__ volatile int sh_stop;
     __shared__ volatile long long sh_req;  // request number << 32 | super-tile << 16 | F rows to stream
     __shared__ volatile int sh_dummy;
-    __shared__ int sh_na;
+    __shared__ int sh_na, sh_cmd;
 
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
     const int gid = lane >> 2, tq = lane & 3;
@@ -197,16 +291,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
     const int64_t n = a.n;
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
-    const int nst = (int)ceil_div(hi - lo, kBT);
-    // the per-key triangle stages both of a lane's keys at once when the ring holds [64][17] per warp
-    const bool two_keys = (size_t)NS * kBR * kPitch >= (size_t)kCW * 64 * 17;
+    const int nst = (int)ceil_div(hi - lo, BT);
     const int bsz = a.b;
+    const uint64_t uid = a.unit0 + (uint64_t)u;
+    // the per-key triangle stages both of a lane's keys at once when the ring holds [64][SP] per warp
+    const bool two_keys = (size_t)NS * kBR * PITCH >= (size_t)kCW * 64 * SP;
 
     const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
     double *st = a.stats + (int64_t)u * (kStatsHead + D);
     double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
     double *Fc = Fu + (int64_t)c * chunk * a.r;
-    auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(kBT, chunk - (int64_t)k * kBT); };
+    auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(BT, chunk - (int64_t)k * BT); };
 
     if (tid == 0) {
         for (int q = 0; q < NS; ++q) {
@@ -214,13 +309,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             mbar_init(&empty[q], kCW);
         }
         mbar_init(colbar, 1);
-        sh_stop = 0;
-        sh_req = 0;
+        flag_st(&sh_stop, 0);
+        flag_st64(&sh_req, 0);
         fence_mbar_init();
     }
     __syncthreads();  // the only CTA-wide barrier: everything after is role-specific
 
-    if (w == kCW) {
+    if (w == kWP) {
         // ============ producer warp: streams F[0:i, own slice] once per block (one bulk copy per row) ============
         if (lane == 0) {
             int stage = 0;
@@ -229,26 +324,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             const uint64_t pol = policy_evict_first();
             while (true) {
                 long long req;
-                while (((req = sh_req) >> 32) == seen) {
-                    if (sh_stop) goto drain;
+                while (((req = flag_ld64(&sh_req)) >> 32) == seen) {
+                    if (flag_ld(&sh_stop)) goto drain;
                     __nanosleep(64);
                 }
                 seen = req >> 32;
                 const int rows = (int)(req & 0xffffLL), k = (int)((req >> 16) & 0xffffLL);
                 {
-                    const double *blk = Fc + (int64_t)k * a.r * kBT;
+                    const double *blkp = Fc + (int64_t)k * a.r * BT;
                     const int wk = tile_w(k);
                     const uint32_t rb = (uint32_t)(wk * sizeof(double));
                     for (int j0 = 0; j0 < rows; j0 += kBR) {
                         const int nr = min(kBR, rows - j0);
                         while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
-                            if (sh_stop) goto drain;
-                            __nanosleep(128);  // ring full: do not steal issue slots from warp 0 (same SMSP)
+                            if (flag_ld(&sh_stop)) goto drain;
+                            __nanosleep(128);  // ring full: do not steal issue slots from the compute warp of this SMSP
                         }
                         mbar_arrive_expect_tx(&full[stage], rb * (uint32_t)nr);
-                        double *dst = ring + (size_t)stage * kBR * kPitch;
-                        for (int rr = 0; rr < nr; ++rr)  // F streams through L2 evict-first (K, p stay)
-                            bulk_g2s_hint(dst + rr * kPitch, blk + (int64_t)(j0 + rr) * wk, rb, &full[stage], pol);
+                        double *dst = ring + (size_t)stage * kBR * PITCH;
+                        // F streams through L2 evict-first so that K, p and the group sums stay resident (keeping
+                        // the first F rows evict-last instead was measured slower: the 126 MB L2 thrashes)
+                        for (int rr = 0; rr < nr; ++rr)
+                            bulk_g2s_hint(dst + rr * PITCH, blkp + (int64_t)(j0 + rr) * wk, rb, &full[stage], pol);
                         issued |= 1u << stage;
                         par = (par & ~(1u << stage)) | (ph << stage);
                         if (++stage == NS) { stage = 0; ph ^= 1u; }
@@ -258,6 +355,89 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         drain:
             for (int q = 0; q < NS; ++q)
                 if (issued & (1u << q)) mbar_wait(&full[q], (par >> q) & 1u);
+        }
+        return;
+    }
+
+    if (w > kWP && w < kWE) return;  // spare warps (register-allocation granularity)
+    if (w == kWE) {
+        // ============ rejection warp: per block, the sequential accept / eliminate loop of step 3 ============
+        // (lane e = column e of the symmetric H in registers; column j is published through shared
+        // memory).  Accepting j subtracts F_x F_e with F_x = H[x][j] / sqrt(H[j][j]), which is also
+        // F[i+aa, s_x] for the later candidates x: the coefficients of every key's triangle.
+        // It runs while the compute warps start the round-update GEMMs (kernel dots and F prefix over
+        // all candidate slots do not depend on acceptance); they pick up its results at ce_sync B.
+        int i = 0, blk = 0;
+        while (true) {
+            ce_sync();  // A: H0 of this block (or the stop command) is in shared memory
+            if (sh_cmd == 0) break;
+            const int e = lane;
+            double hc[NSL];
+#pragma unroll
+            for (int x = 0; x < NSL; ++x) hc[x] = (e < bsz && x < bsz) ? H0[x * NSL + e] : 0.0;
+            const int my_cs = e < bsz ? cs[e] : -1;
+            const double my_vp = e < bsz ? __dmul_rn(vac[e], cp[e]) : 0.0;  // v_e p[s_e]
+            bool my_acc = false;
+            int nacc = 0;
+#pragma unroll 1
+            for (int j = 0; j < bsz && i + nacc < a.r; ++j) {
+                // lane j publishes its column H[:, j] through shared memory (double-buffered by step
+                // parity: the previous user of this buffer finished before the last __syncwarp); H stays
+                // bitwise symmetric, so H[j][e] = H[e][j] = col[e]
+                double *col = colbuf + (j & 1) * NSL;
+                if (lane == j) {
+#pragma unroll
+                    for (int x = 0; x < NSL; ++x) col[x] = hc[x];
+                }
+                __syncwarp();
+                const double hjj = col[j];
+                const double hej = e < NSL ? col[e] : 0.0;  // H[j][e]
+                const int sj = __shfl_sync(0xffffffffu, my_cs, j);
+                const double vp = __shfl_sync(0xffffffffu, my_vp, j);
+                const bool dup = __any_sync(0xffffffffu, my_acc && my_cs == sj);
+                if (!dup && vp < hjj) {
+                    const double rinv = rsqrt_nr(hjj);
+                    const double fe = hej * rinv;  // F[i+nacc, s_e] = H[j][e] / sqrt(H[j][j])
+                    if (e < NSL) Fcand[nacc * NSL + e] = (e > j && e < bsz) ? fe : 0.0;
+#pragma unroll
+                    for (int x = 0; x < NSL; ++x) {
+                        const double fx = col[x] * rinv;  // H[x][j] / sqrt(H[j][j])
+                        if (e > j && x > j) hc[x] = fma(-fx, fe, hc[x]);
+                    }
+                    if (lane == 0) {
+                        sA[nacc] = sj;
+                        jA[nacc] = j;
+                        rinvA[nacc] = rinv;
+                    }
+                    my_acc |= (lane == j);
+                    ++nacc;
+                }
+            }
+            // bookkeeping of the accepted pivots: Fx[aa][a2] = F[i+a2, s_aa], perm (slot -> acceptance
+            // index), the owner CTA's L rows L[i+x][0:i] = F[0:i, s_x] and S
+            __syncwarp();
+            for (int idx = lane; idx < NSL * NSL; idx += 32) {
+                const int aa = idx / NSL, a2 = idx % NSL;
+                Fx[idx] = (aa < nacc && a2 < aa) ? Fcand[a2 * NSL + jA[aa]] : 0.0;
+            }
+            if (lane < NSL) {
+                int pa = -1;
+                for (int x = 0; x < nacc; ++x) pa = (jA[x] == lane) ? x : pa;
+                perm[lane] = pa;
+            }
+            for (int x = 0; x < nacc; ++x) {
+                const int s = sA[x];
+                if (s >= lo && s < hi) {
+                    const int sl = jA[x];
+                    for (int q = lane; q < i; q += 32) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
+                    if (lane == 0) a.S[(int64_t)u * a.r + i + x] = s;
+                }
+            }
+            if (lane == 0) sh_na = nacc;
+            WC_BTRE(14);
+            i += nacc;
+            ++blk;
+            ce_sync();  // B: the compute warps read na, Fx, perm, sA, rinvA
         }
         return;
     }
@@ -350,19 +530,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             theta = 1000.0 * (double)a.r * 2.220446049250313e-16 * T0;
         }
         if (Ttot <= theta) break;  // exhausted (reading Z3), tested at block starts
-        if (tid == 0) sh_req = ((long long)(++nreq) << 32) | (long long)i;  // producer: F[0:i] of super-tile 0
+        if (tid == 0) flag_st64(&sh_req, ((long long)(++nreq) << 32) | (long long)i);  // producer: F[0:i] of super-tile 0
         WC_BTR(10);
 
-        // ---- 1b: candidates, warp w draws j = w, w + 8 by the Eq. 4 inverse CDF with strict '>',
-        // hierarchically: owning CTA (prefix of CTA sums) -> 32-key group (prefix of the group sums
-        // of that CTA's slice) -> key (warp scan of the group's 32 residuals).  Each level falls back
-        // to its last positive entry if rounding leaves no crossing (reading Z2).
-        {
-            // each half-warp draws one candidate (j = w and j = w + 8 at the same time): 16 lanes per
-            // level of the hierarchy, so a warp's two draws share one chain of L2 round trips
+        // ---- 1b: candidates: each half-warp draws one candidate per pass (warp w: j = w + 8 h + 16 pass)
+        // by the Eq. 4 inverse CDF with strict '>', hierarchically: owning CTA (prefix of CTA sums) ->
+        // 32-key group (prefix of the group sums of that CTA's slice) -> key (scan of the group's 32
+        // residuals).  Each level falls back to its last positive entry if rounding leaves no crossing
+        // (reading Z2).
+#pragma unroll 1
+        for (int pass = 0; pass < NSL / 16; ++pass) {
             const int h16 = lane >> 4, l16 = lane & 15;
             const unsigned hm = 0xFFFFu << (16 * h16);
-            const int j = w + kCW * h16;
+            const int j = w + kCW * (h16 + 2 * pass);
             const bool jok = j < bsz;
             const int per16 = (a.cpu + 15) / 16;
             const int b0 = l16 * per16, b1 = min(a.cpu, b0 + per16);
@@ -375,7 +555,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                 if (l16 >= o) incl += y;
             }
             const double Tw = __shfl_sync(0xffffffffu, incl, 15, 16);  // the total in this order
-            const double t = jok ? pivot_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u) * Tw : 0.0;
+            const double t = jok ? pivot_uniform(a.seed, cbase + (uint32_t)j, uid) * Tw : 0.0;
             // level 1: CTA
             const unsigned hit = (__ballot_sync(0xffffffffu, b1 > b0 && incl > t) & hm) >> (16 * h16);
             const unsigned pos = (__ballot_sync(0xffffffffu, b1 > b0 && v > 0.0) & hm) >> (16 * h16);
@@ -476,14 +656,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             s3 = __shfl_sync(0xffffffffu, s3, L3, 16);
             psv = __shfl_sync(0xffffffffu, psv, L3, 16);
             if (l16 == 0 && jok) {
-                const int s = (int)(gstar * 32 + 2 * L3 + s3);
-                cs[j] = s;
+                cs[j] = (int)(gstar * 32 + 2 * L3 + s3);
                 cp[j] = psv;
-                vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, (uint64_t)u);
-                const int64_t cc = s / chunk, off = s - cc * chunk;
-                const int kk = (int)(off / kBT);
-                cfo[j] = cc * chunk * a.r + (int64_t)kk * kBT * a.r + (off % kBT);
-                cwk[j] = (int)std::min<int64_t>(kBT, chunk - (int64_t)kk * kBT);
+                vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, uid);
             }
             if (blk == 0 && j == 0) WC_BTR(11);
         }
@@ -492,49 +667,53 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
 
         // ---- 2: candidate data: the columns F[0:i, s_j] arrive as one bulk copy each from the
         // key-major copy FT (written by the owner thread of each key in earlier blocks), overlapped
-        // with the centred candidate keys (fp64, MMA layout), their kernel dots on the tensor cores
-        // (warps 4-7) and c0; rows [i, i4) and unused slots of Fcol are zeroed.
+        // with the centred candidate keys (fp64, MMA layout) and the parts of c0[j] = <kbar, k_sj - kbar>
         const int i4 = (i + 3) & ~3;
-        if (tid == 0 && i > 0) {  // one bulk copy per candidate: its key-major F row FT[s_j][0:i4]
+        if (tid == 0 && i > 0) {
             const double *FTu = a.FT + (int64_t)u * n * ftl;
             mbar_arrive_expect_tx(colbar, (uint32_t)(bsz * i4 * sizeof(double)));
             for (int j = 0; j < bsz; ++j)
                 bulk_g2s(Fcol + (size_t)j * ldc, FTu + (int64_t)cs[j] * ftl, (uint32_t)(i4 * sizeof(double)), colbar);
         }
         {
-            // thread (e-part, j): j = tid & 15 is fixed per thread; also its part of c0[j] = <kbar, k_sj - kbar>
-            const int j = tid & 15;
+            const int j = tid % NSL;  // fixed per thread
             double s0 = 0.0;
-            for (int e = tid >> 4; e < D; e += kCT / 16) {
+            for (int e = tid / NSL; e < D; e += kCT / NSL) {
                 const double kc = j < bsz ? __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]) : 0.0;
-                kcB[kcb<D>(e, j)] = kc;
+                kcB[kcb<D, NSL>(e, j)] = kc;
                 s0 = fma(kb[e], kc, s0);
             }
-            Hp[tid] = s0;  // Hp is free until the H partials below
+            sm.c0p[tid] = s0;
         }
         cw_sync();
-        // H = h~(K_C, K_C) - F[0:i, C]^T F[0:i, C] on the fp64 tensor cores: warps 4-7 split the
-        // kernel-dot k-steps (now), warps 0-3 the F k-steps (once the gather has landed); the
-        // per-warp partials are summed in fixed warp order
-        if (tid < kBMax) {  // c0[j]: the 16 e-parts of slot j in fixed order
+        if (tid < NSL) {  // c0[j]: the e-parts of slot j in fixed order
             double s0 = 0.0;
 #pragma unroll
-            for (int q = 0; q < kCT / 16; ++q) s0 += Hp[q * 16 + tid];
+            for (int q = 0; q < kCT / NSL; ++q) s0 += sm.c0p[q * NSL + tid];
             c0r[tid] = s0;
         }
-        double Hc[2][2][2];
+        // ---- 3: H = h~(K_C, K_C) - F[0:i, C]^T F[0:i, C] on the fp64 tensor cores, one 8x8 tile
+        // (mt, nt) per warp and pass (all k-steps of the tile in one accumulator, fixed k order: the
+        // (x, e) and (e, x) tiles get the same bits, so H is bitwise symmetric).  Kernel-dot k-steps
+        // first (now), F k-steps once the gather has landed.
+        constexpr int NTILE = NT * NT, TPW = (NTILE + kCW - 1) / kCW;
+        double hk[TPW][2], hf[TPW][2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int q = 0; q < TPW; ++q) hk[q][0] = hk[q][1] = hf[q][0] = hf[q][1] = 0.0;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) Hc[mt][nt][0] = Hc[mt][nt][1] = 0.0;
-        if (w >= 4) {
-            for (int t = w - 4; t < DQ; t += 4) {
-                const double *base = kcB + (size_t)t * 64;
-                const double k0 = base[(0 * 8 + gid) * 4 + tq], k1 = base[(1 * 8 + gid) * 4 + tq];
-                dmma(Hc[0][0][0], Hc[0][0][1], k0, k0);
-                dmma(Hc[0][1][0], Hc[0][1][1], k0, k1);
-                dmma(Hc[1][0][0], Hc[1][0][1], k1, k0);
-                dmma(Hc[1][1][0], Hc[1][1][1], k1, k1);
+        for (int q = 0; q < TPW; ++q) {
+            const int tile = w + kCW * q;
+            if (tile < NTILE) {
+                const int mh = tile / NT, nh = tile % NT;
+                double h2[2] = {0.0, 0.0};  // odd k-steps: a second independent DMMA chain
+#pragma unroll 4
+                for (int t = 0; t < DQ; t += 2) {
+                    const double *b0 = kcB + (size_t)t * NSL * 4, *b1 = b0 + NSL * 4;
+                    dmma(hk[q][0], hk[q][1], b0[(mh * 8 + gid) * 4 + tq], b0[(nh * 8 + gid) * 4 + tq]);
+                    dmma(h2[0], h2[1], b1[(mh * 8 + gid) * 4 + tq], b1[(nh * 8 + gid) * 4 + tq]);
+                }
+                hk[q][0] += h2[0];
+                hk[q][1] += h2[1];
             }
         }
         if (i > 0) {
@@ -542,149 +721,57 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             ++ncol;
         }
         // rows [i, i4) of the copies are stale, slots >= bsz unused: zero them
-        for (int idx = tid; i4 > 0 && idx < kBMax * i4; idx += kCT) {
+        for (int idx = tid; i4 > 0 && idx < NSL * i4; idx += kCT) {
             const int j = idx / i4, q = idx - j * i4;
             if (j >= bsz || q >= i) Fcol[(size_t)j * ldc + q] = 0.0;
         }
         cw_sync();
         WC_BTR(2);
-        if (w < 4) {
-            for (int kq = w; kq < i4 / 4; kq += 4) {
-                const double f0 = Fcol[(size_t)gid * ldc + 4 * kq + tq];
-                const double f1 = Fcol[(size_t)(8 + gid) * ldc + 4 * kq + tq];
-                dmma(Hc[0][0][0], Hc[0][0][1], f0, f0);
-                dmma(Hc[0][1][0], Hc[0][1][1], f0, f1);
-                dmma(Hc[1][0][0], Hc[1][0][1], f1, f0);
-                dmma(Hc[1][1][0], Hc[1][1][1], f1, f1);
+#pragma unroll
+        for (int q = 0; q < TPW; ++q) {
+            const int tile = w + kCW * q;
+            if (tile < NTILE) {
+                const int mh = tile / NT, nh = tile % NT;
+                for (int kq = 0; kq < i4 / 4; ++kq) {
+                    const double f0 = Fcol[(size_t)(mh * 8 + gid) * ldc + 4 * kq + tq];
+                    const double f1 = Fcol[(size_t)(nh * 8 + gid) * ldc + 4 * kq + tq];
+                    dmma(hf[q][0], hf[q][1], f0, f1);
+                }
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int x = mh * 8 + gid, e = nh * 8 + 2 * tq + hh;
+                    H0[x * NSL + e] = (x == e) ? cp[x < bsz ? x : 0]
+                                               : exp(__dadd_rn(__dmul_rn(g, hk[q][hh]), -mstar)) - hf[q][hh];
+                }
             }
         }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) Hp[((w * 4 + mt * 2 + nt) * 32 + lane) * 2 + hh] = Hc[mt][nt][hh];
-        cw_sync();
-        {
-            const int x = tid >> 4, e = tid & 15;
-            const int mt = x >> 3, nt = e >> 3, ln = ((x & 7) << 2) | ((e & 7) >> 1), hh = e & 1;
-            const int off = ((mt * 2 + nt) * 32 + ln) * 2 + hh;
-            double fs = 0.0, ks = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < 4; ++ww) fs += Hp[ww * 256 + off];
-#pragma unroll
-            for (int ww = 4; ww < 8; ++ww) ks += Hp[ww * 256 + off];
-            H0[x * kBMax + e] = (x == e) ? cp[x < bsz ? x : 0] : exp(__dadd_rn(__dmul_rn(g, ks), -mstar)) - fs;
-        }
-        cw_sync();
+        if (tid == 0) sh_cmd = 1;
+        ce_sync();  // A: H0, c0r complete; the rejection warp starts
         WC_BTR(3);
 
-        // ---- 3: rejection in candidate order as a parallel symmetric elimination: thread (x, e)
-        // owns H[x][e]; accepting j subtracts F_x F_e with F_x = H[x][j] / sqrt(H[j][j]), which is
-        // also F[i+aa, s_x] for the later candidates x (the coefficients of the per-key triangle).
-        // (warp 0, lane e = column e of the symmetric H in registers; column j is fetched from lane j
-        // by shuffles -- H[x][j] is lane j's entry x).  Every thread learns na from shared memory.
-        // The elimination runs on the LAST compute warp while the others start the round-update
-        // GEMMs (kernel dots and F prefix over all candidate slots do not depend on acceptance); at
-        // the headline that warp owns no keys of the CTA's slice, so the elimination is hidden.
-        if (w == kElimW) {
-            const int e = lane;
-            double hc[kBMax];
-#pragma unroll
-            for (int x = 0; x < kBMax; ++x) hc[x] = (e < bsz && x < bsz) ? H0[x * kBMax + e] : 0.0;
-            const int my_cs = e < bsz ? cs[e] : -1;
-            const double my_vp = e < bsz ? __dmul_rn(vac[e], cp[e]) : 0.0;  // v_e p[s_e]
-            bool my_acc = false;
-            int nacc = 0;
-#pragma unroll 1
-            for (int j = 0; j < bsz && i + nacc < a.r; ++j) {
-                // lane j publishes its column H[:, j] through shared memory (double-buffered by step
-                // parity: the previous user of this buffer finished before the last __syncwarp);
-                // H stays bitwise symmetric (symmetric DMMA sums, commuted fma products), so
-                // H[j][e] = H[e][j] = col[e] and no register-indexed select chain is needed
-                double *col = rowj + (j & 1) * kBMax;
-                if (lane == j) {
-#pragma unroll
-                    for (int x = 0; x < kBMax; ++x) col[x] = hc[x];
-                }
-                __syncwarp();
-                const double hjj = col[j];
-                const double hej = e < kBMax ? col[e] : 0.0;  // H[j][e] (lanes >= kBMax own no column)
-                const int sj = __shfl_sync(0xffffffffu, my_cs, j);
-                const double vp = __shfl_sync(0xffffffffu, my_vp, j);
-                const bool dup = __any_sync(0xffffffffu, my_acc && my_cs == sj);
-                if (!dup && vp < hjj) {
-                    const double rinv = rsqrt_nr(hjj);
-                    const double fe = hej * rinv;  // F[i+nacc, s_e] = H[j][e] / sqrt(H[j][j])
-                    if (e < kBMax) Fcand[nacc * kBMax + e] = (e > j && e < bsz) ? fe : 0.0;
-#pragma unroll
-                    for (int x = 0; x < kBMax; ++x) {
-                        const double fx = col[x] * rinv;  // H[x][j] / sqrt(H[j][j])
-                        if (e > j && x > j) hc[x] = fma(-fx, fe, hc[x]);
-                    }
-                    if (lane == 0) {
-                        sA[nacc] = sj;
-                        jA[nacc] = j;
-                        rinvA[nacc] = rinv;
-                    }
-                    my_acc |= (lane == j);
-                    ++nacc;
-                }
-            }
-            // the bookkeeping of the accepted pivots, still on this warp while the others run GEMMs:
-            // Fx[aa][a2] = F[i+a2, s_aa], perm (slot -> acceptance index), the owners' L rows and S
-            __syncwarp();  // Fcand, sA, jA written by lane 0 / the column lanes
-            for (int idx = lane; idx < kBMax * kBMax; idx += 32) {
-                const int aa = idx >> 4, a2 = idx & 15;
-                Fx[aa * kBMax + a2] = (aa < nacc && a2 < aa) ? Fcand[a2 * kBMax + jA[aa]] : 0.0;
-            }
-            if (lane < kBMax) {
-                int pa = -1;
-                for (int x = 0; x < nacc; ++x) pa = (jA[x] == lane) ? x : pa;
-                perm[lane] = pa;
-            }
-            for (int x = 0; x < nacc; ++x) {  // owner CTA of each accepted pivot: S and L[i+x][0:i] = F[0:i, s_x]
-                const int s = sA[x];
-                if (s >= lo && s < hi) {
-                    const int sl = jA[x];
-                    for (int q = lane; q < i; q += 32) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
-                    if (lane == 0) a.S[(int64_t)u * a.r + i + x] = s;
-                }
-            }
-            if (lane == 0) sh_na = nacc;
-            WC_BTR(14);
-        }
-        // na, Fx, perm and the owners' L rows / S: after the first super-tile's GEMM phase (below),
-        // once the elimination warp has joined the compute-warp barrier
-        int na = 0;
-        auto finish_elim = [&]() {  // after a compute-warp barrier that follows the elimination
-            na = sh_na;
-            WC_BTR(4);
-            WC_BTR(5);
-        };
-
-        // ---- 4: na F-form rounds over this CTA's keys.  Per 512-key super-tile, warp w owns keys
-        // [64w, 64w+64) as 8 MMA row-tiles of 8; over the 16 candidate slots,
+        // ---- 4: na F-form rounds over this CTA's keys.  Per BT-key super-tile, warp w owns keys
+        // [KPW w, KPW w + KPW) as MT MMA row-tiles of 8; over the NSL candidate slots,
         //   G = h~(K_tile, K_C) - F[0:i, tile]^T F[0:i, C]
         // is accumulated on the fp64 tensor cores (kernel dot, exp in registers, then the F prefix
-        // with negated ring operands); the quad of lanes sharing a key then runs the triangle over
-        // the accepted slots in acceptance order, right-looking, with shuffles.
+        // with negated ring operands); each lane then runs the triangle of its key(s) over the
+        // accepted slots in acceptance order.
+        int na = 0;
         loc = 0.0;
         for (int k = 0; k < nst; ++k) {
-            const int64_t t0 = lo + (int64_t)k * kBT;
+            const int64_t t0 = lo + (int64_t)k * BT;
             const int wk = tile_w(k);
-            double *Fk = Fc + (int64_t)k * a.r * kBT;
-            const int kw = 64 * w;
+            double *Fk = Fc + (int64_t)k * a.r * BT;
+            const int kw = KPW * w;
             const bool wact = t0 + kw < hi;
-            double C[8][2][2];
+            double C[MT][NT][2];
 #pragma unroll
-            for (int mt = 0; mt < 8; ++mt)
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
+                for (int nt = 0; nt < NT; ++nt) C[mt][nt][0] = C[mt][nt][1] = 0.0;
             if (wact) {
-                KC kc[2][8];  // double-buffered K chunks: chunk c + 1 is in flight while c feeds the MMAs
+                KC kc[2][MT];  // double-buffered K chunks: chunk c + 1 is in flight while c feeds the MMAs
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt) {
+                for (int mt = 0; mt < MT; ++mt) {
                     const int64_t key = t0 + kw + 8 * mt + gid;
                     if (key < hi) kc[0][mt].load(Ku + key * D + tq * DQ);
                     else kc[0][mt].zero();
@@ -694,7 +781,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                     const int cb = (t0c / TC) & 1;
                     if (t0c + TC < DQ) {
 #pragma unroll
-                        for (int mt = 0; mt < 8; ++mt) {
+                        for (int mt = 0; mt < MT; ++mt) {
                             const int64_t key = t0 + kw + 8 * mt + gid;
                             if (key < hi) kc[cb ^ 1][mt].load(Ku + key * D + tq * DQ + t0c + TC);
                             else kc[cb ^ 1][mt].zero();
@@ -703,25 +790,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
 #pragma unroll
                     for (int tt = 0; tt < TC; ++tt) {
                         const int t = t0c + tt;
-                        const double bk0 = kcB[((t * 2 + 0) * 8 + gid) * 4 + tq];
-                        const double bk1 = kcB[((t * 2 + 1) * 8 + gid) * 4 + tq];
+                        double bk[NT];
 #pragma unroll
-                        for (int mt = 0; mt < 8; ++mt) {
+                        for (int nt = 0; nt < NT; ++nt) bk[nt] = kcB[((t * NT + nt) * 8 + gid) * 4 + tq];
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
                             const double av = kc[cb][mt].elem(tt);
-                            dmma(C[mt][0][0], C[mt][0][1], av, bk0);
-                            dmma(C[mt][1][0], C[mt][1][1], av, bk1);
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], av, bk[nt]);
                         }
                     }
                 }
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt)
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int sl = 8 * nt + 2 * tq + hh;
                         const double cz = c0r[sl];
                         if (sl < bsz) {  // every drawn candidate (acceptance is not known yet)
 #pragma unroll
-                            for (int mt = 0; mt < 8; ++mt)
+                            for (int mt = 0; mt < MT; ++mt)
                                 C[mt][nt][hh] = exp(__dadd_rn(__dmul_rn(g, C[mt][nt][hh] - cz), -mstar));
                         }
                     }
@@ -731,17 +819,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             for (int j0 = 0; j0 < i; j0 += kBR) {
                 mbar_wait(&full[rstage], rph);
                 if (wact) {
-                    const double *sb = ring + (size_t)rstage * kBR * kPitch;
+                    const double *sb = ring + (size_t)rstage * kBR * PITCH;
                     const bool rowok = j0 + tq < i;
-                    const double bf0 = Fcol[(size_t)gid * ldc + j0 + tq];
-                    const double bf1 = Fcol[(size_t)(8 + gid) * ldc + j0 + tq];
+                    double bf[NT];
 #pragma unroll
-                    for (int mt = 0; mt < 8; ++mt) {
-                        const double av = rowok ? -sb[tq * kPitch + kw + 8 * mt + gid] : 0.0;
-                        dmma(C[mt][0][0], C[mt][0][1], av, bf0);
-                        dmma(C[mt][1][0], C[mt][1][1], av, bf1);
+                    for (int nt = 0; nt < NT; ++nt) bf[nt] = Fcol[(size_t)(nt * 8 + gid) * ldc + j0 + tq];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const double av = rowok ? -sb[tq * PITCH + kw + 8 * mt + gid] : 0.0;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], av, bf[nt]);
                     }
                 }
+                fence_proxy_async_smem();  // this lane's reads of the stage precede the next bulk copy into it
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[rstage]);
                 if (++rstage == NS) {
@@ -751,26 +841,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
             }
             if (k == 0) WC_BTR(7);
             cw_sync();  // every warp is done with the ring before it is reused as staging
-            if (k == 0) finish_elim();  // (the elimination warp has arrived: its results are visible)
-            int pm[4];  // acceptance index of this lane's 4 C columns (slots 8 nt + 2 tq + hh), -1: rejected
+            if (k == 0) {
+                ce_sync();  // B: the rejection warp's na, Fx, perm, sA, rinvA are in shared memory
+                na = sh_na;
+                WC_BTR(4);
+                WC_BTR(5);
+            }
+            int pm[NT * 2];  // acceptance index of this lane's C columns (slots 8 nt + 2 tq + hh), -1: rejected
 #pragma unroll
-            for (int z = 0; z < 4; ++z) pm[z] = perm[8 * (z >> 1) + 2 * tq + (z & 1)];
-            // per-key triangle over the accepted pivots in acceptance order: G is transposed through
-            // the ring (idle until the next block's request) so that lane k owns key 32 h + k of its
-            // warp with all its G values in registers; left-looking:
+            for (int z = 0; z < NT * 2; ++z) pm[z] = perm[8 * (z >> 1) + 2 * tq + (z & 1)];
+            // per-key triangle over the accepted pivots in acceptance order: G is transposed through the
+            // ring (idle until the next request) so that lane k owns keys 32 h + k of its warp with all
+            // their G values at hand; left-looking:
             //   F[i+aa, l] = (G[l, aa] - sum_{a2<aa} F[i+a2, l] F[i+a2, s_aa]) / sqrt(p_{s_aa})
             // then the F row writes (coalesced), the downdate with the clamp (Z4), p_s <- 0, the L
             // entries of pivot keys, and the 32-key group sums.
             if (wact) {
-                double plh[2];  // the residuals of the lane's two keys, loaded before the staging
+                double plh[KPL];  // the residuals of the lane's keys, loaded before the staging
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < KPL; ++h) {
                     const int64_t key = t0 + kw + 32 * h + lane;
                     plh[h] = key < hi ? __ldcg(cur + key) : 0.0;
                 }
                 // per key (lane, half h) after its triangle: residual, key-major FT row, L rows of an
                 // accepted pivot, and the 32-key group sum
-                auto key_epilogue = [&](int h, const double (&f)[kBMax], double pl) {
+                auto key_epilogue = [&](int h, const double (&f)[NSL], double pl) {
                     const int64_t key = t0 + kw + 32 * h + lane;
                     if (key < hi) {
                         nxt[key] = pl;
@@ -778,25 +873,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                         if (i & 1) {  // 16-byte stores from the first even index (FT rows are 32-byte aligned)
                             if (na > 0) ftr[0] = f[0];
 #pragma unroll
-                            for (int aa = 1; aa < kBMax - 1; aa += 2) {
+                            for (int aa = 1; aa < NSL - 1; aa += 2) {
                                 if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
                                 else if (aa < na) ftr[aa] = f[aa];
                             }
-                            if (kBMax - 1 < na) ftr[kBMax - 1] = f[kBMax - 1];
+                            if (NSL - 1 < na) ftr[NSL - 1] = f[NSL - 1];
                         } else {
 #pragma unroll
-                            for (int aa = 0; aa < kBMax; aa += 2) {
+                            for (int aa = 0; aa < NSL; aa += 2) {
                                 if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
                                 else if (aa < na) ftr[aa] = f[aa];
                             }
                         }
                         int xm = -1;  // acceptance index if this key is an accepted pivot (branch-free search)
 #pragma unroll
-                        for (int x = 0; x < kBMax; ++x) xm = (x < na && sA[x] == key) ? x : xm;
+                        for (int x = 0; x < NSL; ++x) xm = (x < na && sA[x] == key) ? x : xm;
                         if (xm >= 0) {  // L[i+x][i..i+x] = F[i..i+x, s_x]
                             double *Lr = a.L + ((int64_t)u * a.r + i + xm) * a.r + i;
 #pragma unroll
-                            for (int a2 = 0; a2 < kBMax; ++a2)
+                            for (int a2 = 0; a2 < NSL; ++a2)
                                 if (a2 <= xm) Lr[a2] = f[a2];
                         }
                     }
@@ -806,105 +901,57 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
                         loc += gs;
                     }
                 };
-                if (two_keys) {
-                    // both of the lane's keys staged at once and their triangles interleaved (two
-                    // independent fp64 chains; per key the same operations in the same order)
-                    double *stg = ring + (size_t)w * 64 * 17;  // [64 keys][17] per warp
+                // stage G rows (keys 8 mt + gid of the warp) for row tiles [mt0, mt0 + 4 KSN) at stg
+                auto stage = [&](double *stg, int mt0, int nmt) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
+                    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                        for (int m4 = 0; m4 < 4; ++m4)
+                        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                                for (int hh = 0; hh < 2; ++hh) {
-                                    const int ai = pm[nt * 2 + hh];
-                                    if (ai >= 0) stg[(32 * h + 8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
-                                }
-                    __syncwarp();
-                    const int64_t key0 = t0 + kw + lane, key1 = key0 + 32;
-                    const double *g0 = stg + lane * 17, *g1 = g0 + 32 * 17;
-                    double *frow0 = Fk + (int64_t)i * wk + kw + lane, *frow1 = frow0 + 32;
-                    double f0[kBMax], f1[kBMax];
-                    double pl0 = plh[0], pl1 = plh[1];
-#pragma unroll
-                    for (int aa = 0; aa < kBMax; ++aa) {
-                        f0[aa] = 0.0;
-                        f1[aa] = 0.0;
-                        if (aa < na) {
-                            double c0v = g0[aa], c1v = g1[aa];
-                            const double *fx = Fx + aa * kBMax;
-#pragma unroll
-                            for (int a2 = 0; a2 < aa; ++a2) {
-                                const double x = fx[a2];
-                                c0v = fma(-f0[a2], x, c0v);
-                                c1v = fma(-f1[a2], x, c1v);
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const int ai = pm[nt * 2 + hh];
+                                if (ai >= 0 && mt >= mt0 && mt < mt0 + nmt)
+                                    stg[(8 * (mt - mt0) + gid) * SP + ai] = C[mt][nt][hh];
                             }
-                            const double ra = rinvA[aa];
-                            const double fv0 = c0v * ra, fv1 = c1v * ra;
-                            f0[aa] = fv0;
-                            f1[aa] = fv1;
-                            if (key0 < hi) frow0[(int64_t)aa * wk] = fv0;
-                            if (key1 < hi) frow1[(int64_t)aa * wk] = fv1;
-                            const int sa = sA[aa];
-                            const double q0 = __dadd_rn(pl0, -__dmul_rn(fv0, fv0));
-                            const double q1 = __dadd_rn(pl1, -__dmul_rn(fv1, fv1));
-                            pl0 = (q0 > 0.0 && key0 != sa) ? q0 : 0.0;
-                            pl1 = (q1 > 0.0 && key1 != sa) ? q1 : 0.0;
-                        }
-                    }
+                };
+                if (KPL == 2 && two_keys) {
+                    // both of the lane's keys staged at once, their triangles interleaved
+                    double *stg = ring + (size_t)w * 64 * SP;
+                    stage(stg, 0, MT);
                     __syncwarp();
-                    key_epilogue(0, f0, pl0);
-                    key_epilogue(1, f1, pl1);
+                    const int64_t keys[2] = {t0 + kw + lane, t0 + kw + 32 + lane};
+                    double *const frows[2] = {Fk + (int64_t)i * wk + kw + lane, Fk + (int64_t)i * wk + kw + 32 + lane};
+                    double f[2][NSL];
+                    double pl[2] = {plh[0], plh[KPL - 1]};
+                    key_triangle<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, f, pl);
+                    __syncwarp();
+                    key_epilogue(0, f[0], pl[0]);
+                    key_epilogue(1, f[1], pl[1]);
                 } else {
-                    double *stg = ring + (size_t)w * 32 * 17;  // [32 keys][17] per warp
+                    double *stg = ring + (size_t)w * 32 * SP;  // [32 keys][SP] per warp
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                        for (int m4 = 0; m4 < 4; ++m4)
-#pragma unroll
-                            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                                for (int hh = 0; hh < 2; ++hh) {
-                                    const int ai = pm[nt * 2 + hh];
-                                    if (ai >= 0) stg[(8 * m4 + gid) * 17 + ai] = C[4 * h + m4][nt][hh];
-                                }
+                    for (int h = 0; h < KPL; ++h) {  // 32 keys of the warp at a time (row tiles 4h .. 4h + 3)
+                        stage(stg, 4 * h, 4);
                         __syncwarp();
-                        const int64_t key = t0 + kw + 32 * h + lane;
-                        double gk[kBMax];
-#pragma unroll
-                        for (int aa = 0; aa < kBMax; ++aa) gk[aa] = aa < na ? stg[lane * 17 + aa] : 0.0;
-                        __syncwarp();
-                        double pl = plh[h];
-                        double *frow = Fk + (int64_t)i * wk + kw + 32 * h + lane;
-                        double f[kBMax];
-#pragma unroll
-                        for (int aa = 0; aa < kBMax; ++aa) {
-                            f[aa] = 0.0;
-                            if (aa < na) {
-                                double cv = gk[aa];
-                                const double *fx = Fx + aa * kBMax;
-#pragma unroll
-                                for (int a2 = 0; a2 < aa; ++a2) cv = fma(-f[a2], fx[a2], cv);
-                                const double fv = cv * rinvA[aa];
-                                f[aa] = fv;
-                                if (key < hi) frow[(int64_t)aa * wk] = fv;
-                                const double q = __dadd_rn(pl, -__dmul_rn(fv, fv));
-                                pl = (q > 0.0 && key != sA[aa]) ? q : 0.0;
-                            }
-                        }
-                        key_epilogue(h, f, pl);
+                        const int64_t keys[1] = {t0 + kw + 32 * h + lane};
+                        double *const frows[1] = {Fk + (int64_t)i * wk + kw + 32 * h + lane};
+                        double f[1][NSL];
+                        double pl[1] = {plh[h]};
+                        key_triangle<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, f, pl);
+                        __syncwarp();  // the staging of this half is consumed
+                        key_epilogue(h, f[0], pl[0]);
                     }
                 }
             }
+            fence_proxy_async_smem();  // the staging accesses to the ring precede the next bulk copies into it
             if (k + 1 < nst) {  // the ring (used as staging above) is free: stream the next super-tile
                 cw_sync();
-                if (tid == 0) sh_req = ((long long)(++nreq) << 32) | ((long long)(k + 1) << 16) | (long long)i;
+                if (tid == 0) flag_st64(&sh_req, ((long long)(++nreq) << 32) | ((long long)(k + 1) << 16) | (long long)i);
             }
         }
         if (nst == 0) {  // a CTA without keys still needs the accepted count
-            cw_sync();
-            finish_elim();
+            ce_sync();
+            na = sh_na;
         }
         WC_BTR(8);
         fence_proxy_async_global();  // this block's F rows are read by later TMA copies
@@ -919,7 +966,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_blocked_kernel(BlkA
         ++blk;
         cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_dummy, 0);
     }
-    if (tid == 0) sh_stop = 1;
+    if (tid == 0) {
+        flag_st(&sh_stop, 1);
+        sh_cmd = 0;
+    }
+    ce_sync();  // A with the stop command: the rejection warp leaves its loop
     if (c == 0 && tid == 0) {
         a.r_eff[u] = i;
         st[5] = T0;
@@ -960,38 +1011,48 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
     }
 }
 
-template <typename T, int D>
-int launch_blocked_td(const Dims &Dm, const void *K, double *stats, SelectBufs b, uint64_t seed, int block,
-                      int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
+// Shared-memory plan of the kernel: NS ring stages (0 if r does not fit the plan).
+template <int D, int NSL> int blocked_stages(int r, int cpu) {
+    using PL = BPlan<NSL>;
+    const int ldc = ((r + 15) & ~15) + 4;
+    const size_t stage_bytes = (size_t)kBR * PL::PITCH * sizeof(double);
+    const size_t fixed = BSmem<D, NSL>(nullptr, 0, ldc, cpu).bytes + 64;
+    // the per-key triangle stages G ([32 keys][NSL + 1] per compute warp) through the idle ring
+    const size_t stg = (size_t)kCW * 32 * PL::SPITCH * sizeof(double);
+    const int ns_min = (int)std::max<size_t>(3, (stg + stage_bytes - 1) / stage_bytes);
+    constexpr size_t kSmemMax = 227 * 1024 - 64;  // dynamic shared memory per CTA (sm_100), minus statics
+    if (fixed + (size_t)ns_min * (stage_bytes + 16) > kSmemMax) return 0;
+    return (int)std::min<size_t>(12, (kSmemMax - fixed) / (stage_bytes + 16));
+}
+
+template <typename T, int D, int NSL>
+int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
+                       int block, int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
+    using PL = BPlan<NSL>;
     BlkArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.gsum = b.gsum;
     a.FT = b.FT;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
-    a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.trace = nullptr;
+    a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
+    const int ldc = ((Dm.r + 15) & ~15) + 4;
+    const int NS = blocked_stages<D, NSL>(Dm.r, a.cpu);
+    if (NS == 0) return -2;  // r too large for this plan
+    (void)sizeof(PL);
+    const size_t smem = BSmem<D, NSL>(nullptr, NS, ldc, a.cpu).bytes + 64;
     static const bool tracing = std::getenv("WC_SELECT_TRACE") != nullptr;
     if (tracing && cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * Dm.r) == cudaSuccess)
         cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 16 * Dm.r, st);
-    const size_t ldc = (size_t)((Dm.r + 15) & ~15) + 4;
-    const size_t fixed = (ldc * kBMax + (size_t)D * kBMax + 3 * kBMax * kBMax + 7 * kBMax + D + 40 + kCW * 4 * 64 +
-                          a.cpu + 64) * sizeof(double) +
-                         kBMax * sizeof(long long) + 5 * kBMax * sizeof(int) + 64;
-    const size_t stage_bytes = (size_t)kBR * kPitch * sizeof(double);
-    // >= 3 stages: the triangle stages G (8 warps x 32 keys x 17 doubles) through the idle ring
-    if (fixed + 3 * (stage_bytes + 16) > 220 * 1024) return -2;  // r too large for the shared-memory plan
-    int NS = (int)std::min<size_t>(12, (220 * 1024 - fixed - 16) / (stage_bytes + 16));
-    const size_t smem = fixed + (size_t)NS * (stage_bytes + 16);
-    auto kt = rpc_select_blocked_kernel<T, D>;
+    auto kt = rpc_select_blocked_kernel<T, D, NSL>;
     cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
     if (cudaMemsetAsync(b.part, 0, sizeof(double) * 2 * kMaxCpu * a.units, st) != cudaSuccess) return -1;
     const dim3 grid(a.units * a.cpu);
     if (a.cpu > 1) {
-        void *args[] = {&a, (void *)&NS};
         // cooperative (co-resident CTAs for the grid barrier) + programmatic stream serialisation
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
-        cfg.blockDim = dim3(kTmaThreads);
+        cfg.blockDim = dim3(kBThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[2];
@@ -1002,22 +1063,30 @@ int launch_blocked_td(const Dims &Dm, const void *K, double *stats, SelectBufs b
         cfg.attrs = attr;
         cfg.numAttrs = 2;
         if (cudaLaunchKernelEx(&cfg, kt, a, NS) != cudaSuccess) return -1;
-        (void)args;
     } else {
-        launch_pdl(kt, grid, dim3(kTmaThreads), smem, st, a, NS);
+        launch_pdl(kt, grid, dim3(kBThreads), smem, st, a, NS);
     }
     if (a.trace) dump_block_trace(a.trace, Dm.r, st);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// b <= 16: 16 candidate slots (512-key super-tiles); 16 < b <= 32: 32 slots (256-key super-tiles),
+// whose candidate columns must fit shared memory next to the ring (r up to ~300).
+template <typename T, int D>
+int launch_blocked_td(const Dims &Dm, const void *K, double *stats, SelectBufs b, uint64_t seed, uint64_t unit0,
+                      int block, int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
+    if (block <= 16) return launch_blocked_tdn<T, D, 16>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+    return launch_blocked_tdn<T, D, 32>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+}
+
 template <typename T>
-int launch_blocked_t(const Dims &Dm, const void *K, double *stats, SelectBufs b, uint64_t seed, int block,
+int launch_blocked_t(const Dims &Dm, const void *K, double *stats, SelectBufs b, uint64_t seed, uint64_t unit0, int block,
                      int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     switch (Dm.d) {
-        case 16: return launch_blocked_td<T, 16>(Dm, K, stats, b, seed, block, S, r_eff, L, st);
-        case 32: return launch_blocked_td<T, 32>(Dm, K, stats, b, seed, block, S, r_eff, L, st);
-        case 64: return launch_blocked_td<T, 64>(Dm, K, stats, b, seed, block, S, r_eff, L, st);
-        case 128: return launch_blocked_td<T, 128>(Dm, K, stats, b, seed, block, S, r_eff, L, st);
+        case 16: return launch_blocked_td<T, 16>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+        case 32: return launch_blocked_td<T, 32>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+        case 64: return launch_blocked_td<T, 64>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+        case 128: return launch_blocked_td<T, 128>(Dm, K, stats, b, seed, unit0, block, S, r_eff, L, st);
     }
     return -1;
 }
@@ -1026,11 +1095,24 @@ int launch_blocked_t(const Dims &Dm, const void *K, double *stats, SelectBufs b,
 
 int select_blocked_max_block() { return kBMax; }
 
-int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBufs b, uint64_t seed, int block,
+bool select_blocked_plan_ok(const Dims &D, int block) {
+    if (block < 2 || block > kBMax) return false;
+    const int cpu = select_ctas_per_unit(D);
+    const bool s16 = block <= 16;
+    switch (D.d) {
+        case 16: return (s16 ? blocked_stages<16, 16>(D.r, cpu) : blocked_stages<16, 32>(D.r, cpu)) > 0;
+        case 32: return (s16 ? blocked_stages<32, 16>(D.r, cpu) : blocked_stages<32, 32>(D.r, cpu)) > 0;
+        case 64: return (s16 ? blocked_stages<64, 16>(D.r, cpu) : blocked_stages<64, 32>(D.r, cpu)) > 0;
+        case 128: return (s16 ? blocked_stages<128, 16>(D.r, cpu) : blocked_stages<128, 32>(D.r, cpu)) > 0;
+    }
+    return false;
+}
+
+int launch_select_blocked(const Dims &D, const void *K, double *stats, SelectBufs b, uint64_t seed, uint64_t unit0, int block,
                           int32_t *S, int32_t *r_eff, double *L, cudaStream_t st) {
     if (block < 2 || block > kBMax) return -1;
-    if (D.dtype == 0) return launch_blocked_t<float>(D, K, stats, b, seed, block, S, r_eff, L, st);
-    return launch_blocked_t<__nv_bfloat16>(D, K, stats, b, seed, block, S, r_eff, L, st);
+    if (D.dtype == 0) return launch_blocked_t<float>(D, K, stats, b, seed, unit0, block, S, r_eff, L, st);
+    return launch_blocked_t<__nv_bfloat16>(D, K, stats, b, seed, unit0, block, S, r_eff, L, st);
 }
 
 }  // namespace wc

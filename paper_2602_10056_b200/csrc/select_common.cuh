@@ -68,7 +68,7 @@ __device__ __forceinline__ void cw_group_barrier(unsigned *ctr, unsigned count, 
         } else {
             __threadfence();
         }
-        *rounds_done = rounds;
+        flag_st(rounds_done, rounds);
     }
     cw_sync();
 }

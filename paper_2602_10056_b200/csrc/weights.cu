@@ -586,7 +586,9 @@ __global__ void __launch_bounds__(kWTc, 1)
         umma::fence_after_sync();
         if (tid == 0) {
             umma::gemm_128xNxK(tO, smem_u32(sP), smem_u32(sm + L::kOffV + buf * L::kV), D, 128, s > 0);
-            umma::commit(bar2);
+            // GEMM2(s) of the earlier slices is retired by the next bar1 commit; only the last one is
+            // waited on through bar2 (one phase: no mbarrier phase completes without a waiter)
+            if (s + 1 == nsl) umma::commit(bar2);
         }
         if (s + 1 < nsl) {
             stage(buf ^ 1);  // B/V buffers of slice s-1: retired by the bar1 wait above
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(kWTc, 1)
         }
     }
     if (nsl > 0) {
-        mbar_wait(bar2, (uint32_t)((nsl - 1) & 1));
+        mbar_wait(bar2, 0u);
         umma::fence_after_sync();
     }
     xch[half * 128 + row] = rowsum;

@@ -128,10 +128,10 @@ def test_product_package_has_no_oracle_dependency():
 def test_block_option_validation(L):
     from paper_2602_10056_b200 import _binding as B
 
-    assert ctypes.sizeof(B.wc_opts) == 32
+    assert ctypes.sizeof(B.wc_opts) == 40
     d = ctypes.c_void_p(0x1000)
     s = _shape()
-    o = B.make_opts(block=17)  # > WC_MAX_BLOCK
+    o = B.make_opts(block=33)  # > WC_MAX_BLOCK
     assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -1
     assert L.wc_version() >= 101
 
@@ -174,3 +174,34 @@ def test_binding_refuses_cpu_tensors():
         B._need(object(), "X", torch.float32, 1)
     with pytest.raises(B.WildcatError, match="required"):
         B._need(None, "X", torch.float32, 1)
+
+
+def test_unknown_flag_and_version(L):
+    from paper_2602_10056_b200 import _binding as B
+
+    s = _shape()
+    o = B.make_opts()
+    o.flags = 1 << 7  # not a WC_* flag
+    d = ctypes.c_void_p(0x1000)
+    need = L.wc_workspace_bytes(ctypes.byref(s), 3)
+    assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, need, None) == -1
+    assert L.wc_version() == 200
+    assert ctypes.sizeof(B.wc_opts) == 40  # beta, rq, seed, flags, block, unit_offset
+    assert L.wc_strerror(-8).decode().startswith("non-finite")
+
+
+def test_block32_plan_limit(L):
+    """16 < b <= 32 runs the 32-slot plan, whose candidate columns must fit shared memory: r = 1024
+    is refused before any launch (WC_EUNSUPPORTED), r = 256 accepted by validation."""
+    from paper_2602_10056_b200 import _binding as B
+
+    d = ctypes.c_void_p(0x1000)
+    big = _shape(n=5000, r=1024, d=128)
+    o = B.make_opts(block=32)
+    assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o), d, d, d, d, None, None, d, 1 << 40, None) == -7
+    o16 = B.make_opts(block=16)
+    small = _shape(n=5000, r=256, d=128)
+    need = L.wc_workspace_bytes(ctypes.byref(small), 3)
+    # r = 256 passes every check; with a too-small workspace the call stops at the workspace check
+    assert L.wildcat_forward(ctypes.byref(small), ctypes.byref(o), d, d, d, d, None, None, d, need - 1, None) == -4
+    assert L.wildcat_forward(ctypes.byref(big), ctypes.byref(o16), d, d, d, d, None, None, d, 1 << 10, None) == -4
