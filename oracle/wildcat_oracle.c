@@ -669,23 +669,23 @@ int wco_forward(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, in
  * Readings (Z12, Z13, Z23):
  *   - kbar is the row mean over ALL n keys of the unit and the recentring is global;
  *     R_Q and the value range are over the unit's full query group / full V;
- *   - bins are contiguous: bin b = rows [b nb, (b+1) nb), nb = n / B; this build requires
- *     B | n (the paper's "evenly divide (or reshape)");
- *   - per bin: R_K^b = max ||k_l - kbar|| over the bin, tau_b = Eq. 7 with n_b = nb
- *     (Z12), RPNys on the bin's centred keys at rank rb = min(ceil(r/B), nb) (Z13), with the
+ *   - bins are contiguous: bin b = rows [b nb, (b+1) nb) with nb = floor(n / B), and the last bin
+ *     also takes the n - B nb remainder rows (the paper's "evenly divide (or reshape)"; Z13);
+ *   - per bin: R_K^b = max ||k_l - kbar|| over the bin, tau_b = Eq. 7 with n_b the bin's
+ *     size (Z12), RPNys on the bin's centred keys at rank rb = min(ceil(r/B), nb) (Z13), with the
  *     Philox stream of unit id u*B + b (Z23), sequential or blocked (block > 1);
  *   - the bin coresets are concatenated in bin order with their valid rows only, so
  *     the unit's coreset is r_eff = sum_b r_eff_b rows; V_S, w from each bin's own Nystrom
  *     weights over its own keys (W block diagonal); then Alg 3 over the whole coreset.
  * Outputs (may be NULL): S [units][B*rb] unit-level key indices, -1 past r_eff;
  * r_eff [units]; binstats [units][B][5] = tau_b, g_b, mstar_b, R_K^b, R_Q;
- * X [units][B*rb][d+1] (rows past r_eff zero).  Returns -2 if B does not divide n.   */
+ * X [units][B*rb][d+1] (rows past r_eff zero).  Returns -2 unless 1 <= B <= min(r, n).   */
 /* ------------------------------------------------------------------------ */
 /* CompressKV (Alg 2) of ONE unit with B >= 1 contiguous bins: the per-unit body of
  * wco_forward_binned, shared with wco_compress_kv.  Ku, Vu [n][d]; Qg [mq][d] the unit's query rows
  * (for R_Q; unused when rq >= 0).  Outputs: S [B*rb] unit-level key indices (-1 past tot),
  * KS [B*rb][d], X [B*rb][d+1] (rows past tot zero), *tot = r_eff, binstats [B][5] (may be NULL).
- * Requires B | n (checked by the callers).                                                      */
+ * Requires 1 <= B <= n (checked by the callers).                                                */
 static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t block, double beta,
                          double rq, uint64_t seed, uint64_t u, const double *Ku, const double *Vu,
                          int64_t mq, const double *Qg, int32_t *S, double *KS, double *X,
@@ -713,8 +713,9 @@ static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t 
     for (int32_t b = 0; b < bins && status == 0; ++b) {
         const double *Kb = Ku + (size_t)b * nb * d;
         const double *Vb = Vu + (size_t)b * nb * d;
+        const int64_t nbb = (b == bins - 1) ? n - (int64_t)(bins - 1) * nb : nb;  /* last bin: + remainder (Z13) */
         double rk2 = 0.0;  /* R_K^b over the bin's centred keys */
-        for (int64_t l = 0; l < nb; ++l) {
+        for (int64_t l = 0; l < nbb; ++l) {
             double s2 = 0.0;
             for (int j = 0; j < d; ++j) {
                 double c = Kb[l * d + j] - kbar[j];
@@ -723,17 +724,17 @@ static int compress_unit(int64_t n, int32_t d, int32_t r, int32_t bins, int32_t 
             if (s2 > rk2) rk2 = s2;
         }
         const double rk = sqrt(rk2);
-        const double tau = (flags & WCO_TAU_ONE) ? 1.0 : wco_temperature(beta, rqu, rk, nb);  /* Z12: n_b */
+        const double tau = (flags & WCO_TAU_ONE) ? 1.0 : wco_temperature(beta, rqu, rk, nbb);  /* Z12: n_b */
         const double g = beta / (tau * tau), mstar = g * rk * rk;
         int32_t re = 0;
         const uint64_t ub = u * (uint64_t)bins + (uint64_t)b;  /* Z23 */
         if (block > 1)
-            status = wco_select_blocked(nb, d, rb, block, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL,
+            status = wco_select_blocked(nbb, d, rb, block, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL,
                                         NULL, NULL, NULL);
         else
-            status = wco_select(nb, d, rb, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL, NULL, NULL);
+            status = wco_select(nbb, d, rb, Kb, kbar, g, mstar, seed, ub, Sb, &re, NULL, NULL, NULL, NULL);
         if (status) break;
-        status = wco_weights(nb, d, rb, Kb, Vb, Sb, re, kbar, g, mstar, Xb);
+        status = wco_weights(nbb, d, rb, Kb, Vb, Sb, re, kbar, g, mstar, Xb);
         if (status) break;
         for (int a = 0; a < re; ++a) {  /* concatenate the bin's valid rows */
             S[tot + a] = (int32_t)(b * nb + Sb[a]);
@@ -772,7 +773,7 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
                        int32_t *S_out, int32_t *reff_out, double *binstats_out, double *X_out,
                        uint64_t unit0, int32_t flags)
 {
-    if (bins < 1 || n % bins != 0 || bins > r) return -2;
+    if (bins < 1 || bins > n || bins > r) return -2;
     const int64_t nb = n / bins;
     int32_t rb = (r + bins - 1) / bins;
     if (rb > nb) rb = (int32_t)nb;
@@ -814,7 +815,7 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
  *   - the first keep_first and the last keep_last tokens are retained exactly ("retain the first
  *     and last 32 context tokens and compress the remaining tokens");
  *   - the middle n_mid = n - keep_first - keep_last tokens are compressed by CompressKV (Alg 2,
- *     P:297-313) with rank r and B bins (B | n_mid), exactly as wco_forward_binned does for a
+ *     P:297-313) with rank r and B <= n_mid bins, exactly as wco_forward_binned does for a
  *     unit whose keys are the middle slice (its own kbar and R_K; R_Q from the unit's query rows
  *     Q [m per q-head] of the prompt, or rq >= 0; Philox unit id u, sub-unit u*B + b);
  *   - reading Z24: the cache is the union of exact and compressed entries, each entry a key row
@@ -828,8 +829,7 @@ int wco_forward_binned(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_
  * coreset rows in the order of Alg 2], zero rows after; c_eff = keep_first + keep_last + r_eff.
  * Outputs: KC [units][C][d], XC [units][C][d+1], c_eff [units], vmin/vmax [units][d],
  * S [units][R] (global token indices of the coreset, -1 past r_eff; may be NULL).
- * Returns -2 on an invalid split (keep_* < 0, n_mid < 0, n_mid > 0 with B not dividing n_mid
- * or B > r).                                                                */
+ * Returns -2 on an invalid split (keep_* < 0, n_mid < 0, n_mid > 0 with B > n_mid or B > r).   */
 /* ------------------------------------------------------------------------ */
 int wco_compress_kv(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n, int32_t d, int32_t r,
                     int32_t bins, int32_t block, int32_t keep_first, int32_t keep_last, double beta, double rq,
@@ -839,7 +839,7 @@ int wco_compress_kv(int32_t batch, int32_t hq, int32_t hkv, int64_t m, int64_t n
 {
     const int64_t nmid = n - keep_first - keep_last;
     if (keep_first < 0 || keep_last < 0 || nmid < 0) return -2;
-    if (nmid > 0 && (bins < 1 || nmid % bins != 0 || bins > r || r < 1)) return -2;
+    if (nmid > 0 && (bins < 1 || bins > nmid || bins > r || r < 1)) return -2;
     int32_t R = 0;
     if (nmid > 0) {
         int32_t rb = (r + bins - 1) / bins;

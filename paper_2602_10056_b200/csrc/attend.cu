@@ -6,6 +6,9 @@
 // online max rescaling across coreset tiles (exact: the shift cancels in num/den).
 #include <algorithm>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -527,32 +530,40 @@ template <int D> struct TcLong {
     static constexpr int kOffTb = kOffBar + 3 * 8, kTotal = kOffTb + 8;
 };
 
+// Per (unit, chunk, part): blockIdx.z = part of kPrepParts splits the chunk's K rows and X columns, so
+// a one-unit call still spreads the image build over many SMs.
+constexpr int kPrepParts = 16;
 template <int D>
 __global__ void __launch_bounds__(256)
     attend_long_prep_kernel(const __nv_bfloat16 *__restrict__ KS, const float *__restrict__ X,
                             const int32_t *__restrict__ r_eff, int r, int nch, unsigned char *__restrict__ img) {
+    pdl_wait();
     using L = TcLong<D>;
     constexpr int RC = L::RC, DC = D + 1, CPR = D / 8;
-    const int ch = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+    const int ch = blockIdx.x, u = blockIdx.y, part = blockIdx.z, tid = threadIdx.x;
     const int re = r_eff[u], s0 = ch * RC;
     unsigned char *dst = img + ((int64_t)u * nch + ch) * L::kImg;
-    for (int e = tid; e < RC * CPR; e += blockDim.x) {
-        const int row = e / CPR, cc = e % CPR;
+    constexpr int KR = RC / kPrepParts;  // K rows of this part
+    for (int e = tid; e < KR * CPR; e += blockDim.x) {
+        const int row = part * KR + e / CPR, cc = e % CPR;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (s0 + row < re) v = __ldg(reinterpret_cast<const uint4 *>(KS + ((int64_t)u * r + s0 + row) * D) + cc);
         *reinterpret_cast<uint4 *>(dst + L::kImgK + umma::sw128_offset(row, cc * 8, RC)) = v;
     }
-    for (int e = tid; e < D * RC; e += blockDim.x) {
-        const int c = e / RC, sl = e % RC;
-        const float x = (s0 + sl < re) ? X[((int64_t)u * r + s0 + sl) * DC + c] : 0.f;
+    // X rows of this part read row-major (coalesced over the d + 1 columns), written transposed
+    for (int e = tid; e < KR * DC; e += blockDim.x) {
+        const int sl = part * KR + e / DC, c = e % DC;
+        const float x = (s0 + sl < re) ? __ldg(X + ((int64_t)u * r + s0 + sl) * DC + c) : 0.f;
+        if (c == D) {
+            reinterpret_cast<float *>(dst + L::kImgW)[sl] = x;
+            continue;
+        }
         const __nv_bfloat16 xh = __float2bfloat16_rn(x);
         *reinterpret_cast<__nv_bfloat16 *>(dst + L::kImgXh + umma::sw128_offset(c, sl, D)) = xh;
         if (L::kSplitX)
             *reinterpret_cast<__nv_bfloat16 *>(dst + L::kImgXl + umma::sw128_offset(c, sl, D)) =
                 __float2bfloat16_rn(x - __bfloat162float(xh));
     }
-    float *wd = reinterpret_cast<float *>(dst + L::kImgW);
-    for (int sl = tid; sl < RC; sl += blockDim.x) wd[sl] = (s0 + sl < re) ? X[((int64_t)u * r + s0 + sl) * DC + D] : 0.f;
 }
 
 template <int D>
@@ -771,8 +782,8 @@ int launch_attend_tc_long(const Dims &Dm, const void *Q, const void *KS, const f
     if (!ws) return -1;
     const int nch = (int)ceil_div(Dm.r, L::RC);
     unsigned char *img = static_cast<unsigned char *>(ws);
-    attend_long_prep_kernel<D><<<dim3(nch, (unsigned)Dm.units()), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, nch, img);
+    launch_pdl(attend_long_prep_kernel<D>, dim3(nch, (unsigned)Dm.units(), kPrepParts), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, nch, img);
     auto kern = attend_tc_long_kernel<D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     const int64_t tph = ceil_div(Dm.m, 128);
@@ -785,6 +796,379 @@ int launch_attend_tc_long(const Dims &Dm, const void *Q, const void *KS, const f
                                               static_cast<const __nv_bfloat16 *>(vmin),
                                               static_cast<const __nv_bfloat16 *>(vmax), Dm.m, nch, Dm.group(), Dm.hq,
                                               Dm.hkv, (float)beta, clip, static_cast<__nv_bfloat16 *>(O), tph, total);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+}
+
+// =====================================================================================
+// Warp-specialised tcgen05 attend (bf16, d in {64, 128}, any r): A5 / Alg 3 with two
+// 128-query tiles in flight per CTA (a "pair" of tiles of one unit), the coreset streamed in chunks of
+// RC = 128 rows (the TcLong images above: [K_S chunk | X_hi^T (| X_lo^T) | w]).
+//   warp 0        producer: Q tiles by TMA tensor copies (128-byte swizzle, the UMMA K-major layout),
+//                 coreset chunk images by 1-D bulk copies into a 2-buffer ring;
+//   warp 1        MMA issuer (one thread): per chunk c, for each tile t of the pair
+//                   GEMM2(t, c-1): O_t += P_t X_{c-1}  (A = P from tensor memory)
+//                   GEMM1(t, c):   S_t  = Q_t K_c^T
+//                 (in-order tensor-core execution makes GEMM1(t, c) overwrite S_t / P_t only after
+//                 GEMM2(t, c-1) has read them);
+//   warps 4-7     softmax / epilogue of tile slot 0, warps 8-11 of slot 1 (thread = query row = TMEM
+//                 lane): row max of the chunk, lazy running max (moves only by > 2^8, then O_t and den
+//                 are rescaled in place), P = exp2(beta log2e s - M) -> bf16 packed into S_t's own
+//                 columns (tcgen05.st), den += P w; after the last chunk O / den, clip (Z14, Z15),
+//                 bf16 rows staged in the slot's Q buffer and written by one bulk copy per tile.
+// TMEM: slot t uses columns [256 t, 256 t + 128) for S_t / P_t and [256 t + 128, 256 t + 128 + d) for O_t.
+// =====================================================================================
+constexpr int kWsThreads = 384;
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(x),
+                 "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// mbarrier wait that traps after ~4 s instead of hanging the GPU (a protocol error then fails the call)
+__device__ __forceinline__ void mbar_wait_ws(uint64_t *bar, uint32_t parity, int tag) {
+    if (mbar_try_wait(bar, parity)) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    while (!mbar_try_wait(bar, parity)) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 4000000000ull) {
+            printf("[attend_ws] block %d thread %d: barrier wait %d timed out\n", blockIdx.x, threadIdx.x, tag);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void wg_sync(int id) {  // named barrier of one 128-thread warpgroup
+    asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+template <int D> struct WsSmem {
+    using L = TcLong<D>;
+    static constexpr int RC = L::RC;
+    static constexpr int kQ = 128 * D * 2;
+    static constexpr int kOffQ = 0;                    // [2][kQ]: Q tiles (then the output staging)
+    static constexpr int kOffRing = 2 * kQ;            // [2][L::kBuf] chunk images
+    static constexpr int kOffBar = kOffRing + 2 * L::kBuf;
+    // barriers: qfull[2], qempty[2], cfull[2], cempty[2], sfull[2], pfull[2], ofull[2]
+    static constexpr int kOffTb = kOffBar + 14 * 8;
+    static constexpr int kTotal = kOffTb + 16;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    attend_ws_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap omap,
+                     const unsigned char *__restrict__ img,
+                     const int32_t *__restrict__ r_eff, const __nv_bfloat16 *__restrict__ vmin,
+                     const __nv_bfloat16 *__restrict__ vmax, int64_t m, int nch_max, int group, int hq, int hkv,
+                     float beta, int clip, int64_t tiles_per_head, int64_t total_tiles) {
+    pdl_wait();
+    using L = TcLong<D>;
+    using W = WsSmem<D>;
+    constexpr int RC = W::RC;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw;
+    if (smem_u32(sm) & 1023u) __trap();
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + W::kOffBar);
+    uint64_t *qfull = bars, *qempty = bars + 2, *cfull = bars + 4, *cempty = bars + 6, *sfull = bars + 8;
+    uint64_t *pfull = bars + 10, *ofull = bars + 12;
+    uint32_t &tbase = *reinterpret_cast<uint32_t *>(sm + W::kOffTb);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+
+    if (w == 0) umma::tmem_alloc(&tbase, 512);
+    if (tid == 0) {
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&qfull[t], 1);
+            mbar_init(&qempty[t], 1);
+            mbar_init(&cfull[t], 1);
+            mbar_init(&cempty[t], 1);
+            mbar_init(&sfull[t], 1);
+            mbar_init(&pfull[t], 128);
+            mbar_init(&ofull[t], 1);
+        }
+        fence_mbar_init();
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tb = tbase;
+
+    const int64_t tpc = ceil_div(total_tiles, (int64_t)gridDim.x);
+    const int64_t t_begin = (int64_t)blockIdx.x * tpc, t_end = std::min<int64_t>(total_tiles, t_begin + tpc);
+    auto unit_of = [&](int64_t tile) {
+        const int64_t head = tile / tiles_per_head;
+        return (int)(head / hq) * hkv + (int)(head % hq) / group;
+    };
+    // the pair sequence: tile A = t, tile B = t + 1 when it exists and shares A's unit (and its chunks)
+    auto pair_b = [&](int64_t t) { return (t + 1 < t_end && unit_of(t + 1) == unit_of(t)) ? t + 1 : (int64_t)-1; };
+    auto nchunks = [&](int u) { return (int)std::max<int64_t>(1, ceil_div(r_eff[u], RC)); };
+
+    if (w == 0) {
+        // ================= producer =================
+        if (lane == 0) {
+            uint32_t nq[2] = {0, 0}, cseq = 0;
+            for (int64_t t = t_begin; t < t_end;) {
+                const int64_t tB = pair_b(t);
+                const int u = unit_of(t);
+                for (int s = 0; s < 2; ++s) {
+                    const int64_t tt = s == 0 ? t : tB;
+                    if (tt < 0) continue;
+                    mbar_wait_ws(&qempty[s], (nq[s] & 1u) ^ 1u, 1);
+                    ++nq[s];
+                    const int64_t head = tt / tiles_per_head, q0 = (tt % tiles_per_head) * 128;
+                    mbar_arrive_expect_tx(&qfull[s], (uint32_t)W::kQ);
+                    unsigned char *dq = sm + W::kOffQ + s * W::kQ;
+#pragma unroll
+                    for (int kb = 0; kb < D / 64; ++kb)  // rows >= m: zero-filled out-of-bounds box rows
+                        tma_load_3d(dq + kb * 128 * 128, &qmap, kb * 64, (int)q0, (int)head, &qfull[s]);
+                }
+                const int C = nchunks(u);
+                for (int c = 0; c < C; ++c, ++cseq) {
+                    const int b = cseq & 1;
+                    mbar_wait_ws(&cempty[b], ((cseq >> 1) & 1u) ^ 1u, 2);
+                    mbar_arrive_expect_tx(&cfull[b], (uint32_t)L::kImg);
+                    bulk_g2s(sm + W::kOffRing + b * L::kBuf, img + ((int64_t)u * nch_max + c) * L::kImg, (uint32_t)L::kImg,
+                             &cfull[b]);
+                }
+                t = tB >= 0 ? tB + 1 : t + 1;
+            }
+        }
+    } else if (w == 1) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            uint32_t nq[2] = {0, 0}, np[2] = {0, 0}, cseq = 0;
+            const uint32_t tS[2] = {tb, tb + 256}, tO[2] = {tb + 128, tb + 384};
+            auto gemm1 = [&](int s, const unsigned char *chunk) {
+                umma::gemm_128xNxK(tS[s], smem_u32(sm + W::kOffQ + s * W::kQ), smem_u32(chunk + L::kImgK), RC, D, false);
+                umma::commit(&sfull[s]);
+            };
+            auto gemm2 = [&](int s, const unsigned char *chunk, bool acc) {
+                mbar_wait_ws(&pfull[s], np[s] & 1u, 3);
+                ++np[s];
+                umma::fence_after_sync();
+                umma::gemm_128xNxK_tmem_a(tO[s], tS[s], smem_u32(chunk + L::kImgXh), D, RC, acc);
+                if (L::kSplitX) umma::gemm_128xNxK_tmem_a(tO[s], tS[s], smem_u32(chunk + L::kImgXl), D, RC, true);
+            };
+            for (int64_t t = t_begin; t < t_end;) {
+                const int64_t tB = pair_b(t);
+                const int ns = tB >= 0 ? 2 : 1;
+                const int C = nchunks(unit_of(t));
+                for (int s = 0; s < ns; ++s) {
+                    mbar_wait_ws(&qfull[s], nq[s] & 1u, 4);
+                    ++nq[s];
+                }
+                const unsigned char *prev = nullptr;
+                for (int c = 0; c < C; ++c, ++cseq) {
+                    const int b = cseq & 1;
+                    const unsigned char *chunk = sm + W::kOffRing + b * L::kBuf;
+                    mbar_wait_ws(&cfull[b], (cseq >> 1) & 1u, 5);
+                    umma::fence_after_sync();
+                    for (int s = 0; s < ns; ++s) {
+                        if (c > 0) gemm2(s, prev, c > 1);
+                        gemm1(s, chunk);
+                    }
+                    if (c > 0) umma::commit(&cempty[(cseq - 1) & 1]);  // chunk c-1: both GEMM2 issued
+                    prev = chunk;
+                }
+                for (int s = 0; s < ns; ++s) {
+                    gemm2(s, prev, C > 1);
+                    umma::commit(&ofull[s]);
+                }
+                umma::commit(&cempty[(cseq - 1) & 1]);
+                t = tB >= 0 ? tB + 1 : t + 1;
+            }
+        }
+    } else if (w >= 4) {
+        // ================= softmax / epilogue warpgroups =================
+        const int s = (w - 4) >> 2;             // tile slot
+        const int row = tid & 127;              // query row of the tile = TMEM lane
+        const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+        const uint32_t tS = tb + 256 * s + lane_off, tO = tb + 256 * s + 128 + lane_off;
+        const float bl2 = beta * 1.4426950408889634f;
+        uint32_t ns_ph = 0, no_ph = 0, cseq = 0;
+        unsigned char *stage = sm + W::kOffQ + s * W::kQ;
+        for (int64_t t = t_begin; t < t_end;) {
+            const int64_t tB = pair_b(t);
+            const int u = unit_of(t);
+            const int re = r_eff[u];
+            const int C = nchunks(u);
+            const int64_t tt = s == 0 ? t : tB;
+            if (tt < 0) {  // slot 1 idle for this pair: follow the chunk sequence only
+                cseq += C;
+                t = t + 1;
+                continue;
+            }
+            float M = -INFINITY, den = 0.f;
+            for (int c = 0; c < C; ++c, ++cseq) {
+                const unsigned char *chunk = sm + W::kOffRing + (cseq & 1) * L::kBuf;
+                const float *sW = reinterpret_cast<const float *>(chunk + L::kImgW);
+                mbar_wait_ws(&sfull[s], ns_ph, 6);
+                ns_ph ^= 1u;
+                umma::fence_after_sync();
+                const int lim = re - c * RC;  // valid columns of this chunk
+                // pass 1: the chunk's row max over valid columns (two TMEM loads in flight per wait)
+                float mx = -INFINITY;
+#pragma unroll
+                for (int g = 0; g < RC / 32; ++g) {
+                    float v[32];
+                    umma::ld32(tS + g * 32, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (g * 32 + i < lim) mx = fmaxf(mx, v[i]);
+                }
+                const float mb = mx * bl2;
+                bool resc = false;
+                float fac = 1.f;
+                if (c == 0) {
+                    M = mb;
+                } else if (mb > M + 8.f) {  // lazy: P <= 2^8 otherwise
+                    fac = ex2_approx(M - mb);
+                    M = mb;
+                    den *= fac;
+                    resc = true;
+                }
+                // warp-uniform (tcgen05.ld / st are warp-collective): rows without a new max scale by 1.
+                // O_t of chunks < c is complete (this chunk's S commit follows their GEMM2)
+                if (__any_sync(0xffffffffu, resc)) {
+#pragma unroll
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        float o[32];
+                        umma::ld32(tO + c0, o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] *= fac;
+                        umma::st32(tO + c0, o);
+                    }
+                }
+                const float Mx = (M == -INFINITY) ? 0.f : M;  // a row with no valid column: all P = 0
+                // pass 2: P = exp2(bl2 s - M) -> bf16 pairs into S_t's columns [0, RC/2) (group g's
+                // pairs overwrite columns already read); den += P w with the fp32 P
+                float dd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int g = 0; g < RC / 32; ++g) {
+                    float v[32];
+                    umma::ld32(tS + g * 32, v);
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int cl = g * 32 + 2 * i;
+                        const float2 w2 = *reinterpret_cast<const float2 *>(sW + cl);
+                        const float p0 = (cl < lim) ? ex2_approx(fmaf(v[2 * i], bl2, -Mx)) : 0.f;
+                        const float p1 = (cl + 1 < lim) ? ex2_approx(fmaf(v[2 * i + 1], bl2, -Mx)) : 0.f;
+                        dd[(2 * i) & 3] = fmaf(p0, w2.x, dd[(2 * i) & 3]);
+                        dd[(2 * i + 1) & 3] = fmaf(p1, w2.y, dd[(2 * i + 1) & 3]);
+                        const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                        pk[i] = *reinterpret_cast<const uint32_t *>(&pb);
+                    }
+                    umma::st16u(tS + g * 16, pk);
+                }
+                den += (dd[0] + dd[1]) + (dd[2] + dd[3]);
+                umma::fence_before_sync();
+                mbar_arrive(&pfull[s]);
+            }
+            // ---- epilogue: O / den, clip, bf16 rows staged in the slot's Q buffer, one bulk store
+            mbar_wait_ws(&ofull[s], no_ph, 7);
+            no_ph ^= 1u;
+            umma::fence_after_sync();
+            const int64_t head = tt / tiles_per_head, q0 = (tt % tiles_per_head) * 128;
+            const float inv = den > 0.f ? 1.f / den : 0.f;
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                float v[32];
+                umma::ld32(tO + c0, v);
+                uint32_t pk[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int col = c0 + 2 * i;
+                    float o0 = v[2 * i] * inv, o1 = v[2 * i + 1] * inv;
+                    if (clip) {
+                        o0 = fminf(fmaxf(o0, __bfloat162float(vmin[(int64_t)u * D + col])), __bfloat162float(vmax[(int64_t)u * D + col]));
+                        o1 = fminf(fmaxf(o1, __bfloat162float(vmin[(int64_t)u * D + col + 1])),
+                                   __bfloat162float(vmax[(int64_t)u * D + col + 1]));
+                    }
+                    const __nv_bfloat162 ob = __floats2bfloat162_rn(o0, o1);
+                    pk[i] = *reinterpret_cast<const uint32_t *>(&ob);
+                }
+                // the 128-byte-swizzled K-major layout of the O tensor map (bank-conflict free by row)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = c0 + 8 * q;
+                    *reinterpret_cast<uint4 *>(stage + umma::sw128_offset(row, col, 128)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+            }
+            fence_proxy_async_smem();
+            wg_sync(3 + s);
+            if (row == 0) {  // rows >= m of the head are outside the O tensor map: clipped by the TMA unit
+#pragma unroll
+                for (int kb = 0; kb < D / 64; ++kb)
+                    tma_store_3d(&omap, stage + kb * 128 * 128, kb * 64, (int)q0, (int)head);
+                tma_store_commit_wait_read();
+                mbar_arrive(&qempty[s]);  // the Q buffer is free for the producer
+            }
+            t = tB >= 0 ? tB + 1 : t + 1;
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (w == 0) umma::tmem_dealloc(tbase, 512);
+}
+
+template <int D>
+int launch_attend_ws(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
+                     const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+    using L = TcLong<D>;
+    using W = WsSmem<D>;
+    if (!ws) return -1;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult qr;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess || !fn)
+            return -1;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    // Q and O as 3-D tensors [batch * hq][m][D] bf16; boxes of 64 columns x 128 rows x 1 head with the
+    // 128-byte swizzle of the UMMA K-major layout: rows past m of a head are out of bounds (zero on
+    // load, dropped on store)
+    CUtensorMap qmap, omap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)D, (cuuint64_t)Dm.m, (cuuint64_t)Dm.batch * Dm.hq};
+    const cuuint64_t gstride[2] = {(cuuint64_t)D * 2, (cuuint64_t)Dm.m * D * 2};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    for (int k = 0; k < 2; ++k)
+        if (encode(k ? &omap : &qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(k ? O : Q), gdim, gstride,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -1;
+    const int nch = (int)ceil_div(Dm.r, L::RC);
+    unsigned char *img = static_cast<unsigned char *>(ws);
+    launch_pdl(attend_long_prep_kernel<D>, dim3(nch, (unsigned)Dm.units(), kPrepParts), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16 *>(KS), X, r_eff, Dm.r, nch, img);
+    auto kern = attend_ws_kernel<D>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, W::kTotal);
+    const int64_t tph = ceil_div(Dm.m, 128);
+    const int64_t total = tph * Dm.hq * Dm.batch;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // whole pairs per CTA: an even tile count per CTA keeps the pairs of a head aligned
+    int64_t tpc = ceil_div(total, (int64_t)sms);
+    tpc += tpc & 1;
+    const int grid = (int)ceil_div(total, tpc);
+    launch_pdl(kern, dim3(grid), dim3(kWsThreads), (size_t)W::kTotal, st, qmap, omap, (const unsigned char *)img, r_eff,
+               static_cast<const __nv_bfloat16 *>(vmin), static_cast<const __nv_bfloat16 *>(vmax), Dm.m, nch,
+               Dm.group(), Dm.hq, Dm.hkv, (float)beta, clip, tph, total);
     return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
@@ -819,13 +1203,15 @@ int launch_attend_t(const Dims &Dm, const void *Q, const void *KS, const float *
 }  // namespace
 
 // 0: CUDA-core kernel, 1: tcgen05 kernel with the coreset resident, 2: tcgen05 kernel streaming r > 256,
-// 3: decode kernel (kvcache.cu) for m <= kDecodeMaxM queries per q-head
+// 3: decode kernel (kvcache.cu) for m <= kDecodeMaxM queries per q-head, 4: warp-specialised tcgen05
+// kernel (two query tiles in flight, TMA, P in tensor memory)
 static int attend_path(const Dims &D) {
-    static const char *mode = std::getenv("WC_ATTEND");  // "cuda": CUDA-core kernel (A/B tests)
+    const char *mode = std::getenv("WC_ATTEND");  // "cuda" / "tc" / "ws": force a path (A/B tests)
     if (mode && std::strcmp(mode, "cuda") == 0) return 0;
     if (D.m > 0 && D.m <= kDecodeMaxM) return 3;
     if (!(D.dtype == 1 && (D.d == 64 || D.d == 128) && D.m > 0)) return 0;
-    return D.r <= 256 ? 1 : 2;
+    if (mode && std::strcmp(mode, "tc") == 0) return D.r <= 256 ? 1 : 2;  // the round-1 tcgen05 kernels
+    return 4;
 }
 
 static int attend_rp(const Dims &D) { return D.r <= 32 ? 32 : D.r <= 64 ? 64 : D.r <= 128 ? 128 : 256; }
@@ -845,7 +1231,7 @@ size_t attend_ws_bytes(const Dims &D) {
         const int stride = D.d == 64 ? img_stride<64>(rp) : img_stride<128>(rp);
         return (size_t)D.units() * stride;
     }
-    if (attend_path(D) != 2) return 0;
+    if (attend_path(D) != 2 && attend_path(D) != 4) return 0;
     const size_t img = D.d == 64 ? TcLong<64>::kImg : TcLong<128>::kImg;
     return D.units() * (size_t)ceil_div(D.r, 128) * img;
 }
@@ -854,6 +1240,10 @@ int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, 
                   const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
     const int path = attend_path(D);
     if (path == 3) return launch_attend_decode(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    if (path == 4) {
+        if (D.d == 64) return launch_attend_ws<64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        return launch_attend_ws<128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    }
     if (path == 2) {
         if (D.d == 64) return launch_attend_tc_long<64>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
         return launch_attend_tc_long<128>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);

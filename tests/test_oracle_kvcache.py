@@ -113,4 +113,5 @@ def test_invalid_split_raises(orc):
     with pytest.raises(ValueError):
         orc.compress_kv(Q, K, V, 4, keep_first=30, keep_last=20)
     with pytest.raises(ValueError):
-        orc.compress_kv(Q, K, V, 8, keep_first=3, keep_last=0, bins=2)  # 37 middle tokens, 2 bins
+        orc.compress_kv(Q, K, V, 60, keep_first=3, keep_last=0, bins=38)  # 37 middle tokens, 38 bins
+    orc.compress_kv(Q, K, V, 8, keep_first=3, keep_last=0, bins=2)  # bins of 18 and 19 (Z13 remainder)
