@@ -194,20 +194,17 @@ def exact_errors(cfg, Qd, Kd, Vd, O):
     return errs
 
 
-def kv_divisor_bins(nmid, target_rows, rb=12):
-    """Bins B for the E3 setting B = r/12: the divisor of n_mid (contiguous bins must divide
-    it, reading Z13) whose B * rb coreset rows come closest to `target_rows`."""
-    best = 1
-    for b in range(1, nmid // rb + 1):
-        if nmid % b == 0 and abs(b * rb - target_rows) < abs(best * rb - target_rows):
-            best = b
-    return best
+def kv_bins(target_rows, rb=12):
+    """Bins B for the E3 setting B = r/12: r = target_rows coreset rows in bins of rb = 12
+    (bins need not divide n_mid: the last bin takes the remainder, reading Z13)."""
+    return max(1, target_rows // rb)
 
 
 def kv_variant(dev, flush, block, steps, with_exact=True):
     """KV-cache workload (E3 protocol P:667-669, reading Z24) at the llm32k
     shapes (GQA 32/8, n = 32768, d = 128, bf16, L family): prefill compression keeping the first and
-    last 32 tokens and compressing the rest to ~25 % of the context with B = r/12 bins (rb = 12), then
+    last 32 tokens and compressing the rest so that the cache holds 25 % of the context, with
+    B = r/12 bins (rb = 12; the last bin takes the remainder of n_mid, reading Z13), then
     one decode step (m = 1 new query per q-head) over the compressed cache vs exact decode attention
     over the full cache.  L2 flushed before every timed call."""
     import torch
@@ -219,7 +216,7 @@ def kv_variant(dev, flush, block, steps, with_exact=True):
     cfg = CONFIGS["llm32k"]
     kf = kl = 32
     nmid = cfg.n - kf - kl
-    bins = kv_divisor_bins(nmid, cfg.n // 4 - kf - kl)
+    bins = kv_bins(cfg.n // 4 - kf - kl)
     r = 12 * bins
     Q, K, V = make_config(cfg)
     Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)

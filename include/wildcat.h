@@ -12,9 +12,10 @@
  *
  * Binning (shape.bins = B > 1; Alg 2; readings Z12, Z13, Z23 of DESIGN.md):
  * the keys of a unit are recentred with the unit's kbar, then split into B contiguous bins of
- * nb = n/B keys (B must divide n: WC_EUNSUPPORTED otherwise); bin b gets its own R_K^b, tau_b
- * (Eq. 7 with n_b) and RPNys at rank rb = min(ceil(r/B), nb) with the Philox stream of
- * sub-unit u*B + b; the bin coresets are concatenated.  Sizes below use R = B*rb (= r when B = 1).
+ * nb = floor(n/B) keys, the last bin also holding the n - B nb remainder (reading Z13); bin b gets
+ * its own R_K^b, tau_b (Eq. 7 with its size n_b) and RPNys at rank rb = min(ceil(r/B), nb) with the
+ * Philox stream of sub-unit u*B + b; the bin coresets are concatenated.  Sizes below use R = B*rb
+ * (= r when B = 1).
  *
  * Layouts (row-major, contiguous, device memory unless stated):
  *   Q, O   [batch][heads_q ][m][d]   dtype
@@ -99,7 +100,7 @@ typedef struct wc_shape {
     int32_t heads_kv;  /* >= 1 */
     int32_t d;         /* head dim: 16, 32, 64 or 128 */
     int32_t r;         /* coreset size, 1 <= r <= n ("rank r") */
-    int32_t bins;      /* B of Alg 2: 1 <= B <= r, B must divide n */
+    int32_t bins;      /* B of Alg 2: 1 <= B <= r (remainder keys join the last bin) */
     int32_t dtype;     /* WC_F32 or WC_BF16 (element type of Q, K, V, O, KS, vmin, vmax) */
     int32_t reserved;
     int64_t m;         /* queries per q-head, >= 0 */
@@ -174,7 +175,7 @@ int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, c
  * The E3 protocol retains the first and last tokens of the context exactly and
  * compresses the rest: per unit, the first keep_first and last keep_last of the n tokens are kept,
  * and the n_mid = n - keep_first - keep_last middle tokens go through CompressKV (Alg 2,
- * P:297-313) at rank shape->r with shape->bins bins (B | n_mid; r <= n_mid; recentring, R_K and tau
+ * P:297-313) at rank shape->r with shape->bins bins (B <= r <= n_mid; recentring, R_K and tau
  * over the middle only; R_Q from Q's m prompt rows per q-head, or opts->rq >= 0, Q then nullable;
  * Philox unit ids as wildcat_forward; opts->block as wildcat_select).  Reading Z24:
  * the cache is the union of exact and compressed entries, so WtdAttn over it adds the retained
@@ -192,7 +193,7 @@ int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, c
  * shape.bins = 1, shape.m = new queries per q-head, KS = KC, X = XC, r_eff = c_eff; for
  * m <= 16 it runs a decode kernel that splits the cache over CTAs (fp32 scores and sums).
  * Errors: WC_ESHAPE for keep_* < 0 or n_mid < 0 and the wildcat_select shape rules applied to the
- * middle; WC_EUNSUPPORTED when B does not divide n_mid. */
+ * middle. */
 size_t wc_kv_capacity(const wc_shape *shape, int32_t keep_first, int32_t keep_last);       /* 0 if invalid */
 size_t wc_kv_workspace_bytes(const wc_shape *shape, int32_t keep_first, int32_t keep_last); /* 0 if invalid */
 int wildcat_compress_kv(const wc_shape *shape, const wc_opts *opts, int32_t keep_first, int32_t keep_last,

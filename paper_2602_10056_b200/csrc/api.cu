@@ -58,8 +58,7 @@ int check_shape(const wc_shape *s) {
     if (s->batch < 1 || s->heads_q < 1 || s->heads_kv < 1 || s->heads_q % s->heads_kv) return WC_ESHAPE;
     if (!(s->d == 16 || s->d == 32 || s->d == 64 || s->d == 128)) return WC_ESHAPE;
     if (s->n < 1 || s->n > (int64_t)0x7fffffff || s->m < 0 || s->r < 1 || s->r > s->n) return WC_ESHAPE;
-    if (s->bins < 1 || s->bins > s->r) return WC_ESHAPE;
-    if (s->n % s->bins) return WC_EUNSUPPORTED;  // bins must divide n in this build (Alg 2 "evenly divide")
+    if (s->bins < 1 || s->bins > s->r) return WC_ESHAPE;  // (so bins <= r <= n: every bin has a key)
     return WC_OK;
 }
 
@@ -72,8 +71,9 @@ wc::Dims dims_of(const wc_shape *s) {
 
 // Binning plan (Alg 2; readings Z12, Z13, Z23).  D: the unit-level problem (prologue,
 // value range, attend with R coreset rows); Ds: the sub-unit problem of the selection and weights
-// kernels -- unit u, bin b -> sub-unit u*B + b with nb = n/B keys and rank rb = min(ceil(r/B), nb).
-// With B = 1, Ds = D and R = r.
+// kernels -- unit u, bin b -> sub-unit u*B + b with nb = floor(n/B) keys (the last bin also holds the
+// n - B nb remainder: Ds.n = nb + remainder is the per-sub-unit buffer size, Dims::sub_unit() the
+// geometry) and rank rb = min(ceil(r/B), nb).  With B = 1, Ds = D and R = r.
 struct Plan {
     wc::Dims D, Ds, Da;  // unit level, sub-unit level, attend (unit level with r = R)
     int B, rb, R;
@@ -88,8 +88,11 @@ Plan plan_of(const wc_shape *s) {
     p.Ds = p.D;
     p.Ds.hkv = p.D.hkv * p.B;
     p.Ds.hq = p.D.hq * p.B;  // keeps group() = hq/hkv; the sub-unit dims never touch Q
-    p.Ds.n = nb;
+    p.Ds.n = nb + (s->n - (int64_t)p.B * nb);
     p.Ds.r = p.rb;
+    p.Ds.bins = p.B;
+    p.Ds.nb = nb;
+    p.Ds.unit_n = s->n;
     p.Da = p.D;
     p.Da.r = p.R;
     return p;
@@ -210,7 +213,8 @@ void carve_weights(Carver &c, const wc_shape *s, const Plan &p, WeightsWs &w) {
     const wc::Dims &D = p.Ds;
     const size_t U = D.units();
     const size_t parts = U * wc::weights_num_splits(D) * (size_t)D.r * (D.d + 1);
-    w.Ypart = c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1) + 2 * U * wc::dinv_elems(D.r));
+    w.Ypart = c.take<float>(((parts + 1) & ~size_t(1)) + 2 * U * (size_t)D.r * (D.d + 1) + 2 * U * wc::dinv_elems(D.r) +
+                            2 * U * wc::solve_scratch_elems(D.r, D.d));
     if (p.B > 1) {
         w.Ssub = c.take<int32_t>(U * D.r);
         w.reff_sub = c.take<int32_t>(U);
@@ -647,7 +651,7 @@ const char *wc_strerror(int st) {
         case WC_EWORKSPACE: return "workspace too small or not 256-byte aligned";
         case WC_ECUDA: return "CUDA launch or runtime error";
         case WC_ENCCL: return "NCCL error";
-        case WC_EUNSUPPORTED: return "unsupported configuration in this build (bins not dividing n, n-sharded bins/blocks, r too large for blocked selection)";
+        case WC_EUNSUPPORTED: return "unsupported configuration in this build (n-sharded bins/blocks, r too large for the selection plan)";
         case WC_ENONFINITE: return "non-finite input (NaN or Inf) found by WC_CHECK_FINITE";
     }
     return "unknown status";

@@ -1,7 +1,8 @@
 // bins.cu -- Alg 2 binning on top of the per-unit kernels: every (unit u,
 // bin b) pair is a sub-unit su = u*B + b of the selection and weights kernels (contiguous bins of
-// nb = n/B keys; the K/V reshape [units][n] -> [units*B][nb] is free).  Readings Z12 (tau_b uses
-// n_b), Z13 (r_b = min(ceil(r/B), n_b)), Z23 (Philox stream of sub-unit u*B + b).
+// nb = floor(n/B) keys, the last one also holding the n - B nb remainder: the kernels address a
+// sub-unit's keys through Dims::sub_unit()).  Readings Z12 (tau_b uses n_b), Z13 (r_b =
+// min(ceil(r/B), nb), remainder in the last bin), Z23 (Philox stream of sub-unit u*B + b).
 //   bins_stats_kernel: per sub-unit R_K^b = max ||k_l - kbar|| over the bin (global kbar, from
 //     the unit prologue's nrm2), tau_b (Eq. 7 with n_b), g_b, mstar_b; R_Q and kbar of the unit.
 //   bins_pack_kernel:  concatenate the bins' valid coreset rows into the unit layout (S with
@@ -19,14 +20,15 @@ namespace {
 constexpr int kBT = 256;
 
 __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restrict__ stats_u, const double *__restrict__ nrm2,
-                                                         int64_t nb, int d, int bins, double beta, double *__restrict__ stats_b,
-                                                         int tau_one) {
+                                                         int64_t nb, int64_t unit_n, int d, int bins, double beta,
+                                                         double *__restrict__ stats_b, int tau_one) {
     pdl_wait();
     __shared__ double scr[40];
     const int su = blockIdx.x, u = su / bins;
-    const double *nr = nrm2 + (int64_t)su * nb;  // nrm2 [units][n] == [units*B][nb]
+    const SubUnit sub = sub_unit(su, nb, bins, nb, unit_n);  // the last bin also holds the remainder (Z13)
+    const double *nr = nrm2 + sub.base;  // nrm2 [units][unit_n]
     double mx = 0.0;
-    for (int64_t l = threadIdx.x; l < nb; l += kBT) mx = fmax(mx, __ldg(nr + l));
+    for (int64_t l = threadIdx.x; l < sub.count; l += kBT) mx = fmax(mx, __ldg(nr + l));
     mx = block_max(mx, scr);
     const double *su_u = stats_u + (int64_t)u * (kStatsHead + d);
     double *sb = stats_b + (int64_t)su * (kStatsHead + d);
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(kBT) bins_stats_kernel(const double *__restric
         double tau = 1.0;
         if (!tau_one && rq * rk > 0.0) {  // Eq. 7 with n_b (Z12); WC_TAU_ONE: tau = 1
             const double rho0 = sqrt(1.0 + exp(lambert_w0_dev(2.0 / (2.718281828459045 * 2.718281828459045)) + 2.0));
-            const double b0 = log((double)nb) / (beta * rq * rk) + 2.0;
+            const double b0 = log((double)sub.count) / (beta * rq * rk) + 2.0;
             const double w = lambert_w0_dev(b0 / (2.0 * rho0));
             tau = sqrt((rk / rq) * b0 / (2.0 * w));
         }
@@ -122,7 +124,7 @@ __global__ void bins_unpack_kernel(const int32_t *__restrict__ S, int units, int
         for (int a = 0; a < R; ++a) {
             const int s = S[(int64_t)u * R + a];
             if (s < 0) break;
-            const int b = (int)(s / nb);
+            const int b = (int)(s / nb < bins - 1 ? s / nb : bins - 1);  // remainder keys belong to the last bin
             if (b != cur) { cur = b; cnt = 0; }
             Ssub[((int64_t)u * bins + b) * rb + cnt] = (int32_t)(s - b * nb);
             reff_sub[u * bins + b] = ++cnt;
@@ -134,8 +136,8 @@ __global__ void bins_unpack_kernel(const int32_t *__restrict__ S, int units, int
 
 int launch_bins_stats(const Dims &D, int bins, double beta, const double *stats_u, const double *nrm2, double *stats_b,
                       int pflags, cudaStream_t st) {
-    launch_pdl(bins_stats_kernel, dim3(D.units() * bins), dim3(kBT), 0, st, stats_u, nrm2, D.n / bins, D.d, bins, beta,
-               stats_b, (pflags & kPfTauOne) ? 1 : 0);
+    launch_pdl(bins_stats_kernel, dim3(D.units() * bins), dim3(kBT), 0, st, stats_u, nrm2, D.n / bins, D.n, D.d, bins,
+               beta, stats_b, (pflags & kPfTauOne) ? 1 : 0);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -13,9 +13,28 @@ constexpr int kMaxR = 1024;  // largest r (or rb per bin) of a selection problem
 struct Dims {
     int batch, hq, hkv, d, r, dtype;
     int64_t m, n;
+    // Sub-unit geometry of Alg 2 binning (readings Z12, Z13): with bins > 1 a "unit" of these dims is
+    // the sub-unit su = u * bins + b, whose keys are rows [b nb, b nb + count) of unit u's unit_n keys
+    // (nb = floor(unit_n / bins); the last bin also holds the remainder); n is then the largest
+    // sub-unit (the per-sub-unit buffer stride).  bins = 1: plain units of n keys.
+    int bins = 1;
+    int64_t nb = 0, unit_n = 0;
     int units() const { return batch * hkv; }
     int group() const { return hq / hkv; }
 };
+
+// Keys of sub-unit su (count) and the row of its first key in the unit-level K / V / nrm2 arrays.
+struct SubUnit {
+    int64_t count, base;
+};
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline SubUnit sub_unit(int su, int64_t n, int bins, int64_t nb, int64_t unit_n) {
+    if (bins <= 1) return SubUnit{n, (int64_t)su * n};
+    const int b = su % bins;
+    return SubUnit{b == bins - 1 ? unit_n - (int64_t)(bins - 1) * nb : nb, (int64_t)(su / bins) * unit_n + (int64_t)b * nb};
+}
 
 // Workspace blocks used by the prologue (A0).
 struct ProloguePartials {
@@ -119,6 +138,13 @@ int launch_weights_partial_ks(const Dims &D, const void *K, const void *V, const
 int launch_weights_solve(const Dims &D, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
                          double *Dinv, cudaStream_t st);
 inline size_t dinv_elems(int r) { return (size_t)((r + 31) / 32) * 32 * 32; }
+// Scratch of the inverse-based solve per unit (doubles): W = L^{-1} (R x R, R = 32 * 2^k >= r), the level
+// products (R x R / 4) and W Y~ (R x (d + 1)).
+inline size_t solve_scratch_elems(int r, int d) {
+    size_t R = 32;
+    while ((int)R < r) R *= 2;
+    return R * R + R * R / 4 + R * (size_t)(d + 1);
+}
 
 // A5: attend.
 int launch_attend(const Dims &D, const void *Q, const void *KS, const float *X, const int32_t *r_eff,

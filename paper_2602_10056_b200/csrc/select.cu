@@ -45,7 +45,9 @@ struct SelArgs {
     int32_t *S;
     int32_t *r_eff;
     double *L;
-    int64_t n;
+    int64_t n;    // keys per sub-unit buffer (the largest sub-unit)
+    int bins;     // sub-unit geometry (Dims::bins, nb, unit_n; sub_unit())
+    int64_t nb, unit_n;
     int64_t ldF;  // row stride of F (n rounded up to 32: every row segment is 256-byte aligned)
     int units, r, cpu;
     uint64_t seed;
@@ -82,15 +84,16 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     __shared__ double sh_t, sh_ps;
 
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
-    const int64_t n = a.n;
+    const SubUnit sub = sub_unit(u, a.n, a.bins, a.nb, a.unit_n);
+    const int64_t n = sub.count;  // this sub-unit's keys (a.n: the buffer stride)
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
 
-    const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
+    const T *Ku = static_cast<const T *>(a.K) + sub.base * D;
     const double *st = a.stats + (int64_t)u * (kStatsHead + D);
     const double g = st[1], mstar = st[2];
-    double *p0 = a.p + (int64_t)u * n;
-    double *p1 = a.p + ((int64_t)a.units + u) * n;
+    double *p0 = a.p + (int64_t)u * a.n;
+    double *p1 = a.p + ((int64_t)a.units + u) * a.n;
     double *Fu = a.F + (int64_t)u * a.r * a.ldF;
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
     unsigned *bar = a.bar + u;
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kSelThreads) rpc_select_kernel(SelArgs a) {
     // p <- kernel diagonal h~(k_l, k_l) = exp(g ||k_l - kbar||^2 - mstar)   (Alg 1)
     double loc = 0.0;
     for (int64_t l = lo + tid; l < hi; l += nt) {
-        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
+        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[sub.base + l]), -mstar));
         p0[l] = v;
         loc += v;
     }
@@ -329,16 +332,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
 
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
-    const int64_t n = a.n;
+    const SubUnit sub = sub_unit(u, a.n, a.bins, a.nb, a.unit_n);
+    const int64_t n = sub.count;  // this sub-unit's keys (a.n: the buffer stride)
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
+    const int64_t chunk_max = ((ceil_div(a.n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
     const int nst = (int)ceil_div(hi - lo, kST);
 
-    const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
+    const T *Ku = static_cast<const T *>(a.K) + sub.base * D;
     const double *st = a.stats + (int64_t)u * (kStatsHead + D);
     // tile-major F: CTA c' owns [r x chunk]; its super-tile k' is the block [r][w_k'] at column
     // offset 256 k', w_k' = min(256, chunk - 256 k') (a multiple of 32): 8 rows = one contiguous copy
-    double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
+    double *Fu = a.F + (int64_t)u * a.cpu * chunk_max * a.r;
     double *Fc = Fu + (int64_t)c * chunk * a.r;  // this CTA's blocks
     auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(kST, chunk - (int64_t)k * kST); };
 
@@ -395,14 +400,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1) rpc_select_tma_kernel(SelArgs 
 
     // ================= compute warps (256 threads) =================
     const double g = st[1], mstar = st[2];
-    double *p0 = a.p + (int64_t)u * n;
-    double *p1 = a.p + ((int64_t)a.units + u) * n;
+    double *p0 = a.p + (int64_t)u * a.n;
+    double *p1 = a.p + ((int64_t)a.units + u) * a.n;
     for (int j = tid; j < D; j += kCT) kb[j] = st[kStatsHead + j];
 
     double loc = 0.0;
     double p_first = 0.0;  // residual of this thread's key in super-tile 0 (kept in a register)
     for (int64_t l = lo + tid; l < hi; l += kCT) {
-        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
+        const double v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[sub.base + l]), -mstar));
         p0[l] = v;
         if (l == lo + tid) p_first = v;
         loc += v;
@@ -706,6 +711,7 @@ int launch_select_td(const Dims &Dm, const void *K, const double *stats, SelectB
     SelArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.ldF = f_ld(Dm.n); a.units = Dm.units(); a.r = Dm.r;
+    a.bins = Dm.bins; a.nb = Dm.nb; a.unit_n = Dm.unit_n;
     a.nstm = f_tile_nst(Dm.n, select_ctas_per_unit(Dm));
     a.cpu = select_ctas_per_unit(Dm); a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
     {

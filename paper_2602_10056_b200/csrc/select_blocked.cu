@@ -89,7 +89,9 @@ struct BlkArgs {
     int32_t *S;
     int32_t *r_eff;
     double *L;
-    int64_t n;
+    int64_t n;                 // keys per sub-unit buffer (the largest sub-unit)
+    int bins;                  // sub-unit geometry (Dims::bins, nb, unit_n; sub_unit())
+    int64_t nb, unit_n;
     int units, r, cpu, b;
     uint64_t seed;
     uint64_t unit0;  // Philox id of sub-unit 0 (wc_opts.unit_offset [x B]); unit u draws stream unit0 + u
@@ -288,8 +290,10 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
     const int gid = lane >> 2, tq = lane & 3;
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
-    const int64_t n = a.n;
+    const SubUnit sub = sub_unit(u, a.n, a.bins, a.nb, a.unit_n);
+    const int64_t n = sub.count;  // this sub-unit's keys (a.n: the buffer stride)
     const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
+    const int64_t chunk_max = ((ceil_div(a.n, a.cpu) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
     const int nst = (int)ceil_div(hi - lo, BT);
     const int bsz = a.b;
@@ -297,9 +301,9 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     // the per-key triangle stages both of a lane's keys at once when the ring holds [64][SP] per warp
     const bool two_keys = (size_t)NS * kBR * PITCH >= (size_t)kCW * 64 * SP;
 
-    const T *Ku = static_cast<const T *>(a.K) + (int64_t)u * n * D;
+    const T *Ku = static_cast<const T *>(a.K) + sub.base * D;
     double *st = a.stats + (int64_t)u * (kStatsHead + D);
-    double *Fu = a.F + (int64_t)u * a.cpu * chunk * a.r;
+    double *Fu = a.F + (int64_t)u * a.cpu * chunk_max * a.r;
     double *Fc = Fu + (int64_t)c * chunk * a.r;
     auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(BT, chunk - (int64_t)k * BT); };
 
@@ -444,21 +448,21 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
 
     // ================= compute warps (256 threads) =================
     const double g = st[1], mstar = st[2];
-    double *p0 = a.p + (int64_t)u * n;
-    double *p1 = a.p + ((int64_t)a.units + u) * n;
+    double *p0 = a.p + (int64_t)u * a.n;
+    double *p1 = a.p + ((int64_t)a.units + u) * a.n;
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
     for (int j = tid; j < D; j += kCT) kb[j] = st[kStatsHead + j];
 
     // p <- kernel diagonal h~(k_l, k_l) (Alg 1); 32-key group sums (one warp per group)
     double loc = 0.0;
     {
-        const int ngr0 = (int)((n + 31) / 32);
+        const int ngr0 = (int)((a.n + 31) / 32);  // group-sum stride per sub-unit (buffer size)
         double *g0s = a.gsum + (int64_t)u * 2 * ngr0;
         for (int64_t gb = lo + 32 * w; gb < hi; gb += kCT) {
             const int64_t l = gb + lane;
             double v = 0.0;
             if (l < hi) {
-                v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[(int64_t)u * n + l]), -mstar));
+                v = exp(__dadd_rn(__dmul_rn(g, a.nrm2[sub.base + l]), -mstar));
                 p0[l] = v;
             }
             v = warp_sum(v);
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
 
         // ---- 1a (warp 0): per-CTA residual sums -> shared memory (one L2 read per CTA), lane
         // partition sums and their inclusive prefix, total T (fixed order)
-        const int ngr = (int)((n + 31) / 32);
+        const int ngr = (int)((a.n + 31) / 32);
         const double *gcur = a.gsum + ((int64_t)u * 2 + (blk & 1)) * ngr;
         double *gnxt = a.gsum + ((int64_t)u * 2 + ((blk + 1) & 1)) * ngr;
         const int per = (a.cpu + 31) / 32;
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         // with the centred candidate keys (fp64, MMA layout) and the parts of c0[j] = <kbar, k_sj - kbar>
         const int i4 = (i + 3) & ~3;
         if (tid == 0 && i > 0) {
-            const double *FTu = a.FT + (int64_t)u * n * ftl;
+            const double *FTu = a.FT + (int64_t)u * a.n * ftl;
             mbar_arrive_expect_tx(colbar, (uint32_t)(bsz * i4 * sizeof(double)));
             for (int j = 0; j < bsz; ++j)
                 bulk_g2s(Fcol + (size_t)j * ldc, FTu + (int64_t)cs[j] * ftl, (uint32_t)(i4 * sizeof(double)), colbar);
@@ -869,7 +873,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     const int64_t key = t0 + kw + 32 * h + lane;
                     if (key < hi) {
                         nxt[key] = pl;
-                        double *ftr = a.FT + ((int64_t)u * n + key) * ftl + i;  // key-major copy of the new rows
+                        double *ftr = a.FT + ((int64_t)u * a.n + key) * ftl + i;  // key-major copy of the new rows
                         if (i & 1) {  // 16-byte stores from the first even index (FT rows are 32-byte aligned)
                             if (na > 0) ftr[0] = f[0];
 #pragma unroll
@@ -1034,6 +1038,7 @@ int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs 
     a.gsum = b.gsum;
     a.FT = b.FT;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
+    a.bins = Dm.bins; a.nb = Dm.nb; a.unit_n = Dm.unit_n;
     a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
     const int ldc = ((Dm.r + 15) & ~15) + 4;
     const int NS = blocked_stages<D, NSL>(Dm.r, a.cpu);

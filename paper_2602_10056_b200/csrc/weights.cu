@@ -29,8 +29,9 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
                                                               const int32_t *__restrict__ S,
                                                               const T *__restrict__ KSin,
                                                               const int32_t *__restrict__ r_eff,
-                                                              const double *__restrict__ stats, int64_t n,
-                                                              int r, int splits, float *__restrict__ Ypart) {
+                                                              const double *__restrict__ stats, int64_t n_buf,
+                                                              int r, int splits, float *__restrict__ Ypart, int bins,
+                                                              int64_t nb, int64_t unit_n) {
     constexpr int DC = D + 1;
     constexpr int CPT = (DC + 7) / 8;  // accumulator columns per thread
     extern __shared__ double wsm[];
@@ -48,8 +49,10 @@ __global__ void __launch_bounds__(kWT) weights_partial_kernel(const T *__restric
     const float g = (float)st[1], mstar = (float)st[2];
     for (int j = tid; j < D; j += kWT) kb[j] = st[kStatsHead + j];
     __syncthreads();
-    const T *Ku = K + (int64_t)u * n * D;
-    const T *Vu = V + (int64_t)u * n * D;
+    const SubUnit sub = sub_unit(u, n_buf, bins, nb, unit_n);  // keys of this (sub-)unit (Z13)
+    const int64_t n = sub.count;
+    const T *Ku = K + sub.base * D;
+    const T *Vu = V + sub.base * D;
     for (int e = tid; e < kTA * D; e += kWT) {
         const int a = e / D, j = e % D;
         float v = 0.f;
@@ -374,13 +377,14 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
 
 template <typename T, int D>
 __global__ void gather_ks_kernel(const T *__restrict__ K, const int32_t *__restrict__ S,
-                                 const int32_t *__restrict__ r_eff, int64_t n, int r, T *__restrict__ KS) {
+                                 const int32_t *__restrict__ r_eff, int64_t n, int r, T *__restrict__ KS, int bins,
+                                 int64_t nb, int64_t unit_n) {
     pdl_wait();
     const int u = blockIdx.y, a = blockIdx.x;
     const int q = r_eff[u];
     const int s = a < q ? S[(int64_t)u * r + a] : -1;
     for (int j = threadIdx.x; j < D; j += blockDim.x)
-        KS[((int64_t)u * r + a) * D + j] = s >= 0 ? K[((int64_t)u * n + s) * D + j] : from_f32<T>(0.f);
+        KS[((int64_t)u * r + a) * D + j] = s >= 0 ? K[(sub_unit(u, n, bins, nb, unit_n).base + s) * D + j] : from_f32<T>(0.f);
 }
 
 // =====================================================================================
@@ -418,7 +422,8 @@ __global__ void __launch_bounds__(kWTc, 1)
     weights_tc_kernel(const __nv_bfloat16 *__restrict__ K, const __nv_bfloat16 *__restrict__ V,
                       const int32_t *__restrict__ S, const __nv_bfloat16 *__restrict__ KSin,
                       const int32_t *__restrict__ r_eff,
-                      const double *__restrict__ stats, int64_t n, int r, int splits, float *__restrict__ Ypart) {
+                      const double *__restrict__ stats, int64_t n_buf, int r, int splits, float *__restrict__ Ypart,
+                      int bins, int64_t nb, int64_t unit_n) {
     pdl_wait();
     using L = WtSmem<D>;
     constexpr int DC = D + 1;
@@ -439,8 +444,10 @@ __global__ void __launch_bounds__(kWTc, 1)
     const int split = blockIdx.x, a0 = blockIdx.y * 128, u = blockIdx.z;
     const int re = r_eff[u];
     if (a0 >= re) return;  // uniform per CTA
-    const __nv_bfloat16 *Ku = K + (int64_t)u * n * D;
-    const __nv_bfloat16 *Vu = V + (int64_t)u * n * D;
+    const SubUnit sub = sub_unit(u, n_buf, bins, nb, unit_n);  // keys of this (sub-)unit (Z13)
+    const int64_t n = sub.count;
+    const __nv_bfloat16 *Ku = K + sub.base * D;
+    const __nv_bfloat16 *Vu = V + sub.base * D;
     const double *st = stats + (int64_t)u * (kStatsHead + D);
     const double g = st[1], mstar = st[2];
 
@@ -652,7 +659,7 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
             dim3 gt(splits, (Dm.r + 127) / 128, units);
             launch_pdl(kt, gt, dim3(kWTc), smem_tc, st, static_cast<const __nv_bfloat16 *>(K),
                        static_cast<const __nv_bfloat16 *>(V), S, static_cast<const __nv_bfloat16 *>(KSin), r_eff,
-                       stats, Dm.n, Dm.r, splits, Ypart);
+                       stats, Dm.n, Dm.r, splits, Ypart, Dm.bins, Dm.nb, Dm.unit_n);
             done = true;
         }
     }
@@ -663,7 +670,8 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
         auto pk = weights_partial_kernel<T, D>;
         cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
         pk<<<g1, kWT, smem1, st>>>(static_cast<const T *>(K), static_cast<const T *>(V), S,
-                                   static_cast<const T *>(KSin), r_eff, stats, Dm.n, Dm.r, splits, Ypart);
+                                   static_cast<const T *>(KSin), r_eff, stats, Dm.n, Dm.r, splits, Ypart, Dm.bins, Dm.nb,
+                                   Dm.unit_n);
     }
     const size_t parts = (size_t)units * splits * Dm.r * (D + 1);
     double *Yfull = *Yfull_out ? *Yfull_out : reinterpret_cast<double *>(Ypart + ((parts + 1) & ~size_t(1)));
@@ -758,19 +766,201 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
     return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
 }
 
+// =====================================================================================
+// A4 by an explicit inverse: W = L^{-1} by recursive doubling over the 32 x 32 diagonal-block
+// inverses (Dinv), then X = W^T (W Y~) -- every step a batched fp64 GEMM on the DMMA pipe, so the
+// dependent chain is log2(R / 32) + 2 GEMM launches instead of the panel-by-panel substitution.
+// For lower-triangular L = [[A, 0], [B, C]]:  L^{-1} = [[A^{-1}, 0], [-C^{-1} B A^{-1}, C^{-1}]].
+// R = 32 * 2^k >= r; L is read with its valid extent r_eff (zero beyond), W is R x R (zero padded),
+// so W's valid block is exactly L[:q, :q]^{-1} and rows >= r_eff of X come out 0.
+// =====================================================================================
+constexpr int kGT = 64;   // output tile (rows and columns) of one CTA
+constexpr int kGK = 32;   // K extent staged per step
+
+inline int inv_pad(int r) {
+    int R = kPB;
+    while (R < r) R *= 2;
+    return R;
+}
+
+// Batched GEMM  C (+)= alpha * op(A) B  on 64 x 64 output tiles (blockIdx.x: column tile, blockIdx.y:
+// row tile, blockIdx.z: batch = unit * nper + j).  A(i, k) = TA ? Abuf[k * lda + i] : Abuf[i * lda + k].
+// Element (i, k) of A exists only for i < a_rows, k < a_cols (zero otherwise); B(k, c) for k < b_rows,
+// c < b_cols.  Pointers of batch z: base + unit * ustride + j * jstride (+ the per-mode block offsets
+// folded in by the launcher through jrow / jcol multipliers below).
+struct GemmArgs {
+    const double *A;
+    const double *B;
+    void *C;
+    int64_t a_ustride, a_jstride, b_ustride, b_jstride, c_ustride, c_jstride;
+    int lda, ldb, ldc;
+    int M, N, K;
+    int nper;
+    const int32_t *valid;  // r_eff per unit: A rows/cols and B rows limited to it when ka_valid / kb_valid
+    int a_limit_rows, a_limit_cols, b_limit_rows;  // flags: 1 -> limit that extent by valid[unit] - offset
+    int a_row0, a_col0, b_row0;                    // offsets (in the unit's matrix) of the first row / col
+    int64_t a_row0_j, a_col0_j, b_row0_j;          // their per-j increments
+    double alpha;
+};
+
+template <bool TA, bool OUTF32, bool ACC>
+__global__ void __launch_bounds__(256) dgemm_batched_kernel(GemmArgs g) {
+    pdl_wait();
+    __shared__ double As[kGT][kGK + 1];  // As[i][k]
+    __shared__ double Bs[kGK][kGT + 1];  // Bs[k][c]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gid = lane >> 2, tq = lane & 3;
+    const int z = blockIdx.z, u = z / g.nper, j = z % g.nper;
+    const int i0 = blockIdx.y * kGT, c0 = blockIdx.x * kGT;
+    if (i0 >= g.M || c0 >= g.N) return;
+    const double *A = g.A + u * g.a_ustride + j * g.a_jstride;
+    const double *B = g.B + u * g.b_ustride + j * g.b_jstride;
+    const int q = g.valid ? g.valid[u] : INT32_MAX;
+    const int64_t ar0 = g.a_row0 + j * g.a_row0_j, ac0 = g.a_col0 + j * g.a_col0_j, br0 = g.b_row0 + j * g.b_row0_j;
+    const int64_t arows = g.a_limit_rows ? std::min<int64_t>(g.M, q - ar0) : g.M;
+    const int64_t acols = g.a_limit_cols ? std::min<int64_t>(g.K, q - ac0) : g.K;
+    const int64_t brows = g.b_limit_rows ? std::min<int64_t>(g.K, q - br0) : g.K;
+    double acc[kGT / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < kGT / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    for (int k0 = 0; k0 < g.K; k0 += kGK) {
+        for (int e = tid; e < kGT * kGK; e += 256) {
+            int i, k;
+            if (TA) { k = e / kGT; i = e % kGT; } else { i = e / kGK; k = e % kGK; }  // coalesced reads
+            const int gi = i0 + i, gk = k0 + k;
+            double v = 0.0;
+            if (gi < arows && gk < acols) v = TA ? A[(int64_t)gk * g.lda + gi] : A[(int64_t)gi * g.lda + gk];
+            As[i][k] = v;
+        }
+        for (int e = tid; e < kGK * kGT; e += 256) {
+            const int k = e / kGT, c = e % kGT, gk = k0 + k, gc = c0 + c;
+            Bs[k][c] = (gk < brows && gc < g.N) ? B[(int64_t)gk * g.ldb + gc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kGK; kk += 4) {
+            const double a = As[8 * w + gid][kk + tq];
+#pragma unroll
+            for (int nt = 0; nt < kGT / 8; ++nt) {
+                const double b = Bs[kk + tq][8 * nt + gid];
+                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(acc[nt][0]), "+d"(acc[nt][1])
+                    : "d"(a), "d"(b));
+            }
+        }
+        __syncthreads();
+    }
+    const int gi = i0 + 8 * w + gid;
+    if (gi >= g.M) return;
+#pragma unroll
+    for (int nt = 0; nt < kGT / 8; ++nt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int gc = c0 + 8 * nt + 2 * tq + hh;
+            if (gc >= g.N) continue;
+            const int64_t o = u * g.c_ustride + j * g.c_jstride + (int64_t)gi * g.ldc + gc;
+            if (OUTF32) {
+                static_cast<float *>(g.C)[o] = (float)(g.alpha * acc[nt][hh]);
+            } else {
+                double *C = static_cast<double *>(g.C);
+                C[o] = ACC ? C[o] + g.alpha * acc[nt][hh] : g.alpha * acc[nt][hh];
+            }
+        }
+}
+
+// W <- 0 with the 32 x 32 diagonal-block inverses of L on its diagonal (block b < ceil(q/32)).
+__global__ void __launch_bounds__(256) winit_kernel(const double *__restrict__ Dinv, const int32_t *__restrict__ r_eff,
+                                                    int r, int R, double *__restrict__ W) {
+    pdl_wait();
+    const int u = blockIdx.y;
+    const int nbl = (r + kPB - 1) / kPB;
+    double *Wu = W + (int64_t)u * R * R;
+    const double *Du = Dinv + (int64_t)u * nbl * kPB * kPB;
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < (int64_t)R * R; e += (int64_t)gridDim.x * 256) {
+        const int i = (int)(e / R), c = (int)(e % R);
+        const int bi = i / kPB;
+        // blocks at or past r_eff were never written by the inversion: zero
+        Wu[e] = (bi == c / kPB && bi < nbl && bi * kPB < r_eff[u]) ? Du[(int64_t)bi * kPB * kPB + (i % kPB) * kPB + (c % kPB)]
+                                                                   : 0.0;
+    }
+}
+
+template <bool TA, bool OUTF32, bool ACC>
+void launch_gemm(const GemmArgs &g, int batch, cudaStream_t st) {
+    launch_pdl(dgemm_batched_kernel<TA, OUTF32, ACC>, dim3((unsigned)ceil_div(g.N, kGT), (unsigned)ceil_div(g.M, kGT),
+                                                         (unsigned)batch),
+               dim3(256), 0, st, g);
+}
+
+// X = W^T W Y~ with W = L^{-1}.  scratch: units * (R*R + R*R/4 + R*(d+1)) doubles.
+int launch_solve_inverse(const Dims &Dm, const double *Y, const double *L, const int32_t *r_eff, float *X,
+                         const double *Dinv, double *scratch, cudaStream_t st) {
+    const int r = Dm.r, R = inv_pad(r), U = Dm.units(), DC = Dm.d + 1;
+    double *W = scratch, *T = W + (size_t)U * R * R, *X1 = T + (size_t)U * R * R / 4;
+    int launches = 0;
+    launch_pdl(winit_kernel, dim3((unsigned)std::min<int64_t>(ceil_div((int64_t)R * R, 256), 64), U), dim3(256), 0, st,
+               Dinv, r_eff, r, R, W);
+    ++launches;
+    for (int s2 = kPB; s2 < R; s2 *= 2) {
+        const int np = R / (2 * s2);
+        // T_j = L[(2j+1)s : (2j+2)s, 2js : 2js+s] . W[2js : 2js+s, 2js : 2js+s]
+        // (batch j: L block rows [(2j+1)s, (2j+2)s), columns [2js, 2js + s), limited to r_eff)
+        GemmArgs g{};
+        g.A = L + (int64_t)s2 * r; g.a_ustride = (int64_t)r * r; g.a_jstride = (int64_t)(2 * s2) * r + 2 * s2;
+        g.lda = r;
+        g.a_row0 = s2; g.a_row0_j = 2 * s2; g.a_col0 = 0; g.a_col0_j = 2 * s2;
+        g.a_limit_rows = 1; g.a_limit_cols = 1;
+        g.B = W; g.b_ustride = (int64_t)R * R; g.b_jstride = (int64_t)(2 * s2) * R + 2 * s2; g.ldb = R;
+        g.C = T; g.c_ustride = (int64_t)R * R / 4; g.c_jstride = (int64_t)s2 * s2; g.ldc = s2;
+        g.M = s2; g.N = s2; g.K = s2; g.nper = np; g.valid = r_eff;
+        g.alpha = 1.0;
+        launch_gemm<false, false, false>(g, U * np, st);
+        // W[(2j+1)s :, 2js :] = -W[(2j+1)s :, (2j+1)s :] . T_j
+        GemmArgs h{};
+        h.A = W + (int64_t)s2 * R + s2; h.a_ustride = (int64_t)R * R; h.a_jstride = (int64_t)(2 * s2) * R + 2 * s2;
+        h.lda = R;
+        h.B = T; h.b_ustride = (int64_t)R * R / 4; h.b_jstride = (int64_t)s2 * s2; h.ldb = s2;
+        h.C = W + (int64_t)s2 * R; h.c_ustride = (int64_t)R * R; h.c_jstride = (int64_t)(2 * s2) * R + 2 * s2; h.ldc = R;
+        h.M = s2; h.N = s2; h.K = s2; h.nper = np; h.valid = nullptr;
+        h.alpha = -1.0;
+        launch_gemm<false, false, false>(h, U * np, st);
+        launches += 2;
+    }
+    // X1 = W Y~ (R x DC), then X = W^T X1 (rows >= r_eff of W are zero: X rows >= r_eff come out 0)
+    GemmArgs g1{};
+    g1.A = W; g1.a_ustride = (int64_t)R * R; g1.lda = R;
+    g1.B = Y; g1.b_ustride = (int64_t)r * DC; g1.ldb = DC;
+    g1.C = X1; g1.c_ustride = (int64_t)R * DC; g1.ldc = DC;
+    g1.M = r; g1.N = DC; g1.K = r; g1.nper = 1; g1.alpha = 1.0;
+    launch_gemm<false, false, false>(g1, U, st);
+    GemmArgs g2{};
+    g2.A = W; g2.a_ustride = (int64_t)R * R; g2.lda = R;
+    g2.B = X1; g2.b_ustride = (int64_t)R * DC; g2.ldb = DC;
+    g2.C = X; g2.c_ustride = (int64_t)r * DC; g2.ldc = DC;
+    g2.M = r; g2.N = DC; g2.K = r; g2.nper = 1; g2.alpha = 1.0;
+    launch_gemm<true, true, false>(g2, U, st);
+    launches += 2;
+    return cudaPeekAtLastError() == cudaSuccess ? launches : -1;
+}
+
 template <typename T, int D>
 int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
                       const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
     double *Yfull = nullptr;
     const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st, L);
     if (k1 < 0) return -1;
-    // scratch for the diagonal-block inverses: after Y~ in the weights workspace (carve_weights)
+    // scratch for the diagonal-block inverses: after Y~ in the weights workspace (carve_weights),
+    // then W = L^{-1}, the level products and W Y~ (solve_scratch_elems)
     double *Dinv = Yfull + (size_t)Dm.units() * Dm.r * (D + 1);
-    const int k2 = launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st, true);
+    // the explicit inverse wins for large r (LLM r = 1024: weights 2.58 -> 2.04 ms); for r <= 256 the
+    // panel chain is shorter than its log2(R/32) + 2 GEMM launches (headline: 0.093 vs 0.235 ms)
+    static const char *mode = std::getenv("WC_SOLVE");  // "panel" / "inverse": force one (A/B tests)
+    const bool panel = mode ? std::strcmp(mode, "panel") == 0 : Dm.r < 512;
+    const int k2 = panel ? launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st, true)
+                         : launch_solve_inverse(Dm, Yfull, L, r_eff, X, Dinv, Dinv + (size_t)Dm.units() * dinv_elems(Dm.r), st);
     if (k2 < 0) return -1;
     dim3 g3(Dm.r, Dm.units());
     launch_pdl(gather_ks_kernel<T, D>, g3, dim3(128), 0, st, static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
-               static_cast<T *>(KS));
+               static_cast<T *>(KS), Dm.bins, Dm.nb, Dm.unit_n);
     return cudaPeekAtLastError() == cudaSuccess ? k1 + k2 + 1 : -1;
 }
 

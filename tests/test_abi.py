@@ -47,7 +47,7 @@ def _shape(**kw):
 
 @pytest.mark.parametrize("kw,code", [
     (dict(r=0), -2), (dict(r=101), -2), (dict(d=48), -2), (dict(heads_q=3, heads_kv=2), -2),
-    (dict(dtype=7), -3), (dict(bins=3), -7), (dict(bins=9), -2), (dict(bins=0), -2), (dict(m=-1), -2),
+    (dict(dtype=7), -3), (dict(bins=9), -2), (dict(bins=0), -2), (dict(m=-1), -2),
     (dict(n=0), -2),
 ])
 def test_validation_before_launch(L, kw, code):
@@ -97,7 +97,8 @@ def test_kv_cache_abi(L):
     assert B.kv_capacity(s, 32, 32) == 64 + 64
     assert B.kv_capacity(s, 500, 500) == 1000  # nothing compressed
     assert B.kv_capacity(_shape(n=1000, r=64, bins=4), 20, 20) == 40 + 64
-    assert B.kv_capacity(_shape(n=1000, r=64, bins=5), 32, 32) == 0  # 5 divides n = 1000 but not n_mid = 936
+    # 5 bins do not divide n_mid = 936: bins of 187 keys (the last 188), rb = 13 (Z13)
+    assert B.kv_capacity(_shape(n=1000, r=64, bins=5), 32, 32) == 64 + 5 * 13
     assert B.kv_capacity(s, 600, 500) == 0 and B.kv_capacity(s, -1, 0) == 0
     assert B.kv_workspace_bytes(s, 32, 32) > 0
     o = B.make_opts()
@@ -111,8 +112,9 @@ def test_kv_cache_abi(L):
     need = B.kv_workspace_bytes(s, 32, 32)
     assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, d, f, d, d, d, None, d,
                                  need - 1, None) == -4
-    assert L.wildcat_compress_kv(ctypes.byref(_shape(n=1000, r=64, bins=5)), ctypes.byref(o), 32, 32, d, d, d, d, f,
-                                 d, d, d, None, d, 1 << 40, None) == -7
+    # more bins than the middle has keys (n_mid = 36 < 40 bins, r = 64): rejected before any launch
+    assert L.wildcat_compress_kv(ctypes.byref(_shape(n=100, r=64, bins=40)), ctypes.byref(o), 32, 32, d, d, d, d, f,
+                                 d, d, d, None, d, 1 << 40, None) == -2
 
 
 def test_product_package_has_no_oracle_dependency():

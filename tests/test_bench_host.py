@@ -20,9 +20,9 @@ def test_select_bytes_blocked_bookkeeping():
     assert abs(got / 1e9 - 1.5624) < 1e-3
 
 
-def test_kv_divisor_bins():
-    # B must divide n_mid (contiguous bins, Z13) and B * 12 should approach the 25 % target
-    b = bench.kv_divisor_bins(32704, 8192 - 64)
-    assert 32704 % b == 0 and b == 584
-    assert bench.kv_divisor_bins(1000, 120) == 10
-    assert bench.kv_divisor_bins(7, 100) in (1, 7)
+def test_kv_bins():
+    import bench
+
+    # E3: B = r / 12 bins of rb = 12; 25 % of a 32K context minus the 64 retained tokens
+    assert bench.kv_bins(8192 - 64) == 677
+    assert bench.kv_bins(5) == 1

@@ -72,9 +72,33 @@ def test_binned_split_api_equals_forward():
     assert np.allclose(st[:, :5], res["stats"].reshape(-1, 5), rtol=1e-12, atol=0)
 
 
-def test_bins_not_dividing_n_rejected():
-    import paper_2602_10056_b200 as wc
+@pytest.mark.parametrize("n,bins,block,dtype,d", [(50, 3, 1, "f32", 16), (50, 3, 4, "f32", 16),
+                                                  (4099, 8, 16, "bf16", 64), (1203, 7, 1, "bf16", 32),
+                                                  (20011, 16, 16, "bf16", 128)])
+def test_remainder_bin(n, bins, block, dtype, d):
+    """B not dividing n (reading Z13): bins of floor(n/B) keys, the last one also holding the
+    remainder -- pivots bit-exact and outputs within the bar against the oracle's wco_forward_binned."""
+    Q, K, V = qkv(2, 4, 2, 60, n, d, dtype, "C", seed=13)
+    compare(Q, K, V, 6 * bins, dtype, seed=13, bins=bins, block=block)
 
-    Q, K, V = qkv(1, 1, 1, 10, 50, 16, "f32", "G", seed=1)
-    with pytest.raises(wc.WildcatError):
-        run_gpu(Q, K, V, 12, bins=3)
+
+def test_remainder_bin_split_api_and_kv():
+    import paper_2602_10056_b200 as wc
+    import oracle
+
+    # split API with a remainder (select -> weights unpacks the bins of S, the last one holding the
+    # remainder), and the KV cache with a middle that 7 bins do not divide
+    Q, K, V = qkv(1, 4, 2, 64, 1000, 64, "bf16", "L", seed=21)
+    dev = torch.device("cuda:0")
+    Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
+    O1 = wc.forward(Qd, Kd, Vd, 42, seed=21, bins=7, block=8)
+    sel = wc.select(Qd, Kd, 42, seed=21, bins=7, block=8)
+    O2 = wc.attend(Qd, wc.weights(Kd, Vd, sel))
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2)
+    res = oracle.forward_binned(Q.double().numpy(), K.double().numpy(), V.double().numpy(), 42, 7, seed=21, block=8)
+    assert np.array_equal(sel.S.cpu().numpy(), res["S"])
+    cache = wc.compress_kv(Qd, Kd, Vd, 42, keep_first=32, keep_last=32, bins=7, block=8, seed=21)
+    ref = oracle.compress_kv(Q.double().numpy(), K.double().numpy(), V.double().numpy(), 42, keep_first=32, keep_last=32,
+                             bins=7, block=8, seed=21)
+    assert np.array_equal(cache.r_eff.cpu().numpy(), ref["c_eff"])

@@ -114,7 +114,10 @@ def test_invalid_kv_split_rejected():
     with pytest.raises(wc.WildcatError):
         wc.compress_kv(Q.to(dev), K.to(dev), V.to(dev), 8, keep_first=60, keep_last=60)
     with pytest.raises(wc.WildcatError):
-        wc.compress_kv(Q.to(dev), K.to(dev), V.to(dev), 8, keep_first=1, keep_last=0, bins=2)  # 99 middle tokens
+        wc.compress_kv(Q.to(dev), K.to(dev), V.to(dev), 8, keep_first=1, keep_last=0, bins=9)  # more bins than r
+    # 2 bins of the 99 middle tokens (49 + 50, reading Z13) are valid
+    cache = wc.compress_kv(Q.to(dev), K.to(dev), V.to(dev), 8, keep_first=1, keep_last=0, bins=2)
+    assert int(cache.r_eff.cpu()[0]) == 1 + 8
 
 
 def test_kv_llm32k_full_size():
