@@ -150,8 +150,8 @@ def config_dict(cfg, args, world, mode, units_per_rank):
     return {"workload": cfg.name, "units": cfg.units, "units_per_gpu": units_per_rank, "n": cfg.n, "m": cfg.m,
             "d": cfg.d, "r": cfg.r, "input_dtype": cfg.dtype, "family": cfg.family,
             "parallelism": (f"units{world}" if mode == "units" else f"nshard{world}-{args.transport}"),
-            "select": ("blocked" if (args.block >= 2 and mode == "units") else "sequential"),
-            "block": args.block if mode == "units" else 1, "bins": args.bins,
+            "select": "blocked" if args.block >= 2 else "sequential",
+            "block": args.block, "bins": args.bins if mode == "units" else 1,
             "l2": f"flushed ({args.flush_mb} MB write) before each step"}
 
 
@@ -306,7 +306,7 @@ def run_reference(args, cfg):
     world = max(1, args.gpus)
     mode = args.mode or ("nshard" if cfg.name.startswith("long") else "units")
     Q, K, V = make_config(cfg)
-    block = args.block if mode == "units" else 1
+    block = args.block if mode == "units" else min(args.block, 16)
     for _ in range(args.warmup):
         cpu_oracle_sample(cfg, Q, K, V, block, args.bins)
     secs, queries = 0.0, 0
@@ -415,12 +415,14 @@ def main():
         Q, K, V, koff = make_long_shard(cfg, world, rank)
         Qd, Kd, Vd = Q.to(dev), K.to(dev), V.to(dev)
         seed = cfg.seed
-        comm = wc.NshardComm.create(transport=args.transport, capacity=cfg.r * (cfg.d + 1) + 64)
+        comm = wc.NshardComm.create(transport=args.transport,
+                                    capacity=max(cfg.r * (cfg.d + 1), 16 * (2 + cfg.d + cfg.r)) + 64)
 
         Obuf = torch.empty_like(Qd)
 
         def step():
-            return wc.forward_nshard(comm, Qd, Kd, Vd, cfg.r, cfg.n, koff, seed=seed, S=S[0], r_eff=R, out=Obuf)
+            return wc.forward_nshard(comm, Qd, Kd, Vd, cfg.r, cfg.n, koff, seed=seed, S=S[0], r_eff=R, out=Obuf,
+                                     block=min(args.block, 16))
     else:
         # PAR2: this rank's units of the batch (unit_partition), Philox ids from unit_offset = uoff
         seed = cfg.seed

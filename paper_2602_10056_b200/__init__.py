@@ -353,13 +353,14 @@ class NshardComm:
 
 
 def forward_nshard(comm: NshardComm, Q, K, V, r, n_global, n_offset, seed=0, beta=None, rq=None, clip=True,
-                   S=None, r_eff=None, out=None, stream=None, **kw):
+                   S=None, r_eff=None, out=None, stream=None, block=1, **kw):
     """Alg 4 for one (batch, kv-head) unit whose keys are sharded over the communicator's ranks.
-    K, V: this rank's [1, 1, n_local, d] shard at global offset n_offset; Q: [1, hq, m_local, d]."""
+    K, V: this rank's [1, 1, n_local, d] shard at global offset n_offset; Q: [1, hq, m_local, d].
+    block >= 2 (<= 16): blocked selection (reading Z22), one candidate exchange per block."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     shape = B.make_shape(Q, K, r)
-    opts = _opts(seed, beta, rq, clip, 1, kw)
+    opts = _opts(seed, beta, rq, clip, block, kw)
     O = torch.empty_like(Q) if out is None else out
     ws = _workspace(shape, B.WC_OP_FORWARD_NSHARD, K.device, stream)
     if out is None:

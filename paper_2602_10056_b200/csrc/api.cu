@@ -625,7 +625,8 @@ int wildcat_forward_nshard(void *comm, const wc_shape *s, int64_t n_global, int6
     if (rc) return rc;
     if (!comm || !o || !K || !V || (s->m > 0 && (!Q || !O))) return WC_EINVAL;
     if (s->batch != 1 || s->heads_kv != 1) return WC_EUNSUPPORTED;
-    if (o->block >= 2 || s->bins != 1) return WC_EUNSUPPORTED;  // blocked / binned selection is single-GPU
+    if (s->bins != 1) return WC_EUNSUPPORTED;               // binned selection is single-GPU
+    if (o->block > 16) return WC_EUNSUPPORTED;              // the n-sharded blocked plan: b <= 16
     if (s->r > WC_MAX_R) return WC_EUNSUPPORTED;                  // the solve's plan
     if (n_offset < 0 || n_global < s->n || n_offset + s->n > n_global || s->r > n_global) return WC_ESHAPE;
     if ((rc = ws_ok(ws, ws_bytes, wc_workspace_bytes(s, WC_OP_FORWARD_NSHARD)))) return rc;

@@ -23,8 +23,9 @@ def comm(request):
     c.close()
 
 
-@pytest.mark.parametrize("n,r,dtype", [(5000, 40, "bf16"), (3001, 24, "f32")])
-def test_nshard_world1_matches_oracle(comm, n, r, dtype):
+@pytest.mark.parametrize("block", [1, 16])
+@pytest.mark.parametrize("n,r,dtype", [(5000, 40, "bf16"), (3001, 24, "f32"), (20000, 100, "bf16")])
+def test_nshard_world1_matches_oracle(comm, n, r, dtype, block):
     import oracle
     import paper_2602_10056_b200 as wc
     from paper_2602_10056_b200.inputs import make_qkv
@@ -33,9 +34,9 @@ def test_nshard_world1_matches_oracle(comm, n, r, dtype):
     dev = torch.device("cuda:0")
     S = torch.empty(r, dtype=torch.int32, device=dev)
     R = torch.empty(1, dtype=torch.int32, device=dev)
-    O = wc.forward_nshard(comm, Q.to(dev), K.to(dev), V.to(dev), r, n, 0, seed=3, S=S, r_eff=R)
+    O = wc.forward_nshard(comm, Q.to(dev), K.to(dev), V.to(dev), r, n, 0, seed=3, S=S, r_eff=R, block=block)
     torch.cuda.synchronize()
-    res = oracle.forward(Q.double().numpy(), K.double().numpy(), V.double().numpy(), r, seed=3)
+    res = oracle.forward(Q.double().numpy(), K.double().numpy(), V.double().numpy(), r, seed=3, block=block)
     assert np.array_equal(S.cpu().numpy(), res["S"][0]) and int(R.cpu()[0]) == res["r_eff"][0]
     err = np.abs(O.float().cpu().numpy() - res["O"]).max() / np.abs(V.double().numpy()).max()
     assert err <= (2e-2 if dtype == "bf16" else 1e-4), err
@@ -60,7 +61,8 @@ def test_nshard_query_shard_and_rq(comm):
     assert err <= 2e-2, err
 
 
-def test_p2p_two_ranks_one_gpu(tmp_path):
+@pytest.mark.parametrize("block", [1, 16])
+def test_p2p_two_ranks_one_gpu(tmp_path, block):
     """The device-initiated transport across two processes (both on the one GPU of the test box:
     CUDA-IPC-mapped mailboxes, peer stores, system-scope flag release / acquire): the two-shard run
     selects the oracle's pivots and matches its outputs.  Shards are whole 2048-key chunks."""
@@ -77,7 +79,9 @@ def test_p2p_two_ranks_one_gpu(tmp_path):
     s.close()
     out = str(tmp_path / "p2p.npz")
     here = os.path.dirname(os.path.abspath(__file__))
-    procs = [subprocess.Popen([sys.executable, os.path.join(here, "nshard_p2p_worker.py"), str(k), "2", str(port), out])
+    env = dict(os.environ, WC_T_BLOCK=str(block))
+    procs = [subprocess.Popen([sys.executable, os.path.join(here, "nshard_p2p_worker.py"), str(k), "2", str(port), out],
+                              env=env)
              for k in range(2)]
     try:
         rcs = [p.wait(timeout=240) for p in procs]
@@ -88,7 +92,7 @@ def test_p2p_two_ranks_one_gpu(tmp_path):
     assert rcs == [0, 0], rcs
     res = np.load(out)
     Q, K, V = make_qkv(1, 2, 1, 256, 8192, 64, "bf16", "G", seed=3)
-    orc = oracle.forward(Q.double().numpy(), K.double().numpy(), V.double().numpy(), 24, seed=7)
+    orc = oracle.forward(Q.double().numpy(), K.double().numpy(), V.double().numpy(), 24, seed=7, block=block)
     assert np.array_equal(res["S"], orc["S"][0]) and int(res["r_eff"][0]) == orc["r_eff"][0]
     err = np.abs(res["O"] - orc["O"]).max() / np.abs(V.double().numpy()).max()
     assert err <= 2e-2, err
