@@ -250,9 +250,9 @@ def kv_variant(dev, flush, block, steps, with_exact=True):
     exact = lambda: Fnn.scaled_dot_product_attention(Qdec, Kd, Vd, enable_gqa=True)
     exact()
     Oe, te = timed(exact, 30)
-    C = cache.KS.shape[1]
+    C = cache.KC.shape[1]
     units = cfg.units
-    cache_bytes = units * C * (cfg.d * 2 + (cfg.d + 1) * 4) + 2 * units * cfg.d * 2
+    cache_bytes = cache.nbytes + 2 * units * cfg.d * 2  # KC, VC (bf16), WC (fp32), value range
     kv_bytes = units * cfg.n * 2 * cfg.d * 2
     dec_us = statistics.median(td) * 1e3
     res = {"workload": "llm32k", "keep_first": kf, "keep_last": kl, "r": r, "bins": bins, "r_per_bin": 12,

@@ -175,30 +175,38 @@ int wildcat_forward(const wc_shape *shape, const wc_opts *opts, const void *Q, c
  * The E3 protocol retains the first and last tokens of the context exactly and
  * compresses the rest: per unit, the first keep_first and last keep_last of the n tokens are kept,
  * and the n_mid = n - keep_first - keep_last middle tokens go through CompressKV (Alg 2,
- * P:297-313) at rank shape->r with shape->bins bins (B <= r <= n_mid; recentring, R_K and tau
- * over the middle only; R_Q from Q's m prompt rows per q-head, or opts->rq >= 0, Q then nullable;
- * Philox unit ids as wildcat_forward; opts->block as wildcat_select).  Reading Z24:
- * the cache is the union of exact and compressed entries, so WtdAttn over it adds the retained
- * tokens' exact terms to the Nystrom estimate of the middle's unnormalised sums:
+ * P:297-313) at rank shape->r with shape->bins bins (B <= r <= n_mid; the last bin takes the
+ * remainder, Z13; recentring, R_K and tau over the middle only; R_Q from Q's m prompt rows per q-head,
+ * or opts->rq >= 0, Q then nullable; Philox unit ids as wildcat_forward; opts->block as wildcat_select).
+ * Reading Z24: the cache is the union of exact and compressed entries, so WtdAttn over it
+ * adds the retained tokens' exact terms to the Nystrom estimate of the middle's unnormalised sums.
+ * The cache is compact -- per row a key, a value and a weight, keys and values in the model dtype:
  *   KC  dtype [units][C][d]    rows: first keep_first tokens | last keep_last tokens | the middle's
  *                              r_eff coreset keys (Alg 2 order) | zero rows
- *   XC  float [units][C][d+1]  matching [value | weight] rows: [v_l, 1] for retained tokens,
- *                              [V_S, w] for coreset rows, zero after
+ *   VC  dtype [units][C][d]    matching values: v_l for retained tokens, V_S (rounded to the dtype)
+ *                              for coreset rows, zero after
+ *   WC  float [units][C]       matching weights: 1 for retained tokens, w for coreset rows, 0 after
  *   c_eff int32 [units]        keep_first + keep_last + r_eff (valid rows of the cache)
  *   vmin, vmax dtype [units][d] range of ALL n values
  *   S   int32 [units][R]       global token index of each coreset row, -1 past r_eff (nullable)
  * C = wc_kv_capacity(shape, keep_first, keep_last) = keep_first + keep_last + R, with R = B*rb of
  * the middle (R = 0 when n_mid = 0; then nothing is compressed and r, bins are not checked).
- * Decode (WtdAttn, Alg 3) over the cache is wildcat_attend with shape.r = C,
- * shape.bins = 1, shape.m = new queries per q-head, KS = KC, X = XC, r_eff = c_eff; for
- * m <= 16 it runs a decode kernel that splits the cache over CTAs (fp32 scores and sums).
  * Errors: WC_ESHAPE for keep_* < 0 or n_mid < 0 and the wildcat_select shape rules applied to the
  * middle. */
 size_t wc_kv_capacity(const wc_shape *shape, int32_t keep_first, int32_t keep_last);       /* 0 if invalid */
 size_t wc_kv_workspace_bytes(const wc_shape *shape, int32_t keep_first, int32_t keep_last); /* 0 if invalid */
 int wildcat_compress_kv(const wc_shape *shape, const wc_opts *opts, int32_t keep_first, int32_t keep_last,
-                        const void *Q, const void *K, const void *V, void *KC, float *XC, int32_t *c_eff,
+                        const void *Q, const void *K, const void *V, void *KC, void *VC, float *WC, int32_t *c_eff,
                         void *vmin, void *vmax, int32_t *S, void *ws, size_t ws_bytes, void *stream);
+
+/* Decode over the compact cache: WtdAttn (Alg 3) of shape->m new queries per q-head
+ * (Q, O [batch][heads_q][m][d]) against the cache rows, with shape->r = C and shape->bins = 1
+ * (shape->n only has to be >= C).  m <= 16 runs the split-cache decode kernel (fp32 scores and sums);
+ * larger m expands the rows to [V_S, w] in the workspace and runs the prefill attend. */
+size_t wc_decode_workspace_bytes(const wc_shape *shape);  /* 0 if invalid */
+int wildcat_decode(const wc_shape *shape, const wc_opts *opts, const void *Q, const void *KC, const void *VC,
+                   const float *WC, const int32_t *c_eff, const void *vmin, const void *vmax, void *O, void *ws,
+                   size_t ws_bytes, void *stream);
 
 /* ---- Key-dimension sharding of one long sequence across GPUs.
  * One process per GPU.  Rank 0 gets a 128-byte NCCL unique id from wc_comm_unique_id and shares
@@ -254,7 +262,7 @@ int wc_timing_enable(int on);
 int wc_timing_read(float *ms, int cap);
 
 /* ABI version (major*100 + minor). */
-int wc_version(void);  /* 200: wc_opts.unit_offset, WC_TAU_ONE / WC_NO_RECENTER / WC_CHECK_FINITE */
+int wc_version(void);  /* 201: compact KV cache (KC, VC, WC) and wildcat_decode; 200: wc_opts.unit_offset, flags */
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ import torch
 from . import _binding as B
 from ._binding import NonFiniteInput, WildcatError, lib  # noqa: F401
 
-__all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "Selection", "Cache", "WildcatError",
+__all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "decode", "Selection", "Cache",
+           "KvCache", "WildcatError",
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range", "compress_kv", "kv_capacity"]
 
 
@@ -66,6 +67,25 @@ class Cache:
     heads_kv: int
     opts: B.wc_opts
     shape: B.wc_shape = None  # the selection's shape (n, r, bins)
+
+
+@dataclass
+class KvCache:
+    """Compact KV cache of compress_kv (reading Z24): per unit C rows of a key, a value (model dtype)
+    and a weight (fp32); rows [0, c_eff) valid."""
+    KC: torch.Tensor      # dtype [units, C, d]
+    VC: torch.Tensor      # dtype [units, C, d]
+    WC: torch.Tensor      # float32 [units, C]
+    vmin: torch.Tensor    # dtype [units, d]
+    vmax: torch.Tensor
+    r_eff: torch.Tensor   # int32 [units]: c_eff
+    heads_kv: int
+    opts: B.wc_opts
+    n: int = 0            # context length the cache was built from
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.KC, self.VC, self.WC))
 
 
 _ws_cache: dict = {}
@@ -147,9 +167,12 @@ def weights(K, V, sel: Selection, stream=None) -> Cache:
     return Cache(KS, X, vmin, vmax, sel.r_eff, shape.heads_kv, sel.opts, shape)
 
 
-def attend(Q, cache: Cache, beta=None, clip=None, stream=None):
+def attend(Q, cache, beta=None, clip=None, stream=None):
+    """Alg 3 WtdAttn of Q over a Cache (weights()) or a compact KvCache (compress_kv: wildcat_decode)."""
     Q = _cont(Q)
     _require_cuda(Q)
+    if isinstance(cache, KvCache):
+        return decode(Q, cache, beta=beta, clip=clip, stream=stream)
     b, hq, m, d = Q.shape
     units, r, _ = cache.KS.shape
     if cache.shape is not None:  # the selection's (n, r, bins) define the coreset layout
@@ -188,6 +211,25 @@ def forward(Q, K, V, r, seed=0, beta=None, rq=None, clip=True, out=None, S=None,
     return O
 
 
+def decode(Q, cache: KvCache, beta=None, clip=None, stream=None):
+    """WtdAttn of Q [batch, hq, m, d] (new queries) over a compact KV cache (wildcat_decode)."""
+    Q = _cont(Q)
+    _require_cuda(Q)
+    b, hq, m, d = Q.shape
+    units, C, _ = cache.KC.shape
+    shape = B.wc_shape(batch=b, heads_q=hq, heads_kv=cache.heads_kv, d=d, r=C, bins=1, dtype=B._dtype_code(Q),
+                       reserved=0, m=m, n=max(C, cache.n))
+    flags = cache.opts.flags if clip is None else ((cache.opts.flags & ~B.WC_NO_CLIP) | (0 if clip else B.WC_NO_CLIP))
+    opts = B.wc_opts(beta=cache.opts.beta if beta is None else float(beta), rq=cache.opts.rq, seed=cache.opts.seed,
+                     flags=flags, block=0, unit_offset=cache.opts.unit_offset)
+    O = torch.empty_like(Q)
+    nb = B.decode_workspace_bytes(shape)
+    ws = _workspace(shape, "decode", Q.device, stream, nbytes=nb) if nb else None
+    _on_stream(stream, O)
+    B.wildcat_decode(shape, opts, Q, cache.KC, cache.VC, cache.WC, cache.r_eff, cache.vmin, cache.vmax, O, ws, stream)
+    return O
+
+
 def kv_capacity(n, r, keep_first=0, keep_last=0, bins=1) -> int:
     """Cache rows per unit of compress_kv: keep_first + keep_last + B * min(ceil(r/B), n_mid/B)."""
     nmid = int(n) - int(keep_first) - int(keep_last)
@@ -195,13 +237,13 @@ def kv_capacity(n, r, keep_first=0, keep_last=0, bins=1) -> int:
 
 
 def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None, rq=None, block=1, S=None,
-                stream=None, **kw) -> Cache:
+                stream=None, **kw) -> KvCache:
     """KV-cache compression (E3 protocol P:667-669; reading Z24): the first keep_first and
     last keep_last tokens of every (batch, kv-head) are kept exactly, the middle goes through
     CompressKV (Alg 2) at rank r with `bins` bins.  Q holds the prompt's queries (for R_Q) or may be
-    None when rq is given.  Returns a Cache whose rows are [retained | coreset | zero] (r_eff = c_eff),
-    ready for attend(Q_new, cache) -- the decode step.  S (int32 [units][R]), if given, receives the
-    global token index of each coreset row."""
+    None when rq is given.  Returns a compact KvCache whose rows are [retained | coreset | zero]
+    (r_eff = c_eff), ready for attend(Q_new, cache) -- the decode step.  S (int32 [units][R]), if given,
+    receives the global token index of each coreset row."""
     Q, K, V = _cont(Q), _cont(K), _cont(V)
     _require_cuda(Q, K, V)
     if Q is None and rq is None:
@@ -214,16 +256,15 @@ def compress_kv(Q, K, V, r, keep_first=0, keep_last=0, bins=1, seed=0, beta=None
         raise WildcatError("compress_kv: invalid split (keep_first/keep_last/r/bins)")
     units, dev = b * hkv, K.device
     KC = torch.empty(units, C, d, dtype=K.dtype, device=dev)
-    XC = torch.empty(units, C, d + 1, dtype=torch.float32, device=dev)
+    VC = torch.empty(units, C, d, dtype=K.dtype, device=dev)
+    WC = torch.empty(units, C, dtype=torch.float32, device=dev)
     ceff = torch.empty(units, dtype=torch.int32, device=dev)
     vmin = torch.empty(units, d, dtype=K.dtype, device=dev)
     vmax = torch.empty(units, d, dtype=K.dtype, device=dev)
     ws = _workspace(shape, "kv", dev, stream, nbytes=B.kv_workspace_bytes(shape, keep_first, keep_last))
-    _on_stream(stream, KC, XC, ceff, vmin, vmax)
-    B.wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, ceff, vmin, vmax, S, ws, stream)
-    cshape = B.wc_shape(batch=b, heads_q=shape.heads_q, heads_kv=hkv, d=d, r=C, bins=1, dtype=shape.dtype,
-                        reserved=0, m=0, n=n)
-    return Cache(KC, XC, vmin, vmax, ceff, hkv, opts, cshape)
+    _on_stream(stream, KC, VC, WC, ceff, vmin, vmax)
+    B.wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, VC, WC, ceff, vmin, vmax, S, ws, stream)
+    return KvCache(KC, VC, WC, vmin, vmax, ceff, hkv, opts, n)
 
 
 class HostForward:

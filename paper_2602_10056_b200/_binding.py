@@ -81,9 +81,13 @@ def lib():
         L.wc_kv_capacity.restype = ctypes.c_size_t
         L.wc_kv_workspace_bytes.argtypes = [S, ctypes.c_int32, ctypes.c_int32]
         L.wc_kv_workspace_bytes.restype = ctypes.c_size_t
-        L.wildcat_compress_kv.argtypes = [S, O, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, P, P,
+        L.wildcat_compress_kv.argtypes = [S, O, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, P, P, P,
                                           ctypes.c_size_t, P]
         L.wildcat_compress_kv.restype = ctypes.c_int
+        L.wc_decode_workspace_bytes.argtypes = [S]
+        L.wc_decode_workspace_bytes.restype = ctypes.c_size_t
+        L.wildcat_decode.argtypes = [S, O, P, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+        L.wildcat_decode.restype = ctypes.c_int
         L.wc_timing_enable.argtypes = [ctypes.c_int]
         L.wc_timing_enable.restype = ctypes.c_int
         L.wc_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
@@ -268,23 +272,47 @@ def kv_workspace_bytes(shape, keep_first, keep_last) -> int:
     return int(lib().wc_kv_workspace_bytes(ctypes.byref(shape), int(keep_first), int(keep_last)))
 
 
-def wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, XC, c_eff, vmin, vmax, S, ws, stream=None):
+def wildcat_compress_kv(shape, opts, keep_first, keep_last, Q, K, V, KC, VC, WC, c_eff, vmin, vmax, S, ws,
+                        stream=None):
     units, _, _, d, tdt = _dims(shape)
     C = kv_capacity(shape, keep_first, keep_last)
     if C == 0:
         raise WildcatError("wildcat_compress_kv: invalid split (keep_first / keep_last / r / bins)")
     dev = _check_qkv(shape, Q, K, V, q_optional=True, need_v=True)
     _need(KC, "KC", tdt, units * C * d, dev)
-    _need(XC, "XC", torch.float32, units * C * (d + 1), dev)
+    _need(VC, "VC", tdt, units * C * d, dev)
+    _need(WC, "WC", torch.float32, units * C, dev)
     _need(c_eff, "c_eff", torch.int32, units, dev)
     _need(vmin, "vmin", tdt, units * d, dev)
     _need(vmax, "vmax", tdt, units * d, dev)
     _need(S, "S", torch.int32, units * (C - int(keep_first) - int(keep_last)), dev, optional=True)
     _check_ws(ws, dev, kv_workspace_bytes(shape, keep_first, keep_last))
     rc = lib().wildcat_compress_kv(ctypes.byref(shape), ctypes.byref(opts), int(keep_first), int(keep_last), _ptr(Q),
-                                   _ptr(K), _ptr(V), _ptr(KC), _ptr(XC), _ptr(c_eff), _ptr(vmin), _ptr(vmax),
-                                   _ptr(S), _ptr(ws), ws.numel(), _stream(stream))
+                                   _ptr(K), _ptr(V), _ptr(KC), _ptr(VC), _ptr(WC), _ptr(c_eff), _ptr(vmin),
+                                   _ptr(vmax), _ptr(S), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "wildcat_compress_kv")
+
+
+def decode_workspace_bytes(shape) -> int:
+    return int(lib().wc_decode_workspace_bytes(ctypes.byref(shape)))
+
+
+def wildcat_decode(shape, opts, Q, KC, VC, WC, c_eff, vmin, vmax, O, ws, stream=None):
+    units, _, C, d, tdt = _dims(shape)
+    nq = shape.batch * shape.heads_q * shape.m * d
+    dev = _need(KC, "KC", tdt, units * C * d)
+    _need(VC, "VC", tdt, units * C * d, dev)
+    _need(WC, "WC", torch.float32, units * C, dev)
+    _need(c_eff, "c_eff", torch.int32, units, dev)
+    _need(Q, "Q", tdt, nq, dev, exact=True, optional=nq == 0)
+    _need(O, "O", tdt, nq, dev, exact=True, optional=nq == 0)
+    _need(vmin, "vmin", tdt, units * d, dev)
+    _need(vmax, "vmax", tdt, units * d, dev)
+    _check_ws(ws, dev, decode_workspace_bytes(shape))
+    rc = lib().wildcat_decode(ctypes.byref(shape), ctypes.byref(opts), _ptr(Q), _ptr(KC), _ptr(VC), _ptr(WC),
+                              _ptr(c_eff), _ptr(vmin), _ptr(vmax), _ptr(O), _ptr(ws), 0 if ws is None else ws.numel(),
+                              _stream(stream))
+    _check(rc, "wildcat_decode")
 
 
 def last_launch_count() -> int:

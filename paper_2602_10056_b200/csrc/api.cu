@@ -546,12 +546,12 @@ size_t wc_kv_workspace_bytes(const wc_shape *s, int32_t keep_first, int32_t keep
 }
 
 int wildcat_compress_kv(const wc_shape *s, const wc_opts *o, int32_t keep_first, int32_t keep_last, const void *Q,
-                        const void *K, const void *V, void *KC, float *XC, int32_t *c_eff, void *vmin, void *vmax,
-                        int32_t *S_out, void *ws, size_t ws_bytes, void *stream) {
+                        const void *K, const void *V, void *KC, void *VC, float *WC, int32_t *c_eff, void *vmin,
+                        void *vmax, int32_t *S_out, void *ws, size_t ws_bytes, void *stream) {
     KvPlan kp;
     int rc = kv_plan(s, keep_first, keep_last, kp);
     if (rc) return rc;
-    if (!o || !K || !V || !KC || !XC || !c_eff || !vmin || !vmax) return WC_EINVAL;
+    if (!o || !K || !V || !KC || !VC || !WC || !c_eff || !vmin || !vmax) return WC_EINVAL;
     if (kp.has_mid && (rc = check_opts(o, &kp.mid))) return rc;
     const double rq = rq_of(o);
     if (kp.has_mid && rq < 0.0 && !Q && s->m > 0) return WC_EINVAL;
@@ -591,12 +591,60 @@ int wildcat_compress_kv(const wc_shape *s, const wc_opts *o, int32_t keep_first,
             return rc;
     }
     tmark(st);
-    if ((k = wc::launch_kv_assemble(Df, K, V, keep_first, keep_last, kp.R, w.KS, w.X, w.S, w.reff, KC, XC, c_eff,
+    if ((k = wc::launch_kv_assemble(Df, K, V, keep_first, keep_last, kp.R, w.KS, w.X, w.S, w.reff, KC, VC, WC, c_eff,
                                     S_out, st)) < 0)
         return WC_ECUDA;
     launches += k;
     tmark(st);
     return finish(launches);
+}
+
+// ---- decode over a compact KV cache (WtdAttn, Alg 3): shape.r = C rows, bins = 1
+static wc::Dims decode_dims(const wc_shape *s) {
+    wc::Dims D = dims_of(s);
+    D.r = s->r;
+    return D;
+}
+
+size_t wc_decode_workspace_bytes(const wc_shape *s) {
+    if (check_shape(s) != WC_OK || s->bins != 1) return 0;
+    const wc::Dims D = decode_dims(s);
+    if (D.m <= wc::kDecodeMaxM) return ((wc::attend_decode_ws_bytes(D) + 255) & ~size_t(255)) + 256;
+    const size_t x = (size_t)D.units() * D.r * (D.d + 1) * sizeof(float);
+    return ((x + 255) & ~size_t(255)) + ((wc::attend_ws_bytes(D) + 255) & ~size_t(255)) + 256;
+}
+
+int wildcat_decode(const wc_shape *s, const wc_opts *o, const void *Q, const void *KC, const void *VC, const float *WC,
+                   const int32_t *c_eff, const void *vmin, const void *vmax, void *O, void *ws, size_t ws_bytes,
+                   void *stream) {
+    int rc = check_shape(s);
+    if (rc) return rc;
+    if (s->bins != 1) return WC_ESHAPE;
+    if ((s->m > 0 && (!Q || !O)) || !KC || !VC || !WC || !c_eff || !vmin || !vmax) return WC_EINVAL;
+    if (o && (o->flags & ~WC_FLAGS_ALL)) return WC_EINVAL;
+    if ((rc = ws_ok(ws, ws_bytes, wc_decode_workspace_bytes(s)))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int clip = (o && (o->flags & WC_NO_CLIP)) ? 0 : 1;
+    int nf = 0;
+    if ((rc = check_finite(o, s->dtype, s->m > 0 ? O : nullptr, {{Q, q_elems(s)}}, st, &nf))) return rc;
+    const wc::Dims D = decode_dims(s);
+    tmark(st, true);
+    int k;
+    if (D.m <= wc::kDecodeMaxM) {
+        k = wc::launch_attend_decode_vw(D, Q, KC, VC, WC, c_eff, vmin, vmax, beta_of(s, o), clip, O, ws, st);
+    } else {  // many queries: expand the cache rows to [V_S, w] and run the general attend
+        float *X = static_cast<float *>(ws);
+        const size_t x = (size_t)D.units() * D.r * (D.d + 1) * sizeof(float);
+        void *aws = static_cast<char *>(ws) + ((x + 255) & ~size_t(255));
+        k = wc::launch_vw_to_x(D, VC, WC, X, st);
+        if (k >= 0) {
+            const int k2 = wc::launch_attend(D, Q, KC, X, c_eff, vmin, vmax, beta_of(s, o), clip, O, aws, st);
+            k = k2 < 0 ? -1 : k + k2;
+        }
+    }
+    if (k < 0) return WC_ECUDA;
+    tmark(st);
+    return finish(k + nf);
 }
 
 int wc_comm_unique_id(void *id128) {
@@ -676,6 +724,6 @@ int wc_timing_read(float *ms, int cap) {
     return k;
 }
 
-int wc_version(void) { return 200; }
+int wc_version(void) { return 201; }
 
 }  // extern "C"

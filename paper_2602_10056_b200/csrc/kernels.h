@@ -161,8 +161,14 @@ int launch_attend_decode(const Dims &D, const void *Q, const void *KS, const flo
 // D: the full-context unit dims (n = all tokens).  Smid / reff_mid / KS / X of the middle may be null
 // when R = 0.
 int launch_kv_assemble(const Dims &D, const void *K, const void *V, int kf, int kl, int R, const void *KS,
-                       const float *X, const int32_t *Smid, const int32_t *reff_mid, void *KC, float *XC,
+                       const float *X, const int32_t *Smid, const int32_t *reff_mid, void *KC, void *VC, float *WC,
                        int32_t *c_eff, int32_t *S_out, cudaStream_t st);
+// Decode over a compact KV cache (KC, VC dtype [units][C][d]; WC fp32 [units][C]): D.r = C, D.m <= kDecodeMaxM.
+int launch_attend_decode_vw(const Dims &D, const void *Q, const void *KC, const void *VC, const float *WC,
+                            const int32_t *c_eff, const void *vmin, const void *vmax, double beta, int clip, void *O,
+                            void *ws, cudaStream_t st);
+// (VC, WC) -> X fp32 rows [units * C][d + 1] (general attend over a compact cache).
+int launch_vw_to_x(const Dims &D, const void *VC, const float *WC, float *X, cudaStream_t st);
 
 // n-sharded forward (nshard.cu).  Single unit per call; NCCL resolved at run time.
 size_t ns_workspace_bytes(const Dims &D);

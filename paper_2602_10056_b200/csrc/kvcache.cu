@@ -2,8 +2,8 @@
 // CompressKV kernels, and the decode-shaped WtdAttn (Alg 3) for few queries per head.
 //
 // Reading Z24: the cache of a unit is the union of exact retained entries and the
-// CompressKV coreset of the middle tokens.  Each cache row is a key row KC[a] plus a [value | weight]
-// row XC[a]:
+// CompressKV coreset of the middle tokens.  Each cache row is a key row KC[a], a value row VC[a] (the
+// cache dtype: V_S rounded like the keys) and a weight WC[a] (fp32):
 //   rows [0, kf)            first kf tokens,  (k_l, [v_l, 1])
 //   rows [kf, kf + kl)      last kl tokens,   (k_l, [v_l, 1])
 //   rows [kf + kl, c_eff)   coreset rows of the middle, (k_s, [V_S, w]_s) in Alg 2 order
@@ -34,8 +34,8 @@ template <typename T>
 __global__ void kv_assemble_kernel(const T *__restrict__ K, const T *__restrict__ V, int64_t n, int d, int kf, int kl,
                                    int R, const T *__restrict__ KS, const float *__restrict__ X,
                                    const int32_t *__restrict__ Smid, const int32_t *__restrict__ reff_mid,
-                                   T *__restrict__ KC, float *__restrict__ XC, int32_t *__restrict__ c_eff,
-                                   int32_t *__restrict__ S_out) {
+                                   T *__restrict__ KC, T *__restrict__ VC, float *__restrict__ WC,
+                                   int32_t *__restrict__ c_eff, int32_t *__restrict__ S_out) {
     const int u = blockIdx.y, kept = kf + kl, C = kept + R, dc = d + 1;
     const int re = reff_mid ? reff_mid[u] : 0;
     const int rows_per_block = blockDim.x / 32;
@@ -43,22 +43,26 @@ __global__ void kv_assemble_kernel(const T *__restrict__ K, const T *__restrict_
     if (blockIdx.x == 0 && threadIdx.x == 0) c_eff[u] = kept + re;
     if (a >= C) return;
     T *kc = KC + ((int64_t)u * C + a) * d;
-    float *xc = XC + ((int64_t)u * C + a) * dc;
-    if (a < kept) {  // retained token (k_l, [v_l, 1])
+    T *vc = VC + ((int64_t)u * C + a) * d;
+    float *wc = WC + (int64_t)u * C + a;
+    if (a < kept) {  // retained token (k_l, v_l, 1)
         const int64_t l = a < kf ? a : n - kl + (a - kf);
         const T *k = K + ((int64_t)u * n + l) * d, *v = V + ((int64_t)u * n + l) * d;
         for (int j = lane; j < d; j += 32) {
             kc[j] = k[j];
-            xc[j] = to_f32(v[j]);
+            vc[j] = v[j];
         }
-        if (lane == 0) xc[d] = 1.f;
+        if (lane == 0) *wc = 1.f;
         return;
     }
     const int j0 = a - kept;  // coreset row j0 of the middle
     if (lane == 0 && S_out) S_out[(int64_t)u * R + j0] = j0 < re ? Smid[(int64_t)u * R + j0] + kf : -1;
     const bool ok = j0 < re;
-    for (int j = lane; j < d; j += 32) kc[j] = ok ? KS[((int64_t)u * R + j0) * d + j] : from_f32<T>(0.f);
-    for (int j = lane; j < dc; j += 32) xc[j] = ok ? X[((int64_t)u * R + j0) * dc + j] : 0.f;
+    for (int j = lane; j < d; j += 32) {
+        kc[j] = ok ? KS[((int64_t)u * R + j0) * d + j] : from_f32<T>(0.f);
+        vc[j] = from_f32<T>(ok ? X[((int64_t)u * R + j0) * dc + j] : 0.f);  // V_S rounded to the cache dtype
+    }
+    if (lane == 0) *wc = ok ? X[((int64_t)u * R + j0) * dc + d] : 0.f;
 }
 
 constexpr int kDecC = 64;   // cache rows per tile
@@ -82,14 +86,17 @@ template <int D, int QR> struct DecSmem {
 
 // One cache tile (kDecC rows of KS and X) held in registers between its global load and its
 // shared-memory store, so the next tile's loads are in flight while the current one is computed.
-template <typename T, int D> struct DecTile {
+template <typename T, int D, bool COMPACT> struct DecTile {
     static constexpr int kKTot = kDecC * D * (int)sizeof(T) / 16;       // 16-byte K vectors per tile
     static constexpr int kKVec = (kKTot + kDecT - 1) / kDecT;             // ... per thread
-    static constexpr int kXF = kDecC * (D + 1) / kDecT;                   // X floats per thread (exact)
-    static constexpr int kXRem = kDecC * (D + 1) - kXF * kDecT;
+    static constexpr int kXF = COMPACT ? 0 : kDecC * (D + 1) / kDecT;     // X floats per thread (exact)
+    static constexpr int kXRem = COMPACT ? 0 : kDecC * (D + 1) - kXF * kDecT;
     uint4 k[kKVec];
-    float x[kXF + 1];
-    __device__ __forceinline__ void load(const T *KSu, const float *Xu, int c0, int nc, int tid) {
+    float x[kXF + 1];  // fp32 [V_S, w] path
+    // [V_S, w] rows from the fp32 X rows, or (Xu == nullptr) from a compact KV cache: values VCu (dtype
+    // [C][D]) and weights WCu (fp32 [C])
+    __device__ __forceinline__ void load(const T *KSu, const float *Xu, const T *VCu, const float *WCu, int c0, int nc,
+                                         int tid) {
         const uint4 *kv = reinterpret_cast<const uint4 *>(KSu + (int64_t)c0 * D);
         constexpr int kPerRow = D * (int)sizeof(T) / 16;
 #pragma unroll
@@ -97,15 +104,31 @@ template <typename T, int D> struct DecTile {
             const int e = tid + i * kDecT;
             k[i] = (e < kKTot && e / kPerRow < nc) ? __ldg(kv + e) : make_uint4(0, 0, 0, 0);
         }
-        const float *xr = Xu + (int64_t)c0 * (D + 1);
         const int lim = nc * (D + 1);
+        if constexpr (!COMPACT) {
+            const float *xr = Xu + (int64_t)c0 * (D + 1);
 #pragma unroll
-        for (int i = 0; i < kXF; ++i) {
-            const int e = tid + i * kDecT;
-            x[i] = e < lim ? __ldg(xr + e) : 0.f;
+            for (int i = 0; i < kXF; ++i) {
+                const int e = tid + i * kDecT;
+                x[i] = e < lim ? __ldg(xr + e) : 0.f;
+            }
+            if (kXRem) x[kXF] = (tid < kXRem && kXF * kDecT + tid < lim) ? __ldg(xr + kXF * kDecT + tid) : 0.f;
+        } else {  // compact cache: 16-byte vectors of the value rows, one weight per thread
+            const uint4 *vr = reinterpret_cast<const uint4 *>(VCu + (int64_t)c0 * D);
+            constexpr int kPerRow = D * (int)sizeof(T) / 16;
+#pragma unroll
+            for (int i = 0; i < kVVec; ++i) {
+                const int e = tid + i * kDecT;
+                v[i] = (e < kVTot && e / kPerRow < nc) ? __ldg(vr + e) : make_uint4(0, 0, 0, 0);
+            }
+            w = tid < nc ? __ldg(WCu + c0 + tid) : 0.f;
         }
-        if (kXRem) x[kXF] = (tid < kXRem && kXF * kDecT + tid < lim) ? __ldg(xr + kXF * kDecT + tid) : 0.f;
     }
+    // compact cache: 16-byte value vectors and the weights of the tile (registers until the store)
+    static constexpr int kVTot = COMPACT ? kDecC * D * (int)sizeof(T) / 16 : 0;
+    static constexpr int kVVec = COMPACT ? (kVTot + kDecT - 1) / kDecT : 1;
+    uint4 v[kVVec];
+    float w;
     // K rows stay raw (bf16 pairs / fp32) in shared memory, row stride kW = D*sizeof(T)/4 + 1 words
     // (odd: the score loop's row-per-lane reads are conflict-free); 4 word stores per vector.
     static constexpr int kW = D * (int)sizeof(T) / 4 + 1;
@@ -118,9 +141,31 @@ template <typename T, int D> struct DecTile {
             uint32_t *dst = ks + row * kW + 4 * c;
             dst[0] = k[i].x; dst[1] = k[i].y; dst[2] = k[i].z; dst[3] = k[i].w;
         }
+        if constexpr (!COMPACT) {
 #pragma unroll
-        for (int i = 0; i < kXF; ++i) xs[tid + i * kDecT] = x[i];
-        if (kXRem && tid < kXRem) xs[kXF * kDecT + tid] = x[kXF];
+            for (int i = 0; i < kXF; ++i) xs[tid + i * kDecT] = x[i];
+            if (kXRem && tid < kXRem) xs[kXF * kDecT + tid] = x[kXF];
+        } else {  // [V_S, w] rows of the fp32 tile from the compact cache
+            constexpr int kEl = 16 / (int)sizeof(T), kPerRow = D / kEl;
+#pragma unroll
+            for (int i = 0; i < kVVec; ++i) {
+                const int e = tid + i * kDecT, row = e / kPerRow, c = (e % kPerRow) * kEl;
+                if (kVTot % kDecT && e >= kVTot) break;
+                const uint32_t wd[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                float *dst = xs + row * (D + 1) + c;
+                if constexpr (sizeof(T) == 2) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        dst[2 * k] = __uint_as_float(wd[k] << 16);
+                        dst[2 * k + 1] = __uint_as_float(wd[k] & 0xffff0000u);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) dst[k] = __uint_as_float(wd[k]);
+                }
+            }
+            if (tid < kDecC) xs[tid * (D + 1) + D] = w;
+        }
     }
 };
 
@@ -142,9 +187,10 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
 //           once from shared memory and P arrives as one vector load per cache row.
 // QR = 4 serves one decode token of a 4-query-head group.
 // part: [units][qz][splits][QR][D + 2] = (max, num[0..D-1], den) per CTA and row (log2 domain).
-template <typename T, int D, int QR>
+template <typename T, int D, int QR, bool COMPACT>
 __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
-    const T *__restrict__ Q, const T *__restrict__ KS, const float *__restrict__ X, const int32_t *__restrict__ r_eff,
+    const T *__restrict__ Q, const T *__restrict__ KS, const float *__restrict__ X, const T *__restrict__ VC,
+    const float *__restrict__ WC, const int32_t *__restrict__ r_eff,
     const T *__restrict__ vmin, const T *__restrict__ vmax, int64_t m, int r, int group, int hq, int hkv, float sl2,
     int clip, T *__restrict__ O, float *__restrict__ part, unsigned *__restrict__ tickets) {
     extern __shared__ float sm[];
@@ -152,7 +198,7 @@ __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
     float *qs = sm + L::kQ, *xs = sm + L::kX, *ps = sm + L::kS, *fs = sm + L::kF, *dens = sm + L::kDen;
     float *red = sm + L::kRed;
     uint32_t *ks = reinterpret_cast<uint32_t *>(sm + L::kK);
-    constexpr int KW = DecTile<T, D>::kW;
+    constexpr int KW = DecTile<T, D, COMPACT>::kW;
     constexpr int TPR = kDecT / QR, DC = D + 1, PW = D + 2, NS = kDecC / TPR;
     constexpr int WPR = TPR > 32 ? TPR / 32 : 1;  // warps per query row (score phase)
     constexpr int RS = kDecT / D;                 // row groups of the P . V_S phase
@@ -166,7 +212,9 @@ __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
     const int re = r_eff[u];
     const int ntiles = (re + kDecC - 1) / kDecC;
     const T *KSu = KS + (int64_t)u * r * D;
-    const float *Xu = X + (int64_t)u * r * DC;
+    const float *Xu = X ? X + (int64_t)u * r * DC : nullptr;
+    const T *VCu = VC ? VC + (int64_t)u * r * D : nullptr;
+    const float *WCu = WC ? WC + (int64_t)u * r : nullptr;
 
     for (int e = tid; e < QR * D; e += kDecT) {
         const int qq = e / D, j = e % D;
@@ -195,15 +243,15 @@ __global__ void __launch_bounds__(kDecT) attend_decode_kernel(
         }
         if (tid < 4) mrun_s[tid] = -INFINITY;
     }
-    DecTile<T, D> tile;
+    DecTile<T, D, COMPACT> tile;
     int tcur = split;
-    if (tcur < ntiles) tile.load(KSu, Xu, tcur * kDecC, min(kDecC, re - tcur * kDecC), tid);
+    if (tcur < ntiles) tile.load(KSu, Xu, VCu, WCu, tcur * kDecC, min(kDecC, re - tcur * kDecC), tid);
     while (tcur < ntiles) {
         const int nc = min(kDecC, re - tcur * kDecC);
         __syncthreads();  // previous tile's readers are done with ks / xs / ps / red
         tile.store(ks, xs, tid);
         const int tnext = tcur + splits;
-        if (tnext < ntiles) tile.load(KSu, Xu, tnext * kDecC, min(kDecC, re - tnext * kDecC), tid);
+        if (tnext < ntiles) tile.load(KSu, Xu, VCu, WCu, tnext * kDecC, min(kDecC, re - tnext * kDecC), tid);
         __syncthreads();
         if constexpr (kMma) {
             float c4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -425,8 +473,9 @@ int decode_splits(const Dims &D) {
 }
 
 template <typename T, int D, int QR>
-int launch_decode_tdq(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                      const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+int launch_decode_tdq(const Dims &Dm, const void *Q, const void *KS, const float *X, const void *VC, const float *WC,
+                      const int32_t *r_eff, const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws,
+                      cudaStream_t st) {
     using L = DecSmem<D, QR>;
     const int splits = decode_splits(Dm);
     const int qz = (int)(((int64_t)Dm.group() * Dm.m + QR - 1) / QR);
@@ -435,32 +484,48 @@ int launch_decode_tdq(const Dims &Dm, const void *Q, const void *KS, const float
         static_cast<char *>(ws) + (size_t)Dm.units() * qz * splits * QR * (D + 2) * sizeof(float));
     if (splits > 1 && cudaMemsetAsync(tickets, 0, (size_t)Dm.units() * qz * sizeof(unsigned), st) != cudaSuccess)
         return -1;
-    auto kern = attend_decode_kernel<T, D, QR>;
+    auto kern = VC ? attend_decode_kernel<T, D, QR, true> : attend_decode_kernel<T, D, QR, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kBytes);
     kern<<<dim3(splits, Dm.units(), qz), kDecT, L::kBytes, st>>>(
-        static_cast<const T *>(Q), static_cast<const T *>(KS), X, r_eff, static_cast<const T *>(vmin),
+        static_cast<const T *>(Q), static_cast<const T *>(KS), X, static_cast<const T *>(VC), WC, r_eff,
+        static_cast<const T *>(vmin),
         static_cast<const T *>(vmax), Dm.m, Dm.r, Dm.group(), Dm.hq, Dm.hkv, (float)(beta * 1.4426950408889634), clip,
         static_cast<T *>(O), part, tickets);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 template <typename T, int D>
-int launch_decode_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                     const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
-    if (decode_qr(Dm) == 4) return launch_decode_tdq<T, D, 4>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
-    return launch_decode_tdq<T, D, kDecQmax>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+int launch_decode_td(const Dims &Dm, const void *Q, const void *KS, const float *X, const void *VC, const float *WC,
+                     const int32_t *r_eff, const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws,
+                     cudaStream_t st) {
+    if (decode_qr(Dm) == 4)
+        return launch_decode_tdq<T, D, 4>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    return launch_decode_tdq<T, D, kDecQmax>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
 }
 
 template <typename T>
-int launch_decode_t(const Dims &Dm, const void *Q, const void *KS, const float *X, const int32_t *r_eff,
-                    const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws, cudaStream_t st) {
+int launch_decode_t(const Dims &Dm, const void *Q, const void *KS, const float *X, const void *VC, const float *WC,
+                    const int32_t *r_eff, const void *vmin, const void *vmax, double beta, int clip, void *O, void *ws,
+                    cudaStream_t st) {
     switch (Dm.d) {
-        case 16: return launch_decode_td<T, 16>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
-        case 32: return launch_decode_td<T, 32>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
-        case 64: return launch_decode_td<T, 64>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
-        case 128: return launch_decode_td<T, 128>(Dm, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        case 16: return launch_decode_td<T, 16>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        case 32: return launch_decode_td<T, 32>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        case 64: return launch_decode_td<T, 64>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
+        case 128: return launch_decode_td<T, 128>(Dm, Q, KS, X, VC, WC, r_eff, vmin, vmax, beta, clip, O, ws, st);
     }
     return -1;
+}
+
+// (VC, WC) -> X = [V_S, w] fp32 rows (the general attend over a compact KV cache, m > 16)
+template <typename T>
+__global__ void vw_to_x_kernel(const T *__restrict__ VC, const float *__restrict__ WC, int64_t rows, int d,
+                               float *__restrict__ X) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * (d + 1);
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / (d + 1);
+        const int c = (int)(e - row * (d + 1));
+        X[e] = c < d ? to_f32(VC[row * d + c]) : WC[row];
+    }
 }
 
 }  // namespace
@@ -476,24 +541,45 @@ int launch_attend_decode(const Dims &D, const void *Q, const void *KS, const flo
                          cudaStream_t st) {
     if (D.m == 0) return 0;
     if (!ws) return -1;
-    if (D.dtype == 0) return launch_decode_t<float>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
-    return launch_decode_t<__nv_bfloat16>(D, Q, KS, X, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    if (D.dtype == 0) return launch_decode_t<float>(D, Q, KS, X, nullptr, nullptr, r_eff, vmin, vmax, beta, clip, O, ws, st);
+    return launch_decode_t<__nv_bfloat16>(D, Q, KS, X, nullptr, nullptr, r_eff, vmin, vmax, beta, clip, O, ws, st);
+}
+
+int launch_attend_decode_vw(const Dims &D, const void *Q, const void *KC, const void *VC, const float *WC,
+                            const int32_t *c_eff, const void *vmin, const void *vmax, double beta, int clip, void *O,
+                            void *ws, cudaStream_t st) {
+    if (D.m == 0) return 0;
+    if (!ws) return -1;
+    if (D.dtype == 0)
+        return launch_decode_t<float>(D, Q, KC, nullptr, VC, WC, c_eff, vmin, vmax, beta, clip, O, ws, st);
+    return launch_decode_t<__nv_bfloat16>(D, Q, KC, nullptr, VC, WC, c_eff, vmin, vmax, beta, clip, O, ws, st);
+}
+
+int launch_vw_to_x(const Dims &D, const void *VC, const float *WC, float *X, cudaStream_t st) {
+    const int64_t rows = (int64_t)D.units() * D.r;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 148, ceil_div(rows * (D.d + 1), 256)));
+    if (D.dtype == 0)
+        vw_to_x_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float *>(VC), WC, rows, D.d, X);
+    else
+        vw_to_x_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(VC), WC, rows, D.d, X);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_kv_assemble(const Dims &D, const void *K, const void *V, int kf, int kl, int R, const void *KS,
-                       const float *X, const int32_t *Smid, const int32_t *reff_mid, void *KC, float *XC,
+                       const float *X, const int32_t *Smid, const int32_t *reff_mid, void *KC, void *VC, float *WC,
                        int32_t *c_eff, int32_t *S_out, cudaStream_t st) {
     const int C = kf + kl + R;
     dim3 g((unsigned)std::max(1, (C + 7) / 8), D.units());
     if (D.dtype == 0)
         kv_assemble_kernel<float><<<g, 256, 0, st>>>(static_cast<const float *>(K), static_cast<const float *>(V), D.n,
                                                      D.d, kf, kl, R, static_cast<const float *>(KS), X, Smid, reff_mid,
-                                                     static_cast<float *>(KC), XC, c_eff, S_out);
+                                                     static_cast<float *>(KC), static_cast<float *>(VC), WC, c_eff,
+                                                     S_out);
     else
         kv_assemble_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(
             static_cast<const __nv_bfloat16 *>(K), static_cast<const __nv_bfloat16 *>(V), D.n, D.d, kf, kl, R,
-            static_cast<const __nv_bfloat16 *>(KS), X, Smid, reff_mid, static_cast<__nv_bfloat16 *>(KC), XC, c_eff,
-            S_out);
+            static_cast<const __nv_bfloat16 *>(KS), X, Smid, reff_mid, static_cast<__nv_bfloat16 *>(KC),
+            static_cast<__nv_bfloat16 *>(VC), WC, c_eff, S_out);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -105,15 +105,15 @@ def test_kv_cache_abi(L):
     d = ctypes.c_void_p(0x1000)
     f = ctypes.c_void_p(0x1000)
     # invalid split -> WC_ESHAPE; null cache output -> WC_EINVAL; small workspace -> WC_EWORKSPACE
-    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 600, 500, d, d, d, d, f, d, d, d, None, d,
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 600, 500, d, d, d, d, d, f, d, d, d, None, d,
                                  1 << 40, None) == -2
-    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, None, f, d, d, d, None, d,
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, None, d, f, d, d, d, None, d,
                                  1 << 40, None) == -1
     need = B.kv_workspace_bytes(s, 32, 32)
-    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, d, f, d, d, d, None, d,
+    assert L.wildcat_compress_kv(ctypes.byref(s), ctypes.byref(o), 32, 32, d, d, d, d, d, f, d, d, d, None, d,
                                  need - 1, None) == -4
     # more bins than the middle has keys (n_mid = 36 < 40 bins, r = 64): rejected before any launch
-    assert L.wildcat_compress_kv(ctypes.byref(_shape(n=100, r=64, bins=40)), ctypes.byref(o), 32, 32, d, d, d, d, f,
+    assert L.wildcat_compress_kv(ctypes.byref(_shape(n=100, r=64, bins=40)), ctypes.byref(o), 32, 32, d, d, d, d, d, f,
                                  d, d, d, None, d, 1 << 40, None) == -2
 
 
@@ -152,7 +152,7 @@ def test_r_above_max_r_is_unsupported_on_every_path(L, block):
         assert L.wildcat_select(ctypes.byref(big), ctypes.byref(o), d, d, d, d, d, d, d, 1 << 40, None) == -7
         assert L.wildcat_weights(ctypes.byref(big), ctypes.byref(o), d, d, d, d, d, d, d, d, d, d, d, 1 << 40,
                                  None) == -7
-        assert L.wildcat_compress_kv(ctypes.byref(big), ctypes.byref(o), 32, 32, d, d, d, d, d, d, d, d, None, d,
+        assert L.wildcat_compress_kv(ctypes.byref(big), ctypes.byref(o), 32, 32, d, d, d, d, d, d, d, d, d, None, d,
                                      1 << 40, None) == -7
         assert L.wildcat_forward_nshard(d, ctypes.byref(big), 5000, 0, ctypes.byref(o), d, d, d, d, None, None, d,
                                         1 << 40, None) == -7
@@ -187,7 +187,7 @@ def test_unknown_flag_and_version(L):
     d = ctypes.c_void_p(0x1000)
     need = L.wc_workspace_bytes(ctypes.byref(s), 3)
     assert L.wildcat_forward(ctypes.byref(s), ctypes.byref(o), d, d, d, d, None, None, d, need, None) == -1
-    assert L.wc_version() == 200
+    assert L.wc_version() == 201
     assert ctypes.sizeof(B.wc_opts) == 40  # beta, rq, seed, flags, block, unit_offset
     assert L.wc_strerror(-8).decode().startswith("non-finite")
 

@@ -47,9 +47,12 @@ def _kv_case(Q, K, V, r, kf, kl, dtype, bins=1, block=1, seed=0, rq=None, Qdec=N
                              rq=-1.0 if rq is None else rq, block=block)
     assert np.array_equal(cache.r_eff.cpu().numpy(), orc["c_eff"])
     assert np.array_equal(S.cpu().numpy()[:, :R], orc["S"])
-    assert np.array_equal(_np(cache.KS), orc["KC"])           # key rows are copies
+    assert np.array_equal(_np(cache.KC), orc["KC"])           # key rows are copies
     kept = kf + kl
-    assert np.array_equal(_np(cache.X)[:, :kept], orc["XC"][:, :kept])  # [v_l, 1] rows exact
+    assert np.array_equal(_np(cache.VC)[:, :kept], orc["XC"][:, :kept, :-1])  # retained (v_l, 1) rows exact
+    assert np.array_equal(_np(cache.WC)[:, :kept], orc["XC"][:, :kept, -1])
+    # coreset rows (V_S rounded to the cache dtype, w in fp32) are checked through the decode outputs
+    # below: as an intermediate, [V_S, w] carries the conditioning of h~(K_S, K_S) (tests/test_gpu_xweights.py)
     assert np.array_equal(_np(cache.vmin), orc["vmin"]) and np.array_equal(_np(cache.vmax), orc["vmax"])
     Oo = oracle.cache_attend(_np(Qn), orc["KC"], orc["XC"], orc["c_eff"], orc["vmin"], orc["vmax"], K.shape[1],
                              clip=clip)
