@@ -82,12 +82,7 @@ struct SelectBufs {
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ceil(n/32)] residual sums of 32-key groups (blocked selection)
-    double *FT;     // [units][n][ft_ld(r)] key-major copy of F (blocked selection)
 };
-#ifdef __CUDACC__
-__host__ __device__
-#endif
-inline int ft_ld(int r) { return (r + 3) / 4 * 4; }  // row stride of FT: 32-byte aligned rows
 constexpr int kMaxCpu = 1024;
 inline int64_t f_ld(int64_t n) { return (n + 31) / 32 * 32; }  // row stride of F (row-major kernel)
 // Tile-major F of the TMA kernel: per unit [cpu][nst][r][256] doubles, nst = 256-key super-tiles per slice.

@@ -85,7 +85,6 @@ struct BlkArgs {
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ngroups] residual sums of 32-key groups
-    double *FT;     // [units][n][ft_ld(r)] key-major F: candidate columns are contiguous rows
     int32_t *S;
     int32_t *r_eff;
     double *L;
@@ -225,8 +224,9 @@ __device__ __forceinline__ void key_triangle(const double *stg, int lane, const 
 // Shared-memory carve of the kernel (the launcher sizes it with the same function).
 template <int D, int NSL> struct BSmem {
     double *ring, *Fcol, *kcB, *H0, *Fcand, *Fx, *colbuf, *cp, *c0r, *vac, *rinvA, *kb, *scr, *c0p, *spart, *sv, *sinc;
-    int *cs, *sA, *jA, *perm;
-    uint64_t *full, *empty, *colbar;
+    int *cs, *sA, *jA, *perm, *cwk;
+    long long *cfo;
+    uint64_t *full, *empty;
     size_t bytes;
     __host__ __device__ BSmem(unsigned char *base, int NS, int ldc, int cpu) {
         using PL = BPlan<NSL>;
@@ -255,10 +255,12 @@ template <int D, int NSL> struct BSmem {
         sA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
         jA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
         perm = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        cwk = reinterpret_cast<int *>(at(NSL * sizeof(int)));
+        o = (o + 7) & ~size_t(7);
+        cfo = reinterpret_cast<long long *>(at(NSL * sizeof(long long)));
         o = (o + 15) & ~size_t(15);
         full = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
         empty = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
-        colbar = reinterpret_cast<uint64_t *>(at(sizeof(uint64_t)));
         bytes = o;
     }
 };
@@ -275,13 +277,13 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     using KC = KChunk<T, TC>;
     extern __shared__ __align__(128) unsigned char smraw[];
     const int ldc = ((a.r + 15) & ~15) + 4;
-    const int ftl = ft_ld(a.r);
     BSmem<D, NSL> sm(smraw, NS, ldc, a.cpu);
     double *ring = sm.ring, *Fcol = sm.Fcol, *kcB = sm.kcB, *H0 = sm.H0, *Fcand = sm.Fcand, *Fx = sm.Fx;
     double *colbuf = sm.colbuf, *cp = sm.cp, *c0r = sm.c0r, *vac = sm.vac, *rinvA = sm.rinvA, *kb = sm.kb;
     double *scr = sm.scr, *spart = sm.spart, *sv = sm.sv, *sinc = sm.sinc;
-    int *cs = sm.cs, *sA = sm.sA, *jA = sm.jA, *perm = sm.perm;
-    uint64_t *full = sm.full, *empty = sm.empty, *colbar = sm.colbar;
+    int *cs = sm.cs, *sA = sm.sA, *jA = sm.jA, *perm = sm.perm, *cwk = sm.cwk;
+    long long *cfo = sm.cfo;
+    uint64_t *full = sm.full, *empty = sm.empty;
     __shared__ volatile int sh_stop;
     __shared__ volatile long long sh_req;  // request number << 32 | super-tile << 16 | F rows to stream
     __shared__ volatile int sh_dummy;
@@ -312,7 +314,6 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], kCW);
         }
-        mbar_init(colbar, 1);
         flag_st(&sh_stop, 0);
         flag_st64(&sh_req, 0);
         fence_mbar_init();
@@ -482,7 +483,6 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     uint32_t cbase = 0;
     double fread = 0.0, fdot = 0.0;
     long long nreq = 0;  // requests published to the producer (thread 0)
-    int ncol = 0;        // candidate-column copy rounds (parity of colbar)
     while (i < a.r) {
         double *cur = (blk & 1) ? p1 : p0;
         double *nxt = (blk & 1) ? p0 : p1;
@@ -660,31 +660,56 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             s3 = __shfl_sync(0xffffffffu, s3, L3, 16);
             psv = __shfl_sync(0xffffffffu, psv, L3, 16);
             if (l16 == 0 && jok) {
-                cs[j] = (int)(gstar * 32 + 2 * L3 + s3);
+                const int sj = (int)(gstar * 32 + 2 * L3 + s3);
+                cs[j] = sj;
                 cp[j] = psv;
                 vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, uid);
+                // where F[0, s_j] lives in the tile-major F (owner CTA, super-tile, column) and the row
+                // stride there: the column gather below reads F[q, s_j] = F[cfo + q * cwk]
+                const int64_t cc = sj / chunk, off = sj - cc * chunk, kk = off / BT;
+                cfo[j] = cc * chunk * a.r + kk * a.r * BT + (off % BT);
+                cwk[j] = (int)std::min<int64_t>(BT, chunk - kk * BT);
             }
             if (blk == 0 && j == 0) WC_BTR(11);
         }
         cw_sync();
         WC_BTR(1);
 
-        // ---- 2: candidate data: the columns F[0:i, s_j] arrive as one bulk copy each from the
-        // key-major copy FT (written by the owner thread of each key in earlier blocks), overlapped
-        // with the centred candidate keys (fp64, MMA layout) and the parts of c0[j] = <kbar, k_sj - kbar>
+        // ---- 2: candidate data: the columns F[0:i, s_j] gathered from the tile-major F (rows written
+        // by the owner CTAs in earlier blocks; 16 independent loads per thread in flight, L2 only: an
+        // L1 line read earlier may straddle into a row another CTA wrote since), the centred
+        // candidate keys (fp64, MMA layout) and the parts of c0[j] = <kbar, k_sj - kbar>
         const int i4 = (i + 3) & ~3;
-        if (tid == 0 && i > 0) {
-            const double *FTu = a.FT + (int64_t)u * a.n * ftl;
-            mbar_arrive_expect_tx(colbar, (uint32_t)(bsz * i4 * sizeof(double)));
-            for (int j = 0; j < bsz; ++j)
-                bulk_g2s(Fcol + (size_t)j * ldc, FTu + (int64_t)cs[j] * ftl, (uint32_t)(i4 * sizeof(double)), colbar);
+        constexpr int KPT = D * NSL / kCT;  // candidate-key elements per thread (slot tid % NSL)
+        const int jk = tid % NSL;           // fixed per thread
+        T kraw[KPT];                        // issued first: their latency overlaps the F gather
+#pragma unroll
+        for (int k = 0; k < KPT; ++k)
+            kraw[k] = jk < bsz ? Ku[(int64_t)cs[jk] * D + tid / NSL + k * (kCT / NSL)] : T(0.0f);
+        {
+            constexpr int kG = 16;
+            const int tot = NSL * i4;
+            for (int base = 0; base < tot; base += kG * kCT) {
+                double vals[kG];
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int idx = base + k * kCT + tid, j = idx / (i4 > 0 ? i4 : 1), q = idx - j * i4;
+                    vals[k] = (idx < tot && j < bsz && q < i) ? __ldcg(Fu + cfo[j] + (int64_t)q * cwk[j]) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int idx = base + k * kCT + tid, j = idx / (i4 > 0 ? i4 : 1), q = idx - j * i4;
+                    if (idx < tot) Fcol[(size_t)j * ldc + q] = vals[k];
+                }
+            }
         }
         {
-            const int j = tid % NSL;  // fixed per thread
             double s0 = 0.0;
-            for (int e = tid / NSL; e < D; e += kCT / NSL) {
-                const double kc = j < bsz ? __dadd_rn(to_f64(Ku[(int64_t)cs[j] * D + e]), -kb[e]) : 0.0;
-                kcB[kcb<D, NSL>(e, j)] = kc;
+#pragma unroll
+            for (int k = 0; k < KPT; ++k) {
+                const int e = tid / NSL + k * (kCT / NSL);
+                const double kc = jk < bsz ? __dadd_rn(to_f64(kraw[k]), -kb[e]) : 0.0;
+                kcB[kcb<D, NSL>(e, jk)] = kc;
                 s0 = fma(kb[e], kc, s0);
             }
             sm.c0p[tid] = s0;
@@ -720,16 +745,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 hk[q][1] += h2[1];
             }
         }
-        if (i > 0) {
-            mbar_wait(colbar, (uint32_t)(ncol & 1));
-            ++ncol;
-        }
-        // rows [i, i4) of the copies are stale, slots >= bsz unused: zero them
-        for (int idx = tid; i4 > 0 && idx < NSL * i4; idx += kCT) {
-            const int j = idx / i4, q = idx - j * i4;
-            if (j >= bsz || q >= i) Fcol[(size_t)j * ldc + q] = 0.0;
-        }
-        cw_sync();
+        cw_sync();  // the gathered columns (rows [i, i4) and slots >= bsz are zero)
         WC_BTR(2);
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
@@ -867,28 +883,12 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     const int64_t key = t0 + kw + 32 * h + lane;
                     plh[h] = key < hi ? __ldcg(cur + key) : 0.0;
                 }
-                // per key (lane, half h) after its triangle: residual, key-major FT row, L rows of an
-                // accepted pivot, and the 32-key group sum
+                // per key (lane, half h) after its triangle: residual, L rows of an accepted pivot, and
+                // the 32-key group sum
                 auto key_epilogue = [&](int h, const double (&f)[NSL], double pl) {
                     const int64_t key = t0 + kw + 32 * h + lane;
                     if (key < hi) {
                         nxt[key] = pl;
-                        double *ftr = a.FT + ((int64_t)u * a.n + key) * ftl + i;  // key-major copy of the new rows
-                        if (i & 1) {  // 16-byte stores from the first even index (FT rows are 32-byte aligned)
-                            if (na > 0) ftr[0] = f[0];
-#pragma unroll
-                            for (int aa = 1; aa < NSL - 1; aa += 2) {
-                                if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
-                                else if (aa < na) ftr[aa] = f[aa];
-                            }
-                            if (NSL - 1 < na) ftr[NSL - 1] = f[NSL - 1];
-                        } else {
-#pragma unroll
-                            for (int aa = 0; aa < NSL; aa += 2) {
-                                if (aa + 1 < na) *reinterpret_cast<double2 *>(ftr + aa) = make_double2(f[aa], f[aa + 1]);
-                                else if (aa < na) ftr[aa] = f[aa];
-                            }
-                        }
                         int xm = -1;  // acceptance index if this key is an accepted pivot (branch-free search)
 #pragma unroll
                         for (int x = 0; x < NSL; ++x) xm = (x < na && sA[x] == key) ? x : xm;
@@ -1015,8 +1015,13 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
     }
 }
 
-// Shared-memory plan of the kernel: NS ring stages (0 if r does not fit the plan).
-template <int D, int NSL> int blocked_stages(int r, int cpu) {
+// Static shared memory of the kernel the plan allows for (ptxas reports 1152 bytes on sm_100a with
+// nvcc 12.9; the launch re-checks against cudaFuncGetAttributes).
+constexpr size_t kSmemStatic = 2048;
+
+// Shared-memory plan of the kernel: NS ring stages (0 if r does not fit the plan); min_only: the
+// smallest ring the per-key staging needs.
+template <int D, int NSL> int blocked_stages(int r, int cpu, bool min_only = false) {
     using PL = BPlan<NSL>;
     const int ldc = ((r + 15) & ~15) + 4;
     const size_t stage_bytes = (size_t)kBR * PL::PITCH * sizeof(double);
@@ -1024,8 +1029,9 @@ template <int D, int NSL> int blocked_stages(int r, int cpu) {
     // the per-key triangle stages G ([32 keys][NSL + 1] per compute warp) through the idle ring
     const size_t stg = (size_t)kCW * 32 * PL::SPITCH * sizeof(double);
     const int ns_min = (int)std::max<size_t>(3, (stg + stage_bytes - 1) / stage_bytes);
-    constexpr size_t kSmemMax = 227 * 1024 - 64;  // dynamic shared memory per CTA (sm_100), minus statics
+    constexpr size_t kSmemMax = 227 * 1024 - kSmemStatic;  // shared memory per CTA (sm_100) minus statics
     if (fixed + (size_t)ns_min * (stage_bytes + 16) > kSmemMax) return 0;
+    if (min_only) return ns_min;
     return (int)std::min<size_t>(12, (kSmemMax - fixed) / (stage_bytes + 16));
 }
 
@@ -1036,20 +1042,29 @@ int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs 
     BlkArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.gsum = b.gsum;
-    a.FT = b.FT;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
     a.bins = Dm.bins; a.nb = Dm.nb; a.unit_n = Dm.unit_n;
     a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
     const int ldc = ((Dm.r + 15) & ~15) + 4;
-    const int NS = blocked_stages<D, NSL>(Dm.r, a.cpu);
+    int NS = blocked_stages<D, NSL>(Dm.r, a.cpu);
     if (NS == 0) return -2;  // r too large for this plan
     (void)sizeof(PL);
+    auto kt = rpc_select_blocked_kernel<T, D, NSL>;
+    // the plan reserves kSmemStatic bytes for the kernel's static shared memory: take any excess
+    // (toolchain-dependent) out of the ring, down to the plan's minimum
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kt) != cudaSuccess) return -1;
+    const size_t extra = fa.sharedSizeBytes > kSmemStatic ? fa.sharedSizeBytes - kSmemStatic : 0;
+    const int drop = (int)((extra + kBR * PL::PITCH * sizeof(double) + 15) / (kBR * PL::PITCH * sizeof(double) + 16));
+    if (drop > 0) {
+        if (NS - drop < blocked_stages<D, NSL>(Dm.r, a.cpu, true)) return -2;
+        NS -= drop;
+    }
     const size_t smem = BSmem<D, NSL>(nullptr, NS, ldc, a.cpu).bytes + 64;
     static const bool tracing = std::getenv("WC_SELECT_TRACE") != nullptr;
     if (tracing && cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * Dm.r) == cudaSuccess)
         cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 16 * Dm.r, st);
-    auto kt = rpc_select_blocked_kernel<T, D, NSL>;
-    cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
     if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
     if (cudaMemsetAsync(b.part, 0, sizeof(double) * 2 * kMaxCpu * a.units, st) != cudaSuccess) return -1;
     const dim3 grid(a.units * a.cpu);
