@@ -376,23 +376,30 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         while (true) {
             ce_sync();  // A: H0 of this block (or the stop command) is in shared memory
             if (sh_cmd == 0) break;
-            const int e = lane;
-            double hc[NSL];
+            // NSL = 16: the two half-warps split the rows of each column (lane = column e, rows
+            // XR * h .. XR * h + XR - 1 of it), halving the fp64 instructions per step that share the
+            // pipe with the compute warps' DMMA; the arithmetic per entry is unchanged
+            constexpr int XH = NSL == 16 ? 2 : 1, XR = NSL / XH;
+            const int e = XH == 2 ? (lane & 15) : lane, h = XH == 2 ? (lane >> 4) : 0;
+            double hc[XR];
 #pragma unroll
-            for (int x = 0; x < NSL; ++x) hc[x] = (e < bsz && x < bsz) ? H0[x * NSL + e] : 0.0;
+            for (int xx = 0; xx < XR; ++xx) {
+                const int x = XR * h + xx;
+                hc[xx] = (e < bsz && x < bsz) ? H0[x * NSL + e] : 0.0;
+            }
             const int my_cs = e < bsz ? cs[e] : -1;
             const double my_vp = e < bsz ? __dmul_rn(vac[e], cp[e]) : 0.0;  // v_e p[s_e]
             bool my_acc = false;
             int nacc = 0;
 #pragma unroll 1
             for (int j = 0; j < bsz && i + nacc < a.r; ++j) {
-                // lane j publishes its column H[:, j] through shared memory (double-buffered by step
+                // the lanes of column j publish it through shared memory (double-buffered by step
                 // parity: the previous user of this buffer finished before the last __syncwarp); H stays
                 // bitwise symmetric, so H[j][e] = H[e][j] = col[e]
                 double *col = colbuf + (j & 1) * NSL;
-                if (lane == j) {
+                if (e == j) {
 #pragma unroll
-                    for (int x = 0; x < NSL; ++x) col[x] = hc[x];
+                    for (int xx = 0; xx < XR; ++xx) col[XR * h + xx] = hc[xx];
                 }
                 __syncwarp();
                 const double hjj = col[j];
@@ -403,18 +410,19 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 if (!dup && vp < hjj) {
                     const double rinv = rsqrt_nr(hjj);
                     const double fe = hej * rinv;  // F[i+nacc, s_e] = H[j][e] / sqrt(H[j][j])
-                    if (e < NSL) Fcand[nacc * NSL + e] = (e > j && e < bsz) ? fe : 0.0;
+                    if (h == 0 && e < NSL) Fcand[nacc * NSL + e] = (e > j && e < bsz) ? fe : 0.0;
 #pragma unroll
-                    for (int x = 0; x < NSL; ++x) {
+                    for (int xx = 0; xx < XR; ++xx) {
+                        const int x = XR * h + xx;
                         const double fx = col[x] * rinv;  // H[x][j] / sqrt(H[j][j])
-                        if (e > j && x > j) hc[x] = fma(-fx, fe, hc[x]);
+                        if (e > j && x > j) hc[xx] = fma(-fx, fe, hc[xx]);
                     }
                     if (lane == 0) {
                         sA[nacc] = sj;
                         jA[nacc] = j;
                         rinvA[nacc] = rinv;
                     }
-                    my_acc |= (lane == j);
+                    my_acc |= (e == j);
                     ++nacc;
                 }
             }
