@@ -594,12 +594,15 @@ def main():
         a_bytes = heads * 2 * cfg.m * cfg.d * e + units * (R_main * cfg.d * e + 4 * R_main * (cfg.d + 1))
         a_flops = heads * 4.0 * cfg.m * R_main * cfg.d
         tp = None
-        tpf = os.path.join(ROOT, "profiles", "r1_ncu_attend_full_summary.txt")
+        ws_path = os.environ.get("WC_ATTEND") not in ("tc", "cuda") and cfg.dtype == "bf16" and cfg.d in (64, 128)
+        tpf = os.path.join(ROOT, "profiles", "r2_ncu_attend_ws_headline_summary.txt" if ws_path
+                           else "r1_ncu_attend_full_summary.txt")
         if cfg.name == "headline" and os.path.exists(tpf):
             for ln in open(tpf):
                 if ln.startswith("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"):
                     tp = float(ln.split()[1]) / 100.0
-        attend_roof = {"kernel": "attend_tc_kernel (+ attend_img_prep_kernel)", "bound": "hbm",
+        attend_roof = {"kernel": "attend_ws_kernel (+ attend_long_prep_kernel)" if ws_path
+                       else "attend_tc_kernel (+ attend_img_prep_kernel)", "bound": "hbm",
                        "achieved": a_bytes / (at_ms / 1e3) / 1e9, "peak": peaks()[0], "unit": "GB/s",
                        "frac": a_bytes / (at_ms / 1e3) / 1e9 / peaks()[0],
                        "tflops": a_flops / (at_ms / 1e3) / 1e12, "tensor_peak_tflops": 1685.2,

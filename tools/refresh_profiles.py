@@ -1,6 +1,8 @@
-"""Copy the round-end evidence of tools/jobs/final.sh from gpurun_out/ into profiles/ (summaries).
-usage: python tools/refresh_profiles.py"""
+"""Copy the evidence of an evidence job (tools/jobs/r2_evidence.sh: files gpurun_out/<prefix>*) into
+profiles/ as summaries named <tag>_*.
+usage: python tools/refresh_profiles.py [prefix (default e_)] [tag (default r2)]"""
 import csv
+import sys
 import json
 import os
 import shutil
@@ -8,6 +10,8 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
+PRE = sys.argv[1] if len(sys.argv) > 1 else "e_"
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r2"
 SCALE = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}
 
 
@@ -31,17 +35,18 @@ keys = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct", "gpu__compute_memory_throughput.avg.pct", "sm__pipe_fp64_cycles_active.avg.pct",
         "sm__pipe_tensor_cycles_active.avg.pct", "launch__registers_per_thread", "launch__grid_size",
         "sm__warps_active.avg.pct")
-h, units, d = summary(os.path.join(G, "f_select.ncu-rep"), os.path.join(P, "r1_ncu_select_final_summary.txt"), keys)
+h, units, d = summary(os.path.join(G, f"{PRE}select.ncu-rep"), os.path.join(P, f"{TAG}_ncu_select_summary.txt"), keys)
 rd, wr = float(d["dram__bytes_read.sum"]), float(d["dram__bytes_write.sum"])
 ur, uw = units[h.index("dram__bytes_read.sum")], units[h.index("dram__bytes_write.sum")]
 json.dump({"config": "headline", "kernel": "rpc_select_blocked_kernel<bf16,128> (block = 16)",
            "dram_bytes_per_launch": int(rd * SCALE[ur] + wr * SCALE[uw]),
-           "source": f"profiles/r1_ncu_select_final_summary.txt (dram__bytes_read.sum {rd} {ur} + dram__bytes_write.sum {wr} {uw})"},
+           "source": f"profiles/{TAG}_ncu_select_summary.txt (dram__bytes_read.sum {rd} {ur} + dram__bytes_write.sum {wr} {uw})"},
           open(os.path.join(P, "select_traffic_headline_b16.json"), "w"), indent=1)
 for k in ("attend", "weights"):
-    summary(os.path.join(G, f"f_{k}.ncu-rep"), os.path.join(P, f"r1_ncu_{k}_full_summary.txt"), keys)
+    if os.path.exists(os.path.join(G, f"{PRE}{k}.ncu-rep")):
+        summary(os.path.join(G, f"{PRE}{k}.ncu-rep"), os.path.join(P, f"{TAG}_ncu_{k}_summary.txt"), keys)
 
-rows = list(csv.reader(open(os.path.join(G, "f_launches.csv"))))
+rows = list(csv.reader(open(os.path.join(G, f"{PRE}launches.csv"))))
 hh, out = None, []
 for r in rows:
     if r and r[0] == "ID":
@@ -56,20 +61,21 @@ start = [i for i, (n, v) in enumerate(out) if "prologue_pass1" in n][1]
 seq = []
 for n, v in out[start:]:
     seq.append((n, v))
-    if "attend_tc_kernel" in n:
+    if "attend_tc_kernel" in n or "attend_ws_kernel" in n:
         break
 tot = sum(v for n, v in seq)
-bench = json.loads(open(os.path.join(G, "f_bench.json")).read().strip().splitlines()[-1])
+bench = json.loads(open(os.path.join(G, f"{PRE}bench.json")).read().strip().splitlines()[-1])
 st = bench["stages_ms"]
-lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv -- python bench.py --steps 2 --warmup 1",
+lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv -- python bench.py --steps 2 --warmup 1"
+         " --no-cpu-baseline --no-e2e --no-exact --no-variants",
          "# headline (n = m = 65536, d = 128, r = 256, bf16, blocked selection b = 16): one wildcat_forward, per-launch",
          "# device time; cold-cache and serialised under ncu, so compare SHARES, not absolutes"]
 lines += [f"{v:10.1f} us  {100 * v / tot:5.1f} %  {n}" for n, v in seq]
 lines.append(f"{tot:10.1f} us  total; selection share {sum(v for n, v in seq if 'select' in n) / tot:.3f} "
              f"(bench stage events: {st['select']:.3f} / {bench['ms_per_step']:.3f} = {st['select'] / bench['ms_per_step']:.3f})")
-open(os.path.join(P, "r1_launches_headline_final_summary.txt"), "w").write("\n".join(lines) + "\n")
-shutil.copy(os.path.join(G, "f_launches.csv"), os.path.join(P, "r1_launches_headline_final.csv"))
-shutil.copy(os.path.join(G, "f_trace.txt"), os.path.join(P, "r1_blocked_trace_headline_final.txt"))
-for a, b in (("f_bench.json", "r1_bench_headline_final.json"), ("f_ref.json", "r1_bench_reference_final.json")):
+open(os.path.join(P, f"{TAG}_launches_headline_summary.txt"), "w").write("\n".join(lines) + "\n")
+shutil.copy(os.path.join(G, f"{PRE}launches.csv"), os.path.join(P, f"{TAG}_launches_headline.csv"))
+shutil.copy(os.path.join(G, f"{PRE}trace.txt"), os.path.join(P, f"{TAG}_blocked_trace_headline.txt"))
+for a, b in ((f"{PRE}bench.json", f"{TAG}_bench_headline.json"), (f"{PRE}ref.json", f"{TAG}_bench_reference.json")):
     open(os.path.join(P, b), "w").write(open(os.path.join(G, a)).read().strip().splitlines()[-1] + "\n")
 print("\n".join(lines))
