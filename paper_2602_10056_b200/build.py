@@ -21,6 +21,9 @@ NVCC_FLAGS = [
 ]
 
 
+NVCC_FLAGS += os.environ.get("WC_NVCC_EXTRA", "").split()
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 

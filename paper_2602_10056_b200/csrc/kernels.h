@@ -82,7 +82,16 @@ struct SelectBufs {
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ceil(n/32)] residual sums of 32-key groups (blocked selection)
+    double *rej;    // [units][kRejStride] the rejection CTA's published block result (blocked selection)
 };
+// Blocked selection with >= kRejMinCpu CTAs per unit: the last CTA owns no keys and runs the block
+// rejection for the unit (its fp64 pipe free of the round-update DMMAs), publishing the result.
+constexpr int kRejMinCpu = 32;
+constexpr int kRejStride = 1280;
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int key_ctas(int cpu) { return cpu >= kRejMinCpu ? cpu - 1 : cpu; }
 constexpr int kMaxCpu = 1024;
 inline int64_t f_ld(int64_t n) { return (n + 31) / 32 * 32; }  // row stride of F (row-major kernel)
 // Tile-major F of the TMA kernel: per unit [cpu][nst][r][256] doubles, nst = 256-key super-tiles per slice.
@@ -93,8 +102,10 @@ inline int f_tile_nst(int64_t n, int cpu) {
 int select_ctas_per_unit(const struct Dims &D);
 inline size_t f_elems_per_unit(int64_t n, int r, int cpu) {
     const size_t rowmajor = (size_t)r * f_ld(n);
-    const int64_t chunk = ((n + cpu - 1) / cpu + 31) / 32 * 32;
-    const size_t tiles = (size_t)cpu * chunk * r;  // TMA kernel: [cpu][r x chunk]
+    const int kc = key_ctas(cpu);  // (the sequential kernel's ceil(n / cpu) slices fit as well)
+    const int64_t chunk = ((n + kc - 1) / kc + 31) / 32 * 32;
+    // TMA kernels: [cpu][r4 x chunk] (the blocked kernel stores rows in quads: r rounded up to 4)
+    const size_t tiles = (size_t)cpu * chunk * (size_t)((r + 3) & ~3);
     return rowmajor > tiles ? rowmajor : tiles;
 }
 

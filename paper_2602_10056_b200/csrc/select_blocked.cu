@@ -66,6 +66,11 @@ __device__ __forceinline__ double accept_uniform(uint64_t seed, uint32_t cand, u
     return (x * 67108864.0 + y) * (1.0 / 9007199254740992.0);
 }
 
+// -x by the sign bit (an integer op: no fp64-pipe instruction ahead of the DMMA that consumes it)
+__device__ __forceinline__ double dneg(double x) {
+    return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+
 // 1/sqrt(h) in fp64: MUFU rsqrt of the float value, then two Newton steps (2^-23 -> 2^-46 -> fp64
 // rounding); the library rsqrt(double) carries a much longer dependent chain.
 __device__ __forceinline__ double rsqrt_nr(double h) {
@@ -85,6 +90,7 @@ struct BlkArgs {
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ngroups] residual sums of 32-key groups
+    double *rej;    // [units][kRejStride]: flag (u64 epoch), na, Fx, rinvA, sA, jA, perm of the last block
     int32_t *S;
     int32_t *r_eff;
     double *L;
@@ -97,6 +103,11 @@ struct BlkArgs {
     unsigned long long *trace;  // debug (WC_SELECT_TRACE): [r][16] globaltimer stamps of CTA 0 per block
 };
 
+constexpr int kTS = 32;  // trace stamps per block
+// a.rej layout per unit (doubles): [0] flag = 1 + the block index of the result (u64 bits), [1] na,
+// then Fx [kBMax^2], rinvA, sA, jA, perm [kBMax each] (the ints as exact doubles)
+constexpr int kRjFx = 8, kRjRinv = kRjFx + 32 * 32, kRjSA = kRjRinv + 32, kRjJA = kRjSA + 32, kRjPerm = kRjJA + 32;
+static_assert(kRjPerm + 32 <= kRejStride, "rejection result layout");
 __device__ __forceinline__ unsigned long long btimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -104,26 +115,33 @@ __device__ __forceinline__ unsigned long long btimer() {
 }
 #define WC_BTR(k)                                                                                   \
     do {                                                                                            \
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + (k)] = btimer(); \
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * kTS + (k)] = btimer(); \
     } while (0)
 #define WC_BTRE(k)                                                                                  \
     do {                                                                                            \
-        if (a.trace && blockIdx.x == 0 && lane == 0 && blk < a.r) a.trace[blk * 16 + (k)] = btimer(); \
+        if (a.trace && blockIdx.x == 0 && lane == 0 && blk < a.r) a.trace[blk * kTS + (k)] = btimer(); \
     } while (0)
 
-constexpr int kBR = 4;  // F rows per ring stage (one DMMA k-step)
+constexpr int kBR = 4;  // F rows per quad = per ring stage = one DMMA k-step
+
+// F layout (per unit, quad-interleaved tile-major): the CTA slices [cpu][chunk keys], each cut into
+// super-tiles of BT keys (the last one wk <= BT wide); within a super-tile the rows come in quads
+// (rows 4Q .. 4Q + 3) stored key-major, F[q, key] at  ((q / 4) * wk + key) * 4 + q % 4.  A quad of a
+// super-tile is one contiguous run (one bulk copy per ring stage) and a candidate's column is one
+// 32-byte sector per quad (the gather reads r4 / 4 sectors instead of r scattered doubles).
+__host__ __device__ __forceinline__ int f_r4(int r) { return (r + 3) & ~3; }
 
 // Plan of the candidate-slot count NSL (16 or 32): NT 8-column MMA n-tiles of slots, MT 8-key MMA
 // row tiles per compute warp (MT * NT * 2 = 32 fp64 accumulators per thread either way), BT keys per
-// super-tile (the tile-major F width), ring row pitch BT + 4 doubles (the 4 rows of a k-step sit 8
-// banks apart, so each half-warp of an A-fragment load is conflict-free).
+// super-tile (the tile-major F width); a ring stage holds one quad [BT][4] (an A-fragment load of
+// 8 keys x 4 rows is 32 consecutive doubles: conflict-free).
 template <int NSL> struct BPlan {
     static constexpr int NT = NSL / 8;
     static constexpr int MT = 128 / NSL;
     static constexpr int KPW = 8 * MT;    // keys per compute warp per super-tile
     static constexpr int KPL = KPW / 32;  // keys per lane in the per-key triangle
     static constexpr int BT = kCW * KPW;  // keys per super-tile (512 for NSL = 16, 256 for NSL = 32)
-    static constexpr int PITCH = BT + 4;
+    static constexpr int STAGE = BT * kBR;  // doubles per ring stage
     static constexpr int SPITCH = NSL + 1;  // staging row pitch (doubles) of the per-key triangle
 };
 
@@ -178,13 +196,13 @@ template <typename T, int TC> struct KChunk {
 
 // Per-key triangle of KSN keys per lane at once (independent fp64 chains interleaved):
 //   F[i+aa, l] = (G[l, aa] - sum_{a2<aa} F[i+a2, l] F[i+a2, s_aa]) * (1 / sqrt(p_{s_aa}))
-// for the accepted slots aa < na in acceptance order; F rows written to frow[h] + aa * wk (key < hi),
-// residual downdate with the clamp (Z4) and p_s <- 0.  stg: the staged G rows [32 KSN keys][NSL + 1].
+// for the accepted slots aa < na in acceptance order, the residual downdate with the clamp (Z4) and
+// p_s <- 0.  stg: the staged G rows [32 KSN keys][NSL + 1]; F[i + aa, key] replaces G[key, aa] there
+// (read just before), for the coalesced write-out of the F rows (write_f_rows).
 template <int NSL, int KSN>
-__device__ __forceinline__ void key_triangle(const double *stg, int lane, const double *Fx, const double *rinvA,
-                                             const int *sA, int na, const int64_t (&key)[KSN], int64_t hi,
-                                             double *const (&frow)[KSN], int wk, double (&f)[KSN][NSL],
-                                             double (&pl)[KSN]) {
+__device__ __forceinline__ void key_triangle(double *stg, int lane, const double *Fx, const double *rinvA,
+                                             const int *sA, int na, const int64_t (&key)[KSN],
+                                             double (&f)[KSN][NSL], double (&pl)[KSN]) {
     constexpr int SP = NSL + 1;
 #pragma unroll
     for (int aa = 0; aa < NSL; ++aa) {
@@ -213,7 +231,7 @@ __device__ __forceinline__ void key_triangle(const double *stg, int lane, const 
             for (int h = 0; h < KSN; ++h) {
                 const double fv = (c0v[h] + c1v[h]) * ra;
                 f[h][aa] = fv;
-                if (key[h] < hi) frow[h][(int64_t)aa * wk] = fv;
+                stg[(32 * h + lane) * SP + aa] = fv;
                 const double qd = __dadd_rn(pl[h], -__dmul_rn(fv, fv));
                 pl[h] = (qd > 0.0 && key[h] != sa) ? qd : 0.0;
             }
@@ -221,11 +239,40 @@ __device__ __forceinline__ void key_triangle(const double *stg, int lane, const 
     }
 }
 
+// Staging row of the warp-local key j (0 .. 63): within each 32-key half, key 8 m + g sits in row 4 g + m,
+// i.e. lane L of the per-key triangle owns key 8 (L & 3) + (L >> 2) of the half.  With the row pitch
+// NSL + 1 the triangle's column reads (row = lane) and the write-out's reads (8 keys x 4 rows) are both
+// conflict-free.
+__device__ __forceinline__ int srow_of(int j) { return (j & ~31) + 4 * (j & 7) + ((j >> 3) & 3); }
+__device__ __forceinline__ int key_of_lane(int lane) { return 8 * (lane & 3) + (lane >> 2); }
+
+// Write-out of the new F rows i .. i + na - 1 of 8 KR consecutive warp-local keys (staging rows
+// srow_of(j) hold F[i + aa, key j] at [row][aa]), plus zeros from row i + na to the end of its quad (so
+// every row of a streamed quad is finite: the F-prefix DMMAs multiply rows >= i by zero B values without a
+// predicate).  Per (row tile, quad) one warp store of 8 keys x 4 rows = 32 consecutive doubles of the
+// quad layout; rows < i of a partial first quad are left alone.  koff: local key -> super-tile offset.
+template <int NSL, typename KOff>
+__device__ __forceinline__ void write_f_rows(const double *stg, int lane, int KR, KOff koff, int64_t t0, int64_t hi,
+                                             double *Fk, int wk, int i, int na) {
+    constexpr int SP = NSL + 1;
+    const int q0 = i >> 2, q1 = (i + na + 3) >> 2;
+    const int t = lane & 3;
+    for (int q = q0; q < q1; ++q) {
+        const int row = 4 * q + t, aa = row - i;
+        for (int rt = 0; rt < KR; ++rt) {
+            const int jl = rt * 8 + (lane >> 2);
+            const int64_t off = koff(jl);
+            if (row >= i && t0 + off < hi)
+                Fk[(int64_t)q * wk * kBR + off * kBR + t] = aa < na ? stg[srow_of(jl) * SP + aa] : 0.0;
+        }
+    }
+}
+
 // Shared-memory carve of the kernel (the launcher sizes it with the same function).
 template <int D, int NSL> struct BSmem {
-    double *ring, *Fcol, *kcB, *H0, *Fcand, *Fx, *colbuf, *cp, *c0r, *vac, *rinvA, *kb, *scr, *c0p, *spart, *sv, *sinc;
-    int *cs, *sA, *jA, *perm, *cwk;
-    long long *cfo;
+    double *ring, *Fcol, *kcB, *H0, *Fcand, *Fx, *colbuf, *cp, *c0r, *vac, *unif, *rinvA, *kb, *scr, *c0p, *spart, *cpre,
+        *sv, *sinc, *rts;
+    int *cs, *sA, *jA, *perm;
     uint64_t *full, *empty;
     size_t bytes;
     __host__ __device__ BSmem(unsigned char *base, int NS, int ldc, int cpu) {
@@ -234,7 +281,7 @@ template <int D, int NSL> struct BSmem {
         // (base == nullptr: only the size is wanted)
         auto at = [&](size_t bytes) { unsigned char *q = base ? base + o : nullptr; o += bytes; return q; };
         auto td = [&](size_t cnt) { return reinterpret_cast<double *>(at(cnt * sizeof(double))); };
-        ring = td((size_t)NS * kBR * PL::PITCH);
+        ring = td((size_t)NS * PL::STAGE);
         Fcol = td((size_t)NSL * ldc);
         kcB = td((size_t)D * NSL);
         H0 = td(NSL * NSL);
@@ -244,20 +291,20 @@ template <int D, int NSL> struct BSmem {
         cp = td(NSL);
         c0r = td(NSL);
         vac = td(NSL);
+        unif = td(NSL);
         rinvA = td(NSL);
-        kb = td(D);
+        kb = td(D + D / 8);
         scr = td(40);
         c0p = td(kCT);
         spart = td(cpu);
+        cpre = td(cpu);
+        rts = td(PL::BT / 8);
         sv = td(32);
         sinc = td(32);
         cs = reinterpret_cast<int *>(at(NSL * sizeof(int)));
         sA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
         jA = reinterpret_cast<int *>(at(NSL * sizeof(int)));
         perm = reinterpret_cast<int *>(at(NSL * sizeof(int)));
-        cwk = reinterpret_cast<int *>(at(NSL * sizeof(int)));
-        o = (o + 7) & ~size_t(7);
-        cfo = reinterpret_cast<long long *>(at(NSL * sizeof(long long)));
         o = (o + 15) & ~size_t(15);
         full = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
         empty = reinterpret_cast<uint64_t *>(at(NS * sizeof(uint64_t)));
@@ -269,7 +316,7 @@ template <typename T, int D, int NSL>
 __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
     pdl_wait();  // the prologue's stats / nrm2 (programmatic dependent launch)
     using PL = BPlan<NSL>;
-    constexpr int NT = PL::NT, MT = PL::MT, KPW = PL::KPW, KPL = PL::KPL, BT = PL::BT, PITCH = PL::PITCH;
+    constexpr int NT = PL::NT, MT = PL::MT, KPW = PL::KPW, KPL = PL::KPL, BT = PL::BT, STAGE = PL::STAGE;
     static_assert(MT == 4 * KPL, "row tiles 4h .. 4h + 3 hold the keys 32h .. 32h + 31 of a warp");
     constexpr int SP = PL::SPITCH;
     constexpr int DQ = D / 4;             // dims per lane per key in the kernel-dot MMA
@@ -280,13 +327,12 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     BSmem<D, NSL> sm(smraw, NS, ldc, a.cpu);
     double *ring = sm.ring, *Fcol = sm.Fcol, *kcB = sm.kcB, *H0 = sm.H0, *Fcand = sm.Fcand, *Fx = sm.Fx;
     double *colbuf = sm.colbuf, *cp = sm.cp, *c0r = sm.c0r, *vac = sm.vac, *rinvA = sm.rinvA, *kb = sm.kb;
-    double *scr = sm.scr, *spart = sm.spart, *sv = sm.sv, *sinc = sm.sinc;
-    int *cs = sm.cs, *sA = sm.sA, *jA = sm.jA, *perm = sm.perm, *cwk = sm.cwk;
-    long long *cfo = sm.cfo;
+    double *rts = sm.rts;  // per row tile residual sums of the current super-tile
+    double *scr = sm.scr, *spart = sm.spart, *cpre = sm.cpre, *sv = sm.sv, *sinc = sm.sinc, *unif = sm.unif;
+    int *cs = sm.cs, *sA = sm.sA, *jA = sm.jA, *perm = sm.perm;
     uint64_t *full = sm.full, *empty = sm.empty;
     __shared__ volatile int sh_stop;
     __shared__ volatile long long sh_req;  // request number << 32 | super-tile << 16 | F rows to stream
-    __shared__ volatile int sh_dummy;
     __shared__ int sh_na, sh_cmd;
 
     const int tid = threadIdx.x, lane = tid & 31, w = warp_index();
@@ -294,19 +340,25 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     const int u = blockIdx.x / a.cpu, c = blockIdx.x % a.cpu;
     const SubUnit sub = sub_unit(u, a.n, a.bins, a.nb, a.unit_n);
     const int64_t n = sub.count;  // this sub-unit's keys (a.n: the buffer stride)
-    const int64_t chunk = ((ceil_div(n, a.cpu) + 31) / 32) * 32;
-    const int64_t chunk_max = ((ceil_div(a.n, a.cpu) + 31) / 32) * 32;
+    // with >= kRejMinCpu CTAs the last CTA of the unit (is_R) owns no keys: it runs the block
+    // rejection and publishes the result to a.rej; the other CTAs' idle rejection warp relays it
+    const bool rej_cta = a.cpu >= kRejMinCpu;
+    const bool is_R = rej_cta && c == a.cpu - 1;
+    const int kcta = key_ctas(a.cpu);
+    const int64_t chunk = ((ceil_div(n, kcta) + 31) / 32) * 32;
+    const int64_t chunk_max = ((ceil_div(a.n, kcta) + 31) / 32) * 32;
     const int64_t lo = std::min<int64_t>(n, (int64_t)c * chunk), hi = std::min<int64_t>(n, lo + chunk);
     const int nst = (int)ceil_div(hi - lo, BT);
     const int bsz = a.b;
     const uint64_t uid = a.unit0 + (uint64_t)u;
     // the per-key triangle stages both of a lane's keys at once when the ring holds [64][SP] per warp
-    const bool two_keys = (size_t)NS * kBR * PITCH >= (size_t)kCW * 64 * SP;
+    const bool two_keys = (size_t)NS * STAGE >= (size_t)kCW * 64 * SP;
 
     const T *Ku = static_cast<const T *>(a.K) + sub.base * D;
     double *st = a.stats + (int64_t)u * (kStatsHead + D);
-    double *Fu = a.F + (int64_t)u * a.cpu * chunk_max * a.r;
-    double *Fc = Fu + (int64_t)c * chunk * a.r;
+    const int r4 = f_r4(a.r);
+    double *Fu = a.F + (int64_t)u * a.cpu * chunk_max * r4;
+    double *Fc = Fu + (int64_t)c * chunk * r4;
     auto tile_w = [&](int k) -> int { return (int)std::min<int64_t>(BT, chunk - (int64_t)k * BT); };
 
     if (tid == 0) {
@@ -336,21 +388,20 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 seen = req >> 32;
                 const int rows = (int)(req & 0xffffLL), k = (int)((req >> 16) & 0xffffLL);
                 {
-                    const double *blkp = Fc + (int64_t)k * a.r * BT;
+                    const double *blkp = Fc + (int64_t)k * r4 * BT;
                     const int wk = tile_w(k);
-                    const uint32_t rb = (uint32_t)(wk * sizeof(double));
+                    const uint32_t qb = (uint32_t)(wk * kBR * sizeof(double));  // one quad of the super-tile
                     for (int j0 = 0; j0 < rows; j0 += kBR) {
-                        const int nr = min(kBR, rows - j0);
                         while (!mbar_try_wait(&empty[stage], ph ^ 1u)) {
                             if (flag_ld(&sh_stop)) goto drain;
                             __nanosleep(128);  // ring full: do not steal issue slots from the compute warp of this SMSP
                         }
-                        mbar_arrive_expect_tx(&full[stage], rb * (uint32_t)nr);
-                        double *dst = ring + (size_t)stage * kBR * PITCH;
+                        mbar_arrive_expect_tx(&full[stage], qb);
+                        double *dst = ring + (size_t)stage * STAGE;
                         // F streams through L2 evict-first so that K, p and the group sums stay resident (keeping
-                        // the first F rows evict-last instead was measured slower: the 126 MB L2 thrashes)
-                        for (int rr = 0; rr < nr; ++rr)
-                            bulk_g2s_hint(dst + rr * PITCH, blkp + (int64_t)(j0 + rr) * wk, rb, &full[stage], pol);
+                        // the first F rows evict-last instead was measured slower: the 126 MB L2 thrashes); rows
+                        // >= i of the last quad are streamed too and ignored by the consumer
+                        bulk_g2s_hint(dst, blkp + (int64_t)j0 * wk, qb, &full[stage], pol);
                         issued |= 1u << stage;
                         par = (par & ~(1u << stage)) | (ph << stage);
                         if (++stage == NS) { stage = 0; ph ^= 1u; }
@@ -365,6 +416,49 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     }
 
     if (w > kWP && w < kWE) return;  // spare warps (register-allocation granularity)
+    if (w == kWE && rej_cta && !is_R) {
+        // ============ relay warp (a key-owning CTA of a unit with a rejection CTA): per block, wait for
+        // the rejection CTA's published result, copy it into shared memory, write the L rows / S of the
+        // accepted pivots this CTA owns; the compute warps pick it up at ce_sync B ============
+        const double *rj = a.rej + (int64_t)u * kRejStride;
+        int i = 0, blk = 0;
+        while (true) {
+            ce_sync();  // A: the candidates and their F columns are in shared memory (or the stop command)
+            if (sh_cmd == 0) break;
+            if (lane == 0) {
+                while (true) {
+                    unsigned long long f;
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(rj) : "memory");
+                    if (f >= (unsigned long long)(blk + 1)) break;
+                    __nanosleep(256);
+                }
+            }
+            __syncwarp();
+            const int nacc = (int)__ldcg(rj + 1);
+            for (int idx = lane; idx < NSL * NSL; idx += 32) Fx[idx] = __ldcg(rj + kRjFx + idx);
+            if (lane < NSL) {
+                rinvA[lane] = __ldcg(rj + kRjRinv + lane);
+                sA[lane] = (int)__ldcg(rj + kRjSA + lane);
+                jA[lane] = (int)__ldcg(rj + kRjJA + lane);
+                perm[lane] = (int)__ldcg(rj + kRjPerm + lane);
+            }
+            __syncwarp();
+            for (int x = 0; x < nacc; ++x) {
+                const int s = sA[x];
+                if (s >= lo && s < hi) {
+                    const int sl = jA[x];
+                    for (int q = lane; q < i; q += 32) a.L[((int64_t)u * a.r + i + x) * a.r + q] = Fcol[(size_t)sl * ldc + q];
+                    if (lane == 0) a.S[(int64_t)u * a.r + i + x] = s;
+                }
+            }
+            if (lane == 0) sh_na = nacc;
+            WC_BTRE(14);
+            i += nacc;
+            ++blk;
+            ce_sync();  // B
+        }
+        return;
+    }
     if (w == kWE) {
         // ============ rejection warp: per block, the sequential accept / eliminate loop of step 3 ============
         // (lane e = column e of the symmetric H in registers; column j is published through shared
@@ -447,6 +541,22 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 }
             }
             if (lane == 0) sh_na = nacc;
+            if (is_R) {  // publish the block's result for the relay warps of the other CTAs
+                __syncwarp();
+                double *rj = a.rej + (int64_t)u * kRejStride;
+                for (int idx = lane; idx < NSL * NSL; idx += 32) rj[kRjFx + idx] = Fx[idx];
+                if (lane < NSL) {
+                    rj[kRjRinv + lane] = rinvA[lane];
+                    rj[kRjSA + lane] = (double)sA[lane];
+                    rj[kRjJA + lane] = (double)jA[lane];
+                    rj[kRjPerm + lane] = (double)perm[lane];
+                }
+                if (lane == 0) rj[1] = (double)nacc;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(rj), "l"((unsigned long long)(blk + 1)) : "memory");
+            }
             WC_BTRE(14);
             i += nacc;
             ++blk;
@@ -460,7 +570,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
     double *p0 = a.p + (int64_t)u * a.n;
     double *p1 = a.p + ((int64_t)a.units + u) * a.n;
     double *partu = a.part + (int64_t)u * 2 * kMaxCpu;
-    for (int j = tid; j < D; j += kCT) kb[j] = st[kStatsHead + j];
+    for (int j = tid; j < D; j += kCT) kb[j + j / 8] = st[kStatsHead + j];  // padded (bank-conflict free reads)
 
     // p <- kernel diagonal h~(k_l, k_l) (Alg 1); 32-key group sums (one warp per group)
     double loc = 0.0;
@@ -480,9 +590,34 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         }
     }
     loc = cw_sum(loc, scr);
+    // Grid-group barrier of the compute threads (as cw_group_barrier); while thread 0 waits for the
+    // other CTAs, warps 1-2 draw the Philox pivot and accept uniforms of the next block's candidates
+    // (they depend only on the candidate counter).
+    auto block_barrier = [&](unsigned ep, uint32_t cb) {
+        cw_sync();
+        if (tid == 0) {
+            if (a.cpu > 1) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.bar + u), "r"(1u) : "memory");
+                const unsigned target = ep * (unsigned)a.cpu;
+                unsigned v;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar + u) : "memory");
+                    if (v >= target) break;
+                    __nanosleep(20);
+                }
+            } else {
+                __threadfence();
+            }
+        } else if (tid >= 32 && tid < 32 + 2 * NSL) {
+            const int jj = (tid - 32) % NSL;
+            if (tid - 32 < NSL) unif[jj] = pivot_uniform(a.seed, cb + (uint32_t)jj, uid);
+            else vac[jj] = accept_uniform(a.seed, cb + (uint32_t)jj, uid);
+        }
+        cw_sync();
+    };
     if (tid == 0) partu[c] = loc;
     unsigned epoch = 1;
-    cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_dummy, 0);
+    block_barrier(epoch++, 0u);
 
     int rstage = 0;
     uint32_t rph = 0;
@@ -497,7 +632,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         const double *pc = partu + (blk & 1) * kMaxCpu;
         double *pn = partu + ((blk + 1) & 1) * kMaxCpu;
         WC_BTR(0);
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + 12] = clock64();
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * kTS + 12] = clock64();
 
         // ---- 1a (warp 0): per-CTA residual sums -> shared memory (one L2 read per CTA), lane
         // partition sums and their inclusive prefix, total T (fixed order)
@@ -519,6 +654,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                         v += xs[q];
                     }
                 }
+                WC_BTR(20);
             } else {
                 for (int cc = b0; cc < b1; ++cc) {
                     const double x = __ldcg(pc + cc);
@@ -534,6 +670,13 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             }
             sv[lane] = v;
             sinc[lane] = incl;
+            // inclusive prefix of the CTA sums in this order: the level-1 search of every candidate
+            double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) ex = 0.0;
+            for (int cc = b0; cc < b1; ++cc) {
+                ex += spart[cc];
+                cpre[cc] = ex;
+            }
         }
         cw_sync();
         const double Ttot = sinc[31];
@@ -558,39 +701,23 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             const bool jok = j < bsz;
             const int per16 = (a.cpu + 15) / 16;
             const int b0 = l16 * per16, b1 = min(a.cpu, b0 + per16);
-            double v = 0.0;
-            for (int cc = b0; cc < b1; ++cc) v += spart[cc];
-            double incl = v;
-#pragma unroll
-            for (int o = 1; o < 16; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, incl, o, 16);
-                if (l16 >= o) incl += y;
+            const double Tw = cpre[a.cpu - 1];  // the total in the prefix's order
+            const double t = jok ? unif[j] * Tw : 0.0;
+            // level 1: the first CTA whose inclusive prefix exceeds t (strict '>'), else the last CTA with a
+            // positive sum; tp = t - the exclusive prefix of that CTA
+            int fh = -1, lp = -1;
+#pragma unroll 4
+            for (int cc = b0; cc < b1; ++cc) {
+                const double pv = cpre[cc], sp = spart[cc];
+                if (fh < 0 && pv > t) fh = cc;
+                if (sp > 0.0) lp = cc;
             }
-            const double Tw = __shfl_sync(0xffffffffu, incl, 15, 16);  // the total in this order
-            const double t = jok ? pivot_uniform(a.seed, cbase + (uint32_t)j, uid) * Tw : 0.0;
-            // level 1: CTA
-            const unsigned hit = (__ballot_sync(0xffffffffu, b1 > b0 && incl > t) & hm) >> (16 * h16);
-            const unsigned pos = (__ballot_sync(0xffffffffu, b1 > b0 && v > 0.0) & hm) >> (16 * h16);
+            const unsigned hit = (__ballot_sync(0xffffffffu, fh >= 0) & hm) >> (16 * h16);
+            const unsigned pos = (__ballot_sync(0xffffffffu, lp >= 0) & hm) >> (16 * h16);
             const int Ln = hit ? __ffs(hit) - 1 : 31 - __clz(pos);
-            int cstar = 0;
-            double tp = 0.0;
-            if (l16 == Ln) {
-                double acc = incl - v;
-                int csel = -1, last = -1;
-                double excl = 0.0, last_excl = 0.0;
-                for (int cc = b0; cc < b1; ++cc) {
-                    const double pvv = spart[cc];
-                    if (pvv > 0.0) { last = cc; last_excl = acc; }
-                    const double nacc = acc + pvv;
-                    if (csel < 0 && hit && nacc > t) { csel = cc; excl = acc; }
-                    acc = nacc;
-                }
-                if (csel < 0) { csel = last; excl = last_excl; }
-                cstar = csel;
-                tp = t - excl;
-            }
-            cstar = __shfl_sync(0xffffffffu, cstar, Ln, 16);
-            tp = __shfl_sync(0xffffffffu, tp, Ln, 16);
+            const int cstar = __shfl_sync(0xffffffffu, hit ? fh : lp, Ln, 16);
+            const double tp = t - (cstar > 0 ? cpre[cstar - 1] : 0.0);
+            if (pass == 0) WC_BTR(16);
             // level 2: 32-key group inside c*'s slice
             const int64_t slo = std::min<int64_t>(n, (int64_t)cstar * chunk);
             const int64_t shi = std::min<int64_t>(n, slo + chunk);
@@ -623,18 +750,18 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 double acc = inc2 - v2;
                 int gsel = -1, last = -1;
                 double excl = 0.0, last_excl = 0.0;
-                for (int q = q0; q < q1; ++q) {
-                    double gg = 0.0;
-                    if (gper <= kG) {
-#pragma unroll
-                        for (int z = 0; z < kG; ++z) gg = (z == q - q0) ? gv[z] : gg;
-                    } else {
-                        gg = __ldcg(gcur + q);
-                    }
+                auto scan = [&](int q, double gg) {
                     if (gg > 0.0) { last = q; last_excl = acc; }
                     const double nacc = acc + gg;
                     if (gsel < 0 && hit2 && nacc > tp) { gsel = q; excl = acc; }
                     acc = nacc;
+                };
+                if (gper <= kG) {  // static register indices (no local-memory copy of gv)
+#pragma unroll
+                    for (int z = 0; z < kG; ++z)
+                        if (z < q1 - q0) scan(q0 + z, gv[z]);
+                } else {
+                    for (int q = q0; q < q1; ++q) scan(q, __ldcg(gcur + q));
                 }
                 if (gsel < 0) { gsel = last; excl = last_excl; }
                 gstar = gsel;
@@ -642,6 +769,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             }
             gstar = __shfl_sync(0xffffffffu, gstar, L2, 16);
             tq2 = __shfl_sync(0xffffffffu, tq2, L2, 16);
+            if (pass == 0) WC_BTR(17);
             // level 3: key inside the group, two keys per lane (in key order)
             const int64_t k0 = (int64_t)gstar * 32 + 2 * l16;
             const double pa = k0 < shi ? __ldcg(cur + k0) : 0.0;
@@ -667,73 +795,95 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             }
             s3 = __shfl_sync(0xffffffffu, s3, L3, 16);
             psv = __shfl_sync(0xffffffffu, psv, L3, 16);
+            const int sj = (int)(gstar * 32 + 2 * L3 + s3);
+            if (pass == 0) WC_BTR(18);
             if (l16 == 0 && jok) {
-                const int sj = (int)(gstar * 32 + 2 * L3 + s3);
                 cs[j] = sj;
                 cp[j] = psv;
-                vac[j] = accept_uniform(a.seed, cbase + (uint32_t)j, uid);
-                // where F[0, s_j] lives in the tile-major F (owner CTA, super-tile, column) and the row
-                // stride there: the column gather below reads F[q, s_j] = F[cfo + q * cwk]
-                const int64_t cc = sj / chunk, off = sj - cc * chunk, kk = off / BT;
-                cfo[j] = cc * chunk * a.r + kk * a.r * BT + (off % BT);
-                cwk[j] = (int)std::min<int64_t>(BT, chunk - kk * BT);
             }
+            // ---- 2 (the same half-warp, right after its draw): the candidate's column F[0:i, s_j], one
+            // 32-byte quad sector per 4 rows of the owner's tile-major F (written by the owner CTAs in
+            // earlier blocks; L2 only: an L1 line read earlier may straddle into a row another CTA wrote
+            // since), and its centred key (fp64, MMA layout) with c0[j] = <kbar, k_sj - kbar>.  Slots
+            // j >= b and the rows [i, i4) are zero.
+            {
+                double *fdst = Fcol + (size_t)j * ldc;
+                const int nq = (i + 3) >> 2;
+                constexpr int EPC = 16 / (int)sizeof(T);  // key elements per 16-byte chunk
+                constexpr int KCH = D / EPC;              // 16-byte chunks per key row
+                constexpr int KCL = (KCH + 15) / 16;      // chunks per lane
+                uint4 kr[KCL];
+                const double *fsrc = Fu;
+                int wkj = 0;
+                if (jok) {
+                    const int64_t cc = sj / chunk, off = sj - cc * chunk, kk = off / BT;
+                    wkj = (int)std::min<int64_t>(BT, chunk - kk * BT);
+                    fsrc = Fu + cc * chunk * r4 + kk * r4 * BT + (off - kk * BT) * kBR;
+#pragma unroll
+                    for (int z = 0; z < KCL; ++z) {
+                        const int ch = l16 + 16 * z;
+                        if (ch < KCH) kr[z] = __ldg(reinterpret_cast<const uint4 *>(Ku + (int64_t)sj * D) + ch);
+                    }
+                }
+                constexpr int kQ = 4;  // quads per lane in flight per pass (64 rows per half-warp pass)
+                for (int qb = 0; qb < nq; qb += 16 * kQ) {
+                    double2 v[kQ][2];
+#pragma unroll
+                    for (int z = 0; z < kQ; ++z) {
+                        const int Q = qb + 16 * z + l16;
+                        if (jok && Q < nq) {
+                            const double2 *src = reinterpret_cast<const double2 *>(fsrc + (int64_t)Q * wkj * kBR);
+                            v[z][0] = __ldcg(src);
+                            v[z][1] = __ldcg(src + 1);
+                        } else {
+                            v[z][0] = v[z][1] = make_double2(0.0, 0.0);
+                        }
+                    }
+#pragma unroll
+                    for (int z = 0; z < kQ; ++z) {
+                        const int Q = qb + 16 * z + l16;
+                        if (Q < nq) {
+                            const int q = 4 * Q;
+                            fdst[q] = v[z][0].x;
+                            fdst[q + 1] = q + 1 < i ? v[z][0].y : 0.0;
+                            fdst[q + 2] = q + 2 < i ? v[z][1].x : 0.0;
+                            fdst[q + 3] = q + 3 < i ? v[z][1].y : 0.0;
+                        }
+                    }
+                }
+                double s0 = 0.0;
+#pragma unroll
+                for (int z = 0; z < KCL; ++z) {
+                    const int ch = l16 + 16 * z;
+                    if (ch < KCH) {
+                        const T *ke = reinterpret_cast<const T *>(&kr[z]);
+#pragma unroll
+                        for (int t = 0; t < EPC; ++t) {
+                            const int e = ch * EPC + t;
+                            const double kbe = kb[e + e / 8];
+                            const double kc = jok ? __dadd_rn(to_f64(ke[t]), -kbe) : 0.0;
+                            kcB[kcb<D, NSL>(e, j)] = kc;
+                            s0 = fma(kbe, kc, s0);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 8; o >= 1; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o, 16);
+                if (l16 == 0) c0r[j] = s0;
+            }
+            if (pass == 0) WC_BTR(19);
             if (blk == 0 && j == 0) WC_BTR(11);
         }
-        cw_sync();
+        cw_sync();  // candidates, their F columns, centred keys and c0 are in shared memory
         WC_BTR(1);
-
-        // ---- 2: candidate data: the columns F[0:i, s_j] gathered from the tile-major F (rows written
-        // by the owner CTAs in earlier blocks; 16 independent loads per thread in flight, L2 only: an
-        // L1 line read earlier may straddle into a row another CTA wrote since), the centred
-        // candidate keys (fp64, MMA layout) and the parts of c0[j] = <kbar, k_sj - kbar>
+        WC_BTR(2);
         const int i4 = (i + 3) & ~3;
-        constexpr int KPT = D * NSL / kCT;  // candidate-key elements per thread (slot tid % NSL)
-        const int jk = tid % NSL;           // fixed per thread
-        T kraw[KPT];                        // issued first: their latency overlaps the F gather
-#pragma unroll
-        for (int k = 0; k < KPT; ++k)
-            kraw[k] = jk < bsz ? Ku[(int64_t)cs[jk] * D + tid / NSL + k * (kCT / NSL)] : T(0.0f);
-        {
-            constexpr int kG = 16;
-            const int tot = NSL * i4;
-            for (int base = 0; base < tot; base += kG * kCT) {
-                double vals[kG];
-#pragma unroll
-                for (int k = 0; k < kG; ++k) {
-                    const int idx = base + k * kCT + tid, j = idx / (i4 > 0 ? i4 : 1), q = idx - j * i4;
-                    vals[k] = (idx < tot && j < bsz && q < i) ? __ldcg(Fu + cfo[j] + (int64_t)q * cwk[j]) : 0.0;
-                }
-#pragma unroll
-                for (int k = 0; k < kG; ++k) {
-                    const int idx = base + k * kCT + tid, j = idx / (i4 > 0 ? i4 : 1), q = idx - j * i4;
-                    if (idx < tot) Fcol[(size_t)j * ldc + q] = vals[k];
-                }
-            }
-        }
-        {
-            double s0 = 0.0;
-#pragma unroll
-            for (int k = 0; k < KPT; ++k) {
-                const int e = tid / NSL + k * (kCT / NSL);
-                const double kc = jk < bsz ? __dadd_rn(to_f64(kraw[k]), -kb[e]) : 0.0;
-                kcB[kcb<D, NSL>(e, jk)] = kc;
-                s0 = fma(kb[e], kc, s0);
-            }
-            sm.c0p[tid] = s0;
-        }
-        cw_sync();
-        if (tid < NSL) {  // c0[j]: the e-parts of slot j in fixed order
-            double s0 = 0.0;
-#pragma unroll
-            for (int q = 0; q < kCT / NSL; ++q) s0 += sm.c0p[q * NSL + tid];
-            c0r[tid] = s0;
-        }
         // ---- 3: H = h~(K_C, K_C) - F[0:i, C]^T F[0:i, C] on the fp64 tensor cores, one 8x8 tile
         // (mt, nt) per warp and pass (all k-steps of the tile in one accumulator, fixed k order: the
         // (x, e) and (e, x) tiles get the same bits, so H is bitwise symmetric).  Kernel-dot k-steps
         // first (now), F k-steps once the gather has landed.
         constexpr int NTILE = NT * NT, TPW = (NTILE + kCW - 1) / kCW;
+        if (!rej_cta || is_R) {  // (a CTA that relays the rejection CTA's result needs no H)
         double hk[TPW][2], hf[TPW][2];
 #pragma unroll
         for (int q = 0; q < TPW; ++q) hk[q][0] = hk[q][1] = hf[q][0] = hf[q][1] = 0.0;
@@ -753,8 +903,6 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 hk[q][1] += h2[1];
             }
         }
-        cw_sync();  // the gathered columns (rows [i, i4) and slots >= bsz are zero)
-        WC_BTR(2);
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
             const int tile = w + kCW * q;
@@ -773,6 +921,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 }
             }
         }
+        }
         if (tid == 0) sh_cmd = 1;
         ce_sync();  // A: H0, c0r complete; the rejection warp starts
         WC_BTR(3);
@@ -788,9 +937,13 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         for (int k = 0; k < nst; ++k) {
             const int64_t t0 = lo + (int64_t)k * BT;
             const int wk = tile_w(k);
-            double *Fk = Fc + (int64_t)k * a.r * BT;
-            const int kw = KPW * w;
-            const bool wact = t0 + kw < hi;
+            double *Fk = Fc + (int64_t)k * r4 * BT;
+            // warp w owns the row tiles w, w + 8, .. of the super-tile (8 keys each, interleaved so that a
+            // partial super-tile spreads over all four SM sub-partitions' DMMA pipes); its warp-local key
+            // j (row tile j / 8, row j % 8) sits at super-tile offset koff(j)
+            auto rto = [&](int mt) { return 8 * (w + kCW * mt); };
+            auto koff = [&](int j) { return rto(j >> 3) + (j & 7); };
+            const bool wact = t0 + 8 * w < hi;
             double C[MT][NT][2];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
@@ -800,7 +953,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 KC kc[2][MT];  // double-buffered K chunks: chunk c + 1 is in flight while c feeds the MMAs
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
-                    const int64_t key = t0 + kw + 8 * mt + gid;
+                    const int64_t key = t0 + rto(mt) + gid;
                     if (key < hi) kc[0][mt].load(Ku + key * D + tq * DQ);
                     else kc[0][mt].zero();
                 }
@@ -810,7 +963,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     if (t0c + TC < DQ) {
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
-                            const int64_t key = t0 + kw + 8 * mt + gid;
+                            const int64_t key = t0 + rto(mt) + gid;
                             if (key < hi) kc[cb ^ 1][mt].load(Ku + key * D + tq * DQ + t0c + TC);
                             else kc[cb ^ 1][mt].zero();
                         }
@@ -843,28 +996,36 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     }
             }
             if (k == 0) WC_BTR(6);
-            // F-prefix dots: rows 0..i-1 of this super-tile from the ring (one k-step per stage)
-            for (int j0 = 0; j0 < i; j0 += kBR) {
-                mbar_wait(&full[rstage], rph);
-                if (wact) {
-                    const double *sb = ring + (size_t)rstage * kBR * PITCH;
-                    const bool rowok = j0 + tq < i;
-                    double bf[NT];
+            // F-prefix dots: rows 0..i-1 of this super-tile from the ring (one k-step per stage),
+            // C -= F[.., tile]^T F[.., C] as C += A (-B): the 2 B values per stage are negated (sign bit),
+            // not the 8 A values.  Rows [i, i4) of the last quad are zero in F (key_triangle) and in Fcol,
+            // so no row predicate is needed.  The stage is released by the mbarrier arrive (release
+            // semantics; every lane's loads have been consumed by its DMMAs before the __syncwarp).
+            {
+                int aoff[MT];
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) bf[nt] = Fcol[(size_t)(nt * 8 + gid) * ldc + j0 + tq];
+                for (int mt = 0; mt < MT; ++mt) aoff[mt] = (rto(mt) + gid) * kBR + tq;
+                const double *bcol = Fcol + (size_t)gid * ldc + tq;
+                for (int j0 = 0; j0 < i; j0 += kBR) {
+                    mbar_wait(&full[rstage], rph);
+                    if (wact) {
+                        const double *sb = ring + (size_t)rstage * STAGE;
+                        double bf[NT];
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const double av = rowok ? -sb[tq * PITCH + kw + 8 * mt + gid] : 0.0;
+                        for (int nt = 0; nt < NT; ++nt) bf[nt] = dneg(bcol[(size_t)nt * 8 * ldc + j0]);
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], av, bf[nt]);
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const double av = sb[aoff[mt]];
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) dmma(C[mt][nt][0], C[mt][nt][1], av, bf[nt]);
+                        }
                     }
-                }
-                fence_proxy_async_smem();  // this lane's reads of the stage precede the next bulk copy into it
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[rstage]);
-                if (++rstage == NS) {
-                    rstage = 0;
-                    rph ^= 1u;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[rstage]);
+                    if (++rstage == NS) {
+                        rstage = 0;
+                        rph ^= 1u;
+                    }
                 }
             }
             if (k == 0) WC_BTR(7);
@@ -888,13 +1049,13 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                 double plh[KPL];  // the residuals of the lane's keys, loaded before the staging
 #pragma unroll
                 for (int h = 0; h < KPL; ++h) {
-                    const int64_t key = t0 + kw + 32 * h + lane;
+                    const int64_t key = t0 + koff(32 * h + key_of_lane(lane));
                     plh[h] = key < hi ? __ldcg(cur + key) : 0.0;
                 }
                 // per key (lane, half h) after its triangle: residual, L rows of an accepted pivot, and
-                // the 32-key group sum
+                // the sum of its row tile (8 lanes; the 32-key group sums follow once all warps are done)
                 auto key_epilogue = [&](int h, const double (&f)[NSL], double pl) {
-                    const int64_t key = t0 + kw + 32 * h + lane;
+                    const int64_t key = t0 + koff(32 * h + key_of_lane(lane));
                     if (key < hi) {
                         nxt[key] = pl;
                         int xm = -1;  // acceptance index if this key is an accepted pivot (branch-free search)
@@ -907,11 +1068,10 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                                 if (a2 <= xm) Lr[a2] = f[a2];
                         }
                     }
-                    const double gs = warp_sum(key < hi ? pl : 0.0);  // one 32-key group (fixed order)
-                    if (lane == 0 && t0 + kw + 32 * h < hi) {
-                        gnxt[(t0 + kw) / 32 + h] = gs;
-                        loc += gs;
-                    }
+                    double rs = key < hi ? pl : 0.0;  // one row tile: lanes m, m + 4, .., m + 28 (fixed butterfly)
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+                    if (lane < 4) rts[w + kCW * (4 * h + lane)] = rs;
                 };
                 // stage G rows (keys 8 mt + gid of the warp) for row tiles [mt0, mt0 + 4 KSN) at stg
                 auto stage = [&](double *stg, int mt0, int nmt) {
@@ -923,37 +1083,53 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                             for (int hh = 0; hh < 2; ++hh) {
                                 const int ai = pm[nt * 2 + hh];
                                 if (ai >= 0 && mt >= mt0 && mt < mt0 + nmt)
-                                    stg[(8 * (mt - mt0) + gid) * SP + ai] = C[mt][nt][hh];
+                                    stg[srow_of(8 * (mt - mt0) + gid) * SP + ai] = C[mt][nt][hh];
                             }
                 };
                 if (KPL == 2 && two_keys) {
                     // both of the lane's keys staged at once, their triangles interleaved
                     double *stg = ring + (size_t)w * 64 * SP;
+                    if (k == 0) WC_BTR(21);
                     stage(stg, 0, MT);
                     __syncwarp();
-                    const int64_t keys[2] = {t0 + kw + lane, t0 + kw + 32 + lane};
-                    double *const frows[2] = {Fk + (int64_t)i * wk + kw + lane, Fk + (int64_t)i * wk + kw + 32 + lane};
+                    if (k == 0) WC_BTR(24);
+                    const int64_t keys[2] = {t0 + koff(key_of_lane(lane)), t0 + koff(32 + key_of_lane(lane))};
                     double f[2][NSL];
                     double pl[2] = {plh[0], plh[KPL - 1]};
-                    key_triangle<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, f, pl);
+                    key_triangle<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
+                    __syncwarp();
+                    if (k == 0) WC_BTR(15);
+                    write_f_rows<NSL>(stg, lane, 8, koff, t0, hi, Fk, wk, i, na);
+                    if (k == 0) WC_BTR(22);
                     __syncwarp();
                     key_epilogue(0, f[0], pl[0]);
                     key_epilogue(1, f[1], pl[1]);
+                    if (k == 0) WC_BTR(23);
                 } else {
                     double *stg = ring + (size_t)w * 32 * SP;  // [32 keys][SP] per warp
 #pragma unroll
                     for (int h = 0; h < KPL; ++h) {  // 32 keys of the warp at a time (row tiles 4h .. 4h + 3)
                         stage(stg, 4 * h, 4);
                         __syncwarp();
-                        const int64_t keys[1] = {t0 + kw + 32 * h + lane};
-                        double *const frows[1] = {Fk + (int64_t)i * wk + kw + 32 * h + lane};
+                        const int64_t keys[1] = {t0 + koff(32 * h + key_of_lane(lane))};
                         double f[1][NSL];
                         double pl[1] = {plh[h]};
-                        key_triangle<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, f, pl);
+                        key_triangle<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
+                        __syncwarp();
+                        write_f_rows<NSL>(stg, lane, 4, [&](int jl) { return koff(32 * h + jl); }, t0, hi, Fk, wk, i, na);
                         __syncwarp();  // the staging of this half is consumed
                         key_epilogue(h, f[0], pl[0]);
                     }
                 }
+            } else if (lane < MT) {
+                rts[w + kCW * lane] = 0.0;  // row tiles past the slice
+            }
+            // the 32-key group sums (row tiles 4g .. 4g + 3, fixed order) and this CTA's running sum
+            cw_sync();
+            if (tid < BT / 32 && t0 + 32 * tid < hi) {
+                const double gs = (rts[4 * tid] + rts[4 * tid + 1]) + (rts[4 * tid + 2] + rts[4 * tid + 3]);
+                gnxt[t0 / 32 + tid] = gs;
+                loc += gs;
             }
             fence_proxy_async_smem();  // the staging accesses to the ring precede the next bulk copies into it
             if (k + 1 < nst) {  // the ring (used as staging above) is free: stream the next super-tile
@@ -970,13 +1146,13 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
         loc = cw_sum(loc, scr);
         if (tid == 0) pn[c] = loc;
         WC_BTR(9);
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * 16 + 13] = clock64();
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && blk < a.r) a.trace[blk * kTS + 13] = clock64();
         fread += (double)i;
         fdot += (double)i * (double)na;
         i += na;
         cbase += (uint32_t)bsz;
         ++blk;
-        cw_group_barrier(a.bar + u, a.cpu, epoch++, &sh_dummy, 0);
+        block_barrier(epoch++, cbase);
     }
     if (tid == 0) {
         flag_st(&sh_stop, 1);
@@ -995,7 +1171,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
 
 // Debug: per-block phase durations of CTA 0 (ns), printed per block.
 void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
-    std::vector<unsigned long long> h((size_t)16 * r);
+    std::vector<unsigned long long> h((size_t)kTS * r);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), dtrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(dtrace);
@@ -1006,18 +1182,24 @@ void dump_block_trace(unsigned long long *dtrace, int r, cudaStream_t st) {
     const char *names[] = {"cand", "gather", "H", "t0_kdot(+elim)", "t0_fdot", "na/Fx", "Lrows", "tiles", "sum",
                            "gbar"};
     for (int b = 0; b < r; ++b) {
-        const unsigned long long *t = &h[(size_t)b * 16];
+        const unsigned long long *t = &h[(size_t)b * kTS];
         if (!t[0] || !t[9]) break;
         std::fprintf(stderr, "[btrace] block %3d:", b);
         unsigned long long last = t[0];
         for (int k = 0; k < 10; ++k) {
-            const unsigned long long v = order[k] == 16 ? (b + 1 < r ? h[(size_t)(b + 1) * 16] : 0) : t[order[k]];
+            const unsigned long long v = order[k] == 16 ? (b + 1 < r ? h[(size_t)(b + 1) * kTS] : 0) : t[order[k]];
             if (!v) continue;
             std::fprintf(stderr, " %s=%llu", names[k], v - last);
             last = v;
         }
         if (b == 0 && t[10] && t[11]) std::fprintf(stderr, " [1a=%llu cand0=%llu]", t[10] - t[0], t[11] - t[10]);
         if (t[14] > t[3]) std::fprintf(stderr, " [elim=%llu]", t[14] - t[3]);
+        if (t[20] && t[16] && t[17] && t[18] && t[19])
+            std::fprintf(stderr, " [poll=%llu L1=%llu L2=%llu L3=%llu gath=%llu]", t[20] - t[0], t[16] - t[20], t[17] - t[16],
+                         t[18] - t[17], t[19] - t[18]);
+        if (t[21] && t[22] && t[23])
+            std::fprintf(stderr, " [pre=%llu stage=%llu tri=%llu wr=%llu epi=%llu gs=%llu]", t[21] - t[5], t[24] - t[21],
+                         t[15] - t[24], t[22] - t[15], t[23] - t[22], t[8] - t[23]);
         if (t[13] > t[12] && t[9] > t[0]) std::fprintf(stderr, " MHz=%.0f", 1e3 * (double)(t[13] - t[12]) / (double)(t[9] - t[0]));
         std::fprintf(stderr, "\n");
     }
@@ -1032,7 +1214,7 @@ constexpr size_t kSmemStatic = 2048;
 template <int D, int NSL> int blocked_stages(int r, int cpu, bool min_only = false) {
     using PL = BPlan<NSL>;
     const int ldc = ((r + 15) & ~15) + 4;
-    const size_t stage_bytes = (size_t)kBR * PL::PITCH * sizeof(double);
+    const size_t stage_bytes = (size_t)PL::STAGE * sizeof(double);
     const size_t fixed = BSmem<D, NSL>(nullptr, 0, ldc, cpu).bytes + 64;
     // the per-key triangle stages G ([32 keys][NSL + 1] per compute warp) through the idle ring
     const size_t stg = (size_t)kCW * 32 * PL::SPITCH * sizeof(double);
@@ -1050,6 +1232,7 @@ int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs 
     BlkArgs a;
     a.K = K; a.stats = stats; a.nrm2 = b.nrm2; a.p = b.p; a.F = b.F; a.part = b.part; a.bar = b.bar;
     a.gsum = b.gsum;
+    a.rej = b.rej;
     a.S = S; a.r_eff = r_eff; a.L = L; a.n = Dm.n; a.units = Dm.units(); a.r = Dm.r;
     a.bins = Dm.bins; a.nb = Dm.nb; a.unit_n = Dm.unit_n;
     a.cpu = select_ctas_per_unit(Dm); a.b = block; a.seed = seed; a.unit0 = unit0; a.trace = nullptr;
@@ -1063,18 +1246,21 @@ int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs 
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, kt) != cudaSuccess) return -1;
     const size_t extra = fa.sharedSizeBytes > kSmemStatic ? fa.sharedSizeBytes - kSmemStatic : 0;
-    const int drop = (int)((extra + kBR * PL::PITCH * sizeof(double) + 15) / (kBR * PL::PITCH * sizeof(double) + 16));
+    const int drop = (int)((extra + PL::STAGE * sizeof(double) + 15) / (PL::STAGE * sizeof(double) + 16));
     if (drop > 0) {
         if (NS - drop < blocked_stages<D, NSL>(Dm.r, a.cpu, true)) return -2;
         NS -= drop;
     }
     const size_t smem = BSmem<D, NSL>(nullptr, NS, ldc, a.cpu).bytes + 64;
     static const bool tracing = std::getenv("WC_SELECT_TRACE") != nullptr;
-    if (tracing && cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * Dm.r) == cudaSuccess)
-        cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * 16 * Dm.r, st);
+    if (tracing && cudaMalloc(&a.trace, sizeof(unsigned long long) * kTS * Dm.r) == cudaSuccess)
+        cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * kTS * Dm.r, st);
     if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
     if (cudaMemsetAsync(b.bar, 0, sizeof(unsigned) * a.units, st) != cudaSuccess) return -1;
     if (cudaMemsetAsync(b.part, 0, sizeof(double) * 2 * kMaxCpu * a.units, st) != cudaSuccess) return -1;
+    if (a.cpu >= kRejMinCpu &&
+        cudaMemset2DAsync(b.rej, kRejStride * sizeof(double), 0, sizeof(double), a.units, st) != cudaSuccess)
+        return -1;  // the flags of the published rejection results
     const dim3 grid(a.units * a.cpu);
     if (a.cpu > 1) {
         // cooperative (co-resident CTAs for the grid barrier) + programmatic stream serialisation

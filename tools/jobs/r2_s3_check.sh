@@ -1,0 +1,6 @@
+# session 3: build, blocked-selection parity, headline bench + per-block trace
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/c_smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests/test_gpu_blocked.py -q -x > gpurun_out/c_blocked.log 2>&1; echo blocked=$?
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-variants --no-exact > gpurun_out/c_bench.json 2> gpurun_out/c_bench.err; echo bench=$?
+WC_SELECT_TRACE=1 timeout 300 python tools/trace_blocked.py 16 > /dev/null 2> gpurun_out/c_trace.txt; echo trace=$?
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/c_gputests.log 2>&1; echo tests=$?
