@@ -7,6 +7,7 @@ Public API (torch tensors in the BHND layout [batch, heads, seq, d], CUDA only):
     cache = weights(K, V, sel)                              # Alg 2 "Compress values"
     O = attend(Q, cache)                                    # Alg 3 WtdAttn
     O = forward_host(Q_cpu, K_cpu, V_cpu, r)                # host buffers in, host result out
+    pipe = HostPipeline(Q_cpu, K_cpu, r); pipe.submit(Qh, Kh, Vh, Oh)  # streamed host batches, copies overlapped
     cache = compress_kv(Q, K, V, r, keep_first=32, keep_last=32)  # KV-cache compression (prefill)
     O_new = attend(Q_new, cache)                            # decode over the compressed cache
     comm = NshardComm.create(group)                         # keys of one sequence sharded over ranks
@@ -25,7 +26,7 @@ import torch
 from . import _binding as B
 from ._binding import NonFiniteInput, WildcatError, lib  # noqa: F401
 
-__all__ = ["forward", "forward_host", "HostForward", "select", "weights", "attend", "decode", "Selection", "Cache",
+__all__ = ["forward", "forward_host", "HostForward", "HostPipeline", "select", "weights", "attend", "decode", "Selection", "Cache",
            "KvCache", "WildcatError",
            "STATS_STRIDE", "NshardComm", "forward_nshard", "shard_range", "compress_kv", "kv_capacity"]
 
@@ -329,6 +330,75 @@ class HostForward:
             dst.copy_(self.Od, non_blocking=True)
         sm.synchronize()
         return self.Oh.clone() if out is None else out
+
+
+class HostPipeline:
+    """Streaming end-to-end WildCat over a sequence of host (CPU, pinned) batches of one shape.
+
+    Each submitted step copies its Q, K, V host->device, runs wildcat_forward (the fused C-ABI
+    call) and copies O device->host into the caller's pinned `out`.  The three parts run on three
+    CUDA streams ordered by events over `slots` device buffer sets, so the H2D of step k+1 and
+    the D2H of step k-1 overlap the compute of step k (B200: the copy engines of both directions and
+    the SMs work at once; one compute stream keeps the compute serial and its workspace shared).
+        pipe = HostPipeline(Q, K, r, block=16)
+        for Qh, Kh, Vh, Oh in batches: pipe.submit(Qh, Kh, Vh, Oh)
+        pipe.synchronize()            # every Oh holds its step's result
+    A step's `out` may be read once pipe.done(step) (or synchronize()) returns; its inputs may be
+    overwritten once pipe.inputs_free(step) does."""
+
+    def __init__(self, Q, K, r, seed=0, beta=None, rq=None, clip=True, block=1, bins=1, device="cuda", slots=2,
+                 **kw):
+        dev = torch.device(device)
+        self.dev, self.nslots = dev, int(slots)
+        mk = lambda t: torch.empty(t.shape, dtype=t.dtype, device=dev)  # noqa: E731
+        self.buf = [dict(Q=mk(Q), K=mk(K), V=mk(K), O=mk(Q)) for _ in range(self.nslots)]
+        self.shape = B.make_shape(self.buf[0]["Q"], self.buf[0]["K"], r, bins=bins)
+        self.opts = _opts(seed, beta, rq, clip, block, kw)
+        self.ws = B.alloc_workspace(self.shape, B.WC_OP_FORWARD, dev)
+        self.s_in, self.s_cmp, self.s_out = (torch.cuda.Stream(dev) for _ in range(3))
+        self.ev_in = [torch.cuda.Event() for _ in range(self.nslots)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(self.nslots)]
+        self.ev_out = [torch.cuda.Event() for _ in range(self.nslots)]
+        self.step = 0
+
+    def submit(self, Qh, Kh, Vh, out):
+        """Enqueue one step (host tensors; pinned for asynchronous copies).  Returns its index."""
+        for t, ref in ((Qh, "Q"), (Kh, "K"), (Vh, "V"), (out, "O")):
+            want = self.buf[0][ref]
+            if t.is_cuda or t.shape != want.shape or t.dtype != want.dtype:
+                raise WildcatError(f"HostPipeline.submit: {ref} must be a host tensor of shape {tuple(want.shape)}")
+        k, s = self.step, self.step % self.nslots
+        b = self.buf[s]
+        with torch.cuda.stream(self.s_in):
+            if k >= self.nslots:  # the compute of step k - slots has read this slot's inputs
+                self.s_in.wait_event(self.ev_cmp[s])
+            b["K"].copy_(Kh, non_blocking=True)
+            b["Q"].copy_(Qh, non_blocking=True)
+            b["V"].copy_(Vh, non_blocking=True)
+            self.ev_in[s].record(self.s_in)
+        self.s_cmp.wait_event(self.ev_in[s])
+        if k >= self.nslots:  # the D2H of step k - slots has read this slot's output
+            self.s_cmp.wait_event(self.ev_out[s])
+        B.wildcat_forward(self.shape, self.opts, b["Q"], b["K"], b["V"], b["O"], None, None, self.ws, self.s_cmp)
+        self.ev_cmp[s].record(self.s_cmp)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.ev_cmp[s])
+            out.copy_(b["O"], non_blocking=True)
+            self.ev_out[s].record(self.s_out)
+        self.step += 1
+        return k
+
+    def done(self, k):
+        """Block until step k's result is in its host `out` (valid for the last `slots` steps)."""
+        self.ev_out[k % self.nslots].synchronize()
+
+    def inputs_free(self, k):
+        """Block until step k's host inputs have been copied (they may then be overwritten)."""
+        self.ev_in[k % self.nslots].synchronize()
+
+    def synchronize(self):
+        for st in (self.s_in, self.s_cmp, self.s_out):
+            st.synchronize()
 
 
 _host_cache: dict = {}

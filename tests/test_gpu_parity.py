@@ -180,6 +180,31 @@ def test_forward_host_matches_device_forward(block):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("block", [1, 16])
+def test_host_pipeline_matches_device_forward(block):
+    # streamed host batches (HostPipeline: H2D / forward / D2H on three event-ordered streams, two
+    # device slots reused every other step) == wildcat_forward on each batch, bit for bit
+    import paper_2602_10056_b200 as wc
+
+    dev = torch.device("cuda:0")
+    batches = [qkv(2, 4, 2, 300, 3000, 64, "bf16", "C", seed=20 + k) for k in range(5)]
+    want = []
+    for Q, K, V in batches:
+        want.append(wc.forward(Q.to(dev), K.to(dev), V.to(dev), 64, seed=12, block=block).cpu())
+    Q0, K0, _ = batches[0]
+    pipe = wc.HostPipeline(Q0, K0, 64, seed=12, block=block)
+    pinned = [tuple(x.pin_memory() for x in b) for b in batches]
+    outs = [torch.empty(Q0.shape, dtype=Q0.dtype, pin_memory=True) for _ in batches]
+    for (Qh, Kh, Vh), Oh in zip(pinned, outs):
+        pipe.submit(Qh, Kh, Vh, Oh)
+    pipe.synchronize()
+    for k, Oh in enumerate(outs):
+        assert torch.equal(Oh, want[k]), k
+    with pytest.raises(wc.WildcatError):
+        pipe.submit(Q0.to(dev), K0, K0, outs[0])
+
+
+@pytest.mark.gpu
 def test_binding_rejects_mismatched_tensors():
     import paper_2602_10056_b200 as wc
     # the C ABI takes raw pointers, so the wrappers must refuse tensors that disagree
