@@ -193,7 +193,7 @@ void carve_select(Carver &c, const Plan &p, SelectWs &w) {
     w.sb.part = c.take<double>(U * 2 * wc::kMaxCpu);
     w.sb.bar = c.take<unsigned>(U);
     w.sb.gsum = c.take<double>(U * 2 * (size_t)((D.n + 31) / 32));
-    w.sb.rej = c.take<double>(U * wc::kRejStride);
+    if (wc::select_ctas_per_unit(D) >= wc::kRejMinCpu) w.sb.rej = c.take<double>(U * wc::kRejStride);
     if (p.B > 1) {
         w.stats_u = c.take<double>((size_t)p.D.units() * WC_STATS_STRIDE(D.d));
         w.Ssub = c.take<int32_t>(U * D.r);

@@ -82,7 +82,7 @@ struct SelectBufs {
     double *part;   // [units][2][kMaxCpu]
     unsigned *bar;  // [units]
     double *gsum;   // [units][2][ceil(n/32)] residual sums of 32-key groups (blocked selection)
-    double *rej;    // [units][kRejStride] the rejection CTA's published block result (blocked selection)
+    double *rej = nullptr;  // [units][kRejStride] the rejection CTA's published block result (blocked selection)
 };
 // Blocked selection with >= kRejMinCpu CTAs per unit: the last CTA owns no keys and runs the block
 // rejection for the unit (its fp64 pipe free of the round-update DMMAs), publishing the result.

@@ -82,7 +82,9 @@ def test_null_and_workspace_errors(L):
 def test_workspace_sizes_scale(L):
     s1 = _shape(n=1000, r=10)
     s2 = _shape(n=2000, r=20)
-    assert L.wc_workspace_bytes(ctypes.byref(s2), 0) > 3 * L.wc_workspace_bytes(ctypes.byref(s1), 0)
+    # n x r grows 4x; the blocked selection's F rows come in quads (r rounded up to a multiple of 4),
+    # which weighs more at r = 10 than at r = 20, and the per-unit scalars do not grow
+    assert L.wc_workspace_bytes(ctypes.byref(s2), 0) > 2.5 * L.wc_workspace_bytes(ctypes.byref(s1), 0)
     big_m = _shape(n=1000, r=10, m=500)
     assert L.wc_workspace_bytes(ctypes.byref(big_m), 2) > 0  # tcgen05 attend: per-unit operand image
     assert L.wc_workspace_bytes(ctypes.byref(_shape(n=1000, r=10, m=500, dtype=0)), 2) == 0  # fp32: none
