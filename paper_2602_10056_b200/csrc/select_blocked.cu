@@ -312,7 +312,9 @@ template <int D, int NSL> struct BSmem {
     }
 };
 
-template <typename T, int D, int NSL>
+// ILV: warps own interleaved row tiles (w, w + 8, ..) of a super-tile, else contiguous 64-key spans
+// (slices of at most BT / 2 keys: one warp per SM sub-partition, the empty warps idle).
+template <typename T, int D, int NSL, bool ILV>
 __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArgs a, int NS) {
     pdl_wait();  // the prologue's stats / nrm2 (programmatic dependent launch)
     using PL = BPlan<NSL>;
@@ -941,9 +943,11 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             // warp w owns the row tiles w, w + 8, .. of the super-tile (8 keys each, interleaved so that a
             // partial super-tile spreads over all four SM sub-partitions' DMMA pipes); its warp-local key
             // j (row tile j / 8, row j % 8) sits at super-tile offset koff(j)
-            auto rto = [&](int mt) { return 8 * (w + kCW * mt); };
+            // (ILV = false, short slices: contiguous 64-key warp spans instead)
+            constexpr int wsr = ILV ? 1 : MT, msr = ILV ? kCW : 1;  // row-tile index = w * wsr + mt * msr
+            auto rto = [&](int mt) { return 8 * (w * wsr + mt * msr); };
             auto koff = [&](int j) { return rto(j >> 3) + (j & 7); };
-            const bool wact = t0 + 8 * w < hi;
+            const bool wact = t0 + 8 * w * wsr < hi;
             double C[MT][NT][2];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
@@ -1071,7 +1075,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     double rs = key < hi ? pl : 0.0;  // one row tile: lanes m, m + 4, .., m + 28 (fixed butterfly)
 #pragma unroll
                     for (int o = 4; o < 32; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-                    if (lane < 4) rts[w + kCW * (4 * h + lane)] = rs;
+                    if (lane < 4) rts[w * wsr + (4 * h + lane) * msr] = rs;
                 };
                 // stage G rows (keys 8 mt + gid of the warp) for row tiles [mt0, mt0 + 4 KSN) at stg
                 auto stage = [&](double *stg, int mt0, int nmt) {
@@ -1122,7 +1126,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     }
                 }
             } else if (lane < MT) {
-                rts[w + kCW * lane] = 0.0;  // row tiles past the slice
+                rts[w * wsr + lane * msr] = 0.0;  // row tiles past the slice
             }
             // the 32-key group sums (row tiles 4g .. 4g + 3, fixed order) and this CTA's running sum
             cw_sync();
@@ -1240,7 +1244,12 @@ int launch_blocked_tdn(const Dims &Dm, const void *K, double *stats, SelectBufs 
     int NS = blocked_stages<D, NSL>(Dm.r, a.cpu);
     if (NS == 0) return -2;  // r too large for this plan
     (void)sizeof(PL);
-    auto kt = rpc_select_blocked_kernel<T, D, NSL>;
+    auto kt = rpc_select_blocked_kernel<T, D, NSL, true>;
+    if constexpr (NSL == 16) {  // slices of at most BT / 2 keys: contiguous warp spans (see ILV)
+        const int kc = key_ctas(a.cpu);
+        const int64_t chunk = ((ceil_div(Dm.n, (int64_t)kc) + 31) / 32) * 32;
+        if (chunk <= PL::BT / 2) kt = rpc_select_blocked_kernel<T, D, NSL, false>;
+    }
     // the plan reserves kSmemStatic bytes for the kernel's static shared memory: take any excess
     // (toolchain-dependent) out of the ring, down to the plan's minimum
     cudaFuncAttributes fa{};
