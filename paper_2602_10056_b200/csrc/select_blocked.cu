@@ -197,10 +197,13 @@ template <typename T, int TC> struct KChunk {
 // Per-key triangle of KSN keys per lane at once (independent fp64 chains interleaved):
 //   F[i+aa, l] = (G[l, aa] - sum_{a2<aa} F[i+a2, l] F[i+a2, s_aa]) * (1 / sqrt(p_{s_aa}))
 // for the accepted slots aa < na in acceptance order, the residual downdate with the clamp (Z4) and
-// p_s <- 0.  stg: the staged G rows [32 KSN keys][NSL + 1]; F[i + aa, key] replaces G[key, aa] there
-// (read just before), for the coalesced write-out of the F rows (write_f_rows).
+// p_s <- 0.  stg: the staged G rows [32 KSN keys][NSL + 1].  DIRECT: F[i + aa, key] is stored (key < hi)
+// at frow[h] + ((i + aa) / 4) * 4 wk + (i + aa) % 4 (frow[h]: the key's column in quad 0 of its
+// super-tile) as soon as it is computed; else it replaces G[key, aa] in stg (read just before) for the
+// coalesced write_f_rows.  Measured: the staged write-out wins on full interleaved super-tiles (the
+// headline), the direct stores on short contiguous slices (ViT).
 template <int NSL, int KSN>
-__device__ __forceinline__ void key_triangle(double *stg, int lane, const double *Fx, const double *rinvA,
+__device__ __forceinline__ void key_triangle_staged(double *stg, int lane, const double *Fx, const double *rinvA,
                                              const int *sA, int na, const int64_t (&key)[KSN],
                                              double (&f)[KSN][NSL], double (&pl)[KSN]) {
     constexpr int SP = NSL + 1;
@@ -239,12 +242,67 @@ __device__ __forceinline__ void key_triangle(double *stg, int lane, const double
     }
 }
 
+// The same triangle with each F[i + aa, key] stored (key < hi) as soon as it is computed, at frow[h] +
+// ((i + aa) / 4) * 4 wk + (i + aa) % 4 (frow[h]: the key's column in quad 0 of its super-tile), and zeros
+// to the end of the last quad.  Measured: the staged write-out (key_triangle_staged + write_f_rows) wins
+// on full interleaved super-tiles (the headline), these direct stores on short contiguous slices (ViT).
+template <int NSL, int KSN>
+__device__ __forceinline__ void key_triangle_direct(double *stg, int lane, const double *Fx, const double *rinvA,
+                                                    const int *sA, int na, const int64_t (&key)[KSN], int64_t hi,
+                                                    double *const (&frow)[KSN], int wk, int i,
+                                                    double (&f)[KSN][NSL], double (&pl)[KSN]) {
+    constexpr int SP = NSL + 1;
+#pragma unroll
+    for (int aa = 0; aa < NSL; ++aa) {
+#pragma unroll
+        for (int h = 0; h < KSN; ++h) f[h][aa] = 0.0;
+        if (aa < na) {
+            const double *fx = Fx + aa * NSL;
+            double c0v[KSN], c1v[KSN];  // two partial sums per key shorten the dependent chain
+#pragma unroll
+            for (int h = 0; h < KSN; ++h) {
+                c0v[h] = stg[(32 * h + lane) * SP + aa];
+                c1v[h] = 0.0;
+            }
+#pragma unroll
+            for (int a2 = 0; a2 < aa; ++a2) {
+                const double x = fx[a2];
+#pragma unroll
+                for (int h = 0; h < KSN; ++h) {
+                    if (a2 & 1) c1v[h] = fma(-f[h][a2], x, c1v[h]);
+                    else c0v[h] = fma(-f[h][a2], x, c0v[h]);
+                }
+            }
+            const double ra = rinvA[aa];
+            const int sa = sA[aa];
+            const int64_t fo = (int64_t)((i + aa) >> 2) * wk * kBR + ((i + aa) & 3);
+#pragma unroll
+            for (int h = 0; h < KSN; ++h) {
+                const double fv = (c0v[h] + c1v[h]) * ra;
+                f[h][aa] = fv;
+                if (key[h] < hi) frow[h][fo] = fv;  // interleaved with the triangle's arithmetic
+                const double qd = __dadd_rn(pl[h], -__dmul_rn(fv, fv));
+                pl[h] = (qd > 0.0 && key[h] != sa) ? qd : 0.0;
+            }
+        }
+    }
+    // rows i + na .. the end of their quad are written as zeros, so every row of a streamed quad is
+    // finite (the F-prefix DMMAs multiply rows >= i by zero B values without a predicate)
+    for (int rr = i + na; rr < ((i + na + 3) & ~3); ++rr) {
+        const int64_t fo = (int64_t)(rr >> 2) * wk * kBR + (rr & 3);
+#pragma unroll
+        for (int h = 0; h < KSN; ++h)
+            if (key[h] < hi) frow[h][fo] = 0.0;
+    }
+}
+
 // Staging row of the warp-local key j (0 .. 63): within each 32-key half, key 8 m + g sits in row 4 g + m,
 // i.e. lane L of the per-key triangle owns key 8 (L & 3) + (L >> 2) of the half.  With the row pitch
 // NSL + 1 the triangle's column reads (row = lane) and the write-out's reads (8 keys x 4 rows) are both
 // conflict-free.
 __device__ __forceinline__ int srow_of(int j) { return (j & ~31) + 4 * (j & 7) + ((j >> 3) & 3); }
 __device__ __forceinline__ int key_of_lane(int lane) { return 8 * (lane & 3) + (lane >> 2); }
+
 
 // Write-out of the new F rows i .. i + na - 1 of 8 KR consecutive warp-local keys (staging rows
 // srow_of(j) hold F[i + aa, key j] at [row][aa]), plus zeros from row i + na to the end of its quad (so
@@ -1002,7 +1060,8 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
             if (k == 0) WC_BTR(6);
             // F-prefix dots: rows 0..i-1 of this super-tile from the ring (one k-step per stage),
             // C -= F[.., tile]^T F[.., C] as C += A (-B): the 2 B values per stage are negated (sign bit),
-            // not the 8 A values.  Rows [i, i4) of the last quad are zero in F (key_triangle) and in Fcol,
+            // not the 8 A values.  Rows [i, i4) of the last quad are zero in F (zero-filled after the
+            // triangle) and in Fcol,
             // so no row predicate is needed.  The stage is released by the mbarrier arrive (release
             // semantics; every lane's loads have been consumed by its DMMAs before the __syncwarp).
             {
@@ -1100,10 +1159,16 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                     const int64_t keys[2] = {t0 + koff(key_of_lane(lane)), t0 + koff(32 + key_of_lane(lane))};
                     double f[2][NSL];
                     double pl[2] = {plh[0], plh[KPL - 1]};
-                    key_triangle<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
-                    __syncwarp();
-                    if (k == 0) WC_BTR(15);
-                    write_f_rows<NSL>(stg, lane, 8, koff, t0, hi, Fk, wk, i, na);
+                    if constexpr (ILV) {
+                        key_triangle_staged<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
+                        __syncwarp();
+                        if (k == 0) WC_BTR(15);
+                        write_f_rows<NSL>(stg, lane, 8, koff, t0, hi, Fk, wk, i, na);
+                    } else {
+                        double *const frows[2] = {Fk + (int64_t)koff(key_of_lane(lane)) * kBR,
+                                                  Fk + (int64_t)koff(32 + key_of_lane(lane)) * kBR};
+                        key_triangle_direct<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, i, f, pl);
+                    }
                     if (k == 0) WC_BTR(22);
                     __syncwarp();
                     key_epilogue(0, f[0], pl[0]);
@@ -1118,10 +1183,18 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                         const int64_t keys[1] = {t0 + koff(32 * h + key_of_lane(lane))};
                         double f[1][NSL];
                         double pl[1] = {plh[h]};
-                        key_triangle<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
+                        if constexpr (ILV) {
+                            key_triangle_staged<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
+                        } else {
+                            double *const frows[1] = {Fk + (int64_t)koff(32 * h + key_of_lane(lane)) * kBR};
+                            key_triangle_direct<NSL, 1>(stg, lane, Fx, rinvA, sA, na, keys, hi, frows, wk, i, f, pl);
+                        }
                         __syncwarp();
-                        write_f_rows<NSL>(stg, lane, 4, [&](int jl) { return koff(32 * h + jl); }, t0, hi, Fk, wk, i, na);
-                        __syncwarp();  // the staging of this half is consumed
+                        if constexpr (ILV) {
+                            write_f_rows<NSL>(stg, lane, 4, [&](int jl) { return koff(32 * h + jl); }, t0, hi, Fk, wk, i,
+                                              na);
+                            __syncwarp();  // the staging of this half is consumed
+                        }
                         key_epilogue(h, f[0], pl[0]);
                     }
                 }
