@@ -309,20 +309,30 @@ __device__ __forceinline__ int key_of_lane(int lane) { return 8 * (lane & 3) + (
 // every row of a streamed quad is finite: the F-prefix DMMAs multiply rows >= i by zero B values without a
 // predicate).  Per (row tile, quad) one warp store of 8 keys x 4 rows = 32 consecutive doubles of the
 // quad layout; rows < i of a partial first quad are left alone.  koff: local key -> super-tile offset.
-template <int NSL, typename KOff>
-__device__ __forceinline__ void write_f_rows(const double *stg, int lane, int KR, KOff koff, int64_t t0, int64_t hi,
+template <int NSL, int KR, typename KOff>
+__device__ __forceinline__ void write_f_rows(const double *stg, int lane, KOff koff, int64_t t0, int64_t hi,
                                              double *Fk, int wk, int i, int na) {
     constexpr int SP = NSL + 1;
     const int q0 = i >> 2, q1 = (i + na + 3) >> 2;
     const int t = lane & 3;
+    // the KR row tiles' offsets once; per quad all KR values are read before the KR stores are issued
+    // (distinct registers: a store does not wait for the previous one to release its operands)
+    int off[KR];
+    bool kin[KR];
+#pragma unroll
+    for (int rt = 0; rt < KR; ++rt) {
+        off[rt] = koff(rt * 8 + (lane >> 2));
+        kin[rt] = t0 + off[rt] < hi;
+    }
     for (int q = q0; q < q1; ++q) {
         const int row = 4 * q + t, aa = row - i;
-        for (int rt = 0; rt < KR; ++rt) {
-            const int jl = rt * 8 + (lane >> 2);
-            const int64_t off = koff(jl);
-            if (row >= i && t0 + off < hi)
-                Fk[(int64_t)q * wk * kBR + off * kBR + t] = aa < na ? stg[srow_of(jl) * SP + aa] : 0.0;
-        }
+        double v[KR];
+#pragma unroll
+        for (int rt = 0; rt < KR; ++rt) v[rt] = aa < na ? stg[srow_of(rt * 8 + (lane >> 2)) * SP + aa] : 0.0;
+        double *fq = Fk + (int64_t)q * wk * kBR + t;
+#pragma unroll
+        for (int rt = 0; rt < KR; ++rt)
+            if (row >= i && kin[rt]) fq[off[rt] * kBR] = v[rt];
     }
 }
 
@@ -1163,7 +1173,7 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                         key_triangle_staged<NSL, 2>(stg, lane, Fx, rinvA, sA, na, keys, f, pl);
                         __syncwarp();
                         if (k == 0) WC_BTR(15);
-                        write_f_rows<NSL>(stg, lane, 8, koff, t0, hi, Fk, wk, i, na);
+                        write_f_rows<NSL, 8>(stg, lane, koff, t0, hi, Fk, wk, i, na);
                     } else {
                         double *const frows[2] = {Fk + (int64_t)koff(key_of_lane(lane)) * kBR,
                                                   Fk + (int64_t)koff(32 + key_of_lane(lane)) * kBR};
@@ -1191,8 +1201,8 @@ __global__ void __launch_bounds__(kBThreads, 1) rpc_select_blocked_kernel(BlkArg
                         }
                         __syncwarp();
                         if constexpr (ILV) {
-                            write_f_rows<NSL>(stg, lane, 4, [&](int jl) { return koff(32 * h + jl); }, t0, hi, Fk, wk, i,
-                                              na);
+                            write_f_rows<NSL, 4>(stg, lane, [&](int jl) { return koff(32 * h + jl); }, t0, hi, Fk, wk,
+                                                 i, na);
                             __syncwarp();  // the staging of this half is consumed
                         }
                         key_epilogue(h, f[0], pl[0]);
