@@ -736,6 +736,175 @@ __global__ void __launch_bounds__(256) weights_solve_small_kernel(const double *
     }
 }
 
+// A4 for r <= 256 with few units: one thread per row of L, C right-hand-side columns per CTA.  Forward
+// substitution L z = y right-looking over the 32-row panels P: the panel's rows finish (z_P = Dinv_PP
+// acc_P), then every later row a subtracts L[a, P] z_P; the backward substitution L^T x = z likewise over
+// the columns of L (row a < 32 P subtracts L[P, a]^T x_P).  Per panel two barriers and 32-term dots.  The
+// panel's L block (forward: rows below it x its 32 columns; backward: its 32 rows x the columns before it)
+// and its Dinv block are copied coalesced into shared memory (cp.async, double-buffered) one panel ahead --
+// no copy depends on z -- so the panel chain carries shared-memory and FMA latency only
+// (weights_solve_kernel streams L blocks through a cp.async ring per step instead).  Rows >= r_eff have
+// zero Y~ rows and Dinv rows / columns and are never updated, so they stay 0.
+constexpr int kSrLd = kPB + 2;                 // forward L / Dinv block: [row][j], row stride 34 doubles
+constexpr int kSrLdB = 8 * kPB + 2;            // backward L block: [j][column a], row stride 258 doubles
+constexpr int kSrLBuf = 8 * kPB * kSrLd;       // doubles per L buffer (>= kPB * kSrLdB)
+constexpr int kSrDBuf = kPB * kSrLd;           // doubles per Dinv buffer
+constexpr size_t kSrSmem = (size_t)2 * (kSrLBuf + kSrDBuf) * sizeof(double);
+static_assert(kPB * kSrLdB <= kSrLBuf, "backward L block fits the buffer");
+
+template <int D, int C>
+__global__ void __launch_bounds__(256) weights_solve_rows_kernel(const double *__restrict__ Y,
+                                                                 const double *__restrict__ L,
+                                                                 const double *__restrict__ Dinv,
+                                                                 const int32_t *__restrict__ r_eff, int r,
+                                                                 float *__restrict__ X) {
+    pdl_wait();
+    constexpr int DC = D + 1, NCH = C >= 4 ? 1 : 4 / C;  // independent FMA chains per column
+    extern __shared__ double srs[];                       // [2][L block], then [2][Dinv block]
+    __shared__ double sacc[kPB][C];
+    __shared__ double sz[8 * kPB][C];
+    const int u = blockIdx.y, a = threadIdx.x, nth = blockDim.x, c0 = blockIdx.x * C;
+    const int q = r_eff[u];
+    const int npan = (q + kPB - 1) / kPB, nbl = (r + kPB - 1) / kPB;
+    const int pa = a / kPB, ra = a % kPB;
+    const double *Lu = L + (int64_t)u * r * r;
+    const double *Du = Dinv + (int64_t)u * nbl * kPB * kPB;
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = (a < q && c0 + c < DC) ? Y[((int64_t)u * r + a) * DC + c0 + c] : 0.0;
+    // copies of panel P (buffer P & 1): the Dinv block, and the L block of the direction
+    // 16-byte copies (two 8-byte ones when odd r leaves L rows 8-byte aligned only); pairs of doubles
+    const bool al16 = (r & 1) == 0;
+    auto cp2 = [&](double *dst, const double *src) {
+        if (al16) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+        } else {
+            cp_async8(dst, src);
+            cp_async8(dst + 1, src + 1);
+        }
+    };
+    auto issue = [&](int P, bool fwd) {
+        double *Lb = srs + (size_t)(P & 1) * kSrLBuf;
+        double *Db = srs + (size_t)2 * kSrLBuf + (size_t)(P & 1) * kSrDBuf;
+        const double *Dp = Du + (int64_t)P * kPB * kPB;  // 16-byte aligned (blocks of 1024 doubles)
+        for (int e = a; e < kPB * kPB / 2; e += nth) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Db + (e >> 4) * kSrLd + 2 * (e & 15))),
+                         "l"(Dp + 2 * e)
+                         : "memory");
+        }
+        if (fwd) {  // L[a][32P + j] for rows a in [32(P+1), q): 16 pairs per row, nth / 16 rows at a time
+            const int ch = a & 15;
+            for (int rr = (P + 1) * kPB + (a >> 4); rr < q; rr += nth >> 4)
+                cp2(Lb + rr * kSrLd + 2 * ch, Lu + (int64_t)rr * r + P * kPB + 2 * ch);
+        } else if (2 * a < P * kPB) {  // L[32P + j][a] for columns a < 32P (rows 32P + j < q)
+            const int nr = min(kPB, q - P * kPB);
+            for (int j = 0; j < nr; ++j) cp2(Lb + j * kSrLdB + 2 * a, Lu + (int64_t)(P * kPB + j) * r + 2 * a);
+        }
+        cp_async_commit();
+    };
+    auto panel = [&](int P, bool fwd) {
+        const double *Lb = srs + (size_t)(P & 1) * kSrLBuf;
+        const double *Db = srs + (size_t)2 * kSrLBuf + (size_t)(P & 1) * kSrDBuf;
+        cp_async_wait<0>();  // this thread's copies of panel P (the only group in flight)
+        if (pa == P) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) sacc[ra][c] = acc[c];
+        }
+        __syncthreads();  // panel P's blocks and sacc visible; every thread is past panel P - 1
+        const int Pn = fwd ? P + 1 : P - 1;
+        if (fwd ? Pn < npan : Pn >= 0) issue(Pn, fwd);  // into the buffer panel P - 1 used
+        if (pa == P) {  // z_P = Dinv_PP acc_P (forward), x_P = Dinv_PP^T acc_P (backward)
+            double t[C][NCH];
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) t[c][h] = 0.0;
+#pragma unroll
+            for (int j = 0; j < kPB; j += 2) {
+                double d0, d1;
+                if (fwd) {  // row ra, 16-byte reads (conflict-free with the 34-double stride)
+                    const double2 v = *reinterpret_cast<const double2 *>(Db + ra * kSrLd + j);
+                    d0 = v.x;
+                    d1 = v.y;
+                } else {
+                    d0 = Db[j * kSrLd + ra];
+                    d1 = Db[(j + 1) * kSrLd + ra];
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    t[c][j % NCH] = fma(d0, sacc[j][c], t[c][j % NCH]);
+                    t[c][(j + 1) % NCH] = fma(d1, sacc[j + 1][c], t[c][(j + 1) % NCH]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                double z = t[c][0];
+#pragma unroll
+                for (int h = 1; h < NCH; ++h) z += t[c][h];
+                acc[c] = z;
+                sz[a][c] = z;
+            }
+        }
+        __syncthreads();
+        if (a < q && (fwd ? pa > P : pa < P)) {
+            double t[C][NCH];
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+#pragma unroll
+                for (int h = 0; h < NCH; ++h) t[c][h] = 0.0;
+            const int jn = fwd ? kPB : min(kPB, q - P * kPB);
+            if (fwd) {
+#pragma unroll
+                for (int j = 0; j < kPB; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(Lb + a * kSrLd + j);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        t[c][j % NCH] = fma(v.x, sz[P * kPB + j][c], t[c][j % NCH]);
+                        t[c][(j + 1) % NCH] = fma(v.y, sz[P * kPB + j + 1][c], t[c][(j + 1) % NCH]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kPB; ++j) {
+                    if (j < jn) {
+                        const double lv = Lb[j * kSrLdB + a];
+#pragma unroll
+                        for (int c = 0; c < C; ++c) t[c][j % NCH] = fma(lv, sz[P * kPB + j][c], t[c][j % NCH]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                double z = t[c][0];
+#pragma unroll
+                for (int h = 1; h < NCH; ++h) z += t[c][h];
+                acc[c] -= z;
+            }
+        }
+    };
+    if (npan > 0) issue(0, true);
+    for (int P = 0; P < npan; ++P) panel(P, true);
+    __syncthreads();  // every thread is past the forward panels (their buffers are reused)
+    if (npan > 0) issue(npan - 1, false);
+    for (int P = npan - 1; P >= 0; --P) panel(P, false);
+    if (a < r) {
+        float *Xr = X + ((int64_t)u * r + a) * DC + c0;
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            if (c0 + c < DC) Xr[c] = a < q ? (float)acc[c] : 0.f;
+    }
+}
+
+// Columns per CTA of weights_solve_rows_kernel (0: not used): r <= 256 and at most one wave of CTAs.
+inline int solve_rows_cols(const Dims &Dm) {
+    if (Dm.r <= kPB || Dm.r > 8 * kPB) return 0;
+    static const char *force = std::getenv("WC_SOLVE_COLS");  // A/B: force C (1, 2, 4, 8)
+    if (force) return std::atoi(force);
+    for (int C = 1; C <= 8; C *= 2)
+        if ((int64_t)Dm.units() * ceil_div(Dm.d + 1, C) <= 148) return C;
+    return 0;
+}
+
 template <int D>
 int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const int32_t *r_eff, float *X,
                    double *Dinv, cudaStream_t st, bool dinv_done = false) {
@@ -744,6 +913,23 @@ int launch_solve_d(const Dims &Dm, const double *Yfull, const double *L, const i
     if (Dm.r <= kPB && Dm.units() >= 148) {  // many small units: both products in one CTA per unit
         launch_pdl(weights_solve_small_kernel<D>, dim3(Dm.units()), dim3(256), 0, st, Yfull, (const double *)Dinv,
                    r_eff, Dm.r, X);
+        return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
+    }
+    static const char *rmode = std::getenv("WC_SOLVE");  // "panel": keep the streamed panel chain (A/B tests)
+    const int Cr = (rmode && std::strcmp(rmode, "panel") == 0) ? 0 : solve_rows_cols(Dm);
+    if (Cr > 0) {
+        const dim3 grid((unsigned)ceil_div(D + 1, Cr), Dm.units()), block((unsigned)(nbl * kPB));
+        const double *Dc = Dinv;
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSrSmem);
+            launch_pdl(kern, grid, block, kSrSmem, st, Yfull, L, Dc, r_eff, Dm.r, X);
+        };
+        switch (Cr) {
+            case 1: go(weights_solve_rows_kernel<D, 1>); break;
+            case 2: go(weights_solve_rows_kernel<D, 2>); break;
+            case 4: go(weights_solve_rows_kernel<D, 4>); break;
+            default: go(weights_solve_rows_kernel<D, 8>); break;
+        }
         return cudaPeekAtLastError() == cudaSuccess ? (dinv_done ? 1 : 2) : -1;
     }
     // few units: 2 columns per CTA (more CTAs on the panel chain); many units: 8 per CTA
