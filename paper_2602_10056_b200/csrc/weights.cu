@@ -132,14 +132,21 @@ __global__ void __launch_bounds__(256) weights_reduce_kernel(const float *__rest
     if (a < r_eff[u]) {
         const float *src = Ypart + (int64_t)u * splits * r * DC + e;
         int sp = 0;
-        for (; sp + 16 <= splits; sp += 16) {  // 16 independent loads in flight, summed in split order
-            float t[16];
+        for (; sp + 32 <= splits; sp += 32) {  // 32 independent loads in flight, summed in split order
+            float t[32];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
+            for (int k = 0; k < 32; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) y += (double)t[k];
+            for (int k = 0; k < 32; ++k) y += (double)t[k];
         }
-        for (; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
+        if (sp < splits) {  // the remaining < 32 splits, all loads in flight
+            float t[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) t[k] = sp + k < splits ? __ldg(src + (int64_t)(sp + k) * r * DC) : 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                if (sp + k < splits) y += (double)t[k];
+        }
     }
     Y[(int64_t)u * r * DC + e] = y;
 }
@@ -163,6 +170,8 @@ __device__ __forceinline__ void dinv_block(const double *__restrict__ L, const i
 #pragma unroll 8
     for (int i = 0; i < kPB; ++i) Lb[i][lane] = (i < nb && lane <= i) ? __ldg(Lu + (int64_t)(p0 + i) * r + p0 + lane) : 0.0;
     __syncwarp();
+    // 1 / L_ii computed by lane i up front, so that no division sits on the substitution's dependent chain
+    const double rdi = lane < nb ? 1.0 / Lb[lane][lane] : 0.0;
     // column c = lane of inv(Lb): x_i = (delta_ic - sum_{j<i} L_ij x_j) / L_ii, i = c .. nb-1
     double x[kPB];
 #pragma unroll
@@ -170,7 +179,8 @@ __device__ __forceinline__ void dinv_block(const double *__restrict__ L, const i
         double acc = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
         for (int j = 0; j < i; ++j) acc = fma(-Lb[i][j], x[j], acc);
-        x[i] = (i < nb && i >= lane) ? acc / Lb[i][i] : 0.0;
+        const double ri = __shfl_sync(0xffffffffu, rdi, i);
+        x[i] = (i < nb && i >= lane) ? acc * ri : 0.0;
     }
     double *Du = Dinv + ((int64_t)u * ((r + kPB - 1) / kPB) + blk) * kPB * kPB;
 #pragma unroll
@@ -207,14 +217,21 @@ __global__ void __launch_bounds__(256) weights_reduce_dinv_kernel(const float *_
     if (a < r_eff[u]) {
         const float *src = Ypart + (int64_t)u * splits * r * DC + e;
         int sp = 0;
-        for (; sp + 16 <= splits; sp += 16) {  // 16 independent loads in flight, summed in split order
-            float t[16];
+        for (; sp + 32 <= splits; sp += 32) {  // 32 independent loads in flight, summed in split order
+            float t[32];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
+            for (int k = 0; k < 32; ++k) t[k] = __ldg(src + (int64_t)(sp + k) * r * DC);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) y += (double)t[k];
+            for (int k = 0; k < 32; ++k) y += (double)t[k];
         }
-        for (; sp < splits; ++sp) y += (double)__ldg(src + (int64_t)sp * r * DC);
+        if (sp < splits) {  // the remaining < 32 splits, all loads in flight
+            float t[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) t[k] = sp + k < splits ? __ldg(src + (int64_t)(sp + k) * r * DC) : 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                if (sp + k < splits) y += (double)t[k];
+        }
     }
     Y[(int64_t)u * r * DC + e] = y;
 }
