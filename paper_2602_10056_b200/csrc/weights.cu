@@ -194,18 +194,37 @@ __global__ void __launch_bounds__(32) weights_dinv_kernel(const double *__restri
     dinv_block(L, r_eff, r, Dinv, blockIdx.x, blockIdx.y, threadIdx.x, Lb);
 }
 
-// weights_reduce_kernel + the diagonal-block inverses in one launch (single-GPU path): blocks
-// [0, nred) reduce the split partials, blocks [nred, nred + r/32) invert one diagonal block each
-// (both depend only on earlier kernels, so they run side by side).
-template <int D>
+// Coreset key row a of unit u for the attend: KS[u][a] = K[S[u][a]] (zeros past r_eff).
+template <typename T, int D>
+__device__ __forceinline__ void gather_ks_row(const T *__restrict__ K, const int32_t *__restrict__ S,
+                                              const int32_t *__restrict__ r_eff, int64_t n, int r, T *__restrict__ KS,
+                                              int bins, int64_t nb, int64_t unit_n, int u, int a) {
+    const int q = r_eff[u];
+    const int s = a < q ? S[(int64_t)u * r + a] : -1;
+    for (int j = threadIdx.x; j < D; j += blockDim.x)
+        KS[((int64_t)u * r + a) * D + j] = s >= 0 ? K[(sub_unit(u, n, bins, nb, unit_n).base + s) * D + j] : from_f32<T>(0.f);
+}
+
+// weights_reduce_kernel + the diagonal-block inverses + the K_S gather in one launch (single-GPU
+// path): blocks [0, nred) reduce the split partials, blocks [nred, nred + nbl) invert one diagonal
+// block each, blocks [nred + nbl, nred + nbl + r) gather one coreset key row each (all depend only on
+// earlier kernels, so they run side by side).
+template <typename T, int D>
 __global__ void __launch_bounds__(256) weights_reduce_dinv_kernel(const float *__restrict__ Ypart,
                                                                   const int32_t *__restrict__ r_eff, int r, int splits,
                                                                   double *__restrict__ Y, const double *__restrict__ L,
-                                                                  double *__restrict__ Dinv, int nred) {
+                                                                  double *__restrict__ Dinv, int nred, int nbl,
+                                                                  const T *__restrict__ K, const int32_t *__restrict__ S,
+                                                                  T *__restrict__ KS, int64_t n, int bins, int64_t nb,
+                                                                  int64_t unit_n) {
     pdl_wait();
     __shared__ double Lb[kPB][kPB + 1];
     constexpr int DC = D + 1;
     const int u = blockIdx.y;
+    if ((int)blockIdx.x >= nred + nbl) {
+        gather_ks_row<T, D>(K, S, r_eff, n, r, KS, bins, nb, unit_n, u, (int)blockIdx.x - nred - nbl);
+        return;
+    }
     if ((int)blockIdx.x >= nred) {
         if (threadIdx.x < 32) dinv_block(L, r_eff, r, Dinv, blockIdx.x - nred, u, threadIdx.x, Lb);
         return;
@@ -392,17 +411,6 @@ __global__ void __launch_bounds__(256) weights_solve_kernel(const double *__rest
     }
 }
 
-template <typename T, int D>
-__global__ void gather_ks_kernel(const T *__restrict__ K, const int32_t *__restrict__ S,
-                                 const int32_t *__restrict__ r_eff, int64_t n, int r, T *__restrict__ KS, int bins,
-                                 int64_t nb, int64_t unit_n) {
-    pdl_wait();
-    const int u = blockIdx.y, a = blockIdx.x;
-    const int q = r_eff[u];
-    const int s = a < q ? S[(int64_t)u * r + a] : -1;
-    for (int j = threadIdx.x; j < D; j += blockDim.x)
-        KS[((int64_t)u * r + a) * D + j] = s >= 0 ? K[(sub_unit(u, n, bins, nb, unit_n).base + s) * D + j] : from_f32<T>(0.f);
-}
 
 // =====================================================================================
 // tcgen05 path for A3 (bf16, d in {64, 128}).  CTA = (n-split, 128 coreset rows, unit), 128
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kWTc, 1)
 template <typename T, int D>
 int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const void *KSin,
                       const int32_t *r_eff, const double *stats, float *Ypart, double **Yfull_out, cudaStream_t st,
-                      const double *L_dinv = nullptr) {
+                      const double *L_dinv = nullptr, void *KSout = nullptr) {
     const int units = Dm.units();
     const int splits = weights_num_splits(Dm);
     static const char *mode = std::getenv("WC_WEIGHTS");  // "cuda": CUDA-core kernel (A/B tests)
@@ -697,8 +705,10 @@ int launch_partial_td(const Dims &Dm, const void *K, const void *V, const int32_
     if (L_dinv) {  // single-GPU path: the diagonal-block inverses of L ride along (Dinv follows Y~)
         const int nbl = (Dm.r + kPB - 1) / kPB;
         double *Dinv = Yfull + (size_t)units * Dm.r * (D + 1);
-        launch_pdl(weights_reduce_dinv_kernel<D>, dim3(gr.x + nbl, units), dim3(256), 0, st, (const float *)Ypart,
-                   r_eff, Dm.r, splits, Yfull, L_dinv, Dinv, (int)gr.x);
+        // (with KSout: the K_S gather of the attend rides along, one block per coreset row)
+        launch_pdl(weights_reduce_dinv_kernel<T, D>, dim3(gr.x + nbl + (KSout ? Dm.r : 0), units), dim3(256), 0, st,
+                   (const float *)Ypart, r_eff, Dm.r, splits, Yfull, L_dinv, Dinv, (int)gr.x, nbl,
+                   static_cast<const T *>(K), S, static_cast<T *>(KSout), Dm.n, Dm.bins, Dm.nb, Dm.unit_n);
     } else {
         launch_pdl(weights_reduce_kernel<D>, gr, dim3(256), 0, st, (const float *)Ypart, r_eff, Dm.r, splits, Yfull);
     }
@@ -1149,7 +1159,8 @@ template <typename T, int D>
 int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_t *S, const int32_t *r_eff,
                       const double *L, const double *stats, float *Ypart, void *KS, float *X, cudaStream_t st) {
     double *Yfull = nullptr;
-    const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st, L);
+    // (the reduction launch also inverts L's diagonal blocks and gathers K_S for the attend)
+    const int k1 = launch_partial_td<T, D>(Dm, K, V, S, nullptr, r_eff, stats, Ypart, &Yfull, st, L, KS);
     if (k1 < 0) return -1;
     // scratch for the diagonal-block inverses: after Y~ in the weights workspace (carve_weights),
     // then W = L^{-1}, the level products and W Y~ (solve_scratch_elems)
@@ -1161,10 +1172,7 @@ int launch_weights_td(const Dims &Dm, const void *K, const void *V, const int32_
     const int k2 = panel ? launch_solve_d<D>(Dm, Yfull, L, r_eff, X, Dinv, st, true)
                          : launch_solve_inverse(Dm, Yfull, L, r_eff, X, Dinv, Dinv + (size_t)Dm.units() * dinv_elems(Dm.r), st);
     if (k2 < 0) return -1;
-    dim3 g3(Dm.r, Dm.units());
-    launch_pdl(gather_ks_kernel<T, D>, g3, dim3(128), 0, st, static_cast<const T *>(K), S, r_eff, Dm.n, Dm.r,
-               static_cast<T *>(KS), Dm.bins, Dm.nb, Dm.unit_n);
-    return cudaPeekAtLastError() == cudaSuccess ? k1 + k2 + 1 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? k1 + k2 : -1;
 }
 
 template <typename T>
